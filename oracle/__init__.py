@@ -1,0 +1,209 @@
+"""CPU oracle for the Slim Scheduler hot path -- TEST INFRASTRUCTURE ONLY.
+
+Only `tests/`, `__graft_entry__.smoke()` and `bench.py`'s cpu_baseline /
+`--impl reference` legs may import this package.  The product path
+(`paper_2510_09018_b200`) never imports it and shares no code with it.
+
+It is the plain definition of the batched forward pass of the segmented
+SlimResNet at a runtime-chosen width, in float64:
+
+* convolution: `oracle.c` (direct sum, fixed kh,kw,ci order; O2),
+* everything else: numpy float64, one line per formula.
+
+Citations: P:n = /root/reference/PAPER.md line n.  The paper fixes none of the
+architecture; the readings used here (ResNet-18-CIFAR, per-width BN selected by
+the segment's own width, eps=1e-5, ...) are listed in DESIGN.md "Readings".
+
+Parity status: every function below is pinned by tests/test_oracle_pins.py
+(brute force, torch float64 library routines, closed forms, invariants).  The
+paper's own numbers (Tables I-V) need trained weights and CIFAR-100 and cannot
+pin anything here: "parity unpinned" against the paper's printed values.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+_lock = threading.Lock()
+_lib = None
+
+# Width set W and BN epsilon (reading #6, PyTorch default).  Kept here,
+# not imported from the CUDA side.
+BN_EPS = 1e-5
+
+
+def build(force: bool = False) -> str:
+    """Compile oracle.c with gcc (-O2, strict IEEE: no -ffast-math) -> liboracle.so."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", "-O2", "-fopenmp", "-fPIC", "-shared", "-fno-fast-math",
+                               "-ffp-contract=off", "-o", tmp, _SRC])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+def _load():
+    global _lib
+    with _lock:
+        if _lib is None:
+            build()
+            lib = ctypes.CDLL(_LIB)
+            dp = ctypes.POINTER(ctypes.c_double)
+            L = ctypes.c_long
+            lib.oracle_conv2d.argtypes = [dp, L, L, L, L, dp, L, L, L, L, L, L, dp]
+            lib.oracle_conv2d.restype = ctypes.c_int
+            lib.oracle_out_size.argtypes = [L, L, L, L]
+            lib.oracle_out_size.restype = L
+            _lib = lib
+    return _lib
+
+
+def _ptr(a):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+# ---------------------------------------------------------------- O1 channels
+def channels(r: float, C: int) -> int:
+    """O1: c(r, C) = ceil(r*C) (north_star "first ceil(r*C) ... channels").
+
+    Computed in integers for the width set {k/4}: r*4 is an exact integer there.
+    """
+    q = r * 4.0
+    if abs(q - round(q)) < 1e-9:
+        return (int(round(q)) * C + 3) // 4
+    return int(np.ceil(r * C - 1e-9))
+
+
+# ---------------------------------------------------------------- O2 conv
+def conv2d(x: np.ndarray, w: np.ndarray, c_out: int, stride: int, pad: int) -> np.ndarray:
+    """O2: width-sliced convolution of dense NHWC x with the full KRSC tensor w.
+
+    x: [B,H,W,c_in] (c_in = x.shape[-1] active channels); w: [Cout_full,k,k,Cin_full].
+    Reads w[:c_out, :, :, :c_in] only.  Returns float64 [B,Ho,Wo,c_out].
+    """
+    lib = _load()
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    w = np.ascontiguousarray(w, dtype=np.float64)
+    B, H, W, c_in = x.shape
+    cout_full, k, k2, cin_full = w.shape
+    assert k == k2
+    Ho = lib.oracle_out_size(H, k, stride, pad)
+    Wo = lib.oracle_out_size(W, k, stride, pad)
+    y = np.empty((B, Ho, Wo, c_out), dtype=np.float64)
+    if B == 0:
+        return y
+    rc = lib.oracle_conv2d(_ptr(x), B, H, W, c_in, _ptr(w), cout_full, k, cin_full, c_out,
+                           stride, pad, _ptr(y))
+    if rc != 0:
+        raise ValueError("oracle_conv2d: bad arguments")
+    return y
+
+
+# ---------------------------------------------------------------- O3 BN, O4 ReLU
+def batchnorm(y: np.ndarray, stats: dict, eps: float = BN_EPS) -> np.ndarray:
+    """O3 (inference BN, unfolded): z = (y - mu) / sqrt(var + eps) * gamma + beta."""
+    c = y.shape[-1]
+    mu = np.asarray(stats["mean"], np.float64)[:c]
+    var = np.asarray(stats["var"], np.float64)[:c]
+    gamma = np.asarray(stats["gamma"], np.float64)[:c]
+    beta = np.asarray(stats["beta"], np.float64)[:c]
+    assert mu.shape[0] == c, "BN statistics shorter than the active channel count"
+    return (y - mu) / np.sqrt(var + eps) * gamma + beta
+
+
+def relu(z: np.ndarray) -> np.ndarray:
+    """O4: max(z, 0)."""
+    return np.maximum(z, 0.0)
+
+
+# ---------------------------------------------------------------- model
+class Model:
+    """Full-width shared weights + per-width BN sets (the paper's slimmable backbone).
+
+    weights: dict layer name -> KRSC array, plus "fc_w" [classes][C3], "fc_b" [classes].
+    bn:      dict layer name -> list over `widths` of dict(gamma, beta, mean, var).
+    Layer names follow the manifest order of synth.layer_specs (stem, s{s}b{b}c1/c2/sc).
+    """
+
+    def __init__(self, weights: dict, bn: dict, widths=(0.25, 0.5, 0.75, 1.0),
+                 base=(64, 128, 256, 512), blocks=(2, 2, 2, 2), eps: float = BN_EPS):
+        self.w = {k: np.ascontiguousarray(v, dtype=np.float64) for k, v in weights.items()}
+        self.bn = bn
+        self.widths = tuple(float(r) for r in widths)
+        self.base = tuple(base)
+        self.blocks = tuple(blocks)
+        self.eps = eps
+
+    def width_index(self, r: float) -> int:
+        for i, q in enumerate(self.widths):
+            if abs(q - r) < 1e-6:
+                return i
+        raise ValueError(f"width {r} not in the slimming set {self.widths}")
+
+    def conv_bn(self, x, name, r, stride, pad, bn_width=None):
+        """conv (O2) at output width c(r, Cout) followed by BN_{name, width r} (O3)."""
+        w = self.w[name]
+        c_out = channels(r, w.shape[0])
+        y = conv2d(x, w, c_out, stride, pad)
+        return batchnorm(y, self.bn[name][self.width_index(r if bn_width is None else bn_width)], self.eps)
+
+    # O5 BasicBlock
+    def basic_block(self, x, s, b, r, bn_width=None):
+        """O5: t = ReLU(BN1(conv3x3_s(x))); u = BN2(conv3x3_1(t));
+        sc = BN_sc(conv1x1_s(x)) for the down-sampling block, else x; out = ReLU(u + sc)."""
+        down = (s > 0 and b == 0)
+        stride = 2 if down else 1
+        t = relu(self.conv_bn(x, f"s{s}b{b}c1", r, stride, 1, bn_width))
+        u = self.conv_bn(t, f"s{s}b{b}c2", r, 1, 1, bn_width)
+        sc = self.conv_bn(x, f"s{s}b{b}sc", r, stride, 0, bn_width) if down else x
+        return relu(u + sc)
+
+    # O7 head
+    def head(self, h, r3):
+        """O7: p = mean over the 4x4 map; logits = b + p @ W_fc[:, :c3]^T."""
+        p = h.mean(axis=(1, 2))                       # [B, c3]
+        c3 = h.shape[-1]
+        # elementwise product + per-row sum (not BLAS gemm: the result must not
+        # depend on the batch size, SURVEY §8(c) "batch independence")
+        return (p[:, None, :] * self.w["fc_w"][None, :, :c3]).sum(axis=-1) + self.w["fc_b"]
+
+    # O6 segment
+    def segment(self, s, x, r_prev, r, head=True, bn_width=None):
+        """O6: segment s at (r_prev, r).  Seg 0: stem conv-BN-ReLU then blocks.
+        Seg s>0: block 0 reads c_{s-1}(r_prev) channels (P:49 key (s, w_req, w_prev)).
+        Seg 3 ends with the head (O7) when head=True.  bn_width overrides the BN
+        set (negative control only)."""
+        x = np.asarray(x, dtype=np.float64)
+        if s == 0:
+            x = relu(self.conv_bn(x, "stem", r, 1, 1, bn_width))
+        else:
+            assert x.shape[-1] == channels(r_prev, self.base[s - 1]), "input width != c(r_prev)"
+        for b in range(self.blocks[s]):
+            x = self.basic_block(x, s, b, r, bn_width)
+        if s == 3 and head:
+            return self.head(x, r)
+        return x
+
+    # O8 chain
+    def chain(self, x, r_per_seg, head=True):
+        """O8: seg0(r0) -> seg1(r0->r1) -> seg2(r1->r2) -> seg3(r2->r3) -> head."""
+        h = self.segment(0, x, None, r_per_seg[0])
+        for s in range(1, 4):
+            h = self.segment(s, h, r_per_seg[s - 1], r_per_seg[s], head=head)
+        return h
+
+
+def per_image_rel_err(got: np.ndarray, ref: np.ndarray) -> np.ndarray:
+    """Tolerance reading D4: per image, max_k |g-o| / max_k |o| (over all elements of the image)."""
+    g = np.asarray(got, np.float64).reshape(got.shape[0], -1)
+    o = np.asarray(ref, np.float64).reshape(ref.shape[0], -1)
+    den = np.abs(o).max(axis=1)
+    num = np.abs(g - o).max(axis=1)
+    return num / np.maximum(den, 1e-30)
