@@ -1,0 +1,211 @@
+/*
+ * slim.h -- C-ABI of libslim.so: the batched forward pass of a segmented,
+ * width-sliced SlimResNet on NVIDIA B200 (sm_100a).  This is the data-parallel
+ * hot path of Slim Scheduler (arXiv 2510.09018); everything around it (PPO
+ * router, greedy executor) is host-side control that calls these entry points.
+ *
+ * Citations: P:n = PAPER.md line n (the paper text); SURVEY §x = SURVEY.md.
+ *   - segmented, universally slimmable backbone ............ P:31
+ *   - request key k = (s, w_req, w_prev), batching by key ... P:49, Alg.1 l.4
+ *   - RUNBATCH(inst, B) on a loaded (segment, width) ........ Alg.1 l.10
+ *   - "Estimate bytes of (s, w)" (CANLOAD) .................. Alg.1 l.14
+ *   - "offload to CPU, free VRAM" (UNLOADERLOOP) ............ Alg.1 l.25
+ *   - widths W = {1.00, 0.75, 0.50, 0.25}, four segments .... P:148
+ * The paper gives no depth, channel counts or normalisation details for its
+ * kernels; DESIGN.md "Readings" lists how each silence is resolved (ResNet-18
+ * CIFAR, switchable per-width BN selected by the segment's own width, eps, ...).
+ *
+ * Conventions (all entry points):
+ *   - Return slim_status; nothing throws across the ABI.  Argument validation
+ *     happens BEFORE anything is enqueued: on SLIM_EINVAL / SLIM_ENOTLOADED no
+ *     work was launched.  Asynchronous device faults are sticky and surface as
+ *     SLIM_ECUDA from the next call or from slim_last_error().
+ *   - Device buffers (in, out, workspace, slab, pool, slots) are caller-owned
+ *     device memory, 16-byte aligned.  The library never frees them and never
+ *     allocates device memory inside forward / launch calls.
+ *   - All device work is enqueued on the caller's `stream` (a cudaStream_t
+ *     passed as void*; NULL = legacy default stream).  No implicit host sync.
+ *   - Activations are dense NHWC.  In SLIM_BF16 mode activations are bf16
+ *     (uint16 bit patterns) with fp32 accumulation and fp32 epilogue math and
+ *     one bf16 rounding per stored tensor; in SLIM_FP32 mode they are fp32
+ *     with fp32 FFMA (no TF32 anywhere).  Logits are always fp32.
+ *   - Width semantics: a width r must be one of cfg.widths (|diff| < 1e-6);
+ *     the active channel count of a C-channel layer is c(r, C) = ceil(r*C).
+ *     The first ceil(r*C) output channels and the first c(r_prev) input
+ *     channels of the FULL-width shared weights are used, selected by TMA
+ *     tensor-map bounds (tile predication), never by copying weights.
+ *   - Thread safety: after loading, forward calls on one context may run
+ *     concurrently from several threads on different streams ONLY when each
+ *     passes its own workspace (slim_forward_ws / slim_forward_chain);
+ *     slim_forward uses the context's internal workspace and is not
+ *     re-entrant.  Load/unload must not overlap forwards of the same segment.
+ */
+#ifndef SLIM_H_
+#define SLIM_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define SLIM_API __attribute__((visibility("default")))
+#else
+#define SLIM_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    SLIM_OK = 0,
+    SLIM_EINVAL = -1,          /* bad argument (width not in set, seg out of range, B>B_max, misaligned ptr, ...) */
+    SLIM_ENOTLOADED = -2,      /* segment not loaded (slim_load_segment) */
+    SLIM_ENOMEM = -3,          /* device / host allocation failed at create or load */
+    SLIM_ECUDA = -4,           /* CUDA runtime / driver error (sticky for async faults) */
+    SLIM_EUNSUPPORTED = -5     /* configuration outside what the kernels implement */
+} slim_status;
+
+typedef enum { SLIM_BF16 = 0, SLIM_FP32 = 1 } slim_dtype;
+
+/* Network configuration (reading D1 = CIFAR ResNet-18). */
+typedef struct {
+    int n_widths;              /* |W|, 1..8 */
+    float widths[8];           /* sorted ascending, each in (0,1]; default {0.25,0.5,0.75,1.0} */
+    int blocks_per_seg[4];     /* BasicBlocks per segment, default {2,2,2,2} (1..4 each) */
+    int base_channels[4];      /* full-width channels C_s, default {64,128,256,512} */
+    int in_channels;           /* image channels, 3 (never sliced) */
+    int num_classes;           /* classifier outputs, 100 for CIFAR-100; never sliced; <= 1024 */
+    int image_hw;              /* input height = width, 32 */
+    int max_batch;             /* B_max: bounds every batch; sizes the internal workspace */
+    float bn_eps;              /* BatchNorm epsilon, 1e-5 */
+    slim_dtype dtype;          /* SLIM_BF16 (default) or SLIM_FP32 */
+} slim_config;
+
+/* Host pointers to ONE segment's full-width weights, fp32 values (copied at load).
+ * conv_w order (the manifest order):
+ *   seg 0   : stem, then per block b: b.c1, b.c2
+ *   seg s>0 : block 0: c1 (3x3 stride 2), c2, sc (1x1 stride 2 projection);
+ *             blocks b>0: c1, c2
+ * Each conv tensor is KRSC [C_out][k][k][C_in] at full width.  fc_w [classes][C_3]
+ * and fc_b [classes] are read for seg 3 only (may be NULL otherwise). */
+typedef struct {
+    const float *conv_w[16];
+    int n_conv;
+    const float *fc_w;
+    const float *fc_b;
+} slim_seg_weights;
+
+/* Inference BatchNorm statistics of one layer at one width; each array has
+ * c(width, C_out) entries.  z = (y - mean)/sqrt(var + eps)*gamma + beta. */
+typedef struct { const float *gamma, *beta, *mean, *var; } slim_bn;
+
+/* The BN statistics of every conv layer of one segment (manifest order) at one width. */
+typedef struct { const slim_bn *per_layer; int n_layers; } slim_bn_set;
+
+typedef struct slim_ctx slim_ctx;
+
+/* ---- lifetime ---------------------------------------------------------- */
+
+/* Create a context on CUDA device `device`; validates cfg and allocates the
+ * internal workspace for cfg->max_batch.  *out = NULL on failure. */
+SLIM_API slim_status slim_create(int device, const slim_config *cfg, slim_ctx **out);
+SLIM_API void slim_destroy(slim_ctx *ctx);
+/* Fill *cfg with the defaults above (B_max = 4096, SLIM_BF16). */
+SLIM_API void slim_default_config(slim_config *cfg);
+
+/* Load segment `seg` (0..3): copies the full-width weights to the device
+ * (bf16 RNE in BF16 mode), folds every width's BN into fp32 (scale, shift) in
+ * fp64 on the host, and encodes the weight tensor maps for every (r_prev, r).
+ * bn_per_width points to cfg.n_widths sets (one per width, same order as
+ * cfg.widths).  Replaces a previously loaded copy.  Synchronous. */
+SLIM_API slim_status slim_load_segment(slim_ctx *ctx, int seg, const slim_seg_weights *w,
+                              const slim_bn_set *bn_per_width);
+/* Alg.1 UNLOADERLOOP: free the segment's device memory. */
+SLIM_API slim_status slim_unload_segment(slim_ctx *ctx, int seg);
+SLIM_API int slim_segment_loaded(const slim_ctx *ctx, int seg);
+
+/* CANLOAD's "Estimate bytes of (s, w)": device bytes of the ACTIVE
+ * weights and folded BN of segment seg at (r_prev, r) in cfg->dtype (the
+ * resident copy is full-width; this is the slice a width-r instance reads). */
+SLIM_API size_t slim_segment_bytes(const slim_config *cfg, int seg, float r_prev, float r);
+
+/* ---- forward ----------------------------------------------------------- */
+
+/* RUNBATCH (Alg.1 l.10) for one segment at key (seg, r, r_prev):
+ *   in : seg 0: [B, H, H, in_channels]; seg s>0: [B, H_{s-1}, H_{s-1}, c_{s-1}(r_prev)]
+ *   out: seg < 3: [B, H_s, H_s, c_s(r)]; seg 3: fp32 logits [B, num_classes]
+ * H_s = image_hw / 2^s.  r_prev is ignored for seg 0.  1 <= B <= max_batch.
+ * Uses the context's internal workspace (not re-entrant; see slim_forward_ws). */
+SLIM_API slim_status slim_forward(slim_ctx *ctx, int seg, float r_prev, float r, int batch,
+                         const void *in, void *out, void *stream);
+SLIM_API size_t slim_forward_workspace_bytes(const slim_ctx *ctx, int seg, float r_prev, float r, int batch);
+SLIM_API slim_status slim_forward_ws(slim_ctx *ctx, int seg, float r_prev, float r, int batch,
+                            const void *in, void *out, void *ws, size_t ws_bytes, void *stream);
+
+/* The whole chain seg0(r0) -> seg1(r0->r1) -> seg2(r1->r2) -> seg3(r2->r3) -> head,
+ * i.e. the composition of slim_forward calls (P:49 re-entry with w_prev).
+ * in: [B, H, H, in_channels]; logits: fp32 [B, num_classes]; ws: device workspace
+ * of at least slim_chain_workspace_bytes(). */
+SLIM_API size_t slim_chain_workspace_bytes(const slim_ctx *ctx, const float r_per_seg[4], int batch);
+SLIM_API slim_status slim_forward_chain(slim_ctx *ctx, const float r_per_seg[4], int batch, const void *in,
+                               float *logits, void *ws, size_t ws_bytes, void *stream);
+
+/* ---- batch packer (Alg.1 l.3-4) --------------------------------- */
+
+/* One queued request: key (seg, w_req, w_prev).  `slot` is the row
+ * of this request's input activation in the caller's activation pool. */
+typedef struct {
+    uint64_t id;
+    int seg;
+    float w_req;
+    float w_prev;              /* ignored when seg == 0 */
+    uint32_t slot;
+} slim_request;
+
+/* One batch of key-equal requests: order[first .. first+batch) (written by
+ * slim_pack) are the request indices, FIFO order preserved. */
+typedef struct {
+    int seg;
+    float r_prev;
+    float r;
+    int batch;
+    int first;
+} slim_launch_desc;
+
+/* Greedy key batching over the FIFO q[0..n): repeatedly peek the head key,
+ * take up to B_max requests with an equal key scanning the whole queue
+ * (non-matching requests keep their relative order, SPEC form_batch), and emit
+ * one descriptor.  Host only.  order: n entries; descs: capacity max_descs
+ * (n suffices).  Keys are validated against cfg's widths (SLIM_EINVAL).  Needs no GPU. */
+SLIM_API slim_status slim_pack(const slim_config *cfg, const slim_request *q, int n, int B_max,
+                      slim_launch_desc *descs, int max_descs, int *n_descs, uint32_t *order);
+
+/* Run one packed batch: gather rows pool[slots[i]] (each pool_row_bytes, device)
+ * into the contiguous slab (device, >= batch rows) with the vectorised gather
+ * kernel, then slim_forward_ws on the slab into out.  slots is a DEVICE array of
+ * desc->batch uint32 row indices; if slots == NULL the pool is already the
+ * contiguous batch and no gather runs. */
+SLIM_API slim_status slim_launch(slim_ctx *ctx, const slim_launch_desc *desc, const uint32_t *slots,
+                        const void *pool, size_t pool_row_bytes, void *slab, void *out,
+                        void *ws, size_t ws_bytes, void *stream);
+
+/* Device gather alone (K8): dst[i] = src[idx[i]] for i < n rows of row_bytes
+ * (multiple of 16).  idx is a device array. */
+SLIM_API slim_status slim_gather(slim_ctx *ctx, const void *src, const uint32_t *idx, int n, size_t row_bytes,
+                        void *dst, void *stream);
+
+/* ---- errors, introspection ------------------------------------------------ */
+SLIM_API slim_status slim_last_error(slim_ctx *ctx);        /* sticky async error (SLIM_OK if none) */
+SLIM_API const char *slim_last_error_msg(const slim_ctx *ctx);
+SLIM_API const char *slim_status_str(slim_status s);
+SLIM_API int slim_version(void);
+/* Number of kernels this context has launched (the bench's gpu_launches). */
+SLIM_API uint64_t slim_launch_count(const slim_ctx *ctx);
+/* Number of SMs of the context's device and the active-channel rule c(r, C). */
+SLIM_API int slim_num_sms(const slim_ctx *ctx);
+SLIM_API int slim_channels(float r, int C);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SLIM_H_ */

@@ -1,0 +1,369 @@
+"""Python binding of libslim.so (include/slim.h) -- argument marshalling only.
+
+Every step of the forward pass runs in the CUDA kernels behind the C-ABI; this
+module only converts Python objects (torch tensors, numpy arrays, floats) to the
+plain pointers and sizes the ABI takes.  There is no CPU fallback: if the shared
+library is missing or the GPU is absent, the calls raise.
+
+Function names mirror the C entry points (slim_create, slim_load_segment,
+slim_forward, slim_forward_chain, slim_pack, slim_launch, ...).  `SlimNet` is a
+convenience wrapper that loads the four segments from a dict of named weights.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+__all__ = [
+    "SlimError", "load_library", "slim_config", "default_config", "slim_create", "slim_destroy",
+    "slim_load_segment", "slim_unload_segment", "slim_segment_bytes", "slim_forward", "slim_forward_ws",
+    "slim_forward_workspace_bytes", "slim_chain_workspace_bytes", "slim_forward_chain", "slim_pack",
+    "slim_launch", "slim_gather", "slim_last_error", "slim_launch_count", "slim_channels", "SlimNet",
+    "manifest", "LIB_PATH",
+]
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libslim.so")
+
+SLIM_OK, SLIM_EINVAL, SLIM_ENOTLOADED, SLIM_ENOMEM, SLIM_ECUDA, SLIM_EUNSUPPORTED = 0, -1, -2, -3, -4, -5
+SLIM_BF16, SLIM_FP32 = 0, 1
+
+
+class SlimError(RuntimeError):
+    def __init__(self, status, msg=""):
+        super().__init__(f"{_STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+_STATUS = {0: "SLIM_OK", -1: "SLIM_EINVAL", -2: "SLIM_ENOTLOADED", -3: "SLIM_ENOMEM", -4: "SLIM_ECUDA",
+           -5: "SLIM_EUNSUPPORTED"}
+
+
+class slim_config(ctypes.Structure):
+    _fields_ = [("n_widths", ctypes.c_int), ("widths", ctypes.c_float * 8), ("blocks_per_seg", ctypes.c_int * 4),
+                ("base_channels", ctypes.c_int * 4), ("in_channels", ctypes.c_int), ("num_classes", ctypes.c_int),
+                ("image_hw", ctypes.c_int), ("max_batch", ctypes.c_int), ("bn_eps", ctypes.c_float),
+                ("dtype", ctypes.c_int)]
+
+
+class slim_seg_weights(ctypes.Structure):
+    _fields_ = [("conv_w", ctypes.c_void_p * 16), ("n_conv", ctypes.c_int), ("fc_w", ctypes.c_void_p),
+                ("fc_b", ctypes.c_void_p)]
+
+
+class slim_bn(ctypes.Structure):
+    _fields_ = [("gamma", ctypes.c_void_p), ("beta", ctypes.c_void_p), ("mean", ctypes.c_void_p),
+                ("var", ctypes.c_void_p)]
+
+
+class slim_bn_set(ctypes.Structure):
+    _fields_ = [("per_layer", ctypes.POINTER(slim_bn)), ("n_layers", ctypes.c_int)]
+
+
+class slim_request(ctypes.Structure):
+    _fields_ = [("id", ctypes.c_uint64), ("seg", ctypes.c_int), ("w_req", ctypes.c_float),
+                ("w_prev", ctypes.c_float), ("slot", ctypes.c_uint32)]
+
+
+class slim_launch_desc(ctypes.Structure):
+    _fields_ = [("seg", ctypes.c_int), ("r_prev", ctypes.c_float), ("r", ctypes.c_float), ("batch", ctypes.c_int),
+                ("first", ctypes.c_int)]
+
+
+_lib = None
+_VP, _SZ, _I, _F = ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_float
+
+
+def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
+    """Load libslim.so; raises (never falls back) if it is missing."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise RuntimeError(f"libslim.so not found at {path}: run `python -m paper_2510_09018_b200.build` "
+                           "(there is no CPU fallback)")
+    lib = ctypes.CDLL(path)
+    sig = {
+        "slim_create": (_I, [_I, ctypes.POINTER(slim_config), ctypes.POINTER(_VP)]),
+        "slim_destroy": (None, [_VP]),
+        "slim_default_config": (None, [ctypes.POINTER(slim_config)]),
+        "slim_load_segment": (_I, [_VP, _I, ctypes.POINTER(slim_seg_weights), ctypes.POINTER(slim_bn_set)]),
+        "slim_unload_segment": (_I, [_VP, _I]),
+        "slim_segment_loaded": (_I, [_VP, _I]),
+        "slim_segment_bytes": (_SZ, [ctypes.POINTER(slim_config), _I, _F, _F]),
+        "slim_forward": (_I, [_VP, _I, _F, _F, _I, _VP, _VP, _VP]),
+        "slim_forward_workspace_bytes": (_SZ, [_VP, _I, _F, _F, _I]),
+        "slim_forward_ws": (_I, [_VP, _I, _F, _F, _I, _VP, _VP, _VP, _SZ, _VP]),
+        "slim_chain_workspace_bytes": (_SZ, [_VP, ctypes.POINTER(_F), _I]),
+        "slim_forward_chain": (_I, [_VP, ctypes.POINTER(_F), _I, _VP, _VP, _VP, _SZ, _VP]),
+        "slim_pack": (_I, [ctypes.POINTER(slim_config), ctypes.POINTER(slim_request), _I, _I,
+                           ctypes.POINTER(slim_launch_desc), _I,
+                           ctypes.POINTER(_I), ctypes.POINTER(ctypes.c_uint32)]),
+        "slim_launch": (_I, [_VP, ctypes.POINTER(slim_launch_desc), _VP, _VP, _SZ, _VP, _VP, _VP, _SZ, _VP]),
+        "slim_gather": (_I, [_VP, _VP, _VP, _I, _SZ, _VP, _VP]),
+        "slim_last_error": (_I, [_VP]),
+        "slim_last_error_msg": (ctypes.c_char_p, [_VP]),
+        "slim_status_str": (ctypes.c_char_p, [_I]),
+        "slim_version": (_I, []),
+        "slim_launch_count": (ctypes.c_uint64, [_VP]),
+        "slim_num_sms": (_I, [_VP]),
+        "slim_channels": (_I, [_F, _I]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+EXPORTED = ("slim_create", "slim_destroy", "slim_default_config", "slim_load_segment", "slim_unload_segment",
+            "slim_segment_loaded", "slim_segment_bytes", "slim_forward", "slim_forward_workspace_bytes",
+            "slim_forward_ws", "slim_chain_workspace_bytes", "slim_forward_chain", "slim_pack", "slim_launch",
+            "slim_gather", "slim_last_error", "slim_last_error_msg", "slim_status_str", "slim_version",
+            "slim_launch_count", "slim_num_sms", "slim_channels")
+
+
+# ------------------------------------------------------------------ marshalling helpers
+def _ptr(x):
+    """Device/host pointer of a torch tensor, numpy array, int or None."""
+    if x is None:
+        return None
+    if isinstance(x, int):
+        return x
+    if isinstance(x, np.ndarray):
+        return x.ctypes.data
+    return x.data_ptr()
+
+
+def _stream(s):
+    if s is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(s, int):
+        return s
+    return s.cuda_stream
+
+
+def _check(ctx, status):
+    if status != SLIM_OK:
+        lib = load_library()
+        msg = lib.slim_last_error_msg(ctx).decode() if ctx else ""
+        raise SlimError(status, msg)
+
+
+def default_config(**kw) -> slim_config:
+    cfg = slim_config()
+    load_library().slim_default_config(ctypes.byref(cfg))
+    for k, v in kw.items():
+        if k == "widths":
+            cfg.n_widths = len(v)
+            for i, r in enumerate(v):
+                cfg.widths[i] = r
+        elif k in ("blocks_per_seg", "base_channels"):
+            for i, c in enumerate(v):
+                getattr(cfg, k)[i] = c
+        elif k == "dtype":
+            cfg.dtype = {"bf16": SLIM_BF16, "fp32": SLIM_FP32}.get(v, v)
+        else:
+            setattr(cfg, k, v)
+    return cfg
+
+
+def manifest(seg: int, blocks_per_seg=(2, 2, 2, 2)):
+    """Layer names of segment `seg` in the ABI manifest order (include/slim.h slim_seg_weights)."""
+    names = ["stem"] if seg == 0 else []
+    for b in range(blocks_per_seg[seg]):
+        names += [f"s{seg}b{b}c1", f"s{seg}b{b}c2"]
+        if seg > 0 and b == 0:
+            names.append(f"s{seg}b{b}sc")
+    return names
+
+
+# ------------------------------------------------------------------ C entry points
+def slim_create(device: int = 0, cfg: slim_config | None = None):
+    lib = load_library()
+    cfg = cfg or default_config()
+    h = ctypes.c_void_p()
+    _check(None, lib.slim_create(device, ctypes.byref(cfg), ctypes.byref(h)))
+    return h.value
+
+
+def slim_destroy(ctx):
+    load_library().slim_destroy(ctx)
+
+
+def slim_load_segment(ctx, seg: int, conv_w: list, bn_per_width: list, fc_w=None, fc_b=None):
+    """conv_w: fp32 host arrays in manifest order; bn_per_width: [width][layer] dicts(gamma,beta,mean,var)."""
+    lib = load_library()
+    keep = []
+    w = slim_seg_weights()
+    w.n_conv = len(conv_w)
+    for i, a in enumerate(conv_w):
+        a = np.ascontiguousarray(a, dtype=np.float32)
+        keep.append(a)
+        w.conv_w[i] = a.ctypes.data
+    if fc_w is not None:
+        fw = np.ascontiguousarray(fc_w, dtype=np.float32)
+        fb = np.ascontiguousarray(fc_b, dtype=np.float32)
+        keep += [fw, fb]
+        w.fc_w, w.fc_b = fw.ctypes.data, fb.ctypes.data
+    sets = (slim_bn_set * len(bn_per_width))()
+    for wi, layers in enumerate(bn_per_width):
+        arr = (slim_bn * len(layers))()
+        for li, st in enumerate(layers):
+            vals = [np.ascontiguousarray(st[k], dtype=np.float32) for k in ("gamma", "beta", "mean", "var")]
+            keep += vals
+            arr[li] = slim_bn(*[v.ctypes.data for v in vals])
+        keep.append(arr)
+        sets[wi] = slim_bn_set(ctypes.cast(arr, ctypes.POINTER(slim_bn)), len(layers))
+    _check(ctx, lib.slim_load_segment(ctx, seg, ctypes.byref(w), sets))
+
+
+def slim_unload_segment(ctx, seg: int):
+    _check(ctx, load_library().slim_unload_segment(ctx, seg))
+
+
+def slim_segment_bytes(cfg: slim_config, seg: int, r_prev: float, r: float) -> int:
+    return load_library().slim_segment_bytes(ctypes.byref(cfg), seg, r_prev, r)
+
+
+def slim_forward(ctx, seg, r_prev, r, batch, x, out, stream=None):
+    _check(ctx, load_library().slim_forward(ctx, seg, r_prev, r, batch, _ptr(x), _ptr(out), _stream(stream)))
+
+
+def slim_forward_workspace_bytes(ctx, seg, r_prev, r, batch) -> int:
+    return load_library().slim_forward_workspace_bytes(ctx, seg, r_prev, r, batch)
+
+
+def slim_forward_ws(ctx, seg, r_prev, r, batch, x, out, ws, ws_bytes, stream=None):
+    _check(ctx, load_library().slim_forward_ws(ctx, seg, r_prev, r, batch, _ptr(x), _ptr(out), _ptr(ws), ws_bytes,
+                                               _stream(stream)))
+
+
+def slim_chain_workspace_bytes(ctx, r_per_seg, batch) -> int:
+    r4 = (ctypes.c_float * 4)(*r_per_seg)
+    return load_library().slim_chain_workspace_bytes(ctx, r4, batch)
+
+
+def slim_forward_chain(ctx, r_per_seg, batch, x, logits, ws, ws_bytes, stream=None):
+    r4 = (ctypes.c_float * 4)(*r_per_seg)
+    _check(ctx, load_library().slim_forward_chain(ctx, r4, batch, _ptr(x), _ptr(logits), _ptr(ws), ws_bytes,
+                                                  _stream(stream)))
+
+
+def slim_pack(cfg: slim_config, requests, B_max: int):
+    """Greedy key batching (host only, no GPU).  requests: iterable of (id, seg, w_req, w_prev, slot).
+    Returns (descs list of dicts, order ndarray)."""
+    reqs = list(requests)
+    n = len(reqs)
+    q = (slim_request * max(n, 1))()
+    for i, (rid, seg, wr, wp, slot) in enumerate(reqs):
+        q[i] = slim_request(rid, seg, wr, wp, slot)
+    descs = (slim_launch_desc * max(n, 1))()
+    order = (ctypes.c_uint32 * max(n, 1))()
+    nd = ctypes.c_int()
+    _check(None, load_library().slim_pack(ctypes.byref(cfg), q, n, B_max, descs, max(n, 1), ctypes.byref(nd), order))
+    out = [dict(seg=d.seg, r_prev=d.r_prev, r=d.r, batch=d.batch, first=d.first) for d in descs[:nd.value]]
+    return out, np.frombuffer(order, dtype=np.uint32, count=n).copy()
+
+
+def slim_launch(ctx, desc: dict, slots, pool, pool_row_bytes, slab, out, ws, ws_bytes, stream=None):
+    d = slim_launch_desc(desc["seg"], desc["r_prev"], desc["r"], desc["batch"], desc.get("first", 0))
+    _check(ctx, load_library().slim_launch(ctx, ctypes.byref(d), _ptr(slots), _ptr(pool), pool_row_bytes,
+                                           _ptr(slab), _ptr(out), _ptr(ws), ws_bytes, _stream(stream)))
+
+
+def slim_gather(ctx, src, idx, n, row_bytes, dst, stream=None):
+    _check(ctx, load_library().slim_gather(ctx, _ptr(src), _ptr(idx), n, row_bytes, _ptr(dst), _stream(stream)))
+
+
+def slim_last_error(ctx) -> int:
+    return load_library().slim_last_error(ctx)
+
+
+def slim_launch_count(ctx) -> int:
+    return load_library().slim_launch_count(ctx)
+
+
+def slim_channels(r: float, C: int) -> int:
+    return load_library().slim_channels(r, C)
+
+
+# ------------------------------------------------------------------ convenience
+class SlimNet:
+    """A context with all four segments loaded from named weights.
+
+    weights: dict layer name -> KRSC fp32 array (+ "fc_w", "fc_b");
+    bn: dict layer name -> list over widths of dict(gamma, beta, mean, var).
+    """
+
+    def __init__(self, weights: dict, bn: dict, device: int = 0, segments=(0, 1, 2, 3), **cfg_kw):
+        self.cfg = default_config(**cfg_kw)
+        self.ctx = slim_create(device, self.cfg)
+        self.widths = tuple(self.cfg.widths[i] for i in range(self.cfg.n_widths))
+        blocks = tuple(self.cfg.blocks_per_seg)
+        for s in segments:
+            names = manifest(s, blocks)
+            conv = [weights[n] for n in names]
+            bn_sets = [[bn[n][wi] for n in names] for wi in range(self.cfg.n_widths)]
+            if s == 3:
+                slim_load_segment(self.ctx, s, conv, bn_sets, weights["fc_w"], weights["fc_b"])
+            else:
+                slim_load_segment(self.ctx, s, conv, bn_sets)
+        self._ws = {}
+
+    @property
+    def act_dtype(self):
+        import torch
+        return torch.bfloat16 if self.cfg.dtype == SLIM_BF16 else torch.float32
+
+    def chain_workspace(self, r_per_seg, batch):
+        import torch
+        nbytes = slim_chain_workspace_bytes(self.ctx, r_per_seg, batch)
+        key = ("chain", nbytes)
+        if key not in self._ws:
+            self._ws = {key: torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{self.device_index}")}
+        return self._ws[key], nbytes
+
+    @property
+    def device_index(self):
+        import torch
+        return torch.cuda.current_device()
+
+    def forward_chain(self, x, r_per_seg, logits=None, stream=None):
+        """x: [B,32,32,3] device tensor of act_dtype.  Returns fp32 logits [B, classes]."""
+        import torch
+        B = x.shape[0]
+        if logits is None:
+            logits = torch.empty(B, self.cfg.num_classes, dtype=torch.float32, device=x.device)
+        ws, nbytes = self.chain_workspace(r_per_seg, B)
+        slim_forward_chain(self.ctx, r_per_seg, B, x, logits, ws, nbytes, stream)
+        return logits
+
+    def segment_out_shape(self, seg, r, B):
+        if seg == 3:
+            return (B, self.cfg.num_classes)
+        H = self.cfg.image_hw >> seg
+        return (B, H, H, slim_channels(r, self.cfg.base_channels[seg]))
+
+    def forward(self, seg, x, r_prev, r, out=None, stream=None):
+        import torch
+        B = x.shape[0]
+        if out is None:
+            dt = torch.float32 if seg == 3 else self.act_dtype
+            out = torch.empty(self.segment_out_shape(seg, r, B), dtype=dt, device=x.device)
+        slim_forward(self.ctx, seg, r_prev, r, B, x, out, stream)
+        return out
+
+    def close(self):
+        if self.ctx:
+            slim_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

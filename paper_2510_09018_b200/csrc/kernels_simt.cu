@@ -1,0 +1,250 @@
+// kernels_simt.cu -- the CUDA-core kernels of the hot path.
+//
+//  * stem: conv3x3 3->c0 + BN + ReLU.  K = 27, arithmetic intensity
+//    ~25 FLOP/B: HBM-bound, and a 6-byte pixel stride is not TMA-addressable, so
+//    it is a direct conv with the weights and a halo'd input tile in shared memory
+//    and 16-byte vector stores (8 output channels per thread).
+//  * head: global average pool over the 4x4 map + FC c3 -> classes,
+//    fp32 logits.  One CTA per image; pooled vector in smem; one warp per class
+//    group with a warp-shuffle dot product.
+//  * gather: 16-byte vectorised, coalesced row gather for the packer.
+//  * FP32 mode ("FP32/TF32-off"): a register-tiled direct conv with the
+//    same three fused epilogues, plain FFMA (tcgen05 has no fp32-input kind).
+#include "slim_internal.h"
+
+#include <cuda_bf16.h>
+
+namespace slim {
+namespace {
+
+__device__ __forceinline__ float bf16_to_f(uint16_t h) { return __uint_as_float(static_cast<uint32_t>(h) << 16); }
+__device__ __forceinline__ uint32_t pack2(float lo, float hi) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
+    return *reinterpret_cast<uint32_t *>(&h);
+}
+
+template <typename T> __device__ __forceinline__ float ld_act(const T *p);
+template <> __device__ __forceinline__ float ld_act<uint16_t>(const uint16_t *p) { return bf16_to_f(*p); }
+template <> __device__ __forceinline__ float ld_act<float>(const float *p) { return *p; }
+
+// ---------------------------------------------------------------- stem
+// Block: one image x kStemRows output rows, all W columns.  Threads map to
+// (pixel, group of 8 output channels) so consecutive threads store consecutive
+// 16-byte (bf16) / 32-byte (fp32) pieces: fully coalesced.
+constexpr int kStemRows = 4;
+constexpr int kStemThreads = 256;
+constexpr int kMaxStemW = 64, kMaxStemC = 4, kMaxStemCout = 64;
+
+template <typename TIn, typename TOut>
+__global__ void __launch_bounds__(kStemThreads)
+    stem_kernel(const TIn *__restrict__ in, const float *__restrict__ w, int cin_full, const float *__restrict__ scale,
+                const float *__restrict__ shift, TOut *__restrict__ out, int H, int W, int cimg, int c0) {
+    __shared__ float s_in[(kStemRows + 2) * (kMaxStemW + 2) * kMaxStemC];
+    __shared__ float s_w[kMaxStemCout * 9 * kMaxStemC];
+    const int n = blockIdx.y;
+    const int h0 = blockIdx.x * kStemRows;
+    const int TW = W + 2;
+    // halo'd input tile rows h0-1 .. h0+kStemRows, cols -1 .. W (zero padded)
+    for (int i = threadIdx.x; i < (kStemRows + 2) * TW * cimg; i += blockDim.x) {
+        const int c = i % cimg, col = (i / cimg) % TW, r = i / (cimg * TW);
+        const int ih = h0 + r - 1, iw = col - 1;
+        float v = 0.f;
+        if (ih >= 0 && ih < H && iw >= 0 && iw < W) v = ld_act(in + ((static_cast<size_t>(n) * H + ih) * W + iw) * cimg + c);
+        s_in[i] = v;
+    }
+    for (int i = threadIdx.x; i < c0 * 9 * cimg; i += blockDim.x) {
+        const int ci = i % cimg, tap = (i / cimg) % 9, co = i / (9 * cimg);
+        s_w[i] = w[(static_cast<size_t>(co) * 9 + tap) * cin_full + ci];
+    }
+    __syncthreads();
+    const int groups = c0 / 8;
+    const int items = kStemRows * W * groups;
+    for (int it = threadIdx.x; it < items; it += blockDim.x) {
+        const int g = it % groups, pix = it / groups;
+        const int r = pix / W, col = pix % W;
+        if (h0 + r >= H) continue;
+        float acc[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j] = 0.f;
+        for (int kh = 0; kh < 3; ++kh)
+            for (int kw = 0; kw < 3; ++kw)
+                for (int ci = 0; ci < cimg; ++ci) {
+                    const float x = s_in[((r + kh) * TW + col + kw) * cimg + ci];
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) acc[j] = fmaf(x, s_w[((g * 8 + j) * 9 + kh * 3 + kw) * cimg + ci], acc[j]);
+                }
+        const size_t o = ((static_cast<size_t>(n) * H + h0 + r) * W + col) * c0 + g * 8;
+        float y[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) y[j] = fmaxf(fmaf(acc[j], scale[g * 8 + j], shift[g * 8 + j]), 0.f);
+        if constexpr (sizeof(TOut) == 2) {
+            uint4 v = make_uint4(pack2(y[0], y[1]), pack2(y[2], y[3]), pack2(y[4], y[5]), pack2(y[6], y[7]));
+            *reinterpret_cast<uint4 *>(out + o) = v;
+        } else {
+            *reinterpret_cast<float4 *>(out + o) = make_float4(y[0], y[1], y[2], y[3]);
+            *reinterpret_cast<float4 *>(out + o + 4) = make_float4(y[4], y[5], y[6], y[7]);
+        }
+    }
+}
+
+// ---------------------------------------------------------------- head
+constexpr int kHeadThreads = 256;
+template <typename TIn>
+__global__ void __launch_bounds__(kHeadThreads)
+    head_kernel(const TIn *__restrict__ in, const float *__restrict__ fc_w, const float *__restrict__ fc_b,
+                float *__restrict__ logits, int P, int c3, int c3_full, int K) {
+    extern __shared__ float s_p[];
+    const int n = blockIdx.x;
+    const TIn *x = in + static_cast<size_t>(n) * P * c3;
+    const float inv = 1.f / static_cast<float>(P);
+    for (int c = threadIdx.x; c < c3; c += blockDim.x) {   // consecutive threads: consecutive channels
+        float s = 0.f;
+        for (int p = 0; p < P; ++p) s += ld_act(x + static_cast<size_t>(p) * c3 + c);
+        s_p[c] = s * inv;
+    }
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    for (int k = warp; k < K; k += nw) {
+        const float *wr = fc_w + static_cast<size_t>(k) * c3_full;
+        float d = 0.f;
+        for (int c = lane; c < c3; c += 32) d = fmaf(s_p[c], __ldg(wr + c), d);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+        if (lane == 0) logits[static_cast<size_t>(n) * K + k] = d + fc_b[k];
+    }
+}
+
+// ---------------------------------------------------------------- gather
+__global__ void gather_kernel(const uint4 *__restrict__ src, size_t src_stride, const uint32_t *__restrict__ idx, int n,
+                              size_t per_row, uint4 *__restrict__ dst) {
+    const size_t total = static_cast<size_t>(n) * per_row;
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const size_t r = i / per_row, off = i - r * per_row;
+        dst[i] = __ldg(src + static_cast<size_t>(idx[r]) * src_stride + off);
+    }
+}
+
+// ---------------------------------------------------------------- FP32 conv
+// One thread computes 4 output pixels (along W) x 4 output channels; weights
+// for the CTA's 32 output channels of one tap-chunk are staged in smem.
+constexpr int kF32Threads = 128;
+__global__ void __launch_bounds__(kF32Threads) conv_f32_kernel(const ConvF32Args a) {
+    const int co_base = blockIdx.y * 32;
+    const int tid = threadIdx.x;
+    const int cq = tid & 7;            // channel quad: co_base + 4*cq .. +3
+    const int pg = tid >> 3;           // pixel group (16 per CTA), 4 pixels each
+    const long pix0 = (static_cast<long>(blockIdx.x) * 16 + pg) * 4;
+    const long npix = static_cast<long>(a.B) * a.Ho * a.Wo;
+    float acc[4][4], acc1[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = acc1[i][j] = 0.f;
+    int pn[4], poh[4], pow_[4];
+    bool pv[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const long p = pix0 + i;
+        pv[i] = p < npix;
+        const long pp = pv[i] ? p : 0;
+        pn[i] = static_cast<int>(pp / (a.Ho * a.Wo));
+        poh[i] = static_cast<int>((pp / a.Wo) % a.Ho);
+        pow_[i] = static_cast<int>(pp % a.Wo);
+    }
+    const int co = co_base + cq * 4;
+    for (int part = 0; part < (a.epi == EPI_BN_PROJ_RELU ? 2 : 1); ++part) {
+        const float *x = part ? a.x1 : a.x;
+        const float *w = part ? a.w1 : a.w;
+        const int H = part ? a.H1 : a.H, W = part ? a.W1 : a.W, cin = part ? a.c_in1 : a.c_in;
+        const int k = part ? 1 : a.k, st = part ? a.stride1 : a.stride, pad = part ? 0 : a.pad;
+        const int cin_full = part ? a.cin1_full : a.cin_full;
+        float(*ac)[4] = part ? acc1 : acc;
+        for (int kh = 0; kh < k; ++kh)
+            for (int kw = 0; kw < k; ++kw) {
+                const float *xr[4];
+                bool ok[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int ih = st * poh[i] + kh - pad, iw = st * pow_[i] + kw - pad;
+                    ok[i] = pv[i] && ih >= 0 && ih < H && iw >= 0 && iw < W;
+                    xr[i] = x + ((static_cast<size_t>(pn[i]) * H + (ok[i] ? ih : 0)) * W + (ok[i] ? iw : 0)) * cin;
+                }
+                const float *wr[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    wr[j] = w + ((static_cast<size_t>(co + j < a.c_out ? co + j : 0) * k + kh) * k + kw) * cin_full;
+                for (int ci = 0; ci < cin; ++ci) {
+                    float xv[4], wv[4];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) xv[i] = ok[i] ? __ldg(xr[i] + ci) : 0.f;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) wv[j] = __ldg(wr[j] + ci);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) ac[i][j] = fmaf(xv[i], wv[j], ac[i][j]);
+                }
+            }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        if (!pv[i]) continue;
+        const size_t o = static_cast<size_t>(pix0 + i) * a.c_out;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int c = co + j;
+            if (c >= a.c_out) continue;
+            float f = fmaf(acc[i][j], a.scale0[c], a.shift0[c]);
+            if (a.epi == EPI_BN_PROJ_RELU) f += fmaf(acc1[i][j], a.scale1[c], a.shift1[c]);
+            if (a.epi == EPI_BN_ADD_RELU) f += a.res[o + c];
+            a.out[o + c] = fmaxf(f, 0.f);
+        }
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_stem_bf16(const uint16_t *in, const float *w, int cin_full, const float *scale, const float *shift,
+                             uint16_t *out, int B, int H, int W, int cimg, int c0, cudaStream_t s) {
+    if (W > kMaxStemW || cimg > kMaxStemC || c0 > kMaxStemCout || c0 % 8) return cudaErrorInvalidValue;
+    dim3 grid((H + kStemRows - 1) / kStemRows, B);
+    stem_kernel<uint16_t, uint16_t><<<grid, kStemThreads, 0, s>>>(in, w, cin_full, scale, shift, out, H, W, cimg, c0);
+    return cudaGetLastError();
+}
+cudaError_t launch_stem_f32(const float *in, const float *w, int cin_full, const float *scale, const float *shift,
+                            float *out, int B, int H, int W, int cimg, int c0, cudaStream_t s) {
+    if (W > kMaxStemW || cimg > kMaxStemC || c0 > kMaxStemCout || c0 % 8) return cudaErrorInvalidValue;
+    dim3 grid((H + kStemRows - 1) / kStemRows, B);
+    stem_kernel<float, float><<<grid, kStemThreads, 0, s>>>(in, w, cin_full, scale, shift, out, H, W, cimg, c0);
+    return cudaGetLastError();
+}
+cudaError_t launch_head_bf16(const uint16_t *in, const float *fc_w, const float *fc_b, float *logits, int B, int P,
+                             int c3, int c3_full, int K, cudaStream_t s) {
+    head_kernel<uint16_t><<<B, kHeadThreads, c3 * sizeof(float), s>>>(in, fc_w, fc_b, logits, P, c3, c3_full, K);
+    return cudaGetLastError();
+}
+cudaError_t launch_head_f32(const float *in, const float *fc_w, const float *fc_b, float *logits, int B, int P, int c3,
+                            int c3_full, int K, cudaStream_t s) {
+    head_kernel<float><<<B, kHeadThreads, c3 * sizeof(float), s>>>(in, fc_w, fc_b, logits, P, c3, c3_full, K);
+    return cudaGetLastError();
+}
+cudaError_t launch_gather(const void *src, size_t src_stride, const uint32_t *idx, int n, size_t row_bytes, void *dst,
+                          cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    const size_t per_row = row_bytes / 16;
+    const size_t total = per_row * n;
+    int blocks = static_cast<int>((total + 255) / 256);
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    gather_kernel<<<blocks, 256, 0, s>>>(static_cast<const uint4 *>(src), src_stride / 16, idx, n, per_row,
+                                         static_cast<uint4 *>(dst));
+    return cudaGetLastError();
+}
+cudaError_t launch_conv_f32(const ConvF32Args &a, cudaStream_t s) {
+    const long npix = static_cast<long>(a.B) * a.Ho * a.Wo;
+    dim3 grid(static_cast<unsigned>((npix + 63) / 64), (a.c_out + 31) / 32);
+    conv_f32_kernel<<<grid, kF32Threads, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+}  // namespace slim

@@ -1,0 +1,790 @@
+// slim_api.cu -- the C-ABI (include/slim.h): context, weight store, BN fold,
+// tensor-map cache, segment/chain sequencing, batch packer and launcher.
+//
+// Host-side only; every arithmetic step of the forward pass runs in the kernels
+// of kernels_umma.cu / kernels_simt.cu.  Citations: P:n = PAPER.md line n.
+#include "slim_internal.h"
+
+#include "../../include/slim.h"
+
+#include <atomic>
+#include <cstdarg>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+using namespace slim;
+
+namespace {
+
+constexpr int kMaxLayers = 16;
+constexpr int kMaxW = 8;
+
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                    const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+struct LayerShape {
+    int cout, cin, k, stride;
+    bool is_stem, reads_prev;   // reads_prev: input width is the previous segment's (block 0 c1 / sc of seg>0)
+};
+
+struct DevLayer {
+    LayerShape sh{};
+    void *w = nullptr;                       // full-width KRSC, bf16 (BF16 mode) or fp32; stem: fp32
+    float *scale[kMaxW] = {};                // folded BN per width, length c(width, cout)
+    float *shift[kMaxW] = {};
+    CUtensorMap tm[kMaxW][kMaxW];            // weight tensor map per (r_prev idx, r idx)
+    bool tm_ok[kMaxW][kMaxW] = {};
+};
+
+struct DevSegment {
+    bool loaded = false;
+    int n_conv = 0;
+    DevLayer L[kMaxLayers];
+    float *fc_w = nullptr, *fc_b = nullptr;
+};
+
+}  // namespace
+
+struct slim_ctx {
+    int device = 0;
+    slim_config cfg{};
+    int num_sms = 148;
+    DevSegment seg[4];
+    void *ws = nullptr;
+    size_t ws_bytes = 0;
+    std::atomic<uint64_t> launches{0};
+    slim_status sticky = SLIM_OK;
+    std::string msg;
+    PFN_encodeTiled encode = nullptr;
+    std::mutex mu;   // guards the lazily filled tensor-map cache
+};
+
+extern "C" int slim_channels(float r, int C) {
+    // c(r, C) = ceil(r*C) (north_star); integer form for r = k/4 (exact for the width set of P:148)
+    const double q = static_cast<double>(r) * 4.0;
+    if (std::fabs(q - std::round(q)) < 1e-6) return (static_cast<int>(std::lround(q)) * C + 3) / 4;
+    return static_cast<int>(std::ceil(static_cast<double>(r) * C - 1e-9));
+}
+
+namespace {
+
+slim_status fail(slim_ctx *ctx, slim_status s, const char *fmt, ...) __attribute__((format(printf, 3, 4)));
+slim_status fail(slim_ctx *ctx, slim_status s, const char *fmt, ...) {
+    if (ctx) {
+        char buf[512];
+        va_list ap;
+        va_start(ap, fmt);
+        vsnprintf(buf, sizeof buf, fmt, ap);
+        va_end(ap);
+        ctx->msg = buf;
+        if (s == SLIM_ECUDA) ctx->sticky = SLIM_ECUDA;
+    }
+    return s;
+}
+
+int width_index(const slim_config &c, float r) {
+    for (int i = 0; i < c.n_widths; ++i)
+        if (std::fabs(c.widths[i] - r) < 1e-6f) return i;
+    return -1;
+}
+
+int seg_hw(const slim_config &c, int s) { return c.image_hw >> s; }
+size_t elem_bytes(const slim_config &c) { return c.dtype == SLIM_BF16 ? 2 : 4; }
+size_t round256(size_t x) { return (x + 255) & ~size_t(255); }
+bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+// Manifest of one segment's conv layers (include/slim.h, slim_seg_weights).
+int segment_layers(const slim_config &c, int s, LayerShape *out) {
+    int n = 0;
+    const int C = c.base_channels[s];
+    if (s == 0) out[n++] = LayerShape{C, c.in_channels, 3, 1, true, false};
+    for (int b = 0; b < c.blocks_per_seg[s]; ++b) {
+        const bool down = (s > 0 && b == 0);
+        const int cin = down ? c.base_channels[s - 1] : C;
+        out[n++] = LayerShape{C, cin, 3, down ? 2 : 1, false, down};
+        out[n++] = LayerShape{C, C, 3, 1, false, false};
+        if (down) out[n++] = LayerShape{C, cin, 1, 2, false, true};
+    }
+    return n;
+}
+
+// index of block b's (c1, c2, sc) in the manifest
+struct BlockIdx {
+    int c1, c2, sc;
+};
+BlockIdx block_layers(const slim_config &c, int s, int b) {
+    int i = (s == 0) ? 1 : 0;
+    for (int bb = 0; bb < b; ++bb) i += (s > 0 && bb == 0) ? 3 : 2;
+    BlockIdx r{i, i + 1, (s > 0 && b == 0) ? i + 2 : -1};
+    return r;
+}
+
+size_t act_bytes(const slim_config &c, int s, float r, int B) {
+    const int H = seg_hw(c, s);
+    return static_cast<size_t>(B) * H * H * slim_channels(r, c.base_channels[s]) * elem_bytes(c);
+}
+size_t seg_ws_bytes(const slim_config &c, int s, float r, int B) { return 3 * round256(act_bytes(c, s, r, B)); }
+
+uint16_t f2bf(float f) {   // round-to-nearest-even (NaN kept NaN)
+    uint32_t u;
+    std::memcpy(&u, &f, 4);
+    if ((u & 0x7F800000u) == 0x7F800000u && (u & 0x7FFFFFu)) return static_cast<uint16_t>((u >> 16) | 0x40);
+    u += 0x7FFFu + ((u >> 16) & 1u);
+    return static_cast<uint16_t>(u >> 16);
+}
+float bf_round(float f) {
+    uint32_t u = static_cast<uint32_t>(f2bf(f)) << 16;
+    float r;
+    std::memcpy(&r, &u, 4);
+    return r;
+}
+
+#define CUDA_TRY(ctx, expr)                                                                            \
+    do {                                                                                               \
+        cudaError_t e__ = (expr);                                                                      \
+        if (e__ != cudaSuccess) return fail((ctx), SLIM_ECUDA, "%s: %s", #expr, cudaGetErrorString(e__)); \
+    } while (0)
+
+bool encode_map(slim_ctx *ctx, CUtensorMap *tm, const void *ptr, int rank, const cuuint64_t *dims,
+                const cuuint64_t *strides, const cuuint32_t *box, const cuuint32_t *es) {
+    CUresult r = ctx->encode(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void *>(ptr), dims, strides, box,
+                             es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+// Activation NHWC [B][H][W][C] bf16 as a 4-D map (C, W, H, B); box (64, bw, bh, bn), traversal stride es in H, W.
+bool encode_act(slim_ctx *ctx, CUtensorMap *tm, const void *ptr, int B, int H, int W, int C, int bw, int bh, int bn,
+                int es) {
+    cuuint64_t dims[4] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)B};
+    cuuint64_t strides[3] = {(cuuint64_t)C * 2, (cuuint64_t)W * C * 2, (cuuint64_t)H * W * C * 2};
+    cuuint32_t box[4] = {(cuuint32_t)kChunk, (cuuint32_t)bw, (cuuint32_t)bh, (cuuint32_t)bn};
+    cuuint32_t est[4] = {1, (cuuint32_t)es, (cuuint32_t)es, 1};
+    return encode_map(ctx, tm, ptr, 4, dims, strides, box, est);
+}
+
+// Weights KRSC [Cout_full][k*k][Cin_full] bf16 as a 3-D map whose BOUNDS are the
+// active prefix (c_in, k*k, c_out): the slice is selected by predication.
+bool encode_w(slim_ctx *ctx, CUtensorMap *tm, const DevLayer &L, int c_in, int c_out, int n_tile) {
+    const int kk = L.sh.k * L.sh.k;
+    cuuint64_t dims[3] = {(cuuint64_t)c_in, (cuuint64_t)kk, (cuuint64_t)c_out};
+    cuuint64_t strides[2] = {(cuuint64_t)L.sh.cin * 2, (cuuint64_t)kk * L.sh.cin * 2};
+    cuuint32_t box[3] = {(cuuint32_t)kChunk, 1, (cuuint32_t)n_tile};
+    cuuint32_t est[3] = {1, 1, 1};
+    return encode_map(ctx, tm, L.w, 3, dims, strides, box, est);
+}
+
+int pick_n_tile(int c_out) {
+    int nt = (c_out + 255) / 256;
+    while (c_out % nt || (c_out / nt) % 16) ++nt;
+    return c_out / nt;
+}
+
+const CUtensorMap *weight_map(slim_ctx *ctx, DevLayer &L, int ri_in, int ri, int c_in, int c_out) {
+    std::lock_guard<std::mutex> g(ctx->mu);
+    if (!L.tm_ok[ri_in][ri]) {
+        if (!encode_w(ctx, &L.tm[ri_in][ri], L, c_in, c_out, pick_n_tile(c_out))) return nullptr;
+        L.tm_ok[ri_in][ri] = true;
+    }
+    return &L.tm[ri_in][ri];
+}
+
+// One tcgen05 conv launch: out = epi(conv(x; L) [, proj(xp; Lp)] [, res]).
+slim_status conv_bf16(slim_ctx *ctx, cudaStream_t st, DevLayer &L, int ri_in, int ri, const void *x, int B, int H,
+                      int W, int c_in, DevLayer *Lp, int ri_in_p, const void *xp, int Hp, int Wp, int c_in_p,
+                      const void *res, void *out, int epi) {
+    const slim_config &c = ctx->cfg;
+    const int k = L.sh.k, s = L.sh.stride, pad = k / 2;
+    const int Ho = (H + 2 * pad - k) / s + 1, Wo = (W + 2 * pad - k) / s + 1;
+    const int c_out = slim_channels(c.widths[ri], L.sh.cout);
+    ConvArgs a{};
+    a.B = B;
+    a.Ho = Ho;
+    a.Wo = Wo;
+    const int P = Ho * Wo;
+    if (P >= kTileM) {
+        if (P % kTileM || kTileM % Wo) return fail(ctx, SLIM_EUNSUPPORTED, "conv: output %dx%d not tileable", Ho, Wo);
+        a.tile_imgs = 1;
+        a.tile_rows = kTileM / Wo;
+        a.tiles_per_img = Ho / a.tile_rows;
+        a.m_tiles = B * a.tiles_per_img;
+    } else {
+        if (kTileM % P) return fail(ctx, SLIM_EUNSUPPORTED, "conv: output %dx%d not tileable", Ho, Wo);
+        a.tile_imgs = kTileM / P;
+        a.tile_rows = Ho;
+        a.tiles_per_img = 1;
+        a.m_tiles = (B + a.tile_imgs - 1) / a.tile_imgs;
+    }
+    a.n_tile = pick_n_tile(c_out);
+    a.n_tiles = c_out / a.n_tile;
+    a.c_out = c_out;
+    a.n_parts = (epi == EPI_BN_PROJ_RELU) ? 2 : 1;
+    a.part[0] = GemmPart{k, s, pad, c_in, (c_in + kChunk - 1) / kChunk, 0};
+    a.part[0].n_kblocks = k * k * a.part[0].n_chunks;
+    if (a.n_parts == 2) {
+        a.part[1] = GemmPart{Lp->sh.k, Lp->sh.stride, 0, c_in_p, (c_in_p + kChunk - 1) / kChunk, 0};
+        a.part[1].n_kblocks = a.part[1].n_chunks;
+    }
+    a.epi = epi;
+    a.scale0 = L.scale[ri];
+    a.shift0 = L.shift[ri];
+    if (a.n_parts == 2) {
+        a.scale1 = Lp->scale[ri];
+        a.shift1 = Lp->shift[ri];
+    }
+    a.acc_stride = (a.n_tile + 31) / 32 * 32;
+    a.acc_stages = 512 / (a.n_parts * a.acc_stride) >= 2 ? 2 : 1;
+    int cols = a.acc_stages * a.n_parts * a.acc_stride, tc = 32;
+    while (tc < cols) tc <<= 1;
+    a.tmem_cols = tc;
+    a.stage_b_bytes = static_cast<uint32_t>(a.n_tile) * 128;
+    a.n_out_chunks = static_cast<uint32_t>((a.n_tile + kChunk - 1) / kChunk);
+    // pipeline depth: two CTAs per SM for narrow tiles (more latency hiding on the
+    // HBM-bound layers), one for wide tiles; 2..8 stages in what remains.
+    const bool two = a.n_tile <= 64;
+    const size_t budget = two ? 113 * 1024 : 226 * 1024;
+    const size_t fixed = 1024 + a.n_out_chunks * 16384 + 8 * (2 * kMaxStages + 5) + 16;
+    int stages = static_cast<int>((budget - fixed) / (kTileABytes + a.stage_b_bytes));
+    a.n_stages = stages < 2 ? 2 : (stages > kMaxStages ? kMaxStages : stages);
+
+    CUtensorMap tA0, tA1, tRes, tOut;
+    if (!encode_act(ctx, &tA0, x, B, H, W, c_in, s * Wo, s * a.tile_rows, a.tile_imgs, s))
+        return fail(ctx, SLIM_ECUDA, "cuTensorMapEncodeTiled(A) failed");
+    const CUtensorMap *tB0 = weight_map(ctx, L, ri_in, ri, c_in, c_out);
+    const CUtensorMap *tB1 = tB0;
+    if (!tB0) return fail(ctx, SLIM_ECUDA, "cuTensorMapEncodeTiled(W) failed");
+    tA1 = tA0;
+    if (a.n_parts == 2) {
+        const int sp = Lp->sh.stride;
+        if (!encode_act(ctx, &tA1, xp, B, Hp, Wp, c_in_p, sp * Wo, sp * a.tile_rows, a.tile_imgs, sp))
+            return fail(ctx, SLIM_ECUDA, "cuTensorMapEncodeTiled(A1) failed");
+        tB1 = weight_map(ctx, *Lp, ri_in_p, ri, c_in_p, c_out);
+        if (!tB1) return fail(ctx, SLIM_ECUDA, "cuTensorMapEncodeTiled(W1) failed");
+    }
+    if (!encode_act(ctx, &tOut, out, B, Ho, Wo, c_out, Wo, a.tile_rows, a.tile_imgs, 1))
+        return fail(ctx, SLIM_ECUDA, "cuTensorMapEncodeTiled(out) failed");
+    tRes = tOut;
+    if (epi == EPI_BN_ADD_RELU && !encode_act(ctx, &tRes, res, B, Ho, Wo, c_out, Wo, a.tile_rows, a.tile_imgs, 1))
+        return fail(ctx, SLIM_ECUDA, "cuTensorMapEncodeTiled(res) failed");
+
+    const size_t smem = conv_umma_smem_bytes(a);
+    const int per_sm = conv_umma_max_ctas_per_sm(smem);
+    const int total = a.m_tiles * a.n_tiles;
+    int grid = ctx->num_sms * per_sm;
+    if (grid > total) grid = total;
+    cudaError_t e = launch_conv_umma(a, tA0, *tB0, tA1, *tB1, tRes, tOut, grid, st);
+    ctx->launches++;
+    if (e != cudaSuccess) return fail(ctx, SLIM_ECUDA, "conv_umma launch: %s", cudaGetErrorString(e));
+    return SLIM_OK;
+}
+
+slim_status conv_f32(slim_ctx *ctx, cudaStream_t st, DevLayer &L, int ri, const void *x, int B, int H, int W,
+                     int c_in, DevLayer *Lp, const void *xp, int Hp, int Wp, int c_in_p, const void *res, void *out,
+                     int epi) {
+    const int k = L.sh.k, s = L.sh.stride, pad = k / 2;
+    ConvF32Args a{};
+    a.x = static_cast<const float *>(x);
+    a.B = B;
+    a.H = H;
+    a.W = W;
+    a.c_in = c_in;
+    a.w = static_cast<const float *>(L.w);
+    a.cin_full = L.sh.cin;
+    a.k = k;
+    a.stride = s;
+    a.pad = pad;
+    a.Ho = (H + 2 * pad - k) / s + 1;
+    a.Wo = (W + 2 * pad - k) / s + 1;
+    a.c_out = slim_channels(ctx->cfg.widths[ri], L.sh.cout);
+    a.scale0 = L.scale[ri];
+    a.shift0 = L.shift[ri];
+    if (epi == EPI_BN_PROJ_RELU) {
+        a.x1 = static_cast<const float *>(xp);
+        a.H1 = Hp;
+        a.W1 = Wp;
+        a.c_in1 = c_in_p;
+        a.stride1 = Lp->sh.stride;
+        a.w1 = static_cast<const float *>(Lp->w);
+        a.cin1_full = Lp->sh.cin;
+        a.scale1 = Lp->scale[ri];
+        a.shift1 = Lp->shift[ri];
+    }
+    a.res = static_cast<const float *>(res);
+    a.out = static_cast<float *>(out);
+    a.epi = epi;
+    cudaError_t e = launch_conv_f32(a, st);
+    ctx->launches++;
+    if (e != cudaSuccess) return fail(ctx, SLIM_ECUDA, "conv_f32 launch: %s", cudaGetErrorString(e));
+    return SLIM_OK;
+}
+
+slim_status check_sticky(slim_ctx *ctx) {
+    if (ctx->sticky != SLIM_OK) return ctx->sticky;
+    cudaError_t e = cudaPeekAtLastError();
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(ctx, SLIM_ECUDA, "asynchronous CUDA error: %s", cudaGetErrorString(e));
+    }
+    return SLIM_OK;
+}
+
+slim_status validate_fwd(slim_ctx *ctx, int seg, float r_prev, float r, int batch, const void *in, const void *out,
+                         int *ri_prev, int *ri) {
+    if (!ctx) return SLIM_EINVAL;
+    const slim_config &c = ctx->cfg;
+    if (seg < 0 || seg > 3) return fail(ctx, SLIM_EINVAL, "seg %d out of range", seg);
+    if (batch < 1 || batch > c.max_batch) return fail(ctx, SLIM_EINVAL, "batch %d not in [1, %d]", batch, c.max_batch);
+    *ri = width_index(c, r);
+    if (*ri < 0) return fail(ctx, SLIM_EINVAL, "width %g not in the slimming set", r);
+    *ri_prev = *ri;
+    if (seg > 0) {
+        *ri_prev = width_index(c, r_prev);
+        if (*ri_prev < 0) return fail(ctx, SLIM_EINVAL, "r_prev %g not in the slimming set", r_prev);
+    }
+    if (!in || !out || !aligned16(in) || !aligned16(out)) return fail(ctx, SLIM_EINVAL, "in/out NULL or not 16-B aligned");
+    if (!ctx->seg[seg].loaded) return fail(ctx, SLIM_ENOTLOADED, "segment %d not loaded", seg);
+    return SLIM_OK;
+}
+
+// The segment schedule (O5/O6 in SURVEY §8(c)); all buffers validated by the caller.
+slim_status run_segment(slim_ctx *ctx, int seg, int ri_prev, int ri, int B, const void *in, void *out, void *ws,
+                        cudaStream_t st) {
+    const slim_config &c = ctx->cfg;
+    DevSegment &S = ctx->seg[seg];
+    const bool bf = c.dtype == SLIM_BF16;
+    const float r = c.widths[ri];
+    const int H = seg_hw(c, seg);
+    const int C = slim_channels(r, c.base_channels[seg]);
+    const size_t buf = round256(act_bytes(c, seg, r, B));
+    char *bufs[3] = {static_cast<char *>(ws), static_cast<char *>(ws) + buf, static_cast<char *>(ws) + 2 * buf};
+    const void *cur = in;
+    int curH = (seg == 0) ? H : (H * 2), curC = (seg == 0) ? c.in_channels : slim_channels(c.widths[ri_prev], c.base_channels[seg - 1]);
+    if (seg == 0) {
+        DevLayer &Ls = S.L[0];
+        cudaError_t e = bf ? launch_stem_bf16(static_cast<const uint16_t *>(in), static_cast<const float *>(Ls.w),
+                                              Ls.sh.cin, Ls.scale[ri], Ls.shift[ri], reinterpret_cast<uint16_t *>(bufs[0]),
+                                              B, H, H, c.in_channels, C, st)
+                           : launch_stem_f32(static_cast<const float *>(in), static_cast<const float *>(Ls.w),
+                                             Ls.sh.cin, Ls.scale[ri], Ls.shift[ri], reinterpret_cast<float *>(bufs[0]),
+                                             B, H, H, c.in_channels, C, st);
+        ctx->launches++;
+        if (e != cudaSuccess) return fail(ctx, SLIM_ECUDA, "stem launch: %s", cudaGetErrorString(e));
+        cur = bufs[0];
+        curH = H;
+        curC = C;
+    }
+    const int nb = c.blocks_per_seg[seg];
+    for (int b = 0; b < nb; ++b) {
+        const BlockIdx bi = block_layers(c, seg, b);
+        const bool down = seg > 0 && b == 0;
+        const int ri_in = down ? ri_prev : ri;
+        // pick T and dst among the 3 workspace buffers, never aliasing cur
+        char *free_[3];
+        int nf = 0;
+        for (int i = 0; i < 3; ++i)
+            if (bufs[i] != cur) free_[nf++] = bufs[i];
+        char *T = free_[0];
+        void *dst = (b == nb - 1 && seg < 3) ? out : free_[1];
+        slim_status s1, s2;
+        if (bf) {
+            s1 = conv_bf16(ctx, st, S.L[bi.c1], ri_in, ri, cur, B, curH, curH, curC, nullptr, 0, nullptr, 0, 0, 0,
+                           nullptr, T, EPI_BN_RELU);
+            if (s1) return s1;
+            if (down)
+                s2 = conv_bf16(ctx, st, S.L[bi.c2], ri, ri, T, B, H, H, C, &S.L[bi.sc], ri_in, cur, curH, curH, curC,
+                               nullptr, dst, EPI_BN_PROJ_RELU);
+            else
+                s2 = conv_bf16(ctx, st, S.L[bi.c2], ri, ri, T, B, H, H, C, nullptr, 0, nullptr, 0, 0, 0, cur, dst,
+                               EPI_BN_ADD_RELU);
+        } else {
+            s1 = conv_f32(ctx, st, S.L[bi.c1], ri, cur, B, curH, curH, curC, nullptr, nullptr, 0, 0, 0, nullptr, T,
+                          EPI_BN_RELU);
+            if (s1) return s1;
+            if (down)
+                s2 = conv_f32(ctx, st, S.L[bi.c2], ri, T, B, H, H, C, &S.L[bi.sc], cur, curH, curH, curC, nullptr, dst,
+                              EPI_BN_PROJ_RELU);
+            else
+                s2 = conv_f32(ctx, st, S.L[bi.c2], ri, T, B, H, H, C, nullptr, nullptr, 0, 0, 0, cur, dst,
+                              EPI_BN_ADD_RELU);
+        }
+        if (s2) return s2;
+        cur = dst;
+        curH = H;
+        curC = C;
+    }
+    if (seg == 3) {
+        cudaError_t e = bf ? launch_head_bf16(static_cast<const uint16_t *>(cur), S.fc_w, S.fc_b,
+                                              static_cast<float *>(out), B, H * H, C, c.base_channels[3],
+                                              c.num_classes, st)
+                           : launch_head_f32(static_cast<const float *>(cur), S.fc_w, S.fc_b, static_cast<float *>(out),
+                                             B, H * H, C, c.base_channels[3], c.num_classes, st);
+        ctx->launches++;
+        if (e != cudaSuccess) return fail(ctx, SLIM_ECUDA, "head launch: %s", cudaGetErrorString(e));
+    }
+    return SLIM_OK;
+}
+
+void free_segment(DevSegment &S) {
+    for (int l = 0; l < S.n_conv; ++l) {
+        DevLayer &L = S.L[l];
+        cudaFree(L.w);
+        for (int i = 0; i < kMaxW; ++i) {
+            cudaFree(L.scale[i]);
+            cudaFree(L.shift[i]);
+        }
+        L = DevLayer{};
+    }
+    cudaFree(S.fc_w);
+    cudaFree(S.fc_b);
+    S = DevSegment{};
+}
+
+}  // namespace
+
+// =============================================================================
+extern "C" {
+
+int slim_version(void) { return 1; }
+
+const char *slim_status_str(slim_status s) {
+    switch (s) {
+        case SLIM_OK: return "SLIM_OK";
+        case SLIM_EINVAL: return "SLIM_EINVAL";
+        case SLIM_ENOTLOADED: return "SLIM_ENOTLOADED";
+        case SLIM_ENOMEM: return "SLIM_ENOMEM";
+        case SLIM_ECUDA: return "SLIM_ECUDA";
+        case SLIM_EUNSUPPORTED: return "SLIM_EUNSUPPORTED";
+    }
+    return "unknown";
+}
+
+void slim_default_config(slim_config *cfg) {
+    std::memset(cfg, 0, sizeof *cfg);
+    cfg->n_widths = 4;
+    cfg->widths[0] = 0.25f;
+    cfg->widths[1] = 0.5f;
+    cfg->widths[2] = 0.75f;
+    cfg->widths[3] = 1.0f;
+    for (int s = 0; s < 4; ++s) cfg->blocks_per_seg[s] = 2;
+    cfg->base_channels[0] = 64;
+    cfg->base_channels[1] = 128;
+    cfg->base_channels[2] = 256;
+    cfg->base_channels[3] = 512;
+    cfg->in_channels = 3;
+    cfg->num_classes = 100;
+    cfg->image_hw = 32;
+    cfg->max_batch = 4096;
+    cfg->bn_eps = 1e-5f;
+    cfg->dtype = SLIM_BF16;
+}
+
+slim_status slim_create(int device, const slim_config *cfg, slim_ctx **out) {
+    if (!out) return SLIM_EINVAL;
+    *out = nullptr;
+    if (!cfg) return SLIM_EINVAL;
+    const slim_config &c = *cfg;
+    if (c.n_widths < 1 || c.n_widths > kMaxW) return SLIM_EINVAL;
+    for (int i = 0; i < c.n_widths; ++i) {
+        if (!(c.widths[i] > 0.f && c.widths[i] <= 1.f)) return SLIM_EINVAL;
+        if (i && !(c.widths[i] > c.widths[i - 1])) return SLIM_EINVAL;
+    }
+    if (c.in_channels < 1 || c.in_channels > 4 || c.num_classes < 1 || c.num_classes > 1024 || c.max_batch < 1 ||
+        !(c.bn_eps > 0.f) || (c.dtype != SLIM_BF16 && c.dtype != SLIM_FP32))
+        return SLIM_EINVAL;
+    if (c.image_hw < 16 || c.image_hw % 8) return SLIM_EUNSUPPORTED;
+    for (int s = 0; s < 4; ++s) {
+        if (c.blocks_per_seg[s] < 1 || c.blocks_per_seg[s] > 4) return SLIM_EINVAL;
+        if (c.base_channels[s] < 16 || c.base_channels[s] > 1024) return SLIM_EINVAL;
+        for (int i = 0; i < c.n_widths; ++i) {   // kernels need channel prefixes in multiples of 16
+            const int ch = slim_channels(c.widths[i], c.base_channels[s]);
+            if (ch % 16) return SLIM_EUNSUPPORTED;
+            if (s == 0 && ch > 64) return SLIM_EUNSUPPORTED;   // stem kernel holds <= 64 output channels
+        }
+    }
+    slim_ctx *ctx = new slim_ctx();
+    ctx->device = device;
+    ctx->cfg = c;
+    if (cudaSetDevice(device) != cudaSuccess) {
+        delete ctx;
+        return SLIM_ECUDA;
+    }
+    cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
+    cudaDriverEntryPointQueryResult q;
+    void *fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn) {
+        delete ctx;
+        return SLIM_ECUDA;
+    }
+    ctx->encode = reinterpret_cast<PFN_encodeTiled>(fn);
+    // internal workspace for slim_forward: max over segments at the widest width, B_max
+    size_t ws = 0;
+    for (int s = 0; s < 4; ++s) {
+        const size_t b = seg_ws_bytes(c, s, c.widths[c.n_widths - 1], c.max_batch);
+        ws = b > ws ? b : ws;
+    }
+    if (cudaMalloc(&ctx->ws, ws) != cudaSuccess) {
+        cudaGetLastError();
+        delete ctx;
+        return SLIM_ENOMEM;
+    }
+    ctx->ws_bytes = ws;
+    *out = ctx;
+    return SLIM_OK;
+}
+
+void slim_destroy(slim_ctx *ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    for (int s = 0; s < 4; ++s) free_segment(ctx->seg[s]);
+    cudaFree(ctx->ws);
+    delete ctx;
+}
+
+int slim_segment_loaded(const slim_ctx *ctx, int seg) {
+    return ctx && seg >= 0 && seg < 4 && ctx->seg[seg].loaded ? 1 : 0;
+}
+
+slim_status slim_load_segment(slim_ctx *ctx, int seg, const slim_seg_weights *w, const slim_bn_set *bn) {
+    if (!ctx) return SLIM_EINVAL;
+    const slim_config &c = ctx->cfg;
+    if (seg < 0 || seg > 3 || !w || !bn) return fail(ctx, SLIM_EINVAL, "load: bad arguments");
+    LayerShape shp[kMaxLayers];
+    const int n = segment_layers(c, seg, shp);
+    if (w->n_conv != n) return fail(ctx, SLIM_EINVAL, "load: seg %d expects %d conv tensors, got %d", seg, n, w->n_conv);
+    for (int l = 0; l < n; ++l)
+        if (!w->conv_w[l]) return fail(ctx, SLIM_EINVAL, "load: conv_w[%d] is NULL", l);
+    if (seg == 3 && (!w->fc_w || !w->fc_b)) return fail(ctx, SLIM_EINVAL, "load: seg 3 needs fc_w and fc_b");
+    for (int i = 0; i < c.n_widths; ++i) {
+        if (bn[i].n_layers != n || !bn[i].per_layer)
+            return fail(ctx, SLIM_EINVAL, "load: BN set %d has %d layers, expected %d", i, bn[i].n_layers, n);
+        for (int l = 0; l < n; ++l) {
+            const slim_bn &b = bn[i].per_layer[l];
+            if (!b.gamma || !b.beta || !b.mean || !b.var) return fail(ctx, SLIM_EINVAL, "load: BN arrays NULL");
+        }
+    }
+    cudaSetDevice(ctx->device);
+    cudaDeviceSynchronize();   // no forward of this segment may be in flight (documented contract)
+    free_segment(ctx->seg[seg]);
+    DevSegment &S = ctx->seg[seg];
+    S.n_conv = n;
+    const bool bf = c.dtype == SLIM_BF16;
+    for (int l = 0; l < n; ++l) {
+        DevLayer &L = S.L[l];
+        L.sh = shp[l];
+        const size_t cnt = static_cast<size_t>(L.sh.cout) * L.sh.k * L.sh.k * L.sh.cin;
+        if (L.sh.is_stem || !bf) {   // CUDA-core kernels read fp32 (bf16-rounded in BF16 mode)
+            std::vector<float> h(w->conv_w[l], w->conv_w[l] + cnt);
+            if (bf)
+                for (auto &v : h) v = bf_round(v);
+            CUDA_TRY(ctx, cudaMalloc(&L.w, cnt * 4));
+            CUDA_TRY(ctx, cudaMemcpy(L.w, h.data(), cnt * 4, cudaMemcpyHostToDevice));
+        } else {
+            std::vector<uint16_t> h(cnt);
+            for (size_t i = 0; i < cnt; ++i) h[i] = f2bf(w->conv_w[l][i]);
+            CUDA_TRY(ctx, cudaMalloc(&L.w, cnt * 2));
+            CUDA_TRY(ctx, cudaMemcpy(L.w, h.data(), cnt * 2, cudaMemcpyHostToDevice));
+        }
+        // switchable BN, folded per width in fp64: s = gamma/sqrt(var+eps), t = beta - mean*s
+        for (int i = 0; i < c.n_widths; ++i) {
+            const int ch = slim_channels(c.widths[i], L.sh.cout);
+            const slim_bn &b = bn[i].per_layer[l];
+            std::vector<float> sc(ch), sh(ch);
+            for (int k = 0; k < ch; ++k) {
+                const double s = static_cast<double>(b.gamma[k]) /
+                                 std::sqrt(static_cast<double>(b.var[k]) + static_cast<double>(c.bn_eps));
+                sc[k] = static_cast<float>(s);
+                sh[k] = static_cast<float>(static_cast<double>(b.beta[k]) - static_cast<double>(b.mean[k]) * s);
+            }
+            CUDA_TRY(ctx, cudaMalloc(&L.scale[i], ch * 4));
+            CUDA_TRY(ctx, cudaMalloc(&L.shift[i], ch * 4));
+            CUDA_TRY(ctx, cudaMemcpy(L.scale[i], sc.data(), ch * 4, cudaMemcpyHostToDevice));
+            CUDA_TRY(ctx, cudaMemcpy(L.shift[i], sh.data(), ch * 4, cudaMemcpyHostToDevice));
+        }
+    }
+    if (seg == 3) {
+        const size_t fw = static_cast<size_t>(c.num_classes) * c.base_channels[3];
+        CUDA_TRY(ctx, cudaMalloc(&S.fc_w, fw * 4));
+        CUDA_TRY(ctx, cudaMalloc(&S.fc_b, c.num_classes * 4));
+        CUDA_TRY(ctx, cudaMemcpy(S.fc_w, w->fc_w, fw * 4, cudaMemcpyHostToDevice));
+        CUDA_TRY(ctx, cudaMemcpy(S.fc_b, w->fc_b, c.num_classes * 4, cudaMemcpyHostToDevice));
+    }
+    S.loaded = true;
+    return SLIM_OK;
+}
+
+slim_status slim_unload_segment(slim_ctx *ctx, int seg) {
+    if (!ctx || seg < 0 || seg > 3) return SLIM_EINVAL;
+    cudaSetDevice(ctx->device);
+    cudaDeviceSynchronize();
+    free_segment(ctx->seg[seg]);
+    return SLIM_OK;
+}
+
+size_t slim_segment_bytes(const slim_config *cfg, int seg, float r_prev, float r) {
+    if (!cfg || seg < 0 || seg > 3) return 0;
+    const slim_config &c = *cfg;
+    if (width_index(c, r) < 0 || (seg > 0 && width_index(c, r_prev) < 0)) return 0;
+    LayerShape shp[kMaxLayers];
+    const int n = segment_layers(c, seg, shp);
+    size_t bytes = 0;
+    for (int l = 0; l < n; ++l) {
+        const LayerShape &L = shp[l];
+        const int co = slim_channels(r, L.cout);
+        const int ci = L.is_stem ? L.cin : slim_channels(L.reads_prev ? r_prev : r, L.cin);
+        const size_t eb = (L.is_stem || c.dtype == SLIM_FP32) ? 4 : 2;
+        bytes += static_cast<size_t>(co) * L.k * L.k * ci * eb + 2 * static_cast<size_t>(co) * 4;
+    }
+    if (seg == 3) bytes += static_cast<size_t>(c.num_classes) * (slim_channels(r, c.base_channels[3]) + 1) * 4;
+    return bytes;
+}
+
+size_t slim_forward_workspace_bytes(const slim_ctx *ctx, int seg, float, float r, int batch) {
+    if (!ctx || seg < 0 || seg > 3 || batch < 1) return 0;
+    return seg_ws_bytes(ctx->cfg, seg, r, batch);
+}
+
+slim_status slim_forward_ws(slim_ctx *ctx, int seg, float r_prev, float r, int batch, const void *in, void *out,
+                            void *ws, size_t ws_bytes, void *stream) {
+    int ri_prev, ri;
+    slim_status s = validate_fwd(ctx, seg, r_prev, r, batch, in, out, &ri_prev, &ri);
+    if (s) return s;
+    if (!ws || !aligned16(ws) || ws_bytes < seg_ws_bytes(ctx->cfg, seg, r, batch))
+        return fail(ctx, SLIM_EINVAL, "workspace too small or misaligned");
+    if ((s = check_sticky(ctx))) return s;
+    return run_segment(ctx, seg, ri_prev, ri, batch, in, out, ws, static_cast<cudaStream_t>(stream));
+}
+
+slim_status slim_forward(slim_ctx *ctx, int seg, float r_prev, float r, int batch, const void *in, void *out,
+                         void *stream) {
+    if (!ctx) return SLIM_EINVAL;
+    return slim_forward_ws(ctx, seg, r_prev, r, batch, in, out, ctx->ws, ctx->ws_bytes, stream);
+}
+
+size_t slim_chain_workspace_bytes(const slim_ctx *ctx, const float r[4], int batch) {
+    if (!ctx || !r || batch < 1) return 0;
+    size_t inter = 0, segws = 0;
+    for (int s = 0; s < 4; ++s) {
+        const size_t a = round256(act_bytes(ctx->cfg, s, r[s], batch));
+        const size_t w = seg_ws_bytes(ctx->cfg, s, r[s], batch);
+        inter = a > inter ? a : inter;
+        segws = w > segws ? w : segws;
+    }
+    return 2 * inter + segws;
+}
+
+slim_status slim_forward_chain(slim_ctx *ctx, const float r[4], int batch, const void *in, float *logits, void *ws,
+                               size_t ws_bytes, void *stream) {
+    if (!ctx || !r) return SLIM_EINVAL;
+    int rip[4], ri[4];
+    slim_status s;
+    for (int k = 0; k < 4; ++k)
+        if ((s = validate_fwd(ctx, k, k ? r[k - 1] : r[0], r[k], batch, in, logits, &rip[k], &ri[k]))) return s;
+    const size_t need = slim_chain_workspace_bytes(ctx, r, batch);
+    if (!ws || !aligned16(ws) || ws_bytes < need) return fail(ctx, SLIM_EINVAL, "chain workspace too small");
+    if ((s = check_sticky(ctx))) return s;
+    size_t inter = 0;
+    for (int k = 0; k < 4; ++k) {
+        const size_t a = round256(act_bytes(ctx->cfg, k, r[k], batch));
+        inter = a > inter ? a : inter;
+    }
+    char *o[2] = {static_cast<char *>(ws), static_cast<char *>(ws) + inter};
+    char *segws = static_cast<char *>(ws) + 2 * inter;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const void *cur = in;
+    for (int k = 0; k < 4; ++k) {
+        void *dst = (k == 3) ? static_cast<void *>(logits) : o[k & 1];
+        if ((s = run_segment(ctx, k, rip[k], ri[k], batch, cur, dst, segws, st))) return s;
+        cur = dst;
+    }
+    return SLIM_OK;
+}
+
+slim_status slim_pack(const slim_config *cfg, const slim_request *q, int n, int B_max, slim_launch_desc *descs,
+                      int max_descs, int *n_descs, uint32_t *order) {
+    if (!cfg || n < 0 || B_max < 1 || !n_descs || (n > 0 && (!q || !descs || !order))) return SLIM_EINVAL;
+    *n_descs = 0;
+    const slim_config &c = *cfg;
+    // key -> FIFO of request indices; a key is (seg, w_req idx, w_prev idx)
+    std::unordered_map<int, std::vector<int>> buckets;
+    std::vector<int> key_of(n);
+    for (int i = 0; i < n; ++i) {
+        const int wr = width_index(c, q[i].w_req);
+        const int wp = q[i].seg == 0 ? 0 : width_index(c, q[i].w_prev);
+        if (q[i].seg < 0 || q[i].seg > 3 || wr < 0 || wp < 0) return SLIM_EINVAL;
+        key_of[i] = (q[i].seg * kMaxW + wr) * kMaxW + wp;
+        buckets[key_of[i]].push_back(i);
+    }
+    std::unordered_map<int, size_t> head;   // consumed prefix of each bucket
+    std::vector<char> taken(n, 0);
+    int pos = 0, nd = 0;
+    for (int i = 0; i < n; ++i) {   // Alg.1 LOOP: peek the FIFO head's key ...
+        if (taken[i]) continue;
+        if (nd >= max_descs) return SLIM_EINVAL;
+        std::vector<int> &bk = buckets[key_of[i]];
+        size_t &h = head[key_of[i]];
+        slim_launch_desc d;
+        d.seg = q[i].seg;
+        d.r = q[i].w_req;
+        d.r_prev = q[i].seg == 0 ? q[i].w_req : q[i].w_prev;
+        d.first = pos;
+        d.batch = 0;
+        while (h < bk.size() && d.batch < B_max) {   // ... FORM-BATCH: up to B_max with that key, FIFO order
+            const int j = bk[h++];
+            taken[j] = 1;
+            order[pos++] = static_cast<uint32_t>(j);
+            d.batch++;
+        }
+        descs[nd++] = d;
+    }
+    *n_descs = nd;
+    return SLIM_OK;
+}
+
+slim_status slim_gather(slim_ctx *ctx, const void *src, const uint32_t *idx, int n, size_t row_bytes, void *dst,
+                        void *stream) {
+    if (!ctx || n < 0 || (n > 0 && (!src || !idx || !dst)) || row_bytes % 16 || !aligned16(src) || !aligned16(dst))
+        return ctx ? fail(ctx, SLIM_EINVAL, "gather: bad arguments") : SLIM_EINVAL;
+    if (n == 0) return SLIM_OK;
+    cudaError_t e = launch_gather(src, row_bytes, idx, n, row_bytes, dst, static_cast<cudaStream_t>(stream));
+    ctx->launches++;
+    if (e != cudaSuccess) return fail(ctx, SLIM_ECUDA, "gather launch: %s", cudaGetErrorString(e));
+    return SLIM_OK;
+}
+
+slim_status slim_launch(slim_ctx *ctx, const slim_launch_desc *d, const uint32_t *slots, const void *pool,
+                        size_t pool_row_bytes, void *slab, void *out, void *ws, size_t ws_bytes, void *stream) {
+    if (!ctx || !d) return SLIM_EINVAL;
+    int ri_prev, ri;
+    slim_status s = validate_fwd(ctx, d->seg, d->r_prev, d->r, d->batch, pool, out, &ri_prev, &ri);
+    if (s) return s;
+    const slim_config &c = ctx->cfg;
+    const int Hin = d->seg == 0 ? c.image_hw : seg_hw(c, d->seg - 1);
+    const int Cin = d->seg == 0 ? c.in_channels : slim_channels(d->r_prev, c.base_channels[d->seg - 1]);
+    const size_t row = static_cast<size_t>(Hin) * Hin * Cin * elem_bytes(c);
+    const void *in = pool;
+    if (slots) {
+        if (!slab || !aligned16(slab) || pool_row_bytes < row || pool_row_bytes % 16 || row % 16)
+            return fail(ctx, SLIM_EINVAL, "launch: slab/pool rows invalid");
+        cudaError_t e = launch_gather(pool, pool_row_bytes, slots, d->batch, row, slab, static_cast<cudaStream_t>(stream));
+        ctx->launches++;
+        if (e != cudaSuccess) return fail(ctx, SLIM_ECUDA, "gather launch: %s", cudaGetErrorString(e));
+        in = slab;
+    }
+    return slim_forward_ws(ctx, d->seg, d->r_prev, d->r, d->batch, in, out, ws, ws_bytes, stream);
+}
+
+slim_status slim_last_error(slim_ctx *ctx) {
+    if (!ctx) return SLIM_EINVAL;
+    return check_sticky(ctx);
+}
+const char *slim_last_error_msg(const slim_ctx *ctx) { return ctx ? ctx->msg.c_str() : "no context"; }
+uint64_t slim_launch_count(const slim_ctx *ctx) { return ctx ? ctx->launches.load() : 0; }
+int slim_num_sms(const slim_ctx *ctx) { return ctx ? ctx->num_sms : 0; }
+
+}  // extern "C"

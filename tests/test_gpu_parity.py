@@ -1,0 +1,238 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the fp64 CPU oracle.
+
+Tolerance (north_star; reading D4): per image, max|GPU - oracle| <= tau * max|oracle|
+over that image's output elements, tau = 2e-2 in bf16 mode, 1e-4 in FP32 mode.
+Bit-exact checks where the arithmetic is exact (closed form, prefix isolation,
+batch independence, chain = composition of segments).
+Inputs: seeded synthetic (synth/), shapes of the paper's workload (CIFAR-100-shaped
+32x32x3 images); batch sizes span several M-tiles with a ragged tail.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+import paper_2510_09018_b200 as slim
+
+pytestmark = pytest.mark.gpu
+
+TAU_BF16 = 2e-2
+TAU_FP32 = 1e-4
+W4 = synth.WIDTHS
+
+
+def _dev(a, dtype=torch.bfloat16):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).to(dtype).cuda()
+
+
+@pytest.fixture(scope="module")
+def params():
+    return synth.make_weights(), synth.make_bn()
+
+
+@pytest.fixture(scope="module")
+def net(params):
+    w, bn = params
+    n = slim.SlimNet(w, bn, max_batch=512)
+    yield n
+    n.close()
+
+
+@pytest.fixture(scope="module")
+def ref(params):
+    return oracle.Model(*params)
+
+
+def _seg_input(seg, r_prev, B, seed):
+    """bf16-representable input of segment `seg`: images for seg 0, else a non-negative
+    post-ReLU-like activation [B, H_{s-1}, H_{s-1}, c_{s-1}(r_prev)]."""
+    if seg == 0:
+        return synth.make_images(B, offset=seed)
+    H = 32 >> (seg - 1)
+    C = synth.active_channels(r_prev, synth.BASE_CHANNELS[seg - 1])
+    g = np.random.default_rng(1000 + seed)
+    return synth.round_bf16(np.abs(g.standard_normal((B, H, H, C), dtype=np.float32)))
+
+
+def _check(got, exp, tau, what):
+    err = oracle.per_image_rel_err(got, exp)
+    assert np.isfinite(got).all(), f"{what}: non-finite output"
+    assert err.max() <= tau, f"{what}: worst per-image rel err {err.max():.3e} > {tau} (median {np.median(err):.2e})"
+    return err
+
+
+# ------------------------------------------------------------------ per segment, every (r_prev, r)
+@pytest.mark.parametrize("r", W4)
+def test_segment0_parity(net, ref, r):
+    x = _seg_input(0, None, 9, 0)
+    got = net.forward(0, _dev(x), r, r).float().cpu().numpy()
+    _check(got, ref.segment(0, x, None, r), TAU_BF16, f"seg0 r={r}")
+
+
+@pytest.mark.parametrize("seg", [1, 2, 3])
+@pytest.mark.parametrize("r_prev", W4)
+@pytest.mark.parametrize("r", W4)
+def test_segment_parity_all_width_pairs(net, ref, seg, r_prev, r):
+    B = 9   # seg2: 2 images per M-tile, seg3: 8 -> ragged last tile
+    x = _seg_input(seg, r_prev, B, seg)
+    got = net.forward(seg, _dev(x), r_prev, r).float().cpu().numpy()
+    _check(got, ref.segment(seg, x, r_prev, r), TAU_BF16, f"seg{seg} ({r_prev}->{r})")
+
+
+# ------------------------------------------------------------------ whole chain
+@pytest.mark.parametrize("tup", synth.TABLE_TUPLES)
+def test_chain_parity_table_tuples(net, ref, tup):
+    """The 8 width tuples of PAPER.md Tables I-II, full chain + head, logits per image."""
+    x = synth.make_images(12, offset=7)
+    got = net.forward_chain(_dev(x), tup).cpu().numpy()
+    _check(got, ref.chain(x, tup), TAU_BF16, f"chain {tup}")
+
+
+def test_chain_equals_composition_bitwise(net):
+    x = _dev(synth.make_images(10, offset=8))
+    tup = (1.0, 0.5, 0.25, 0.75)
+    a = net.forward_chain(x, tup)
+    h = net.forward(0, x, tup[0], tup[0])
+    for s in range(1, 4):
+        h = net.forward(s, h, tup[s - 1], tup[s])
+    torch.cuda.synchronize()
+    assert torch.equal(a, h)
+
+
+def test_batch_independence_bitwise(net):
+    x = synth.make_images(130, offset=9)
+    tup = (0.5, 0.75, 1.0, 0.25)
+    full = net.forward_chain(_dev(x), tup).cpu()
+    for idx in ([0], [129], list(range(37, 44))):
+        part = net.forward_chain(_dev(x[idx]), tup).cpu()
+        assert torch.equal(part, full[idx]), idx
+
+
+def test_sampled_parity_at_bench_size(net, ref):
+    """B=128 (CFG2, the bench config) at every width; 6 sampled images through the oracle
+    (batch independence makes a sample exact)."""
+    x = synth.make_images(128, offset=10)
+    pick = [0, 1, 63, 64, 126, 127]
+    for r in W4:
+        got = net.forward_chain(_dev(x), (r,) * 4).cpu().numpy()[pick]
+        _check(got, ref.chain(x[pick], (r,) * 4), TAU_BF16, f"B=128 r={r}")
+
+
+# ------------------------------------------------------------------ invariants
+def test_nan_prefix_isolation_bitwise(params):
+    """Weights outside the active prefix are NaN: output finite and bitwise unchanged
+    (the prefix is selected by TMA bounds, not read-and-masked)."""
+    w, bn = params
+    r_prev, r = 0.5, 0.25
+    clean = slim.SlimNet(w, bn, max_batch=16, segments=(1,))
+    dirty = slim.SlimNet(synth.nan_poison_weights(w, r_prev, r), bn, max_batch=16, segments=(1,))
+    x = _dev(_seg_input(1, r_prev, 5, 11))
+    a = clean.forward(1, x, r_prev, r)
+    b = dirty.forward(1, x, r_prev, r)
+    torch.cuda.synchronize()
+    assert torch.isfinite(b.float()).all()
+    assert torch.equal(a, b)
+    clean.close()
+    dirty.close()
+
+
+def test_bn_width_selection_negative_control(net, ref):
+    x = synth.make_images(4, offset=12)
+    got = net.forward(0, _dev(x), 0.25, 0.25).float().cpu().numpy()
+    _check(got, ref.segment(0, x, None, 0.25), TAU_BF16, "bn select")
+    wrong = ref.segment(0, x, None, 0.25, bn_width=0.5)
+    assert oracle.per_image_rel_err(got, wrong).min() > 5 * TAU_BF16
+
+
+def _delta_params():
+    weights, bn = {}, {}
+    for sp in synth.layer_specs():
+        wt = np.zeros((sp["cout"], sp["k"], sp["k"], sp["cin"]), np.float32)
+        c = sp["k"] // 2
+        for i in range(min(sp["cout"], sp["cin"])):
+            wt[i, c, c, i] = 1.0
+        weights[sp["name"]] = wt
+        bn[sp["name"]] = [dict(gamma=np.full(n, 0.5, np.float32), beta=np.zeros(n, np.float32),
+                               mean=np.zeros(n, np.float32), var=np.full(n, np.float32(0.25 - 1e-5), np.float32))
+                          for n in (synth.active_channels(r, sp["cout"]) for r in W4)]
+    weights["fc_w"] = synth.make_weights()["fc_w"]
+    weights["fc_b"] = np.zeros(100, np.float32)
+    return weights, bn
+
+
+def test_closed_form_delta_network_bitwise():
+    """Centre-tap delta kernels, BN folding to exactly s=1, t=0: seg0 = 4*relu(x) on channels<3,
+    each later segment = 4*h[::2, ::2] -- powers of two, exact in bf16, so bitwise."""
+    net = slim.SlimNet(*_delta_params(), max_batch=16)
+    x = synth.make_images(3, offset=13)
+    rx = np.maximum(x, 0)
+    tup = (0.75, 0.25, 1.0, 0.5)
+    h = net.forward(0, _dev(x), tup[0], tup[0])
+    exp = np.zeros(tuple(h.shape), np.float32)
+    exp[..., :3] = 4 * rx
+    assert np.array_equal(h.float().cpu().numpy(), exp)
+    for s in (1, 2):
+        h = net.forward(s, h, tup[s - 1], tup[s])
+        exp = np.zeros(tuple(h.shape), np.float32)
+        exp[..., :3] = 4 ** (s + 1) * rx[:, ::2 ** s, ::2 ** s, :]
+        assert np.array_equal(h.float().cpu().numpy(), exp), s
+    net.close()
+
+
+# ------------------------------------------------------------------ error paths
+def test_error_paths(net):
+    x = _dev(synth.make_images(2, offset=14))
+    with pytest.raises(slim.SlimError, match="EINVAL"):
+        net.forward(0, x, 0.3, 0.3)                    # width not in the set
+    with pytest.raises(slim.SlimError, match="EINVAL"):
+        slim.slim_forward(net.ctx, 0, 0.25, 0.25, 10_000, x, x)   # B > B_max
+    with pytest.raises(slim.SlimError, match="EINVAL"):
+        slim.slim_forward(net.ctx, 4, 0.25, 0.25, 2, x, x)        # seg out of range
+    assert slim.slim_last_error(net.ctx) == 0
+
+
+def test_not_loaded(params):
+    w, bn = params
+    n = slim.SlimNet(w, bn, max_batch=4, segments=(0,))
+    x = _dev(_seg_input(1, 0.25, 2, 15))
+    with pytest.raises(slim.SlimError, match="ENOTLOADED"):
+        n.forward(1, x, 0.25, 0.25)
+    slim.slim_unload_segment(n.ctx, 0)
+    with pytest.raises(slim.SlimError, match="ENOTLOADED"):
+        n.forward(0, _dev(synth.make_images(2)), 0.25, 0.25)
+    n.close()
+
+
+# ------------------------------------------------------------------ packer + gather launch
+def test_pack_gather_launch_matches_direct(net, ref):
+    """Requests scattered in a pool, grouped by key (s, w_req, w_prev), gathered by the K8
+    kernel and run; each output equals the direct forward of the same images."""
+    rng = np.random.default_rng(16)
+    n = 23
+    seg = 1
+    keys = [(0.5, 0.25), (1.0, 0.25), (0.5, 0.75)]
+    pool_np = _seg_input(1, 1.0, n, 16)                       # pool rows sized for the widest r_prev
+    reqs = []
+    for i in range(n):
+        wr, wp = keys[rng.integers(0, 3)]
+        reqs.append((i, seg, wr, wp, i))
+    descs, order = slim.slim_pack(net.cfg, reqs, 8)
+    C_full = synth.BASE_CHANNELS[0]
+    row_bytes = 32 * 32 * C_full * 2
+    for d in descs:
+        idx = order[d["first"]:d["first"] + d["batch"]]
+        cin = synth.active_channels(d["r_prev"], C_full)
+        # the pool holds each request's activation at its own width r_prev (dense prefix per row)
+        pool = np.zeros((n, 32, 32, C_full), np.float32)
+        pool.reshape(n, -1)[:, :32 * 32 * cin] = pool_np[..., :cin].reshape(n, -1)
+        pool_d = _dev(pool)
+        slots = torch.from_numpy(idx.astype(np.int32)).cuda()
+        slab = torch.empty(d["batch"], 32, 32, cin, dtype=torch.bfloat16, device="cuda")
+        out = torch.empty(net.segment_out_shape(seg, d["r"], d["batch"]), dtype=torch.bfloat16, device="cuda")
+        ws_b = slim.slim_forward_workspace_bytes(net.ctx, seg, d["r_prev"], d["r"], d["batch"])
+        ws = torch.empty(ws_b, dtype=torch.uint8, device="cuda")
+        slim.slim_launch(net.ctx, d, slots, pool_d, row_bytes, slab, out, ws, ws_b)
+        direct = net.forward(seg, _dev(pool_np[idx][..., :cin]), d["r_prev"], d["r"])
+        torch.cuda.synchronize()
+        assert torch.equal(out, direct)
