@@ -1,0 +1,328 @@
+#!/usr/bin/env python
+"""bench.py -- images/s of the width-sliced SlimResNet forward on B200 (BASELINE.json metric).
+
+Workload (BASELINE.json configs[1], "CFG2"): the full segmented SlimResNet
+(4 segments + pool/FC, 100 classes) at each width ratio r in {0.25, 0.5, 0.75, 1.0},
+batch 128, synthetic CIFAR-100-shaped 32x32x3 inputs, random-init weights
+(synth/, seeded).  One STEP = one full-chain forward of a 128-image batch at
+every width (512 images), through the C-ABI (slim_forward_chain, CUDA-graph
+replay).  Multi-GPU (torchrun, one rank per GPU): every rank runs its own
+batches (weak scaling, no data-path collective) and all-gathers a float32[8]
+telemetry record per step over NCCL on a side stream (north_star).
+
+Timing: W warm-up steps, then K steps, each bracketed by CUDA events on the
+launching stream; L2 is flushed (256 MiB write) before every timed step, outside
+the events; barrier + synchronize around the region; max over ranks.
+
+`--impl reference` times the fp64 CPU oracle (oracle/) on a bounded sample of the
+same workload (one image per width per step) -- the base contract's reference arm
+for a tier with no reference implementation.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "SlimResNet images/s per width at 1/2/4/8 B200; tensor-pipe % of peak"
+WIDTHS = (0.25, 0.5, 0.75, 1.0)
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return dict(hbm=d["hbm_gbs"], bf16=d["bf16_tflops"], bf16_sus=d.get("bf16_tflops_sustained"),
+                    src="measured (MEASURED_PEAKS.json)")
+    return dict(hbm=6650.0, bf16=1590.0, bf16_sus=1400.0, src="fallback (B200_PROFILING.md)")
+
+
+def _dist():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def _cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count()
+
+
+# ------------------------------------------------------------------ CPU oracle legs
+def oracle_throughput(target_s: float = 15.0, batch_per_width: int | None = None):
+    """The fp64 oracle as it stands on this host's cores: images/s on a bounded sample of CFG2
+    (equal images per width, like the GPU step)."""
+    import oracle
+    import synth
+    m = oracle.Model(synth.make_weights(), synth.make_bn())
+    x = synth.make_images(128, offset=1)
+    if batch_per_width is None:   # size the sample to ~target_s of CPU work
+        t0 = time.perf_counter()
+        for r in WIDTHS:
+            m.chain(x[:1], (r,) * 4)
+        t1 = time.perf_counter() - t0
+        batch_per_width = max(1, min(128, int(target_s / max(t1, 1e-3))))
+    t0 = time.perf_counter()
+    for r in WIDTHS:
+        m.chain(x[:batch_per_width], (r,) * 4)
+    dt = time.perf_counter() - t0
+    n = batch_per_width * len(WIDTHS)
+    return dict(value=n / dt, unit="images/s", cores=_cores(), kind="oracle",
+                sample=f"{batch_per_width} images x {len(WIDTHS)} widths of the CFG2 chain (fp64 C oracle, "
+                       f"OpenMP over rows), {dt:.1f} s")
+
+
+def run_reference(args):
+    world, rank, _ = _dist()
+    if rank != 0:
+        return 0
+    import oracle
+    import synth
+    m = oracle.Model(synth.make_weights(), synth.make_bn())
+    x = synth.make_images(128, offset=1)
+    step = lambda k: [m.chain(x[k % 128:k % 128 + 1], (r,) * 4) for r in WIDTHS]
+    for k in range(args.warmup):
+        step(k)
+    t0 = time.perf_counter()
+    for k in range(args.steps):
+        step(k)
+    dt = time.perf_counter() - t0
+    imgs = len(WIDTHS) * args.steps
+    value = imgs / dt
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": 0,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "CFG2: full SlimResNet chain (4 segments + pool/FC, 100 classes) at each width "
+                               "r in {0.25,0.5,0.75,1.0}; reference step = 1 image per width", "batch": 1,
+                   "image": [32, 32, 3], "widths": list(WIDTHS)},
+        "cpu_baseline": {"value": value, "unit": "images/s", "cores": _cores(), "kind": "oracle",
+                         "sample": f"{args.steps} steps x 1 image per width of the CFG2 chain"},
+        "e2e": {"value": value, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+# ------------------------------------------------------------------ GPU arm
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import synth
+    import paper_2510_09018_b200 as slim
+    from paper_2510_09018_b200 import build as slim_build
+    from paper_2510_09018_b200.telemetry import NvmlSampler, TelemetryExchange, pack_record
+
+    world, rank, local = _dist()
+    assert torch.cuda.is_available(), "bench.py (ours) needs a GPU; the oracle arm is --impl reference"
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    slim_build.build()
+
+    B = args.batch
+    weights, bn = synth.make_weights(), synth.make_bn()
+    net = slim.SlimNet(weights, bn, device=local, max_batch=max(B, 16))
+    if not args.no_graph:
+        slim.slim_set_graph_mode(net.ctx, True)
+    stream = torch.cuda.current_stream(dev)
+    xs = {r: torch.from_numpy(synth.make_images(B, offset=100 + rank * 8 + i)).to(torch.bfloat16).to(dev)
+          for i, r in enumerate(WIDTHS)}
+    logits = {r: torch.empty(B, 100, dtype=torch.float32, device=dev) for r in WIDTHS}
+    wsb = max(slim.slim_chain_workspace_bytes(net.ctx, (r,) * 4, B) for r in WIDTHS)
+    ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
+    telem = TelemetryExchange(device=dev) if world > 1 else None
+
+    def chain(r):
+        slim.slim_forward_chain(net.ctx, (r,) * 4, B, xs[r], logits[r], ws, wsb, stream)
+
+    def step():
+        for r in WIDTHS:
+            chain(r)
+
+    for _ in range(args.warmup):
+        flush.zero_()
+        step()
+        if telem:
+            telem.tick(pack_record(rank=rank))
+    torch.cuda.synchronize()
+
+    # ---------------- timed region
+    K = args.steps
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    evw = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in WIDTHS]
+           for _ in range(K)]
+    sampler = NvmlSampler(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = slim.slim_launch_count(net.ctx)
+    e0 = sampler.energy_mj()
+    sampler.start()
+    for k in range(K):
+        flush.zero_()
+        ev[k][0].record(stream)
+        for i, r in enumerate(WIDTHS):
+            evw[k][i][0].record(stream)
+            chain(r)
+            evw[k][i][1].record(stream)
+        ev[k][1].record(stream)
+        if telem:
+            telem.tick(pack_record(rank=rank, completed=(k + 1) * B * len(WIDTHS)))
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    sampler.stop()
+    e1 = sampler.energy_mj()
+    launches = slim.slim_launch_count(net.ctx) - launches0
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    total_ms = sum(step_ms)
+    width_ms = [sum(evw[k][i][0].elapsed_time(evw[k][i][1]) for k in range(K)) for i in range(len(WIDTHS))]
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_max_ms = float(t.item())
+    imgs_per_step = B * len(WIDTHS)
+    value = world * imgs_per_step * K / (total_max_ms / 1e3)
+    per_width = {str(r): B * K / (width_ms[i] / 1e3) for i, r in enumerate(WIDTHS)}
+    clocks = sampler.summary()
+    energy = ((e1 - e0) / 1e3 / (imgs_per_step * K)) if (e0 is not None and e1 is not None) else None
+
+    # ---------------- profiled replay (per-launch CUDA events, no graph) for the roofline object
+    KP = min(K, args.profile_steps)
+    slim.slim_profile_begin(net.ctx, KP * 80 + 16)
+    for _ in range(KP):
+        flush.zero_()
+        step()
+    recs = slim.slim_profile_end(net.ctx)
+    peaks = _peaks()
+    by_kind = {}
+    for rc in recs:
+        d = by_kind.setdefault(rc["kind"], dict(ms=0.0, flops=0.0, bytes=0.0, n=0, roof_ms=0.0))
+        d["ms"] += rc["ms"]
+        d["flops"] += rc["flops"]
+        d["bytes"] += rc["bytes"]
+        d["n"] += 1
+        d["roof_ms"] += max(rc["flops"] / (peaks["bf16"] * 1e12), rc["bytes"] / (peaks["hbm"] * 1e9)) * 1e3
+    kern_ms = sum(d["ms"] for d in by_kind.values())
+    dom = max(by_kind, key=lambda k: by_kind[k]["ms"])
+    D = by_kind[dom]
+    tensor_time = D["flops"] / (peaks["bf16"] * 1e12)
+    hbm_time = D["bytes"] / (peaks["hbm"] * 1e9)
+    if tensor_time >= hbm_time:
+        achieved = D["flops"] / (D["ms"] / 1e3) / 1e12
+        roof = {"bound": "tensor", "achieved": achieved, "peak": peaks["bf16"], "unit": "TFLOP/s",
+                "frac": achieved / peaks["bf16"]}
+    else:
+        achieved = D["bytes"] / (D["ms"] / 1e3) / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm"], "unit": "GB/s",
+                "frac": achieved / peaks["hbm"]}
+    roof.update({
+        "kernel": dom, "launches_profiled": D["n"], "share_of_kernel_time": D["ms"] / kern_ms,
+        "peak_source": peaks["src"] + ", bf16 burst",
+        "per_layer_roofline_frac": D["roof_ms"] / D["ms"],
+        "algorithmic_flops_per_launch": D["flops"] / D["n"], "algorithmic_bytes_per_launch": D["bytes"] / D["n"],
+        "traffic": _ncu_traffic(),
+    })
+
+    # ---------------- e2e through the public API with host buffers
+    xh = {r: xs[r].cpu().pin_memory() for r in WIDTHS}
+    lh = {r: torch.empty(B, 100, dtype=torch.float32).pin_memory() for r in WIDTHS}
+    KE = max(1, min(K, args.e2e_steps))
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(KE):
+        for r in WIDTHS:
+            xs[r].copy_(xh[r], non_blocking=True)
+            chain(r)
+            lh[r].copy_(logits[r], non_blocking=True)
+        stream.synchronize()
+    e2e_s = time.perf_counter() - t0
+    te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_val = world * imgs_per_step * KE / float(te.item())
+
+    if rank == 0:
+        cpu = oracle_throughput(args.cpu_seconds) if (world == 1 and not args.no_cpu) else None
+        line = {
+            "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world, "steps": K,
+            "warmup": args.warmup, "ms_per_step": total_max_ms / K, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded N(0,1) images, random-init weights)",
+            "config": {"workload": "CFG2: full SlimResNet chain (4 segments + pool/FC, 100 classes) at each width "
+                                   "r in {0.25,0.5,0.75,1.0}, batch 128 per width, 1 step = 4 x 128 images",
+                       "batch": B, "image": [32, 32, 3], "widths": list(WIDTHS),
+                       "parallelism": f"dp{world} (independent per-GPU batches)",
+                       "l2": "flushed (256 MiB write) before every timed step", "graphs": not args.no_graph},
+            "per_width_images_per_s": per_width,
+            "per_width_ms_per_batch": {str(r): width_ms[i] / K for i, r in enumerate(WIDTHS)},
+            "roofline": roof,
+            "kernel_time_by_kind_ms_per_step": {k: v["ms"] / KP for k, v in by_kind.items()},
+            "gpu_launches": launches,
+            "energy_j_per_image": energy,
+            "clocks": clocks,
+            "e2e": {"value": e2e_val, "unit": "images/s", "h2d_bytes_per_step": sum(x.numel() * 2 for x in xh.values()),
+                    "d2h_bytes_per_step": sum(l.numel() * 4 for l in lh.values()),
+                    "api": "SlimNet / slim_forward_chain with pinned-host input copy + logits read-back per step"},
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line))
+        if args.json_out:
+            with open(args.json_out, "w") as f:
+                json.dump(dict(line, profile=recs[:200]), f, indent=1)
+    net.close()
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def _ncu_traffic():
+    """dram bytes per conv launch from the committed ncu --set full summary, if present."""
+    p = os.path.join(ROOT, "profiles", "ncu_conv_summary.json")
+    if not os.path.exists(p):
+        return None
+    try:
+        return json.load(open(p)).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=1000)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--batch", type=int, default=128)
+    ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--profile-steps", type=int, default=50)
+    ap.add_argument("--e2e-steps", type=int, default=200)
+    ap.add_argument("--json-out", default=None)
+    args = ap.parse_args(argv)
+    assert args.warmup >= 0 and args.steps >= 1
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

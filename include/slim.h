@@ -194,6 +194,33 @@ SLIM_API slim_status slim_launch(slim_ctx *ctx, const slim_launch_desc *desc, co
 SLIM_API slim_status slim_gather(slim_ctx *ctx, const void *src, const uint32_t *idx, int n, size_t row_bytes,
                         void *dst, void *stream);
 
+/* ---- execution modes and profiling ------------------------------------- */
+
+/* Graph mode (default off): slim_forward_ws / slim_forward_chain capture their
+ * launch sequence into a CUDA graph the first time a given argument list
+ * (key, batch, buffer pointers) is seen and replay it afterwards -- one
+ * cudaGraphLaunch per call instead of ~18 kernel launches.  Captured graphs
+ * bake in the buffer addresses; loading/unloading a segment drops them. */
+SLIM_API slim_status slim_set_graph_mode(slim_ctx *ctx, int enable);
+
+/* Per-launch profiling: while on, every kernel launch is bracketed by CUDA
+ * events on its stream and described by its algorithmic work (SURVEY §8(d):
+ * sliced FLOPs = 2*MACs; bytes = layer-materialised traffic: input, weights,
+ * residual / projection input read once, output written once).  Graph replay
+ * is bypassed while profiling.  begin() allocates the events (at most
+ * max_launches records); end() synchronises and returns the records. */
+typedef enum { SLIM_K_STEM = 0, SLIM_K_CONV_UMMA = 1, SLIM_K_HEAD = 2, SLIM_K_GATHER = 3, SLIM_K_CONV_F32 = 4 } slim_kernel_kind;
+typedef struct {
+    int kind;                  /* slim_kernel_kind */
+    int seg, layer;            /* segment, manifest index of the conv (stem = 0 in seg 0; head/gather: -1) */
+    int batch;
+    float r_prev, r;
+    double flops, bytes;       /* algorithmic work of this launch */
+    float ms;                  /* event-measured duration */
+} slim_profile_record;
+SLIM_API slim_status slim_profile_begin(slim_ctx *ctx, int max_launches);
+SLIM_API slim_status slim_profile_end(slim_ctx *ctx, slim_profile_record *out, int max_out, int *n_out);
+
 /* ---- errors, introspection ------------------------------------------------ */
 SLIM_API slim_status slim_last_error(slim_ctx *ctx);        /* sticky async error (SLIM_OK if none) */
 SLIM_API const char *slim_last_error_msg(const slim_ctx *ctx);

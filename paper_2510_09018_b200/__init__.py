@@ -66,6 +66,15 @@ class slim_request(ctypes.Structure):
                 ("w_prev", ctypes.c_float), ("slot", ctypes.c_uint32)]
 
 
+class slim_profile_record(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int), ("seg", ctypes.c_int), ("layer", ctypes.c_int), ("batch", ctypes.c_int),
+                ("r_prev", ctypes.c_float), ("r", ctypes.c_float), ("flops", ctypes.c_double),
+                ("bytes", ctypes.c_double), ("ms", ctypes.c_float)]
+
+
+KERNEL_KINDS = {0: "stem", 1: "conv_umma", 2: "head", 3: "gather", 4: "conv_f32"}
+
+
 class slim_launch_desc(ctypes.Structure):
     _fields_ = [("seg", ctypes.c_int), ("r_prev", ctypes.c_float), ("r", ctypes.c_float), ("batch", ctypes.c_int),
                 ("first", ctypes.c_int)]
@@ -109,6 +118,9 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "slim_launch_count": (ctypes.c_uint64, [_VP]),
         "slim_num_sms": (_I, [_VP]),
         "slim_channels": (_I, [_F, _I]),
+        "slim_set_graph_mode": (_I, [_VP, _I]),
+        "slim_profile_begin": (_I, [_VP, _I]),
+        "slim_profile_end": (_I, [_VP, ctypes.POINTER(slim_profile_record), _I, ctypes.POINTER(_I)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -122,7 +134,8 @@ EXPORTED = ("slim_create", "slim_destroy", "slim_default_config", "slim_load_seg
             "slim_segment_loaded", "slim_segment_bytes", "slim_forward", "slim_forward_workspace_bytes",
             "slim_forward_ws", "slim_chain_workspace_bytes", "slim_forward_chain", "slim_pack", "slim_launch",
             "slim_gather", "slim_last_error", "slim_last_error_msg", "slim_status_str", "slim_version",
-            "slim_launch_count", "slim_num_sms", "slim_channels")
+            "slim_launch_count", "slim_num_sms", "slim_channels", "slim_set_graph_mode", "slim_profile_begin",
+            "slim_profile_end")
 
 
 # ------------------------------------------------------------------ marshalling helpers
@@ -289,6 +302,25 @@ def slim_launch_count(ctx) -> int:
 
 def slim_channels(r: float, C: int) -> int:
     return load_library().slim_channels(r, C)
+
+
+def slim_set_graph_mode(ctx, enable: bool):
+    _check(ctx, load_library().slim_set_graph_mode(ctx, int(bool(enable))))
+
+
+def slim_profile_begin(ctx, max_launches: int):
+    _check(ctx, load_library().slim_profile_begin(ctx, max_launches))
+
+
+def slim_profile_end(ctx, max_out: int = 1 << 20):
+    """Synchronises; returns a list of dicts (kind, seg, layer, batch, r_prev, r, flops, bytes, ms)."""
+    lib = load_library()
+    n = ctypes.c_int()
+    _check(ctx, lib.slim_profile_end(ctx, None, 0, ctypes.byref(n)))
+    recs = (slim_profile_record * max(n.value, 1))()
+    _check(ctx, lib.slim_profile_end(ctx, recs, n.value, ctypes.byref(n)))
+    return [dict(kind=KERNEL_KINDS.get(r.kind, r.kind), seg=r.seg, layer=r.layer, batch=r.batch, r_prev=r.r_prev,
+                 r=r.r, flops=r.flops, bytes=r.bytes, ms=r.ms) for r in recs[:n.value]]
 
 
 # ------------------------------------------------------------------ convenience

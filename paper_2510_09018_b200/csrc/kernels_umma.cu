@@ -28,6 +28,9 @@
 
 #include <cuda_bf16.h>
 
+#include <map>
+#include <mutex>
+
 namespace slim {
 namespace {
 
@@ -396,11 +399,21 @@ size_t conv_umma_smem_bytes(const ConvArgs &a) {
 }
 
 int conv_umma_max_ctas_per_sm(size_t smem_bytes) {
+    // cached per shared-memory size: the occupancy query costs microseconds of host time
+    static std::mutex mu;
+    static std::map<size_t, int> cache;
+    std::lock_guard<std::mutex> g(mu);
+    auto it = cache.find(smem_bytes);
+    if (it != cache.end()) return it->second;
     int n = 0;
     cudaFuncSetAttribute(conv_umma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, conv_umma_kernel, kConvThreads, smem_bytes) != cudaSuccess)
-        return 1;
-    return n < 1 ? 1 : n;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, conv_umma_kernel, kConvThreads, smem_bytes) != cudaSuccess) {
+        cudaGetLastError();
+        n = 1;
+    }
+    n = n < 1 ? 1 : n;
+    cache[smem_bytes] = n;
+    return n;
 }
 
 cudaError_t launch_conv_umma(const ConvArgs &a, const CUtensorMap &tmA0, const CUtensorMap &tmB0,

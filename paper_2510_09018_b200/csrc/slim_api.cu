@@ -63,6 +63,19 @@ struct slim_ctx {
     std::string msg;
     PFN_encodeTiled encode = nullptr;
     std::mutex mu;   // guards the lazily filled tensor-map cache
+    // profiling: an event pair around every launch while prof_on
+    bool prof_on = false;
+    std::vector<cudaEvent_t> prof_ev;
+    std::vector<slim_profile_record> prof_rec;
+    // graph mode: captured launch sequences keyed by the full argument list
+    struct GraphEntry {
+        cudaGraphExec_t exec;
+        uint64_t n_kernels;
+    };
+    bool graph_mode = false;
+    cudaStream_t cap_stream = nullptr;
+    std::mutex graph_mu;
+    std::unordered_map<std::string, GraphEntry> graphs;
 };
 
 extern "C" int slim_channels(float r, int C) {
@@ -151,6 +164,34 @@ float bf_round(float f) {
         if (e__ != cudaSuccess) return fail((ctx), SLIM_ECUDA, "%s: %s", #expr, cudaGetErrorString(e__)); \
     } while (0)
 
+// Brackets one kernel launch: counts it and, while profiling, records an event pair
+// and the launch's algorithmic work.
+struct LaunchProf {
+    slim_ctx *ctx;
+    cudaStream_t st;
+    int idx = -1;
+    LaunchProf(slim_ctx *c, cudaStream_t s) : ctx(c), st(s) {
+        if (ctx->prof_on && 2 * (ctx->prof_rec.size() + 1) <= ctx->prof_ev.size()) {
+            idx = static_cast<int>(ctx->prof_rec.size());
+            cudaEventRecord(ctx->prof_ev[2 * idx], st);
+        }
+    }
+    void done(int kind, int seg, int layer, float r_prev, float r, int B, double flops, double bytes) {
+        ctx->launches++;
+        if (idx >= 0) {
+            cudaEventRecord(ctx->prof_ev[2 * idx + 1], st);
+            slim_profile_record rec{kind, seg, layer, B, r_prev, r, flops, bytes, 0.f};
+            ctx->prof_rec.push_back(rec);
+        }
+    }
+};
+
+void clear_graphs(slim_ctx *ctx) {
+    std::lock_guard<std::mutex> g(ctx->graph_mu);
+    for (auto &kv : ctx->graphs) cudaGraphExecDestroy(kv.second.exec);
+    ctx->graphs.clear();
+}
+
 bool encode_map(slim_ctx *ctx, CUtensorMap *tm, const void *ptr, int rank, const cuuint64_t *dims,
                 const cuuint64_t *strides, const cuuint32_t *box, const cuuint32_t *es) {
     CUresult r = ctx->encode(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void *>(ptr), dims, strides, box,
@@ -195,13 +236,47 @@ const CUtensorMap *weight_map(slim_ctx *ctx, DevLayer &L, int ri_in, int ri, int
     return &L.tm[ri_in][ri];
 }
 
-// One tcgen05 conv launch: out = epi(conv(x; L) [, proj(xp; Lp)] [, res]).
-slim_status conv_bf16(slim_ctx *ctx, cudaStream_t st, DevLayer &L, int ri_in, int ri, const void *x, int B, int H,
-                      int W, int c_in, DevLayer *Lp, int ri_in_p, const void *xp, int Hp, int Wp, int c_in_p,
-                      const void *res, void *out, int epi) {
+// One conv launch of a BasicBlock: out = epi(conv(x; L) [+ proj(xp; Lp)] [+ res]).
+struct ConvCall {
+    int seg = 0, layer = 0;                  // for profiling records
+    DevLayer *L = nullptr;
+    int ri_in = 0;                           // width index that sets c_in (r_prev for block-0 c1 of seg>0)
+    const void *x = nullptr;
+    int H = 0, W = 0, c_in = 0;
+    DevLayer *Lp = nullptr;                  // 1x1 stride-2 projection (EPI_BN_PROJ_RELU)
+    int ri_in_p = 0, layer_p = 0;
+    const void *xp = nullptr;
+    int Hp = 0, Wp = 0, c_in_p = 0;
+    const void *res = nullptr;               // identity residual (EPI_BN_ADD_RELU)
+    void *out = nullptr;
+    int epi = EPI_BN_RELU;
+};
+
+// Algorithmic work: 2*MACs of the sliced conv(s); bytes = input(s),
+// sliced weights, residual read once, output written once, folded BN vectors.
+void conv_work(const slim_config &c, const ConvCall &cc, int ri, int B, int Ho, int Wo, double *flops,
+               double *bytes) {
+    const double eb = static_cast<double>(elem_bytes(c));
+    const int k = cc.L->sh.k;
+    const double c_out = slim_channels(c.widths[ri], cc.L->sh.cout);
+    const double pix = static_cast<double>(B) * Ho * Wo;
+    double f = 2.0 * pix * c_out * k * k * cc.c_in;
+    double b = eb * (static_cast<double>(B) * cc.H * cc.W * cc.c_in + c_out * k * k * cc.c_in + pix * c_out) +
+               8.0 * c_out;
+    if (cc.epi == EPI_BN_ADD_RELU) b += eb * pix * c_out;
+    if (cc.epi == EPI_BN_PROJ_RELU) {
+        f += 2.0 * pix * c_out * cc.c_in_p;
+        b += eb * (static_cast<double>(B) * cc.Hp * cc.Wp * cc.c_in_p + c_out * cc.c_in_p) + 8.0 * c_out;
+    }
+    *flops = f;
+    *bytes = b;
+}
+
+slim_status conv_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, int ri, int B) {
     const slim_config &c = ctx->cfg;
+    DevLayer &L = *cc.L;
     const int k = L.sh.k, s = L.sh.stride, pad = k / 2;
-    const int Ho = (H + 2 * pad - k) / s + 1, Wo = (W + 2 * pad - k) / s + 1;
+    const int Ho = (cc.H + 2 * pad - k) / s + 1, Wo = (cc.W + 2 * pad - k) / s + 1;
     const int c_out = slim_channels(c.widths[ri], L.sh.cout);
     ConvArgs a{};
     a.B = B;
@@ -224,19 +299,19 @@ slim_status conv_bf16(slim_ctx *ctx, cudaStream_t st, DevLayer &L, int ri_in, in
     a.n_tile = pick_n_tile(c_out);
     a.n_tiles = c_out / a.n_tile;
     a.c_out = c_out;
-    a.n_parts = (epi == EPI_BN_PROJ_RELU) ? 2 : 1;
-    a.part[0] = GemmPart{k, s, pad, c_in, (c_in + kChunk - 1) / kChunk, 0};
+    a.n_parts = (cc.epi == EPI_BN_PROJ_RELU) ? 2 : 1;
+    a.part[0] = GemmPart{k, s, pad, cc.c_in, (cc.c_in + kChunk - 1) / kChunk, 0};
     a.part[0].n_kblocks = k * k * a.part[0].n_chunks;
     if (a.n_parts == 2) {
-        a.part[1] = GemmPart{Lp->sh.k, Lp->sh.stride, 0, c_in_p, (c_in_p + kChunk - 1) / kChunk, 0};
+        a.part[1] = GemmPart{cc.Lp->sh.k, cc.Lp->sh.stride, 0, cc.c_in_p, (cc.c_in_p + kChunk - 1) / kChunk, 0};
         a.part[1].n_kblocks = a.part[1].n_chunks;
     }
-    a.epi = epi;
+    a.epi = cc.epi;
     a.scale0 = L.scale[ri];
     a.shift0 = L.shift[ri];
     if (a.n_parts == 2) {
-        a.scale1 = Lp->scale[ri];
-        a.shift1 = Lp->shift[ri];
+        a.scale1 = cc.Lp->scale[ri];
+        a.shift1 = cc.Lp->shift[ri];
     }
     a.acc_stride = (a.n_tile + 31) / 32 * 32;
     a.acc_stages = 512 / (a.n_parts * a.acc_stride) >= 2 ? 2 : 1;
@@ -254,23 +329,24 @@ slim_status conv_bf16(slim_ctx *ctx, cudaStream_t st, DevLayer &L, int ri_in, in
     a.n_stages = stages < 2 ? 2 : (stages > kMaxStages ? kMaxStages : stages);
 
     CUtensorMap tA0, tA1, tRes, tOut;
-    if (!encode_act(ctx, &tA0, x, B, H, W, c_in, s * Wo, s * a.tile_rows, a.tile_imgs, s))
+    if (!encode_act(ctx, &tA0, cc.x, B, cc.H, cc.W, cc.c_in, s * Wo, s * a.tile_rows, a.tile_imgs, s))
         return fail(ctx, SLIM_ECUDA, "cuTensorMapEncodeTiled(A) failed");
-    const CUtensorMap *tB0 = weight_map(ctx, L, ri_in, ri, c_in, c_out);
+    const CUtensorMap *tB0 = weight_map(ctx, L, cc.ri_in, ri, cc.c_in, c_out);
     const CUtensorMap *tB1 = tB0;
     if (!tB0) return fail(ctx, SLIM_ECUDA, "cuTensorMapEncodeTiled(W) failed");
     tA1 = tA0;
     if (a.n_parts == 2) {
-        const int sp = Lp->sh.stride;
-        if (!encode_act(ctx, &tA1, xp, B, Hp, Wp, c_in_p, sp * Wo, sp * a.tile_rows, a.tile_imgs, sp))
+        const int sp = cc.Lp->sh.stride;
+        if (!encode_act(ctx, &tA1, cc.xp, B, cc.Hp, cc.Wp, cc.c_in_p, sp * Wo, sp * a.tile_rows, a.tile_imgs, sp))
             return fail(ctx, SLIM_ECUDA, "cuTensorMapEncodeTiled(A1) failed");
-        tB1 = weight_map(ctx, *Lp, ri_in_p, ri, c_in_p, c_out);
+        tB1 = weight_map(ctx, *cc.Lp, cc.ri_in_p, ri, cc.c_in_p, c_out);
         if (!tB1) return fail(ctx, SLIM_ECUDA, "cuTensorMapEncodeTiled(W1) failed");
     }
-    if (!encode_act(ctx, &tOut, out, B, Ho, Wo, c_out, Wo, a.tile_rows, a.tile_imgs, 1))
+    if (!encode_act(ctx, &tOut, cc.out, B, Ho, Wo, c_out, Wo, a.tile_rows, a.tile_imgs, 1))
         return fail(ctx, SLIM_ECUDA, "cuTensorMapEncodeTiled(out) failed");
     tRes = tOut;
-    if (epi == EPI_BN_ADD_RELU && !encode_act(ctx, &tRes, res, B, Ho, Wo, c_out, Wo, a.tile_rows, a.tile_imgs, 1))
+    if (cc.epi == EPI_BN_ADD_RELU &&
+        !encode_act(ctx, &tRes, cc.res, B, Ho, Wo, c_out, Wo, a.tile_rows, a.tile_imgs, 1))
         return fail(ctx, SLIM_ECUDA, "cuTensorMapEncodeTiled(res) failed");
 
     const size_t smem = conv_umma_smem_bytes(a);
@@ -278,48 +354,54 @@ slim_status conv_bf16(slim_ctx *ctx, cudaStream_t st, DevLayer &L, int ri_in, in
     const int total = a.m_tiles * a.n_tiles;
     int grid = ctx->num_sms * per_sm;
     if (grid > total) grid = total;
+    double flops, bytes;
+    conv_work(c, cc, ri, B, Ho, Wo, &flops, &bytes);
+    LaunchProf prof(ctx, st);
     cudaError_t e = launch_conv_umma(a, tA0, *tB0, tA1, *tB1, tRes, tOut, grid, st);
-    ctx->launches++;
+    prof.done(SLIM_K_CONV_UMMA, cc.seg, cc.layer, c.widths[cc.ri_in], c.widths[ri], B, flops, bytes);
     if (e != cudaSuccess) return fail(ctx, SLIM_ECUDA, "conv_umma launch: %s", cudaGetErrorString(e));
     return SLIM_OK;
 }
 
-slim_status conv_f32(slim_ctx *ctx, cudaStream_t st, DevLayer &L, int ri, const void *x, int B, int H, int W,
-                     int c_in, DevLayer *Lp, const void *xp, int Hp, int Wp, int c_in_p, const void *res, void *out,
-                     int epi) {
+slim_status conv_f32(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, int ri, int B) {
+    const slim_config &c = ctx->cfg;
+    DevLayer &L = *cc.L;
     const int k = L.sh.k, s = L.sh.stride, pad = k / 2;
     ConvF32Args a{};
-    a.x = static_cast<const float *>(x);
+    a.x = static_cast<const float *>(cc.x);
     a.B = B;
-    a.H = H;
-    a.W = W;
-    a.c_in = c_in;
+    a.H = cc.H;
+    a.W = cc.W;
+    a.c_in = cc.c_in;
     a.w = static_cast<const float *>(L.w);
     a.cin_full = L.sh.cin;
     a.k = k;
     a.stride = s;
     a.pad = pad;
-    a.Ho = (H + 2 * pad - k) / s + 1;
-    a.Wo = (W + 2 * pad - k) / s + 1;
-    a.c_out = slim_channels(ctx->cfg.widths[ri], L.sh.cout);
+    a.Ho = (cc.H + 2 * pad - k) / s + 1;
+    a.Wo = (cc.W + 2 * pad - k) / s + 1;
+    a.c_out = slim_channels(c.widths[ri], L.sh.cout);
     a.scale0 = L.scale[ri];
     a.shift0 = L.shift[ri];
-    if (epi == EPI_BN_PROJ_RELU) {
-        a.x1 = static_cast<const float *>(xp);
-        a.H1 = Hp;
-        a.W1 = Wp;
-        a.c_in1 = c_in_p;
-        a.stride1 = Lp->sh.stride;
-        a.w1 = static_cast<const float *>(Lp->w);
-        a.cin1_full = Lp->sh.cin;
-        a.scale1 = Lp->scale[ri];
-        a.shift1 = Lp->shift[ri];
+    if (cc.epi == EPI_BN_PROJ_RELU) {
+        a.x1 = static_cast<const float *>(cc.xp);
+        a.H1 = cc.Hp;
+        a.W1 = cc.Wp;
+        a.c_in1 = cc.c_in_p;
+        a.stride1 = cc.Lp->sh.stride;
+        a.w1 = static_cast<const float *>(cc.Lp->w);
+        a.cin1_full = cc.Lp->sh.cin;
+        a.scale1 = cc.Lp->scale[ri];
+        a.shift1 = cc.Lp->shift[ri];
     }
-    a.res = static_cast<const float *>(res);
-    a.out = static_cast<float *>(out);
-    a.epi = epi;
+    a.res = static_cast<const float *>(cc.res);
+    a.out = static_cast<float *>(cc.out);
+    a.epi = cc.epi;
+    double flops, bytes;
+    conv_work(c, cc, ri, B, a.Ho, a.Wo, &flops, &bytes);
+    LaunchProf prof(ctx, st);
     cudaError_t e = launch_conv_f32(a, st);
-    ctx->launches++;
+    prof.done(SLIM_K_CONV_F32, cc.seg, cc.layer, c.widths[cc.ri_in], c.widths[ri], B, flops, bytes);
     if (e != cudaSuccess) return fail(ctx, SLIM_ECUDA, "conv_f32 launch: %s", cudaGetErrorString(e));
     return SLIM_OK;
 }
@@ -358,22 +440,28 @@ slim_status run_segment(slim_ctx *ctx, int seg, int ri_prev, int ri, int B, cons
     const slim_config &c = ctx->cfg;
     DevSegment &S = ctx->seg[seg];
     const bool bf = c.dtype == SLIM_BF16;
+    const double eb = static_cast<double>(elem_bytes(c));
     const float r = c.widths[ri];
     const int H = seg_hw(c, seg);
     const int C = slim_channels(r, c.base_channels[seg]);
     const size_t buf = round256(act_bytes(c, seg, r, B));
     char *bufs[3] = {static_cast<char *>(ws), static_cast<char *>(ws) + buf, static_cast<char *>(ws) + 2 * buf};
     const void *cur = in;
-    int curH = (seg == 0) ? H : (H * 2), curC = (seg == 0) ? c.in_channels : slim_channels(c.widths[ri_prev], c.base_channels[seg - 1]);
+    int curH = (seg == 0) ? H : (H * 2);
+    int curC = (seg == 0) ? c.in_channels : slim_channels(c.widths[ri_prev], c.base_channels[seg - 1]);
     if (seg == 0) {
         DevLayer &Ls = S.L[0];
+        const double pix = static_cast<double>(B) * H * H;
+        const double flops = 2.0 * pix * C * 9 * c.in_channels;
+        const double bytes = eb * pix * (c.in_channels + C) + 4.0 * C * 9 * c.in_channels + 8.0 * C;
+        LaunchProf prof(ctx, st);
         cudaError_t e = bf ? launch_stem_bf16(static_cast<const uint16_t *>(in), static_cast<const float *>(Ls.w),
                                               Ls.sh.cin, Ls.scale[ri], Ls.shift[ri], reinterpret_cast<uint16_t *>(bufs[0]),
                                               B, H, H, c.in_channels, C, st)
                            : launch_stem_f32(static_cast<const float *>(in), static_cast<const float *>(Ls.w),
                                              Ls.sh.cin, Ls.scale[ri], Ls.shift[ri], reinterpret_cast<float *>(bufs[0]),
                                              B, H, H, c.in_channels, C, st);
-        ctx->launches++;
+        prof.done(SLIM_K_STEM, 0, 0, r, r, B, flops, bytes);
         if (e != cudaSuccess) return fail(ctx, SLIM_ECUDA, "stem launch: %s", cudaGetErrorString(e));
         cur = bufs[0];
         curH = H;
@@ -391,43 +479,99 @@ slim_status run_segment(slim_ctx *ctx, int seg, int ri_prev, int ri, int B, cons
             if (bufs[i] != cur) free_[nf++] = bufs[i];
         char *T = free_[0];
         void *dst = (b == nb - 1 && seg < 3) ? out : free_[1];
-        slim_status s1, s2;
-        if (bf) {
-            s1 = conv_bf16(ctx, st, S.L[bi.c1], ri_in, ri, cur, B, curH, curH, curC, nullptr, 0, nullptr, 0, 0, 0,
-                           nullptr, T, EPI_BN_RELU);
-            if (s1) return s1;
-            if (down)
-                s2 = conv_bf16(ctx, st, S.L[bi.c2], ri, ri, T, B, H, H, C, &S.L[bi.sc], ri_in, cur, curH, curH, curC,
-                               nullptr, dst, EPI_BN_PROJ_RELU);
-            else
-                s2 = conv_bf16(ctx, st, S.L[bi.c2], ri, ri, T, B, H, H, C, nullptr, 0, nullptr, 0, 0, 0, cur, dst,
-                               EPI_BN_ADD_RELU);
+        ConvCall c1;   // t = relu(BN1(conv3x3_s(x)))
+        c1.seg = seg;
+        c1.layer = bi.c1;
+        c1.L = &S.L[bi.c1];
+        c1.ri_in = ri_in;
+        c1.x = cur;
+        c1.H = c1.W = curH;
+        c1.c_in = curC;
+        c1.out = T;
+        c1.epi = EPI_BN_RELU;
+        ConvCall c2;   // out = relu(BN2(conv3x3(t)) + shortcut)
+        c2.seg = seg;
+        c2.layer = bi.c2;
+        c2.L = &S.L[bi.c2];
+        c2.ri_in = ri;
+        c2.x = T;
+        c2.H = c2.W = H;
+        c2.c_in = C;
+        c2.out = dst;
+        if (down) {
+            c2.epi = EPI_BN_PROJ_RELU;
+            c2.Lp = &S.L[bi.sc];
+            c2.layer_p = bi.sc;
+            c2.ri_in_p = ri_in;
+            c2.xp = cur;
+            c2.Hp = c2.Wp = curH;
+            c2.c_in_p = curC;
         } else {
-            s1 = conv_f32(ctx, st, S.L[bi.c1], ri, cur, B, curH, curH, curC, nullptr, nullptr, 0, 0, 0, nullptr, T,
-                          EPI_BN_RELU);
-            if (s1) return s1;
-            if (down)
-                s2 = conv_f32(ctx, st, S.L[bi.c2], ri, T, B, H, H, C, &S.L[bi.sc], cur, curH, curH, curC, nullptr, dst,
-                              EPI_BN_PROJ_RELU);
-            else
-                s2 = conv_f32(ctx, st, S.L[bi.c2], ri, T, B, H, H, C, nullptr, nullptr, 0, 0, 0, cur, dst,
-                              EPI_BN_ADD_RELU);
+            c2.epi = EPI_BN_ADD_RELU;
+            c2.res = cur;
         }
+        slim_status s1 = bf ? conv_bf16(ctx, st, c1, ri, B) : conv_f32(ctx, st, c1, ri, B);
+        if (s1) return s1;
+        slim_status s2 = bf ? conv_bf16(ctx, st, c2, ri, B) : conv_f32(ctx, st, c2, ri, B);
         if (s2) return s2;
         cur = dst;
         curH = H;
         curC = C;
     }
     if (seg == 3) {
+        const double K = c.num_classes;
+        const double flops = 2.0 * B * C * K + static_cast<double>(B) * H * H * C;
+        const double bytes = eb * B * H * H * C + 4.0 * K * (C + 1) + 4.0 * B * K;
+        LaunchProf prof(ctx, st);
         cudaError_t e = bf ? launch_head_bf16(static_cast<const uint16_t *>(cur), S.fc_w, S.fc_b,
                                               static_cast<float *>(out), B, H * H, C, c.base_channels[3],
                                               c.num_classes, st)
                            : launch_head_f32(static_cast<const float *>(cur), S.fc_w, S.fc_b, static_cast<float *>(out),
                                              B, H * H, C, c.base_channels[3], c.num_classes, st);
-        ctx->launches++;
+        prof.done(SLIM_K_HEAD, 3, -1, r, r, B, flops, bytes);
         if (e != cudaSuccess) return fail(ctx, SLIM_ECUDA, "head launch: %s", cudaGetErrorString(e));
     }
     return SLIM_OK;
+}
+
+// Graph mode: replay a captured launch sequence for an identical argument list.
+template <class F>
+slim_status run_graphed(slim_ctx *ctx, const std::string &key, cudaStream_t st, F &&body) {
+    if (!ctx->graph_mode || ctx->prof_on) return body(st);
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return body(st);
+    std::lock_guard<std::mutex> g(ctx->graph_mu);
+    auto it = ctx->graphs.find(key);
+    if (it == ctx->graphs.end()) {
+        const uint64_t l0 = ctx->launches.load();
+        CUDA_TRY(ctx, cudaStreamBeginCapture(ctx->cap_stream, cudaStreamCaptureModeThreadLocal));
+        slim_status s = body(ctx->cap_stream);
+        cudaGraph_t graph = nullptr;
+        cudaError_t e = cudaStreamEndCapture(ctx->cap_stream, &graph);
+        if (s != SLIM_OK) {
+            if (graph) cudaGraphDestroy(graph);
+            return s;
+        }
+        if (e != cudaSuccess) return fail(ctx, SLIM_ECUDA, "graph capture: %s", cudaGetErrorString(e));
+        cudaGraphExec_t exec = nullptr;
+        e = cudaGraphInstantiate(&exec, graph, 0);
+        cudaGraphDestroy(graph);
+        if (e != cudaSuccess) return fail(ctx, SLIM_ECUDA, "graph instantiate: %s", cudaGetErrorString(e));
+        const uint64_t n = ctx->launches.load() - l0;
+        ctx->launches -= n;   // counted when replayed
+        it = ctx->graphs.emplace(key, slim_ctx::GraphEntry{exec, n}).first;
+    }
+    CUDA_TRY(ctx, cudaGraphLaunch(it->second.exec, st));
+    ctx->launches += it->second.n_kernels;
+    return SLIM_OK;
+}
+
+template <class... T>
+std::string make_key(T... v) {
+    std::string k;
+    int dummy[] = {(k.append(reinterpret_cast<const char *>(&v), sizeof(v)), 0)...};
+    (void)dummy;
+    return k;
 }
 
 void free_segment(DevSegment &S) {
@@ -534,6 +678,11 @@ slim_status slim_create(int device, const slim_config *cfg, slim_ctx **out) {
         return SLIM_ENOMEM;
     }
     ctx->ws_bytes = ws;
+    if (cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking) != cudaSuccess) {
+        cudaFree(ctx->ws);
+        delete ctx;
+        return SLIM_ECUDA;
+    }
     *out = ctx;
     return SLIM_OK;
 }
@@ -541,6 +690,10 @@ slim_status slim_create(int device, const slim_config *cfg, slim_ctx **out) {
 void slim_destroy(slim_ctx *ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
+    cudaDeviceSynchronize();
+    clear_graphs(ctx);
+    for (auto ev : ctx->prof_ev) cudaEventDestroy(ev);
+    if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
     for (int s = 0; s < 4; ++s) free_segment(ctx->seg[s]);
     cudaFree(ctx->ws);
     delete ctx;
@@ -570,6 +723,7 @@ slim_status slim_load_segment(slim_ctx *ctx, int seg, const slim_seg_weights *w,
     }
     cudaSetDevice(ctx->device);
     cudaDeviceSynchronize();   // no forward of this segment may be in flight (documented contract)
+    clear_graphs(ctx);         // captured graphs hold the old weight addresses
     free_segment(ctx->seg[seg]);
     DevSegment &S = ctx->seg[seg];
     S.n_conv = n;
@@ -622,6 +776,7 @@ slim_status slim_unload_segment(slim_ctx *ctx, int seg) {
     if (!ctx || seg < 0 || seg > 3) return SLIM_EINVAL;
     cudaSetDevice(ctx->device);
     cudaDeviceSynchronize();
+    clear_graphs(ctx);
     free_segment(ctx->seg[seg]);
     return SLIM_OK;
 }
@@ -657,7 +812,11 @@ slim_status slim_forward_ws(slim_ctx *ctx, int seg, float r_prev, float r, int b
     if (!ws || !aligned16(ws) || ws_bytes < seg_ws_bytes(ctx->cfg, seg, r, batch))
         return fail(ctx, SLIM_EINVAL, "workspace too small or misaligned");
     if ((s = check_sticky(ctx))) return s;
-    return run_segment(ctx, seg, ri_prev, ri, batch, in, out, ws, static_cast<cudaStream_t>(stream));
+    const std::string key = make_key('S', seg, ri_prev, ri, batch, in, static_cast<const void *>(out),
+                                     static_cast<const void *>(ws));
+    return run_graphed(ctx, key, static_cast<cudaStream_t>(stream), [&](cudaStream_t st) {
+        return run_segment(ctx, seg, ri_prev, ri, batch, in, out, ws, st);
+    });
 }
 
 slim_status slim_forward(slim_ctx *ctx, int seg, float r_prev, float r, int batch, const void *in, void *out,
@@ -695,14 +854,18 @@ slim_status slim_forward_chain(slim_ctx *ctx, const float r[4], int batch, const
     }
     char *o[2] = {static_cast<char *>(ws), static_cast<char *>(ws) + inter};
     char *segws = static_cast<char *>(ws) + 2 * inter;
-    cudaStream_t st = static_cast<cudaStream_t>(stream);
-    const void *cur = in;
-    for (int k = 0; k < 4; ++k) {
-        void *dst = (k == 3) ? static_cast<void *>(logits) : o[k & 1];
-        if ((s = run_segment(ctx, k, rip[k], ri[k], batch, cur, dst, segws, st))) return s;
-        cur = dst;
-    }
-    return SLIM_OK;
+    const std::string key = make_key('C', ri[0], ri[1], ri[2], ri[3], batch, in, static_cast<const void *>(logits),
+                                     static_cast<const void *>(ws));
+    return run_graphed(ctx, key, static_cast<cudaStream_t>(stream), [&](cudaStream_t st) {
+        const void *cur = in;
+        for (int k = 0; k < 4; ++k) {
+            void *dst = (k == 3) ? static_cast<void *>(logits) : o[k & 1];
+            slim_status s2 = run_segment(ctx, k, rip[k], ri[k], batch, cur, dst, segws, st);
+            if (s2) return s2;
+            cur = dst;
+        }
+        return SLIM_OK;
+    });
 }
 
 slim_status slim_pack(const slim_config *cfg, const slim_request *q, int n, int B_max, slim_launch_desc *descs,
@@ -751,8 +914,9 @@ slim_status slim_gather(slim_ctx *ctx, const void *src, const uint32_t *idx, int
     if (!ctx || n < 0 || (n > 0 && (!src || !idx || !dst)) || row_bytes % 16 || !aligned16(src) || !aligned16(dst))
         return ctx ? fail(ctx, SLIM_EINVAL, "gather: bad arguments") : SLIM_EINVAL;
     if (n == 0) return SLIM_OK;
+    LaunchProf prof(ctx, static_cast<cudaStream_t>(stream));
     cudaError_t e = launch_gather(src, row_bytes, idx, n, row_bytes, dst, static_cast<cudaStream_t>(stream));
-    ctx->launches++;
+    prof.done(SLIM_K_GATHER, -1, -1, 0.f, 0.f, n, 0.0, 2.0 * n * static_cast<double>(row_bytes) + 4.0 * n);
     if (e != cudaSuccess) return fail(ctx, SLIM_ECUDA, "gather launch: %s", cudaGetErrorString(e));
     return SLIM_OK;
 }
@@ -771,12 +935,51 @@ slim_status slim_launch(slim_ctx *ctx, const slim_launch_desc *d, const uint32_t
     if (slots) {
         if (!slab || !aligned16(slab) || pool_row_bytes < row || pool_row_bytes % 16 || row % 16)
             return fail(ctx, SLIM_EINVAL, "launch: slab/pool rows invalid");
-        cudaError_t e = launch_gather(pool, pool_row_bytes, slots, d->batch, row, slab, static_cast<cudaStream_t>(stream));
-        ctx->launches++;
+        LaunchProf prof(ctx, static_cast<cudaStream_t>(stream));
+        cudaError_t e =
+            launch_gather(pool, pool_row_bytes, slots, d->batch, row, slab, static_cast<cudaStream_t>(stream));
+        prof.done(SLIM_K_GATHER, d->seg, -1, d->r_prev, d->r, d->batch, 0.0,
+                  2.0 * d->batch * static_cast<double>(row) + 4.0 * d->batch);
         if (e != cudaSuccess) return fail(ctx, SLIM_ECUDA, "gather launch: %s", cudaGetErrorString(e));
         in = slab;
     }
     return slim_forward_ws(ctx, d->seg, d->r_prev, d->r, d->batch, in, out, ws, ws_bytes, stream);
+}
+
+slim_status slim_set_graph_mode(slim_ctx *ctx, int enable) {
+    if (!ctx) return SLIM_EINVAL;
+    if (!enable) clear_graphs(ctx);
+    ctx->graph_mode = enable != 0;
+    return SLIM_OK;
+}
+
+slim_status slim_profile_begin(slim_ctx *ctx, int max_launches) {
+    if (!ctx || max_launches < 1) return SLIM_EINVAL;
+    cudaSetDevice(ctx->device);
+    while (ctx->prof_ev.size() < 2 * static_cast<size_t>(max_launches)) {
+        cudaEvent_t ev;
+        CUDA_TRY(ctx, cudaEventCreate(&ev));
+        ctx->prof_ev.push_back(ev);
+    }
+    ctx->prof_rec.clear();
+    ctx->prof_rec.reserve(max_launches);
+    ctx->prof_on = true;
+    return SLIM_OK;
+}
+
+slim_status slim_profile_end(slim_ctx *ctx, slim_profile_record *out, int max_out, int *n_out) {
+    if (!ctx || !n_out) return SLIM_EINVAL;
+    ctx->prof_on = false;
+    CUDA_TRY(ctx, cudaDeviceSynchronize());
+    int n = 0;
+    for (size_t i = 0; i < ctx->prof_rec.size() && n < max_out; ++i, ++n) {
+        float ms = 0.f;
+        CUDA_TRY(ctx, cudaEventElapsedTime(&ms, ctx->prof_ev[2 * i], ctx->prof_ev[2 * i + 1]));
+        ctx->prof_rec[i].ms = ms;
+        if (out) out[n] = ctx->prof_rec[i];
+    }
+    *n_out = out ? n : static_cast<int>(ctx->prof_rec.size());
+    return SLIM_OK;
 }
 
 slim_status slim_last_error(slim_ctx *ctx) {

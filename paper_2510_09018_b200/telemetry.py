@@ -1,0 +1,159 @@
+"""Per-device telemetry: NVML sampling and the NCCL all-gather of the router's state.
+
+PAPER.md:49 -- the executor "samples utilization and emits telemetry data
+(utilization, VRAM, per-segment queue sizes, latency percentiles)"; Eq. 1
+ -- the router state holds, per server i, (q_i, P_i, U_i).  Each rank
+packs one float32[8] record (SI units, SURVEY §8(c) reading #15):
+
+    [queue_len, power_W, util_frac, mean_latency_s, energy_J_since_tick,
+     completed, vram_used_GB, rank]
+
+and `TelemetryExchange.tick()` all-gathers the records of all ranks with one
+`all_gather_into_tensor` (NCCL over NVLink on GPUs, gloo on CPU) on a side stream.
+This is host-side control plumbing, not the compute path.
+"""
+from __future__ import annotations
+
+import threading
+import time
+
+import numpy as np
+
+RECORD_LEN = 8
+FIELDS = ("queue_len", "power_W", "util_frac", "mean_latency_s", "energy_J", "completed", "vram_used_GB", "rank")
+
+# NVML clock-event reason bits (nvml.h) -> names used in the bench JSON line
+_REASONS = {0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x10: "sync_boost",
+            0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+            0x100: "display_clock_setting"}
+
+
+def reason_names(mask: int):
+    return [n for b, n in _REASONS.items() if mask & b]
+
+
+def pack_record(queue_len=0.0, power_w=0.0, util=0.0, mean_latency_s=0.0, energy_j=0.0, completed=0.0,
+                vram_gb=0.0, rank=0.0) -> np.ndarray:
+    return np.array([queue_len, power_w, util, mean_latency_s, energy_j, completed, vram_gb, rank], np.float32)
+
+
+def util_variance(utils) -> float:
+    """Var(U/100) of Eq. 7: population variance of utilisation fractions.
+    SPEC example: [0, 1] -> 0.25."""
+    u = np.asarray(utils, np.float64)
+    return float(((u - u.mean()) ** 2).mean()) if u.size else 0.0
+
+
+class NvmlSampler:
+    """Background sampler of SM clock, power, utilisation and clock-event reasons."""
+
+    def __init__(self, device_index: int = 0, period_s: float = 0.01):
+        self.period = period_s
+        self.samples = []
+        self._stop = threading.Event()
+        self._thr = None
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_sm = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self._nv = None
+            self.max_sm = None
+
+    def energy_mj(self):
+        if not self.ok:
+            return None
+        try:
+            return self._nv.nvmlDeviceGetTotalEnergyConsumption(self._h)
+        except Exception:
+            return None
+
+    def sample(self):
+        nv, h = self._nv, self._h
+        try:
+            reasons = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+        except Exception:
+            reasons = nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+        return dict(t=time.time(), sm=nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM),
+                    power_w=nv.nvmlDeviceGetPowerUsage(h) / 1000.0,
+                    util=nv.nvmlDeviceGetUtilizationRates(h).gpu / 100.0, reasons=int(reasons),
+                    mem_gb=nv.nvmlDeviceGetMemoryInfo(h).used / 2 ** 30)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.sample())
+            except Exception:
+                pass
+            self._stop.wait(self.period)
+
+    def start(self):
+        if self.ok:
+            self.samples = []
+            self._stop.clear()
+            self._thr = threading.Thread(target=self._run, daemon=True)
+            self._thr.start()
+
+    def stop(self):
+        if self._thr is not None:
+            self._stop.set()
+            self._thr.join()
+            self._thr = None
+            try:
+                self.samples.append(self.sample())
+            except Exception:
+                pass
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_sm, "reasons": [], "samples": 0}
+        sm = sorted(s["sm"] for s in self.samples)
+        mask = 0
+        for s in self.samples:
+            mask |= s["reasons"]
+        return {"sm_mhz": float(sm[len(sm) // 2]), "sm_max_mhz": self.max_sm, "reasons": reason_names(mask),
+                "samples": len(self.samples), "power_w_max": max(s["power_w"] for s in self.samples)}
+
+
+class TelemetryExchange:
+    """One all_gather_into_tensor of float32[8] per rank per router tick."""
+
+    def __init__(self, group=None, device=None):
+        import torch
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.device = device if device is not None else "cpu"
+        self.send = torch.zeros(RECORD_LEN, dtype=torch.float32, device=self.device)
+        self.recv = torch.zeros(self.world * RECORD_LEN, dtype=torch.float32, device=self.device)
+        self.stream = torch.cuda.Stream(device=self.device) if str(self.device).startswith("cuda") else None
+
+    def tick(self, record: np.ndarray, wait: bool = False):
+        """Start the all-gather of this rank's record; returns a handle (or the gathered [world, 8] array)."""
+        import torch
+        rec = torch.from_numpy(np.asarray(record, np.float32))
+        if self.stream is not None:
+            cur = torch.cuda.current_stream(self.device)
+            self.stream.wait_stream(cur)
+            with torch.cuda.stream(self.stream):
+                self.send.copy_(rec, non_blocking=True)
+                work = self.dist.all_gather_into_tensor(self.recv, self.send, group=self.group, async_op=True)
+        else:
+            self.send.copy_(rec)
+            work = self.dist.all_gather_into_tensor(self.recv, self.send, group=self.group, async_op=True)
+        if wait:
+            work.wait()
+            if self.stream is not None:
+                self.stream.synchronize()
+            return self.recv.view(self.world, RECORD_LEN).cpu().numpy()
+        return work
+
+    def gathered(self) -> np.ndarray:
+        if self.stream is not None:
+            self.stream.synchronize()
+        return self.recv.view(self.world, RECORD_LEN).cpu().numpy()

@@ -236,3 +236,40 @@ def test_pack_gather_launch_matches_direct(net, ref):
         direct = net.forward(seg, _dev(pool_np[idx][..., :cin]), d["r_prev"], d["r"])
         torch.cuda.synchronize()
         assert torch.equal(out, direct)
+
+
+# ------------------------------------------------------------------ graph mode + profiling
+def test_graph_mode_bitwise_and_launch_count(params):
+    w, bn = params
+    n = slim.SlimNet(w, bn, max_batch=32)
+    x = _dev(synth.make_images(20, offset=17))
+    tup = (0.25, 1.0, 0.75, 0.5)
+    a = n.forward_chain(x, tup).clone()
+    c0 = slim.slim_launch_count(n.ctx)
+    n.forward_chain(x, tup)
+    per_chain = slim.slim_launch_count(n.ctx) - c0
+    assert per_chain == 1 + 4 + 4 * 3 + 1          # stem + 2 convs x 8 blocks + head
+    slim.slim_set_graph_mode(n.ctx, True)
+    logits = torch.empty_like(a)
+    for _ in range(3):
+        n.forward_chain(x, tup, logits=logits)
+        torch.cuda.synchronize()
+        assert torch.equal(logits, a)
+    c1 = slim.slim_launch_count(n.ctx)
+    n.forward_chain(x, tup, logits=logits)
+    assert slim.slim_launch_count(n.ctx) - c1 == per_chain
+    n.close()
+
+
+def test_profile_records_cover_every_launch(net):
+    x = _dev(synth.make_images(16, offset=18))
+    slim.slim_profile_begin(net.ctx, 64)
+    net.forward_chain(x, (1.0,) * 4)
+    recs = slim.slim_profile_end(net.ctx)
+    assert len(recs) == 18
+    kinds = [r["kind"] for r in recs]
+    assert kinds[0] == "stem" and kinds[-1] == "head" and kinds.count("conv_umma") == 16
+    assert all(r["ms"] > 0 for r in recs)
+    # sliced FLOPs of the r=1 chain: 1110.94 MFLOP per image
+    total = sum(r["flops"] for r in recs) / 16
+    assert abs(total / 1e6 - 1110.94) / 1110.94 < 2e-3
