@@ -88,29 +88,123 @@ __global__ void __launch_bounds__(kStemThreads)
 }
 
 // ---------------------------------------------------------------- head
+// Grid (ceil(B/8), ceil(K/kHeadClasses)).  A CTA pools its 8 images into smem
+// (fp32; 16 independent loads in flight per thread), then each warp takes classes
+// k of its group; each lane holds its slice of the FC row in registers (all loads
+// issued before the FMAs) and accumulates the 8 images at once; warp-shuffle sum.
 constexpr int kHeadThreads = 256;
+constexpr int kHeadImgs = 8;
+constexpr int kHeadClasses = 16;
+constexpr int kHeadMaxC = 1024;   // c3 <= 1024 -> <= 32 channels per lane
 template <typename TIn>
 __global__ void __launch_bounds__(kHeadThreads)
     head_kernel(const TIn *__restrict__ in, const float *__restrict__ fc_w, const float *__restrict__ fc_b,
-                float *__restrict__ logits, int P, int c3, int c3_full, int K) {
-    extern __shared__ float s_p[];
-    const int n = blockIdx.x;
-    const TIn *x = in + static_cast<size_t>(n) * P * c3;
+                float *__restrict__ logits, int B, int P, int c3, int c3_full, int K) {
+    extern __shared__ float s_p[];   // [kHeadImgs][c3]
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    const int n0 = blockIdx.x * kHeadImgs;
+    const int ni = min(kHeadImgs, B - n0);
     const float inv = 1.f / static_cast<float>(P);
-    for (int c = threadIdx.x; c < c3; c += blockDim.x) {   // consecutive threads: consecutive channels
-        float s = 0.f;
-        for (int p = 0; p < P; ++p) s += ld_act(x + static_cast<size_t>(p) * c3 + c);
-        s_p[c] = s * inv;
+    for (int i = threadIdx.x; i < kHeadImgs * c3; i += blockDim.x) {   // consecutive threads: consecutive channels
+        const int img = i / c3, c = i - img * c3;
+        float sum = 0.f;
+        if (img < ni) {
+            const TIn *x = in + (static_cast<size_t>(n0 + img) * P) * c3 + c;
+            int p = 0;
+            for (; p + 8 <= P; p += 8) {
+                float v[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) v[u] = ld_act(x + static_cast<size_t>(p + u) * c3);
+#pragma unroll
+                for (int u = 0; u < 8; ++u) sum += v[u];
+            }
+            for (; p < P; ++p) sum += ld_act(x + static_cast<size_t>(p) * c3);
+        }
+        s_p[i] = sum * inv;
     }
     __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-    for (int k = warp; k < K; k += nw) {
+    const int k_end = min(K, (blockIdx.y + 1) * kHeadClasses);
+    for (int k = blockIdx.y * kHeadClasses + warp; k < k_end; k += nw) {
         const float *wr = fc_w + static_cast<size_t>(k) * c3_full;
-        float d = 0.f;
-        for (int c = lane; c < c3; c += 32) d = fmaf(s_p[c], __ldg(wr + c), d);
+        float w[kHeadMaxC / 32];
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
-        if (lane == 0) logits[static_cast<size_t>(n) * K + k] = d + fc_b[k];
+        for (int i = 0; i < kHeadMaxC / 32; ++i) {
+            const int c = lane + 32 * i;
+            w[i] = (c < c3) ? __ldg(wr + c) : 0.f;
+        }
+        float d[kHeadImgs];
+#pragma unroll
+        for (int j = 0; j < kHeadImgs; ++j) d[j] = 0.f;
+#pragma unroll
+        for (int i = 0; i < kHeadMaxC / 32; ++i) {
+            const int c = lane + 32 * i;
+            if (c < c3) {
+#pragma unroll
+                for (int j = 0; j < kHeadImgs; ++j) d[j] = fmaf(s_p[j * c3 + c], w[i], d[j]);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < kHeadImgs; ++j)
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) d[j] += __shfl_xor_sync(0xffffffffu, d[j], o);
+        if (lane < ni) {
+            float v = d[0];
+#pragma unroll
+            for (int j = 1; j < kHeadImgs; ++j) v = (lane == j) ? d[j] : v;
+            logits[static_cast<size_t>(n0 + lane) * K + k] = v + fc_b[k];
+        }
+    }
+}
+
+// FC on pooled fp32 features (global average pool fused into the last conv's
+// epilogue): grid (ceil(B/8), ceil(K/16)); the 8 pooled vectors are loaded with
+// independent 16-byte loads, each FC row is held in registers, warp-shuffle sums.
+__global__ void __launch_bounds__(kHeadThreads)
+    fc_kernel(const float *__restrict__ pooled, const float *__restrict__ fc_w, const float *__restrict__ fc_b,
+              float *__restrict__ logits, int B, int c3, int c3_full, int K) {
+    extern __shared__ float s_p[];   // [kHeadImgs][c3]
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    const int n0 = blockIdx.x * kHeadImgs;
+    const int ni = min(kHeadImgs, B - n0);
+    const int nv = ni * c3 / 4;
+    const float4 *src = reinterpret_cast<const float4 *>(pooled + static_cast<size_t>(n0) * c3);
+    for (int i = threadIdx.x; i < kHeadImgs * c3 / 4; i += blockDim.x)
+        reinterpret_cast<float4 *>(s_p)[i] = i < nv ? __ldg(src + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    const int k_end = min(K, (blockIdx.y + 1) * kHeadClasses);
+    for (int k = blockIdx.y * kHeadClasses + warp; k < k_end; k += nw) {
+        const float *wr = fc_w + static_cast<size_t>(k) * c3_full;
+        float w[kHeadMaxC / 32];
+#pragma unroll
+        for (int i = 0; i < kHeadMaxC / 32; ++i) {
+            const int c = lane + 32 * i;
+            w[i] = (c < c3) ? __ldg(wr + c) : 0.f;
+        }
+        float d[kHeadImgs];
+#pragma unroll
+        for (int j = 0; j < kHeadImgs; ++j) d[j] = 0.f;
+#pragma unroll
+        for (int i = 0; i < kHeadMaxC / 32; ++i) {
+            const int c = lane + 32 * i;
+            if (c < c3) {
+#pragma unroll
+                for (int j = 0; j < kHeadImgs; ++j) d[j] = fmaf(s_p[j * c3 + c], w[i], d[j]);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < kHeadImgs; ++j)
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) d[j] += __shfl_xor_sync(0xffffffffu, d[j], o);
+        if (lane < ni) {
+            float v = d[0];
+#pragma unroll
+            for (int j = 1; j < kHeadImgs; ++j) v = (lane == j) ? d[j] : v;
+            logits[static_cast<size_t>(n0 + lane) * K + k] = v + fc_b[k];
+        }
     }
 }
 
@@ -219,15 +313,40 @@ cudaError_t launch_stem_f32(const float *in, const float *w, int cin_full, const
     stem_kernel<float, float><<<grid, kStemThreads, 0, s>>>(in, w, cin_full, scale, shift, out, H, W, cimg, c0);
     return cudaGetLastError();
 }
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, bool pdl,
+                       Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 cudaError_t launch_head_bf16(const uint16_t *in, const float *fc_w, const float *fc_b, float *logits, int B, int P,
-                             int c3, int c3_full, int K, cudaStream_t s) {
-    head_kernel<uint16_t><<<B, kHeadThreads, c3 * sizeof(float), s>>>(in, fc_w, fc_b, logits, P, c3, c3_full, K);
-    return cudaGetLastError();
+                             int c3, int c3_full, int K, cudaStream_t s, bool pdl) {
+    return launch_pdl(head_kernel<uint16_t>,
+                      dim3((B + kHeadImgs - 1) / kHeadImgs, (K + kHeadClasses - 1) / kHeadClasses), dim3(kHeadThreads),
+                      kHeadImgs * c3 * sizeof(float), s, pdl, in, fc_w, fc_b, logits, B, P, c3, c3_full, K);
 }
 cudaError_t launch_head_f32(const float *in, const float *fc_w, const float *fc_b, float *logits, int B, int P, int c3,
-                            int c3_full, int K, cudaStream_t s) {
-    head_kernel<float><<<B, kHeadThreads, c3 * sizeof(float), s>>>(in, fc_w, fc_b, logits, P, c3, c3_full, K);
-    return cudaGetLastError();
+                            int c3_full, int K, cudaStream_t s, bool pdl) {
+    return launch_pdl(head_kernel<float>,
+                      dim3((B + kHeadImgs - 1) / kHeadImgs, (K + kHeadClasses - 1) / kHeadClasses), dim3(kHeadThreads),
+                      kHeadImgs * c3 * sizeof(float), s, pdl, in, fc_w, fc_b, logits, B, P, c3, c3_full, K);
+}
+cudaError_t launch_fc_f32(const float *pooled, const float *fc_w, const float *fc_b, float *logits, int B, int c3,
+                          int c3_full, int K, cudaStream_t s, bool pdl) {
+    if (c3 % 4 || c3 > kHeadMaxC) return cudaErrorInvalidValue;
+    return launch_pdl(fc_kernel, dim3((B + kHeadImgs - 1) / kHeadImgs, (K + kHeadClasses - 1) / kHeadClasses),
+                      dim3(kHeadThreads), kHeadImgs * c3 * sizeof(float), s, pdl, pooled, fc_w, fc_b, logits, B, c3,
+                      c3_full, K);
 }
 cudaError_t launch_gather(const void *src, size_t src_stride, const uint32_t *idx, int n, size_t row_bytes, void *dst,
                           cudaStream_t s) {

@@ -28,12 +28,19 @@
 
 #include <cuda_bf16.h>
 
+#include <cstdio>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 
 namespace slim {
 namespace {
 
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -177,22 +184,30 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     // 1024-byte alignment: SW128 TMA boxes and UMMA descriptors (base_offset = 0)
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int S = a.n_stages;
+    const uint32_t chunk_bytes = a.n_out_chunks * 16384u;   // one 128-pixel x n_tile tile, SW128
     const uint32_t sA = smem_u32(smem);
     const uint32_t sB = sA + S * kTileABytes;
     const uint32_t sOut = sB + S * a.stage_b_bytes;
+    const uint32_t sRes = sOut + chunk_bytes;
+    const int n_res = (a.epi == EPI_BN_ADD_RELU) ? a.res_slots : 0;
     uint8_t *pOut = smem + (sOut - sA);
-    uint64_t *bars = reinterpret_cast<uint64_t *>(pOut + a.n_out_chunks * 16384);
+    uint8_t *pRes = smem + (sRes - sA);
+    float *sBN = reinterpret_cast<float *>(pRes + n_res * chunk_bytes);   // scale0|shift0|scale1|shift1, c_out each
+    uint64_t *bars = reinterpret_cast<uint64_t *>(sBN + 4 * a.c_out);
     const uint32_t bar0 = smem_u32(bars);
-    // barrier map: full[0,S) empty[S,2S) tmem_full[2S,2S+2) tmem_empty[2S+2,2S+4) res[2S+4]
+    // barrier map: full[0,S) empty[S,2S) tmem_full[2S,2S+2) tmem_empty[2S+2,2S+4) res_full[2S+4,+2) res_empty[2S+6,+2)
     auto full_bar = [&](int i) { return bar0 + 8u * i; };
     auto empty_bar = [&](int i) { return bar0 + 8u * (S + i); };
     auto tfull_bar = [&](int i) { return bar0 + 8u * (2 * S + i); };
     auto tempty_bar = [&](int i) { return bar0 + 8u * (2 * S + 2 + i); };
-    const uint32_t res_bar = bar0 + 8u * (2 * S + 4);
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * S + 5);
+    auto rfull_bar = [&](int i) { return bar0 + 8u * (2 * S + 4 + i); };
+    auto rempty_bar = [&](int i) { return bar0 + 8u * (2 * S + 6 + i); };
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * S + 8);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int total = a.m_tiles * a.n_tiles;
+    unsigned long long *tr = a.trace ? a.trace + blockIdx.x * 8 : nullptr;
+    if (tr && threadIdx.x == 0) tr[0] = gtimer();
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < S; ++i) {
@@ -202,8 +217,9 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         for (int i = 0; i < 2; ++i) {
             mbar_init(tfull_bar(i), 1);
             mbar_init(tempty_bar(i), 128);
+            mbar_init(rfull_bar(i), 1);
+            mbar_init(rempty_bar(i), 128);
         }
-        mbar_init(res_bar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         prefetch_tmap(&tmA0);
         prefetch_tmap(&tmB0);
@@ -211,7 +227,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
             prefetch_tmap(&tmA1);
             prefetch_tmap(&tmB1);
         }
-        prefetch_tmap(&tmOut);
+        if (!a.pool_out) prefetch_tmap(&tmOut);
         if (a.epi == EPI_BN_ADD_RELU) prefetch_tmap(&tmRes);
     }
     if (warp == 1) {
@@ -220,19 +236,47 @@ __global__ void __launch_bounds__(kConvThreads, 1)
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
+    // the folded BN vectors are weights (not produced by the previous kernel): stage
+    // them in smem before the PDL wait so the epilogue never waits on global loads
+    for (int i = threadIdx.x; i < a.c_out; i += blockDim.x) {
+        sBN[i] = a.scale0[i];
+        sBN[a.c_out + i] = a.shift0[i];
+        if (a.n_parts > 1) {
+            sBN[2 * a.c_out + i] = a.scale1[i];
+            sBN[3 * a.c_out + i] = a.shift1[i];
+        }
+    }
+    // PDL: everything above overlapped the previous kernel's tail; wait for its
+    // results to be visible before any dependent global read, then let the next
+    // kernel start its own prologue as SMs free up.
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    if (tr && threadIdx.x == 0) tr[1] = gtimer();
 
     if (warp == 0) {
         // ===================== TMA producer (one thread) =====================
         if (lane == 0) {
-            int stage = 0;
-            uint32_t phase = 0;
+            int stage = 0, rs = 0;
+            uint32_t phase = 0, rphase = 0;
             const uint32_t tx = kTileABytes + a.stage_b_bytes;
             for (int t = blockIdx.x; t < total; t += gridDim.x) {
                 const TileCoord tc = tile_coord(a, t);
+                if (n_res) {   // residual tile of this output tile, prefetched a tile ahead of its epilogue
+                    mbar_wait(rempty_bar(rs), rphase ^ 1);
+                    if (a.debug & 8) mbar_arrive(rfull_bar(rs));
+                    else mbar_expect_tx(rfull_bar(rs), chunk_bytes);
+                    for (uint32_t j = 0; j < a.n_out_chunks && !(a.debug & 8); ++j)
+                        tma_load_4d(sRes + rs * chunk_bytes + j * 16384u, &tmRes, rfull_bar(rs), tc.co0 + j * kChunk, 0,
+                                    tc.h0, tc.n0);
+                    if (++rs == n_res) {
+                        rs = 0;
+                        rphase ^= 1;
+                    }
+                }
                 for (int p = 0; p < a.n_parts; ++p) {
                     const GemmPart &gp = a.part[p];
                     const CUtensorMap *tA = p ? &tmA1 : &tmA0;
@@ -241,10 +285,14 @@ __global__ void __launch_bounds__(kConvThreads, 1)
                         const int tap = kb / gp.n_chunks, ch = kb - tap * gp.n_chunks;
                         const int kh = tap / gp.ksize, kw = tap - kh * gp.ksize;
                         mbar_wait(empty_bar(stage), phase ^ 1);
-                        mbar_expect_tx(full_bar(stage), tx);
-                        tma_load_4d(sA + stage * kTileABytes, tA, full_bar(stage), ch * kChunk, kw - gp.pad,
-                                    tc.h0 * gp.stride + kh - gp.pad, tc.n0);
-                        tma_load_3d(sB + stage * a.stage_b_bytes, tB, full_bar(stage), ch * kChunk, tap, tc.co0);
+                        if (a.debug & 1) {
+                            mbar_arrive(full_bar(stage));
+                        } else {
+                            mbar_expect_tx(full_bar(stage), tx);
+                            tma_load_4d(sA + stage * kTileABytes, tA, full_bar(stage), ch * kChunk, kw - gp.pad,
+                                        tc.h0 * gp.stride + kh - gp.pad, tc.n0);
+                            tma_load_3d(sB + stage * a.stage_b_bytes, tB, full_bar(stage), ch * kChunk, tap, tc.co0);
+                        }
                         if (++stage == S) {
                             stage = 0;
                             phase ^= 1;
@@ -252,6 +300,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
                     }
                 }
             }
+            if (tr) tr[2] = gtimer();
         }
     } else if (warp == 1) {
         // ===================== MMA issuer (one thread) =======================
@@ -273,8 +322,9 @@ __global__ void __launch_bounds__(kConvThreads, 1)
                         tc_fence_after();
                         const uint64_t ad = umma_desc_sw128(sA + stage * kTileABytes);
                         const uint64_t bd = umma_desc_sw128(sB + stage * a.stage_b_bytes);
-                        for (int kk = 0; kk < nk; ++kk)   // K=16 per MMA = 32 bytes inside the 128-B atom
-                            umma_bf16(d, ad + 2 * kk, bd + 2 * kk, idesc, (kb | kk) != 0);
+                        if (!(a.debug & 2))
+                            for (int kk = 0; kk < nk; ++kk)   // K=16 per MMA = 32 bytes inside the 128-B atom
+                                umma_bf16(d, ad + 2 * kk, bd + 2 * kk, idesc, (kb | kk) != 0);
                         umma_commit(empty_bar(stage));   // frees the smem slot when these MMAs finish
                         if (++stage == S) {
                             stage = 0;
@@ -288,6 +338,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
                     aphase ^= 1;
                 }
             }
+            if (tr) tr[3] = gtimer();
         }
     } else {
         // ===================== epilogue (warps 2..5) =========================
@@ -296,24 +347,21 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         const bool leader = (warp == 2 && lane == 0);
         const uint32_t lane_addr = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
         const int sw = row & 7;
-        int as = 0;
+        const float *s0 = sBN, *t0 = sBN + a.c_out, *s1 = sBN + 2 * a.c_out, *t1 = sBN + 3 * a.c_out;
+        // fused pool: the image of this row and its pixel count P (P divides 32)
+        const int P = a.Ho * a.Wo;
+        int as = 0, rs = 0;
         uint32_t aphase = 0, rphase = 0;
         for (int t = blockIdx.x; t < total; t += gridDim.x) {
             const TileCoord tc = tile_coord(a, t);
             mbar_wait(tfull_bar(as), aphase);
             tc_fence_after();
-            if (leader) bulk_wait_read0();   // previous tile's stores have left the staging buffer
-            if (a.epi == EPI_BN_ADD_RELU) {
-                if (leader) {
-                    mbar_expect_tx(res_bar, a.n_out_chunks * 16384u);
-                    for (uint32_t j = 0; j < a.n_out_chunks; ++j)
-                        tma_load_4d(sOut + j * 16384u, &tmRes, res_bar, tc.co0 + j * kChunk, 0, tc.h0, tc.n0);
-                }
-                mbar_wait(res_bar, rphase);
-                rphase ^= 1;
-            } else {
+            if (!a.pool_out) {
+                if (leader) bulk_wait_read0();   // previous tile's stores have left the staging buffer
                 named_bar_sync(1, 128);
             }
+            if (n_res) mbar_wait(rfull_bar(rs), rphase);
+            const uint8_t *resp = pRes + rs * chunk_bytes;
             const uint32_t col0 = static_cast<uint32_t>(as * a.n_parts * a.acc_stride);
             for (int g = 0; g < a.n_tile / 16; ++g) {
                 uint32_t v[16], u[16];
@@ -323,35 +371,19 @@ __global__ void __launch_bounds__(kConvThreads, 1)
                 const int cl = g * 16;             // channel inside the tile
                 const int cg = tc.co0 + cl;        // global output channel
                 float f[16];
-                const float4 *s4 = reinterpret_cast<const float4 *>(a.scale0 + cg);
-                const float4 *t4 = reinterpret_cast<const float4 *>(a.shift0 + cg);
 #pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    const float4 s = __ldg(s4 + i), b = __ldg(t4 + i);
-                    f[4 * i + 0] = fmaf(__uint_as_float(v[4 * i + 0]), s.x, b.x);
-                    f[4 * i + 1] = fmaf(__uint_as_float(v[4 * i + 1]), s.y, b.y);
-                    f[4 * i + 2] = fmaf(__uint_as_float(v[4 * i + 2]), s.z, b.z);
-                    f[4 * i + 3] = fmaf(__uint_as_float(v[4 * i + 3]), s.w, b.w);
-                }
+                for (int i = 0; i < 16; ++i) f[i] = fmaf(__uint_as_float(v[i]), s0[cg + i], t0[cg + i]);
                 if (a.epi == EPI_BN_PROJ_RELU) {
-                    const float4 *s14 = reinterpret_cast<const float4 *>(a.scale1 + cg);
-                    const float4 *t14 = reinterpret_cast<const float4 *>(a.shift1 + cg);
 #pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        const float4 s = __ldg(s14 + i), b = __ldg(t14 + i);
-                        f[4 * i + 0] += fmaf(__uint_as_float(u[4 * i + 0]), s.x, b.x);
-                        f[4 * i + 1] += fmaf(__uint_as_float(u[4 * i + 1]), s.y, b.y);
-                        f[4 * i + 2] += fmaf(__uint_as_float(u[4 * i + 2]), s.z, b.z);
-                        f[4 * i + 3] += fmaf(__uint_as_float(u[4 * i + 3]), s.w, b.w);
-                    }
+                    for (int i = 0; i < 16; ++i) f[i] += fmaf(__uint_as_float(u[i]), s1[cg + i], t1[cg + i]);
                 }
-                // staging: chunk cl/64, row `row`, 16-B pieces (cl%64)/8 and +1, SW128 swizzled
-                uint8_t *rowp = pOut + (cl >> 6) * 16384 + row * 128;
+                // 16-B pieces (cl%64)/8 and +1 of row `row` in chunk cl/64, SW128 swizzled
                 const int q16 = (cl & 63) >> 3;
-                uint4 *p0 = reinterpret_cast<uint4 *>(rowp + (((q16) ^ sw) << 4));
-                uint4 *p1 = reinterpret_cast<uint4 *>(rowp + (((q16 + 1) ^ sw) << 4));
-                if (a.epi == EPI_BN_ADD_RELU) {
-                    const uint4 r0 = *p0, r1 = *p1;
+                const uint32_t off0 = (cl >> 6) * 16384 + row * 128 + (((q16) ^ sw) << 4);
+                const uint32_t off1 = (cl >> 6) * 16384 + row * 128 + (((q16 + 1) ^ sw) << 4);
+                if (n_res) {
+                    const uint4 r0 = *reinterpret_cast<const uint4 *>(resp + off0);
+                    const uint4 r1 = *reinterpret_cast<const uint4 *>(resp + off1);
                     const uint32_t rr[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
 #pragma unroll
                     for (int i = 0; i < 8; ++i) {
@@ -359,27 +391,55 @@ __global__ void __launch_bounds__(kConvThreads, 1)
                         f[2 * i + 1] += bf16_hi(rr[i]);
                     }
                 }
-                uint32_t o[8];
 #pragma unroll
-                for (int i = 0; i < 8; ++i) o[i] = pack_bf16(fmaxf(f[2 * i], 0.f), fmaxf(f[2 * i + 1], 0.f));
-                *p0 = make_uint4(o[0], o[1], o[2], o[3]);
-                *p1 = make_uint4(o[4], o[5], o[6], o[7]);
+                for (int i = 0; i < 16; ++i) f[i] = fmaxf(f[i], 0.f);
+                if (a.pool_out) {
+                    // rows of one image are P consecutive lanes (P | 32): butterfly over them
+#pragma unroll
+                    for (int i = 0; i < 16; ++i)
+                        for (int o = 1; o < P; o <<= 1) f[i] += __shfl_xor_sync(0xffffffffu, f[i], o);
+                    const int n = tc.n0 + row / P;
+                    if ((lane % P) == 0 && n < a.B) {
+                        const float inv = 1.f / static_cast<float>(P);
+                        float4 *dst = reinterpret_cast<float4 *>(a.pool_out + static_cast<size_t>(n) * a.c_out + cg);
+#pragma unroll
+                        for (int i = 0; i < 4; ++i)
+                            dst[i] = make_float4(f[4 * i] * inv, f[4 * i + 1] * inv, f[4 * i + 2] * inv, f[4 * i + 3] * inv);
+                    }
+                } else {
+                    uint32_t o[8];
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) o[i] = pack_bf16(f[2 * i], f[2 * i + 1]);
+                    *reinterpret_cast<uint4 *>(pOut + off0) = make_uint4(o[0], o[1], o[2], o[3]);
+                    *reinterpret_cast<uint4 *>(pOut + off1) = make_uint4(o[4], o[5], o[6], o[7]);
+                }
             }
             tc_fence_before();
             mbar_arrive(tempty_bar(as));     // TMEM accumulator may be overwritten
-            fence_proxy_async();             // generic smem writes -> visible to the TMA (async proxy)
-            named_bar_sync(1, 128);
-            if (leader) {
-                for (uint32_t j = 0; j < a.n_out_chunks; ++j)
-                    tma_store_4d(&tmOut, sOut + j * 16384u, tc.co0 + j * kChunk, 0, tc.h0, tc.n0);
-                bulk_commit();
+            if (n_res) {
+                mbar_arrive(rempty_bar(rs));  // residual slot may be refilled
+                if (++rs == n_res) {
+                    rs = 0;
+                    rphase ^= 1;
+                }
+            }
+            if (!a.pool_out) {
+                fence_proxy_async();          // generic smem writes -> visible to the TMA (async proxy)
+                named_bar_sync(1, 128);
+                if (leader && !(a.debug & 4)) {
+                    for (uint32_t j = 0; j < a.n_out_chunks; ++j)
+                        tma_store_4d(&tmOut, sOut + j * 16384u, tc.co0 + j * kChunk, 0, tc.h0, tc.n0);
+                    bulk_commit();
+                }
             }
             if (++as == a.acc_stages) {
                 as = 0;
                 aphase ^= 1;
             }
         }
+        if (tr && leader) tr[4] = gtimer();
         if (leader) bulk_wait0();
+        if (tr && leader) tr[5] = gtimer();
     }
 
     tc_fence_before();
@@ -389,13 +449,177 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(a.tmem_cols)
                      : "memory");
     }
+    if (tr && threadIdx.x == 0) tr[6] = gtimer();
 }
 
+// ============================================================================
+// Stem on tcgen05: conv3x3, c_img (=3) -> c0, + BN + ReLU.
+// K = 9*c_img = 27 is padded to 32 (two K=16 MMAs); the A operand (one im2col
+// row of 27 bf16 values per output pixel) is built in shared memory by the
+// 128 threads from a halo'd input tile (the 6-byte pixel stride of the raw
+// image is not TMA-addressable), B (the c0 x 27 weight slice) is staged once per
+// CTA.  Tile = 128 pixels (tile_rows full image rows); several CTAs per SM.
+// Epilogue as the conv kernel: TMEM -> fp32 BN/ReLU -> bf16 -> SW128 staging -> TMA store.
+constexpr int kStemThreads = 128;
+constexpr int kStemMaxHaloB = 6 * 32 * 4 * 2;   // (rows+2) x W x c_img bf16 bytes, rows*W = 128, W <= 32, c_img <= 4
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void *src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
+// Halo rows h0-1 .. h0+rows of image n (raw bf16, contiguous in NHWC) -> smem buffer;
+// rows outside the image are zero-filled.  16-byte cp.async, one commit group.
+__device__ __forceinline__ void stem_fetch_halo(const StemArgs &a, uint8_t *buf, int t) {
+    const int tiles_per_img = a.H / a.tile_rows;
+    const int n = t / tiles_per_img, h0 = (t - n * tiles_per_img) * a.tile_rows;
+    const int row_b = a.W * a.cimg * 2;                  // bytes per image row (multiple of 16)
+    const int per_row = row_b / 16;
+    const int total = (a.tile_rows + 2) * per_row;
+    for (int i = threadIdx.x; i < total; i += kStemThreads) {
+        const int r = i / per_row, j = i - r * per_row;
+        const int ih = h0 - 1 + r;
+        uint8_t *dst = buf + r * row_b + j * 16;
+        if (ih >= 0 && ih < a.H)
+            cp_async16(smem_u32(dst), reinterpret_cast<const uint8_t *>(a.in) +
+                                          (static_cast<size_t>(n) * a.H + ih) * row_b + j * 16);
+        else
+            *reinterpret_cast<uint4 *>(dst) = make_uint4(0, 0, 0, 0);
+    }
+    cp_async_commit();
+}
+
+__global__ void __launch_bounds__(kStemThreads)
+    stem_umma_kernel(const __grid_constant__ CUtensorMap tmOut, const StemArgs a) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t *sA = smem;                 // 128 rows x 128 B (SW128), K in [0,32) used
+    uint8_t *sB = smem + 16384;         // c0 rows x 128 B (SW128)
+    uint8_t *sOut = sB + 8192;          // 128 rows x 128 B staging (SW128)
+    uint8_t *sIn = sOut + 16384;        // 2 x halo buffers (raw bf16)
+    float *sBN = reinterpret_cast<float *>(sIn + 2 * kStemMaxHaloB);   // scale[64] | shift[64]
+    uint64_t *bar = reinterpret_cast<uint64_t *>(sBN + 128);
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bar + 1);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int cimg = a.cimg, K = 9 * cimg, W = a.W;
+
+    // zero A and B once (K padding 27..63 stays zero), stage the weight slice as bf16 and the BN vectors
+    for (int i = tid; i < (16384 + 8192) / 16; i += kStemThreads) reinterpret_cast<uint4 *>(sA)[i] = make_uint4(0, 0, 0, 0);
+    __syncthreads();
+    for (int i = tid; i < a.c0 * K; i += kStemThreads) {
+        const int co = i / K, k = i - co * K;
+        const int chunk = k >> 3, swz = (chunk ^ (co & 7)) << 4;
+        *reinterpret_cast<__nv_bfloat16 *>(sB + co * 128 + swz + (k & 7) * 2) =
+            __float2bfloat16_rn(a.w[static_cast<size_t>(co) * a.w_stride + k]);
+    }
+    for (int i = tid; i < a.c0; i += kStemThreads) {
+        sBN[i] = a.scale[i];
+        sBN[64 + i] = a.shift[i];
+    }
+    if (tid == 0) {
+        mbar_init(smem_u32(bar), 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(a.tmem_cols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("griddepcontrol.wait;" ::: "memory");          // PDL: inputs of the previous kernel are visible
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    fence_proxy_async();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const uint32_t idesc = umma_idesc_bf16(kTileM, a.c0);
+    const int q = warp & 3, row = q * 32 + lane, sw = row & 7;
+    const int r_pix = row / W, c_pix = row - r_pix * W;
+    uint32_t phase = 0;
+    int buf = 0;
+    const int tiles_per_img = a.H / a.tile_rows;
+    if (static_cast<int>(blockIdx.x) < a.m_tiles) stem_fetch_halo(a, sIn, blockIdx.x);
+    for (int t = blockIdx.x; t < a.m_tiles; t += gridDim.x) {
+        const int n = t / tiles_per_img, h0 = (t - n * tiles_per_img) * a.tile_rows;
+        // prefetch the next tile's halo into the other buffer, then wait for this one
+        const int tn = t + gridDim.x;
+        if (tn < a.m_tiles) stem_fetch_halo(a, sIn + (buf ^ 1) * kStemMaxHaloB, tn);
+        else cp_async_commit();
+        cp_async_wait1();
+        if (tid == 0) bulk_wait_read0();       // previous tile's TMA store has read the staging buffer
+        __syncthreads();
+        {   // im2col row of pixel `row`: k = (kh*3 + kw)*cimg + ci; zero padding in W by predicate
+            const __nv_bfloat16 *hb = reinterpret_cast<const __nv_bfloat16 *>(sIn + buf * kStemMaxHaloB);
+            uint32_t packed[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) packed[j] = 0;
+            for (int k = 0; k < K; ++k) {
+                const int tap = k / cimg, ci = k - tap * cimg, kh = tap / 3, kw = tap - kh * 3;
+                const int col = c_pix + kw - 1;
+                const uint32_t b = (col >= 0 && col < W)
+                                       ? static_cast<uint32_t>(__bfloat16_as_ushort(hb[((r_pix + kh) * W + col) * cimg + ci]))
+                                       : 0u;
+                packed[k >> 1] |= (k & 1) ? (b << 16) : b;
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j)   // 16-byte chunks 0..3 hold K = 0..31
+                *reinterpret_cast<uint4 *>(sA + row * 128 + ((j ^ sw) << 4)) =
+                    make_uint4(packed[4 * j], packed[4 * j + 1], packed[4 * j + 2], packed[4 * j + 3]);
+        }
+        buf ^= 1;
+        fence_proxy_async();                   // generic smem writes -> visible to the tensor core
+        tc_fence_before();
+        __syncthreads();
+        if (tid == 0) {
+            tc_fence_after();
+            const uint64_t ad = umma_desc_sw128(smem_u32(sA)), bd = umma_desc_sw128(smem_u32(sB));
+            umma_bf16(tmem, ad, bd, idesc, 0);
+            umma_bf16(tmem, ad + 2, bd + 2, idesc, 1);
+            umma_commit(smem_u32(bar));
+        }
+        mbar_wait(smem_u32(bar), phase);
+        phase ^= 1;
+        tc_fence_after();
+        const uint32_t lane_addr = tmem + (static_cast<uint32_t>(q * 32) << 16);
+        for (int g = 0; g < a.c0 / 16; ++g) {
+            uint32_t v[16];
+            tmem_ld16(lane_addr + g * 16, v);
+            tmem_wait_ld();
+            float f[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) f[i] = fmaxf(fmaf(__uint_as_float(v[i]), sBN[g * 16 + i], sBN[64 + g * 16 + i]), 0.f);
+            const int q16 = (g * 16) >> 3;
+            uint8_t *rowp = sOut + row * 128;
+            *reinterpret_cast<uint4 *>(rowp + (((q16) ^ sw) << 4)) =
+                make_uint4(pack_bf16(f[0], f[1]), pack_bf16(f[2], f[3]), pack_bf16(f[4], f[5]), pack_bf16(f[6], f[7]));
+            *reinterpret_cast<uint4 *>(rowp + (((q16 + 1) ^ sw) << 4)) =
+                make_uint4(pack_bf16(f[8], f[9]), pack_bf16(f[10], f[11]), pack_bf16(f[12], f[13]), pack_bf16(f[14], f[15]));
+        }
+        fence_proxy_async();
+        tc_fence_before();
+        __syncthreads();
+        if (tid == 0) {
+            tma_store_4d(&tmOut, smem_u32(sOut), 0, 0, h0, n);
+            bulk_commit();
+        }
+    }
+    if (tid == 0) bulk_wait0();
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(a.tmem_cols) : "memory");
+    }
+}
 }  // namespace
 
 size_t conv_umma_smem_bytes(const ConvArgs &a) {
+    const size_t chunk = static_cast<size_t>(a.n_out_chunks) * 16384;
+    const int n_res = (a.epi == EPI_BN_ADD_RELU) ? a.res_slots : 0;
     return 1024 /*alignment slack*/ + static_cast<size_t>(a.n_stages) * (kTileABytes + a.stage_b_bytes) +
-           static_cast<size_t>(a.n_out_chunks) * 16384 + 8 * (2 * kMaxStages + 5) + 16;
+           chunk * (1 + n_res) + 16 * static_cast<size_t>(a.c_out) + 8 * (2 * a.n_stages + 8) + 16;
 }
 
 int conv_umma_max_ctas_per_sm(size_t smem_bytes) {
@@ -407,6 +631,7 @@ int conv_umma_max_ctas_per_sm(size_t smem_bytes) {
     if (it != cache.end()) return it->second;
     int n = 0;
     cudaFuncSetAttribute(conv_umma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(conv_umma_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, conv_umma_kernel, kConvThreads, smem_bytes) != cudaSuccess) {
         cudaGetLastError();
         n = 1;
@@ -418,16 +643,62 @@ int conv_umma_max_ctas_per_sm(size_t smem_bytes) {
 
 cudaError_t launch_conv_umma(const ConvArgs &a, const CUtensorMap &tmA0, const CUtensorMap &tmB0,
                              const CUtensorMap &tmA1, const CUtensorMap &tmB1, const CUtensorMap &tmRes,
-                             const CUtensorMap &tmOut, int grid, cudaStream_t stream) {
-    const size_t smem = conv_umma_smem_bytes(a);
+                             const CUtensorMap &tmOut, int grid, cudaStream_t stream, bool pdl) {
     static bool attr_set = false;
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(conv_umma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
-    conv_umma_kernel<<<grid, kConvThreads, smem, stream>>>(tmA0, tmB0, tmA1, tmB1, tmRes, tmOut, a);
-    return cudaGetLastError();
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kConvThreads);
+    cfg.dynamicSmemBytes = conv_umma_smem_bytes(a);
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, conv_umma_kernel, tmA0, tmB0, tmA1, tmB1, tmRes, tmOut, a);
+}
+
+size_t stem_umma_smem_bytes() { return 1024 + 16384 + 8192 + 16384 + 2 * kStemMaxHaloB + 128 * 4 + 16; }
+
+cudaError_t launch_stem_umma(const StemArgs &a, const CUtensorMap &tmOut, int grid, cudaStream_t stream, bool pdl) {
+    const size_t smem = stem_umma_smem_bytes();
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kStemThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, stem_umma_kernel, tmOut, a);
+}
+
+int stem_umma_max_ctas_per_sm() {
+    static int n = -1;
+    if (n < 0) {
+        int v = 0;
+        cudaFuncSetAttribute(stem_umma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+        // the occupancy API otherwise assumes the smallest shared-memory carveout that fits one CTA
+        cudaFuncSetAttribute(stem_umma_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, stem_umma_kernel, kStemThreads,
+                                                                      stem_umma_smem_bytes());
+        if (getenv("SLIM_DEBUG"))
+            fprintf(stderr, "[slim] stem occupancy: %d CTAs/SM (%s), smem %zu\n", v, cudaGetErrorString(e),
+                    stem_umma_smem_bytes());
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            v = 1;
+        }
+        n = v < 1 ? 1 : (v > 6 ? 6 : v);
+    }
+    return n;
 }
 
 }  // namespace slim

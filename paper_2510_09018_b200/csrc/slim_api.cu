@@ -11,6 +11,7 @@
 #include <cstdarg>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -38,8 +39,8 @@ struct DevLayer {
     void *w = nullptr;                       // full-width KRSC, bf16 (BF16 mode) or fp32; stem: fp32
     float *scale[kMaxW] = {};                // folded BN per width, length c(width, cout)
     float *shift[kMaxW] = {};
-    CUtensorMap tm[kMaxW][kMaxW];            // weight tensor map per (r_prev idx, r idx)
-    bool tm_ok[kMaxW][kMaxW] = {};
+    CUtensorMap tm[kMaxW][kMaxW][17];        // weight tensor map per (r_prev idx, r idx, n_tile/16)
+    bool tm_ok[kMaxW][kMaxW][17] = {};
 };
 
 struct DevSegment {
@@ -73,9 +74,11 @@ struct slim_ctx {
         uint64_t n_kernels;
     };
     bool graph_mode = false;
+    bool pdl = true;   // programmatic dependent launch between consecutive kernels (off while profiling)
     cudaStream_t cap_stream = nullptr;
     std::mutex graph_mu;
     std::unordered_map<std::string, GraphEntry> graphs;
+    unsigned long long *trace = nullptr;   // diagnostics: SLIM_CONV_TRACE -> per-CTA timestamps of the last conv
 };
 
 extern "C" int slim_channels(float r, int C) {
@@ -221,19 +224,36 @@ bool encode_w(slim_ctx *ctx, CUtensorMap *tm, const DevLayer &L, int c_in, int c
     return encode_map(ctx, tm, L.w, 3, dims, strides, box, est);
 }
 
-int pick_n_tile(int c_out) {
-    int nt = (c_out + 255) / 256;
-    while (c_out % nt || (c_out / nt) % 16) ++nt;
-    return c_out / nt;
+// N per CTA tile: the widest divisor of c_out that is a multiple of 16 and <= 256
+// (the UMMA N limit), narrowed down to 64 while the grid would leave most SMs idle
+// (small-M layers late in the network, SURVEY §7 "hard parts" #3).  When there are
+// several N tiles each must be a multiple of 64 channels.
+int pick_n_tile(int c_out, int m_tiles = 1 << 30, int num_sms = 148) {
+    int best = 0;
+    for (int nt = 1; nt <= c_out / 16; ++nt) {
+        if (c_out % nt || (c_out / nt) % 16) continue;
+        const int n = c_out / nt;
+        // several N tiles must each cover whole 64-channel staging chunks: the output
+        // TMA box is 64 channels wide and would spill into the neighbour tile otherwise
+        if (nt > 1 && n % 64) continue;
+        if (n > 256) continue;
+        if (best == 0) best = n;   // widest legal tile
+        if (static_cast<long>(m_tiles) * nt * 10 >= static_cast<long>(num_sms) * 8 || n <= 64) {
+            best = n;
+            break;
+        }
+        best = n;
+    }
+    return best;
 }
 
-const CUtensorMap *weight_map(slim_ctx *ctx, DevLayer &L, int ri_in, int ri, int c_in, int c_out) {
+const CUtensorMap *weight_map(slim_ctx *ctx, DevLayer &L, int ri_in, int ri, int c_in, int c_out, int n_tile) {
     std::lock_guard<std::mutex> g(ctx->mu);
-    if (!L.tm_ok[ri_in][ri]) {
-        if (!encode_w(ctx, &L.tm[ri_in][ri], L, c_in, c_out, pick_n_tile(c_out))) return nullptr;
-        L.tm_ok[ri_in][ri] = true;
+    if (!L.tm_ok[ri_in][ri][n_tile >> 4]) {
+        if (!encode_w(ctx, &L.tm[ri_in][ri][n_tile >> 4], L, c_in, c_out, n_tile)) return nullptr;
+        L.tm_ok[ri_in][ri][n_tile >> 4] = true;
     }
-    return &L.tm[ri_in][ri];
+    return &L.tm[ri_in][ri][n_tile >> 4];
 }
 
 // One conv launch of a BasicBlock: out = epi(conv(x; L) [+ proj(xp; Lp)] [+ res]).
@@ -249,6 +269,7 @@ struct ConvCall {
     int Hp = 0, Wp = 0, c_in_p = 0;
     const void *res = nullptr;               // identity residual (EPI_BN_ADD_RELU)
     void *out = nullptr;
+    float *pool_out = nullptr;               // fused global average pool (fp32 [B][c_out]) instead of `out`
     int epi = EPI_BN_RELU;
 };
 
@@ -296,7 +317,7 @@ slim_status conv_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, int ri
         a.tiles_per_img = 1;
         a.m_tiles = (B + a.tile_imgs - 1) / a.tile_imgs;
     }
-    a.n_tile = pick_n_tile(c_out);
+    a.n_tile = pick_n_tile(c_out, a.m_tiles, ctx->num_sms);
     a.n_tiles = c_out / a.n_tile;
     a.c_out = c_out;
     a.n_parts = (cc.epi == EPI_BN_PROJ_RELU) ? 2 : 1;
@@ -313,6 +334,9 @@ slim_status conv_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, int ri
         a.scale1 = cc.Lp->scale[ri];
         a.shift1 = cc.Lp->shift[ri];
     }
+    static const int conv_debug = getenv("SLIM_CONV_DEBUG") ? atoi(getenv("SLIM_CONV_DEBUG")) : 0;
+    a.debug = conv_debug;
+    a.trace = ctx->trace;   // diagnostics only
     a.acc_stride = (a.n_tile + 31) / 32 * 32;
     a.acc_stages = 512 / (a.n_parts * a.acc_stride) >= 2 ? 2 : 1;
     int cols = a.acc_stages * a.n_parts * a.acc_stride, tc = 32;
@@ -320,18 +344,24 @@ slim_status conv_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, int ri
     a.tmem_cols = tc;
     a.stage_b_bytes = static_cast<uint32_t>(a.n_tile) * 128;
     a.n_out_chunks = static_cast<uint32_t>((a.n_tile + kChunk - 1) / kChunk);
-    // pipeline depth: two CTAs per SM for narrow tiles (more latency hiding on the
-    // HBM-bound layers), one for wide tiles; 2..8 stages in what remains.
-    const bool two = a.n_tile <= 64;
+    a.res_slots = a.n_out_chunks <= 2 ? 2 : 1;
+    a.pool_out = cc.pool_out;
+    if (a.pool_out && (P > 32 || 32 % P || (a.tile_imgs == 1 && P != kTileM)))
+        return fail(ctx, SLIM_EUNSUPPORTED, "fused pool needs Ho*Wo dividing 32");
+    // pipeline depth: two CTAs per SM for very narrow tiles, one otherwise; 2..8 stages
+    // in what the staging / residual ring / BN vectors leave
+    const bool two = a.n_tile <= 32;
     const size_t budget = two ? 113 * 1024 : 226 * 1024;
-    const size_t fixed = 1024 + a.n_out_chunks * 16384 + 8 * (2 * kMaxStages + 5) + 16;
+    const size_t chunk = static_cast<size_t>(a.n_out_chunks) * 16384;
+    const size_t fixed = 1024 + chunk * (1 + (cc.epi == EPI_BN_ADD_RELU ? a.res_slots : 0)) +
+                         16 * static_cast<size_t>(c_out) + 8 * (2 * kMaxStages + 8) + 16;
     int stages = static_cast<int>((budget - fixed) / (kTileABytes + a.stage_b_bytes));
     a.n_stages = stages < 2 ? 2 : (stages > kMaxStages ? kMaxStages : stages);
 
     CUtensorMap tA0, tA1, tRes, tOut;
     if (!encode_act(ctx, &tA0, cc.x, B, cc.H, cc.W, cc.c_in, s * Wo, s * a.tile_rows, a.tile_imgs, s))
         return fail(ctx, SLIM_ECUDA, "cuTensorMapEncodeTiled(A) failed");
-    const CUtensorMap *tB0 = weight_map(ctx, L, cc.ri_in, ri, cc.c_in, c_out);
+    const CUtensorMap *tB0 = weight_map(ctx, L, cc.ri_in, ri, cc.c_in, c_out, a.n_tile);
     const CUtensorMap *tB1 = tB0;
     if (!tB0) return fail(ctx, SLIM_ECUDA, "cuTensorMapEncodeTiled(W) failed");
     tA1 = tA0;
@@ -339,10 +369,10 @@ slim_status conv_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, int ri
         const int sp = cc.Lp->sh.stride;
         if (!encode_act(ctx, &tA1, cc.xp, B, cc.Hp, cc.Wp, cc.c_in_p, sp * Wo, sp * a.tile_rows, a.tile_imgs, sp))
             return fail(ctx, SLIM_ECUDA, "cuTensorMapEncodeTiled(A1) failed");
-        tB1 = weight_map(ctx, *cc.Lp, cc.ri_in_p, ri, cc.c_in_p, c_out);
+        tB1 = weight_map(ctx, *cc.Lp, cc.ri_in_p, ri, cc.c_in_p, c_out, a.n_tile);
         if (!tB1) return fail(ctx, SLIM_ECUDA, "cuTensorMapEncodeTiled(W1) failed");
     }
-    if (!encode_act(ctx, &tOut, cc.out, B, Ho, Wo, c_out, Wo, a.tile_rows, a.tile_imgs, 1))
+    if (!encode_act(ctx, &tOut, cc.pool_out ? cc.x : cc.out, B, Ho, Wo, c_out, Wo, a.tile_rows, a.tile_imgs, 1))
         return fail(ctx, SLIM_ECUDA, "cuTensorMapEncodeTiled(out) failed");
     tRes = tOut;
     if (cc.epi == EPI_BN_ADD_RELU &&
@@ -357,9 +387,11 @@ slim_status conv_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, int ri
     double flops, bytes;
     conv_work(c, cc, ri, B, Ho, Wo, &flops, &bytes);
     LaunchProf prof(ctx, st);
-    cudaError_t e = launch_conv_umma(a, tA0, *tB0, tA1, *tB1, tRes, tOut, grid, st);
+    cudaError_t e = launch_conv_umma(a, tA0, *tB0, tA1, *tB1, tRes, tOut, grid, st, ctx->pdl && !ctx->prof_on);
     prof.done(SLIM_K_CONV_UMMA, cc.seg, cc.layer, c.widths[cc.ri_in], c.widths[ri], B, flops, bytes);
-    if (e != cudaSuccess) return fail(ctx, SLIM_ECUDA, "conv_umma launch: %s", cudaGetErrorString(e));
+    if (e != cudaSuccess)
+        return fail(ctx, SLIM_ECUDA, "conv_umma launch (grid %d, smem %zu, n_tile %d, stages %d): %s", grid, smem,
+                    a.n_tile, a.n_stages, cudaGetErrorString(e));
     return SLIM_OK;
 }
 
@@ -454,14 +486,37 @@ slim_status run_segment(slim_ctx *ctx, int seg, int ri_prev, int ri, int B, cons
         const double pix = static_cast<double>(B) * H * H;
         const double flops = 2.0 * pix * C * 9 * c.in_channels;
         const double bytes = eb * pix * (c.in_channels + C) + 4.0 * C * 9 * c.in_channels + 8.0 * C;
-        LaunchProf prof(ctx, st);
-        cudaError_t e = bf ? launch_stem_bf16(static_cast<const uint16_t *>(in), static_cast<const float *>(Ls.w),
-                                              Ls.sh.cin, Ls.scale[ri], Ls.shift[ri], reinterpret_cast<uint16_t *>(bufs[0]),
-                                              B, H, H, c.in_channels, C, st)
-                           : launch_stem_f32(static_cast<const float *>(in), static_cast<const float *>(Ls.w),
-                                             Ls.sh.cin, Ls.scale[ri], Ls.shift[ri], reinterpret_cast<float *>(bufs[0]),
-                                             B, H, H, c.in_channels, C, st);
-        prof.done(SLIM_K_STEM, 0, 0, r, r, B, flops, bytes);
+        cudaError_t e;
+        if (bf) {
+            StemArgs sa{};
+            sa.in = static_cast<const uint16_t *>(in);
+            sa.w = static_cast<const float *>(Ls.w);
+            sa.w_stride = 9 * Ls.sh.cin;
+            sa.scale = Ls.scale[ri];
+            sa.shift = Ls.shift[ri];
+            sa.B = B;
+            sa.H = H;
+            sa.W = H;
+            sa.cimg = c.in_channels;
+            sa.c0 = C;
+            sa.tile_rows = kTileM / H;
+            sa.m_tiles = B * (H / sa.tile_rows);
+            sa.tmem_cols = C <= 32 ? 32 : 64;
+            CUtensorMap tOut;
+            if (!encode_act(ctx, &tOut, bufs[0], B, H, H, C, H, sa.tile_rows, 1, 1))
+                return fail(ctx, SLIM_ECUDA, "cuTensorMapEncodeTiled(stem out) failed");
+            int grid = ctx->num_sms * stem_umma_max_ctas_per_sm();
+            if (grid > sa.m_tiles) grid = sa.m_tiles;
+            LaunchProf prof(ctx, st);
+            e = launch_stem_umma(sa, tOut, grid, st, ctx->pdl && !ctx->prof_on);
+            prof.done(SLIM_K_STEM, 0, 0, r, r, B, flops, bytes);
+        } else {
+            LaunchProf prof(ctx, st);
+            e = launch_stem_f32(static_cast<const float *>(in), static_cast<const float *>(Ls.w), Ls.sh.cin,
+                                Ls.scale[ri], Ls.shift[ri], reinterpret_cast<float *>(bufs[0]), B, H, H,
+                                c.in_channels, C, st);
+            prof.done(SLIM_K_STEM, 0, 0, r, r, B, flops, bytes);
+        }
         if (e != cudaSuccess) return fail(ctx, SLIM_ECUDA, "stem launch: %s", cudaGetErrorString(e));
         cur = bufs[0];
         curH = H;
@@ -489,6 +544,9 @@ slim_status run_segment(slim_ctx *ctx, int seg, int ri_prev, int ri, int B, cons
         c1.c_in = curC;
         c1.out = T;
         c1.epi = EPI_BN_RELU;
+        // the network's last conv pools in its epilogue (BF16 mode): the segment-3 output
+        // never goes to memory; the head is then the FC alone
+        const bool fuse_pool = bf && seg == 3 && b == nb - 1 && H * H <= 32 && 32 % (H * H) == 0;
         ConvCall c2;   // out = relu(BN2(conv3x3(t)) + shortcut)
         c2.seg = seg;
         c2.layer = bi.c2;
@@ -498,6 +556,7 @@ slim_status run_segment(slim_ctx *ctx, int seg, int ri_prev, int ri, int B, cons
         c2.H = c2.W = H;
         c2.c_in = C;
         c2.out = dst;
+        if (fuse_pool) c2.pool_out = reinterpret_cast<float *>(dst);
         if (down) {
             c2.epi = EPI_BN_PROJ_RELU;
             c2.Lp = &S.L[bi.sc];
@@ -520,14 +579,19 @@ slim_status run_segment(slim_ctx *ctx, int seg, int ri_prev, int ri, int B, cons
     }
     if (seg == 3) {
         const double K = c.num_classes;
-        const double flops = 2.0 * B * C * K + static_cast<double>(B) * H * H * C;
-        const double bytes = eb * B * H * H * C + 4.0 * K * (C + 1) + 4.0 * B * K;
+        const bool pooled = bf && H * H <= 32 && 32 % (H * H) == 0;   // see fuse_pool above
+        const double flops = 2.0 * B * C * K + (pooled ? 0.0 : static_cast<double>(B) * H * H * C);
+        const double bytes = (pooled ? 4.0 * B * C : eb * B * H * H * C) + 4.0 * K * (C + 1) + 4.0 * B * K;
         LaunchProf prof(ctx, st);
-        cudaError_t e = bf ? launch_head_bf16(static_cast<const uint16_t *>(cur), S.fc_w, S.fc_b,
-                                              static_cast<float *>(out), B, H * H, C, c.base_channels[3],
-                                              c.num_classes, st)
-                           : launch_head_f32(static_cast<const float *>(cur), S.fc_w, S.fc_b, static_cast<float *>(out),
-                                             B, H * H, C, c.base_channels[3], c.num_classes, st);
+        const bool pdl = ctx->pdl && !ctx->prof_on;
+        cudaError_t e = pooled ? launch_fc_f32(static_cast<const float *>(cur), S.fc_w, S.fc_b, static_cast<float *>(out),
+                                               B, C, c.base_channels[3], c.num_classes, st, pdl)
+                        : bf ? launch_head_bf16(static_cast<const uint16_t *>(cur), S.fc_w, S.fc_b,
+                                                static_cast<float *>(out), B, H * H, C, c.base_channels[3],
+                                                c.num_classes, st, pdl)
+                             : launch_head_f32(static_cast<const float *>(cur), S.fc_w, S.fc_b,
+                                               static_cast<float *>(out), B, H * H, C, c.base_channels[3],
+                                               c.num_classes, st, pdl);
         prof.done(SLIM_K_HEAD, 3, -1, r, r, B, flops, bytes);
         if (e != cudaSuccess) return fail(ctx, SLIM_ECUDA, "head launch: %s", cudaGetErrorString(e));
     }
@@ -642,6 +706,8 @@ slim_status slim_create(int device, const slim_config *cfg, slim_ctx **out) {
         !(c.bn_eps > 0.f) || (c.dtype != SLIM_BF16 && c.dtype != SLIM_FP32))
         return SLIM_EINVAL;
     if (c.image_hw < 16 || c.image_hw % 8) return SLIM_EUNSUPPORTED;
+    // BF16 stem/conv tiling: a 128-pixel tile is whole image rows and the stem's halo rows are 16-B multiples
+    if (c.dtype == SLIM_BF16 && (c.image_hw > 32 || (c.image_hw * c.in_channels) % 8)) return SLIM_EUNSUPPORTED;
     for (int s = 0; s < 4; ++s) {
         if (c.blocks_per_seg[s] < 1 || c.blocks_per_seg[s] > 4) return SLIM_EINVAL;
         if (c.base_channels[s] < 16 || c.base_channels[s] > 1024) return SLIM_EINVAL;
@@ -678,6 +744,7 @@ slim_status slim_create(int device, const slim_config *cfg, slim_ctx **out) {
         return SLIM_ENOMEM;
     }
     ctx->ws_bytes = ws;
+    if (getenv("SLIM_CONV_TRACE")) cudaMalloc(&ctx->trace, 4096 * 8 * sizeof(unsigned long long));
     if (cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking) != cudaSuccess) {
         cudaFree(ctx->ws);
         delete ctx;
@@ -989,5 +1056,11 @@ slim_status slim_last_error(slim_ctx *ctx) {
 const char *slim_last_error_msg(const slim_ctx *ctx) { return ctx ? ctx->msg.c_str() : "no context"; }
 uint64_t slim_launch_count(const slim_ctx *ctx) { return ctx ? ctx->launches.load() : 0; }
 int slim_num_sms(const slim_ctx *ctx) { return ctx ? ctx->num_sms : 0; }
+// diagnostics (not in slim.h): copy the per-CTA timestamps of the last traced conv launch
+SLIM_API int slimdbg_trace(slim_ctx *ctx, unsigned long long *host, int n) {
+    if (!ctx || !ctx->trace) return -1;
+    cudaDeviceSynchronize();
+    return cudaMemcpy(host, ctx->trace, sizeof(unsigned long long) * n, cudaMemcpyDeviceToHost) == cudaSuccess ? 0 : -1;
+}
 
 }  // extern "C"

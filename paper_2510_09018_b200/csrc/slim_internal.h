@@ -42,20 +42,41 @@ struct ConvArgs {
     int n_stages, acc_stages, acc_stride, tmem_cols;
     uint32_t stage_b_bytes;   // n_tile * 128
     uint32_t n_out_chunks;    // ceil(n_tile / 64) staging buffers of 16 KiB
+    int res_slots;            // residual prefetch ring depth (EPI_BN_ADD_RELU), 1 or 2
+    // fused global-average-pool (last conv of the network): instead of storing the
+    // [B,Ho,Wo,c_out] tile, average each image's Ho*Wo rows and write fp32 pooled[B][c_out]
+    float *pool_out;          // nullptr = normal store
+    int debug;                // diagnostics only (env SLIM_CONV_DEBUG): 1 = no TMA loads, 2 = no MMAs
+    unsigned long long *trace;   // diagnostics only (env SLIM_CONV_TRACE): per-CTA %globaltimer stamps
 };
 
 size_t conv_umma_smem_bytes(const ConvArgs &a);
 cudaError_t launch_conv_umma(const ConvArgs &a, const CUtensorMap &tmA0, const CUtensorMap &tmB0,
                              const CUtensorMap &tmA1, const CUtensorMap &tmB1, const CUtensorMap &tmRes,
-                             const CUtensorMap &tmOut, int grid, cudaStream_t stream);
+                             const CUtensorMap &tmOut, int grid, cudaStream_t stream, bool pdl);
 int conv_umma_max_ctas_per_sm(size_t smem_bytes);
+
+// stem (conv3x3 c_img -> c0 + BN + ReLU) on tcgen05, A built in smem (kernels_umma.cu)
+struct StemArgs {
+    const uint16_t *in;            // [B][H][W][cimg] bf16
+    const float *w;                // [c0_full][9*cimg] fp32 (bf16-representable), rows >= c0 unread
+    int w_stride;                  // 9*cimg_full
+    const float *scale, *shift;    // folded BN at this width, c0 entries
+    int B, H, W, cimg, c0;
+    int tile_rows, m_tiles, tmem_cols;
+};
+cudaError_t launch_stem_umma(const StemArgs &a, const CUtensorMap &tmOut, int grid, cudaStream_t stream, bool pdl);
+int stem_umma_max_ctas_per_sm();
 
 // ---- CUDA-core kernels (kernels_simt.cu) ------------------------------------
 cudaError_t launch_stem_bf16(const uint16_t *in, const float *w, int cin_full, const float *scale,
                              const float *shift, uint16_t *out, int B, int H, int W, int cimg, int c0,
                              cudaStream_t s);
 cudaError_t launch_head_bf16(const uint16_t *in, const float *fc_w, const float *fc_b, float *logits,
-                             int B, int P, int c3, int c3_full, int K, cudaStream_t s);
+                             int B, int P, int c3, int c3_full, int K, cudaStream_t s, bool pdl);
+// FC head on pooled fp32 features [B][c3] (pool fused into the last conv)
+cudaError_t launch_fc_f32(const float *pooled, const float *fc_w, const float *fc_b, float *logits, int B, int c3,
+                          int c3_full, int K, cudaStream_t s, bool pdl);
 // dst row i (row_bytes, multiple of 16) = src + idx[i]*src_stride (bytes)
 cudaError_t launch_gather(const void *src, size_t src_stride, const uint32_t *idx, int n, size_t row_bytes,
                           void *dst, cudaStream_t s);
@@ -76,6 +97,6 @@ cudaError_t launch_stem_f32(const float *in, const float *w, int cin_full, const
                             const float *shift, float *out, int B, int H, int W, int cimg, int c0,
                             cudaStream_t s);
 cudaError_t launch_head_f32(const float *in, const float *fc_w, const float *fc_b, float *logits,
-                            int B, int P, int c3, int c3_full, int K, cudaStream_t s);
+                            int B, int P, int c3, int c3_full, int K, cudaStream_t s, bool pdl);
 
 }  // namespace slim

@@ -34,7 +34,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_exports_are_exactly_the_abi():
     out = subprocess.check_output(["nm", "-D", "--defined-only", slim.LIB_PATH], text=True)
-    exported = sorted({l.split()[-1] for l in out.splitlines() if l.split()[-2] == "T" and "slim" in l.split()[-1]})
+    exported = sorted({l.split()[-1] for l in out.splitlines() if l.split()[-2] == "T" and l.split()[-1].startswith("slim_")})
     assert exported == _declared()
 
 
