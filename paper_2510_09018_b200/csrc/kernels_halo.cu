@@ -1,0 +1,417 @@
+// kernels_halo.cu -- stride-1 3x3 width-sliced conv on tcgen05 with ONE halo load per
+// channel chunk serving all nine filter taps ("kw-split accumulators").
+//
+// Same operation as conv_umma_kernel (kernels_umma.cu): out = relu(s*conv(x) + t [+ res]),
+// the first c_in / c_out channels of the full-width KRSC weights selected by TMA bounds.
+// Different data movement, because on B200 the per-tap design is bound by TMA
+// issue rate (~28-48 B/cycle/SM for one issuing thread, tools/ubench):
+//
+//   A: the tile is `rows` whole image rows (rows*W = 128 pixels); its input halo,
+//      rows h0-1 .. h0+rows (zero-filled outside the image by TMA), is ONE box
+//      [64 ch, W, rows+2, 1].  For tap row kh the UMMA A operand is the contiguous
+//      128-row window starting at halo row kh (a descriptor offset of kh*W*128 B).
+//   kw: instead of shifting A by one pixel (which breaks the 8-row core-matrix
+//      layout at row ends), each kw has its own TMEM accumulator
+//          acc_kw[h][w] = sum_kh x[h+kh-1][w] . W[kh][kw]
+//      and the epilogue forms out[h][w] = acc_0[h][w-1] + acc_1[h][w] + acc_2[h][w+1]
+//      with warp shuffles (W divides 32, so a pixel's W-neighbours are lanes +-1 of
+//      the same warp; zero at w = 0 / W-1 is the conv's zero padding).
+//   B: the 9 taps x n_tile x 64-channel weight block is one box [64, n_tile, 9]
+//      (weight-stationary: loaded once per CTA when all chunks fit in smem), else
+//      streamed per (chunk, kh) as [64, n_tile, 3].
+// Roles (384 threads): warp 0 = A producer, warp 1 = MMA issuer, warp 2 = B producer,
+// warp 3 = residual prefetch, warps 4..11 = epilogue (two warps per TMEM lane quarter).
+#include "slim_internal.h"
+#include "ptx_sm100.cuh"
+
+namespace slim {
+using namespace ptx;
+namespace {
+
+constexpr int kHaloThreads = 384;   // warps 0 A, 1 MMA, 2 B, 3 idle, 4..11 epilogue
+
+__global__ void __launch_bounds__(kHaloThreads, 1)
+    conv_halo_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                     const __grid_constant__ CUtensorMap tmRes, const __grid_constant__ CUtensorMap tmOut,
+                     const HaloArgs a) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const uint32_t chunk_bytes = a.n_out_chunks * 16384u;
+    const int n_res = (a.epi == EPI_BN_ADD_RELU) ? a.res_slots : 0;
+    const uint32_t sA = smem_u32(smem);
+    const uint32_t sB = sA + a.sa * a.a_bytes;
+    const uint32_t sOut = sB + a.sb * a.b_bytes;
+    const uint32_t sRes = sOut + chunk_bytes;
+    uint8_t *pOut = smem + (sOut - sA);
+    uint8_t *pRes = smem + (sRes - sA);
+    float *sBN = reinterpret_cast<float *>(pRes + n_res * chunk_bytes);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(sBN + 2 * a.c_out);
+    const uint32_t bar0 = smem_u32(bars);
+    // barriers: a_full[4] a_empty[4] b_full[4] b_empty[4] t_full[2] t_empty[2] r_full[2] r_empty[2]
+    auto a_full = [&](int i) { return bar0 + 8u * i; };
+    auto a_empty = [&](int i) { return bar0 + 8u * (4 + i); };
+    auto b_full = [&](int i) { return bar0 + 8u * (8 + i); };
+    auto b_empty = [&](int i) { return bar0 + 8u * (12 + i); };
+    auto t_full = [&](int i) { return bar0 + 8u * (16 + i); };
+    auto t_empty = [&](int i) { return bar0 + 8u * (18 + i); };
+    auto r_full = [&](int i) { return bar0 + 8u * (20 + i); };
+    auto r_empty = [&](int i) { return bar0 + 8u * (22 + i); };
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 24);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int total = a.m_tiles * a.n_tiles;
+    unsigned long long *tr = a.trace ? a.trace + blockIdx.x * 8 : nullptr;
+    unsigned long long *td = (a.trace && blockIdx.x == 0) ? a.trace + 2048 : nullptr;   // per-tile detail, CTA 0
+#define TD(role, tile, pt) \
+    if (td && (tile) < 64) td[(role) * 256 + (tile) * 4 + (pt)] = gtimer()
+    if (tr && threadIdx.x == 0) tr[0] = gtimer();
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < 4; ++i) {
+            mbar_init(a_full(i), 1);
+            mbar_init(a_empty(i), 1);
+            mbar_init(b_full(i), 1);
+            mbar_init(b_empty(i), 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(t_full(i), 1);
+            mbar_init(t_empty(i), kEpiThreads);
+            mbar_init(r_full(i), 1);
+            mbar_init(r_empty(i), kEpiThreads);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        prefetch_tmap(&tmA);
+        prefetch_tmap(&tmB);
+        prefetch_tmap(&tmOut);
+        if (n_res) prefetch_tmap(&tmRes);
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(a.tmem_cols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    for (int i = threadIdx.x; i < a.c_out; i += blockDim.x) {
+        sBN[i] = a.scale[i];
+        sBN[a.c_out + i] = a.shift[i];
+    }
+    // weight-stationary B does not depend on the previous kernel: start it before the PDL wait
+    __syncthreads();
+    if (a.stationary && warp == 2 && lane == 0) {
+        mbar_expect_tx(b_full(0), a.b_bytes);
+        const uint32_t per_chunk = 9u * a.n_tile * 128u;
+        for (int ch = 0; ch < a.n_chunks; ++ch) tma_load_3d(sB + ch * per_chunk, &tmB, b_full(0), ch * kChunk, 0, 0);
+    }
+    pdl_wait();
+    pdl_launch_dependents();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+    if (tr && threadIdx.x == 0) tr[1] = gtimer();
+    const int tiles_per_img = a.tiles_per_img;
+
+    if (warp == 0) {
+        // ===================== A producer ============================================
+        if (lane == 0) {
+            int s = 0;
+            uint32_t ph = 0;
+            for (int t = blockIdx.x; t < total; t += gridDim.x) {
+                const int mt = t % a.m_tiles;
+                const int n = mt / tiles_per_img, h0 = (mt - n * tiles_per_img) * a.rows;
+                const int ti = (t - blockIdx.x) / gridDim.x;
+                TD(0, ti, 0);
+                for (int ch = 0; ch < a.n_chunks; ++ch) {
+                    mbar_wait(a_empty(s), ph ^ 1);
+                    if (ch == 0) TD(0, ti, 2);
+                    mbar_expect_tx(a_full(s), a.a_bytes);
+                    tma_load_4d(sA + s * a.a_bytes, &tmA, a_full(s), ch * kChunk, 0, h0 - 1, n);
+                    if (++s == a.sa) {
+                        s = 0;
+                        ph ^= 1;
+                    }
+                }
+            }
+            if (tr) tr[2] = gtimer();
+        }
+    } else if (warp == 3) {
+        // ===================== residual prefetch (own warp: never gates the A ring) ===
+        if (lane == 0 && n_res) {
+            int rs = 0;
+            uint32_t rph = 0;
+            for (int t = blockIdx.x; t < total; t += gridDim.x) {
+                const int mt = t % a.m_tiles, nt = t / a.m_tiles;
+                const int n = mt / tiles_per_img, h0 = (mt - n * tiles_per_img) * a.rows, co0 = nt * a.n_tile;
+                const int ti = (t - blockIdx.x) / gridDim.x;
+                mbar_wait(r_empty(rs), rph ^ 1);
+                TD(0, ti, 1);
+                if (a.debug & 8) {
+                    mbar_arrive(r_full(rs));
+                } else {
+                    mbar_expect_tx(r_full(rs), chunk_bytes);
+                    for (uint32_t j = 0; j < a.n_out_chunks; ++j)
+                        tma_load_4d(sRes + rs * chunk_bytes + j * 16384u, &tmRes, r_full(rs), co0 + j * kChunk, 0, h0, n);
+                }
+                if (++rs == n_res) {
+                    rs = 0;
+                    rph ^= 1;
+                }
+            }
+        }
+    } else if (warp == 2) {
+        // ===================== B producer (streaming weights) ======================
+        if (lane == 0 && !a.stationary) {
+            int s = 0;
+            uint32_t ph = 0;
+            for (int t = blockIdx.x; t < total; t += gridDim.x) {
+                const int co0 = (t / a.m_tiles) * a.n_tile;
+                for (int ch = 0; ch < a.n_chunks; ++ch)
+                    for (int kh = 0; kh < 3; ++kh) {
+                        mbar_wait(b_empty(s), ph ^ 1);
+                        mbar_expect_tx(b_full(s), a.b_bytes);
+                        tma_load_3d(sB + s * a.b_bytes, &tmB, b_full(s), ch * kChunk, co0, kh * 3);
+                        if (++s == a.sb) {
+                            s = 0;
+                            ph ^= 1;
+                        }
+                    }
+            }
+        }
+    } else if (warp == 1) {
+        // ===================== MMA issuer ===========================================
+        // Lean issue loop: descriptors are base + offset adds (start-address field, 16-B
+        // units), the kh x kw x kk nest has constant trip counts and is fully unrolled --
+        // a single issuing thread is otherwise instruction-bound (~120 cycles per MMA,
+        // tools/ubench) instead of tensor/smem-bound (~48 cycles at N=64).
+        {   // the whole warp runs the loop (uniform operands); one elected lane issues
+            const uint32_t idesc = umma_idesc_bf16(kTileM, a.n_tile);
+            const uint32_t tap16 = static_cast<uint32_t>(a.n_tile) * 8u;      // n_tile*128 B in 16-B units
+            const uint32_t row16 = static_cast<uint32_t>(a.W) * 8u;           // one halo row (W pixels x 128 B)
+            const uint64_t adesc0 = umma_desc_sw128(sA), bdesc0 = umma_desc_sw128(sB);
+            const uint32_t a_slot16 = a.a_bytes >> 4, b_slot16 = a.b_bytes >> 4;
+            const uint32_t accs = static_cast<uint32_t>(a.acc_stride);
+            int s = 0, bs = 0, as = 0;
+            uint32_t ph = 0, bph = 0, aph = 0;
+            if (a.stationary) {
+                mbar_wait(b_full(0), 0);
+                tc_fence_after();
+            }
+            for (int t = blockIdx.x; t < total; t += gridDim.x) {
+                const int ti = (t - blockIdx.x) / gridDim.x;
+                if (lane == 0) TD(1, ti, 0);
+                mbar_wait(t_empty(as), aph ^ 1);
+                if (lane == 0) TD(1, ti, 1);
+                tc_fence_after();
+                const uint32_t acc = tmem_base + static_cast<uint32_t>(as * 3) * accs;
+                for (int ch = 0; ch < a.n_chunks; ++ch) {
+                    const int nk = min(4, (a.c_in - ch * kChunk + 15) >> 4);
+                    mbar_wait(a_full(s), ph);
+                    if (ch == 0 && lane == 0) TD(1, ti, 2);
+                    tc_fence_after();
+                    const uint64_t ad = adesc0 + s * a_slot16;
+                    if (ch == 0 && lane == 0) TD(3, ti, 0);
+                    if (a.stationary) {
+                        // one elected issue block for the whole chunk (27 or 36 MMAs, no waits inside)
+                        const uint64_t bch = bdesc0 + static_cast<uint32_t>(ch * 9) * tap16;
+                        if (elect_one() && !(a.debug & 2)) {
+                            if (nk == 4) {
+#pragma unroll
+                                for (int kh = 0; kh < 3; ++kh)
+#pragma unroll
+                                    for (int kw = 0; kw < 3; ++kw)
+#pragma unroll
+                                        for (int kk = 0; kk < 4; ++kk)
+                                            umma_bf16(acc + kw * accs, ad + kh * row16 + 2 * kk,
+                                                      bch + (kh * 3 + kw) * tap16 + 2 * kk, idesc, (ch | kh | kk) != 0);
+                            } else {
+#pragma unroll
+                                for (int kh = 0; kh < 3; ++kh)
+#pragma unroll
+                                    for (int kw = 0; kw < 3; ++kw)
+                                        for (int kk = 0; kk < nk; ++kk)
+                                            umma_bf16(acc + kw * accs, ad + kh * row16 + 2 * kk,
+                                                      bch + (kh * 3 + kw) * tap16 + 2 * kk, idesc, (ch | kh | kk) != 0);
+                            }
+                        }
+                        __syncwarp();
+                    } else {
+#pragma unroll
+                        for (int kh = 0; kh < 3; ++kh) {
+                            mbar_wait(b_full(bs), bph);
+                            tc_fence_after();
+                            const uint64_t bd = bdesc0 + bs * b_slot16;
+                            const uint64_t adk = ad + kh * row16;
+                            if (elect_one()) {
+                                if (!(a.debug & 2)) {
+#pragma unroll
+                                    for (int kw = 0; kw < 3; ++kw)
+#pragma unroll
+                                        for (int kk = 0; kk < 4; ++kk)
+                                            if (kk < nk)
+                                                umma_bf16(acc + kw * accs, adk + 2 * kk, bd + kw * tap16 + 2 * kk, idesc,
+                                                          (ch | kh | kk) != 0);
+                                }
+                                umma_commit(b_empty(bs));
+                            }
+                            __syncwarp();
+                            if (++bs == a.sb) {
+                                bs = 0;
+                                bph ^= 1;
+                            }
+                        }
+                    }
+                    if (ch == 0 && lane == 0) TD(3, ti, 1);
+                    if (elect_one()) umma_commit(a_empty(s));
+                    __syncwarp();
+                    if (ch == 0 && lane == 0) TD(3, ti, 2);
+                    if (++s == a.sa) {
+                        s = 0;
+                        ph ^= 1;
+                    }
+                }
+                if (elect_one()) umma_commit(t_full(as));
+                __syncwarp();
+                if (lane == 0) {
+                    TD(1, ti, 3);
+                    TD(3, ti, 3);
+                }
+                if (++as == a.acc_stages) {
+                    as = 0;
+                    aph ^= 1;
+                }
+            }
+            if (tr && lane == 0) tr[3] = gtimer();
+        }
+    } else if (warp >= kEpiWarp0) {
+        // ===================== epilogue (warps 4..11, two per TMEM lane quarter) ====
+        const int q = warp & 3;
+        const int half = (warp - kEpiWarp0) >> 2;
+        const int row = q * 32 + lane;
+        const int w = lane % a.W;                  // W divides 32: pixel column of this row
+        const bool leader = (warp == kEpiWarp0 && lane == 0);
+        const uint32_t lane_addr = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
+        const int sw = row & 7;
+        const float *s0 = sBN, *t0 = sBN + a.c_out;
+        int as = 0, rs = 0;
+        uint32_t aph = 0, rph = 0;
+        for (int t = blockIdx.x; t < total; t += gridDim.x) {
+            const int mt = t % a.m_tiles, nt = t / a.m_tiles;
+            const int n = mt / tiles_per_img, h0 = (mt - n * tiles_per_img) * a.rows, co0 = nt * a.n_tile;
+            const int ti = (t - blockIdx.x) / gridDim.x;
+            mbar_wait(t_full(as), aph);
+            if (leader) TD(2, ti, 0);
+            tc_fence_after();
+            if (leader) bulk_wait_read0();
+            if (leader) TD(2, ti, 1);
+            named_bar_sync(1, kEpiThreads);
+            if (n_res) mbar_wait(r_full(rs), rph);
+            if (leader) TD(2, ti, 2);
+            const uint8_t *resp = pRes + rs * chunk_bytes;
+            const uint32_t col0 = static_cast<uint32_t>(as * 3 * a.acc_stride);
+            for (int g = half; g < a.n_tile / 16 && !(a.debug & 16); g += 2) {
+                uint32_t v0[16], v1[16], v2[16];
+                tmem_ld16(lane_addr + col0 + g * 16, v0);
+                tmem_ld16(lane_addr + col0 + a.acc_stride + g * 16, v1);
+                tmem_ld16(lane_addr + col0 + 2 * a.acc_stride + g * 16, v2);
+                tmem_wait_ld();
+                const int cl = g * 16, cg = co0 + cl;
+                float f[16];
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    // out[w] = acc_0[w-1] + acc_1[w] + acc_2[w+1]  (zero padding at the row ends)
+                    const float left = __shfl_up_sync(0xffffffffu, __uint_as_float(v0[i]), 1);
+                    const float right = __shfl_down_sync(0xffffffffu, __uint_as_float(v2[i]), 1);
+                    float y = __uint_as_float(v1[i]);
+                    if (w > 0) y += left;
+                    if (w < a.W - 1) y += right;
+                    f[i] = fmaf(y, s0[cg + i], t0[cg + i]);
+                }
+                const int q16 = (cl & 63) >> 3;
+                const uint32_t off0 = (cl >> 6) * 16384 + row * 128 + (((q16) ^ sw) << 4);
+                const uint32_t off1 = (cl >> 6) * 16384 + row * 128 + (((q16 + 1) ^ sw) << 4);
+                if (n_res) {
+                    const uint4 r0 = *reinterpret_cast<const uint4 *>(resp + off0);
+                    const uint4 r1 = *reinterpret_cast<const uint4 *>(resp + off1);
+                    const uint32_t rr[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        f[2 * i] += bf16_lo(rr[i]);
+                        f[2 * i + 1] += bf16_hi(rr[i]);
+                    }
+                }
+                uint32_t o[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) o[i] = pack_bf16(fmaxf(f[2 * i], 0.f), fmaxf(f[2 * i + 1], 0.f));
+                *reinterpret_cast<uint4 *>(pOut + off0) = make_uint4(o[0], o[1], o[2], o[3]);
+                *reinterpret_cast<uint4 *>(pOut + off1) = make_uint4(o[4], o[5], o[6], o[7]);
+            }
+            tc_fence_before();
+            mbar_arrive(t_empty(as));
+            if (n_res) {
+                mbar_arrive(r_empty(rs));
+                if (++rs == n_res) {
+                    rs = 0;
+                    rph ^= 1;
+                }
+            }
+            fence_proxy_async();
+            named_bar_sync(1, kEpiThreads);
+            if (leader && !(a.debug & 4)) {
+                TD(2, ti, 3);
+                for (uint32_t j = 0; j < a.n_out_chunks; ++j)
+                    tma_store_4d(&tmOut, sOut + j * 16384u, co0 + j * kChunk, 0, h0, n);
+                bulk_commit();
+            }
+            if (++as == a.acc_stages) {
+                as = 0;
+                aph ^= 1;
+            }
+        }
+        if (tr && leader) tr[4] = gtimer();
+        if (leader) bulk_wait0();
+        if (tr && leader) tr[5] = gtimer();
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(a.tmem_cols)
+                     : "memory");
+    }
+    if (tr && threadIdx.x == 0) tr[6] = gtimer();
+}
+
+}  // namespace
+
+size_t conv_halo_smem_bytes(const HaloArgs &a) {
+    const size_t chunk = static_cast<size_t>(a.n_out_chunks) * 16384;
+    const int n_res = (a.epi == EPI_BN_ADD_RELU) ? a.res_slots : 0;
+    return 1024 + static_cast<size_t>(a.sa) * a.a_bytes + static_cast<size_t>(a.sb) * a.b_bytes + chunk * (1 + n_res) +
+           8 * static_cast<size_t>(a.c_out) + 8 * 24 + 16;
+}
+
+cudaError_t launch_conv_halo(const HaloArgs &a, const CUtensorMap &tmA, const CUtensorMap &tmB,
+                             const CUtensorMap &tmRes, const CUtensorMap &tmOut, int grid, cudaStream_t stream,
+                             bool pdl) {
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(conv_halo_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        if (e != cudaSuccess) return e;
+        cudaFuncSetAttribute(conv_halo_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        attr_set = true;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kHaloThreads);
+    cfg.dynamicSmemBytes = conv_halo_smem_bytes(a);
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, conv_halo_kernel, tmA, tmB, tmRes, tmOut, a);
+}
+
+}  // namespace slim

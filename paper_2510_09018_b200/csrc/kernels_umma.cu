@@ -25,6 +25,7 @@
 // epilogue (tcgen05.ld -> BN/residual/ReLU in fp32 -> bf16 -> swizzled smem ->
 // TMA store; the residual tile arrives by TMA into the same staging buffer).
 #include "slim_internal.h"
+#include "ptx_sm100.cuh"
 
 #include <cuda_bf16.h>
 
@@ -34,129 +35,8 @@
 #include <mutex>
 
 namespace slim {
+using namespace ptx;
 namespace {
-
-__device__ __forceinline__ unsigned long long gtimer() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    return t;
-}
-__device__ __forceinline__ uint32_t smem_u32(const void *p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-// ---- mbarrier ---------------------------------------------------------------
-__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
-}
-__device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
-    uint32_t ok;
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(ok)
-        : "r"(bar), "r"(parity)
-        : "memory");
-    return ok != 0;
-}
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-    while (!mbar_try_wait(bar, parity)) {
-    }
-}
-
-// ---- TMA ----------------------------------------------------------------------
-__device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap *tm, uint32_t bar, int c0, int c1,
-                                            int c2, int c3) {
-    asm volatile(
-        "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(dst),
-        "l"(reinterpret_cast<uint64_t>(tm)), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
-        : "memory");
-}
-__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap *tm, uint32_t bar, int c0, int c1,
-                                            int c2) {
-    asm volatile(
-        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(dst),
-        "l"(reinterpret_cast<uint64_t>(tm)), "r"(bar), "r"(c0), "r"(c1), "r"(c2)
-        : "memory");
-}
-__device__ __forceinline__ void tma_store_4d(const CUtensorMap *tm, uint32_t src, int c0, int c1, int c2, int c3) {
-    asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.tile.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(
-                     reinterpret_cast<uint64_t>(tm)),
-                 "r"(src), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
-                 : "memory");
-}
-__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
-__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-__device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t n) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
-__device__ __forceinline__ void prefetch_tmap(const CUtensorMap *tm) {
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(tm)) : "memory");
-}
-
-// ---- tcgen05 ------------------------------------------------------------------
-__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-
-// Shared-memory matrix descriptor, K-major, 128-byte swizzle (SM100 "version 1"):
-// start>>4 [0,14), LBO>>4 [16,30) (=1, unused for swizzled K-major), SBO>>4 [32,46)
-// (= 1024 B between 8-row core-matrix groups), version [46,48) = 1, layout [61,64) = 2.
-__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
-    uint64_t d = 0;
-    d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
-    d |= static_cast<uint64_t>(1) << 16;
-    d |= static_cast<uint64_t>(1024 >> 4) << 32;
-    d |= static_cast<uint64_t>(1) << 46;
-    d |= static_cast<uint64_t>(2) << 61;
-    return d;
-}
-// Instruction descriptor kind::f16: D=f32 [4,6)=1, A=bf16 [7,10)=1, B=bf16 [10,13)=1,
-// both K-major, N>>3 at [17,23), M>>4 at [24,29).
-__device__ __forceinline__ uint32_t umma_idesc_bf16(int M, int N) {
-    return (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(N >> 3) << 17) |
-           (static_cast<uint32_t>(M >> 4) << 24);
-}
-__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                          uint32_t accumulate) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
-        : "memory");
-}
-__device__ __forceinline__ void umma_commit(uint32_t bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
-                 : "memory");
-}
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
-        "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, [%16];"
-        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-        : "r"(taddr)
-        : "memory");
-}
-__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
-
-__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
-    __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);   // RNE, one rounding per stored value
-    return *reinterpret_cast<uint32_t *>(&h);
-}
-__device__ __forceinline__ float bf16_lo(uint32_t u) { return __uint_as_float(u << 16); }
-__device__ __forceinline__ float bf16_hi(uint32_t u) { return __uint_as_float(u & 0xFFFF0000u); }
 
 struct TileCoord {
     int n0, h0, co0;
@@ -211,14 +91,14 @@ __global__ void __launch_bounds__(kConvThreads, 1)
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < S; ++i) {
-            mbar_init(full_bar(i), 1);
+            mbar_init(full_bar(i), 2);    // A producer + B producer
             mbar_init(empty_bar(i), 1);
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(tfull_bar(i), 1);
-            mbar_init(tempty_bar(i), 128);
+            mbar_init(tempty_bar(i), kEpiThreads);
             mbar_init(rfull_bar(i), 1);
-            mbar_init(rempty_bar(i), 128);
+            mbar_init(rempty_bar(i), kEpiThreads);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         prefetch_tmap(&tmA0);
@@ -257,15 +137,16 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     const uint32_t tmem_base = *tmem_slot;
     if (tr && threadIdx.x == 0) tr[1] = gtimer();
 
-    if (warp == 0) {
-        // ===================== TMA producer (one thread) =====================
+    if (warp == 0 || warp == 2) {
+        // ============ TMA producers: warp 0 = residual + A (activations), warp 2 = B (weights) ============
+        // (two issuing threads: one thread caps at ~28-48 B/cycle/SM of TMA traffic, tools/ubench)
         if (lane == 0) {
+            const bool isA = (warp == 0);
             int stage = 0, rs = 0;
             uint32_t phase = 0, rphase = 0;
-            const uint32_t tx = kTileABytes + a.stage_b_bytes;
             for (int t = blockIdx.x; t < total; t += gridDim.x) {
                 const TileCoord tc = tile_coord(a, t);
-                if (n_res) {   // residual tile of this output tile, prefetched a tile ahead of its epilogue
+                if (false && isA && n_res) {   // (residual prefetch runs on warp 3, below)
                     mbar_wait(rempty_bar(rs), rphase ^ 1);
                     if (a.debug & 8) mbar_arrive(rfull_bar(rs));
                     else mbar_expect_tx(rfull_bar(rs), chunk_bytes);
@@ -287,10 +168,12 @@ __global__ void __launch_bounds__(kConvThreads, 1)
                         mbar_wait(empty_bar(stage), phase ^ 1);
                         if (a.debug & 1) {
                             mbar_arrive(full_bar(stage));
-                        } else {
-                            mbar_expect_tx(full_bar(stage), tx);
+                        } else if (isA) {
+                            mbar_expect_tx(full_bar(stage), kTileABytes);
                             tma_load_4d(sA + stage * kTileABytes, tA, full_bar(stage), ch * kChunk, kw - gp.pad,
                                         tc.h0 * gp.stride + kh - gp.pad, tc.n0);
+                        } else {
+                            mbar_expect_tx(full_bar(stage), a.stage_b_bytes);
                             tma_load_3d(sB + stage * a.stage_b_bytes, tB, full_bar(stage), ch * kChunk, tap, tc.co0);
                         }
                         if (++stage == S) {
@@ -300,12 +183,37 @@ __global__ void __launch_bounds__(kConvThreads, 1)
                     }
                 }
             }
-            if (tr) tr[2] = gtimer();
+            if (tr && isA) tr[2] = gtimer();
+        }
+    } else if (warp == 3) {
+        // ===================== residual prefetch (own warp: never gates the A/B ring) =========
+        if (lane == 0 && n_res) {
+            int rs = 0;
+            uint32_t rphase = 0;
+            for (int t = blockIdx.x; t < total; t += gridDim.x) {
+                const TileCoord tc = tile_coord(a, t);
+                mbar_wait(rempty_bar(rs), rphase ^ 1);
+                if (a.debug & 8) {
+                    mbar_arrive(rfull_bar(rs));
+                } else {
+                    mbar_expect_tx(rfull_bar(rs), chunk_bytes);
+                    for (uint32_t j = 0; j < a.n_out_chunks; ++j)
+                        tma_load_4d(sRes + rs * chunk_bytes + j * 16384u, &tmRes, rfull_bar(rs), tc.co0 + j * kChunk, 0,
+                                    tc.h0, tc.n0);
+                }
+                if (++rs == n_res) {
+                    rs = 0;
+                    rphase ^= 1;
+                }
+            }
         }
     } else if (warp == 1) {
         // ===================== MMA issuer (one thread) =======================
-        if (lane == 0) {
+        // lean loop: descriptor = base + offset adds, K-steps unrolled (see kernels_halo.cu)
+        {   // whole warp runs the loop (uniform operands), one elected lane issues
             const uint32_t idesc = umma_idesc_bf16(kTileM, a.n_tile);
+            const uint64_t adesc0 = umma_desc_sw128(sA), bdesc0 = umma_desc_sw128(sB);
+            const uint32_t a16 = kTileABytes >> 4, b16 = a.stage_b_bytes >> 4;
             int stage = 0, as = 0;
             uint32_t phase = 0, aphase = 0;
             for (int t = blockIdx.x; t < total; t += gridDim.x) {
@@ -314,37 +222,45 @@ __global__ void __launch_bounds__(kConvThreads, 1)
                 for (int p = 0; p < a.n_parts; ++p) {
                     const GemmPart &gp = a.part[p];
                     const uint32_t d = tmem_base + static_cast<uint32_t>((as * a.n_parts + p) * a.acc_stride);
+                    const int nchunks = gp.n_chunks;
+                    int ch = 0;
                     for (int kb = 0; kb < gp.n_kblocks; ++kb) {
-                        const int ch = kb % gp.n_chunks;
-                        int nk = (gp.c_in - ch * kChunk + 15) >> 4;
-                        nk = nk > 4 ? 4 : nk;
+                        const int nk = min(4, (gp.c_in - ch * kChunk + 15) >> 4);
                         mbar_wait(full_bar(stage), phase);
                         tc_fence_after();
-                        const uint64_t ad = umma_desc_sw128(sA + stage * kTileABytes);
-                        const uint64_t bd = umma_desc_sw128(sB + stage * a.stage_b_bytes);
-                        if (!(a.debug & 2))
-                            for (int kk = 0; kk < nk; ++kk)   // K=16 per MMA = 32 bytes inside the 128-B atom
-                                umma_bf16(d, ad + 2 * kk, bd + 2 * kk, idesc, (kb | kk) != 0);
-                        umma_commit(empty_bar(stage));   // frees the smem slot when these MMAs finish
+                        const uint64_t ad = adesc0 + stage * a16;
+                        const uint64_t bd = bdesc0 + stage * b16;
+                        if (elect_one()) {
+#pragma unroll
+                            for (int kk = 0; kk < 4; ++kk)   // K=16 per MMA = 32 bytes inside the 128-B atom
+                                if (kk < nk && !(a.debug & 2))
+                                    umma_bf16(d, ad + 2 * kk, bd + 2 * kk, idesc, (kb | kk) != 0);
+                            umma_commit(empty_bar(stage));   // frees the smem slot when these MMAs finish
+                        }
+                        __syncwarp();
                         if (++stage == S) {
                             stage = 0;
                             phase ^= 1;
                         }
+                        if (++ch == nchunks) ch = 0;
                     }
                 }
-                umma_commit(tfull_bar(as));   // accumulator ready for the epilogue
+                if (elect_one()) umma_commit(tfull_bar(as));   // accumulator ready for the epilogue
+                __syncwarp();
                 if (++as == a.acc_stages) {
                     as = 0;
                     aphase ^= 1;
                 }
             }
-            if (tr) tr[3] = gtimer();
+            if (tr && lane == 0) tr[3] = gtimer();
         }
-    } else {
-        // ===================== epilogue (warps 2..5) =========================
+    } else if (warp >= kEpiWarp0) {
+        // ===================== epilogue (warps 4..11) ========================
+        // two warps per TMEM lane quarter; warp half h takes column groups h, h+2, ...
         const int q = warp & 3;              // TMEM lane quarter this warp may access
+        const int half = (warp - kEpiWarp0) >> 2;
         const int row = q * 32 + lane;       // pixel row inside the 128-pixel tile
-        const bool leader = (warp == 2 && lane == 0);
+        const bool leader = (warp == kEpiWarp0 && lane == 0);
         const uint32_t lane_addr = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
         const int sw = row & 7;
         const float *s0 = sBN, *t0 = sBN + a.c_out, *s1 = sBN + 2 * a.c_out, *t1 = sBN + 3 * a.c_out;
@@ -358,12 +274,12 @@ __global__ void __launch_bounds__(kConvThreads, 1)
             tc_fence_after();
             if (!a.pool_out) {
                 if (leader) bulk_wait_read0();   // previous tile's stores have left the staging buffer
-                named_bar_sync(1, 128);
+                named_bar_sync(1, kEpiThreads);
             }
             if (n_res) mbar_wait(rfull_bar(rs), rphase);
             const uint8_t *resp = pRes + rs * chunk_bytes;
             const uint32_t col0 = static_cast<uint32_t>(as * a.n_parts * a.acc_stride);
-            for (int g = 0; g < a.n_tile / 16; ++g) {
+            for (int g = half; g < a.n_tile / 16; g += 2) {
                 uint32_t v[16], u[16];
                 tmem_ld16(lane_addr + col0 + g * 16, v);
                 if (a.epi == EPI_BN_PROJ_RELU) tmem_ld16(lane_addr + col0 + a.acc_stride + g * 16, u);
@@ -396,8 +312,11 @@ __global__ void __launch_bounds__(kConvThreads, 1)
                 if (a.pool_out) {
                     // rows of one image are P consecutive lanes (P | 32): butterfly over them
 #pragma unroll
-                    for (int i = 0; i < 16; ++i)
-                        for (int o = 1; o < P; o <<= 1) f[i] += __shfl_xor_sync(0xffffffffu, f[i], o);
+                    for (int o = 1; o < 32; o <<= 1) {
+                        if (o >= P) break;
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) f[i] += __shfl_xor_sync(0xffffffffu, f[i], o);
+                    }
                     const int n = tc.n0 + row / P;
                     if ((lane % P) == 0 && n < a.B) {
                         const float inv = 1.f / static_cast<float>(P);
@@ -425,7 +344,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
             }
             if (!a.pool_out) {
                 fence_proxy_async();          // generic smem writes -> visible to the TMA (async proxy)
-                named_bar_sync(1, 128);
+                named_bar_sync(1, kEpiThreads);
                 if (leader && !(a.debug & 4)) {
                     for (uint32_t j = 0; j < a.n_out_chunks; ++j)
                         tma_store_4d(&tmOut, sOut + j * 16384u, tc.co0 + j * kChunk, 0, tc.h0, tc.n0);
@@ -461,6 +380,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
 // CTA.  Tile = 128 pixels (tile_rows full image rows); several CTAs per SM.
 // Epilogue as the conv kernel: TMEM -> fp32 BN/ReLU -> bf16 -> SW128 staging -> TMA store.
 constexpr int kStemThreads = 128;
+
 constexpr int kStemMaxHaloB = 6 * 32 * 4 * 2;   // (rows+2) x W x c_img bf16 bytes, rows*W = 128, W <= 32, c_img <= 4
 
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void *src) {

@@ -41,6 +41,8 @@ struct DevLayer {
     float *shift[kMaxW] = {};
     CUtensorMap tm[kMaxW][kMaxW][17];        // weight tensor map per (r_prev idx, r idx, n_tile/16)
     bool tm_ok[kMaxW][kMaxW][17] = {};
+    CUtensorMap tmh[kMaxW][9][2];            // halo-kernel weight maps per (r idx, n_tile/16 - 1 (<=128), taps 3|9)
+    bool tmh_ok[kMaxW][9][2] = {};
 };
 
 struct DevSegment {
@@ -228,6 +230,16 @@ bool encode_w(slim_ctx *ctx, CUtensorMap *tm, const DevLayer &L, int c_in, int c
 // (the UMMA N limit), narrowed down to 64 while the grid would leave most SMs idle
 // (small-M layers late in the network, SURVEY §7 "hard parts" #3).  When there are
 // several N tiles each must be a multiple of 64 channels.
+// Weights as a 3-D map (ci, co, tap) -- strides co: 9*Cin_full*2, tap: Cin_full*2 -- so a box
+// [64, n_tile, taps] lands as `taps` consecutive K-major n_tile x 64 operand tiles.
+bool encode_w_taps(slim_ctx *ctx, CUtensorMap *tm, const DevLayer &L, int c_in, int c_out, int n_tile, int taps) {
+    cuuint64_t dims[3] = {(cuuint64_t)c_in, (cuuint64_t)c_out, 9};
+    cuuint64_t strides[2] = {(cuuint64_t)9 * L.sh.cin * 2, (cuuint64_t)L.sh.cin * 2};
+    cuuint32_t box[3] = {(cuuint32_t)kChunk, (cuuint32_t)n_tile, (cuuint32_t)taps};
+    cuuint32_t est[3] = {1, 1, 1};
+    return encode_map(ctx, tm, L.w, 3, dims, strides, box, est);
+}
+
 int pick_n_tile(int c_out, int m_tiles = 1 << 30, int num_sms = 148) {
     int best = 0;
     for (int nt = 1; nt <= c_out / 16; ++nt) {
@@ -293,7 +305,127 @@ void conv_work(const slim_config &c, const ConvCall &cc, int ri, int B, int Ho, 
     *bytes = b;
 }
 
+// Stride-1 3x3 conv with one halo load per channel chunk (kernels_halo.cu).  Returns
+// SLIM_EUNSUPPORTED (nothing launched) when the layer does not fit its constraints.
+slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, int ri, int B) {
+    static const bool disabled = getenv("SLIM_NO_HALO") != nullptr;
+    const slim_config &c = ctx->cfg;
+    DevLayer &L = *cc.L;
+    if (disabled || L.sh.k != 3 || L.sh.stride != 1 || cc.epi == EPI_BN_PROJ_RELU || cc.pool_out) return SLIM_EUNSUPPORTED;
+    const int H = cc.H, W = cc.W;
+    if (W > 32 || 32 % W || H * W < kTileM || kTileM % W || H % (kTileM / W)) return SLIM_EUNSUPPORTED;
+    const int c_out = slim_channels(c.widths[ri], L.sh.cout);
+    HaloArgs a{};
+    a.B = B;
+    a.H = H;
+    a.W = W;
+    a.rows = kTileM / W;
+    a.tiles_per_img = H / a.rows;
+    a.m_tiles = B * a.tiles_per_img;
+    // N tile <= 128: three accumulators of it must fit the 512 TMEM columns
+    int nt = 1;
+    for (;; ++nt) {
+        if (nt > c_out / 16) return SLIM_EUNSUPPORTED;
+        if (c_out % nt || (c_out / nt) % 16 || (nt > 1 && (c_out / nt) % 64)) continue;
+        if (c_out / nt <= 128) break;
+    }
+    a.n_tile = c_out / nt;
+    a.n_tiles = nt;
+    a.c_out = c_out;
+    a.c_in = cc.c_in;
+    a.n_chunks = (cc.c_in + kChunk - 1) / kChunk;
+    a.epi = cc.epi;
+    a.scale = L.scale[ri];
+    a.shift = L.shift[ri];
+    a.acc_stride = (a.n_tile + 31) / 32 * 32;
+    a.acc_stages = 6 * a.acc_stride <= 512 ? 2 : 1;
+    int cols = a.acc_stages * 3 * a.acc_stride, tc = 32;
+    while (tc < cols) tc <<= 1;
+    a.tmem_cols = tc;
+    a.a_bytes = static_cast<uint32_t>(kTileM + 2 * W) * 128u;
+    a.n_out_chunks = static_cast<uint32_t>((a.n_tile + kChunk - 1) / kChunk);
+    const size_t chunk = static_cast<size_t>(a.n_out_chunks) * 16384;
+    const size_t budget = 226 * 1024;
+    const size_t fixed0 = 1024 + chunk + 8 * static_cast<size_t>(c_out) + 8 * 24 + 16;
+    const uint32_t all_w = static_cast<uint32_t>(a.n_chunks) * 9u * a.n_tile * 128u;
+    a.res_slots = (cc.epi == EPI_BN_ADD_RELU) ? 2 : 0;
+    a.stationary = (nt == 1 && all_w <= 100 * 1024) ? 1 : 0;
+    if (a.stationary) {
+        a.b_bytes = all_w;
+        a.sb = 1;
+    } else {
+        a.b_bytes = 3u * a.n_tile * 128u;
+    }
+    // fit: A slots 2..3, B slots 2..4 (streaming), residual slots 2 -> 1 if tight
+    for (;;) {
+        const size_t res = chunk * a.res_slots;
+        size_t left = budget - fixed0 - res;
+        if (a.stationary) {
+            if (left < a.b_bytes + 2 * a.a_bytes) {
+                if (a.res_slots == 2) { a.res_slots = 1; continue; }
+                return SLIM_EUNSUPPORTED;
+            }
+            left -= a.b_bytes;
+            a.sa = static_cast<int>(left / a.a_bytes);
+            a.sa = a.sa > 4 ? 4 : a.sa;
+        } else {
+            if (left < 2 * a.a_bytes + 2 * a.b_bytes) {
+                if (a.res_slots == 2) { a.res_slots = 1; continue; }
+                return SLIM_EUNSUPPORTED;
+            }
+            a.sa = 2;
+            left -= 2 * a.a_bytes;
+            a.sb = static_cast<int>(left / a.b_bytes);
+            a.sb = a.sb > 4 ? 4 : a.sb;
+            if (a.sb >= 4 && left - 4 * a.b_bytes >= a.a_bytes) a.sa = 3;
+        }
+        break;
+    }
+    if (a.res_slots == 0) a.res_slots = 1;   // unused without a residual
+    static const int conv_debug = getenv("SLIM_CONV_DEBUG") ? atoi(getenv("SLIM_CONV_DEBUG")) : 0;
+    a.debug = conv_debug;
+    a.trace = ctx->trace;
+
+    CUtensorMap tA, tRes, tOut;
+    if (!encode_act(ctx, &tA, cc.x, B, H, W, cc.c_in, W, a.rows + 2, 1, 1))
+        return fail(ctx, SLIM_ECUDA, "cuTensorMapEncodeTiled(halo A) failed");
+    const int taps = a.stationary ? 9 : 3;
+    const CUtensorMap *tB;
+    {
+        std::lock_guard<std::mutex> g(ctx->mu);
+        bool &ok = L.tmh_ok[ri][a.n_tile / 16 - 1][a.stationary];
+        CUtensorMap &m = L.tmh[ri][a.n_tile / 16 - 1][a.stationary];
+        if (!ok) {
+            if (!encode_w_taps(ctx, &m, L, cc.c_in, c_out, a.n_tile, taps))
+                return fail(ctx, SLIM_ECUDA, "cuTensorMapEncodeTiled(halo W) failed");
+            ok = true;
+        }
+        tB = &m;
+    }
+    if (!encode_act(ctx, &tOut, cc.out, B, H, W, c_out, W, a.rows, 1, 1))
+        return fail(ctx, SLIM_ECUDA, "cuTensorMapEncodeTiled(halo out) failed");
+    tRes = tOut;
+    if (cc.epi == EPI_BN_ADD_RELU && !encode_act(ctx, &tRes, cc.res, B, H, W, c_out, W, a.rows, 1, 1))
+        return fail(ctx, SLIM_ECUDA, "cuTensorMapEncodeTiled(halo res) failed");
+    const int total = a.m_tiles * a.n_tiles;
+    int grid = ctx->num_sms;
+    if (grid > total) grid = total;
+    double flops, bytes;
+    conv_work(c, cc, ri, B, H, W, &flops, &bytes);
+    LaunchProf prof(ctx, st);
+    cudaError_t e = launch_conv_halo(a, tA, *tB, tRes, tOut, grid, st, ctx->pdl && !ctx->prof_on);
+    prof.done(SLIM_K_CONV_UMMA, cc.seg, cc.layer, c.widths[cc.ri_in], c.widths[ri], B, flops, bytes);
+    if (e != cudaSuccess)
+        return fail(ctx, SLIM_ECUDA, "conv_halo launch (grid %d, smem %zu): %s", grid, conv_halo_smem_bytes(a),
+                    cudaGetErrorString(e));
+    return SLIM_OK;
+}
+
 slim_status conv_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, int ri, int B) {
+    {
+        const slim_status hs = conv_halo_bf16(ctx, st, cc, ri, B);
+        if (hs != SLIM_EUNSUPPORTED) return hs;
+    }
     const slim_config &c = ctx->cfg;
     DevLayer &L = *cc.L;
     const int k = L.sh.k, s = L.sh.stride, pad = k / 2;

@@ -15,8 +15,10 @@ namespace slim {
 constexpr int kTileM = 128;        // UMMA M (cta_group::1): TMEM lane = tile row
 constexpr int kChunk = 64;         // channels per K-block = one 128-byte SW128 row
 constexpr int kTileABytes = kTileM * kChunk * 2;   // 16 KiB A operand per K-block
-constexpr int kConvThreads = 192;  // warp0 TMA, warp1 MMA (+TMEM alloc), warps2-5 epilogue
+constexpr int kConvThreads = 384;  // warp0 A-TMA, warp1 MMA (+TMEM alloc), warp2 B-TMA, warps4-11 epilogue
 constexpr int kMaxStages = 8;
+constexpr int kEpiWarp0 = 4;       // first epilogue warp (warp 3 idles)
+constexpr int kEpiThreads = 256;   // 8 epilogue warps, two per TMEM lane quarter
 
 enum EpiMode : int {
     EPI_BN_RELU = 0,        // relu(s*acc + t)                       (stem-less conv1, K1)
@@ -51,6 +53,27 @@ struct ConvArgs {
 };
 
 size_t conv_umma_smem_bytes(const ConvArgs &a);
+
+// stride-1 3x3 conv, one halo box per channel chunk + kw-split accumulators (kernels_halo.cu)
+struct HaloArgs {
+    int B, H, W;              // output = input spatial size (stride 1, pad 1)
+    int rows, tiles_per_img;  // tile = rows full image rows, rows*W = 128
+    int m_tiles, n_tiles, n_tile, c_out, c_in, n_chunks;
+    int epi;                  // EPI_BN_RELU or EPI_BN_ADD_RELU
+    const float *scale, *shift;
+    int stationary;           // all weights resident in smem (one B slot of n_chunks*9 taps)
+    int sa, sb;               // A ring slots (one per chunk), B ring slots (one per (chunk, kh)) -- each <= 4
+    int acc_stride, acc_stages, tmem_cols;
+    uint32_t a_bytes, b_bytes;
+    uint32_t n_out_chunks;
+    int res_slots;
+    int debug;
+    unsigned long long *trace;
+};
+size_t conv_halo_smem_bytes(const HaloArgs &a);
+cudaError_t launch_conv_halo(const HaloArgs &a, const CUtensorMap &tmA, const CUtensorMap &tmB,
+                             const CUtensorMap &tmRes, const CUtensorMap &tmOut, int grid, cudaStream_t stream,
+                             bool pdl);
 cudaError_t launch_conv_umma(const ConvArgs &a, const CUtensorMap &tmA0, const CUtensorMap &tmB0,
                              const CUtensorMap &tmA1, const CUtensorMap &tmB1, const CUtensorMap &tmRes,
                              const CUtensorMap &tmOut, int grid, cudaStream_t stream, bool pdl);

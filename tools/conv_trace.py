@@ -34,3 +34,18 @@ print(f"B={B} r={r} seg={seg} ctas={len(t)}")
 for i, n in enumerate(names):
     col = t[:, i] - base
     print(f"{n:14s} min {col.min()/1e3:7.2f} med {np.median(col)/1e3:7.2f} max {col.max()/1e3:7.2f} us")
+# per-tile detail of CTA 0 (halo kernel only): roles A(0) MMA(1) EPI(2), 4 points each
+d = buf[2048:2048 + 4 * 256].astype(np.int64).reshape(4, 64, 4)
+if d.any():
+    t0 = buf.reshape(-1, 8)[0, 1].astype(np.int64)
+    labels = {0: ["A:start", "A:res_slot", "A:a_slot", "-"], 1: ["M:start", "M:tmem", "M:a_full", "M:commit"],
+              2: ["E:t_full", "E:rd_done", "E:res_ok", "E:store"], 3: ["M:mma0", "M:mma_end", "M:c_a", "M:c_t"]}
+    for ti in range(8):
+        row = []
+        for role in (0, 1, 3, 2):
+            for pt in range(4):
+                v = d[role, ti, pt]
+                if v:
+                    row.append(f"{labels[role][pt]}={(v - t0) / 1e3:6.2f}")
+        if row:
+            print(f"tile {ti}: " + " ".join(row))
