@@ -293,6 +293,154 @@ def run_ours(args):
     return 0
 
 
+def _clock_energy_json(sampler, e0, e1, n_images):
+    return sampler.summary(), (((e1 - e0) / 1e3 / n_images) if (e0 is not None and e1 is not None) else None)
+
+
+def run_stream(args):
+    """CFG4 (N=1) / CFG5 (torchrun N>1): the mixed-width request stream through the key packer,
+    gather, segment forwards and scatter; requests routed to ranks by a replicated policy."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import synth
+    import paper_2510_09018_b200 as slim
+    from paper_2510_09018_b200 import build as slim_build
+    from paper_2510_09018_b200 import router
+    from paper_2510_09018_b200.stream import StreamExecutor
+    from paper_2510_09018_b200.telemetry import NvmlSampler, TelemetryExchange, pack_record
+
+    world, rank, local = _dist()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    slim_build.build()
+    net = slim.SlimNet(synth.make_weights(), synth.make_bn(), device=local, max_batch=args.bmax)
+    slim.slim_set_graph_mode(net.ctx, True)
+    n_total = args.requests * world
+    devs, tups, grps = router.route(n_total, world, args.policy)
+    mine = router.shard(devs, rank)
+    tuples = np.asarray([router.TABLE_TUPLES[t] for t in tups[mine]], np.float32)
+    x = torch.from_numpy(synth.make_images(len(mine), offset=200 + rank)).to(torch.bfloat16).to(dev)
+    ex = StreamExecutor(net, n_max=len(mine), B_max=args.bmax, device=dev)
+    telem = TelemetryExchange(device=dev) if world > 1 else None
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(args.warmup):
+        ex.run(x, tuples, stream)
+    torch.cuda.synchronize()
+    sampler = NvmlSampler(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    l0 = slim.slim_launch_count(net.ctx)
+    e0 = sampler.energy_mj()
+    sampler.start()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for k in range(args.steps):
+        ex.run(x, tuples, stream)
+        if telem:
+            telem.tick(pack_record(rank=rank, completed=(k + 1) * len(mine)))
+    b.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    sampler.stop()
+    e1 = sampler.energy_mj()
+    ms = a.elapsed_time(b)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    value = n_total * args.steps / (float(t.item()) / 1e3)
+    clocks, energy = _clock_energy_json(sampler, e0, e1, len(mine) * args.steps)
+    batches = [b for seg in ex.last_batches for b in seg]
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": float(t.item()) / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": f"{'CFG5' if world > 1 else 'CFG4'}: mixed-width request stream "
+                                   f"(width tuples of Tables I-II), greedy (segment, w_req, w_prev) batching, "
+                                   f"B_max={args.bmax}, routing={args.policy}",
+                       "requests_per_rank": args.requests, "parallelism": f"dp{world} routed"},
+            "batches_per_step_rank0": len(batches), "mean_batch_rank0": float(np.mean(batches)),
+            "gpu_launches": slim.slim_launch_count(net.ctx) - l0, "energy_j_per_image": energy, "clocks": clocks,
+        }))
+    net.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def run_points(args):
+    """cfg1: seg 0 at r=0.25, B=8 (BASELINE configs[0]); sweep: CFG3, B in 1..4096 x widths.
+    One JSON line per point (graph replay, L2 flushed before each timed replay batch)."""
+    import torch
+
+    import synth
+    import paper_2510_09018_b200 as slim
+    from paper_2510_09018_b200 import build as slim_build
+
+    world, rank, local = _dist()
+    if rank != 0:
+        return 0
+    torch.cuda.set_device(local)
+    slim_build.build()
+    peaks = _peaks()
+    points = [(8, 0.25, "seg0")] if args.workload == "cfg1" else \
+        [(B, r, "chain") for B in (1, 2, 4, 8, 16, 32, 64, 128, 256, 512, 1024, 2048, 4096) for r in WIDTHS]
+    bmax = max(p[0] for p in points)
+    net = slim.SlimNet(synth.make_weights(), synth.make_bn(), device=local, max_batch=bmax)
+    slim.slim_set_graph_mode(net.ctx, True)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    xall = torch.from_numpy(synth.make_images(bmax, offset=300)).to(torch.bfloat16).cuda()
+    st = torch.cuda.current_stream()
+    for B, r, kind in points:
+        x = xall[:B]
+        if kind == "seg0":
+            out = torch.empty(B, 32, 32, slim.slim_channels(r, 64), dtype=torch.bfloat16, device="cuda")
+            wsb = slim.slim_forward_workspace_bytes(net.ctx, 0, r, r, B)
+            ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+            fn = lambda: slim.slim_forward_ws(net.ctx, 0, r, r, B, x, out, ws, wsb, st)
+        else:
+            out = torch.empty(B, 100, dtype=torch.float32, device="cuda")
+            wsb = slim.slim_chain_workspace_bytes(net.ctx, (r,) * 4, B)
+            ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+            fn = lambda: slim.slim_forward_chain(net.ctx, (r,) * 4, B, x, out, ws, wsb, st)
+        for _ in range(max(3, args.warmup)):
+            fn()
+        reps = max(1, min(args.steps, 20000 // max(1, B)))
+        # per-launch records for the roofline of this point (profiled pass, no graph)
+        slim.slim_profile_begin(net.ctx, 64)
+        fn()
+        recs = slim.slim_profile_end(net.ctx)
+        flops = sum(x_["flops"] for x_ in recs)
+        roof_s = sum(max(x_["flops"] / (peaks["bf16"] * 1e12), x_["bytes"] / (peaks["hbm"] * 1e9)) for x_ in recs)
+        flush.zero_()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        for _ in range(reps):
+            fn()
+        b.record(st)
+        torch.cuda.synchronize()
+        us = a.elapsed_time(b) / reps * 1e3
+        print(json.dumps({
+            "metric": METRIC, "value": B / us * 1e6, "unit": "images/s", "n_gpus": 1, "steps": reps,
+            "warmup": max(3, args.warmup), "ms_per_step": us / 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": ("CFG1: segment 0 (first residual stage) r=0.25 B=8" if kind == "seg0"
+                                    else "CFG3: full chain batch sweep"), "batch": B, "width": r,
+                       "l2": "flushed once before the timed replays (steady-state L2 reuse across replays)"},
+            "us_per_call": us, "tflops": flops / (us * 1e-6) / 1e12,
+            "per_layer_roofline_frac": roof_s / (us * 1e-6), "gpu_launches_per_call": len(recs),
+        }), flush=True)
+    net.close()
+    return 0
+
+
 def _ncu_traffic():
     """dram bytes per conv launch from the committed ncu --set full summary, if present."""
     p = os.path.join(ROOT, "profiles", "ncu_conv_summary.json")
@@ -317,10 +465,20 @@ def main(argv=None):
     ap.add_argument("--profile-steps", type=int, default=50)
     ap.add_argument("--e2e-steps", type=int, default=200)
     ap.add_argument("--json-out", default=None)
+    ap.add_argument("--workload", choices=("cfg2", "cfg1", "sweep", "stream"), default="cfg2",
+                    help="cfg2 (default, BASELINE configs[1]); cfg1 = seg0 r=0.25 B=8; sweep = CFG3 batch sweep "
+                         "(one JSON line per point); stream = CFG4/CFG5 mixed-width routed request stream")
+    ap.add_argument("--requests", type=int, default=1024, help="stream: requests per rank per step")
+    ap.add_argument("--bmax", type=int, default=256, help="stream: B_max of the key batching")
+    ap.add_argument("--policy", default="random", help="stream: routing policy (random | slim | table_rr)")
     args = ap.parse_args(argv)
     assert args.warmup >= 0 and args.steps >= 1
     if args.impl == "reference":
         return run_reference(args)
+    if args.workload == "stream":
+        return run_stream(args)
+    if args.workload in ("cfg1", "sweep"):
+        return run_points(args)
     return run_ours(args)
 
 

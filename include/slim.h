@@ -194,6 +194,12 @@ SLIM_API slim_status slim_launch(slim_ctx *ctx, const slim_launch_desc *desc, co
 SLIM_API slim_status slim_gather(slim_ctx *ctx, const void *src, const uint32_t *idx, int n, size_t row_bytes,
                         void *dst, void *stream);
 
+/* Device scatter (inverse of slim_gather): row i of src (row_bytes, multiple of 16)
+ * goes to dst + idx[i]*dst_stride; used to return a packed batch's outputs to the
+ * per-request activation pool of the next segment (P:49 re-entry with w_prev). */
+SLIM_API slim_status slim_scatter(slim_ctx *ctx, const void *src, const uint32_t *idx, int n, size_t row_bytes,
+                                  void *dst, size_t dst_stride, void *stream);
+
 /* ---- execution modes and profiling ------------------------------------- */
 
 /* Graph mode (default off): slim_forward_ws / slim_forward_chain capture their

@@ -20,7 +20,7 @@ __all__ = [
     "SlimError", "load_library", "slim_config", "default_config", "slim_create", "slim_destroy",
     "slim_load_segment", "slim_unload_segment", "slim_segment_bytes", "slim_forward", "slim_forward_ws",
     "slim_forward_workspace_bytes", "slim_chain_workspace_bytes", "slim_forward_chain", "slim_pack",
-    "slim_launch", "slim_gather", "slim_last_error", "slim_launch_count", "slim_channels", "SlimNet",
+    "slim_launch", "slim_gather", "slim_scatter", "slim_last_error", "slim_launch_count", "slim_channels", "SlimNet",
     "manifest", "LIB_PATH",
 ]
 
@@ -111,6 +111,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
                            ctypes.POINTER(_I), ctypes.POINTER(ctypes.c_uint32)]),
         "slim_launch": (_I, [_VP, ctypes.POINTER(slim_launch_desc), _VP, _VP, _SZ, _VP, _VP, _VP, _SZ, _VP]),
         "slim_gather": (_I, [_VP, _VP, _VP, _I, _SZ, _VP, _VP]),
+        "slim_scatter": (_I, [_VP, _VP, _VP, _I, _SZ, _VP, _SZ, _VP]),
         "slim_last_error": (_I, [_VP]),
         "slim_last_error_msg": (ctypes.c_char_p, [_VP]),
         "slim_status_str": (ctypes.c_char_p, [_I]),
@@ -133,7 +134,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
 EXPORTED = ("slim_create", "slim_destroy", "slim_default_config", "slim_load_segment", "slim_unload_segment",
             "slim_segment_loaded", "slim_segment_bytes", "slim_forward", "slim_forward_workspace_bytes",
             "slim_forward_ws", "slim_chain_workspace_bytes", "slim_forward_chain", "slim_pack", "slim_launch",
-            "slim_gather", "slim_last_error", "slim_last_error_msg", "slim_status_str", "slim_version",
+            "slim_gather", "slim_scatter", "slim_last_error", "slim_last_error_msg", "slim_status_str", "slim_version",
             "slim_launch_count", "slim_num_sms", "slim_channels", "slim_set_graph_mode", "slim_profile_begin",
             "slim_profile_end")
 
@@ -290,6 +291,11 @@ def slim_launch(ctx, desc: dict, slots, pool, pool_row_bytes, slab, out, ws, ws_
 
 def slim_gather(ctx, src, idx, n, row_bytes, dst, stream=None):
     _check(ctx, load_library().slim_gather(ctx, _ptr(src), _ptr(idx), n, row_bytes, _ptr(dst), _stream(stream)))
+
+
+def slim_scatter(ctx, src, idx, n, row_bytes, dst, dst_stride, stream=None):
+    _check(ctx, load_library().slim_scatter(ctx, _ptr(src), _ptr(idx), n, row_bytes, _ptr(dst), dst_stride,
+                                            _stream(stream)))
 
 
 def slim_last_error(ctx) -> int:

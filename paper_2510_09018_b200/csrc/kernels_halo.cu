@@ -102,12 +102,12 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
         const uint32_t per_chunk = 9u * a.n_tile * 128u;
         for (int ch = 0; ch < a.n_chunks; ++ch) tma_load_3d(sB + ch * per_chunk, &tmB, b_full(0), ch * kChunk, 0, 0);
     }
-    pdl_wait();
-    pdl_launch_dependents();
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    if (warp != 2) pdl_wait();   // the weight producer does not depend on the previous kernel
+    pdl_launch_dependents();
     if (tr && threadIdx.x == 0) tr[1] = gtimer();
     const int tiles_per_img = a.tiles_per_img;
 

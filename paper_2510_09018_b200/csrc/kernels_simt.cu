@@ -165,6 +165,16 @@ __global__ void __launch_bounds__(kHeadThreads)
     fc_kernel(const float *__restrict__ pooled, const float *__restrict__ fc_w, const float *__restrict__ fc_b,
               float *__restrict__ logits, int B, int c3, int c3_full, int K) {
     extern __shared__ float s_p[];   // [kHeadImgs][c3]
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    const int k0 = blockIdx.y * kHeadClasses + warp, k1 = k0 + nw;   // kHeadClasses == 2 * warps
+    // FC rows are weights (not produced by the previous kernel): load them before the PDL wait
+    float w0[kHeadMaxC / 32], w1[kHeadMaxC / 32];
+#pragma unroll
+    for (int i = 0; i < kHeadMaxC / 32; ++i) {
+        const int c = lane + 32 * i;
+        w0[i] = (c < c3 && k0 < K) ? __ldg(fc_w + static_cast<size_t>(k0) * c3_full + c) : 0.f;
+        w1[i] = (c < c3 && k1 < K) ? __ldg(fc_w + static_cast<size_t>(k1) * c3_full + c) : 0.f;
+    }
     asm volatile("griddepcontrol.wait;" ::: "memory");
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const int n0 = blockIdx.x * kHeadImgs;
@@ -174,37 +184,37 @@ __global__ void __launch_bounds__(kHeadThreads)
     for (int i = threadIdx.x; i < kHeadImgs * c3 / 4; i += blockDim.x)
         reinterpret_cast<float4 *>(s_p)[i] = i < nv ? __ldg(src + i) : make_float4(0.f, 0.f, 0.f, 0.f);
     __syncthreads();
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-    const int k_end = min(K, (blockIdx.y + 1) * kHeadClasses);
-    for (int k = blockIdx.y * kHeadClasses + warp; k < k_end; k += nw) {
-        const float *wr = fc_w + static_cast<size_t>(k) * c3_full;
-        float w[kHeadMaxC / 32];
+    float d0[kHeadImgs], d1[kHeadImgs];
 #pragma unroll
-        for (int i = 0; i < kHeadMaxC / 32; ++i) {
-            const int c = lane + 32 * i;
-            w[i] = (c < c3) ? __ldg(wr + c) : 0.f;
-        }
-        float d[kHeadImgs];
+    for (int j = 0; j < kHeadImgs; ++j) d0[j] = d1[j] = 0.f;
 #pragma unroll
-        for (int j = 0; j < kHeadImgs; ++j) d[j] = 0.f;
+    for (int i = 0; i < kHeadMaxC / 32; ++i) {
+        const int c = lane + 32 * i;
+        if (c < c3) {
 #pragma unroll
-        for (int i = 0; i < kHeadMaxC / 32; ++i) {
-            const int c = lane + 32 * i;
-            if (c < c3) {
-#pragma unroll
-                for (int j = 0; j < kHeadImgs; ++j) d[j] = fmaf(s_p[j * c3 + c], w[i], d[j]);
+            for (int j = 0; j < kHeadImgs; ++j) {
+                const float p = s_p[j * c3 + c];
+                d0[j] = fmaf(p, w0[i], d0[j]);
+                d1[j] = fmaf(p, w1[i], d1[j]);
             }
         }
+    }
 #pragma unroll
-        for (int j = 0; j < kHeadImgs; ++j)
+    for (int j = 0; j < kHeadImgs; ++j)
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) d[j] += __shfl_xor_sync(0xffffffffu, d[j], o);
-        if (lane < ni) {
-            float v = d[0];
-#pragma unroll
-            for (int j = 1; j < kHeadImgs; ++j) v = (lane == j) ? d[j] : v;
-            logits[static_cast<size_t>(n0 + lane) * K + k] = v + fc_b[k];
+        for (int o = 16; o > 0; o >>= 1) {
+            d0[j] += __shfl_xor_sync(0xffffffffu, d0[j], o);
+            d1[j] += __shfl_xor_sync(0xffffffffu, d1[j], o);
         }
+    if (lane < ni) {
+        float v0 = d0[0], v1 = d1[0];
+#pragma unroll
+        for (int j = 1; j < kHeadImgs; ++j) {
+            v0 = (lane == j) ? d0[j] : v0;
+            v1 = (lane == j) ? d1[j] : v1;
+        }
+        if (k0 < K) logits[static_cast<size_t>(n0 + lane) * K + k0] = v0 + fc_b[k0];
+        if (k1 < K) logits[static_cast<size_t>(n0 + lane) * K + k1] = v1 + fc_b[k1];
     }
 }
 
@@ -216,6 +226,18 @@ __global__ void gather_kernel(const uint4 *__restrict__ src, size_t src_stride, 
          i += static_cast<size_t>(gridDim.x) * blockDim.x) {
         const size_t r = i / per_row, off = i - r * per_row;
         dst[i] = __ldg(src + static_cast<size_t>(idx[r]) * src_stride + off);
+    }
+}
+
+// scatter (inverse of gather): dst + idx[r]*dst_stride <- src row r
+__global__ void scatter_kernel(const uint4 *__restrict__ src, const uint32_t *__restrict__ idx, int n, size_t per_row,
+                               uint4 *__restrict__ dst, size_t dst_stride) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    const size_t total = static_cast<size_t>(n) * per_row;
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const size_t r = i / per_row, off = i - r * per_row;
+        dst[static_cast<size_t>(idx[r]) * dst_stride + off] = __ldg(src + i);
     }
 }
 
@@ -357,6 +379,17 @@ cudaError_t launch_gather(const void *src, size_t src_stride, const uint32_t *id
     if (blocks > 148 * 16) blocks = 148 * 16;
     gather_kernel<<<blocks, 256, 0, s>>>(static_cast<const uint4 *>(src), src_stride / 16, idx, n, per_row,
                                          static_cast<uint4 *>(dst));
+    return cudaGetLastError();
+}
+cudaError_t launch_scatter(const void *src, const uint32_t *idx, int n, size_t row_bytes, void *dst, size_t dst_stride,
+                           cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    const size_t per_row = row_bytes / 16;
+    const size_t total = per_row * n;
+    int blocks = static_cast<int>((total + 255) / 256);
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    scatter_kernel<<<blocks, 256, 0, s>>>(static_cast<const uint4 *>(src), idx, n, per_row, static_cast<uint4 *>(dst),
+                                          dst_stride / 16);
     return cudaGetLastError();
 }
 cudaError_t launch_conv_f32(const ConvF32Args &a, cudaStream_t s) {

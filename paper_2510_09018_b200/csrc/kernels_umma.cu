@@ -129,12 +129,14 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     // PDL: everything above overlapped the previous kernel's tail; wait for its
     // results to be visible before any dependent global read, then let the next
     // kernel start its own prologue as SMs free up.
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    // (warp 2, the weight producer, does not wait: weights are not produced by the previous kernel,
+    // so its first TMA loads overlap the previous kernel's tail)
+    if (warp != 2) asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (tr && threadIdx.x == 0) tr[1] = gtimer();
 
     if (warp == 0 || warp == 2) {

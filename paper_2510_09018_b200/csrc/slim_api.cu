@@ -637,7 +637,8 @@ slim_status run_segment(slim_ctx *ctx, int seg, int ri_prev, int ri, int B, cons
             CUtensorMap tOut;
             if (!encode_act(ctx, &tOut, bufs[0], B, H, H, C, H, sa.tile_rows, 1, 1))
                 return fail(ctx, SLIM_ECUDA, "cuTensorMapEncodeTiled(stem out) failed");
-            int grid = ctx->num_sms * stem_umma_max_ctas_per_sm();
+            // ~45 KB smem and 64 TMEM columns per CTA: four CTAs per SM hide the per-tile latency chain
+            int grid = ctx->num_sms * 4;
             if (grid > sa.m_tiles) grid = sa.m_tiles;
             LaunchProf prof(ctx, st);
             e = launch_stem_umma(sa, tOut, grid, st, ctx->pdl && !ctx->prof_on);
@@ -1117,6 +1118,19 @@ slim_status slim_gather(slim_ctx *ctx, const void *src, const uint32_t *idx, int
     cudaError_t e = launch_gather(src, row_bytes, idx, n, row_bytes, dst, static_cast<cudaStream_t>(stream));
     prof.done(SLIM_K_GATHER, -1, -1, 0.f, 0.f, n, 0.0, 2.0 * n * static_cast<double>(row_bytes) + 4.0 * n);
     if (e != cudaSuccess) return fail(ctx, SLIM_ECUDA, "gather launch: %s", cudaGetErrorString(e));
+    return SLIM_OK;
+}
+
+slim_status slim_scatter(slim_ctx *ctx, const void *src, const uint32_t *idx, int n, size_t row_bytes, void *dst,
+                         size_t dst_stride, void *stream) {
+    if (!ctx || n < 0 || (n > 0 && (!src || !idx || !dst)) || row_bytes % 16 || dst_stride % 16 || dst_stride < row_bytes ||
+        !aligned16(src) || !aligned16(dst))
+        return ctx ? fail(ctx, SLIM_EINVAL, "scatter: bad arguments") : SLIM_EINVAL;
+    if (n == 0) return SLIM_OK;
+    LaunchProf prof(ctx, static_cast<cudaStream_t>(stream));
+    cudaError_t e = launch_scatter(src, idx, n, row_bytes, dst, dst_stride, static_cast<cudaStream_t>(stream));
+    prof.done(SLIM_K_GATHER, -1, -1, 0.f, 0.f, n, 0.0, 2.0 * n * static_cast<double>(row_bytes) + 4.0 * n);
+    if (e != cudaSuccess) return fail(ctx, SLIM_ECUDA, "scatter launch: %s", cudaGetErrorString(e));
     return SLIM_OK;
 }
 

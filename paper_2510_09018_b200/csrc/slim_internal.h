@@ -104,6 +104,10 @@ cudaError_t launch_fc_f32(const float *pooled, const float *fc_w, const float *f
 cudaError_t launch_gather(const void *src, size_t src_stride, const uint32_t *idx, int n, size_t row_bytes,
                           void *dst, cudaStream_t s);
 
+// dst + idx[i]*dst_stride (bytes) <- src row i (row_bytes, multiple of 16)
+cudaError_t launch_scatter(const void *src, const uint32_t *idx, int n, size_t row_bytes, void *dst, size_t dst_stride,
+                           cudaStream_t s);
+
 // FP32 mode (TF32 off): SIMT direct conv with the same fused epilogues.
 struct ConvF32Args {
     const float *x;  int B, H, W, c_in;          // part 0 input, dense NHWC

@@ -1,0 +1,99 @@
+"""Request-stream executor (CFG4): greedy key batching + gather + segment forwards.
+
+A request carries a width tuple (w_0..w_3) and re-enters the queue after each
+segment with key k = (s, w_req = w_s, w_prev = w_{s-1}).  Per
+segment this executor
+
+  1. groups the live requests by key with the ABI packer (`slim_pack`, Alg. 1
+     lines 3-4: FIFO head key, up to B_max requests of that key),
+  2. runs each group with `slim_launch`: the device gather kernel copies the
+     requests' activations from the segment's input pool into a contiguous slab,
+     then the segment forward runs on it (RUNBATCH, Alg. 1 l.10),
+  3. scatters the group's outputs back to the next segment's pool (`slim_scatter`),
+     or the logits for segment 3.
+
+Every data movement and all arithmetic run in libslim's kernels; this module only
+sequences calls (host control, SURVEY §3 stack 2).  Buffers are allocated once
+for n_max requests; graph mode caches one CUDA graph per (group shape, buffers).
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import SlimNet, slim_channels, slim_forward_workspace_bytes, slim_launch, slim_pack, slim_scatter
+
+
+class StreamExecutor:
+    def __init__(self, net: SlimNet, n_max: int, B_max: int = 256, device=None):
+        self.net = net
+        self.cfg = net.cfg
+        self.n_max = n_max
+        self.B_max = B_max
+        self.dev = torch.device(device if device is not None else f"cuda:{torch.cuda.current_device()}")
+        cfg = self.cfg
+        self.eb = 2 if cfg.dtype == 0 else 4
+        self.adt = torch.bfloat16 if cfg.dtype == 0 else torch.float32
+        hw = cfg.image_hw
+        wmax = cfg.widths[cfg.n_widths - 1]
+        # per-segment input pools, rows sized for the widest previous width (dense prefix per row)
+        self.row_elems = [hw * hw * cfg.in_channels]
+        for s in range(1, 4):
+            h = hw >> (s - 1)
+            self.row_elems.append(h * h * slim_channels(wmax, cfg.base_channels[s - 1]))
+        self.pools = [None] + [torch.empty(n_max * self.row_elems[s], dtype=self.adt, device=self.dev)
+                               for s in range(1, 4)]
+        self.logits = torch.empty(n_max, cfg.num_classes, dtype=torch.float32, device=self.dev)
+        self.slab = torch.empty(B_max * max(self.row_elems), dtype=self.adt, device=self.dev)
+        out_elems = max(max(self.row_elems[1:]), cfg.num_classes * 4 // self.eb)
+        self.out = torch.empty(B_max * out_elems, dtype=self.adt, device=self.dev)
+        self.wsb = max(slim_forward_workspace_bytes(net.ctx, s, wmax, wmax, B_max) for s in range(4))
+        self.ws = torch.empty(self.wsb, dtype=torch.uint8, device=self.dev)
+        self.order_h = torch.empty(4 * n_max, dtype=torch.int32).pin_memory()
+        self.order_d = torch.empty(4 * n_max, dtype=torch.int32, device=self.dev)
+        self._plan_key = None
+        self.last_batches = []
+
+    def _plan(self, tuples: np.ndarray):
+        """Pack all four segments (host only; cached for a repeated stream)."""
+        key = (tuples.shape[0], hash(tuples.tobytes()))
+        if key == self._plan_key:
+            return self._plan_cache
+        n = tuples.shape[0]
+        plan = []
+        for s in range(4):
+            reqs = [(i, s, float(tuples[i, s]), float(tuples[i, s - 1]) if s else 0.0, i) for i in range(n)]
+            descs, order = slim_pack(self.cfg, reqs, self.B_max)
+            plan.append((descs, order.astype(np.int32)))
+        self._plan_key, self._plan_cache = key, plan
+        self.order_h[:4 * n].view(4, n).copy_(torch.from_numpy(np.stack([p[1] for p in plan])))
+        self.order_d[:4 * n].copy_(self.order_h[:4 * n], non_blocking=True)
+        self.last_batches = [[d["batch"] for d in p[0]] for p in plan]
+        return plan
+
+    def run(self, images: torch.Tensor, tuples: np.ndarray, stream=None) -> torch.Tensor:
+        """images: device [n, H, W, C] (activation dtype); tuples: [n, 4] width per segment.
+        Returns the logits [n, classes] (a view into the executor's buffer)."""
+        n = images.shape[0]
+        assert n <= self.n_max and tuples.shape == (n, 4)
+        plan = self._plan(np.asarray(tuples, np.float32))
+        st = stream if stream is not None else torch.cuda.current_stream(self.dev)
+        hw, cfg = self.cfg.image_hw, self.cfg
+        for s in range(4):
+            descs, _ = plan[s]
+            pool = images if s == 0 else self.pools[s]
+            pool_row = self.row_elems[s] * self.eb
+            base = s * n
+            for d in descs:
+                b, first = d["batch"], d["first"]
+                idx = self.order_d[base + first: base + first + b]
+                slim_launch(self.net.ctx, d, idx, pool, pool_row, self.slab, self.out, self.ws, self.wsb, st)
+                if s < 3:
+                    h = hw >> s
+                    row = h * h * slim_channels(d["r"], cfg.base_channels[s]) * self.eb
+                    slim_scatter(self.net.ctx, self.out, idx, b, row, self.pools[s + 1],
+                                 self.row_elems[s + 1] * self.eb, st)
+                else:
+                    slim_scatter(self.net.ctx, self.out, idx, b, cfg.num_classes * 4, self.logits,
+                                 cfg.num_classes * 4, st)
+        return self.logits[:n]

@@ -273,3 +273,48 @@ def test_profile_records_cover_every_launch(net):
     # sliced FLOPs of the r=1 chain: 1110.94 MFLOP per image
     total = sum(r["flops"] for r in recs) / 16
     assert abs(total / 1e6 - 1110.94) / 1110.94 < 2e-3
+
+
+# ------------------------------------------------------------------ FP32 mode (TF32 off)
+@pytest.fixture(scope="module")
+def net32(params):
+    w, bn = params
+    n = slim.SlimNet(w, bn, max_batch=64, dtype="fp32")
+    yield n
+    n.close()
+
+
+@pytest.mark.parametrize("tup", [(1.0, 1.0, 1.0, 1.0), (0.25, 0.25, 0.25, 0.25), (1.0, 0.75, 0.5, 0.25),
+                                 (0.5, 0.25, 1.0, 0.75)])
+def test_fp32_chain_parity(net32, ref, tup):
+    """FP32 storage + FFMA accumulation (SIMT kernels, no TF32): <= 1e-4 per image (north_star)."""
+    x = synth.make_images(9, offset=19)
+    got = net32.forward_chain(_dev(x, torch.float32), tup).cpu().numpy()
+    _check(got, ref.chain(x, tup), TAU_FP32, f"fp32 chain {tup}")
+
+
+@pytest.mark.parametrize("seg,r_prev,r", [(0, None, 0.75), (1, 0.25, 1.0), (2, 1.0, 0.5), (3, 0.5, 0.25)])
+def test_fp32_segment_parity(net32, ref, seg, r_prev, r):
+    x = _seg_input(seg, r_prev if r_prev else 0.25, 5, 20)
+    got = net32.forward(seg, _dev(x, torch.float32), r_prev if seg else r, r).cpu().numpy()
+    _check(got, ref.segment(seg, x, r_prev, r), TAU_FP32, f"fp32 seg{seg}")
+
+
+# ------------------------------------------------------------------ request stream (CFG4)
+def test_stream_executor_matches_per_request_chain(net):
+    """Mixed-width stream: key batching per segment + gather/scatter; each request's logits are
+    bitwise the chain of its own tuple (batch independence makes grouping invisible)."""
+    from paper_2510_09018_b200.stream import StreamExecutor
+    from paper_2510_09018_b200.router import TABLE_TUPLES
+    rng = np.random.default_rng(21)
+    n = 61
+    tup = np.asarray([TABLE_TUPLES[i] for i in rng.integers(0, len(TABLE_TUPLES), n)], np.float32)
+    x = synth.make_images(n, offset=21)
+    ex = StreamExecutor(net, n_max=64, B_max=8)
+    got = ex.run(_dev(x), tup).clone()
+    torch.cuda.synchronize()
+    assert max(max(b) for b in ex.last_batches) <= 8
+    for t in set(map(tuple, tup.tolist())):
+        idx = [i for i in range(n) if tuple(tup[i].tolist()) == t]
+        ref_l = net.forward_chain(_dev(x[idx]), t)
+        assert torch.equal(got[idx], ref_l), t
