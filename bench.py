@@ -23,7 +23,6 @@ from __future__ import annotations
 import argparse
 import json
 import os
-import statistics
 import sys
 import time
 
@@ -143,16 +142,25 @@ def run_ours(args):
           for i, r in enumerate(WIDTHS)}
     logits = {r: torch.empty(B, 100, dtype=torch.float32, device=dev) for r in WIDTHS}
     wsb = max(slim.slim_chain_workspace_bytes(net.ctx, (r,) * 4, B) for r in WIDTHS)
-    ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
+    # one workspace and one stream per width instance: the four (segment-chain, width)
+    # instances of a step serve their batches concurrently (Alg. 1 runs every loaded
+    # instance independently); --sequential runs them one after another
+    wss = {r: torch.empty(wsb, dtype=torch.uint8, device=dev) for r in WIDTHS}
+    streams = {r: (stream if args.sequential else torch.cuda.Stream(device=dev)) for r in WIDTHS}
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
     telem = TelemetryExchange(device=dev) if world > 1 else None
 
-    def chain(r):
-        slim.slim_forward_chain(net.ctx, (r,) * 4, B, xs[r], logits[r], ws, wsb, stream)
+    def chain(r, st=None):
+        slim.slim_forward_chain(net.ctx, (r,) * 4, B, xs[r], logits[r], wss[r], wsb, st if st is not None else streams[r])
 
     def step():
+        fork = torch.cuda.Event()
+        fork.record(stream)
         for r in WIDTHS:
+            streams[r].wait_event(fork)
             chain(r)
+        for r in WIDTHS:
+            stream.wait_stream(streams[r])
 
     for _ in range(args.warmup):
         flush.zero_()
@@ -164,8 +172,6 @@ def run_ours(args):
     # ---------------- timed region
     K = args.steps
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
-    evw = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in WIDTHS]
-           for _ in range(K)]
     sampler = NvmlSampler(local)
     if world > 1:
         dist.barrier()
@@ -176,10 +182,7 @@ def run_ours(args):
     for k in range(K):
         flush.zero_()
         ev[k][0].record(stream)
-        for i, r in enumerate(WIDTHS):
-            evw[k][i][0].record(stream)
-            chain(r)
-            evw[k][i][1].record(stream)
+        step()
         ev[k][1].record(stream)
         if telem:
             telem.tick(pack_record(rank=rank, completed=(k + 1) * B * len(WIDTHS)))
@@ -191,23 +194,36 @@ def run_ours(args):
     launches = slim.slim_launch_count(net.ctx) - launches0
     step_ms = [a.elapsed_time(b) for a, b in ev]
     total_ms = sum(step_ms)
-    width_ms = [sum(evw[k][i][0].elapsed_time(evw[k][i][1]) for k in range(K)) for i in range(len(WIDTHS))]
     t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_max_ms = float(t.item())
     imgs_per_step = B * len(WIDTHS)
     value = world * imgs_per_step * K / (total_max_ms / 1e3)
-    per_width = {str(r): B * K / (width_ms[i] / 1e3) for i, r in enumerate(WIDTHS)}
     clocks = sampler.summary()
     energy = ((e1 - e0) / 1e3 / (imgs_per_step * K)) if (e0 is not None and e1 is not None) else None
+
+    # ---------------- per-width images/s: each width's chain alone (L2 flushed before it)
+    KW = max(1, min(K, args.profile_steps * 4))
+    width_ms = []
+    for r in WIDTHS:
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(KW)]
+        for k in range(KW):
+            flush.zero_()
+            evs[k][0].record(stream)
+            chain(r, stream)
+            evs[k][1].record(stream)
+        torch.cuda.synchronize()
+        width_ms.append(sum(x.elapsed_time(y) for x, y in evs))
+    per_width = {str(r): B * KW / (width_ms[i] / 1e3) for i, r in enumerate(WIDTHS)}
 
     # ---------------- profiled replay (per-launch CUDA events, no graph) for the roofline object
     KP = min(K, args.profile_steps)
     slim.slim_profile_begin(net.ctx, KP * 80 + 16)
     for _ in range(KP):
         flush.zero_()
-        step()
+        for r in WIDTHS:
+            chain(r, stream)
     recs = slim.slim_profile_end(net.ctx)
     peaks = _peaks()
     by_kind = {}
@@ -249,10 +265,12 @@ def run_ours(args):
     t0 = time.perf_counter()
     for _ in range(KE):
         for r in WIDTHS:
-            xs[r].copy_(xh[r], non_blocking=True)
-            chain(r)
-            lh[r].copy_(logits[r], non_blocking=True)
-        stream.synchronize()
+            with torch.cuda.stream(streams[r]):
+                xs[r].copy_(xh[r], non_blocking=True)
+                chain(r)
+                lh[r].copy_(logits[r], non_blocking=True)
+        for r in WIDTHS:
+            streams[r].synchronize()
     e2e_s = time.perf_counter() - t0
     te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
     if world > 1:
@@ -269,9 +287,11 @@ def run_ours(args):
                                    "r in {0.25,0.5,0.75,1.0}, batch 128 per width, 1 step = 4 x 128 images",
                        "batch": B, "image": [32, 32, 3], "widths": list(WIDTHS),
                        "parallelism": f"dp{world} (independent per-GPU batches)",
-                       "l2": "flushed (256 MiB write) before every timed step", "graphs": not args.no_graph},
+                       "l2": "flushed (256 MiB write) before every timed step", "graphs": not args.no_graph,
+                       "instances": "sequential" if args.sequential else
+                                    "4 width instances, one CUDA stream each, run concurrently"},
             "per_width_images_per_s": per_width,
-            "per_width_ms_per_batch": {str(r): width_ms[i] / K for i, r in enumerate(WIDTHS)},
+            "per_width_ms_per_batch": {str(r): width_ms[i] / KW for i, r in enumerate(WIDTHS)},
             "roofline": roof,
             "kernel_time_by_kind_ms_per_step": {k: v["ms"] / KP for k, v in by_kind.items()},
             "gpu_launches": launches,
@@ -460,6 +480,7 @@ def main(argv=None):
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--batch", type=int, default=128)
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--sequential", action="store_true", help="run the 4 width instances one after another")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--profile-steps", type=int, default=50)

@@ -450,6 +450,20 @@ slim_status conv_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, int ri
         a.m_tiles = (B + a.tile_imgs - 1) / a.tile_imgs;
     }
     a.n_tile = pick_n_tile(c_out, a.m_tiles, ctx->num_sms);
+    // shared memory must hold >= 2 pipeline stages next to the staging tile, the residual
+    // ring and the BN vectors: narrow the N tile (to a smaller 64-multiple) until it does
+    for (;;) {
+        const uint32_t nch = static_cast<uint32_t>((a.n_tile + kChunk - 1) / kChunk);
+        const size_t chk = static_cast<size_t>(nch) * 16384;
+        const int nres = cc.epi == EPI_BN_ADD_RELU ? (nch <= 2 ? 2 : 1) : 0;
+        const size_t need = 1024 + chk * (1 + nres) + 16 * static_cast<size_t>(c_out) + 8 * (2 * kMaxStages + 8) + 16 +
+                            2 * (kTileABytes + static_cast<size_t>(a.n_tile) * 128);
+        if (need <= 226 * 1024) break;
+        int nt2 = c_out / a.n_tile + 1;
+        while (nt2 <= c_out / 64 && (c_out % nt2 || (c_out / nt2) % 64)) ++nt2;
+        if (nt2 > c_out / 64) return fail(ctx, SLIM_EUNSUPPORTED, "conv: no N tile fits shared memory");
+        a.n_tile = c_out / nt2;
+    }
     a.n_tiles = c_out / a.n_tile;
     a.c_out = c_out;
     a.n_parts = (cc.epi == EPI_BN_PROJ_RELU) ? 2 : 1;
