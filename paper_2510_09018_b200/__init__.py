@@ -24,7 +24,7 @@ __all__ = [
     "manifest", "LIB_PATH",
 ]
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libslim.so")
+LIB_PATH = os.environ.get("SLIM_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libslim.so")
 
 SLIM_OK, SLIM_EINVAL, SLIM_ENOTLOADED, SLIM_ENOMEM, SLIM_ECUDA, SLIM_EUNSUPPORTED = 0, -1, -2, -3, -4, -5
 SLIM_BF16, SLIM_FP32 = 0, 1

@@ -30,13 +30,18 @@ namespace {
 
 constexpr int kHaloThreads = 384;   // warps 0 A, 1 MMA, 2 B, 3 idle, 4..11 epilogue
 
+// kNarrow: runtime channel-chunk geometry (16/32-channel boxes); false folds 64-channel / 128-B rows.
+template <bool kNarrow>
 __global__ void __launch_bounds__(kHaloThreads, 1)
     conv_halo_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmRes, const __grid_constant__ CUtensorMap tmOut,
                      const HaloArgs a) {
     extern __shared__ uint8_t smem_raw[];
+    const int CK = kNarrow ? CK : kChunk, RBK = kNarrow ? RBK : 128;
+    const int CO_CHUNK = kNarrow ? CO_CHUNK : kChunk, RBO = kNarrow ? RBO : 128;
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    const uint32_t chunk_bytes = a.n_out_chunks * 16384u;
+    const uint32_t oc_bytes = 128u * RBO;
+    const uint32_t chunk_bytes = a.n_out_chunks * oc_bytes;
     const int n_res = (a.epi == EPI_BN_ADD_RELU) ? a.res_slots : 0;
     const uint32_t sA = smem_u32(smem);
     const uint32_t sB = sA + a.sa * a.a_bytes;
@@ -98,9 +103,10 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
     // weight-stationary B does not depend on the previous kernel: start it before the PDL wait
     __syncthreads();
     if (a.stationary && warp == 2 && lane == 0) {
-        mbar_expect_tx(b_full(0), a.b_bytes);
-        const uint32_t per_chunk = 9u * a.n_tile * 128u;
-        for (int ch = 0; ch < a.n_chunks; ++ch) tma_load_3d(sB + ch * per_chunk, &tmB, b_full(0), ch * kChunk, 0, 0);
+        // exact box bytes (the slot itself is rounded up to 1 KiB)
+        mbar_expect_tx(b_full(0), static_cast<uint32_t>(a.n_chunks) * 9u * a.n_tile * RBK);
+        const uint32_t per_chunk = 9u * a.n_tile * RBK;
+        for (int ch = 0; ch < a.n_chunks; ++ch) tma_load_3d(sB + ch * per_chunk, &tmB, b_full(0), ch * CK, 0, 0);
     }
     tc_fence_before();
     __syncthreads();
@@ -125,7 +131,7 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
                     mbar_wait(a_empty(s), ph ^ 1);
                     if (ch == 0) TD(0, ti, 2);
                     mbar_expect_tx(a_full(s), a.a_bytes);
-                    tma_load_4d(sA + s * a.a_bytes, &tmA, a_full(s), ch * kChunk, 0, h0 - 1, n);
+                    tma_load_4d(sA + s * a.a_bytes, &tmA, a_full(s), ch * CK, 0, h0 - 1, n);
                     if (++s == a.sa) {
                         s = 0;
                         ph ^= 1;
@@ -150,7 +156,7 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
                 } else {
                     mbar_expect_tx(r_full(rs), chunk_bytes);
                     for (uint32_t j = 0; j < a.n_out_chunks; ++j)
-                        tma_load_4d(sRes + rs * chunk_bytes + j * 16384u, &tmRes, r_full(rs), co0 + j * kChunk, 0, h0, n);
+                        tma_load_4d(sRes + rs * chunk_bytes + j * oc_bytes, &tmRes, r_full(rs), co0 + j * CO_CHUNK, 0, h0, n);
                 }
                 if (++rs == n_res) {
                     rs = 0;
@@ -168,8 +174,8 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
                 for (int ch = 0; ch < a.n_chunks; ++ch)
                     for (int kh = 0; kh < 3; ++kh) {
                         mbar_wait(b_empty(s), ph ^ 1);
-                        mbar_expect_tx(b_full(s), a.b_bytes);
-                        tma_load_3d(sB + s * a.b_bytes, &tmB, b_full(s), ch * kChunk, co0, kh * 3);
+                        mbar_expect_tx(b_full(s), 3u * a.n_tile * RBK);
+                        tma_load_3d(sB + s * a.b_bytes, &tmB, b_full(s), ch * CK, co0, kh * 3);
                         if (++s == a.sb) {
                             s = 0;
                             ph ^= 1;
@@ -185,9 +191,10 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
         // tools/ubench) instead of tensor/smem-bound (~48 cycles at N=64).
         {   // the whole warp runs the loop (uniform operands); one elected lane issues
             const uint32_t idesc = umma_idesc_bf16(kTileM, a.n_tile);
-            const uint32_t tap16 = static_cast<uint32_t>(a.n_tile) * 8u;      // n_tile*128 B in 16-B units
-            const uint32_t row16 = static_cast<uint32_t>(a.W) * 8u;           // one halo row (W pixels x 128 B)
-            const uint64_t adesc0 = umma_desc_sw128(sA), bdesc0 = umma_desc_sw128(sB);
+            const uint32_t tap16 = static_cast<uint32_t>(a.n_tile * RBK) >> 4;   // one tap's B tile, 16-B units
+            const uint32_t row16 = static_cast<uint32_t>(a.W * RBK) >> 4;        // one halo row of W pixels
+            const uint64_t adesc0 = umma_desc_kmajor(sA, RBK), bdesc0 = umma_desc_kmajor(sB, RBK);
+            const int kmax = CK >> 4;
             const uint32_t a_slot16 = a.a_bytes >> 4, b_slot16 = a.b_bytes >> 4;
             const uint32_t accs = static_cast<uint32_t>(a.acc_stride);
             int s = 0, bs = 0, as = 0;
@@ -204,7 +211,7 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
                 tc_fence_after();
                 const uint32_t acc = tmem_base + static_cast<uint32_t>(as * 3) * accs;
                 for (int ch = 0; ch < a.n_chunks; ++ch) {
-                    const int nk = min(4, (a.c_in - ch * kChunk + 15) >> 4);
+                    const int nk = min(kmax, (a.c_in - ch * CK + 15) >> 4);
                     mbar_wait(a_full(s), ph);
                     if (ch == 0 && lane == 0) TD(1, ti, 2);
                     tc_fence_after();
@@ -287,10 +294,13 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
         const int q = warp & 3;
         const int half = (warp - kEpiWarp0) >> 2;
         const int row = q * 32 + lane;
+        // TMA swizzle of the staging tile (rbo-byte rows): 16-B piece q of this row lives at q ^ row_x
+        const int co_shift = CO_CHUNK == 16 ? 4 : (CO_CHUNK == 32 ? 5 : 6);
+        const uint32_t row_off = static_cast<uint32_t>(row * RBO);
+        const int row_x = (row >> (RBO == 128 ? 0 : (RBO == 64 ? 1 : 2))) & ((RBO >> 4) - 1);
         const int w = lane % a.W;                  // W divides 32: pixel column of this row
         const bool leader = (warp == kEpiWarp0 && lane == 0);
         const uint32_t lane_addr = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
-        const int sw = row & 7;
         const float *s0 = sBN, *t0 = sBN + a.c_out;
         int as = 0, rs = 0;
         uint32_t aph = 0, rph = 0;
@@ -326,9 +336,9 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
                     if (w < a.W - 1) y += right;
                     f[i] = fmaf(y, s0[cg + i], t0[cg + i]);
                 }
-                const int q16 = (cl & 63) >> 3;
-                const uint32_t off0 = (cl >> 6) * 16384 + row * 128 + (((q16) ^ sw) << 4);
-                const uint32_t off1 = (cl >> 6) * 16384 + row * 128 + (((q16 + 1) ^ sw) << 4);
+                const int oc = cl >> co_shift, q16 = (cl & (CO_CHUNK - 1)) >> 3;
+                const uint32_t off0 = oc * oc_bytes + row_off + ((q16 ^ row_x) << 4);
+                const uint32_t off1 = oc * oc_bytes + row_off + (((q16 + 1) ^ row_x) << 4);
                 if (n_res) {
                     const uint4 r0 = *reinterpret_cast<const uint4 *>(resp + off0);
                     const uint4 r1 = *reinterpret_cast<const uint4 *>(resp + off1);
@@ -359,7 +369,7 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
             if (leader && !(a.debug & 4)) {
                 TD(2, ti, 3);
                 for (uint32_t j = 0; j < a.n_out_chunks; ++j)
-                    tma_store_4d(&tmOut, sOut + j * 16384u, co0 + j * kChunk, 0, h0, n);
+                    tma_store_4d(&tmOut, sOut + j * oc_bytes, co0 + j * CO_CHUNK, 0, h0, n);
                 bulk_commit();
             }
             if (++as == a.acc_stages) {
@@ -385,7 +395,7 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
 }  // namespace
 
 size_t conv_halo_smem_bytes(const HaloArgs &a) {
-    const size_t chunk = static_cast<size_t>(a.n_out_chunks) * 16384;
+    const size_t chunk = static_cast<size_t>(a.n_out_chunks) * 128 * a.rbo;
     const int n_res = (a.epi == EPI_BN_ADD_RELU) ? a.res_slots : 0;
     return 1024 + static_cast<size_t>(a.sa) * a.a_bytes + static_cast<size_t>(a.sb) * a.b_bytes + chunk * (1 + n_res) +
            8 * static_cast<size_t>(a.c_out) + 8 * 24 + 16;
@@ -396,9 +406,12 @@ cudaError_t launch_conv_halo(const HaloArgs &a, const CUtensorMap &tmA, const CU
                              bool pdl) {
     static bool attr_set = false;
     if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(conv_halo_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        if (e != cudaSuccess) return e;
-        cudaFuncSetAttribute(conv_halo_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        for (int m = 0; m < 2; ++m) {
+            auto fn = m ? conv_halo_kernel<true> : conv_halo_kernel<false>;
+            cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+            if (e != cudaSuccess) return e;
+            cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        }
         attr_set = true;
     }
     cudaLaunchConfig_t cfg{};
@@ -411,7 +424,8 @@ cudaError_t launch_conv_halo(const HaloArgs &a, const CUtensorMap &tmA, const CU
     attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, conv_halo_kernel, tmA, tmB, tmRes, tmOut, a);
+    const bool narrow = a.ck != kChunk || a.co_chunk != kChunk;
+    return cudaLaunchKernelEx(&cfg, narrow ? conv_halo_kernel<true> : conv_halo_kernel<false>, tmA, tmB, tmRes, tmOut, a);
 }
 
 }  // namespace slim

@@ -55,6 +55,36 @@ __device__ __forceinline__ TileCoord tile_coord(const ConvArgs &a, int t) {
     return c;
 }
 
+// Tile sequence of this CTA.  mc == 1: tiles blockIdx.x, +gridDim.x, ... over m_tiles x n_tiles.
+// mc > 1: cluster c walks M tiles c, c + n_clusters, ...; CTA rank j of the cluster takes N tiles
+// j, j + mc, ... of that M tile, so all CTAs of a cluster run the same k-block sequence in lockstep.
+struct TileSeq {
+    int start, step, total, rank;
+};
+__device__ __forceinline__ TileSeq tile_seq(const ConvArgs &a, int mc) {
+    TileSeq q;
+    if (mc == 1) {
+        q.start = blockIdx.x;
+        q.step = gridDim.x;
+        q.total = a.m_tiles * a.n_tiles;
+        q.rank = 0;
+    } else {
+        q.rank = static_cast<int>(blockIdx.x) % mc;
+        q.start = static_cast<int>(blockIdx.x) / mc;
+        q.step = static_cast<int>(gridDim.x) / mc;
+        q.total = a.m_tiles * (a.n_tiles / mc);
+    }
+    return q;
+}
+__device__ __forceinline__ int seq_tile(const ConvArgs &a, const TileSeq &q, int v, int mc) {
+    if (mc == 1) return v;
+    const int mt = v % a.m_tiles, nn = v / a.m_tiles;
+    return (nn * mc + q.rank) * a.m_tiles + mt;
+}
+
+// kMode bit 0: cluster multicast of A (a.mc > 1); bit 1: narrow boxes (runtime ck / rbk /
+// co_chunk).  Mode 0 folds every layout constant (64-channel chunks, 128-B rows, no cluster).
+template <int kMode>
 __global__ void __launch_bounds__(kConvThreads, 1)
     conv_umma_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ CUtensorMap tmB0,
                      const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUtensorMap tmB1,
@@ -63,10 +93,15 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     extern __shared__ uint8_t smem_raw[];
     // 1024-byte alignment: SW128 TMA boxes and UMMA descriptors (base_offset = 0)
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    constexpr bool kMC = (kMode & 1) != 0, kNarrow = (kMode & 2) != 0;
+    const int MC = kMC ? a.mc : 1;
+    const int RBO = kNarrow ? a.rbo : 128, CO_CHUNK = kNarrow ? a.co_chunk : kChunk;
+    const uint32_t A_TILE = kNarrow ? a.a_tile_bytes : static_cast<uint32_t>(kTileABytes);
     const int S = a.n_stages;
-    const uint32_t chunk_bytes = a.n_out_chunks * 16384u;   // one 128-pixel x n_tile tile, SW128
+    const uint32_t oc_bytes = 128u * RBO;                  // one staging chunk: 128 pixels x co_chunk
+    const uint32_t chunk_bytes = a.n_out_chunks * oc_bytes;  // one 128-pixel x n_tile tile
     const uint32_t sA = smem_u32(smem);
-    const uint32_t sB = sA + S * kTileABytes;
+    const uint32_t sB = sA + S * A_TILE;
     const uint32_t sOut = sB + S * a.stage_b_bytes;
     const uint32_t sRes = sOut + chunk_bytes;
     const int n_res = (a.epi == EPI_BN_ADD_RELU) ? a.res_slots : 0;
@@ -85,14 +120,15 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * S + 8);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int total = a.m_tiles * a.n_tiles;
+    const TileSeq tq = tile_seq(a, MC);
+    const uint16_t mc_mask = static_cast<uint16_t>((1u << MC) - 1);
     unsigned long long *tr = a.trace ? a.trace + blockIdx.x * 8 : nullptr;
     if (tr && threadIdx.x == 0) tr[0] = gtimer();
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < S; ++i) {
-            mbar_init(full_bar(i), 2);    // A producer + B producer
-            mbar_init(empty_bar(i), 1);
+            mbar_init(full_bar(i), 2);        // A producer + B producer of this CTA
+            mbar_init(empty_bar(i), MC);    // the MMA commit of every CTA of the cluster
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(tfull_bar(i), 1);
@@ -131,6 +167,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     // kernel start its own prologue as SMs free up.
     tc_fence_before();
     __syncthreads();
+    if (kMC) cluster_sync_all();   // every CTA's barriers exist before anyone multicasts into them
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     // (warp 2, the weight producer, does not wait: weights are not produced by the previous kernel,
@@ -146,14 +183,15 @@ __global__ void __launch_bounds__(kConvThreads, 1)
             const bool isA = (warp == 0);
             int stage = 0, rs = 0;
             uint32_t phase = 0, rphase = 0;
-            for (int t = blockIdx.x; t < total; t += gridDim.x) {
-                const TileCoord tc = tile_coord(a, t);
+            uint32_t kb_g = 0;   // k-block counter: the multicast issuer of A rotates over the cluster
+            for (int v = tq.start; v < tq.total; v += tq.step) {
+                const TileCoord tc = tile_coord(a, seq_tile(a, tq, v, MC));
                 if (false && isA && n_res) {   // (residual prefetch runs on warp 3, below)
                     mbar_wait(rempty_bar(rs), rphase ^ 1);
                     if (a.debug & 8) mbar_arrive(rfull_bar(rs));
                     else mbar_expect_tx(rfull_bar(rs), chunk_bytes);
                     for (uint32_t j = 0; j < a.n_out_chunks && !(a.debug & 8); ++j)
-                        tma_load_4d(sRes + rs * chunk_bytes + j * 16384u, &tmRes, rfull_bar(rs), tc.co0 + j * kChunk, 0,
+                        tma_load_4d(sRes + rs * chunk_bytes + j * oc_bytes, &tmRes, rfull_bar(rs), tc.co0 + j * CO_CHUNK, 0,
                                     tc.h0, tc.n0);
                     if (++rs == n_res) {
                         rs = 0;
@@ -162,6 +200,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
                 }
                 for (int p = 0; p < a.n_parts; ++p) {
                     const GemmPart &gp = a.part[p];
+                    const int GP_CK = kNarrow ? gp.ck : kChunk, GP_RBK = kNarrow ? gp.rbk : 128;
                     const CUtensorMap *tA = p ? &tmA1 : &tmA0;
                     const CUtensorMap *tB = p ? &tmB1 : &tmB0;
                     for (int kb = 0; kb < gp.n_kblocks; ++kb) {
@@ -171,17 +210,22 @@ __global__ void __launch_bounds__(kConvThreads, 1)
                         if (a.debug & 1) {
                             mbar_arrive(full_bar(stage));
                         } else if (isA) {
-                            mbar_expect_tx(full_bar(stage), kTileABytes);
-                            tma_load_4d(sA + stage * kTileABytes, tA, full_bar(stage), ch * kChunk, kw - gp.pad,
-                                        tc.h0 * gp.stride + kh - gp.pad, tc.n0);
+                            mbar_expect_tx(full_bar(stage), 128u * GP_RBK);
+                            if (!kMC)
+                                tma_load_4d(sA + stage * A_TILE, tA, full_bar(stage), ch * GP_CK, kw - gp.pad,
+                                            tc.h0 * gp.stride + kh - gp.pad, tc.n0);
+                            else if (static_cast<int>(kb_g % MC) == tq.rank)
+                                tma_load_4d_mc(sA + stage * A_TILE, tA, full_bar(stage), ch * GP_CK, kw - gp.pad,
+                                               tc.h0 * gp.stride + kh - gp.pad, tc.n0, mc_mask);
                         } else {
-                            mbar_expect_tx(full_bar(stage), a.stage_b_bytes);
-                            tma_load_3d(sB + stage * a.stage_b_bytes, tB, full_bar(stage), ch * kChunk, tap, tc.co0);
+                            mbar_expect_tx(full_bar(stage), static_cast<uint32_t>(a.n_tile) * GP_RBK);
+                            tma_load_3d(sB + stage * a.stage_b_bytes, tB, full_bar(stage), ch * GP_CK, tap, tc.co0);
                         }
                         if (++stage == S) {
                             stage = 0;
                             phase ^= 1;
                         }
+                        ++kb_g;
                     }
                 }
             }
@@ -192,15 +236,15 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         if (lane == 0 && n_res) {
             int rs = 0;
             uint32_t rphase = 0;
-            for (int t = blockIdx.x; t < total; t += gridDim.x) {
-                const TileCoord tc = tile_coord(a, t);
+            for (int v = tq.start; v < tq.total; v += tq.step) {
+                const TileCoord tc = tile_coord(a, seq_tile(a, tq, v, MC));
                 mbar_wait(rempty_bar(rs), rphase ^ 1);
                 if (a.debug & 8) {
                     mbar_arrive(rfull_bar(rs));
                 } else {
                     mbar_expect_tx(rfull_bar(rs), chunk_bytes);
                     for (uint32_t j = 0; j < a.n_out_chunks; ++j)
-                        tma_load_4d(sRes + rs * chunk_bytes + j * 16384u, &tmRes, rfull_bar(rs), tc.co0 + j * kChunk, 0,
+                        tma_load_4d(sRes + rs * chunk_bytes + j * oc_bytes, &tmRes, rfull_bar(rs), tc.co0 + j * CO_CHUNK, 0,
                                     tc.h0, tc.n0);
                 }
                 if (++rs == n_res) {
@@ -214,20 +258,22 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         // lean loop: descriptor = base + offset adds, K-steps unrolled (see kernels_halo.cu)
         {   // whole warp runs the loop (uniform operands), one elected lane issues
             const uint32_t idesc = umma_idesc_bf16(kTileM, a.n_tile);
-            const uint64_t adesc0 = umma_desc_sw128(sA), bdesc0 = umma_desc_sw128(sB);
-            const uint32_t a16 = kTileABytes >> 4, b16 = a.stage_b_bytes >> 4;
+            const uint32_t a16 = A_TILE >> 4, b16 = a.stage_b_bytes >> 4;
             int stage = 0, as = 0;
             uint32_t phase = 0, aphase = 0;
-            for (int t = blockIdx.x; t < total; t += gridDim.x) {
+            for (int v = tq.start; v < tq.total; v += tq.step) {
                 mbar_wait(tempty_bar(as), aphase ^ 1);
                 tc_fence_after();
                 for (int p = 0; p < a.n_parts; ++p) {
                     const GemmPart &gp = a.part[p];
+                    const int GP_CK = kNarrow ? gp.ck : kChunk, GP_RBK = kNarrow ? gp.rbk : 128;
                     const uint32_t d = tmem_base + static_cast<uint32_t>((as * a.n_parts + p) * a.acc_stride);
+                    const uint64_t adesc0 = umma_desc_kmajor(sA, GP_RBK), bdesc0 = umma_desc_kmajor(sB, GP_RBK);
+                    const int kmax = GP_CK >> 4;
                     const int nchunks = gp.n_chunks;
                     int ch = 0;
                     for (int kb = 0; kb < gp.n_kblocks; ++kb) {
-                        const int nk = min(4, (gp.c_in - ch * kChunk + 15) >> 4);
+                        const int nk = min(kmax, (gp.c_in - ch * GP_CK + 15) >> 4);
                         mbar_wait(full_bar(stage), phase);
                         tc_fence_after();
                         const uint64_t ad = adesc0 + stage * a16;
@@ -237,7 +283,9 @@ __global__ void __launch_bounds__(kConvThreads, 1)
                             for (int kk = 0; kk < 4; ++kk)   // K=16 per MMA = 32 bytes inside the 128-B atom
                                 if (kk < nk && !(a.debug & 2))
                                     umma_bf16(d, ad + 2 * kk, bd + 2 * kk, idesc, (kb | kk) != 0);
-                            umma_commit(empty_bar(stage));   // frees the smem slot when these MMAs finish
+                            // frees the smem slot (in every CTA of the cluster) when these MMAs finish
+                            if (!kMC) umma_commit(empty_bar(stage));
+                            else umma_commit_mc(empty_bar(stage), mc_mask);
                         }
                         __syncwarp();
                         if (++stage == S) {
@@ -262,16 +310,19 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         const int q = warp & 3;              // TMEM lane quarter this warp may access
         const int half = (warp - kEpiWarp0) >> 2;
         const int row = q * 32 + lane;       // pixel row inside the 128-pixel tile
+        // TMA swizzle of the staging tile (rbo-byte rows): 16-B piece q of this row lives at q ^ row_x
+        const int co_shift = CO_CHUNK == 16 ? 4 : (CO_CHUNK == 32 ? 5 : 6);
+        const uint32_t row_off = static_cast<uint32_t>(row * RBO);
+        const int row_x = (row >> (RBO == 128 ? 0 : (RBO == 64 ? 1 : 2))) & ((RBO >> 4) - 1);
         const bool leader = (warp == kEpiWarp0 && lane == 0);
         const uint32_t lane_addr = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
-        const int sw = row & 7;
         const float *s0 = sBN, *t0 = sBN + a.c_out, *s1 = sBN + 2 * a.c_out, *t1 = sBN + 3 * a.c_out;
         // fused pool: the image of this row and its pixel count P (P divides 32)
         const int P = a.Ho * a.Wo;
         int as = 0, rs = 0;
         uint32_t aphase = 0, rphase = 0;
-        for (int t = blockIdx.x; t < total; t += gridDim.x) {
-            const TileCoord tc = tile_coord(a, t);
+        for (int v = tq.start; v < tq.total; v += tq.step) {
+            const TileCoord tc = tile_coord(a, seq_tile(a, tq, v, MC));
             mbar_wait(tfull_bar(as), aphase);
             tc_fence_after();
             if (!a.pool_out) {
@@ -295,10 +346,10 @@ __global__ void __launch_bounds__(kConvThreads, 1)
 #pragma unroll
                     for (int i = 0; i < 16; ++i) f[i] += fmaf(__uint_as_float(u[i]), s1[cg + i], t1[cg + i]);
                 }
-                // 16-B pieces (cl%64)/8 and +1 of row `row` in chunk cl/64, SW128 swizzled
-                const int q16 = (cl & 63) >> 3;
-                const uint32_t off0 = (cl >> 6) * 16384 + row * 128 + (((q16) ^ sw) << 4);
-                const uint32_t off1 = (cl >> 6) * 16384 + row * 128 + (((q16 + 1) ^ sw) << 4);
+                // 16-B pieces q16 and q16+1 of row `row` in staging chunk cl/co_chunk (TMA-swizzled)
+                const int oc = cl >> co_shift, q16 = (cl & (CO_CHUNK - 1)) >> 3;
+                const uint32_t off0 = oc * oc_bytes + row_off + ((q16 ^ row_x) << 4);
+                const uint32_t off1 = oc * oc_bytes + row_off + (((q16 + 1) ^ row_x) << 4);
                 if (n_res) {
                     const uint4 r0 = *reinterpret_cast<const uint4 *>(resp + off0);
                     const uint4 r1 = *reinterpret_cast<const uint4 *>(resp + off1);
@@ -349,7 +400,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
                 named_bar_sync(1, kEpiThreads);
                 if (leader && !(a.debug & 4)) {
                     for (uint32_t j = 0; j < a.n_out_chunks; ++j)
-                        tma_store_4d(&tmOut, sOut + j * 16384u, tc.co0 + j * kChunk, 0, tc.h0, tc.n0);
+                        tma_store_4d(&tmOut, sOut + j * oc_bytes, tc.co0 + j * CO_CHUNK, 0, tc.h0, tc.n0);
                     bulk_commit();
                 }
             }
@@ -365,6 +416,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
 
     tc_fence_before();
     __syncthreads();
+    if (kMC) cluster_sync_all();   // no CTA leaves while a peer may still multicast into it
     if (warp == 1) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(a.tmem_cols)
@@ -538,9 +590,9 @@ __global__ void __launch_bounds__(kStemThreads)
 }  // namespace
 
 size_t conv_umma_smem_bytes(const ConvArgs &a) {
-    const size_t chunk = static_cast<size_t>(a.n_out_chunks) * 16384;
+    const size_t chunk = static_cast<size_t>(a.n_out_chunks) * 128 * a.rbo;
     const int n_res = (a.epi == EPI_BN_ADD_RELU) ? a.res_slots : 0;
-    return 1024 /*alignment slack*/ + static_cast<size_t>(a.n_stages) * (kTileABytes + a.stage_b_bytes) +
+    return 1024 /*alignment slack*/ + static_cast<size_t>(a.n_stages) * (a.a_tile_bytes + a.stage_b_bytes) +
            chunk * (1 + n_res) + 16 * static_cast<size_t>(a.c_out) + 8 * (2 * a.n_stages + 8) + 16;
 }
 
@@ -552,9 +604,9 @@ int conv_umma_max_ctas_per_sm(size_t smem_bytes) {
     auto it = cache.find(smem_bytes);
     if (it != cache.end()) return it->second;
     int n = 0;
-    cudaFuncSetAttribute(conv_umma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    cudaFuncSetAttribute(conv_umma_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, conv_umma_kernel, kConvThreads, smem_bytes) != cudaSuccess) {
+    cudaFuncSetAttribute(conv_umma_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(conv_umma_kernel<0>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, conv_umma_kernel<0>, kConvThreads, smem_bytes) != cudaSuccess) {
         cudaGetLastError();
         n = 1;
     }
@@ -563,26 +615,49 @@ int conv_umma_max_ctas_per_sm(size_t smem_bytes) {
     return n;
 }
 
+namespace {
+typedef void (*ConvKernelFn)(CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, ConvArgs);
+ConvKernelFn conv_kernel_for(int mode) {
+    switch (mode) {
+        case 1: return conv_umma_kernel<1>;
+        case 2: return conv_umma_kernel<2>;
+        case 3: return conv_umma_kernel<3>;
+        default: return conv_umma_kernel<0>;
+    }
+}
+}  // namespace
+
 cudaError_t launch_conv_umma(const ConvArgs &a, const CUtensorMap &tmA0, const CUtensorMap &tmB0,
                              const CUtensorMap &tmA1, const CUtensorMap &tmB1, const CUtensorMap &tmRes,
                              const CUtensorMap &tmOut, int grid, cudaStream_t stream, bool pdl) {
     static bool attr_set = false;
     if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(conv_umma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        if (e != cudaSuccess) return e;
+        for (int m = 0; m < 4; ++m) {
+            cudaError_t e = cudaFuncSetAttribute(conv_kernel_for(m), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 227 * 1024);
+            if (e != cudaSuccess) return e;
+            cudaFuncSetAttribute(conv_kernel_for(m), cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        }
         attr_set = true;
     }
+    // layout constants fold away in mode 0 (all chunks 64 channels / 128-B rows, no cluster)
+    bool narrow = a.co_chunk != kChunk || a.part[0].ck != kChunk || (a.n_parts > 1 && a.part[1].ck != kChunk);
+    const int mode = (a.mc > 1 ? 1 : 0) | (narrow ? 2 : 0);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(kConvThreads);
     cfg.dynamicSmemBytes = conv_umma_smem_bytes(a);
     cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = a.mc;
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, conv_umma_kernel, tmA0, tmB0, tmA1, tmB1, tmRes, tmOut, a);
+    cfg.numAttrs = a.mc > 1 ? 2 : 1;   // cluster launch only when multicasting
+    return cudaLaunchKernelEx(&cfg, conv_kernel_for(mode), tmA0, tmB0, tmA1, tmB1, tmRes, tmOut, a);
 }
 
 size_t stem_umma_smem_bytes() { return 1024 + 16384 + 8192 + 16384 + 2 * kStemMaxHaloB + 128 * 4 + 16; }

@@ -67,6 +67,29 @@ __device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap *tm,
         "l"(reinterpret_cast<uint64_t>(tm)), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
         : "memory");
 }
+// A box multicast to every CTA of the cluster in cta_mask (same smem / mbarrier offsets).
+__device__ __forceinline__ void tma_load_4d_mc(uint32_t dst, const CUtensorMap *tm, uint32_t bar, int c0, int c1, int c2,
+                                               int c3, uint16_t cta_mask) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.multicast::cluster"
+        " [%0], [%1, {%3, %4, %5, %6}], [%2], %7;" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(tm)), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "h"(cta_mask)
+        : "memory");
+}
+__device__ __forceinline__ void umma_commit_mc(uint32_t bar, uint16_t cta_mask) {
+    asm volatile(
+        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
+        "h"(cta_mask)
+        : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
 __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap *tm, uint32_t bar, int c0, int c1,
                                             int c2) {
     asm volatile(
@@ -173,6 +196,14 @@ __device__ __forceinline__ uint64_t umma_desc_kmajor(uint32_t saddr, int row_byt
     d |= static_cast<uint64_t>(1) << 46;
     d |= layout << 61;
     return d;
+}
+// Byte offset of 16-byte piece q of row `row` in a TMA-swizzled tile with `rb`-byte rows
+// (rb = 32 | 64 | 128 <-> SWIZZLE_32B | 64B | 128B): address bits [4, 4+log2(rb/16)) are
+// XORed with bits [7, ...) of the linear offset.
+__device__ __forceinline__ uint32_t swz_off(int row, int q, int rb) {
+    const int pieces = rb >> 4;                      // 2, 4 or 8 pieces per row
+    const int sh = pieces == 8 ? 0 : (pieces == 4 ? 1 : 2);
+    return static_cast<uint32_t>(row * rb + ((q ^ ((row >> sh) & (pieces - 1))) << 4));
 }
 __device__ __forceinline__ void tmem_ld16_nowait(uint32_t taddr, uint32_t (&v)[16]) { tmem_ld16(taddr, v); }
 

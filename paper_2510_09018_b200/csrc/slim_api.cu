@@ -197,22 +197,33 @@ void clear_graphs(slim_ctx *ctx) {
     ctx->graphs.clear();
 }
 
+CUtensorMapSwizzle swizzle_for(int box_c) {   // box inner bytes = 2*box_c = the swizzle span
+    return box_c == 16 ? CU_TENSOR_MAP_SWIZZLE_32B : (box_c == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B);
+}
+
 bool encode_map(slim_ctx *ctx, CUtensorMap *tm, const void *ptr, int rank, const cuuint64_t *dims,
                 const cuuint64_t *strides, const cuuint32_t *box, const cuuint32_t *es) {
     CUresult r = ctx->encode(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void *>(ptr), dims, strides, box,
-                             es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                             es, CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle_for(static_cast<int>(box[0])),
                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }
 
-// Activation NHWC [B][H][W][C] bf16 as a 4-D map (C, W, H, B); box (64, bw, bh, bn), traversal stride es in H, W.
+// Activation NHWC [B][H][W][C] bf16 as a 4-D map (C, W, H, B); box (box_c, bw, bh, bn), traversal
+// stride es in H, W.  box_c = 16 | 32 | 64 channels selects SWIZZLE_32B | 64B | 128B.
 bool encode_act(slim_ctx *ctx, CUtensorMap *tm, const void *ptr, int B, int H, int W, int C, int bw, int bh, int bn,
-                int es) {
+                int es, int box_c = kChunk) {
     cuuint64_t dims[4] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)B};
     cuuint64_t strides[3] = {(cuuint64_t)C * 2, (cuuint64_t)W * C * 2, (cuuint64_t)H * W * C * 2};
-    cuuint32_t box[4] = {(cuuint32_t)kChunk, (cuuint32_t)bw, (cuuint32_t)bh, (cuuint32_t)bn};
+    cuuint32_t box[4] = {(cuuint32_t)box_c, (cuuint32_t)bw, (cuuint32_t)bh, (cuuint32_t)bn};
     cuuint32_t est[4] = {1, (cuuint32_t)es, (cuuint32_t)es, 1};
     return encode_map(ctx, tm, ptr, 4, dims, strides, box, est);
+}
+
+// channels per operand chunk: exact narrow boxes for 16 / 32 channels, else 64 (128-B rows)
+int chunk_ch(int c) {
+    static const bool wide = getenv("SLIM_WIDE_BOX") != nullptr;   // diagnostics: always 64-channel boxes
+    return (!wide && (c == 16 || c == 32)) ? c : kChunk;
 }
 
 // Weights KRSC [Cout_full][k*k][Cin_full] bf16 as a 3-D map whose BOUNDS are the
@@ -221,7 +232,7 @@ bool encode_w(slim_ctx *ctx, CUtensorMap *tm, const DevLayer &L, int c_in, int c
     const int kk = L.sh.k * L.sh.k;
     cuuint64_t dims[3] = {(cuuint64_t)c_in, (cuuint64_t)kk, (cuuint64_t)c_out};
     cuuint64_t strides[2] = {(cuuint64_t)L.sh.cin * 2, (cuuint64_t)kk * L.sh.cin * 2};
-    cuuint32_t box[3] = {(cuuint32_t)kChunk, 1, (cuuint32_t)n_tile};
+    cuuint32_t box[3] = {(cuuint32_t)chunk_ch(c_in), 1, (cuuint32_t)n_tile};
     cuuint32_t est[3] = {1, 1, 1};
     return encode_map(ctx, tm, L.w, 3, dims, strides, box, est);
 }
@@ -232,10 +243,11 @@ bool encode_w(slim_ctx *ctx, CUtensorMap *tm, const DevLayer &L, int c_in, int c
 // several N tiles each must be a multiple of 64 channels.
 // Weights as a 3-D map (ci, co, tap) -- strides co: 9*Cin_full*2, tap: Cin_full*2 -- so a box
 // [64, n_tile, taps] lands as `taps` consecutive K-major n_tile x 64 operand tiles.
-bool encode_w_taps(slim_ctx *ctx, CUtensorMap *tm, const DevLayer &L, int c_in, int c_out, int n_tile, int taps) {
+bool encode_w_taps(slim_ctx *ctx, CUtensorMap *tm, const DevLayer &L, int c_in, int c_out, int n_tile, int taps,
+                   int box_c) {
     cuuint64_t dims[3] = {(cuuint64_t)c_in, (cuuint64_t)c_out, 9};
     cuuint64_t strides[2] = {(cuuint64_t)9 * L.sh.cin * 2, (cuuint64_t)L.sh.cin * 2};
-    cuuint32_t box[3] = {(cuuint32_t)kChunk, (cuuint32_t)n_tile, (cuuint32_t)taps};
+    cuuint32_t box[3] = {(cuuint32_t)box_c, (cuuint32_t)n_tile, (cuuint32_t)taps};
     cuuint32_t est[3] = {1, 1, 1};
     return encode_map(ctx, tm, L.w, 3, dims, strides, box, est);
 }
@@ -333,7 +345,14 @@ slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, i
     a.n_tiles = nt;
     a.c_out = c_out;
     a.c_in = cc.c_in;
-    a.n_chunks = (cc.c_in + kChunk - 1) / kChunk;
+    // 64-channel boxes unless SLIM_HALO_NARROW (16/32-channel boxes measured no faster here)
+    static const bool halo_narrow = getenv("SLIM_HALO_NARROW") != nullptr;
+    auto hch = [&](int ch) { return halo_narrow ? chunk_ch(ch) : kChunk; };
+    a.ck = hch(cc.c_in);
+    a.rbk = 2 * a.ck;
+    a.n_chunks = (cc.c_in + a.ck - 1) / a.ck;
+    a.co_chunk = hch(a.n_tile);
+    a.rbo = 2 * a.co_chunk;
     a.epi = cc.epi;
     a.scale = L.scale[ri];
     a.shift = L.shift[ri];
@@ -342,21 +361,26 @@ slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, i
     int cols = a.acc_stages * 3 * a.acc_stride, tc = 32;
     while (tc < cols) tc <<= 1;
     a.tmem_cols = tc;
-    a.a_bytes = static_cast<uint32_t>(kTileM + 2 * W) * 128u;
-    a.n_out_chunks = static_cast<uint32_t>((a.n_tile + kChunk - 1) / kChunk);
-    const size_t chunk = static_cast<size_t>(a.n_out_chunks) * 16384;
-    const size_t budget = 226 * 1024;
+    a.a_bytes = static_cast<uint32_t>(kTileM + 2 * W) * a.rbk;
+    a.n_out_chunks = static_cast<uint32_t>((a.n_tile + a.co_chunk - 1) / a.co_chunk);
+    const size_t chunk = static_cast<size_t>(a.n_out_chunks) * 128 * a.rbo;
+    // narrow layers (exact 16/32-channel boxes): two CTAs per SM (smem and 2x256 TMEM columns fit)
+    // (two CTAs per SM for narrow layers measured slower: SLIM_HALO_TWO=1 to try)
+    static const bool two_cta = getenv("SLIM_HALO_TWO") != nullptr;
+    const bool two = two_cta && a.n_tile <= 32 && a.ck <= 32;
+    const size_t budget = two ? 110 * 1024 : 226 * 1024;
     const size_t fixed0 = 1024 + chunk + 8 * static_cast<size_t>(c_out) + 8 * 24 + 16;
-    const uint32_t all_w = static_cast<uint32_t>(a.n_chunks) * 9u * a.n_tile * 128u;
+    auto r1k = [](uint32_t x) { return (x + 1023u) & ~1023u; };
+    const uint32_t all_w = r1k(static_cast<uint32_t>(a.n_chunks) * 9u * a.n_tile * a.rbk);
     a.res_slots = (cc.epi == EPI_BN_ADD_RELU) ? 2 : 0;
     a.stationary = (nt == 1 && all_w <= 100 * 1024) ? 1 : 0;
     if (a.stationary) {
         a.b_bytes = all_w;
         a.sb = 1;
     } else {
-        a.b_bytes = 3u * a.n_tile * 128u;
+        a.b_bytes = r1k(3u * a.n_tile * a.rbk);
     }
-    // fit: A slots 2..3, B slots 2..4 (streaming), residual slots 2 -> 1 if tight
+    // fit: A slots 2..4, B slots 2..4 (streaming), residual slots 2 -> 1 if tight
     for (;;) {
         const size_t res = chunk * a.res_slots;
         size_t left = budget - fixed0 - res;
@@ -387,7 +411,7 @@ slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, i
     a.trace = ctx->trace;
 
     CUtensorMap tA, tRes, tOut;
-    if (!encode_act(ctx, &tA, cc.x, B, H, W, cc.c_in, W, a.rows + 2, 1, 1))
+    if (!encode_act(ctx, &tA, cc.x, B, H, W, cc.c_in, W, a.rows + 2, 1, 1, a.ck))
         return fail(ctx, SLIM_ECUDA, "cuTensorMapEncodeTiled(halo A) failed");
     const int taps = a.stationary ? 9 : 3;
     const CUtensorMap *tB;
@@ -396,19 +420,19 @@ slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, i
         bool &ok = L.tmh_ok[ri][a.n_tile / 16 - 1][a.stationary];
         CUtensorMap &m = L.tmh[ri][a.n_tile / 16 - 1][a.stationary];
         if (!ok) {
-            if (!encode_w_taps(ctx, &m, L, cc.c_in, c_out, a.n_tile, taps))
+            if (!encode_w_taps(ctx, &m, L, cc.c_in, c_out, a.n_tile, taps, a.ck))
                 return fail(ctx, SLIM_ECUDA, "cuTensorMapEncodeTiled(halo W) failed");
             ok = true;
         }
         tB = &m;
     }
-    if (!encode_act(ctx, &tOut, cc.out, B, H, W, c_out, W, a.rows, 1, 1))
+    if (!encode_act(ctx, &tOut, cc.out, B, H, W, c_out, W, a.rows, 1, 1, a.co_chunk))
         return fail(ctx, SLIM_ECUDA, "cuTensorMapEncodeTiled(halo out) failed");
     tRes = tOut;
-    if (cc.epi == EPI_BN_ADD_RELU && !encode_act(ctx, &tRes, cc.res, B, H, W, c_out, W, a.rows, 1, 1))
+    if (cc.epi == EPI_BN_ADD_RELU && !encode_act(ctx, &tRes, cc.res, B, H, W, c_out, W, a.rows, 1, 1, a.co_chunk))
         return fail(ctx, SLIM_ECUDA, "cuTensorMapEncodeTiled(halo res) failed");
     const int total = a.m_tiles * a.n_tiles;
-    int grid = ctx->num_sms;
+    int grid = ctx->num_sms * (two ? 2 : 1);
     if (grid > total) grid = total;
     double flops, bytes;
     conv_work(c, cc, ri, B, H, W, &flops, &bytes);
@@ -453,8 +477,9 @@ slim_status conv_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, int ri
     // shared memory must hold >= 2 pipeline stages next to the staging tile, the residual
     // ring and the BN vectors: narrow the N tile (to a smaller 64-multiple) until it does
     for (;;) {
-        const uint32_t nch = static_cast<uint32_t>((a.n_tile + kChunk - 1) / kChunk);
-        const size_t chk = static_cast<size_t>(nch) * 16384;
+        const int coc = chunk_ch(a.n_tile);
+        const uint32_t nch = static_cast<uint32_t>((a.n_tile + coc - 1) / coc);
+        const size_t chk = static_cast<size_t>(nch) * 128 * 2 * coc;
         const int nres = cc.epi == EPI_BN_ADD_RELU ? (nch <= 2 ? 2 : 1) : 0;
         const size_t need = 1024 + chk * (1 + nres) + 16 * static_cast<size_t>(c_out) + 8 * (2 * kMaxStages + 8) + 16 +
                             2 * (kTileABytes + static_cast<size_t>(a.n_tile) * 128);
@@ -467,10 +492,14 @@ slim_status conv_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, int ri
     a.n_tiles = c_out / a.n_tile;
     a.c_out = c_out;
     a.n_parts = (cc.epi == EPI_BN_PROJ_RELU) ? 2 : 1;
-    a.part[0] = GemmPart{k, s, pad, cc.c_in, (cc.c_in + kChunk - 1) / kChunk, 0};
+    {
+        const int ck0 = chunk_ch(cc.c_in);
+        a.part[0] = GemmPart{k, s, pad, cc.c_in, ck0, 2 * ck0, (cc.c_in + ck0 - 1) / ck0, 0};
+    }
     a.part[0].n_kblocks = k * k * a.part[0].n_chunks;
     if (a.n_parts == 2) {
-        a.part[1] = GemmPart{cc.Lp->sh.k, cc.Lp->sh.stride, 0, cc.c_in_p, (cc.c_in_p + kChunk - 1) / kChunk, 0};
+        const int ck1 = chunk_ch(cc.c_in_p);
+        a.part[1] = GemmPart{cc.Lp->sh.k, cc.Lp->sh.stride, 0, cc.c_in_p, ck1, 2 * ck1, (cc.c_in_p + ck1 - 1) / ck1, 0};
         a.part[1].n_kblocks = a.part[1].n_chunks;
     }
     a.epi = cc.epi;
@@ -488,8 +517,14 @@ slim_status conv_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, int ri
     int cols = a.acc_stages * a.n_parts * a.acc_stride, tc = 32;
     while (tc < cols) tc <<= 1;
     a.tmem_cols = tc;
-    a.stage_b_bytes = static_cast<uint32_t>(a.n_tile) * 128;
-    a.n_out_chunks = static_cast<uint32_t>((a.n_tile + kChunk - 1) / kChunk);
+    {
+        const int rbk = a.n_parts == 2 ? (a.part[0].rbk > a.part[1].rbk ? a.part[0].rbk : a.part[1].rbk) : a.part[0].rbk;
+        a.a_tile_bytes = static_cast<uint32_t>(kTileM) * rbk;
+        a.stage_b_bytes = (static_cast<uint32_t>(a.n_tile) * rbk + 1023u) & ~1023u;
+    }
+    a.co_chunk = chunk_ch(a.n_tile);
+    a.rbo = 2 * a.co_chunk;
+    a.n_out_chunks = static_cast<uint32_t>((a.n_tile + a.co_chunk - 1) / a.co_chunk);
     a.res_slots = a.n_out_chunks <= 2 ? 2 : 1;
     a.pool_out = cc.pool_out;
     if (a.pool_out && (P > 32 || 32 % P || (a.tile_imgs == 1 && P != kTileM)))
@@ -498,14 +533,14 @@ slim_status conv_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, int ri
     // in what the staging / residual ring / BN vectors leave
     const bool two = a.n_tile <= 32;
     const size_t budget = two ? 113 * 1024 : 226 * 1024;
-    const size_t chunk = static_cast<size_t>(a.n_out_chunks) * 16384;
+    const size_t chunk = static_cast<size_t>(a.n_out_chunks) * 128 * a.rbo;
     const size_t fixed = 1024 + chunk * (1 + (cc.epi == EPI_BN_ADD_RELU ? a.res_slots : 0)) +
                          16 * static_cast<size_t>(c_out) + 8 * (2 * kMaxStages + 8) + 16;
-    int stages = static_cast<int>((budget - fixed) / (kTileABytes + a.stage_b_bytes));
+    int stages = static_cast<int>((budget - fixed) / (a.a_tile_bytes + a.stage_b_bytes));
     a.n_stages = stages < 2 ? 2 : (stages > kMaxStages ? kMaxStages : stages);
 
     CUtensorMap tA0, tA1, tRes, tOut;
-    if (!encode_act(ctx, &tA0, cc.x, B, cc.H, cc.W, cc.c_in, s * Wo, s * a.tile_rows, a.tile_imgs, s))
+    if (!encode_act(ctx, &tA0, cc.x, B, cc.H, cc.W, cc.c_in, s * Wo, s * a.tile_rows, a.tile_imgs, s, a.part[0].ck))
         return fail(ctx, SLIM_ECUDA, "cuTensorMapEncodeTiled(A) failed");
     const CUtensorMap *tB0 = weight_map(ctx, L, cc.ri_in, ri, cc.c_in, c_out, a.n_tile);
     const CUtensorMap *tB1 = tB0;
@@ -513,16 +548,18 @@ slim_status conv_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, int ri
     tA1 = tA0;
     if (a.n_parts == 2) {
         const int sp = cc.Lp->sh.stride;
-        if (!encode_act(ctx, &tA1, cc.xp, B, cc.Hp, cc.Wp, cc.c_in_p, sp * Wo, sp * a.tile_rows, a.tile_imgs, sp))
+        if (!encode_act(ctx, &tA1, cc.xp, B, cc.Hp, cc.Wp, cc.c_in_p, sp * Wo, sp * a.tile_rows, a.tile_imgs, sp,
+                        a.part[1].ck))
             return fail(ctx, SLIM_ECUDA, "cuTensorMapEncodeTiled(A1) failed");
         tB1 = weight_map(ctx, *cc.Lp, cc.ri_in_p, ri, cc.c_in_p, c_out, a.n_tile);
         if (!tB1) return fail(ctx, SLIM_ECUDA, "cuTensorMapEncodeTiled(W1) failed");
     }
-    if (!encode_act(ctx, &tOut, cc.pool_out ? cc.x : cc.out, B, Ho, Wo, c_out, Wo, a.tile_rows, a.tile_imgs, 1))
+    if (!encode_act(ctx, &tOut, cc.pool_out ? cc.x : cc.out, B, Ho, Wo, c_out, Wo, a.tile_rows, a.tile_imgs, 1,
+                    a.co_chunk))
         return fail(ctx, SLIM_ECUDA, "cuTensorMapEncodeTiled(out) failed");
     tRes = tOut;
     if (cc.epi == EPI_BN_ADD_RELU &&
-        !encode_act(ctx, &tRes, cc.res, B, Ho, Wo, c_out, Wo, a.tile_rows, a.tile_imgs, 1))
+        !encode_act(ctx, &tRes, cc.res, B, Ho, Wo, c_out, Wo, a.tile_rows, a.tile_imgs, 1, a.co_chunk))
         return fail(ctx, SLIM_ECUDA, "cuTensorMapEncodeTiled(res) failed");
 
     const size_t smem = conv_umma_smem_bytes(a);
@@ -530,14 +567,31 @@ slim_status conv_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, int ri
     const int total = a.m_tiles * a.n_tiles;
     int grid = ctx->num_sms * per_sm;
     if (grid > total) grid = total;
+    // A-tile multicast: a cluster of mc CTAs (<= 8, dividing n_tiles) shares each M tile
+    static const bool no_mc = getenv("SLIM_NO_MC") != nullptr;
+    a.mc = 1;
+    static const int mc_max = getenv("SLIM_MC_MAX") ? atoi(getenv("SLIM_MC_MAX")) : 1;   // multicast measured slower
+    if (!no_mc && a.n_tiles > 1 && per_sm == 1) {
+        for (int m = mc_max; m >= 2; --m)
+            if (a.n_tiles % m == 0) {
+                a.mc = m;
+                break;
+            }
+    }
+    if (a.mc > 1) {
+        const int vt = a.m_tiles * (a.n_tiles / a.mc);
+        int nclusters = ctx->num_sms / a.mc;
+        if (nclusters > vt) nclusters = vt;
+        grid = nclusters * a.mc;
+    }
     double flops, bytes;
     conv_work(c, cc, ri, B, Ho, Wo, &flops, &bytes);
     LaunchProf prof(ctx, st);
     cudaError_t e = launch_conv_umma(a, tA0, *tB0, tA1, *tB1, tRes, tOut, grid, st, ctx->pdl && !ctx->prof_on);
     prof.done(SLIM_K_CONV_UMMA, cc.seg, cc.layer, c.widths[cc.ri_in], c.widths[ri], B, flops, bytes);
     if (e != cudaSuccess)
-        return fail(ctx, SLIM_ECUDA, "conv_umma launch (grid %d, smem %zu, n_tile %d, stages %d): %s", grid, smem,
-                    a.n_tile, a.n_stages, cudaGetErrorString(e));
+        return fail(ctx, SLIM_ECUDA, "conv_umma launch (grid %d, cluster %d, smem %zu, n_tile %d, stages %d): %s", grid,
+                    a.mc, smem, a.n_tile, a.n_stages, cudaGetErrorString(e));
     return SLIM_OK;
 }
 

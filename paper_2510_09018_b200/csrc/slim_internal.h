@@ -29,7 +29,9 @@ enum EpiMode : int {
 struct GemmPart {          // one GEMM accumulated into one TMEM accumulator
     int ksize, stride, pad;
     int c_in;              // active input channels (TMA bound: channels >= c_in read as 0)
-    int n_chunks;          // ceil(c_in / 64)
+    int ck;                // channels per K-block chunk: 16 | 32 (exact narrow boxes) | 64
+    int rbk;               // operand row bytes = 2*ck = the swizzle span (32 | 64 | 128 B)
+    int n_chunks;          // ceil(c_in / ck)
     int n_kblocks;         // ksize*ksize*n_chunks
 };
 
@@ -42,9 +44,14 @@ struct ConvArgs {
     int epi;
     const float *scale0, *shift0, *scale1, *shift1;   // folded BN of the two accumulators
     int n_stages, acc_stages, acc_stride, tmem_cols;
-    uint32_t stage_b_bytes;   // n_tile * 128
-    uint32_t n_out_chunks;    // ceil(n_tile / 64) staging buffers of 16 KiB
+    uint32_t a_tile_bytes;    // 128 * max part rbk (one A stage)
+    uint32_t stage_b_bytes;   // n_tile * max part rbk, rounded up to 1 KiB
+    int co_chunk, rbo;        // output channels per staging chunk (16 | 32 | 64) and its row bytes
+    uint32_t n_out_chunks;    // ceil(n_tile / co_chunk) staging chunks of 128*rbo bytes
     int res_slots;            // residual prefetch ring depth (EPI_BN_ADD_RELU), 1 or 2
+    int mc;                   // cluster size along N (1 = no cluster): the mc CTAs of a cluster compute the
+                              // same M tile for different N tiles; each k-block's A box is loaded once and
+                              // TMA-multicast to all of them
     // fused global-average-pool (last conv of the network): instead of storing the
     // [B,Ho,Wo,c_out] tile, average each image's Ho*Wo rows and write fp32 pooled[B][c_out]
     float *pool_out;          // nullptr = normal store
@@ -64,6 +71,8 @@ struct HaloArgs {
     int stationary;           // all weights resident in smem (one B slot of n_chunks*9 taps)
     int sa, sb;               // A ring slots (one per chunk), B ring slots (one per (chunk, kh)) -- each <= 4
     int acc_stride, acc_stages, tmem_cols;
+    int ck, rbk;              // input channels per chunk (16 | 32 | 64) and operand row bytes
+    int co_chunk, rbo;        // output channels per staging chunk and its row bytes
     uint32_t a_bytes, b_bytes;
     uint32_t n_out_chunks;
     int res_slots;

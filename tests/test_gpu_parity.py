@@ -318,3 +318,23 @@ def test_stream_executor_matches_per_request_chain(net):
         idx = [i for i in range(n) if tuple(tup[i].tolist()) == t]
         ref_l = net.forward_chain(_dev(x[idx]), t)
         assert torch.equal(got[idx], ref_l), t
+
+
+def test_cluster_multicast_path_parity(params, ref):
+    """The A-tile multicast variant (cluster of CTAs sharing an M tile; off by default, SLIM_MC_MAX)
+    computes the same results: run it through a subprocess with the env var set."""
+    import subprocess, sys, os
+    code = (
+        "import numpy as np, torch, synth, oracle, paper_2510_09018_b200 as slim\n"
+        "w, bn = synth.make_weights(), synth.make_bn()\n"
+        "net = slim.SlimNet(w, bn, max_batch=64)\n"
+        "x = synth.make_images(40, offset=23)\n"
+        "got = net.forward_chain(torch.from_numpy(x).to(torch.bfloat16).cuda(), (1.0, 1.0, 1.0, 1.0)).cpu().numpy()\n"
+        "err = oracle.per_image_rel_err(got[:4], oracle.Model(w, bn).chain(x[:4], (1.0,) * 4))\n"
+        "print(err.max())\n"
+    )
+    env = dict(os.environ, SLIM_MC_MAX="4")
+    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300,
+                         cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert float(out.stdout.strip().splitlines()[-1]) <= TAU_BF16
