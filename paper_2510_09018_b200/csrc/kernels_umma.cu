@@ -123,11 +123,14 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     const TileSeq tq = tile_seq(a, MC);
     const uint16_t mc_mask = static_cast<uint16_t>((1u << MC) - 1);
     unsigned long long *tr = a.trace ? a.trace + blockIdx.x * 8 : nullptr;
+    // aggregate wait times per CTA (register accumulators, one store per role at the end)
+    unsigned long long *tw = a.trace ? a.trace + 2048 + blockIdx.x * 8 : nullptr;
+    unsigned long long acc_w0 = 0, acc_w1 = 0;
     if (tr && threadIdx.x == 0) tr[0] = gtimer();
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < S; ++i) {
-            mbar_init(full_bar(i), 2);        // A producer + B producer of this CTA
+            mbar_init(full_bar(i), 1);        // the owning producer's arrive.expect_tx (A + B bytes)
             mbar_init(empty_bar(i), MC);    // the MMA commit of every CTA of the cluster
         }
         for (int i = 0; i < 2; ++i) {
@@ -170,56 +173,50 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     if (kMC) cluster_sync_all();   // every CTA's barriers exist before anyone multicasts into them
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
-    // (warp 2, the weight producer, does not wait: weights are not produced by the previous kernel,
-    // so its first TMA loads overlap the previous kernel's tail)
-    if (warp != 2) asm volatile("griddepcontrol.wait;" ::: "memory");
+    // (every producer loads activations, so every warp waits -- griddepcontrol.wait is per thread)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (tr && threadIdx.x == 0) tr[1] = gtimer();
 
-    if (warp == 0 || warp == 2) {
-        // ============ TMA producers: warp 0 = residual + A (activations), warp 2 = B (weights) ============
-        // (two issuing threads: one thread caps at ~28-48 B/cycle/SM of TMA traffic, tools/ubench)
-        if (lane == 0) {
-            const bool isA = (warp == 0);
-            int stage = 0, rs = 0;
-            uint32_t phase = 0, rphase = 0;
-            uint32_t kb_g = 0;   // k-block counter: the multicast issuer of A rotates over the cluster
+    if (warp == 0 || warp == 2 || warp == 12 || warp == 13) {
+        // ============ TMA producers: n_prod warps, k-block kb owned by warp kb % n_prod ============
+        // One thread issues at most ~1 TMA per ~500 cycles (tools/ubench: throughput scales with
+        // issuing threads, not box bytes), so A+B loads are spread over up to four issuing warps.
+        const int pi = warp == 0 ? 0 : (warp == 2 ? 1 : (warp == 12 ? 2 : 3));
+        if (lane == 0 && pi < a.n_prod) {
+            int stage = 0;
+            uint32_t phase = 0;
+            uint32_t kb_g = 0;   // k-block counter: producer ownership and the multicast issuer rotate on it
             for (int v = tq.start; v < tq.total; v += tq.step) {
                 const TileCoord tc = tile_coord(a, seq_tile(a, tq, v, MC));
-                if (false && isA && n_res) {   // (residual prefetch runs on warp 3, below)
-                    mbar_wait(rempty_bar(rs), rphase ^ 1);
-                    if (a.debug & 8) mbar_arrive(rfull_bar(rs));
-                    else mbar_expect_tx(rfull_bar(rs), chunk_bytes);
-                    for (uint32_t j = 0; j < a.n_out_chunks && !(a.debug & 8); ++j)
-                        tma_load_4d(sRes + rs * chunk_bytes + j * oc_bytes, &tmRes, rfull_bar(rs), tc.co0 + j * CO_CHUNK, 0,
-                                    tc.h0, tc.n0);
-                    if (++rs == n_res) {
-                        rs = 0;
-                        rphase ^= 1;
-                    }
-                }
                 for (int p = 0; p < a.n_parts; ++p) {
                     const GemmPart &gp = a.part[p];
                     const int GP_CK = kNarrow ? gp.ck : kChunk, GP_RBK = kNarrow ? gp.rbk : 128;
                     const CUtensorMap *tA = p ? &tmA1 : &tmA0;
                     const CUtensorMap *tB = p ? &tmB1 : &tmB0;
                     for (int kb = 0; kb < gp.n_kblocks; ++kb) {
-                        const int tap = kb / gp.n_chunks, ch = kb - tap * gp.n_chunks;
-                        const int kh = tap / gp.ksize, kw = tap - kh * gp.ksize;
-                        mbar_wait(empty_bar(stage), phase ^ 1);
-                        if (a.debug & 1) {
-                            mbar_arrive(full_bar(stage));
-                        } else if (isA) {
-                            mbar_expect_tx(full_bar(stage), 128u * GP_RBK);
-                            if (!kMC)
-                                tma_load_4d(sA + stage * A_TILE, tA, full_bar(stage), ch * GP_CK, kw - gp.pad,
-                                            tc.h0 * gp.stride + kh - gp.pad, tc.n0);
-                            else if (static_cast<int>(kb_g % MC) == tq.rank)
-                                tma_load_4d_mc(sA + stage * A_TILE, tA, full_bar(stage), ch * GP_CK, kw - gp.pad,
-                                               tc.h0 * gp.stride + kh - gp.pad, tc.n0, mc_mask);
-                        } else {
-                            mbar_expect_tx(full_bar(stage), static_cast<uint32_t>(a.n_tile) * GP_RBK);
-                            tma_load_3d(sB + stage * a.stage_b_bytes, tB, full_bar(stage), ch * GP_CK, tap, tc.co0);
+                        if (static_cast<int>(kb_g % a.n_prod) == pi) {
+                            const int tap = kb / gp.n_chunks, ch = kb - tap * gp.n_chunks;
+                            const int kh = tap / gp.ksize, kw = tap - kh * gp.ksize;
+                            {
+                                const unsigned long long w0 = tw ? gtimer() : 0;
+                                mbar_wait(empty_bar(stage), phase ^ 1);
+                                if (tw) acc_w0 += gtimer() - w0;
+                            }
+                            if (a.debug & 1) {
+                                mbar_arrive(full_bar(stage));
+                            } else {
+                                const uint32_t b_bytes = static_cast<uint32_t>(a.n_tile) * GP_RBK;
+                                mbar_expect_tx(full_bar(stage), 128u * GP_RBK + b_bytes);
+                                const int ah = tc.h0 * gp.stride + kh - gp.pad;
+                                if (!kMC)
+                                    tma_load_4d(sA + stage * A_TILE, tA, full_bar(stage), ch * GP_CK, kw - gp.pad, ah,
+                                                tc.n0);
+                                else if (static_cast<int>(kb_g % MC) == tq.rank)
+                                    tma_load_4d_mc(sA + stage * A_TILE, tA, full_bar(stage), ch * GP_CK, kw - gp.pad, ah,
+                                                   tc.n0, mc_mask);
+                                tma_load_3d(sB + stage * a.stage_b_bytes, tB, full_bar(stage), ch * GP_CK, tap, tc.co0);
+                            }
                         }
                         if (++stage == S) {
                             stage = 0;
@@ -229,7 +226,8 @@ __global__ void __launch_bounds__(kConvThreads, 1)
                     }
                 }
             }
-            if (tr && isA) tr[2] = gtimer();
+            if (tr && warp == 0) tr[2] = gtimer();
+            if (tw && pi < 2) tw[pi] = acc_w0;
         }
     } else if (warp == 3) {
         // ===================== residual prefetch (own warp: never gates the A/B ring) =========
@@ -262,7 +260,11 @@ __global__ void __launch_bounds__(kConvThreads, 1)
             int stage = 0, as = 0;
             uint32_t phase = 0, aphase = 0;
             for (int v = tq.start; v < tq.total; v += tq.step) {
-                mbar_wait(tempty_bar(as), aphase ^ 1);
+                {
+                    const unsigned long long w0 = tw ? gtimer() : 0;
+                    mbar_wait(tempty_bar(as), aphase ^ 1);
+                    if (tw) acc_w1 += gtimer() - w0;
+                }
                 tc_fence_after();
                 for (int p = 0; p < a.n_parts; ++p) {
                     const GemmPart &gp = a.part[p];
@@ -274,7 +276,11 @@ __global__ void __launch_bounds__(kConvThreads, 1)
                     int ch = 0;
                     for (int kb = 0; kb < gp.n_kblocks; ++kb) {
                         const int nk = min(kmax, (gp.c_in - ch * GP_CK + 15) >> 4);
-                        mbar_wait(full_bar(stage), phase);
+                        {
+                            const unsigned long long w0 = tw ? gtimer() : 0;
+                            mbar_wait(full_bar(stage), phase);
+                            if (tw) acc_w0 += gtimer() - w0;
+                        }
                         tc_fence_after();
                         const uint64_t ad = adesc0 + stage * a16;
                         const uint64_t bd = bdesc0 + stage * b16;
@@ -303,8 +309,12 @@ __global__ void __launch_bounds__(kConvThreads, 1)
                 }
             }
             if (tr && lane == 0) tr[3] = gtimer();
+            if (tw && lane == 0) {
+                tw[2] = acc_w0;
+                tw[3] = acc_w1;
+            }
         }
-    } else if (warp >= kEpiWarp0) {
+    } else if (warp >= kEpiWarp0 && warp < kEpiWarp0 + 8) {
         // ===================== epilogue (warps 4..11) ========================
         // two warps per TMEM lane quarter; warp half h takes column groups h, h+2, ...
         const int q = warp & 3;              // TMEM lane quarter this warp may access
@@ -323,7 +333,11 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         uint32_t aphase = 0, rphase = 0;
         for (int v = tq.start; v < tq.total; v += tq.step) {
             const TileCoord tc = tile_coord(a, seq_tile(a, tq, v, MC));
-            mbar_wait(tfull_bar(as), aphase);
+            {
+                const unsigned long long w0 = tw ? gtimer() : 0;
+                mbar_wait(tfull_bar(as), aphase);
+                if (tw) acc_w0 += gtimer() - w0;
+            }
             tc_fence_after();
             if (!a.pool_out) {
                 if (leader) bulk_wait_read0();   // previous tile's stores have left the staging buffer
@@ -410,6 +424,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
             }
         }
         if (tr && leader) tr[4] = gtimer();
+        if (tw && leader) tw[4] = acc_w0;
         if (leader) bulk_wait0();
         if (tr && leader) tr[5] = gtimer();
     }

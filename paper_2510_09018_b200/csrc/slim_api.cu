@@ -436,6 +436,7 @@ slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, i
     if (grid > total) grid = total;
     double flops, bytes;
     conv_work(c, cc, ri, B, H, W, &flops, &bytes);
+    if (ctx->trace) cudaMemsetAsync(ctx->trace, 0, 4096 * 8 * sizeof(unsigned long long), st);   // diagnostics
     LaunchProf prof(ctx, st);
     cudaError_t e = launch_conv_halo(a, tA, *tB, tRes, tOut, grid, st, ctx->pdl && !ctx->prof_on);
     prof.done(SLIM_K_CONV_UMMA, cc.seg, cc.layer, c.widths[cc.ri_in], c.widths[ri], B, flops, bytes);
@@ -539,8 +540,16 @@ slim_status conv_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, int ri
     int stages = static_cast<int>((budget - fixed) / (a.a_tile_bytes + a.stage_b_bytes));
     a.n_stages = stages < 2 ? 2 : (stages > kMaxStages ? kMaxStages : stages);
 
+    // TMA issue is bounded per issuing thread (~1 instruction per ~500 cycles), so up to four
+    // producer warps take turns by k-block
+    static const int nprod = getenv("SLIM_NPROD") ? atoi(getenv("SLIM_NPROD")) : 3;
+    a.n_prod = nprod < 1 ? 1 : (nprod > 4 ? 4 : nprod);
+    // producers take k-blocks round-robin and each checks its stage's empty barrier by parity:
+    // with n_stages >= n_prod a producer is never two phases ahead on a stage (no parity aliasing)
+    if (a.n_prod > a.n_stages) a.n_prod = a.n_stages;
+    const int box_rows = a.tile_rows, box_imgs = a.tile_imgs;
     CUtensorMap tA0, tA1, tRes, tOut;
-    if (!encode_act(ctx, &tA0, cc.x, B, cc.H, cc.W, cc.c_in, s * Wo, s * a.tile_rows, a.tile_imgs, s, a.part[0].ck))
+    if (!encode_act(ctx, &tA0, cc.x, B, cc.H, cc.W, cc.c_in, s * Wo, s * box_rows, box_imgs, s, a.part[0].ck))
         return fail(ctx, SLIM_ECUDA, "cuTensorMapEncodeTiled(A) failed");
     const CUtensorMap *tB0 = weight_map(ctx, L, cc.ri_in, ri, cc.c_in, c_out, a.n_tile);
     const CUtensorMap *tB1 = tB0;
@@ -548,7 +557,7 @@ slim_status conv_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, int ri
     tA1 = tA0;
     if (a.n_parts == 2) {
         const int sp = cc.Lp->sh.stride;
-        if (!encode_act(ctx, &tA1, cc.xp, B, cc.Hp, cc.Wp, cc.c_in_p, sp * Wo, sp * a.tile_rows, a.tile_imgs, sp,
+        if (!encode_act(ctx, &tA1, cc.xp, B, cc.Hp, cc.Wp, cc.c_in_p, sp * Wo, sp * box_rows, box_imgs, sp,
                         a.part[1].ck))
             return fail(ctx, SLIM_ECUDA, "cuTensorMapEncodeTiled(A1) failed");
         tB1 = weight_map(ctx, *cc.Lp, cc.ri_in_p, ri, cc.c_in_p, c_out, a.n_tile);
@@ -586,6 +595,7 @@ slim_status conv_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, int ri
     }
     double flops, bytes;
     conv_work(c, cc, ri, B, Ho, Wo, &flops, &bytes);
+    if (ctx->trace) cudaMemsetAsync(ctx->trace, 0, 4096 * 8 * sizeof(unsigned long long), st);   // diagnostics
     LaunchProf prof(ctx, st);
     cudaError_t e = launch_conv_umma(a, tA0, *tB0, tA1, *tB1, tRes, tOut, grid, st, ctx->pdl && !ctx->prof_on);
     prof.done(SLIM_K_CONV_UMMA, cc.seg, cc.layer, c.widths[cc.ri_in], c.widths[ri], B, flops, bytes);

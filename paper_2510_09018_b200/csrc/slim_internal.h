@@ -15,7 +15,8 @@ namespace slim {
 constexpr int kTileM = 128;        // UMMA M (cta_group::1): TMEM lane = tile row
 constexpr int kChunk = 64;         // channels per K-block = one 128-byte SW128 row
 constexpr int kTileABytes = kTileM * kChunk * 2;   // 16 KiB A operand per K-block
-constexpr int kConvThreads = 384;  // warp0 A-TMA, warp1 MMA (+TMEM alloc), warp2 B-TMA, warps4-11 epilogue
+constexpr int kConvThreads = 448;  // warps 0,2,12,13 TMA producers, warp1 MMA (+TMEM alloc), warp3 residual TMA,
+                                   // warps4-11 epilogue
 constexpr int kMaxStages = 8;
 constexpr int kEpiWarp0 = 4;       // first epilogue warp (warp 3 idles)
 constexpr int kEpiThreads = 256;   // 8 epilogue warps, two per TMEM lane quarter
@@ -49,6 +50,7 @@ struct ConvArgs {
     int co_chunk, rbo;        // output channels per staging chunk (16 | 32 | 64) and its row bytes
     uint32_t n_out_chunks;    // ceil(n_tile / co_chunk) staging chunks of 128*rbo bytes
     int res_slots;            // residual prefetch ring depth (EPI_BN_ADD_RELU), 1 or 2
+    int n_prod;               // TMA producer warps (1..4); k-block kb is loaded by producer kb % n_prod
     int mc;                   // cluster size along N (1 = no cluster): the mc CTAs of a cluster compute the
                               // same M tile for different N tiles; each k-block's A box is loaded once and
                               // TMA-multicast to all of them

@@ -49,3 +49,9 @@ if d.any():
                     row.append(f"{labels[role][pt]}={(v - t0) / 1e3:6.2f}")
         if row:
             print(f"tile {ti}: " + " ".join(row))
+w = buf[2048:2048 + 148 * 8].astype(np.int64).reshape(148, 8)
+w = w[w[:, 2] > 0]
+if len(w):
+    med = np.median(w, axis=0) / 1e3
+    print(f"median per-CTA waits (us): A-prod empty {med[0]:.2f}  B-prod empty {med[1]:.2f}  MMA full {med[2]:.2f}  "
+          f"MMA tmem-empty {med[3]:.2f}  epi t_full {med[4]:.2f}  (n={len(w)})")
