@@ -37,8 +37,8 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
                      const __grid_constant__ CUtensorMap tmRes, const __grid_constant__ CUtensorMap tmOut,
                      const HaloArgs a) {
     extern __shared__ uint8_t smem_raw[];
-    const int CK = kNarrow ? CK : kChunk, RBK = kNarrow ? RBK : 128;
-    const int CO_CHUNK = kNarrow ? CO_CHUNK : kChunk, RBO = kNarrow ? RBO : 128;
+    const int CK = kNarrow ? a.ck : kChunk, RBK = kNarrow ? a.rbk : 128;
+    const int CO_CHUNK = kNarrow ? a.co_chunk : kChunk, RBO = kNarrow ? a.rbo : 128;
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const uint32_t oc_bytes = 128u * RBO;
     const uint32_t chunk_bytes = a.n_out_chunks * oc_bytes;
@@ -46,7 +46,8 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
     const uint32_t sA = smem_u32(smem);
     const uint32_t sB = sA + a.sa * a.a_bytes;
     const uint32_t sOut = sB + a.sb * a.b_bytes;
-    const uint32_t sRes = sOut + chunk_bytes;
+    const int n_grp = a.epi_groups;
+    const uint32_t sRes = sOut + n_grp * chunk_bytes;
     uint8_t *pOut = smem + (sOut - sA);
     uint8_t *pRes = smem + (sRes - sA);
     float *sBN = reinterpret_cast<float *>(pRes + n_res * chunk_bytes);
@@ -80,9 +81,9 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(t_full(i), 1);
-            mbar_init(t_empty(i), kEpiThreads);
+            mbar_init(t_empty(i), kEpiThreads / n_grp);
             mbar_init(r_full(i), 1);
-            mbar_init(r_empty(i), kEpiThreads);
+            mbar_init(r_empty(i), kEpiThreads / n_grp);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         prefetch_tmap(&tmA);
@@ -190,7 +191,10 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
         // a single issuing thread is otherwise instruction-bound (~120 cycles per MMA,
         // tools/ubench) instead of tensor/smem-bound (~48 cycles at N=64).
         {   // the whole warp runs the loop (uniform operands); one elected lane issues
-            const uint32_t idesc = umma_idesc_bf16(kTileM, a.n_tile);
+            // kw_fuse taps per MMA: N = kw_fuse * n_tile covers adjacent accumulators / B tap blocks
+            const int kf = a.kw_fuse;
+            const uint32_t idesc = umma_idesc_bf16(kTileM, a.n_tile * kf);
+            const uint32_t idesc_r = umma_idesc_bf16(kTileM, a.n_tile * (kf == 2 ? 1 : kf));
             const uint32_t tap16 = static_cast<uint32_t>(a.n_tile * RBK) >> 4;   // one tap's B tile, 16-B units
             const uint32_t row16 = static_cast<uint32_t>(a.W * RBK) >> 4;        // one halo row of W pixels
             const uint64_t adesc0 = umma_desc_kmajor(sA, RBK), bdesc0 = umma_desc_kmajor(sB, RBK);
@@ -209,7 +213,7 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
                 mbar_wait(t_empty(as), aph ^ 1);
                 if (lane == 0) TD(1, ti, 1);
                 tc_fence_after();
-                const uint32_t acc = tmem_base + static_cast<uint32_t>(as * 3) * accs;
+                const uint32_t acc = tmem_base + static_cast<uint32_t>(as * a.stage_cols);
                 for (int ch = 0; ch < a.n_chunks; ++ch) {
                     const int nk = min(kmax, (a.c_in - ch * CK + 15) >> 4);
                     mbar_wait(a_full(s), ph);
@@ -221,7 +225,23 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
                         // one elected issue block for the whole chunk (27 or 36 MMAs, no waits inside)
                         const uint64_t bch = bdesc0 + static_cast<uint32_t>(ch * 9) * tap16;
                         if (elect_one() && !(a.debug & 2)) {
-                            if (nk == 4) {
+                            if (kf == 3) {
+                                // one MMA per (kh, k-step) writes all three kw accumulators
+#pragma unroll
+                                for (int kh = 0; kh < 3; ++kh)
+                                    for (int kk = 0; kk < nk; ++kk)
+                                        umma_bf16(acc, ad + kh * row16 + 2 * kk, bch + (kh * 3) * tap16 + 2 * kk, idesc,
+                                                  (ch | kh | kk) != 0);
+                            } else if (kf == 2) {
+#pragma unroll
+                                for (int kh = 0; kh < 3; ++kh)
+                                    for (int kk = 0; kk < nk; ++kk) {
+                                        umma_bf16(acc, ad + kh * row16 + 2 * kk, bch + (kh * 3) * tap16 + 2 * kk, idesc,
+                                                  (ch | kh | kk) != 0);
+                                        umma_bf16(acc + 2 * accs, ad + kh * row16 + 2 * kk,
+                                                  bch + (kh * 3 + 2) * tap16 + 2 * kk, idesc_r, (ch | kh | kk) != 0);
+                                    }
+                            } else if (nk == 4) {
 #pragma unroll
                                 for (int kh = 0; kh < 3; ++kh)
 #pragma unroll
@@ -251,12 +271,12 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
                             if (elect_one()) {
                                 if (!(a.debug & 2)) {
 #pragma unroll
-                                    for (int kw = 0; kw < 3; ++kw)
+                                    for (int kw = 0; kw < 3; kw += kf)
 #pragma unroll
                                         for (int kk = 0; kk < 4; ++kk)
                                             if (kk < nk)
-                                                umma_bf16(acc + kw * accs, adk + 2 * kk, bd + kw * tap16 + 2 * kk, idesc,
-                                                          (ch | kh | kk) != 0);
+                                                umma_bf16(acc + kw * accs, adk + 2 * kk, bd + kw * tap16 + 2 * kk,
+                                                          kw ? idesc_r : idesc, (ch | kh | kk) != 0);
                                 }
                                 umma_commit(b_empty(bs));
                             }
@@ -291,50 +311,61 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
         }
     } else if (warp >= kEpiWarp0) {
         // ===================== epilogue (warps 4..11, two per TMEM lane quarter) ====
+        // n_grp == 2: warps 4-7 take the even tiles, 8-11 the odd ones (accumulator stage,
+        // residual slot, staging buffer and named barrier of their own), so two tiles'
+        // epilogues overlap; n_grp == 1: the two halves split the columns of every tile.
         const int q = warp & 3;
         const int half = (warp - kEpiWarp0) >> 2;
+        const int grp = n_grp == 2 ? half : 0;
+        const int g0 = n_grp == 2 ? 0 : half, gstep = n_grp == 2 ? 1 : 2;
+        const int gthreads = kEpiThreads / n_grp;
         const int row = q * 32 + lane;
         // TMA swizzle of the staging tile (rbo-byte rows): 16-B piece q of this row lives at q ^ row_x
         const int co_shift = CO_CHUNK == 16 ? 4 : (CO_CHUNK == 32 ? 5 : 6);
         const uint32_t row_off = static_cast<uint32_t>(row * RBO);
         const int row_x = (row >> (RBO == 128 ? 0 : (RBO == 64 ? 1 : 2))) & ((RBO >> 4) - 1);
         const int w = lane % a.W;                  // W divides 32: pixel column of this row
-        const bool leader = (warp == kEpiWarp0 && lane == 0);
+        const bool leader = (warp == kEpiWarp0 + 4 * grp && lane == 0);
         const uint32_t lane_addr = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
         const float *s0 = sBN, *t0 = sBN + a.c_out;
-        int as = 0, rs = 0;
-        uint32_t aph = 0, rph = 0;
-        for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        const uint32_t sOutG = sOut + grp * chunk_bytes;
+        uint8_t *pOutG = pOut + grp * chunk_bytes;
+        for (int t = blockIdx.x + grp * gridDim.x; t < total; t += n_grp * gridDim.x) {
             const int mt = t % a.m_tiles, nt = t / a.m_tiles;
             const int n = mt / tiles_per_img, h0 = (mt - n * tiles_per_img) * a.rows, co0 = nt * a.n_tile;
             const int ti = (t - blockIdx.x) / gridDim.x;
+            const int as = ti % a.acc_stages, rs = n_res ? ti % n_res : 0;
+            const uint32_t aph = (ti / a.acc_stages) & 1, rph = n_res ? (ti / n_res) & 1 : 0;
             mbar_wait(t_full(as), aph);
             if (leader) TD(2, ti, 0);
             tc_fence_after();
-            if (leader) bulk_wait_read0();
+            if (leader) bulk_wait_read0();   // this group's previous store has left the staging tile
             if (leader) TD(2, ti, 1);
-            named_bar_sync(1, kEpiThreads);
+            named_bar_sync(1 + grp, gthreads);
             if (n_res) mbar_wait(r_full(rs), rph);
             if (leader) TD(2, ti, 2);
             const uint8_t *resp = pRes + rs * chunk_bytes;
-            const uint32_t col0 = static_cast<uint32_t>(as * 3 * a.acc_stride);
-            for (int g = half; g < a.n_tile / 16 && !(a.debug & 16); g += 2) {
-                uint32_t v0[16], v1[16], v2[16];
-                tmem_ld16(lane_addr + col0 + g * 16, v0);
-                tmem_ld16(lane_addr + col0 + a.acc_stride + g * 16, v1);
-                tmem_ld16(lane_addr + col0 + 2 * a.acc_stride + g * 16, v2);
-                tmem_wait_ld();
+            const uint32_t col0 = static_cast<uint32_t>(as * a.stage_cols);
+            const int G = (a.debug & 16) ? 0 : a.n_tile / 16;
+            // one 16-column group: out[w] = acc_0[w-1] + acc_1[w] + acc_2[w+1] (zero padding at the
+            // row ends), BN, residual, ReLU, bf16 into the swizzled staging tile
+            auto process = [&](int g, const uint32_t(&v0)[16], const uint32_t(&v1)[16], const uint32_t(&v2)[16]) {
                 const int cl = g * 16, cg = co0 + cl;
+                float sc[16], sh[16];
+#pragma unroll
+                for (int i = 0; i < 16; i += 4) {
+                    *reinterpret_cast<float4 *>(sc + i) = *reinterpret_cast<const float4 *>(s0 + cg + i);
+                    *reinterpret_cast<float4 *>(sh + i) = *reinterpret_cast<const float4 *>(t0 + cg + i);
+                }
                 float f[16];
 #pragma unroll
                 for (int i = 0; i < 16; ++i) {
-                    // out[w] = acc_0[w-1] + acc_1[w] + acc_2[w+1]  (zero padding at the row ends)
                     const float left = __shfl_up_sync(0xffffffffu, __uint_as_float(v0[i]), 1);
                     const float right = __shfl_down_sync(0xffffffffu, __uint_as_float(v2[i]), 1);
                     float y = __uint_as_float(v1[i]);
                     if (w > 0) y += left;
                     if (w < a.W - 1) y += right;
-                    f[i] = fmaf(y, s0[cg + i], t0[cg + i]);
+                    f[i] = fmaf(y, sc[i], sh[i]);
                 }
                 const int oc = cl >> co_shift, q16 = (cl & (CO_CHUNK - 1)) >> 3;
                 const uint32_t off0 = oc * oc_bytes + row_off + ((q16 ^ row_x) << 4);
@@ -352,29 +383,58 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
                 uint32_t o[8];
 #pragma unroll
                 for (int i = 0; i < 8; ++i) o[i] = pack_bf16(fmaxf(f[2 * i], 0.f), fmaxf(f[2 * i + 1], 0.f));
-                *reinterpret_cast<uint4 *>(pOut + off0) = make_uint4(o[0], o[1], o[2], o[3]);
-                *reinterpret_cast<uint4 *>(pOut + off1) = make_uint4(o[4], o[5], o[6], o[7]);
-            }
-            tc_fence_before();
-            mbar_arrive(t_empty(as));
-            if (n_res) {
-                mbar_arrive(r_empty(rs));
-                if (++rs == n_res) {
-                    rs = 0;
-                    rph ^= 1;
+                *reinterpret_cast<uint4 *>(pOutG + off0) = make_uint4(o[0], o[1], o[2], o[3]);
+                *reinterpret_cast<uint4 *>(pOutG + off1) = make_uint4(o[4], o[5], o[6], o[7]);
+            };
+            auto load = [&](int g, uint32_t(&v0)[16], uint32_t(&v1)[16], uint32_t(&v2)[16]) {
+                tmem_ld16(lane_addr + col0 + g * 16, v0);
+                tmem_ld16(lane_addr + col0 + a.acc_stride + g * 16, v1);
+                tmem_ld16(lane_addr + col0 + 2 * a.acc_stride + g * 16, v2);
+            };
+            // software pipeline over column groups: the TMEM loads of group g+1 are in flight while
+            // group g is computed; the accumulator stage is released as soon as its last load landed
+            bool released = false;
+            auto landed = [&](int gn, uint32_t(&v0)[16], uint32_t(&v1)[16], uint32_t(&v2)[16]) {
+                tmem_wait_ld();
+                reg_fence16(v0);
+                reg_fence16(v1);
+                reg_fence16(v2);
+                if (gn >= G) {
+                    tc_fence_before();
+                    mbar_arrive(t_empty(as));
+                    released = true;
+                }
+            };
+            {
+                uint32_t a0[16], a1[16], a2[16], b0[16], b1[16], b2[16];
+                int g = g0;
+                if (g < G) load(g, a0, a1, a2);
+                while (g < G) {
+                    int gn = g + gstep;
+                    landed(gn, a0, a1, a2);
+                    if (gn < G) load(gn, b0, b1, b2);
+                    process(g, a0, a1, a2);
+                    g = gn;
+                    if (g >= G) break;
+                    gn = g + gstep;
+                    landed(gn, b0, b1, b2);
+                    if (gn < G) load(gn, a0, a1, a2);
+                    process(g, b0, b1, b2);
+                    g = gn;
                 }
             }
+            if (!released) {
+                tc_fence_before();
+                mbar_arrive(t_empty(as));
+            }
+            if (n_res) mbar_arrive(r_empty(rs));
             fence_proxy_async();
-            named_bar_sync(1, kEpiThreads);
+            named_bar_sync(1 + grp, gthreads);
             if (leader && !(a.debug & 4)) {
                 TD(2, ti, 3);
                 for (uint32_t j = 0; j < a.n_out_chunks; ++j)
-                    tma_store_4d(&tmOut, sOut + j * oc_bytes, co0 + j * CO_CHUNK, 0, h0, n);
+                    tma_store_4d(&tmOut, sOutG + j * oc_bytes, co0 + j * CO_CHUNK, 0, h0, n);
                 bulk_commit();
-            }
-            if (++as == a.acc_stages) {
-                as = 0;
-                aph ^= 1;
             }
         }
         if (tr && leader) tr[4] = gtimer();
@@ -397,7 +457,8 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
 size_t conv_halo_smem_bytes(const HaloArgs &a) {
     const size_t chunk = static_cast<size_t>(a.n_out_chunks) * 128 * a.rbo;
     const int n_res = (a.epi == EPI_BN_ADD_RELU) ? a.res_slots : 0;
-    return 1024 + static_cast<size_t>(a.sa) * a.a_bytes + static_cast<size_t>(a.sb) * a.b_bytes + chunk * (1 + n_res) +
+    return 1024 + static_cast<size_t>(a.sa) * a.a_bytes + static_cast<size_t>(a.sb) * a.b_bytes +
+           chunk * (a.epi_groups + n_res) +
            8 * static_cast<size_t>(a.c_out) + 8 * 24 + 16;
 }
 

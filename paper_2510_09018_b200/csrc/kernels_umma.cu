@@ -440,168 +440,6 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     if (tr && threadIdx.x == 0) tr[6] = gtimer();
 }
 
-// ============================================================================
-// Stem on tcgen05: conv3x3, c_img (=3) -> c0, + BN + ReLU.
-// K = 9*c_img = 27 is padded to 32 (two K=16 MMAs); the A operand (one im2col
-// row of 27 bf16 values per output pixel) is built in shared memory by the
-// 128 threads from a halo'd input tile (the 6-byte pixel stride of the raw
-// image is not TMA-addressable), B (the c0 x 27 weight slice) is staged once per
-// CTA.  Tile = 128 pixels (tile_rows full image rows); several CTAs per SM.
-// Epilogue as the conv kernel: TMEM -> fp32 BN/ReLU -> bf16 -> SW128 staging -> TMA store.
-constexpr int kStemThreads = 128;
-
-constexpr int kStemMaxHaloB = 6 * 32 * 4 * 2;   // (rows+2) x W x c_img bf16 bytes, rows*W = 128, W <= 32, c_img <= 4
-
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void *src) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
-
-// Halo rows h0-1 .. h0+rows of image n (raw bf16, contiguous in NHWC) -> smem buffer;
-// rows outside the image are zero-filled.  16-byte cp.async, one commit group.
-__device__ __forceinline__ void stem_fetch_halo(const StemArgs &a, uint8_t *buf, int t) {
-    const int tiles_per_img = a.H / a.tile_rows;
-    const int n = t / tiles_per_img, h0 = (t - n * tiles_per_img) * a.tile_rows;
-    const int row_b = a.W * a.cimg * 2;                  // bytes per image row (multiple of 16)
-    const int per_row = row_b / 16;
-    const int total = (a.tile_rows + 2) * per_row;
-    for (int i = threadIdx.x; i < total; i += kStemThreads) {
-        const int r = i / per_row, j = i - r * per_row;
-        const int ih = h0 - 1 + r;
-        uint8_t *dst = buf + r * row_b + j * 16;
-        if (ih >= 0 && ih < a.H)
-            cp_async16(smem_u32(dst), reinterpret_cast<const uint8_t *>(a.in) +
-                                          (static_cast<size_t>(n) * a.H + ih) * row_b + j * 16);
-        else
-            *reinterpret_cast<uint4 *>(dst) = make_uint4(0, 0, 0, 0);
-    }
-    cp_async_commit();
-}
-
-__global__ void __launch_bounds__(kStemThreads)
-    stem_umma_kernel(const __grid_constant__ CUtensorMap tmOut, const StemArgs a) {
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint8_t *sA = smem;                 // 128 rows x 128 B (SW128), K in [0,32) used
-    uint8_t *sB = smem + 16384;         // c0 rows x 128 B (SW128)
-    uint8_t *sOut = sB + 8192;          // 128 rows x 128 B staging (SW128)
-    uint8_t *sIn = sOut + 16384;        // 2 x halo buffers (raw bf16)
-    float *sBN = reinterpret_cast<float *>(sIn + 2 * kStemMaxHaloB);   // scale[64] | shift[64]
-    uint64_t *bar = reinterpret_cast<uint64_t *>(sBN + 128);
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bar + 1);
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int cimg = a.cimg, K = 9 * cimg, W = a.W;
-
-    // zero A and B once (K padding 27..63 stays zero), stage the weight slice as bf16 and the BN vectors
-    for (int i = tid; i < (16384 + 8192) / 16; i += kStemThreads) reinterpret_cast<uint4 *>(sA)[i] = make_uint4(0, 0, 0, 0);
-    __syncthreads();
-    for (int i = tid; i < a.c0 * K; i += kStemThreads) {
-        const int co = i / K, k = i - co * K;
-        const int chunk = k >> 3, swz = (chunk ^ (co & 7)) << 4;
-        *reinterpret_cast<__nv_bfloat16 *>(sB + co * 128 + swz + (k & 7) * 2) =
-            __float2bfloat16_rn(a.w[static_cast<size_t>(co) * a.w_stride + k]);
-    }
-    for (int i = tid; i < a.c0; i += kStemThreads) {
-        sBN[i] = a.scale[i];
-        sBN[64 + i] = a.shift[i];
-    }
-    if (tid == 0) {
-        mbar_init(smem_u32(bar), 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    if (warp == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                     "r"(a.tmem_cols)
-                     : "memory");
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-    }
-    asm volatile("griddepcontrol.wait;" ::: "memory");          // PDL: inputs of the previous kernel are visible
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    fence_proxy_async();
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    const uint32_t tmem = *tmem_slot;
-    const uint32_t idesc = umma_idesc_bf16(kTileM, a.c0);
-    const int q = warp & 3, row = q * 32 + lane, sw = row & 7;
-    const int r_pix = row / W, c_pix = row - r_pix * W;
-    uint32_t phase = 0;
-    int buf = 0;
-    const int tiles_per_img = a.H / a.tile_rows;
-    if (static_cast<int>(blockIdx.x) < a.m_tiles) stem_fetch_halo(a, sIn, blockIdx.x);
-    for (int t = blockIdx.x; t < a.m_tiles; t += gridDim.x) {
-        const int n = t / tiles_per_img, h0 = (t - n * tiles_per_img) * a.tile_rows;
-        // prefetch the next tile's halo into the other buffer, then wait for this one
-        const int tn = t + gridDim.x;
-        if (tn < a.m_tiles) stem_fetch_halo(a, sIn + (buf ^ 1) * kStemMaxHaloB, tn);
-        else cp_async_commit();
-        cp_async_wait1();
-        if (tid == 0) bulk_wait_read0();       // previous tile's TMA store has read the staging buffer
-        __syncthreads();
-        {   // im2col row of pixel `row`: k = (kh*3 + kw)*cimg + ci; zero padding in W by predicate
-            const __nv_bfloat16 *hb = reinterpret_cast<const __nv_bfloat16 *>(sIn + buf * kStemMaxHaloB);
-            uint32_t packed[16];
-#pragma unroll
-            for (int j = 0; j < 16; ++j) packed[j] = 0;
-            for (int k = 0; k < K; ++k) {
-                const int tap = k / cimg, ci = k - tap * cimg, kh = tap / 3, kw = tap - kh * 3;
-                const int col = c_pix + kw - 1;
-                const uint32_t b = (col >= 0 && col < W)
-                                       ? static_cast<uint32_t>(__bfloat16_as_ushort(hb[((r_pix + kh) * W + col) * cimg + ci]))
-                                       : 0u;
-                packed[k >> 1] |= (k & 1) ? (b << 16) : b;
-            }
-#pragma unroll
-            for (int j = 0; j < 4; ++j)   // 16-byte chunks 0..3 hold K = 0..31
-                *reinterpret_cast<uint4 *>(sA + row * 128 + ((j ^ sw) << 4)) =
-                    make_uint4(packed[4 * j], packed[4 * j + 1], packed[4 * j + 2], packed[4 * j + 3]);
-        }
-        buf ^= 1;
-        fence_proxy_async();                   // generic smem writes -> visible to the tensor core
-        tc_fence_before();
-        __syncthreads();
-        if (tid == 0) {
-            tc_fence_after();
-            const uint64_t ad = umma_desc_sw128(smem_u32(sA)), bd = umma_desc_sw128(smem_u32(sB));
-            umma_bf16(tmem, ad, bd, idesc, 0);
-            umma_bf16(tmem, ad + 2, bd + 2, idesc, 1);
-            umma_commit(smem_u32(bar));
-        }
-        mbar_wait(smem_u32(bar), phase);
-        phase ^= 1;
-        tc_fence_after();
-        const uint32_t lane_addr = tmem + (static_cast<uint32_t>(q * 32) << 16);
-        for (int g = 0; g < a.c0 / 16; ++g) {
-            uint32_t v[16];
-            tmem_ld16(lane_addr + g * 16, v);
-            tmem_wait_ld();
-            float f[16];
-#pragma unroll
-            for (int i = 0; i < 16; ++i) f[i] = fmaxf(fmaf(__uint_as_float(v[i]), sBN[g * 16 + i], sBN[64 + g * 16 + i]), 0.f);
-            const int q16 = (g * 16) >> 3;
-            uint8_t *rowp = sOut + row * 128;
-            *reinterpret_cast<uint4 *>(rowp + (((q16) ^ sw) << 4)) =
-                make_uint4(pack_bf16(f[0], f[1]), pack_bf16(f[2], f[3]), pack_bf16(f[4], f[5]), pack_bf16(f[6], f[7]));
-            *reinterpret_cast<uint4 *>(rowp + (((q16 + 1) ^ sw) << 4)) =
-                make_uint4(pack_bf16(f[8], f[9]), pack_bf16(f[10], f[11]), pack_bf16(f[12], f[13]), pack_bf16(f[14], f[15]));
-        }
-        fence_proxy_async();
-        tc_fence_before();
-        __syncthreads();
-        if (tid == 0) {
-            tma_store_4d(&tmOut, smem_u32(sOut), 0, 0, h0, n);
-            bulk_commit();
-        }
-    }
-    if (tid == 0) bulk_wait0();
-    tc_fence_before();
-    __syncthreads();
-    if (warp == 0) {
-        tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(a.tmem_cols) : "memory");
-    }
-}
 }  // namespace
 
 size_t conv_umma_smem_bytes(const ConvArgs &a) {
@@ -673,44 +511,6 @@ cudaError_t launch_conv_umma(const ConvArgs &a, const CUtensorMap &tmA0, const C
     cfg.attrs = attr;
     cfg.numAttrs = a.mc > 1 ? 2 : 1;   // cluster launch only when multicasting
     return cudaLaunchKernelEx(&cfg, conv_kernel_for(mode), tmA0, tmB0, tmA1, tmB1, tmRes, tmOut, a);
-}
-
-size_t stem_umma_smem_bytes() { return 1024 + 16384 + 8192 + 16384 + 2 * kStemMaxHaloB + 128 * 4 + 16; }
-
-cudaError_t launch_stem_umma(const StemArgs &a, const CUtensorMap &tmOut, int grid, cudaStream_t stream, bool pdl) {
-    const size_t smem = stem_umma_smem_bytes();
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(kStemThreads);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, stem_umma_kernel, tmOut, a);
-}
-
-int stem_umma_max_ctas_per_sm() {
-    static int n = -1;
-    if (n < 0) {
-        int v = 0;
-        cudaFuncSetAttribute(stem_umma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-        // the occupancy API otherwise assumes the smallest shared-memory carveout that fits one CTA
-        cudaFuncSetAttribute(stem_umma_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, stem_umma_kernel, kStemThreads,
-                                                                      stem_umma_smem_bytes());
-        if (getenv("SLIM_DEBUG"))
-            fprintf(stderr, "[slim] stem occupancy: %d CTAs/SM (%s), smem %zu\n", v, cudaGetErrorString(e),
-                    stem_umma_smem_bytes());
-        if (e != cudaSuccess) {
-            cudaGetLastError();
-            v = 1;
-        }
-        n = v < 1 ? 1 : (v > 6 ? 6 : v);
-    }
-    return n;
 }
 
 }  // namespace slim

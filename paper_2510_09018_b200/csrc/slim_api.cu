@@ -202,9 +202,10 @@ CUtensorMapSwizzle swizzle_for(int box_c) {   // box inner bytes = 2*box_c = the
 }
 
 bool encode_map(slim_ctx *ctx, CUtensorMap *tm, const void *ptr, int rank, const cuuint64_t *dims,
-                const cuuint64_t *strides, const cuuint32_t *box, const cuuint32_t *es) {
+                const cuuint64_t *strides, const cuuint32_t *box, const cuuint32_t *es, bool swizzle = true) {
     CUresult r = ctx->encode(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void *>(ptr), dims, strides, box,
-                             es, CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle_for(static_cast<int>(box[0])),
+                             es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                             swizzle ? swizzle_for(static_cast<int>(box[0])) : CU_TENSOR_MAP_SWIZZLE_NONE,
                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }
@@ -356,20 +357,27 @@ slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, i
     a.epi = cc.epi;
     a.scale = L.scale[ri];
     a.shift = L.shift[ri];
-    a.acc_stride = (a.n_tile + 31) / 32 * 32;
-    a.acc_stages = 6 * a.acc_stride <= 512 ? 2 : 1;
-    int cols = a.acc_stages * 3 * a.acc_stride, tc = 32;
+    // kw taps share one MMA (N = k*n_tile <= 256, the three accumulators adjacent in TMEM, the
+    // tap blocks of B adjacent in smem) unless SLIM_HALO_NOFUSE
+    static const bool nofuse = getenv("SLIM_HALO_NOFUSE") != nullptr;
+    a.kw_fuse = nofuse ? 1 : (3 * a.n_tile <= 256 ? 3 : (2 * a.n_tile <= 256 ? 2 : 1));
+    a.acc_stride = a.kw_fuse > 1 ? a.n_tile : (a.n_tile + 31) / 32 * 32;
+    a.stage_cols = (3 * a.acc_stride + 31) / 32 * 32;
+    a.acc_stages = 2 * a.stage_cols <= 512 ? 2 : 1;
+    int cols = a.acc_stages * a.stage_cols, tc = 32;
     while (tc < cols) tc <<= 1;
     a.tmem_cols = tc;
     a.a_bytes = static_cast<uint32_t>(kTileM + 2 * W) * a.rbk;
     a.n_out_chunks = static_cast<uint32_t>((a.n_tile + a.co_chunk - 1) / a.co_chunk);
     const size_t chunk = static_cast<size_t>(a.n_out_chunks) * 128 * a.rbo;
+    static const bool one_group = getenv("SLIM_HALO_EPI1") != nullptr;
+    a.epi_groups = (!one_group && a.acc_stages == 2) ? 2 : 1;
     // narrow layers (exact 16/32-channel boxes): two CTAs per SM (smem and 2x256 TMEM columns fit)
     // (two CTAs per SM for narrow layers measured slower: SLIM_HALO_TWO=1 to try)
     static const bool two_cta = getenv("SLIM_HALO_TWO") != nullptr;
     const bool two = two_cta && a.n_tile <= 32 && a.ck <= 32;
     const size_t budget = two ? 110 * 1024 : 226 * 1024;
-    const size_t fixed0 = 1024 + chunk + 8 * static_cast<size_t>(c_out) + 8 * 24 + 16;
+    auto fixed0 = [&]() { return 1024 + chunk * a.epi_groups + 8 * static_cast<size_t>(c_out) + 8 * 24 + 16; };
     auto r1k = [](uint32_t x) { return (x + 1023u) & ~1023u; };
     const uint32_t all_w = r1k(static_cast<uint32_t>(a.n_chunks) * 9u * a.n_tile * a.rbk);
     a.res_slots = (cc.epi == EPI_BN_ADD_RELU) ? 2 : 0;
@@ -383,9 +391,10 @@ slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, i
     // fit: A slots 2..4, B slots 2..4 (streaming), residual slots 2 -> 1 if tight
     for (;;) {
         const size_t res = chunk * a.res_slots;
-        size_t left = budget - fixed0 - res;
+        size_t left = budget - fixed0() - res;
         if (a.stationary) {
             if (left < a.b_bytes + 2 * a.a_bytes) {
+                if (a.epi_groups == 2) { a.epi_groups = 1; continue; }
                 if (a.res_slots == 2) { a.res_slots = 1; continue; }
                 return SLIM_EUNSUPPORTED;
             }
@@ -394,6 +403,7 @@ slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, i
             a.sa = a.sa > 4 ? 4 : a.sa;
         } else {
             if (left < 2 * a.a_bytes + 2 * a.b_bytes) {
+                if (a.epi_groups == 2) { a.epi_groups = 1; continue; }
                 if (a.res_slots == 2) { a.res_slots = 1; continue; }
                 return SLIM_EUNSUPPORTED;
             }
@@ -711,15 +721,24 @@ slim_status run_segment(slim_ctx *ctx, int seg, int ri_prev, int ri, int B, cons
             sa.c0 = C;
             sa.tile_rows = kTileM / H;
             sa.m_tiles = B * (H / sa.tile_rows);
-            sa.tmem_cols = C <= 32 ? 32 : 64;
-            CUtensorMap tOut;
+            sa.tmem_cols = C <= 16 ? 64 : 128;   // two accumulator stages of round32(C) columns
+            CUtensorMap tIn, tOut;
+            {   // the image as flat rows: (W*cimg, H, B), box = the tile's rows plus the 3x3 halo
+                const cuuint64_t rowe = static_cast<cuuint64_t>(H) * c.in_channels;
+                cuuint64_t dims[3] = {rowe, (cuuint64_t)H, (cuuint64_t)B};
+                cuuint64_t strides[2] = {rowe * 2, rowe * 2 * H};
+                cuuint32_t box[3] = {(cuuint32_t)rowe, (cuuint32_t)(sa.tile_rows + 2), 1};
+                cuuint32_t est[3] = {1, 1, 1};
+                if (!encode_map(ctx, &tIn, in, 3, dims, strides, box, est, false))
+                    return fail(ctx, SLIM_ECUDA, "cuTensorMapEncodeTiled(stem in) failed");
+            }
             if (!encode_act(ctx, &tOut, bufs[0], B, H, H, C, H, sa.tile_rows, 1, 1))
                 return fail(ctx, SLIM_ECUDA, "cuTensorMapEncodeTiled(stem out) failed");
-            // ~45 KB smem and 64 TMEM columns per CTA: four CTAs per SM hide the per-tile latency chain
-            int grid = ctx->num_sms * 4;
+            // persistent: one CTA per SM, halo fetch / im2col / MMA / store of consecutive tiles overlap
+            int grid = ctx->num_sms;
             if (grid > sa.m_tiles) grid = sa.m_tiles;
             LaunchProf prof(ctx, st);
-            e = launch_stem_umma(sa, tOut, grid, st, ctx->pdl && !ctx->prof_on);
+            e = launch_stem_umma(sa, tIn, tOut, grid, st, ctx->pdl && !ctx->prof_on);
             prof.done(SLIM_K_STEM, 0, 0, r, r, B, flops, bytes);
         } else {
             LaunchProf prof(ctx, st);

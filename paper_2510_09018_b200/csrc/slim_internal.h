@@ -78,6 +78,9 @@ struct HaloArgs {
     uint32_t a_bytes, b_bytes;
     uint32_t n_out_chunks;
     int res_slots;
+    int kw_fuse;              // kw taps per MMA (1..3): their accumulators are adjacent (acc_stride = n_tile)
+    int stage_cols;           // TMEM columns per accumulator stage (3 kw accumulators, 32-aligned)
+    int epi_groups;           // 2: epilogue warps 4-7 / 8-11 take even / odd tiles; 1: they split columns
     int debug;
     unsigned long long *trace;
 };
@@ -99,8 +102,9 @@ struct StemArgs {
     int B, H, W, cimg, c0;
     int tile_rows, m_tiles, tmem_cols;
 };
-cudaError_t launch_stem_umma(const StemArgs &a, const CUtensorMap &tmOut, int grid, cudaStream_t stream, bool pdl);
-int stem_umma_max_ctas_per_sm();
+// (kernels_stem.cu) tmIn: the image as a 3-D map (W*cimg, H, B), box (W*cimg, tile_rows+2, 1), no swizzle
+cudaError_t launch_stem_umma(const StemArgs &a, const CUtensorMap &tmIn, const CUtensorMap &tmOut, int grid,
+                             cudaStream_t stream, bool pdl);
 
 // ---- CUDA-core kernels (kernels_simt.cu) ------------------------------------
 cudaError_t launch_stem_bf16(const uint16_t *in, const float *w, int cin_full, const float *scale,
