@@ -7,6 +7,7 @@
 
 #include "../../include/slim.h"
 
+#include <algorithm>
 #include <atomic>
 #include <cstdarg>
 #include <cmath>
@@ -43,6 +44,8 @@ struct DevLayer {
     bool tm_ok[kMaxW][kMaxW][17] = {};
     CUtensorMap tmh[kMaxW][9][2];            // halo-kernel weight maps per (r idx, n_tile/16 - 1 (<=128), taps 3|9)
     bool tmh_ok[kMaxW][9][2] = {};
+    CUtensorMap tms[kMaxW][kMaxW];           // split-K kernel weight maps (64-channel boxes) per (r_prev idx, r idx)
+    bool tms_ok[kMaxW][kMaxW] = {};
 };
 
 struct DevSegment {
@@ -229,11 +232,11 @@ int chunk_ch(int c) {
 
 // Weights KRSC [Cout_full][k*k][Cin_full] bf16 as a 3-D map whose BOUNDS are the
 // active prefix (c_in, k*k, c_out): the slice is selected by predication.
-bool encode_w(slim_ctx *ctx, CUtensorMap *tm, const DevLayer &L, int c_in, int c_out, int n_tile) {
+bool encode_w(slim_ctx *ctx, CUtensorMap *tm, const DevLayer &L, int c_in, int c_out, int n_tile, int box_c = 0) {
     const int kk = L.sh.k * L.sh.k;
     cuuint64_t dims[3] = {(cuuint64_t)c_in, (cuuint64_t)kk, (cuuint64_t)c_out};
     cuuint64_t strides[2] = {(cuuint64_t)L.sh.cin * 2, (cuuint64_t)kk * L.sh.cin * 2};
-    cuuint32_t box[3] = {(cuuint32_t)chunk_ch(c_in), 1, (cuuint32_t)n_tile};
+    cuuint32_t box[3] = {(cuuint32_t)(box_c ? box_c : chunk_ch(c_in)), 1, (cuuint32_t)n_tile};
     cuuint32_t est[3] = {1, 1, 1};
     return encode_map(ctx, tm, L.w, 3, dims, strides, box, est);
 }
@@ -456,10 +459,179 @@ slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, i
     return SLIM_OK;
 }
 
+// Split-K over a cluster (kernels_splitk.cu) for layers whose M is too small to fill the SMs with
+// wide tiles.  The split count depends only on the layer shape and the context's max_batch (never
+// on B), so a layer's fp32 summation order -- and its output bits -- are batch independent.
+// Returns SLIM_EUNSUPPORTED (nothing launched) when the layer does not qualify.
+slim_status conv_splitk_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, int ri, int B) {
+    static const bool disabled = getenv("SLIM_NO_SPLITK") != nullptr;
+    // clusters of 8 measured far slower than 4 (cluster scheduling): 4 unless SLIM_SPLITK_MAX
+    static const int ks_max = getenv("SLIM_SPLITK_MAX") ? atoi(getenv("SLIM_SPLITK_MAX")) : 4;
+    const slim_config &c = ctx->cfg;
+    DevLayer &L = *cc.L;
+    if (disabled) return SLIM_EUNSUPPORTED;
+    const int k = L.sh.k, s = L.sh.stride, pad = k / 2;
+    const int Ho = (cc.H + 2 * pad - k) / s + 1, Wo = (cc.W + 2 * pad - k) / s + 1;
+    const int c_out = slim_channels(c.widths[ri], L.sh.cout);
+    const int P = Ho * Wo;
+    SplitArgs a{};
+    a.B = B;
+    a.Ho = Ho;
+    a.Wo = Wo;
+    int m_ref;
+    if (P >= kTileM) {
+        if (P % kTileM || kTileM % Wo) return SLIM_EUNSUPPORTED;
+        a.tile_imgs = 1;
+        a.tile_rows = kTileM / Wo;
+        a.tiles_per_img = Ho / a.tile_rows;
+        a.m_tiles = B * a.tiles_per_img;
+        m_ref = c.max_batch * a.tiles_per_img;
+    } else {
+        if (kTileM % P) return SLIM_EUNSUPPORTED;
+        a.tile_imgs = kTileM / P;
+        a.tile_rows = Ho;
+        a.tiles_per_img = 1;
+        a.m_tiles = (B + a.tile_imgs - 1) / a.tile_imgs;
+        m_ref = (c.max_batch + a.tile_imgs - 1) / a.tile_imgs;
+    }
+    a.n_parts = (cc.epi == EPI_BN_PROJ_RELU) ? 2 : 1;
+    // widest N tile: a divisor of c_out, multiple of 16, <= 256, both parts' accumulators in TMEM
+    int nt = 0;
+    for (int d = 256; d >= 16; d -= 16)
+        if (c_out % d == 0 && a.n_parts * d <= 512) {
+            nt = d;
+            break;
+        }
+    if (!nt) return SLIM_EUNSUPPORTED;
+    a.n_tile = nt;
+    a.c_out = c_out;
+    const int n_tiles = c_out / nt;
+    a.part[0] = GemmPart{k, s, pad, cc.c_in, kChunk, 128, (cc.c_in + kChunk - 1) / kChunk, 0};
+    a.part[0].n_kblocks = k * k * a.part[0].n_chunks;
+    if (a.n_parts == 2) {
+        a.part[1] = GemmPart{cc.Lp->sh.k, cc.Lp->sh.stride, 0, cc.c_in_p, kChunk, 128, (cc.c_in_p + kChunk - 1) / kChunk, 0};
+        a.part[1].n_kblocks = a.part[1].n_chunks;
+    }
+    const int G = a.part[0].n_kblocks + (a.n_parts == 2 ? a.part[1].n_kblocks : 0);
+    a.epi = cc.epi;
+    a.scale0 = L.scale[ri];
+    a.shift0 = L.shift[ri];
+    if (a.n_parts == 2) {
+        a.scale1 = cc.Lp->scale[ri];
+        a.shift1 = cc.Lp->shift[ri];
+    }
+    a.pool_out = cc.pool_out;
+    if (a.pool_out && (P > 32 || 32 % P || a.tile_imgs == 1)) return SLIM_EUNSUPPORTED;
+    a.stage_bytes = 16384u + static_cast<uint32_t>(nt) * 128u;
+    int tc = 32;
+    while (tc < a.n_parts * nt) tc <<= 1;
+    a.tmem_cols = tc;
+    // Split count from a cycle model at B = max_batch (so the choice -- and the fp32 summation
+    // order -- never depends on B).  Measured on B200 (tools/layer_times.py): these
+    // layers are bound by L2->SM operand traffic at ~32 B/cycle per SM when all SMs stream, so a
+    // k-block costs max(its A+B bytes / 32, 4 UMMAs of N), times
+    // the number of waves.  A split adds ~4000 + 1000*ks cycles (cluster launch, two cluster barriers,
+    // the reduction epilogue after the last MMA) and the DSMEM push at ~16 B/cycle.
+    auto cyc = [](double n) { return std::max(36.0 + n / 4.0, n / 2.0); };
+    auto blk = [&](double n) { return std::max((16384.0 + n * 128.0) / 32.0, 4.0 * cyc(n)); };
+    const int sms = ctx->num_sms;
+    auto waves = [&](long ctas) { return static_cast<double>((ctas + sms - 1) / sms); };
+    double best_cost;
+    {
+        const int n_ns = pick_n_tile(c_out, m_ref, sms);
+        best_cost = waves(static_cast<long>(m_ref) * (c_out / n_ns)) * G * blk(n_ns);
+    }
+    static const bool force = getenv("SLIM_SPLITK_FORCE") != nullptr;   // tests: exercise the kernel
+    if (force) best_cost = 1e300;
+    int best_ks = 0;
+    for (int ks = 2; ks <= std::min(8, ks_max); ++ks) {
+        if (nt % ks || (nt / ks) % 16 || G < ks) continue;
+        const double cost = waves(static_cast<long>(m_ref) * n_tiles * ks) *
+                            (std::ceil(static_cast<double>(G) / ks) * blk(nt) + 4000.0 + 1000.0 * ks +
+                             (ks - 1) * a.n_parts * 128.0 * (nt / ks) * 4.0 / 16.0);
+        if (cost < best_cost) {
+            best_cost = cost;
+            best_ks = ks;
+        }
+    }
+    if (getenv("SLIM_DEBUG"))
+        fprintf(stderr, "[slim] splitk seg%d L%d c_in %d c_out %d G %d m_ref %d: ks %d\n", cc.seg, cc.layer, cc.c_in,
+                c_out, G, m_ref, best_ks);
+    bool fits = false;
+    for (int ks = best_ks; ks >= 2 && !fits; --ks) {
+        if (nt % ks || (nt / ks) % 16 || G < ks) continue;
+        a.ks = ks;
+        a.w_o = nt / ks;
+        a.co_chunk = a.w_o % 64 == 0 ? 64 : (a.w_o % 32 == 0 ? 32 : 16);
+        a.rbo = 2 * a.co_chunk;
+        a.n_out_chunks = static_cast<uint32_t>(a.w_o / a.co_chunk);
+        const size_t slice = static_cast<size_t>(a.n_out_chunks) * 128 * a.rbo;
+        const size_t fixed = 1024 + slice * (cc.epi == EPI_BN_ADD_RELU ? 2 : 1) + 16 * static_cast<size_t>(a.w_o) +
+                             8 * (2 * 8 + 2) + 16;
+        int stages = static_cast<int>((226 * 1024 - fixed) / a.stage_bytes);
+        if (stages > 8) stages = 8;
+        a.n_stages = stages;
+        fits = stages >= 2 && static_cast<size_t>(stages) * a.stage_bytes >= conv_splitk_recv_bytes(a);
+    }
+    if (!fits) return SLIM_EUNSUPPORTED;
+    static const int nprod = getenv("SLIM_NPROD") ? atoi(getenv("SLIM_NPROD")) : 3;
+    a.n_prod = nprod < 1 ? 1 : (nprod > 3 ? 3 : nprod);
+    if (a.n_prod > a.n_stages) a.n_prod = a.n_stages;
+
+    CUtensorMap tA0, tA1, tRes, tOut;
+    if (!encode_act(ctx, &tA0, cc.x, B, cc.H, cc.W, cc.c_in, s * Wo, s * a.tile_rows, a.tile_imgs, s, kChunk))
+        return fail(ctx, SLIM_ECUDA, "cuTensorMapEncodeTiled(split A) failed");
+    const CUtensorMap *tB0, *tB1;
+    {
+        std::lock_guard<std::mutex> g(ctx->mu);
+        if (!L.tms_ok[cc.ri_in][ri]) {
+            if (!encode_w(ctx, &L.tms[cc.ri_in][ri], L, cc.c_in, c_out, nt, kChunk))
+                return fail(ctx, SLIM_ECUDA, "cuTensorMapEncodeTiled(split W) failed");
+            L.tms_ok[cc.ri_in][ri] = true;
+        }
+        tB0 = tB1 = &L.tms[cc.ri_in][ri];
+        if (a.n_parts == 2) {
+            DevLayer &Lp = *cc.Lp;
+            if (!Lp.tms_ok[cc.ri_in_p][ri]) {
+                if (!encode_w(ctx, &Lp.tms[cc.ri_in_p][ri], Lp, cc.c_in_p, c_out, nt, kChunk))
+                    return fail(ctx, SLIM_ECUDA, "cuTensorMapEncodeTiled(split W1) failed");
+                Lp.tms_ok[cc.ri_in_p][ri] = true;
+            }
+            tB1 = &Lp.tms[cc.ri_in_p][ri];
+        }
+    }
+    tA1 = tA0;
+    if (a.n_parts == 2) {
+        const int sp = cc.Lp->sh.stride;
+        if (!encode_act(ctx, &tA1, cc.xp, B, cc.Hp, cc.Wp, cc.c_in_p, sp * Wo, sp * a.tile_rows, a.tile_imgs, sp,
+                        kChunk))
+            return fail(ctx, SLIM_ECUDA, "cuTensorMapEncodeTiled(split A1) failed");
+    }
+    if (!encode_act(ctx, &tOut, cc.pool_out ? cc.x : cc.out, B, Ho, Wo, c_out, Wo, a.tile_rows, a.tile_imgs, 1,
+                    a.co_chunk))
+        return fail(ctx, SLIM_ECUDA, "cuTensorMapEncodeTiled(split out) failed");
+    tRes = tOut;
+    if (cc.epi == EPI_BN_ADD_RELU &&
+        !encode_act(ctx, &tRes, cc.res, B, Ho, Wo, c_out, Wo, a.tile_rows, a.tile_imgs, 1, a.co_chunk))
+        return fail(ctx, SLIM_ECUDA, "cuTensorMapEncodeTiled(split res) failed");
+    const int grid = a.m_tiles * n_tiles * a.ks;
+    double flops, bytes;
+    conv_work(c, cc, ri, B, Ho, Wo, &flops, &bytes);
+    LaunchProf prof(ctx, st);
+    cudaError_t e = launch_conv_splitk(a, tA0, *tB0, tA1, *tB1, tRes, tOut, grid, st, ctx->pdl && !ctx->prof_on);
+    prof.done(SLIM_K_CONV_UMMA, cc.seg, cc.layer, c.widths[cc.ri_in], c.widths[ri], B, flops, bytes);
+    if (e != cudaSuccess)
+        return fail(ctx, SLIM_ECUDA, "conv_splitk launch (grid %d, ks %d, n_tile %d, smem %zu, stages %d): %s", grid,
+                    a.ks, nt, conv_splitk_smem_bytes(a), a.n_stages, cudaGetErrorString(e));
+    return SLIM_OK;
+}
+
 slim_status conv_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, int ri, int B) {
     {
         const slim_status hs = conv_halo_bf16(ctx, st, cc, ri, B);
         if (hs != SLIM_EUNSUPPORTED) return hs;
+        const slim_status ss = conv_splitk_bf16(ctx, st, cc, ri, B);
+        if (ss != SLIM_EUNSUPPORTED) return ss;
     }
     const slim_config &c = ctx->cfg;
     DevLayer &L = *cc.L;

@@ -63,6 +63,30 @@ struct ConvArgs {
 
 size_t conv_umma_smem_bytes(const ConvArgs &a);
 
+// split-K conv over a thread-block cluster with a DSMEM reduction (kernels_splitk.cu)
+struct SplitArgs {
+    int B, Ho, Wo;
+    int tile_imgs, tile_rows, tiles_per_img, m_tiles;
+    int n_tile, c_out;        // output tile 128 x n_tile (n_tile | c_out, <= 256, n_parts*n_tile <= 512)
+    int n_parts;
+    GemmPart part[2];         // 64-channel chunks (ck = 64, 128-B rows) for both parts
+    int epi;
+    const float *scale0, *shift0, *scale1, *shift1;
+    int ks;                   // K splits = cluster size (2..8); CTA r of a cluster takes k-blocks [r*G/ks, (r+1)*G/ks)
+    int w_o;                  // output channels each CTA finishes: n_tile / ks (multiple of 16)
+    int co_chunk, rbo;        // staging chunk of the owner slice (16 | 32 | 64 channels) and its row bytes
+    uint32_t n_out_chunks;    // w_o / co_chunk
+    int n_stages;
+    uint32_t stage_bytes;     // A 16 KiB + B n_tile*128 B; the drained stages hold the DSMEM receive buffer
+    int n_prod, tmem_cols;
+    float *pool_out;
+};
+size_t conv_splitk_smem_bytes(const SplitArgs &a);
+size_t conv_splitk_recv_bytes(const SplitArgs &a);
+cudaError_t launch_conv_splitk(const SplitArgs &a, const CUtensorMap &tmA0, const CUtensorMap &tmB0,
+                               const CUtensorMap &tmA1, const CUtensorMap &tmB1, const CUtensorMap &tmRes,
+                               const CUtensorMap &tmOut, int grid, cudaStream_t stream, bool pdl);
+
 // stride-1 3x3 conv, one halo box per channel chunk + kw-split accumulators (kernels_halo.cu)
 struct HaloArgs {
     int B, H, W;              // output = input spatial size (stride 1, pad 1)

@@ -338,3 +338,38 @@ def test_cluster_multicast_path_parity(params, ref):
                          cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     assert out.returncode == 0, out.stderr[-2000:]
     assert float(out.stdout.strip().splitlines()[-1]) <= TAU_BF16
+
+
+def test_splitk_cluster_path_parity():
+    """The split-K conv (cluster of CTAs over K, fp32 partials reduced through DSMEM; chosen by a
+    cost model, forced here with SLIM_SPLITK_FORCE) matches the oracle on segments 1-3 for every
+    (r_prev, r), including the projection shortcut and the fused pool, and stays bitwise batch
+    independent (fixed rank-order reduction)."""
+    import subprocess, sys, os
+    code = (
+        "import numpy as np, torch, synth, oracle, paper_2510_09018_b200 as slim\n"
+        "w, bn = synth.make_weights(), synth.make_bn()\n"
+        "net = slim.SlimNet(w, bn, max_batch=128)\n"
+        "ref = oracle.Model(w, bn)\n"
+        "W = synth.WIDTHS\n"
+        "worst = 0.0\n"
+        "for seg in (1, 2, 3):\n"
+        "    H = 32 >> (seg - 1)\n"
+        "    for rp in W:\n"
+        "        C = synth.active_channels(rp, synth.BASE_CHANNELS[seg - 1])\n"
+        "        g = np.random.default_rng(77 + seg)\n"
+        "        x = synth.round_bf16(np.abs(g.standard_normal((9, H, H, C), dtype=np.float32)))\n"
+        "        xd = torch.from_numpy(x).to(torch.bfloat16).cuda()\n"
+        "        for r in W:\n"
+        "            got = net.forward(seg, xd, rp, r)\n"
+        "            sub = net.forward(seg, xd[2:5].contiguous(), rp, r)\n"
+        "            assert torch.equal(got[2:5], sub), ('batch independence', seg, rp, r)\n"
+        "            err = oracle.per_image_rel_err(got.float().cpu().numpy(), ref.segment(seg, x, rp, r))\n"
+        "            worst = max(worst, float(err.max()))\n"
+        "print(worst)\n"
+    )
+    env = dict(os.environ, SLIM_SPLITK_FORCE="1")
+    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600,
+                         cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert float(out.stdout.strip().splitlines()[-1]) <= TAU_BF16
