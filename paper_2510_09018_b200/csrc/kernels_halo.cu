@@ -28,7 +28,9 @@ namespace slim {
 using namespace ptx;
 namespace {
 
-constexpr int kHaloThreads = 384;   // warps 0 A, 1 MMA, 2 B, 3 idle, 4..11 epilogue
+constexpr int kHaloEpiWarps = 16;   // four per TMEM lane quarter: the epilogue is latency bound
+constexpr int kHaloEpiThreads = kHaloEpiWarps * 32;
+constexpr int kHaloThreads = (4 + kHaloEpiWarps) * 32;   // warps 0 A, 1 MMA, 2 B, 3 residual, 4..19 epilogue
 
 // kNarrow: runtime channel-chunk geometry (16/32-channel boxes); false folds 64-channel / 128-B rows.
 template <bool kNarrow>
@@ -39,7 +41,8 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
     extern __shared__ uint8_t smem_raw[];
     const int CK = kNarrow ? a.ck : kChunk, RBK = kNarrow ? a.rbk : 128;
     const int CO_CHUNK = kNarrow ? a.co_chunk : kChunk, RBO = kNarrow ? a.rbo : 128;
-    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // 1 KiB alignment without leaving the shared address space (LDS/STS, not generic LD/ST)
+    uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     const uint32_t oc_bytes = 128u * RBO;
     const uint32_t chunk_bytes = a.n_out_chunks * oc_bytes;
     const int n_res = (a.epi == EPI_BN_ADD_RELU) ? a.res_slots : 0;
@@ -81,9 +84,9 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(t_full(i), 1);
-            mbar_init(t_empty(i), kEpiThreads / n_grp);
+            mbar_init(t_empty(i), kHaloEpiThreads / n_grp);
             mbar_init(r_full(i), 1);
-            mbar_init(r_empty(i), kEpiThreads / n_grp);
+            mbar_init(r_empty(i), kHaloEpiThreads / n_grp);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         prefetch_tmap(&tmA);
@@ -310,26 +313,28 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
             if (tr && lane == 0) tr[3] = gtimer();
         }
     } else if (warp >= kEpiWarp0) {
-        // ===================== epilogue (warps 4..11, two per TMEM lane quarter) ====
-        // n_grp == 2: warps 4-7 take the even tiles, 8-11 the odd ones (accumulator stage,
+        // ===================== epilogue (warps 4..19, four per TMEM lane quarter) ===
+        // n_grp == 2: warps 4-11 take the even tiles, 12-19 the odd ones (accumulator stage,
         // residual slot, staging buffer and named barrier of their own), so two tiles'
-        // epilogues overlap; n_grp == 1: the two halves split the columns of every tile.
+        // epilogues overlap; inside a group the warps of one lane quarter split the columns.
         const int q = warp & 3;
-        const int half = (warp - kEpiWarp0) >> 2;
-        const int grp = n_grp == 2 ? half : 0;
-        const int g0 = n_grp == 2 ? 0 : half, gstep = n_grp == 2 ? 1 : 2;
-        const int gthreads = kEpiThreads / n_grp;
+        const int quad = (warp - kEpiWarp0) >> 2;          // 0..3
+        const int cw = 4 / n_grp;                           // column ways per group
+        const int grp = quad / cw;
+        const int g0 = quad % cw, gstep = cw;
+        const int gthreads = kHaloEpiThreads / n_grp;
         const int row = q * 32 + lane;
         // TMA swizzle of the staging tile (rbo-byte rows): 16-B piece q of this row lives at q ^ row_x
         const int co_shift = CO_CHUNK == 16 ? 4 : (CO_CHUNK == 32 ? 5 : 6);
         const uint32_t row_off = static_cast<uint32_t>(row * RBO);
         const int row_x = (row >> (RBO == 128 ? 0 : (RBO == 64 ? 1 : 2))) & ((RBO >> 4) - 1);
         const int w = lane % a.W;                  // W divides 32: pixel column of this row
-        const bool leader = (warp == kEpiWarp0 + 4 * grp && lane == 0);
+        const bool leader = (warp == kEpiWarp0 + 4 * cw * grp && lane == 0);
         const uint32_t lane_addr = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
         const float *s0 = sBN, *t0 = sBN + a.c_out;
         const uint32_t sOutG = sOut + grp * chunk_bytes;
         uint8_t *pOutG = pOut + grp * chunk_bytes;
+        const float mL = w > 0 ? 1.f : 0.f, mR = w < a.W - 1 ? 1.f : 0.f;   // conv zero padding in W
         for (int t = blockIdx.x + grp * gridDim.x; t < total; t += n_grp * gridDim.x) {
             const int mt = t % a.m_tiles, nt = t / a.m_tiles;
             const int n = mt / tiles_per_img, h0 = (mt - n * tiles_per_img) * a.rows, co0 = nt * a.n_tile;
@@ -346,26 +351,24 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
             if (leader) TD(2, ti, 2);
             const uint8_t *resp = pRes + rs * chunk_bytes;
             const uint32_t col0 = static_cast<uint32_t>(as * a.stage_cols);
-            const int G = (a.debug & 16) ? 0 : a.n_tile / 16;
-            // one 16-column group: out[w] = acc_0[w-1] + acc_1[w] + acc_2[w+1] (zero padding at the
-            // row ends), BN, residual, ReLU, bf16 into the swizzled staging tile
-            auto process = [&](int g, const uint32_t(&v0)[16], const uint32_t(&v1)[16], const uint32_t(&v2)[16]) {
+            for (int g = g0; g < a.n_tile / 16 && !(a.debug & 16); g += gstep) {
+                uint32_t v0[16], v1[16], v2[16];
+                tmem_ld16(lane_addr + col0 + g * 16, v0);
+                tmem_ld16(lane_addr + col0 + a.acc_stride + g * 16, v1);
+                tmem_ld16(lane_addr + col0 + 2 * a.acc_stride + g * 16, v2);
+                tmem_wait_ld();
+                reg_fence16(v0);
+                reg_fence16(v1);
+                reg_fence16(v2);
                 const int cl = g * 16, cg = co0 + cl;
-                float sc[16], sh[16];
-#pragma unroll
-                for (int i = 0; i < 16; i += 4) {
-                    *reinterpret_cast<float4 *>(sc + i) = *reinterpret_cast<const float4 *>(s0 + cg + i);
-                    *reinterpret_cast<float4 *>(sh + i) = *reinterpret_cast<const float4 *>(t0 + cg + i);
-                }
                 float f[16];
 #pragma unroll
                 for (int i = 0; i < 16; ++i) {
+                    // out[w] = acc_0[w-1] + acc_1[w] + acc_2[w+1]  (zero padding at the row ends)
                     const float left = __shfl_up_sync(0xffffffffu, __uint_as_float(v0[i]), 1);
                     const float right = __shfl_down_sync(0xffffffffu, __uint_as_float(v2[i]), 1);
-                    float y = __uint_as_float(v1[i]);
-                    if (w > 0) y += left;
-                    if (w < a.W - 1) y += right;
-                    f[i] = fmaf(y, sc[i], sh[i]);
+                    const float y = fmaf(mR, right, fmaf(mL, left, __uint_as_float(v1[i])));
+                    f[i] = fmaf(y, s0[cg + i], t0[cg + i]);
                 }
                 const int oc = cl >> co_shift, q16 = (cl & (CO_CHUNK - 1)) >> 3;
                 const uint32_t off0 = oc * oc_bytes + row_off + ((q16 ^ row_x) << 4);
@@ -385,48 +388,9 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
                 for (int i = 0; i < 8; ++i) o[i] = pack_bf16(fmaxf(f[2 * i], 0.f), fmaxf(f[2 * i + 1], 0.f));
                 *reinterpret_cast<uint4 *>(pOutG + off0) = make_uint4(o[0], o[1], o[2], o[3]);
                 *reinterpret_cast<uint4 *>(pOutG + off1) = make_uint4(o[4], o[5], o[6], o[7]);
-            };
-            auto load = [&](int g, uint32_t(&v0)[16], uint32_t(&v1)[16], uint32_t(&v2)[16]) {
-                tmem_ld16(lane_addr + col0 + g * 16, v0);
-                tmem_ld16(lane_addr + col0 + a.acc_stride + g * 16, v1);
-                tmem_ld16(lane_addr + col0 + 2 * a.acc_stride + g * 16, v2);
-            };
-            // software pipeline over column groups: the TMEM loads of group g+1 are in flight while
-            // group g is computed; the accumulator stage is released as soon as its last load landed
-            bool released = false;
-            auto landed = [&](int gn, uint32_t(&v0)[16], uint32_t(&v1)[16], uint32_t(&v2)[16]) {
-                tmem_wait_ld();
-                reg_fence16(v0);
-                reg_fence16(v1);
-                reg_fence16(v2);
-                if (gn >= G) {
-                    tc_fence_before();
-                    mbar_arrive(t_empty(as));
-                    released = true;
-                }
-            };
-            {
-                uint32_t a0[16], a1[16], a2[16], b0[16], b1[16], b2[16];
-                int g = g0;
-                if (g < G) load(g, a0, a1, a2);
-                while (g < G) {
-                    int gn = g + gstep;
-                    landed(gn, a0, a1, a2);
-                    if (gn < G) load(gn, b0, b1, b2);
-                    process(g, a0, a1, a2);
-                    g = gn;
-                    if (g >= G) break;
-                    gn = g + gstep;
-                    landed(gn, b0, b1, b2);
-                    if (gn < G) load(gn, a0, a1, a2);
-                    process(g, b0, b1, b2);
-                    g = gn;
-                }
             }
-            if (!released) {
-                tc_fence_before();
-                mbar_arrive(t_empty(as));
-            }
+            tc_fence_before();
+            mbar_arrive(t_empty(as));
             if (n_res) mbar_arrive(r_empty(rs));
             fence_proxy_async();
             named_bar_sync(1 + grp, gthreads);
