@@ -19,8 +19,13 @@
 //   B: the 9 taps x n_tile x 64-channel weight block is one box [64, n_tile, 9]
 //      (weight-stationary: loaded once per CTA when all chunks fit in smem), else
 //      streamed per (chunk, kh) as [64, n_tile, 3].
-// Roles (384 threads): warp 0 = A producer, warp 1 = MMA issuer, warp 2 = B producer,
-// warp 3 = residual prefetch, warps 4..11 = epilogue (two warps per TMEM lane quarter).
+//   Small images (H*W < 128, segments 2-3): a tile is tile_imgs = 128/(H*W) whole images and
+//      every activation map is addressed as (C, W, N, H) -- image inside row -- so the halo box
+//      [64, W, tile_imgs, H+2] lands row-major as (row, image, column): the kh window is again
+//      one contiguous 128-row run (offset kh*tile_imgs*W rows), a pixel's W-neighbours are
+//      lanes +-1, and the output / residual boxes use the same order (no reshuffle).
+// Roles: warp 0 = A producer, warp 1 = MMA issuer, warp 2 = B producer, warp 3 = residual
+// prefetch, warps 4..19 = epilogue (four per TMEM lane quarter).
 #include "slim_internal.h"
 #include "ptx_sm100.cuh"
 
@@ -135,7 +140,7 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
                     mbar_wait(a_empty(s), ph ^ 1);
                     if (ch == 0) TD(0, ti, 2);
                     mbar_expect_tx(a_full(s), a.a_bytes);
-                    tma_load_4d(sA + s * a.a_bytes, &tmA, a_full(s), ch * CK, 0, h0 - 1, n);
+                    tma_load_4d(sA + s * a.a_bytes, &tmA, a_full(s), ch * CK, 0, n * a.tile_imgs, h0 - 1);
                     if (++s == a.sa) {
                         s = 0;
                         ph ^= 1;
@@ -160,7 +165,8 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
                 } else {
                     mbar_expect_tx(r_full(rs), chunk_bytes);
                     for (uint32_t j = 0; j < a.n_out_chunks; ++j)
-                        tma_load_4d(sRes + rs * chunk_bytes + j * oc_bytes, &tmRes, r_full(rs), co0 + j * CO_CHUNK, 0, h0, n);
+                        tma_load_4d(sRes + rs * chunk_bytes + j * oc_bytes, &tmRes, r_full(rs), co0 + j * CO_CHUNK, 0,
+                                    n * a.tile_imgs, h0);
                 }
                 if (++rs == n_res) {
                     rs = 0;
@@ -199,7 +205,7 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
             const uint32_t idesc = umma_idesc_bf16(kTileM, a.n_tile * kf);
             const uint32_t idesc_r = umma_idesc_bf16(kTileM, a.n_tile * (kf == 2 ? 1 : kf));
             const uint32_t tap16 = static_cast<uint32_t>(a.n_tile * RBK) >> 4;   // one tap's B tile, 16-B units
-            const uint32_t row16 = static_cast<uint32_t>(a.W * RBK) >> 4;        // one halo row of W pixels
+            const uint32_t row16 = static_cast<uint32_t>(a.row_px * RBK) >> 4;   // one halo row (tile_imgs x W px)
             const uint64_t adesc0 = umma_desc_kmajor(sA, RBK), bdesc0 = umma_desc_kmajor(sB, RBK);
             const int kmax = CK >> 4;
             const uint32_t a_slot16 = a.a_bytes >> 4, b_slot16 = a.b_bytes >> 4;
@@ -397,7 +403,7 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
             if (leader && !(a.debug & 4)) {
                 TD(2, ti, 3);
                 for (uint32_t j = 0; j < a.n_out_chunks; ++j)
-                    tma_store_4d(&tmOut, sOutG + j * oc_bytes, co0 + j * CO_CHUNK, 0, h0, n);
+                    tma_store_4d(&tmOut, sOutG + j * oc_bytes, co0 + j * CO_CHUNK, 0, n * a.tile_imgs, h0);
                 bulk_commit();
             }
         }

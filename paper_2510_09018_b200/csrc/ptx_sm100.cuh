@@ -54,8 +54,13 @@ __device__ __forceinline__ bool mbar_try_wait_sleep(uint32_t bar, uint32_t parit
     return ok != 0;
 }
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+#ifdef SLIM_SPIN_WAIT
+    while (!mbar_try_wait(bar, parity)) {
+    }
+#else
     while (!mbar_try_wait_sleep(bar, parity)) {
     }
+#endif
 }
 
 // ---- TMA ----------------------------------------------------------------------

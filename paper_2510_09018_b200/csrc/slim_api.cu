@@ -224,6 +224,17 @@ bool encode_act(slim_ctx *ctx, CUtensorMap *tm, const void *ptr, int B, int H, i
     return encode_map(ctx, tm, ptr, 4, dims, strides, box, est);
 }
 
+// The same NHWC activation addressed as (C, W, N, H) -- the image index inside the row index --
+// so that a box [box_c, W, bn, bh] lands in shared memory as (row, image, column) (halo kernel).
+bool encode_act_rowmajor(slim_ctx *ctx, CUtensorMap *tm, const void *ptr, int B, int H, int W, int C, int bn, int bh,
+                         int box_c) {
+    cuuint64_t dims[4] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)B, (cuuint64_t)H};
+    cuuint64_t strides[3] = {(cuuint64_t)C * 2, (cuuint64_t)H * W * C * 2, (cuuint64_t)W * C * 2};
+    cuuint32_t box[4] = {(cuuint32_t)box_c, (cuuint32_t)W, (cuuint32_t)bn, (cuuint32_t)bh};
+    cuuint32_t est[4] = {1, 1, 1, 1};
+    return encode_map(ctx, tm, ptr, 4, dims, strides, box, est);
+}
+
 // channels per operand chunk: exact narrow boxes for 16 / 32 channels, else 64 (128-B rows)
 int chunk_ch(int c) {
     static const bool wide = getenv("SLIM_WIDE_BOX") != nullptr;   // diagnostics: always 64-channel boxes
@@ -329,21 +340,37 @@ slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, i
     DevLayer &L = *cc.L;
     if (disabled || L.sh.k != 3 || L.sh.stride != 1 || cc.epi == EPI_BN_PROJ_RELU || cc.pool_out) return SLIM_EUNSUPPORTED;
     const int H = cc.H, W = cc.W;
-    if (W > 32 || 32 % W || H * W < kTileM || kTileM % W || H % (kTileM / W)) return SLIM_EUNSUPPORTED;
+    static const bool no_small = getenv("SLIM_HALO_NO_SMALL") != nullptr;   // A/B: small images via per-tap conv
+    if (W > 32 || 32 % W) return SLIM_EUNSUPPORTED;
     const int c_out = slim_channels(c.widths[ri], L.sh.cout);
     HaloArgs a{};
     a.B = B;
     a.H = H;
     a.W = W;
-    a.rows = kTileM / W;
-    a.tiles_per_img = H / a.rows;
-    a.m_tiles = B * a.tiles_per_img;
+    if (H * W >= kTileM) {   // a tile is kTileM/W whole rows of one image
+        if (kTileM % W || H % (kTileM / W)) return SLIM_EUNSUPPORTED;
+        a.tile_imgs = 1;
+        a.rows = kTileM / W;
+        a.tiles_per_img = H / a.rows;
+        a.m_tiles = B * a.tiles_per_img;
+    } else {                 // a tile is kTileM/(H*W) whole images
+        if (no_small || kTileM % (H * W)) return SLIM_EUNSUPPORTED;
+        a.tile_imgs = kTileM / (H * W);
+        a.rows = H;
+        a.tiles_per_img = 1;
+        a.m_tiles = (B + a.tile_imgs - 1) / a.tile_imgs;
+    }
+    a.row_px = a.tile_imgs * W;
     // N tile <= 128: three accumulators of it must fit the 512 TMEM columns
+    // (128-channel layers: two N tiles of 64 keep two accumulator stages + the fused N=192 MMA,
+    // measured faster than one tile of 128; 96 channels cannot split into 64-channel tiles)
+    static const int halo_nmax_env = getenv("SLIM_HALO_NMAX") ? atoi(getenv("SLIM_HALO_NMAX")) : 0;
+    const int halo_nmax = halo_nmax_env ? halo_nmax_env : (c_out % 64 == 0 && c_out > 64 ? 64 : 128);
     int nt = 1;
     for (;; ++nt) {
         if (nt > c_out / 16) return SLIM_EUNSUPPORTED;
         if (c_out % nt || (c_out / nt) % 16 || (nt > 1 && (c_out / nt) % 64)) continue;
-        if (c_out / nt <= 128) break;
+        if (c_out / nt <= halo_nmax) break;
     }
     a.n_tile = c_out / nt;
     a.n_tiles = nt;
@@ -370,7 +397,7 @@ slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, i
     int cols = a.acc_stages * a.stage_cols, tc = 32;
     while (tc < cols) tc <<= 1;
     a.tmem_cols = tc;
-    a.a_bytes = static_cast<uint32_t>(kTileM + 2 * W) * a.rbk;
+    a.a_bytes = static_cast<uint32_t>(kTileM + 2 * a.row_px) * a.rbk;
     a.n_out_chunks = static_cast<uint32_t>((a.n_tile + a.co_chunk - 1) / a.co_chunk);
     const size_t chunk = static_cast<size_t>(a.n_out_chunks) * 128 * a.rbo;
     static const bool one_group = getenv("SLIM_HALO_EPI1") != nullptr;
@@ -424,7 +451,7 @@ slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, i
     a.trace = ctx->trace;
 
     CUtensorMap tA, tRes, tOut;
-    if (!encode_act(ctx, &tA, cc.x, B, H, W, cc.c_in, W, a.rows + 2, 1, 1, a.ck))
+    if (!encode_act_rowmajor(ctx, &tA, cc.x, B, H, W, cc.c_in, a.tile_imgs, a.rows + 2, a.ck))
         return fail(ctx, SLIM_ECUDA, "cuTensorMapEncodeTiled(halo A) failed");
     const int taps = a.stationary ? 9 : 3;
     const CUtensorMap *tB;
@@ -439,10 +466,11 @@ slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, i
         }
         tB = &m;
     }
-    if (!encode_act(ctx, &tOut, cc.out, B, H, W, c_out, W, a.rows, 1, 1, a.co_chunk))
+    if (!encode_act_rowmajor(ctx, &tOut, cc.out, B, H, W, c_out, a.tile_imgs, a.rows, a.co_chunk))
         return fail(ctx, SLIM_ECUDA, "cuTensorMapEncodeTiled(halo out) failed");
     tRes = tOut;
-    if (cc.epi == EPI_BN_ADD_RELU && !encode_act(ctx, &tRes, cc.res, B, H, W, c_out, W, a.rows, 1, 1, a.co_chunk))
+    if (cc.epi == EPI_BN_ADD_RELU &&
+        !encode_act_rowmajor(ctx, &tRes, cc.res, B, H, W, c_out, a.tile_imgs, a.rows, a.co_chunk))
         return fail(ctx, SLIM_ECUDA, "cuTensorMapEncodeTiled(halo res) failed");
     const int total = a.m_tiles * a.n_tiles;
     int grid = ctx->num_sms * (two ? 2 : 1);

@@ -90,7 +90,8 @@ cudaError_t launch_conv_splitk(const SplitArgs &a, const CUtensorMap &tmA0, cons
 // stride-1 3x3 conv, one halo box per channel chunk + kw-split accumulators (kernels_halo.cu)
 struct HaloArgs {
     int B, H, W;              // output = input spatial size (stride 1, pad 1)
-    int rows, tiles_per_img;  // tile = rows full image rows, rows*W = 128
+    int rows, tiles_per_img;  // tile = rows full image rows of tile_imgs images, rows*W*tile_imgs = 128
+    int tile_imgs, row_px;    // images per tile (1 unless H*W < 128); pixels per halo row = tile_imgs*W
     int m_tiles, n_tiles, n_tile, c_out, c_in, n_chunks;
     int epi;                  // EPI_BN_RELU or EPI_BN_ADD_RELU
     const float *scale, *shift;
