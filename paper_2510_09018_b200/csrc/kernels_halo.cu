@@ -42,6 +42,7 @@ template <bool kNarrow>
 __global__ void __launch_bounds__(kHaloThreads, 1)
     conv_halo_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmRes, const __grid_constant__ CUtensorMap tmOut,
+                     const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUtensorMap tmB1,
                      const HaloArgs a) {
     extern __shared__ uint8_t smem_raw[];
     const int CK = kNarrow ? a.ck : kChunk, RBK = kNarrow ? a.rbk : 128;
@@ -52,14 +53,15 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
     const uint32_t chunk_bytes = a.n_out_chunks * oc_bytes;
     const int n_res = (a.epi == EPI_BN_ADD_RELU) ? a.res_slots : 0;
     const uint32_t sA = smem_u32(smem);
-    const uint32_t sB = sA + a.sa * a.a_bytes;
+    const uint32_t sB = sA + a.sa * a.a_slot;
     const uint32_t sOut = sB + a.sb * a.b_bytes;
     const int n_grp = a.epi_groups;
     const uint32_t sRes = sOut + n_grp * chunk_bytes;
     uint8_t *pOut = smem + (sOut - sA);
     uint8_t *pRes = smem + (sRes - sA);
     float *sBN = reinterpret_cast<float *>(pRes + n_res * chunk_bytes);
-    uint64_t *bars = reinterpret_cast<uint64_t *>(sBN + 2 * a.c_out);
+    const bool proj = a.epi == EPI_BN_PROJ_RELU;   // + 1x1 stride-2 projection shortcut (4th accumulator)
+    uint64_t *bars = reinterpret_cast<uint64_t *>(sBN + (proj ? 4 : 2) * a.c_out);
     const uint32_t bar0 = smem_u32(bars);
     // barriers: a_full[4] a_empty[4] b_full[4] b_empty[4] t_full[2] t_empty[2] r_full[2] r_empty[2]
     auto a_full = [&](int i) { return bar0 + 8u * i; };
@@ -108,6 +110,10 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
     for (int i = threadIdx.x; i < a.c_out; i += blockDim.x) {
         sBN[i] = a.scale[i];
         sBN[a.c_out + i] = a.shift[i];
+        if (proj) {
+            sBN[2 * a.c_out + i] = a.scale1[i];
+            sBN[3 * a.c_out + i] = a.shift1[i];
+        }
     }
     // weight-stationary B does not depend on the previous kernel: start it before the PDL wait
     __syncthreads();
@@ -140,7 +146,20 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
                     mbar_wait(a_empty(s), ph ^ 1);
                     if (ch == 0) TD(0, ti, 2);
                     mbar_expect_tx(a_full(s), a.a_bytes);
-                    tma_load_4d(sA + s * a.a_bytes, &tmA, a_full(s), ch * CK, 0, n * a.tile_imgs, h0 - 1);
+                    tma_load_4d(sA + s * a.a_slot, &tmA, a_full(s), ch * CK, 0, n * a.tile_imgs, h0 - 1);
+                    if (++s == a.sa) {
+                        s = 0;
+                        ph ^= 1;
+                    }
+                }
+                // projection chunks: the stride-2 sampled block input (128 px x 64 ch) and its
+                // 1x1 weights (n_tile x 64) share one A slot
+                const int co0 = (t / a.m_tiles) * a.n_tile;
+                for (int cp = 0; proj && cp < a.n_chunks_p; ++cp) {
+                    mbar_wait(a_empty(s), ph ^ 1);
+                    mbar_expect_tx(a_full(s), 16384u + static_cast<uint32_t>(a.n_tile) * 128u);
+                    tma_load_4d(sA + s * a.a_slot, &tmA1, a_full(s), cp * kChunk, 0, n * a.tile_imgs, 2 * h0);
+                    tma_load_3d(sA + s * a.a_slot + 16384u, &tmB1, a_full(s), cp * kChunk, 0, co0);
                     if (++s == a.sa) {
                         s = 0;
                         ph ^= 1;
@@ -208,7 +227,7 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
             const uint32_t row16 = static_cast<uint32_t>(a.row_px * RBK) >> 4;   // one halo row (tile_imgs x W px)
             const uint64_t adesc0 = umma_desc_kmajor(sA, RBK), bdesc0 = umma_desc_kmajor(sB, RBK);
             const int kmax = CK >> 4;
-            const uint32_t a_slot16 = a.a_bytes >> 4, b_slot16 = a.b_bytes >> 4;
+            const uint32_t a_slot16 = a.a_slot >> 4, b_slot16 = a.b_bytes >> 4;
             const uint32_t accs = static_cast<uint32_t>(a.acc_stride);
             int s = 0, bs = 0, as = 0;
             uint32_t ph = 0, bph = 0, aph = 0;
@@ -305,6 +324,27 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
                         ph ^= 1;
                     }
                 }
+                if (proj) {
+                    const uint32_t idesc_p = umma_idesc_bf16(kTileM, a.n_tile);
+                    const uint64_t pdesc0 = umma_desc_kmajor(sA, 128);
+                    for (int cp = 0; cp < a.n_chunks_p; ++cp) {
+                        const int nk = min(4, (a.c_in_p - cp * kChunk + 15) >> 4);
+                        mbar_wait(a_full(s), ph);
+                        tc_fence_after();
+                        if (elect_one()) {
+                            const uint64_t ad = pdesc0 + s * a_slot16;
+                            for (int kk = 0; kk < nk; ++kk)
+                                umma_bf16(acc + 3 * accs, ad + 2 * kk, ad + (16384u >> 4) + 2 * kk, idesc_p,
+                                          (cp | kk) != 0);
+                            umma_commit(a_empty(s));
+                        }
+                        __syncwarp();
+                        if (++s == a.sa) {
+                            s = 0;
+                            ph ^= 1;
+                        }
+                    }
+                }
                 if (elect_one()) umma_commit(t_full(as));
                 __syncwarp();
                 if (lane == 0) {
@@ -376,6 +416,14 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
                     const float y = fmaf(mR, right, fmaf(mL, left, __uint_as_float(v1[i])));
                     f[i] = fmaf(y, s0[cg + i], t0[cg + i]);
                 }
+                if (proj) {   // + s_sc * proj + t_sc (the shortcut's own BN)
+                    tmem_ld16(lane_addr + col0 + 3 * a.acc_stride + g * 16, v0);
+                    tmem_wait_ld();
+                    reg_fence16(v0);
+                    const float *s1 = sBN + 2 * a.c_out, *t1 = sBN + 3 * a.c_out;
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) f[i] += fmaf(__uint_as_float(v0[i]), s1[cg + i], t1[cg + i]);
+                }
                 const int oc = cl >> co_shift, q16 = (cl & (CO_CHUNK - 1)) >> 3;
                 const uint32_t off0 = oc * oc_bytes + row_off + ((q16 ^ row_x) << 4);
                 const uint32_t off1 = oc * oc_bytes + row_off + (((q16 + 1) ^ row_x) << 4);
@@ -427,14 +475,14 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
 size_t conv_halo_smem_bytes(const HaloArgs &a) {
     const size_t chunk = static_cast<size_t>(a.n_out_chunks) * 128 * a.rbo;
     const int n_res = (a.epi == EPI_BN_ADD_RELU) ? a.res_slots : 0;
-    return 1024 + static_cast<size_t>(a.sa) * a.a_bytes + static_cast<size_t>(a.sb) * a.b_bytes +
+    return 1024 + static_cast<size_t>(a.sa) * a.a_slot + static_cast<size_t>(a.sb) * a.b_bytes +
            chunk * (a.epi_groups + n_res) +
-           8 * static_cast<size_t>(a.c_out) + 8 * 24 + 16;
+           (a.epi == EPI_BN_PROJ_RELU ? 16 : 8) * static_cast<size_t>(a.c_out) + 8 * 24 + 16;
 }
 
 cudaError_t launch_conv_halo(const HaloArgs &a, const CUtensorMap &tmA, const CUtensorMap &tmB,
-                             const CUtensorMap &tmRes, const CUtensorMap &tmOut, int grid, cudaStream_t stream,
-                             bool pdl) {
+                             const CUtensorMap &tmRes, const CUtensorMap &tmOut, const CUtensorMap &tmA1,
+                             const CUtensorMap &tmB1, int grid, cudaStream_t stream, bool pdl) {
     static bool attr_set = false;
     if (!attr_set) {
         for (int m = 0; m < 2; ++m) {
@@ -456,7 +504,8 @@ cudaError_t launch_conv_halo(const HaloArgs &a, const CUtensorMap &tmA, const CU
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     const bool narrow = a.ck != kChunk || a.co_chunk != kChunk;
-    return cudaLaunchKernelEx(&cfg, narrow ? conv_halo_kernel<true> : conv_halo_kernel<false>, tmA, tmB, tmRes, tmOut, a);
+    return cudaLaunchKernelEx(&cfg, narrow ? conv_halo_kernel<true> : conv_halo_kernel<false>, tmA, tmB, tmRes, tmOut,
+                              tmA1, tmB1, a);
 }
 
 }  // namespace slim

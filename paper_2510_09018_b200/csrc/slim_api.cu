@@ -226,12 +226,13 @@ bool encode_act(slim_ctx *ctx, CUtensorMap *tm, const void *ptr, int B, int H, i
 
 // The same NHWC activation addressed as (C, W, N, H) -- the image index inside the row index --
 // so that a box [box_c, W, bn, bh] lands in shared memory as (row, image, column) (halo kernel).
+// es = 2: traversal stride 2 in W and H (box W*es x bh*es elements, every other one delivered).
 bool encode_act_rowmajor(slim_ctx *ctx, CUtensorMap *tm, const void *ptr, int B, int H, int W, int C, int bn, int bh,
-                         int box_c) {
+                         int box_c, int es = 1) {
     cuuint64_t dims[4] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)B, (cuuint64_t)H};
     cuuint64_t strides[3] = {(cuuint64_t)C * 2, (cuuint64_t)H * W * C * 2, (cuuint64_t)W * C * 2};
-    cuuint32_t box[4] = {(cuuint32_t)box_c, (cuuint32_t)W, (cuuint32_t)bn, (cuuint32_t)bh};
-    cuuint32_t est[4] = {1, 1, 1, 1};
+    cuuint32_t box[4] = {(cuuint32_t)box_c, (cuuint32_t)W, (cuuint32_t)bn, (cuuint32_t)(bh * es)};
+    cuuint32_t est[4] = {1, (cuuint32_t)es, 1, (cuuint32_t)es};
     return encode_map(ctx, tm, ptr, 4, dims, strides, box, est);
 }
 
@@ -338,7 +339,11 @@ slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, i
     static const bool disabled = getenv("SLIM_NO_HALO") != nullptr;
     const slim_config &c = ctx->cfg;
     DevLayer &L = *cc.L;
-    if (disabled || L.sh.k != 3 || L.sh.stride != 1 || cc.epi == EPI_BN_PROJ_RELU || cc.pool_out) return SLIM_EUNSUPPORTED;
+    static const bool no_proj = getenv("SLIM_HALO_NO_PROJ") != nullptr;
+    if (disabled || L.sh.k != 3 || L.sh.stride != 1 || cc.pool_out) return SLIM_EUNSUPPORTED;
+    const bool proj = cc.epi == EPI_BN_PROJ_RELU;
+    if (proj && (no_proj || cc.Lp->sh.k != 1 || cc.Lp->sh.stride != 2 || cc.Hp != 2 * cc.H || cc.Wp != 2 * cc.W))
+        return SLIM_EUNSUPPORTED;
     const int H = cc.H, W = cc.W;
     static const bool no_small = getenv("SLIM_HALO_NO_SMALL") != nullptr;   // A/B: small images via per-tap conv
     if (W > 32 || 32 % W) return SLIM_EUNSUPPORTED;
@@ -392,12 +397,21 @@ slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, i
     static const bool nofuse = getenv("SLIM_HALO_NOFUSE") != nullptr;
     a.kw_fuse = nofuse ? 1 : (3 * a.n_tile <= 256 ? 3 : (2 * a.n_tile <= 256 ? 2 : 1));
     a.acc_stride = a.kw_fuse > 1 ? a.n_tile : (a.n_tile + 31) / 32 * 32;
-    a.stage_cols = (3 * a.acc_stride + 31) / 32 * 32;
+    a.stage_cols = (3 * a.acc_stride + (proj ? a.n_tile : 0) + 31) / 32 * 32;
     a.acc_stages = 2 * a.stage_cols <= 512 ? 2 : 1;
     int cols = a.acc_stages * a.stage_cols, tc = 32;
     while (tc < cols) tc <<= 1;
     a.tmem_cols = tc;
     a.a_bytes = static_cast<uint32_t>(kTileM + 2 * a.row_px) * a.rbk;
+    a.a_slot = (a.a_bytes + 1023u) & ~1023u;
+    if (proj) {   // a projection chunk = 128 px x 64 ch + its n_tile x 64 weights in one slot
+        if (a.ck != kChunk) return SLIM_EUNSUPPORTED;
+        a.scale1 = cc.Lp->scale[ri];
+        a.shift1 = cc.Lp->shift[ri];
+        a.c_in_p = cc.c_in_p;
+        a.n_chunks_p = (cc.c_in_p + kChunk - 1) / kChunk;
+        a.a_slot = std::max<uint32_t>(a.a_slot, 16384u + static_cast<uint32_t>(a.n_tile) * 128u);
+    }
     a.n_out_chunks = static_cast<uint32_t>((a.n_tile + a.co_chunk - 1) / a.co_chunk);
     const size_t chunk = static_cast<size_t>(a.n_out_chunks) * 128 * a.rbo;
     static const bool one_group = getenv("SLIM_HALO_EPI1") != nullptr;
@@ -407,7 +421,9 @@ slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, i
     static const bool two_cta = getenv("SLIM_HALO_TWO") != nullptr;
     const bool two = two_cta && a.n_tile <= 32 && a.ck <= 32;
     const size_t budget = two ? 110 * 1024 : 226 * 1024;
-    auto fixed0 = [&]() { return 1024 + chunk * a.epi_groups + 8 * static_cast<size_t>(c_out) + 8 * 24 + 16; };
+    auto fixed0 = [&]() {
+        return 1024 + chunk * a.epi_groups + (proj ? 16 : 8) * static_cast<size_t>(c_out) + 8 * 24 + 16;
+    };
     auto r1k = [](uint32_t x) { return (x + 1023u) & ~1023u; };
     const uint32_t all_w = r1k(static_cast<uint32_t>(a.n_chunks) * 9u * a.n_tile * a.rbk);
     a.res_slots = (cc.epi == EPI_BN_ADD_RELU) ? 2 : 0;
@@ -423,25 +439,25 @@ slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, i
         const size_t res = chunk * a.res_slots;
         size_t left = budget - fixed0() - res;
         if (a.stationary) {
-            if (left < a.b_bytes + 2 * a.a_bytes) {
+            if (left < a.b_bytes + 2 * a.a_slot) {
                 if (a.epi_groups == 2) { a.epi_groups = 1; continue; }
                 if (a.res_slots == 2) { a.res_slots = 1; continue; }
                 return SLIM_EUNSUPPORTED;
             }
             left -= a.b_bytes;
-            a.sa = static_cast<int>(left / a.a_bytes);
+            a.sa = static_cast<int>(left / a.a_slot);
             a.sa = a.sa > 4 ? 4 : a.sa;
         } else {
-            if (left < 2 * a.a_bytes + 2 * a.b_bytes) {
+            if (left < 2 * a.a_slot + 2 * a.b_bytes) {
                 if (a.epi_groups == 2) { a.epi_groups = 1; continue; }
                 if (a.res_slots == 2) { a.res_slots = 1; continue; }
                 return SLIM_EUNSUPPORTED;
             }
             a.sa = 2;
-            left -= 2 * a.a_bytes;
+            left -= 2 * a.a_slot;
             a.sb = static_cast<int>(left / a.b_bytes);
             a.sb = a.sb > 4 ? 4 : a.sb;
-            if (a.sb >= 4 && left - 4 * a.b_bytes >= a.a_bytes) a.sa = 3;
+            if (a.sb >= 4 && left - 4 * a.b_bytes >= a.a_slot) a.sa = 3;
         }
         break;
     }
@@ -479,7 +495,14 @@ slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, i
     conv_work(c, cc, ri, B, H, W, &flops, &bytes);
     if (ctx->trace) cudaMemsetAsync(ctx->trace, 0, 4096 * 8 * sizeof(unsigned long long), st);   // diagnostics
     LaunchProf prof(ctx, st);
-    cudaError_t e = launch_conv_halo(a, tA, *tB, tRes, tOut, grid, st, ctx->pdl && !ctx->prof_on);
+    CUtensorMap tA1 = tA, tB1 = tA;
+    if (proj) {
+        if (!encode_act_rowmajor(ctx, &tA1, cc.xp, B, cc.Hp, cc.Wp, cc.c_in_p, a.tile_imgs, a.rows, kChunk, 2))
+            return fail(ctx, SLIM_ECUDA, "cuTensorMapEncodeTiled(halo proj A) failed");
+        if (!encode_w(ctx, &tB1, *cc.Lp, cc.c_in_p, c_out, a.n_tile, kChunk))
+            return fail(ctx, SLIM_ECUDA, "cuTensorMapEncodeTiled(halo proj W) failed");
+    }
+    cudaError_t e = launch_conv_halo(a, tA, *tB, tRes, tOut, tA1, tB1, grid, st, ctx->pdl && !ctx->prof_on);
     prof.done(SLIM_K_CONV_UMMA, cc.seg, cc.layer, c.widths[cc.ri_in], c.widths[ri], B, flops, bytes);
     if (e != cudaSuccess)
         return fail(ctx, SLIM_ECUDA, "conv_halo launch (grid %d, smem %zu): %s", grid, conv_halo_smem_bytes(a),

@@ -93,14 +93,17 @@ struct HaloArgs {
     int rows, tiles_per_img;  // tile = rows full image rows of tile_imgs images, rows*W*tile_imgs = 128
     int tile_imgs, row_px;    // images per tile (1 unless H*W < 128); pixels per halo row = tile_imgs*W
     int m_tiles, n_tiles, n_tile, c_out, c_in, n_chunks;
-    int epi;                  // EPI_BN_RELU or EPI_BN_ADD_RELU
+    int epi;                  // EPI_BN_RELU, EPI_BN_ADD_RELU or EPI_BN_PROJ_RELU (1x1 stride-2 shortcut)
     const float *scale, *shift;
+    const float *scale1, *shift1;   // projection BN (EPI_BN_PROJ_RELU)
+    int c_in_p, n_chunks_p;   // projection input channels and 64-channel chunks
     int stationary;           // all weights resident in smem (one B slot of n_chunks*9 taps)
     int sa, sb;               // A ring slots (one per chunk), B ring slots (one per (chunk, kh)) -- each <= 4
     int acc_stride, acc_stages, tmem_cols;
     int ck, rbk;              // input channels per chunk (16 | 32 | 64) and operand row bytes
     int co_chunk, rbo;        // output channels per staging chunk and its row bytes
-    uint32_t a_bytes, b_bytes;
+    uint32_t a_bytes, b_bytes;   // halo box bytes (expect_tx), B slot bytes
+    uint32_t a_slot;             // A ring slot stride (>= a_bytes; a projection chunk also fits)
     uint32_t n_out_chunks;
     int res_slots;
     int kw_fuse;              // kw taps per MMA (1..3): their accumulators are adjacent (acc_stride = n_tile)
@@ -111,8 +114,8 @@ struct HaloArgs {
 };
 size_t conv_halo_smem_bytes(const HaloArgs &a);
 cudaError_t launch_conv_halo(const HaloArgs &a, const CUtensorMap &tmA, const CUtensorMap &tmB,
-                             const CUtensorMap &tmRes, const CUtensorMap &tmOut, int grid, cudaStream_t stream,
-                             bool pdl);
+                             const CUtensorMap &tmRes, const CUtensorMap &tmOut, const CUtensorMap &tmA1,
+                             const CUtensorMap &tmB1, int grid, cudaStream_t stream, bool pdl);
 cudaError_t launch_conv_umma(const ConvArgs &a, const CUtensorMap &tmA0, const CUtensorMap &tmB0,
                              const CUtensorMap &tmA1, const CUtensorMap &tmB1, const CUtensorMap &tmRes,
                              const CUtensorMap &tmOut, int grid, cudaStream_t stream, bool pdl);
