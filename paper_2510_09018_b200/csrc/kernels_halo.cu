@@ -38,7 +38,9 @@ constexpr int kHaloEpiThreads = kHaloEpiWarps * 32;
 constexpr int kHaloThreads = (4 + kHaloEpiWarps) * 32;   // warps 0 A, 1 MMA, 2 B, 3 residual, 4..19 epilogue
 
 // kNarrow: runtime channel-chunk geometry (16/32-channel boxes); false folds 64-channel / 128-B rows.
-template <bool kNarrow>
+// kVar: 0 = plain / residual epilogue, 1 = + projection shortcut, 2 = + fused average pool
+// (compile-time, so the common variant carries none of the other two's code)
+template <bool kNarrow, int kVar>
 __global__ void __launch_bounds__(kHaloThreads, 1)
     conv_halo_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmRes, const __grid_constant__ CUtensorMap tmOut,
@@ -60,7 +62,8 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
     uint8_t *pOut = smem + (sOut - sA);
     uint8_t *pRes = smem + (sRes - sA);
     float *sBN = reinterpret_cast<float *>(pRes + n_res * chunk_bytes);
-    const bool proj = a.epi == EPI_BN_PROJ_RELU;   // + 1x1 stride-2 projection shortcut (4th accumulator)
+    constexpr bool proj = kVar == 1;   // + 1x1 stride-2 projection shortcut (4th accumulator)
+    constexpr bool pool = kVar == 2;   // fused global average pool instead of the store
     uint64_t *bars = reinterpret_cast<uint64_t *>(sBN + (proj ? 4 : 2) * a.c_out);
     const uint32_t bar0 = smem_u32(bars);
     // barriers: a_full[4] a_empty[4] b_full[4] b_empty[4] t_full[2] t_empty[2] r_full[2] r_empty[2]
@@ -437,6 +440,24 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
                         f[2 * i + 1] += bf16_hi(rr[i]);
                     }
                 }
+                if (pool) {
+                    // fused global average pool (last conv): sum the W pixels of this image row
+                    // (lanes of one image are W consecutive lanes), park it per (row = lane quarter,
+                    // image, channel) in the staging tile; rows are summed below in fixed order
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) f[i] = fmaxf(f[i], 0.f);
+                    for (int o = 1; o < a.W; o <<= 1) {
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) f[i] += __shfl_xor_sync(0xffffffffu, f[i], o);
+                    }
+                    if (w == 0) {
+                        float4 *dst = reinterpret_cast<float4 *>(
+                            pOutG + 4u * ((q * a.tile_imgs + lane / a.W) * a.n_tile + cl));
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) dst[i] = make_float4(f[4 * i], f[4 * i + 1], f[4 * i + 2], f[4 * i + 3]);
+                    }
+                    continue;
+                }
                 uint32_t o[8];
 #pragma unroll
                 for (int i = 0; i < 8; ++i) o[i] = pack_bf16(fmaxf(f[2 * i], 0.f), fmaxf(f[2 * i + 1], 0.f));
@@ -446,6 +467,22 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
             tc_fence_before();
             mbar_arrive(t_empty(as));
             if (n_res) mbar_arrive(r_empty(rs));
+            if (pool) {
+                named_bar_sync(1 + grp, gthreads);
+                const int tig = ((quad - grp * cw) * 4 + q) * 32 + lane;
+                const float inv = 1.f / static_cast<float>(a.rows * a.W);
+                const float *sp = reinterpret_cast<const float *>(pOutG);
+                const int per_row = a.tile_imgs * a.n_tile;
+                for (int idx = tig; idx < per_row; idx += gthreads) {
+                    const int im = idx / a.n_tile, c = idx - im * a.n_tile;
+                    float sum = 0.f;
+                    for (int h = 0; h < a.rows; ++h) sum += sp[h * per_row + idx];
+                    const int nimg = n * a.tile_imgs + im;
+                    if (nimg < a.B) a.pool_out[static_cast<size_t>(nimg) * a.c_out + co0 + c] = sum * inv;
+                }
+                named_bar_sync(1 + grp, gthreads);   // the parked sums may be overwritten by the next tile
+                continue;
+            }
             fence_proxy_async();
             named_bar_sync(1 + grp, gthreads);
             if (leader && !(a.debug & 4)) {
@@ -483,14 +520,17 @@ size_t conv_halo_smem_bytes(const HaloArgs &a) {
 cudaError_t launch_conv_halo(const HaloArgs &a, const CUtensorMap &tmA, const CUtensorMap &tmB,
                              const CUtensorMap &tmRes, const CUtensorMap &tmOut, const CUtensorMap &tmA1,
                              const CUtensorMap &tmB1, int grid, cudaStream_t stream, bool pdl) {
+    using Fn = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, HaloArgs);
+    static const Fn fns[2][3] = {{conv_halo_kernel<false, 0>, conv_halo_kernel<false, 1>, conv_halo_kernel<false, 2>},
+                                 {conv_halo_kernel<true, 0>, conv_halo_kernel<true, 1>, conv_halo_kernel<true, 2>}};
     static bool attr_set = false;
     if (!attr_set) {
-        for (int m = 0; m < 2; ++m) {
-            auto fn = m ? conv_halo_kernel<true> : conv_halo_kernel<false>;
-            cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-            if (e != cudaSuccess) return e;
-            cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-        }
+        for (int m = 0; m < 2; ++m)
+            for (int v = 0; v < 3; ++v) {
+                cudaError_t e = cudaFuncSetAttribute(fns[m][v], cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+                if (e != cudaSuccess) return e;
+                cudaFuncSetAttribute(fns[m][v], cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+            }
         attr_set = true;
     }
     cudaLaunchConfig_t cfg{};
@@ -504,8 +544,8 @@ cudaError_t launch_conv_halo(const HaloArgs &a, const CUtensorMap &tmA, const CU
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     const bool narrow = a.ck != kChunk || a.co_chunk != kChunk;
-    return cudaLaunchKernelEx(&cfg, narrow ? conv_halo_kernel<true> : conv_halo_kernel<false>, tmA, tmB, tmRes, tmOut,
-                              tmA1, tmB1, a);
+    const int var = a.epi == EPI_BN_PROJ_RELU ? 1 : (a.pool_out ? 2 : 0);
+    return cudaLaunchKernelEx(&cfg, fns[narrow ? 1 : 0][var], tmA, tmB, tmRes, tmOut, tmA1, tmB1, a);
 }
 
 }  // namespace slim

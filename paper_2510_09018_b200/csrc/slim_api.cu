@@ -340,7 +340,7 @@ slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, i
     const slim_config &c = ctx->cfg;
     DevLayer &L = *cc.L;
     static const bool no_proj = getenv("SLIM_HALO_NO_PROJ") != nullptr;
-    if (disabled || L.sh.k != 3 || L.sh.stride != 1 || cc.pool_out) return SLIM_EUNSUPPORTED;
+    if (disabled || L.sh.k != 3 || L.sh.stride != 1) return SLIM_EUNSUPPORTED;
     const bool proj = cc.epi == EPI_BN_PROJ_RELU;
     if (proj && (no_proj || cc.Lp->sh.k != 1 || cc.Lp->sh.stride != 2 || cc.Hp != 2 * cc.H || cc.Wp != 2 * cc.W))
         return SLIM_EUNSUPPORTED;
@@ -366,6 +366,9 @@ slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, i
         a.m_tiles = (B + a.tile_imgs - 1) / a.tile_imgs;
     }
     a.row_px = a.tile_imgs * W;
+    // fused pool: one image row per TMEM lane quarter (the 4x4 images of the last segment)
+    if (cc.pool_out && (a.tile_imgs == 1 || a.row_px != 32 || a.rows != 4)) return SLIM_EUNSUPPORTED;
+    a.pool_out = cc.pool_out;
     // N tile <= 128: three accumulators of it must fit the 512 TMEM columns
     // (128-channel layers: two N tiles of 64 keep two accumulator stages + the fused N=192 MMA,
     // measured faster than one tile of 128; 96 channels cannot split into 64-channel tiles)
@@ -482,7 +485,7 @@ slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, i
         }
         tB = &m;
     }
-    if (!encode_act_rowmajor(ctx, &tOut, cc.out, B, H, W, c_out, a.tile_imgs, a.rows, a.co_chunk))
+    if (!encode_act_rowmajor(ctx, &tOut, cc.pool_out ? cc.x : cc.out, B, H, W, c_out, a.tile_imgs, a.rows, a.co_chunk))
         return fail(ctx, SLIM_ECUDA, "cuTensorMapEncodeTiled(halo out) failed");
     tRes = tOut;
     if (cc.epi == EPI_BN_ADD_RELU &&
