@@ -66,16 +66,16 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
     constexpr bool pool = kVar == 2;   // fused global average pool instead of the store
     uint64_t *bars = reinterpret_cast<uint64_t *>(sBN + (proj ? 4 : 2) * a.c_out);
     const uint32_t bar0 = smem_u32(bars);
-    // barriers: a_full[4] a_empty[4] b_full[4] b_empty[4] t_full[2] t_empty[2] r_full[2] r_empty[2]
+    // barriers: a_full[4] a_empty[4] b_full[4] b_empty[4] t_full[4] t_empty[4] r_full[4] r_empty[4]
     auto a_full = [&](int i) { return bar0 + 8u * i; };
     auto a_empty = [&](int i) { return bar0 + 8u * (4 + i); };
     auto b_full = [&](int i) { return bar0 + 8u * (8 + i); };
     auto b_empty = [&](int i) { return bar0 + 8u * (12 + i); };
     auto t_full = [&](int i) { return bar0 + 8u * (16 + i); };
-    auto t_empty = [&](int i) { return bar0 + 8u * (18 + i); };
-    auto r_full = [&](int i) { return bar0 + 8u * (20 + i); };
-    auto r_empty = [&](int i) { return bar0 + 8u * (22 + i); };
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 24);
+    auto t_empty = [&](int i) { return bar0 + 8u * (20 + i); };
+    auto r_full = [&](int i) { return bar0 + 8u * (24 + i); };
+    auto r_empty = [&](int i) { return bar0 + 8u * (28 + i); };
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 32);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int total = a.m_tiles * a.n_tiles;
@@ -92,7 +92,7 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
             mbar_init(b_full(i), 1);
             mbar_init(b_empty(i), 1);
         }
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < 4; ++i) {
             mbar_init(t_full(i), 1);
             mbar_init(t_empty(i), kHaloEpiThreads / n_grp);
             mbar_init(r_full(i), 1);
@@ -363,9 +363,9 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
         }
     } else if (warp >= kEpiWarp0) {
         // ===================== epilogue (warps 4..19, four per TMEM lane quarter) ===
-        // n_grp == 2: warps 4-11 take the even tiles, 12-19 the odd ones (accumulator stage,
-        // residual slot, staging buffer and named barrier of their own), so two tiles'
-        // epilogues overlap; inside a group the warps of one lane quarter split the columns.
+        // n_grp (1, 2 or 4) tile groups: group g takes tiles ti = g mod n_grp with accumulator
+        // stages, residual slots, a staging buffer and a named barrier of its own, so n_grp tiles'
+        // epilogues overlap; inside a group the 4/n_grp warps of a lane quarter split the columns.
         const int q = warp & 3;
         const int quad = (warp - kEpiWarp0) >> 2;          // 0..3
         const int cw = 4 / n_grp;                           // column ways per group
@@ -514,7 +514,7 @@ size_t conv_halo_smem_bytes(const HaloArgs &a) {
     const int n_res = (a.epi == EPI_BN_ADD_RELU) ? a.res_slots : 0;
     return 1024 + static_cast<size_t>(a.sa) * a.a_slot + static_cast<size_t>(a.sb) * a.b_bytes +
            chunk * (a.epi_groups + n_res) +
-           (a.epi == EPI_BN_PROJ_RELU ? 16 : 8) * static_cast<size_t>(a.c_out) + 8 * 24 + 16;
+           (a.epi == EPI_BN_PROJ_RELU ? 16 : 8) * static_cast<size_t>(a.c_out) + 8 * 32 + 16;
 }
 
 cudaError_t launch_conv_halo(const HaloArgs &a, const CUtensorMap &tmA, const CUtensorMap &tmB,

@@ -401,7 +401,10 @@ slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, i
     a.kw_fuse = nofuse ? 1 : (3 * a.n_tile <= 256 ? 3 : (2 * a.n_tile <= 256 ? 2 : 1));
     a.acc_stride = a.kw_fuse > 1 ? a.n_tile : (a.n_tile + 31) / 32 * 32;
     a.stage_cols = (3 * a.acc_stride + (proj ? a.n_tile : 0) + 31) / 32 * 32;
-    a.acc_stages = 2 * a.stage_cols <= 512 ? 2 : 1;
+    // up to four accumulator stages (narrow layers): the MMA runs further ahead of the epilogue,
+    // whose per-tile latency chain (not its work) bounds narrow widths
+    static const int max_stages = getenv("SLIM_HALO_STAGES") ? atoi(getenv("SLIM_HALO_STAGES")) : 4;
+    a.acc_stages = (4 * a.stage_cols <= 512 && max_stages >= 4) ? 4 : (2 * a.stage_cols <= 512 && max_stages >= 2 ? 2 : 1);
     int cols = a.acc_stages * a.stage_cols, tc = 32;
     while (tc < cols) tc <<= 1;
     a.tmem_cols = tc;
@@ -418,18 +421,19 @@ slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, i
     a.n_out_chunks = static_cast<uint32_t>((a.n_tile + a.co_chunk - 1) / a.co_chunk);
     const size_t chunk = static_cast<size_t>(a.n_out_chunks) * 128 * a.rbo;
     static const bool one_group = getenv("SLIM_HALO_EPI1") != nullptr;
-    a.epi_groups = (!one_group && a.acc_stages == 2) ? 2 : 1;
+    a.epi_groups = one_group ? 1 : a.acc_stages;
     // narrow layers (exact 16/32-channel boxes): two CTAs per SM (smem and 2x256 TMEM columns fit)
     // (two CTAs per SM for narrow layers measured slower: SLIM_HALO_TWO=1 to try)
     static const bool two_cta = getenv("SLIM_HALO_TWO") != nullptr;
     const bool two = two_cta && a.n_tile <= 32 && a.ck <= 32;
     const size_t budget = two ? 110 * 1024 : 226 * 1024;
     auto fixed0 = [&]() {
-        return 1024 + chunk * a.epi_groups + (proj ? 16 : 8) * static_cast<size_t>(c_out) + 8 * 24 + 16;
+        return 1024 + chunk * a.epi_groups + (proj ? 16 : 8) * static_cast<size_t>(c_out) + 8 * 32 + 16;
     };
     auto r1k = [](uint32_t x) { return (x + 1023u) & ~1023u; };
     const uint32_t all_w = r1k(static_cast<uint32_t>(a.n_chunks) * 9u * a.n_tile * a.rbk);
-    a.res_slots = (cc.epi == EPI_BN_ADD_RELU) ? 2 : 0;
+    // residual slots: a multiple of the tile groups (each slot serves one group, parity waits)
+    a.res_slots = (cc.epi == EPI_BN_ADD_RELU) ? std::max(2, a.epi_groups) : 0;
     a.stationary = (nt == 1 && all_w <= 100 * 1024) ? 1 : 0;
     if (a.stationary) {
         a.b_bytes = all_w;
@@ -443,7 +447,11 @@ slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, i
         size_t left = budget - fixed0() - res;
         if (a.stationary) {
             if (left < a.b_bytes + 2 * a.a_slot) {
-                if (a.epi_groups == 2) { a.epi_groups = 1; continue; }
+                if (a.epi_groups > 1) {   // fewer tile groups (stages stay: a multiple of the groups)
+                    a.epi_groups >>= 1;
+                    if (a.res_slots) a.res_slots = std::max(2, a.epi_groups);
+                    continue;
+                }
                 if (a.res_slots == 2) { a.res_slots = 1; continue; }
                 return SLIM_EUNSUPPORTED;
             }
@@ -452,7 +460,11 @@ slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, i
             a.sa = a.sa > 4 ? 4 : a.sa;
         } else {
             if (left < 2 * a.a_slot + 2 * a.b_bytes) {
-                if (a.epi_groups == 2) { a.epi_groups = 1; continue; }
+                if (a.epi_groups > 1) {   // fewer tile groups (stages stay: a multiple of the groups)
+                    a.epi_groups >>= 1;
+                    if (a.res_slots) a.res_slots = std::max(2, a.epi_groups);
+                    continue;
+                }
                 if (a.res_slots == 2) { a.res_slots = 1; continue; }
                 return SLIM_EUNSUPPORTED;
             }
