@@ -380,6 +380,17 @@ slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, i
         if (c_out % nt || (c_out / nt) % 16 || (nt > 1 && (c_out / nt) % 64)) continue;
         if (c_out / nt <= halo_nmax) break;
     }
+    // too few tiles to fill the SMs (narrow late layers): narrower N tiles of 32 / 16 channels with
+    // exact-width output boxes -- each CTA's serial latency chain (MMA, epilogue) shrinks with it
+    static const bool no_fill = getenv("SLIM_HALO_NOFILL") != nullptr;
+    bool narrow_out = false;
+    if (!no_fill && a.m_tiles * nt * 10 < ctx->num_sms * 8 && !cc.pool_out)
+        for (int n2 : {32, 16}) {
+            if (n2 >= c_out / nt || c_out % n2 || a.m_tiles * (c_out / n2) > ctx->num_sms) continue;   // one wave
+            nt = c_out / n2;
+            narrow_out = true;
+            if (a.m_tiles * nt * 10 >= ctx->num_sms * 8) break;
+        }
     a.n_tile = c_out / nt;
     a.n_tiles = nt;
     a.c_out = c_out;
@@ -390,7 +401,7 @@ slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, i
     a.ck = hch(cc.c_in);
     a.rbk = 2 * a.ck;
     a.n_chunks = (cc.c_in + a.ck - 1) / a.ck;
-    a.co_chunk = hch(a.n_tile);
+    a.co_chunk = narrow_out ? a.n_tile : hch(a.n_tile);
     a.rbo = 2 * a.co_chunk;
     a.epi = cc.epi;
     a.scale = L.scale[ri];
