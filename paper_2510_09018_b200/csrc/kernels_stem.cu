@@ -8,8 +8,8 @@
 // Persistent, warp-specialised, one CTA per SM:
 //   warp 0      TMA producer: input halo ring (4 slots)
 //   warp 1      MMA issuer: NK = K/16 MMAs (M=128, N=c0) per tile into 2 TMEM accumulator stages
-//   warps 4-7   im2col builders: halo -> SW128 K-major A ring (3 slots)
-//   warps 8-11  epilogue: TMEM -> fp32 BN + ReLU -> bf16 -> SW128 staging (2 slots) -> TMA store
+//   warps 4-7, 16-19  im2col builders, two tile groups: halo -> SW128 K-major A ring (4 slots)
+//   warps 8-15  epilogue, two tile groups: TMEM -> fp32 BN + ReLU -> bf16 -> SW128 staging -> TMA store
 // so the fetch, build, MMA and store of consecutive tiles overlap.
 #include "slim_internal.h"
 #include "ptx_sm100.cuh"
@@ -18,8 +18,8 @@ namespace slim {
 using namespace ptx;
 namespace {
 
-constexpr int kStemThreads = 384;
-constexpr int kInSlots = 4, kASlots = 3, kAccStages = 2, kOutSlots = 2;
+constexpr int kStemThreads = 640;   // warps 0 TMA, 1 MMA, 4-7 + 16-19 im2col, 8-15 epilogue (two tile groups)
+constexpr int kInSlots = 4, kASlots = 4, kAccStages = 2, kOutSlots = 2;   // slots: multiples of the 2 groups
 constexpr uint32_t kInSlotBytes = 1536;   // (128/W + 2) * W * c_img * 2 <= (128 + 64) * 4 * 2
 
 template <int CIMG>
@@ -45,19 +45,18 @@ __global__ void __launch_bounds__(kStemThreads, 1)
     auto t_empty = [&](int i) { return bar0 + 8u * (2 * kInSlots + 2 * kASlots + kAccStages + i); };
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    // diagnostics: td[role*64 + tile] of CTA 0 (role 0 halo issued, 1 built, 2 MMA issued, 3 stored)
+    unsigned long long *td = (a.trace && blockIdx.x == 0) ? a.trace + 3584 : nullptr;
+    if (td && tid == 0) td[4 * 64] = gtimer();
     const int W = a.W, rows = a.tile_rows, c0 = a.c0;
     const int acc_cols = (c0 + 31) & ~31;   // TMEM columns per accumulator stage
     const int tiles_per_img = a.H / rows;
     const uint32_t in_bytes = static_cast<uint32_t>((rows + 2) * W * CIMG * 2);
 
     // ---- prologue (weights and BN are not produced by the previous kernel: before the PDL wait)
-    for (int i = tid; i < 8192 / 16; i += kStemThreads) reinterpret_cast<uint4 *>(pB)[i] = make_uint4(0, 0, 0, 0);
-    __syncthreads();
-    for (int i = tid; i < c0 * K; i += kStemThreads) {
-        const int co = i / K, k = i - co * K;
-        *reinterpret_cast<__nv_bfloat16 *>(pB + co * 128 + (((k >> 3) ^ (co & 7)) << 4) + (k & 7) * 2) =
-            __float2bfloat16_rn(a.w[static_cast<size_t>(co) * a.w_stride + k]);
-    }
+    // the B tile: a straight copy of the image built at load time (rows < c0 are read)
+    for (int i = tid; i < c0 * 8; i += kStemThreads)
+        reinterpret_cast<uint4 *>(pB)[i] = reinterpret_cast<const uint4 *>(a.b_img)[i];
     for (int i = tid; i < c0; i += kStemThreads) {
         sBN[i] = a.scale[i];
         sBN[64 + i] = a.shift[i];
@@ -90,6 +89,7 @@ __global__ void __launch_bounds__(kStemThreads, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    if (td && tid == 0) td[4 * 64 + 1] = gtimer();
     pdl_wait();   // the output buffer may still be read by the previous kernel; the image may be its output
     pdl_launch_dependents();
 
@@ -103,6 +103,7 @@ __global__ void __launch_bounds__(kStemThreads, 1)
                 mbar_wait(in_empty(s), ph ^ 1);
                 mbar_expect_tx(in_full(s), in_bytes);
                 tma_load_3d(smem_u32(pIn + s * kInSlotBytes), &tmIn, in_full(s), 0, h0 - 1, n);
+                if (td) td[(t - blockIdx.x) / gridDim.x] = gtimer();
                 if (++s == kInSlots) {
                     s = 0;
                     ph ^= 1;
@@ -126,6 +127,7 @@ __global__ void __launch_bounds__(kStemThreads, 1)
                     umma_bf16(tmem + static_cast<uint32_t>(as * acc_cols), ad + 2 * kk, bd + 2 * kk, idesc, kk > 0);
                 umma_commit(a_empty(s));
                 umma_commit(t_full(as));
+                if (td) td[2 * 64 + (t - blockIdx.x) / gridDim.x] = gtimer();
             }
             __syncwarp();
             if (++s == kASlots) {
@@ -137,13 +139,17 @@ __global__ void __launch_bounds__(kStemThreads, 1)
                 aph ^= 1;
             }
         }
-    } else if (warp >= 4 && warp < 8) {
-        // ===================== im2col builders: one output pixel (A row) per thread ======
-        const int row = tid - 128, sw = row & 7;
+    } else if ((warp >= 4 && warp < 8) || warp >= 16) {
+        // ===================== im2col builders: one output pixel (A row) per thread =======
+        // two groups: warps 4-7 build the even tiles, 16-19 the odd ones (input / A slots
+        // ti mod 4 are then always the same group's, so the parity waits stay in order)
+        const int bg = warp >= 16 ? 1 : 0;
+        const int row = tid - (bg ? 512 : 128), sw = row & 7;
         const int r_pix = row / W, c_pix = row - r_pix * W;
-        int s = 0, as = 0;
-        uint32_t ph = 0, aph = 0;
-        for (int t = blockIdx.x; t < a.m_tiles; t += gridDim.x) {
+        for (int t = blockIdx.x + bg * gridDim.x; t < a.m_tiles; t += 2 * gridDim.x) {
+            const int ti = (t - blockIdx.x) / gridDim.x;
+            const int s = ti % kInSlots, as = ti % kASlots;
+            const uint32_t ph = (ti / kInSlots) & 1, aph = (ti / kASlots) & 1;
             mbar_wait(in_full(s), ph);
             const uint16_t *hb = reinterpret_cast<const uint16_t *>(pIn + s * kInSlotBytes);
             uint32_t packed[NK * 8];
@@ -164,10 +170,6 @@ __global__ void __launch_bounds__(kStemThreads, 1)
                     }
                 }
             mbar_arrive(in_empty(s));   // halo slot consumed
-            if (++s == kInSlots) {
-                s = 0;
-                ph ^= 1;
-            }
             mbar_wait(a_empty(as), aph ^ 1);
             uint8_t *dst = pA + as * 16384 + row * 128;
 #pragma unroll
@@ -176,25 +178,25 @@ __global__ void __launch_bounds__(kStemThreads, 1)
                     make_uint4(packed[4 * j], packed[4 * j + 1], packed[4 * j + 2], packed[4 * j + 3]);
             fence_proxy_async();        // generic smem writes -> visible to the tensor core
             mbar_arrive(a_full(as));
-            if (++as == kASlots) {
-                as = 0;
-                aph ^= 1;
-            }
+            if (td && row == 0) td[64 + ti] = gtimer();
         }
-    } else if (warp >= 8) {
-        // ===================== epilogue ================================================
+    } else if (warp >= 8 && warp < 16) {
+        // ===================== epilogue: warps 8-11 take the even tiles, 12-15 the odd ones ====
+        const int grp = (warp - 8) >> 2;
         const int q = warp & 3, row = q * 32 + lane, sw = row & 7;
-        const bool leader = (warp == 8 && lane == 0);
+        const bool leader = (warp == 8 + 4 * grp && lane == 0);
         const uint32_t lane_addr = tmem + (static_cast<uint32_t>(q * 32) << 16);
-        int as = 0, os = 0;
-        uint32_t aph = 0;
-        for (int t = blockIdx.x; t < a.m_tiles; t += gridDim.x) {
+        uint8_t *pOutG = pOut + grp * 16384;   // staging slot of this group
+        for (int t = blockIdx.x + grp * gridDim.x; t < a.m_tiles; t += 2 * gridDim.x) {
             const int n = t / tiles_per_img, h0 = (t - n * tiles_per_img) * rows;
+            const int ti = (t - blockIdx.x) / gridDim.x;
+            const int as = ti & 1;                          // accumulator stage = tile parity = group
+            const uint32_t aph = (ti >> 1) & 1;
             mbar_wait(t_full(as), aph);
             tc_fence_after();
-            if (leader) bulk_wait_read<kOutSlots - 1>();   // the store that last used slot os has read it
-            named_bar_sync(1, 128);
-            uint8_t *rowp = pOut + os * 16384 + row * 128;
+            if (leader) bulk_wait_read0();   // this group's previous store has left the staging slot
+            named_bar_sync(1 + grp, 128);
+            uint8_t *rowp = pOutG + row * 128;
             for (int g = 0; g < c0 / 16; ++g) {
                 uint32_t v[16];
                 tmem_ld16(lane_addr + static_cast<uint32_t>(as * acc_cols + g * 16), v);
@@ -213,21 +215,18 @@ __global__ void __launch_bounds__(kStemThreads, 1)
             tc_fence_before();
             mbar_arrive(t_empty(as));
             fence_proxy_async();
-            named_bar_sync(1, 128);
+            named_bar_sync(1 + grp, 128);
             if (leader) {
-                tma_store_4d(&tmOut, smem_u32(pOut + os * 16384), 0, 0, h0, n);
+                tma_store_4d(&tmOut, smem_u32(pOutG), 0, 0, h0, n);
                 bulk_commit();
+                if (td) td[3 * 64 + ti] = gtimer();
             }
-            if (++as == kAccStages) {
-                as = 0;
-                aph ^= 1;
-            }
-            if (++os == kOutSlots) os = 0;
         }
         if (leader) bulk_wait0();
     }
     tc_fence_before();
     __syncthreads();
+    if (td && tid == 0) td[4 * 64 + 2] = gtimer();
     if (warp == 1) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(a.tmem_cols) : "memory");

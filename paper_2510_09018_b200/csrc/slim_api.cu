@@ -44,6 +44,7 @@ struct DevLayer {
     bool tm_ok[kMaxW][kMaxW][17] = {};
     CUtensorMap tmh[kMaxW][9][2];            // halo-kernel weight maps per (r idx, n_tile/16 - 1 (<=128), taps 3|9)
     bool tmh_ok[kMaxW][9][2] = {};
+    void *stem_b = nullptr;                  // stem: the UMMA B operand image (64 rows x 128 B, SW128, bf16, K zero-padded)
     CUtensorMap tms[kMaxW][kMaxW];           // split-K kernel weight maps (64-channel boxes) per (r_prev idx, r idx)
     bool tms_ok[kMaxW][kMaxW] = {};
 };
@@ -519,7 +520,7 @@ slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, i
     if (grid > total) grid = total;
     double flops, bytes;
     conv_work(c, cc, ri, B, H, W, &flops, &bytes);
-    if (ctx->trace) cudaMemsetAsync(ctx->trace, 0, 4096 * 8 * sizeof(unsigned long long), st);   // diagnostics
+    if (ctx->trace) cudaMemsetAsync(ctx->trace, 0, 3584 * sizeof(unsigned long long), st);   // diagnostics (stem: 3584..)
     LaunchProf prof(ctx, st);
     CUtensorMap tA1 = tA, tB1 = tA;
     if (proj) {
@@ -854,7 +855,7 @@ slim_status conv_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, int ri
     }
     double flops, bytes;
     conv_work(c, cc, ri, B, Ho, Wo, &flops, &bytes);
-    if (ctx->trace) cudaMemsetAsync(ctx->trace, 0, 4096 * 8 * sizeof(unsigned long long), st);   // diagnostics
+    if (ctx->trace) cudaMemsetAsync(ctx->trace, 0, 3584 * sizeof(unsigned long long), st);   // diagnostics (stem: 3584..)
     LaunchProf prof(ctx, st);
     cudaError_t e = launch_conv_umma(a, tA0, *tB0, tA1, *tB1, tRes, tOut, grid, st, ctx->pdl && !ctx->prof_on);
     prof.done(SLIM_K_CONV_UMMA, cc.seg, cc.layer, c.widths[cc.ri_in], c.widths[ri], B, flops, bytes);
@@ -960,6 +961,7 @@ slim_status run_segment(slim_ctx *ctx, int seg, int ri_prev, int ri, int B, cons
             StemArgs sa{};
             sa.in = static_cast<const uint16_t *>(in);
             sa.w = static_cast<const float *>(Ls.w);
+            sa.b_img = Ls.stem_b;
             sa.w_stride = 9 * Ls.sh.cin;
             sa.scale = Ls.scale[ri];
             sa.shift = Ls.shift[ri];
@@ -971,6 +973,8 @@ slim_status run_segment(slim_ctx *ctx, int seg, int ri_prev, int ri, int B, cons
             sa.tile_rows = kTileM / H;
             sa.m_tiles = B * (H / sa.tile_rows);
             sa.tmem_cols = C <= 16 ? 64 : 128;   // two accumulator stages of round32(C) columns
+            sa.trace = ctx->trace;
+            if (ctx->trace) cudaMemsetAsync(ctx->trace + 3584, 0, 512 * sizeof(unsigned long long), st);
             CUtensorMap tIn, tOut;
             {   // the image as flat rows: (W*cimg, H, B), box = the tile's rows plus the 3x3 halo
                 const cuuint64_t rowe = static_cast<cuuint64_t>(H) * c.in_channels;
@@ -1121,6 +1125,7 @@ void free_segment(DevSegment &S) {
     for (int l = 0; l < S.n_conv; ++l) {
         DevLayer &L = S.L[l];
         cudaFree(L.w);
+        cudaFree(L.stem_b);
         for (int i = 0; i < kMaxW; ++i) {
             cudaFree(L.scale[i]);
             cudaFree(L.shift[i]);
@@ -1284,6 +1289,18 @@ slim_status slim_load_segment(slim_ctx *ctx, int seg, const slim_seg_weights *w,
                 for (auto &v : h) v = bf_round(v);
             CUDA_TRY(ctx, cudaMalloc(&L.w, cnt * 4));
             CUDA_TRY(ctx, cudaMemcpy(L.w, h.data(), cnt * 4, cudaMemcpyHostToDevice));
+            if (L.sh.is_stem && bf && L.sh.cout <= 64 && 9 * L.sh.cin <= 64) {
+                // the stem's B operand as the kernel's shared-memory image: row co (K-major, 128 B) holds
+                // w[co][k] for k < 9*c_img, 16-B piece j at (j ^ (co & 7)) (SWIZZLE_128B); rows >= c0 of a
+                // width are never read (N = c0)
+                std::vector<uint16_t> img(64 * 64, 0);
+                const int K = 9 * L.sh.cin;
+                for (int co = 0; co < L.sh.cout; ++co)
+                    for (int k = 0; k < K; ++k)
+                        img[co * 64 + (((k >> 3) ^ (co & 7)) << 3) + (k & 7)] = f2bf(h[static_cast<size_t>(co) * K + k]);
+                CUDA_TRY(ctx, cudaMalloc(&L.stem_b, img.size() * 2));
+                CUDA_TRY(ctx, cudaMemcpy(L.stem_b, img.data(), img.size() * 2, cudaMemcpyHostToDevice));
+            }
         } else {
             std::vector<uint16_t> h(cnt);
             for (size_t i = 0; i < cnt; ++i) h[i] = f2bf(w->conv_w[l][i]);

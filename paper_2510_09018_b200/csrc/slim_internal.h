@@ -126,10 +126,12 @@ int conv_umma_max_ctas_per_sm(size_t smem_bytes);
 struct StemArgs {
     const uint16_t *in;            // [B][H][W][cimg] bf16
     const float *w;                // [c0_full][9*cimg] fp32 (bf16-representable), rows >= c0 unread
+    const void *b_img;             // the same weights as the kernel's SW128 bf16 B tile (8 KiB, built at load)
     int w_stride;                  // 9*cimg_full
     const float *scale, *shift;    // folded BN at this width, c0 entries
     int B, H, W, cimg, c0;
     int tile_rows, m_tiles, tmem_cols;
+    unsigned long long *trace;     // diagnostics only (SLIM_CONV_TRACE): CTA 0 role x tile %globaltimer stamps
 };
 // (kernels_stem.cu) tmIn: the image as a 3-D map (W*cimg, H, B), box (W*cimg, tile_rows+2, 1), no swizzle
 cudaError_t launch_stem_umma(const StemArgs &a, const CUtensorMap &tmIn, const CUtensorMap &tmOut, int grid,
