@@ -38,7 +38,8 @@ constexpr int kHaloEpiThreads = kHaloEpiWarps * 32;
 constexpr int kHaloThreads = (4 + kHaloEpiWarps) * 32;   // warps 0 A, 1 MMA, 2 B, 3 residual, 4..19 epilogue
 
 // kNarrow: runtime channel-chunk geometry (16/32-channel boxes); false folds 64-channel / 128-B rows.
-// kVar: 0 = plain / residual epilogue, 1 = + projection shortcut, 2 = + fused average pool
+// kVar: 0 = plain / residual epilogue, 1 = + projection shortcut, 2 = + fused average pool,
+// 3 = stride-2 conv (parity planes, see below)
 // (compile-time, so the common variant carries none of the other two's code)
 template <bool kNarrow, int kVar>
 __global__ void __launch_bounds__(kHaloThreads, 1)
@@ -64,6 +65,14 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
     float *sBN = reinterpret_cast<float *>(pRes + n_res * chunk_bytes);
     constexpr bool proj = kVar == 1;   // + 1x1 stride-2 projection shortcut (4th accumulator)
     constexpr bool pool = kVar == 2;   // fused global average pool instead of the store
+    // kVar 3: stride-2 conv (block-0 conv1 of segments 1-3).  The input splits into row-parity x
+    // column-parity planes, each one TMA box with traversal stride 2: per chunk an "odd-row pair"
+    // slot (rows 2h-1, rows+1 of them; odd | even columns) serves kh = 0 and 2 (row offsets 0, 1)
+    // and an "even-row pair" slot (rows 2h) serves kh = 1.  kw = 0 and 2 read the odd columns
+    // (2w-1 = odd col w-1, 2w+1 = odd col w): one MMA of N = 2n into [acc_kw0 | acc_kw2]; kw = 1
+    // reads the even columns: one MMA of N = n into acc_kw1.  Epilogue: acc_kw0[w-1] + acc_kw2[w]
+    // + acc_kw1[w].  A traffic = the input once (4x the output tile) instead of 9x.
+    constexpr bool s2 = kVar == 3;
     uint64_t *bars = reinterpret_cast<uint64_t *>(sBN + (proj ? 4 : 2) * a.c_out);
     const uint32_t bar0 = smem_u32(bars);
     // barriers: a_full[4] a_empty[4] b_full[4] b_empty[4] t_full[4] t_empty[4] r_full[4] r_empty[4]
@@ -124,7 +133,16 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
         // exact box bytes (the slot itself is rounded up to 1 KiB)
         mbar_expect_tx(b_full(0), static_cast<uint32_t>(a.n_chunks) * 9u * a.n_tile * RBK);
         const uint32_t per_chunk = 9u * a.n_tile * RBK;
-        for (int ch = 0; ch < a.n_chunks; ++ch) tma_load_3d(sB + ch * per_chunk, &tmB, b_full(0), ch * CK, 0, 0);
+        if (!s2) {
+            for (int ch = 0; ch < a.n_chunks; ++ch) tma_load_3d(sB + ch * per_chunk, &tmB, b_full(0), ch * CK, 0, 0);
+        } else {   // one-tap boxes, per kh in the order kw = 0, 2, 1
+            const uint32_t tapb = static_cast<uint32_t>(a.n_tile) * RBK;
+            for (int ch = 0; ch < a.n_chunks; ++ch)
+                for (int kh = 0; kh < 3; ++kh)
+                    for (int j = 0; j < 3; ++j)
+                        tma_load_3d(sB + ch * per_chunk + (kh * 3 + j) * tapb, &tmB, b_full(0), ch * CK, 0,
+                                    kh * 3 + (j == 0 ? 0 : (j == 1 ? 2 : 1)));
+        }
     }
     tc_fence_before();
     __syncthreads();
@@ -145,11 +163,33 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
                 const int n = mt / tiles_per_img, h0 = (mt - n * tiles_per_img) * a.rows;
                 const int ti = (t - blockIdx.x) / gridDim.x;
                 TD(0, ti, 0);
-                for (int ch = 0; ch < a.n_chunks; ++ch) {
+                for (int ch = 0; ch < a.n_chunks && !s2; ++ch) {
                     mbar_wait(a_empty(s), ph ^ 1);
                     if (ch == 0) TD(0, ti, 2);
                     mbar_expect_tx(a_full(s), a.a_bytes);
                     tma_load_4d(sA + s * a.a_slot, &tmA, a_full(s), ch * CK, 0, n * a.tile_imgs, h0 - 1);
+                    if (++s == a.sa) {
+                        s = 0;
+                        ph ^= 1;
+                    }
+                }
+                for (int ch = 0; ch < a.n_chunks && s2; ++ch) {
+                    // odd-row pair (tmA1: rows+1 rows from input row 2h0-1), then even-row pair
+                    // (tmA: rows rows from 2h0); each pair = odd-column plane, even-column plane
+                    const uint32_t oplane = static_cast<uint32_t>((a.rows + 1) * a.row_px) * RBK;
+                    const uint32_t eplane = static_cast<uint32_t>(a.rows * a.row_px) * RBK;
+                    mbar_wait(a_empty(s), ph ^ 1);
+                    mbar_expect_tx(a_full(s), 2u * oplane);
+                    tma_load_4d(sA + s * a.a_slot, &tmA1, a_full(s), ch * CK, 1, n * a.tile_imgs, 2 * h0 - 1);
+                    tma_load_4d(sA + s * a.a_slot + oplane, &tmA1, a_full(s), ch * CK, 0, n * a.tile_imgs, 2 * h0 - 1);
+                    if (++s == a.sa) {
+                        s = 0;
+                        ph ^= 1;
+                    }
+                    mbar_wait(a_empty(s), ph ^ 1);
+                    mbar_expect_tx(a_full(s), 2u * eplane);
+                    tma_load_4d(sA + s * a.a_slot, &tmA, a_full(s), ch * CK, 1, n * a.tile_imgs, 2 * h0);
+                    tma_load_4d(sA + s * a.a_slot + eplane, &tmA, a_full(s), ch * CK, 0, n * a.tile_imgs, 2 * h0);
                     if (++s == a.sa) {
                         s = 0;
                         ph ^= 1;
@@ -204,10 +244,18 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
             for (int t = blockIdx.x; t < total; t += gridDim.x) {
                 const int co0 = (t / a.m_tiles) * a.n_tile;
                 for (int ch = 0; ch < a.n_chunks; ++ch)
-                    for (int kh = 0; kh < 3; ++kh) {
+                    for (int kq = 0; kq < 3; ++kq) {
+                        const int kh = s2 ? (kq == 0 ? 0 : (kq == 1 ? 2 : 1)) : kq;   // s2 consumes kh 0, 2, 1
                         mbar_wait(b_empty(s), ph ^ 1);
                         mbar_expect_tx(b_full(s), 3u * a.n_tile * RBK);
-                        tma_load_3d(sB + s * a.b_bytes, &tmB, b_full(s), ch * CK, co0, kh * 3);
+                        if (!s2) {
+                            tma_load_3d(sB + s * a.b_bytes, &tmB, b_full(s), ch * CK, co0, kh * 3);
+                        } else {   // one-tap boxes in the order kw = 0, 2, 1
+                            const uint32_t tapb = static_cast<uint32_t>(a.n_tile) * RBK;
+                            tma_load_3d(sB + s * a.b_bytes, &tmB, b_full(s), ch * CK, co0, kh * 3);
+                            tma_load_3d(sB + s * a.b_bytes + tapb, &tmB, b_full(s), ch * CK, co0, kh * 3 + 2);
+                            tma_load_3d(sB + s * a.b_bytes + 2 * tapb, &tmB, b_full(s), ch * CK, co0, kh * 3 + 1);
+                        }
                         if (++s == a.sb) {
                             s = 0;
                             ph ^= 1;
@@ -245,7 +293,57 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
                 if (lane == 0) TD(1, ti, 1);
                 tc_fence_after();
                 const uint32_t acc = tmem_base + static_cast<uint32_t>(as * a.stage_cols);
-                for (int ch = 0; ch < a.n_chunks; ++ch) {
+                if (s2) {
+                    const uint32_t idesc2 = umma_idesc_bf16(kTileM, 2 * a.n_tile), idesc1 = umma_idesc_bf16(kTileM, a.n_tile);
+                    const uint32_t oplane16 = static_cast<uint32_t>((a.rows + 1) * a.row_px * RBK) >> 4;
+                    const uint32_t eplane16 = static_cast<uint32_t>(a.rows * a.row_px * RBK) >> 4;
+                    for (int ch = 0; ch < a.n_chunks; ++ch) {
+                        const int nk = min(kmax, (a.c_in - ch * CK + 15) >> 4);
+                        for (int pr = 0; pr < 2; ++pr) {   // pr 0: odd-row pair (kh 0, 2), pr 1: even-row pair (kh 1)
+                            mbar_wait(a_full(s), ph);
+                            tc_fence_after();
+                            const uint64_t ad = adesc0 + s * a_slot16;
+                            const uint32_t plane16 = pr ? eplane16 : oplane16;
+                            for (int q = 0; q < (pr ? 1 : 2); ++q) {
+                                const int kh = pr ? 1 : 2 * q;
+                                const uint32_t roff = (kh == 2) ? row16 : 0u;
+                                uint64_t bk;
+                                if (a.stationary) {
+                                    bk = bdesc0 + static_cast<uint32_t>(ch * 9 + kh * 3) * tap16;
+                                } else {
+                                    mbar_wait(b_full(bs), bph);
+                                    tc_fence_after();
+                                    bk = bdesc0 + bs * b_slot16;
+                                }
+                                if (elect_one() && !(a.debug & 2)) {
+                                    for (int kk = 0; kk < nk; ++kk) {
+                                        const bool accum = (ch | kh | kk) != 0;
+                                        // odd columns -> [acc_kw0 | acc_kw2], even columns -> acc_kw1
+                                        umma_bf16(acc, ad + roff + 2 * kk, bk + 2 * kk, idesc2, accum);
+                                        umma_bf16(acc + 2 * accs, ad + plane16 + roff + 2 * kk, bk + 2 * tap16 + 2 * kk,
+                                                  idesc1, accum);
+                                    }
+                                }
+                                __syncwarp();
+                                if (!a.stationary) {
+                                    if (elect_one()) umma_commit(b_empty(bs));
+                                    __syncwarp();
+                                    if (++bs == a.sb) {
+                                        bs = 0;
+                                        bph ^= 1;
+                                    }
+                                }
+                            }
+                            if (elect_one()) umma_commit(a_empty(s));
+                            __syncwarp();
+                            if (++s == a.sa) {
+                                s = 0;
+                                ph ^= 1;
+                            }
+                        }
+                    }
+                }
+                for (int ch = 0; ch < a.n_chunks && !s2; ++ch) {
                     const int nk = min(kmax, (a.c_in - ch * CK + 15) >> 4);
                     mbar_wait(a_full(s), ph);
                     if (ch == 0 && lane == 0) TD(1, ti, 2);
@@ -415,8 +513,13 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
                 for (int i = 0; i < 16; ++i) {
                     // out[w] = acc_0[w-1] + acc_1[w] + acc_2[w+1]  (zero padding at the row ends)
                     const float left = __shfl_up_sync(0xffffffffu, __uint_as_float(v0[i]), 1);
-                    const float right = __shfl_down_sync(0xffffffffu, __uint_as_float(v2[i]), 1);
-                    const float y = fmaf(mR, right, fmaf(mL, left, __uint_as_float(v1[i])));
+                    float y;
+                    if (s2) {   // acc_kw0[w-1] + acc_kw2[w] + acc_kw1[w]
+                        y = fmaf(mL, left, __uint_as_float(v1[i]) + __uint_as_float(v2[i]));
+                    } else {
+                        const float right = __shfl_down_sync(0xffffffffu, __uint_as_float(v2[i]), 1);
+                        y = fmaf(mR, right, fmaf(mL, left, __uint_as_float(v1[i])));
+                    }
                     f[i] = fmaf(y, s0[cg + i], t0[cg + i]);
                 }
                 if (proj) {   // + s_sc * proj + t_sc (the shortcut's own BN)
@@ -521,12 +624,14 @@ cudaError_t launch_conv_halo(const HaloArgs &a, const CUtensorMap &tmA, const CU
                              const CUtensorMap &tmRes, const CUtensorMap &tmOut, const CUtensorMap &tmA1,
                              const CUtensorMap &tmB1, int grid, cudaStream_t stream, bool pdl) {
     using Fn = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, HaloArgs);
-    static const Fn fns[2][3] = {{conv_halo_kernel<false, 0>, conv_halo_kernel<false, 1>, conv_halo_kernel<false, 2>},
-                                 {conv_halo_kernel<true, 0>, conv_halo_kernel<true, 1>, conv_halo_kernel<true, 2>}};
+    static const Fn fns[2][4] = {{conv_halo_kernel<false, 0>, conv_halo_kernel<false, 1>, conv_halo_kernel<false, 2>,
+                                  conv_halo_kernel<false, 3>},
+                                 {conv_halo_kernel<true, 0>, conv_halo_kernel<true, 1>, conv_halo_kernel<true, 2>,
+                                  conv_halo_kernel<true, 3>}};
     static bool attr_set = false;
     if (!attr_set) {
         for (int m = 0; m < 2; ++m)
-            for (int v = 0; v < 3; ++v) {
+            for (int v = 0; v < 4; ++v) {
                 cudaError_t e = cudaFuncSetAttribute(fns[m][v], cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
                 if (e != cudaSuccess) return e;
                 cudaFuncSetAttribute(fns[m][v], cudaFuncAttributePreferredSharedMemoryCarveout, 100);
@@ -544,7 +649,7 @@ cudaError_t launch_conv_halo(const HaloArgs &a, const CUtensorMap &tmA, const CU
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     const bool narrow = a.ck != kChunk || a.co_chunk != kChunk;
-    const int var = a.epi == EPI_BN_PROJ_RELU ? 1 : (a.pool_out ? 2 : 0);
+    const int var = a.stride2 ? 3 : (a.epi == EPI_BN_PROJ_RELU ? 1 : (a.pool_out ? 2 : 0));
     return cudaLaunchKernelEx(&cfg, fns[narrow ? 1 : 0][var], tmA, tmB, tmRes, tmOut, tmA1, tmB1, a);
 }
 

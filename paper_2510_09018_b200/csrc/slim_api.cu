@@ -341,11 +341,14 @@ slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, i
     const slim_config &c = ctx->cfg;
     DevLayer &L = *cc.L;
     static const bool no_proj = getenv("SLIM_HALO_NO_PROJ") != nullptr;
-    if (disabled || L.sh.k != 3 || L.sh.stride != 1) return SLIM_EUNSUPPORTED;
+    static const bool no_s2 = getenv("SLIM_HALO_NO_S2") != nullptr;
+    if (disabled || L.sh.k != 3 || (L.sh.stride != 1 && L.sh.stride != 2)) return SLIM_EUNSUPPORTED;
+    const bool s2 = L.sh.stride == 2;   // stride-2 conv1 (parity planes): plain BN + ReLU epilogue only
+    if (s2 && (no_s2 || cc.epi != EPI_BN_RELU || cc.pool_out || cc.H % 2 || cc.W % 2)) return SLIM_EUNSUPPORTED;
     const bool proj = cc.epi == EPI_BN_PROJ_RELU;
     if (proj && (no_proj || cc.Lp->sh.k != 1 || cc.Lp->sh.stride != 2 || cc.Hp != 2 * cc.H || cc.Wp != 2 * cc.W))
         return SLIM_EUNSUPPORTED;
-    const int H = cc.H, W = cc.W;
+    const int H = s2 ? cc.H / 2 : cc.H, W = s2 ? cc.W / 2 : cc.W;   // output size
     static const bool no_small = getenv("SLIM_HALO_NO_SMALL") != nullptr;   // A/B: small images via per-tap conv
     if (W > 32 || 32 % W) return SLIM_EUNSUPPORTED;
     const int c_out = slim_channels(c.widths[ri], L.sh.cout);
@@ -411,6 +414,11 @@ slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, i
     // tap blocks of B adjacent in smem) unless SLIM_HALO_NOFUSE
     static const bool nofuse = getenv("SLIM_HALO_NOFUSE") != nullptr;
     a.kw_fuse = nofuse ? 1 : (3 * a.n_tile <= 256 ? 3 : (2 * a.n_tile <= 256 ? 2 : 1));
+    if (s2) {   // [acc_kw0 | acc_kw2 | acc_kw1] adjacent; kw 0 and 2 as one N = 2n MMA
+        if (2 * a.n_tile > 256) return SLIM_EUNSUPPORTED;
+        a.kw_fuse = 3;
+        a.stride2 = 1;
+    }
     a.acc_stride = a.kw_fuse > 1 ? a.n_tile : (a.n_tile + 31) / 32 * 32;
     a.stage_cols = (3 * a.acc_stride + (proj ? a.n_tile : 0) + 31) / 32 * 32;
     // up to four accumulator stages (narrow layers): the MMA runs further ahead of the epilogue,
@@ -421,6 +429,7 @@ slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, i
     while (tc < cols) tc <<= 1;
     a.tmem_cols = tc;
     a.a_bytes = static_cast<uint32_t>(kTileM + 2 * a.row_px) * a.rbk;
+    if (s2) a.a_bytes = 2u * static_cast<uint32_t>((a.rows + 1) * a.row_px) * a.rbk;   // odd-row pair (the larger)
     a.a_slot = (a.a_bytes + 1023u) & ~1023u;
     if (proj) {   // a projection chunk = 128 px x 64 ch + its n_tile x 64 weights in one slot
         if (a.ck != kChunk) return SLIM_EUNSUPPORTED;
@@ -493,12 +502,19 @@ slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, i
     a.debug = conv_debug;
     a.trace = ctx->trace;
 
-    CUtensorMap tA, tRes, tOut;
-    if (!encode_act_rowmajor(ctx, &tA, cc.x, B, H, W, cc.c_in, a.tile_imgs, a.rows + 2, a.ck))
+    CUtensorMap tA, tRes, tOut, tA1, tB1, tBs;
+    if (!s2 && !encode_act_rowmajor(ctx, &tA, cc.x, B, H, W, cc.c_in, a.tile_imgs, a.rows + 2, a.ck))
         return fail(ctx, SLIM_ECUDA, "cuTensorMapEncodeTiled(halo A) failed");
+    if (s2 && (!encode_act_rowmajor(ctx, &tA, cc.x, B, cc.H, cc.W, cc.c_in, a.tile_imgs, a.rows, a.ck, 2) ||
+               !encode_act_rowmajor(ctx, &tA1, cc.x, B, cc.H, cc.W, cc.c_in, a.tile_imgs, a.rows + 1, a.ck, 2)))
+        return fail(ctx, SLIM_ECUDA, "cuTensorMapEncodeTiled(halo s2 A) failed");
     const int taps = a.stationary ? 9 : 3;
     const CUtensorMap *tB;
-    {
+    if (s2) {   // one-tap boxes (the kernel reorders kw per kh); c_in = c(r_prev): not cached per r
+        if (!encode_w_taps(ctx, &tBs, L, cc.c_in, c_out, a.n_tile, 1, a.ck))
+            return fail(ctx, SLIM_ECUDA, "cuTensorMapEncodeTiled(halo s2 W) failed");
+        tB = &tBs;
+    } else {
         std::lock_guard<std::mutex> g(ctx->mu);
         bool &ok = L.tmh_ok[ri][a.n_tile / 16 - 1][a.stationary];
         CUtensorMap &m = L.tmh[ri][a.n_tile / 16 - 1][a.stationary];
@@ -522,7 +538,8 @@ slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, i
     conv_work(c, cc, ri, B, H, W, &flops, &bytes);
     if (ctx->trace) cudaMemsetAsync(ctx->trace, 0, 3584 * sizeof(unsigned long long), st);   // diagnostics (stem: 3584..)
     LaunchProf prof(ctx, st);
-    CUtensorMap tA1 = tA, tB1 = tA;
+    if (!s2) tA1 = tA;
+    tB1 = tA;
     if (proj) {
         if (!encode_act_rowmajor(ctx, &tA1, cc.xp, B, cc.Hp, cc.Wp, cc.c_in_p, a.tile_imgs, a.rows, kChunk, 2))
             return fail(ctx, SLIM_ECUDA, "cuTensorMapEncodeTiled(halo proj A) failed");
