@@ -39,7 +39,7 @@ constexpr int kHaloThreads = (4 + kHaloEpiWarps) * 32;   // warps 0 A, 1 MMA, 2 
 
 // kNarrow: runtime channel-chunk geometry (16/32-channel boxes); false folds 64-channel / 128-B rows.
 // kVar: 0 = plain / residual epilogue, 1 = + projection shortcut, 2 = + fused average pool,
-// 3 = stride-2 conv (parity planes, see below)
+// 3 = stride-2 conv (parity planes), 4 = three shifted halo boxes (no kw accumulators), see below
 // (compile-time, so the common variant carries none of the other two's code)
 template <bool kNarrow, int kVar>
 __global__ void __launch_bounds__(kHaloThreads, 1)
@@ -73,6 +73,10 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
     // reads the even columns: one MMA of N = n into acc_kw1.  Epilogue: acc_kw0[w-1] + acc_kw2[w]
     // + acc_kw1[w].  A traffic = the input once (4x the output tile) instead of 9x.
     constexpr bool s2 = kVar == 3;
+    // kVar 4 ("x3"): each chunk's slot holds THREE halo boxes shifted by kw-1 columns (TMA zero-fills
+    // the row ends), so every tap is a pure descriptor offset into its box: one accumulator, no
+    // shuffles -- for epilogue-bound layers (seg 0, one 64-channel chunk) at 3x the A traffic.
+    constexpr bool x3 = kVar == 4;
     uint64_t *bars = reinterpret_cast<uint64_t *>(sBN + (proj ? 4 : 2) * a.c_out);
     const uint32_t bar0 = smem_u32(bars);
     // barriers: a_full[4] a_empty[4] b_full[4] b_empty[4] t_full[4] t_empty[4] r_full[4] r_empty[4]
@@ -164,10 +168,22 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
                 const int ti = (t - blockIdx.x) / gridDim.x;
                 TD(0, ti, 0);
                 for (int ch = 0; ch < a.n_chunks && !s2; ++ch) {
-                    mbar_wait(a_empty(s), ph ^ 1);
-                    if (ch == 0) TD(0, ti, 2);
-                    mbar_expect_tx(a_full(s), a.a_bytes);
-                    tma_load_4d(sA + s * a.a_slot, &tmA, a_full(s), ch * CK, 0, n * a.tile_imgs, h0 - 1);
+                    if (x3) {   // one slot per kw-shifted box
+                        for (int kw = 0; kw < 3; ++kw) {
+                            mbar_wait(a_empty(s), ph ^ 1);
+                            mbar_expect_tx(a_full(s), a.a_bytes);
+                            tma_load_4d(sA + s * a.a_slot, &tmA, a_full(s), ch * CK, kw - 1, n * a.tile_imgs, h0 - 1);
+                            if (kw < 2 && ++s == a.sa) {
+                                s = 0;
+                                ph ^= 1;
+                            }
+                        }
+                    } else {
+                        mbar_wait(a_empty(s), ph ^ 1);
+                        if (ch == 0) TD(0, ti, 2);
+                        mbar_expect_tx(a_full(s), a.a_bytes);
+                        tma_load_4d(sA + s * a.a_slot, &tmA, a_full(s), ch * CK, 0, n * a.tile_imgs, h0 - 1);
+                    }
                     if (++s == a.sa) {
                         s = 0;
                         ph ^= 1;
@@ -343,7 +359,31 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
                         }
                     }
                 }
-                for (int ch = 0; ch < a.n_chunks && !s2; ++ch) {
+                for (int ch = 0; ch < a.n_chunks && x3; ++ch) {
+                    // x3: one A slot per kw box; weights stationary (host guarantees)
+                    const int nk = min(kmax, (a.c_in - ch * CK + 15) >> 4);
+                    const uint32_t idesc1 = umma_idesc_bf16(kTileM, a.n_tile);
+                    const uint64_t bch = bdesc0 + static_cast<uint32_t>(ch * 9) * tap16;
+                    for (int kw = 0; kw < 3; ++kw) {
+                        mbar_wait(a_full(s), ph);
+                        tc_fence_after();
+                        const uint64_t ad = adesc0 + s * a_slot16;
+                        if (elect_one() && !(a.debug & 2)) {
+#pragma unroll
+                            for (int kh = 0; kh < 3; ++kh)
+                                for (int kk = 0; kk < nk; ++kk)
+                                    umma_bf16(acc, ad + kh * row16 + 2 * kk, bch + (kh * 3 + kw) * tap16 + 2 * kk, idesc1,
+                                              (ch | kw | kh | kk) != 0);
+                            umma_commit(a_empty(s));
+                        }
+                        __syncwarp();
+                        if (++s == a.sa) {
+                            s = 0;
+                            ph ^= 1;
+                        }
+                    }
+                }
+                for (int ch = 0; ch < a.n_chunks && !s2 && !x3; ++ch) {
                     const int nk = min(kmax, (a.c_in - ch * CK + 15) >> 4);
                     mbar_wait(a_full(s), ph);
                     if (ch == 0 && lane == 0) TD(1, ti, 2);
@@ -501,19 +541,27 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
             for (int g = g0; g < a.n_tile / 16 && !(a.debug & 16); g += gstep) {
                 uint32_t v0[16], v1[16], v2[16];
                 tmem_ld16(lane_addr + col0 + g * 16, v0);
-                tmem_ld16(lane_addr + col0 + a.acc_stride + g * 16, v1);
-                tmem_ld16(lane_addr + col0 + 2 * a.acc_stride + g * 16, v2);
+                if (!x3) {
+                    tmem_ld16(lane_addr + col0 + a.acc_stride + g * 16, v1);
+                    tmem_ld16(lane_addr + col0 + 2 * a.acc_stride + g * 16, v2);
+                }
                 tmem_wait_ld();
                 reg_fence16(v0);
-                reg_fence16(v1);
-                reg_fence16(v2);
+                if (!x3) {
+                    reg_fence16(v1);
+                    reg_fence16(v2);
+                }
                 const int cl = g * 16, cg = co0 + cl;
                 float f[16];
 #pragma unroll
                 for (int i = 0; i < 16; ++i) {
                     // out[w] = acc_0[w-1] + acc_1[w] + acc_2[w+1]  (zero padding at the row ends)
-                    const float left = __shfl_up_sync(0xffffffffu, __uint_as_float(v0[i]), 1);
                     float y;
+                    if (x3) {
+                        f[i] = fmaf(__uint_as_float(v0[i]), s0[cg + i], t0[cg + i]);
+                        continue;
+                    }
+                    const float left = __shfl_up_sync(0xffffffffu, __uint_as_float(v0[i]), 1);
                     if (s2) {   // acc_kw0[w-1] + acc_kw2[w] + acc_kw1[w]
                         y = fmaf(mL, left, __uint_as_float(v1[i]) + __uint_as_float(v2[i]));
                     } else {
@@ -624,14 +672,14 @@ cudaError_t launch_conv_halo(const HaloArgs &a, const CUtensorMap &tmA, const CU
                              const CUtensorMap &tmRes, const CUtensorMap &tmOut, const CUtensorMap &tmA1,
                              const CUtensorMap &tmB1, int grid, cudaStream_t stream, bool pdl) {
     using Fn = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, HaloArgs);
-    static const Fn fns[2][4] = {{conv_halo_kernel<false, 0>, conv_halo_kernel<false, 1>, conv_halo_kernel<false, 2>,
-                                  conv_halo_kernel<false, 3>},
+    static const Fn fns[2][5] = {{conv_halo_kernel<false, 0>, conv_halo_kernel<false, 1>, conv_halo_kernel<false, 2>,
+                                  conv_halo_kernel<false, 3>, conv_halo_kernel<false, 4>},
                                  {conv_halo_kernel<true, 0>, conv_halo_kernel<true, 1>, conv_halo_kernel<true, 2>,
-                                  conv_halo_kernel<true, 3>}};
+                                  conv_halo_kernel<true, 3>, conv_halo_kernel<true, 4>}};
     static bool attr_set = false;
     if (!attr_set) {
         for (int m = 0; m < 2; ++m)
-            for (int v = 0; v < 4; ++v) {
+            for (int v = 0; v < 5; ++v) {
                 cudaError_t e = cudaFuncSetAttribute(fns[m][v], cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
                 if (e != cudaSuccess) return e;
                 cudaFuncSetAttribute(fns[m][v], cudaFuncAttributePreferredSharedMemoryCarveout, 100);
@@ -649,7 +697,7 @@ cudaError_t launch_conv_halo(const HaloArgs &a, const CUtensorMap &tmA, const CU
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     const bool narrow = a.ck != kChunk || a.co_chunk != kChunk;
-    const int var = a.stride2 ? 3 : (a.epi == EPI_BN_PROJ_RELU ? 1 : (a.pool_out ? 2 : 0));
+    const int var = a.stride2 ? 3 : (a.x3 ? 4 : (a.epi == EPI_BN_PROJ_RELU ? 1 : (a.pool_out ? 2 : 0)));
     return cudaLaunchKernelEx(&cfg, fns[narrow ? 1 : 0][var], tmA, tmB, tmRes, tmOut, tmA1, tmB1, a);
 }
 

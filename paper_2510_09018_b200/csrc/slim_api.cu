@@ -414,6 +414,15 @@ slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, i
     // tap blocks of B adjacent in smem) unless SLIM_HALO_NOFUSE
     static const bool nofuse = getenv("SLIM_HALO_NOFUSE") != nullptr;
     a.kw_fuse = nofuse ? 1 : (3 * a.n_tile <= 256 ? 3 : (2 * a.n_tile <= 256 ? 2 : 1));
+    // x3 (three kw-shifted boxes, one accumulator, no shuffles): an alternative for the epilogue-bound
+    // single-chunk layers (seg 0); measured 15% slower there (3x A traffic, N=64 MMAs): SLIM_HALO_X3=1
+    static const int x3_env = getenv("SLIM_HALO_X3") ? atoi(getenv("SLIM_HALO_X3")) : -1;
+    const bool x3 = !s2 && !proj && !cc.pool_out && cc.c_in <= kChunk && nt == 1 && 9 * a.n_tile * 128 <= 100 * 1024 &&
+                    x3_env == 1;   // (weights stationary) measured slower than the kw accumulators: opt-in
+    if (x3) {
+        a.x3 = 1;
+        a.kw_fuse = 1;
+    }
     if (s2) {   // [acc_kw0 | acc_kw2 | acc_kw1] adjacent; kw 0 and 2 as one N = 2n MMA
         if (2 * a.n_tile > 256) return SLIM_EUNSUPPORTED;
         a.kw_fuse = 3;
@@ -421,6 +430,7 @@ slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, i
     }
     a.acc_stride = a.kw_fuse > 1 ? a.n_tile : (a.n_tile + 31) / 32 * 32;
     a.stage_cols = (3 * a.acc_stride + (proj ? a.n_tile : 0) + 31) / 32 * 32;
+    if (x3) a.stage_cols = (a.n_tile + 31) / 32 * 32;   // one accumulator
     // up to four accumulator stages (narrow layers): the MMA runs further ahead of the epilogue,
     // whose per-tile latency chain (not its work) bounds narrow widths
     static const int max_stages = getenv("SLIM_HALO_STAGES") ? atoi(getenv("SLIM_HALO_STAGES")) : 4;
@@ -431,6 +441,7 @@ slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, i
     a.a_bytes = static_cast<uint32_t>(kTileM + 2 * a.row_px) * a.rbk;
     if (s2) a.a_bytes = 2u * static_cast<uint32_t>((a.rows + 1) * a.row_px) * a.rbk;   // odd-row pair (the larger)
     a.a_slot = (a.a_bytes + 1023u) & ~1023u;
+
     if (proj) {   // a projection chunk = 128 px x 64 ch + its n_tile x 64 weights in one slot
         if (a.ck != kChunk) return SLIM_EUNSUPPORTED;
         a.scale1 = cc.Lp->scale[ri];
