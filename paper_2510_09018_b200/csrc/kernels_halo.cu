@@ -553,9 +553,25 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
                 }
                 const int cl = g * 16, cg = co0 + cl;
                 float f[16];
+                if (!x3 && !s2) {
+                    // out[w] = acc_0[w-1] + acc_1[w] + acc_2[w+1] (zero padding at the row ends), then BN:
+                    // packed fp32x2 FMAs (per-lane rounding identical to the scalar form)
+                    const unsigned long long mL2 = f2pk(mL, mL), mR2 = f2pk(mR, mR);
 #pragma unroll
-                for (int i = 0; i < 16; ++i) {
-                    // out[w] = acc_0[w-1] + acc_1[w] + acc_2[w+1]  (zero padding at the row ends)
+                    for (int i = 0; i < 16; i += 2) {
+                        const float l0 = __shfl_up_sync(0xffffffffu, __uint_as_float(v0[i]), 1);
+                        const float l1 = __shfl_up_sync(0xffffffffu, __uint_as_float(v0[i + 1]), 1);
+                        const float r0 = __shfl_down_sync(0xffffffffu, __uint_as_float(v2[i]), 1);
+                        const float r1 = __shfl_down_sync(0xffffffffu, __uint_as_float(v2[i + 1]), 1);
+                        const unsigned long long y = ffma2(
+                            mR2, f2pk(r0, r1), ffma2(mL2, f2pk(l0, l1), f2pk(__uint_as_float(v1[i]), __uint_as_float(v1[i + 1]))));
+                        const float2 sc = *reinterpret_cast<const float2 *>(s0 + cg + i);
+                        const float2 sh = *reinterpret_cast<const float2 *>(t0 + cg + i);
+                        f2upk(ffma2(y, f2pk(sc.x, sc.y), f2pk(sh.x, sh.y)), f[i], f[i + 1]);
+                    }
+                }
+#pragma unroll
+                for (int i = 0; i < 16 && (x3 || s2); ++i) {
                     float y;
                     if (x3) {
                         f[i] = fmaf(__uint_as_float(v0[i]), s0[cg + i], t0[cg + i]);
@@ -576,7 +592,14 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
                     reg_fence16(v0);
                     const float *s1 = sBN + 2 * a.c_out, *t1 = sBN + 3 * a.c_out;
 #pragma unroll
-                    for (int i = 0; i < 16; ++i) f[i] += fmaf(__uint_as_float(v0[i]), s1[cg + i], t1[cg + i]);
+                    for (int i = 0; i < 16; i += 2) {   // f + (s1 * p + t1), pairwise packed
+                        const float2 sc = *reinterpret_cast<const float2 *>(s1 + cg + i);
+                        const float2 sh = *reinterpret_cast<const float2 *>(t1 + cg + i);
+                        const unsigned long long pr =
+                            ffma2(f2pk(__uint_as_float(v0[i]), __uint_as_float(v0[i + 1])), f2pk(sc.x, sc.y),
+                                  f2pk(sh.x, sh.y));
+                        f2upk(fadd2(f2pk(f[i], f[i + 1]), pr), f[i], f[i + 1]);
+                    }
                 }
                 const int oc = cl >> co_shift, q16 = (cl & (CO_CHUNK - 1)) >> 3;
                 const uint32_t off0 = oc * oc_bytes + row_off + ((q16 ^ row_x) << 4);
@@ -586,10 +609,9 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
                     const uint4 r1 = *reinterpret_cast<const uint4 *>(resp + off1);
                     const uint32_t rr[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
 #pragma unroll
-                    for (int i = 0; i < 8; ++i) {
-                        f[2 * i] += bf16_lo(rr[i]);
-                        f[2 * i + 1] += bf16_hi(rr[i]);
-                    }
+                    for (int i = 0; i < 8; ++i)
+                        f2upk(fadd2(f2pk(f[2 * i], f[2 * i + 1]), f2pk(bf16_lo(rr[i]), bf16_hi(rr[i]))), f[2 * i],
+                              f[2 * i + 1]);
                 }
                 if (pool) {
                     // fused global average pool (last conv): sum the W pixels of this image row
