@@ -77,6 +77,11 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
     // the row ends), so every tap is a pure descriptor offset into its box: one accumulator, no
     // shuffles -- for epilogue-bound layers (seg 0, one 64-channel chunk) at 3x the A traffic.
     constexpr bool x3 = kVar == 4;
+    // kVar 5 ("x2"): two boxes per chunk -- unshifted (kw = 1 and kw = 2 as one N = 2n MMA into
+    // [acc_m | acc_2]) and shifted by -1 column (kw = 0, N = n into acc_m) -- so the epilogue reads
+    // two accumulators (acc_m[w] + acc_2[w+1]) instead of three: TMEM reads (~64 B/cycle/SM) are what
+    // pace the three-accumulator epilogue of single-chunk layers.
+    constexpr bool x2 = kVar == 5;
     uint64_t *bars = reinterpret_cast<uint64_t *>(sBN + (proj ? 4 : 2) * a.c_out);
     const uint32_t bar0 = smem_u32(bars);
     // barriers: a_full[4] a_empty[4] b_full[4] b_empty[4] t_full[4] t_empty[4] r_full[4] r_empty[4]
@@ -168,12 +173,13 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
                 const int ti = (t - blockIdx.x) / gridDim.x;
                 TD(0, ti, 0);
                 for (int ch = 0; ch < a.n_chunks && !s2; ++ch) {
-                    if (x3) {   // one slot per kw-shifted box
-                        for (int kw = 0; kw < 3; ++kw) {
+                    if (x3 || x2) {   // one slot per kw-shifted box (x2: shifts 0 then -1)
+                        for (int kw = 0; kw < (x2 ? 2 : 3); ++kw) {
                             mbar_wait(a_empty(s), ph ^ 1);
                             mbar_expect_tx(a_full(s), a.a_bytes);
-                            tma_load_4d(sA + s * a.a_slot, &tmA, a_full(s), ch * CK, kw - 1, n * a.tile_imgs, h0 - 1);
-                            if (kw < 2 && ++s == a.sa) {
+                            tma_load_4d(sA + s * a.a_slot, &tmA, a_full(s), ch * CK, x2 ? -kw : kw - 1,
+                                        n * a.tile_imgs, h0 - 1);
+                            if (kw < (x2 ? 1 : 2) && ++s == a.sa) {
                                 s = 0;
                                 ph ^= 1;
                             }
@@ -383,7 +389,36 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
                         }
                     }
                 }
-                for (int ch = 0; ch < a.n_chunks && !s2 && !x3; ++ch) {
+                for (int ch = 0; ch < a.n_chunks && x2; ++ch) {
+                    // x2: slot 0 = unshifted box -> [acc_m | acc_2] (N = 2n, taps kw 1, 2 adjacent in B),
+                    //     slot 1 = box shifted -1 -> acc_m (N = n, tap kw 0); weights stationary
+                    const int nk = min(kmax, (a.c_in - ch * CK + 15) >> 4);
+                    const uint32_t idesc1 = umma_idesc_bf16(kTileM, a.n_tile), idesc2 = umma_idesc_bf16(kTileM, 2 * a.n_tile);
+                    const uint64_t bch = bdesc0 + static_cast<uint32_t>(ch * 9) * tap16;
+                    for (int bx = 0; bx < 2; ++bx) {
+                        mbar_wait(a_full(s), ph);
+                        tc_fence_after();
+                        const uint64_t ad = adesc0 + s * a_slot16;
+                        if (elect_one() && !(a.debug & 2)) {
+#pragma unroll
+                            for (int kh = 0; kh < 3; ++kh)
+                                for (int kk = 0; kk < nk; ++kk) {
+                                    if (bx == 0)
+                                        umma_bf16(acc, ad + kh * row16 + 2 * kk, bch + (kh * 3 + 1) * tap16 + 2 * kk, idesc2,
+                                                  (ch | kh | kk) != 0);
+                                    else
+                                        umma_bf16(acc, ad + kh * row16 + 2 * kk, bch + (kh * 3) * tap16 + 2 * kk, idesc1, true);
+                                }
+                            umma_commit(a_empty(s));
+                        }
+                        __syncwarp();
+                        if (++s == a.sa) {
+                            s = 0;
+                            ph ^= 1;
+                        }
+                    }
+                }
+                for (int ch = 0; ch < a.n_chunks && !s2 && !x3 && !x2; ++ch) {
                     const int nk = min(kmax, (a.c_in - ch * CK + 15) >> 4);
                     mbar_wait(a_full(s), ph);
                     if (ch == 0 && lane == 0) TD(1, ti, 2);
@@ -541,19 +576,34 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
             for (int g = g0; g < a.n_tile / 16 && !(a.debug & 16); g += gstep) {
                 uint32_t v0[16], v1[16], v2[16];
                 tmem_ld16(lane_addr + col0 + g * 16, v0);
-                if (!x3) {
+                if (x2) tmem_ld16(lane_addr + col0 + a.acc_stride + g * 16, v2);   // acc_m, acc_2
+                if (!x3 && !x2) {
                     tmem_ld16(lane_addr + col0 + a.acc_stride + g * 16, v1);
                     tmem_ld16(lane_addr + col0 + 2 * a.acc_stride + g * 16, v2);
                 }
                 tmem_wait_ld();
                 reg_fence16(v0);
-                if (!x3) {
+                if (x2) reg_fence16(v2);
+                if (!x3 && !x2) {
                     reg_fence16(v1);
                     reg_fence16(v2);
                 }
                 const int cl = g * 16, cg = co0 + cl;
                 float f[16];
-                if (!x3 && !s2) {
+                if (x2) {   // out[w] = acc_m[w] + acc_2[w+1], then BN (packed fp32x2)
+                    const unsigned long long mR2 = f2pk(mR, mR);
+#pragma unroll
+                    for (int i = 0; i < 16; i += 2) {
+                        const float r0 = __shfl_down_sync(0xffffffffu, __uint_as_float(v2[i]), 1);
+                        const float r1 = __shfl_down_sync(0xffffffffu, __uint_as_float(v2[i + 1]), 1);
+                        const unsigned long long y =
+                            ffma2(mR2, f2pk(r0, r1), f2pk(__uint_as_float(v0[i]), __uint_as_float(v0[i + 1])));
+                        const float2 sc = *reinterpret_cast<const float2 *>(s0 + cg + i);
+                        const float2 sh = *reinterpret_cast<const float2 *>(t0 + cg + i);
+                        f2upk(ffma2(y, f2pk(sc.x, sc.y), f2pk(sh.x, sh.y)), f[i], f[i + 1]);
+                    }
+                }
+                if (!x3 && !s2 && !x2) {
                     // out[w] = acc_0[w-1] + acc_1[w] + acc_2[w+1] (zero padding at the row ends), then BN:
                     // packed fp32x2 FMAs (per-lane rounding identical to the scalar form)
                     const unsigned long long mL2 = f2pk(mL, mL), mR2 = f2pk(mR, mR);
@@ -694,14 +744,14 @@ cudaError_t launch_conv_halo(const HaloArgs &a, const CUtensorMap &tmA, const CU
                              const CUtensorMap &tmRes, const CUtensorMap &tmOut, const CUtensorMap &tmA1,
                              const CUtensorMap &tmB1, int grid, cudaStream_t stream, bool pdl) {
     using Fn = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, HaloArgs);
-    static const Fn fns[2][5] = {{conv_halo_kernel<false, 0>, conv_halo_kernel<false, 1>, conv_halo_kernel<false, 2>,
-                                  conv_halo_kernel<false, 3>, conv_halo_kernel<false, 4>},
+    static const Fn fns[2][6] = {{conv_halo_kernel<false, 0>, conv_halo_kernel<false, 1>, conv_halo_kernel<false, 2>,
+                                  conv_halo_kernel<false, 3>, conv_halo_kernel<false, 4>, conv_halo_kernel<false, 5>},
                                  {conv_halo_kernel<true, 0>, conv_halo_kernel<true, 1>, conv_halo_kernel<true, 2>,
-                                  conv_halo_kernel<true, 3>, conv_halo_kernel<true, 4>}};
+                                  conv_halo_kernel<true, 3>, conv_halo_kernel<true, 4>, conv_halo_kernel<true, 5>}};
     static bool attr_set = false;
     if (!attr_set) {
         for (int m = 0; m < 2; ++m)
-            for (int v = 0; v < 5; ++v) {
+            for (int v = 0; v < 6; ++v) {
                 cudaError_t e = cudaFuncSetAttribute(fns[m][v], cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
                 if (e != cudaSuccess) return e;
                 cudaFuncSetAttribute(fns[m][v], cudaFuncAttributePreferredSharedMemoryCarveout, 100);
@@ -719,7 +769,7 @@ cudaError_t launch_conv_halo(const HaloArgs &a, const CUtensorMap &tmA, const CU
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     const bool narrow = a.ck != kChunk || a.co_chunk != kChunk;
-    const int var = a.stride2 ? 3 : (a.x3 ? 4 : (a.epi == EPI_BN_PROJ_RELU ? 1 : (a.pool_out ? 2 : 0)));
+    const int var = a.stride2 ? 3 : (a.x3 == 1 ? 4 : (a.x3 == 2 ? 5 : (a.epi == EPI_BN_PROJ_RELU ? 1 : (a.pool_out ? 2 : 0))));
     return cudaLaunchKernelEx(&cfg, fns[narrow ? 1 : 0][var], tmA, tmB, tmRes, tmOut, tmA1, tmB1, a);
 }
 

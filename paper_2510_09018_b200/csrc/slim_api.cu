@@ -417,10 +417,13 @@ slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, i
     // x3 (three kw-shifted boxes, one accumulator, no shuffles): an alternative for the epilogue-bound
     // single-chunk layers (seg 0); measured 15% slower there (3x A traffic, N=64 MMAs): SLIM_HALO_X3=1
     static const int x3_env = getenv("SLIM_HALO_X3") ? atoi(getenv("SLIM_HALO_X3")) : -1;
-    const bool x3 = !s2 && !proj && !cc.pool_out && cc.c_in <= kChunk && nt == 1 && 9 * a.n_tile * 128 <= 100 * 1024 &&
-                    x3_env == 1;   // (weights stationary) measured slower than the kw accumulators: opt-in
-    if (x3) {
-        a.x3 = 1;
+    // x2 (two boxes, two accumulators, 2/3 of the TMEM reads): SLIM_HALO_X3=2, measured 5% slower at seg 0
+    const bool xbox_ok = !s2 && !proj && !cc.pool_out && cc.c_in <= kChunk && nt == 1 && 9 * a.n_tile * 128 <= 100 * 1024 &&
+                         2 * a.n_tile <= 256;   // (weights stationary)
+    const int xmode = !xbox_ok ? 0 : (x3_env >= 0 ? x3_env : 0);   // both measured slower than kw accumulators
+    const bool x3 = xmode == 1, x2 = xmode == 2;
+    if (x3 || x2) {
+        a.x3 = xmode;
         a.kw_fuse = 1;
     }
     if (s2) {   // [acc_kw0 | acc_kw2 | acc_kw1] adjacent; kw 0 and 2 as one N = 2n MMA
@@ -431,6 +434,10 @@ slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, i
     a.acc_stride = a.kw_fuse > 1 ? a.n_tile : (a.n_tile + 31) / 32 * 32;
     a.stage_cols = (3 * a.acc_stride + (proj ? a.n_tile : 0) + 31) / 32 * 32;
     if (x3) a.stage_cols = (a.n_tile + 31) / 32 * 32;   // one accumulator
+    if (x2) {                                            // [acc_m | acc_2] adjacent (one N = 2n MMA)
+        a.acc_stride = a.n_tile;
+        a.stage_cols = (2 * a.n_tile + 31) / 32 * 32;
+    }
     // up to four accumulator stages (narrow layers): the MMA runs further ahead of the epilogue,
     // whose per-tile latency chain (not its work) bounds narrow widths
     static const int max_stages = getenv("SLIM_HALO_STAGES") ? atoi(getenv("SLIM_HALO_STAGES")) : 4;
