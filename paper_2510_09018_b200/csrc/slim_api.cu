@@ -388,6 +388,13 @@ slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, i
     // exact-width output boxes -- each CTA's serial latency chain (MMA, epilogue) shrinks with it
     static const bool no_fill = getenv("SLIM_HALO_NOFILL") != nullptr;
     bool narrow_out = false;
+    // (experiment) SLIM_HALO_SPLITN=32: 32-channel N tiles for single-chunk layers -> more accumulator
+    // stages / tile groups in flight per CTA
+    static const int splitn = getenv("SLIM_HALO_SPLITN") ? atoi(getenv("SLIM_HALO_SPLITN")) : 0;
+    if ((splitn == 32 || splitn == 16) && !cc.pool_out && cc.c_in <= kChunk && c_out / nt > splitn && c_out % splitn == 0) {
+        nt = c_out / splitn;
+        narrow_out = true;
+    }
     if (!no_fill && a.m_tiles * nt * 10 < ctx->num_sms * 8 && !cc.pool_out)
         for (int n2 : {32, 16}) {
             if (n2 >= c_out / nt || c_out % n2 || a.m_tiles * (c_out / n2) > ctx->num_sms) continue;   // one wave

@@ -1,6 +1,7 @@
 """Summarise an ncu --set full report of the chain kernels into profiles/ (markdown + json).
 
     python tools/ncu_summary.py gpurun_out/prof_chain.ncu-rep profiles/r01_ncu_chain
+    python tools/ncu_summary.py gpurun_out/prof_chain_raw.csv profiles/r01_ncu_chain   # exported raw page
 """
 import csv
 import io
@@ -23,7 +24,10 @@ WANT = {
 
 
 def main(rep, out_prefix):
-    raw = subprocess.check_output(["ncu", "-i", rep, "--page", "raw", "--csv"], text=True, stderr=subprocess.DEVNULL)
+    if rep.endswith(".csv"):   # `ncu -i rep --page raw --csv` exported on the GPU box
+        raw = open(rep).read()
+    else:
+        raw = subprocess.check_output(["ncu", "-i", rep, "--page", "raw", "--csv"], text=True, stderr=subprocess.DEVNULL)
     rows = list(csv.reader(io.StringIO(raw)))
     h, units = rows[0], rows[1]
     recs = []
