@@ -373,3 +373,40 @@ def test_splitk_cluster_path_parity():
                          cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     assert out.returncode == 0, out.stderr[-2000:]
     assert float(out.stdout.strip().splitlines()[-1]) <= TAU_BF16
+
+
+@pytest.mark.parametrize("env", [
+    "SLIM_NO_HALO=1",                      # every conv through the per-tap kernel (+ split-K where chosen)
+    "SLIM_HALO_NO_S2=1 SLIM_HALO_NO_PROJ=1 SLIM_HALO_NO_SMALL=1",   # halo only for large stride-1 layers
+    "SLIM_HALO_X3=1",                      # three shifted boxes, one accumulator (opt-in variant)
+    "SLIM_HALO_X3=2",                      # two boxes, two accumulators (opt-in variant)
+    "SLIM_HALO_STAGES=1 SLIM_HALO_EPI1=1",  # one accumulator stage, one epilogue group
+    "SLIM_HALO_NARROW=1",                  # 16/32-channel operand boxes
+    "SLIM_NPROD=1",                        # one TMA producer in the per-tap kernel
+])
+def test_kernel_variant_parity(env):
+    """Every kernel variant / fallback a runtime switch can select computes the same network:
+    chains at a mixed width tuple and at r=1 against the oracle (subprocess: the switches are
+    read once per process)."""
+    import subprocess, sys, os
+    code = (
+        "import numpy as np, torch, synth, oracle, paper_2510_09018_b200 as slim\n"
+        "w, bn = synth.make_weights(), synth.make_bn()\n"
+        "net = slim.SlimNet(w, bn, max_batch=64)\n"
+        "ref = oracle.Model(w, bn)\n"
+        "x = synth.make_images(10, offset=31)\n"
+        "xd = torch.from_numpy(x).to(torch.bfloat16).cuda()\n"
+        "worst = 0.0\n"
+        "for t in ((1.0, 1.0, 1.0, 1.0), (0.25, 0.75, 0.5, 1.0)):\n"
+        "    got = net.forward_chain(xd, t).cpu().numpy()\n"
+        "    worst = max(worst, float(oracle.per_image_rel_err(got[:3], ref.chain(x[:3], t)).max()))\n"
+        "print(worst)\n"
+    )
+    e = dict(os.environ)
+    for kv in env.split():
+        k, v = kv.split("=")
+        e[k] = v
+    out = subprocess.run([sys.executable, "-c", code], env=e, capture_output=True, text=True, timeout=600,
+                         cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert float(out.stdout.strip().splitlines()[-1]) <= TAU_BF16, env
