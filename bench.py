@@ -256,21 +256,44 @@ def run_ours(args):
     })
 
     # ---------------- e2e through the public API with host buffers
+    # Every step copies its images from pinned host memory and reads its logits back.  As a
+    # serving loop would, the H2D copy of step k+1 runs on a copy stream into the other of two
+    # device input buffers while step k computes (events order buffer reuse).
     xh = {r: xs[r].cpu().pin_memory() for r in WIDTHS}
-    lh = {r: torch.empty(B, 100, dtype=torch.float32).pin_memory() for r in WIDTHS}
+    lh = {r: [torch.empty(B, 100, dtype=torch.float32).pin_memory() for _ in range(2)] for r in WIDTHS}
+    xin = {r: [xs[r], torch.empty_like(xs[r])] for r in WIDTHS}
+    cstreams = {r: torch.cuda.Stream(device=dev) for r in WIDTHS}
+    ev_ready = {r: [torch.cuda.Event(), torch.cuda.Event()] for r in WIDTHS}
+    ev_free = {r: [torch.cuda.Event(), torch.cuda.Event()] for r in WIDTHS}
     KE = max(1, min(K, args.e2e_steps))
+    for _ in range(2):   # warm both input buffers' graphs
+        for r in WIDTHS:
+            for b in range(2):
+                slim.slim_forward_chain(net.ctx, (r,) * 4, B, xin[r][b], logits[r], wss[r], wsb, streams[r])
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    for _ in range(KE):
+    for k in range(KE):
+        b = k & 1
+        flush.zero_()                                  # L2 flushed between steps, as in the device-timed loop
+        fork = torch.cuda.Event()
+        fork.record(stream)
         for r in WIDTHS:
-            with torch.cuda.stream(streams[r]):
-                xs[r].copy_(xh[r], non_blocking=True)
-                chain(r)
-                lh[r].copy_(logits[r], non_blocking=True)
-        for r in WIDTHS:
-            streams[r].synchronize()
+            cs, st = cstreams[r], streams[r]
+            st.wait_event(fork)
+            cs.wait_event(ev_free[r][b])              # the chain that last read buffer b is done
+            with torch.cuda.stream(cs):
+                xin[r][b].copy_(xh[r], non_blocking=True)
+                ev_ready[r][b].record(cs)
+            st.wait_event(ev_ready[r][b])
+            slim.slim_forward_chain(net.ctx, (r,) * 4, B, xin[r][b], logits[r], wss[r], wsb, st)
+            ev_free[r][b].record(st)
+            with torch.cuda.stream(st):
+                lh[r][b].copy_(logits[r], non_blocking=True)
+    for r in WIDTHS:
+        streams[r].synchronize()
+        cstreams[r].synchronize()
     e2e_s = time.perf_counter() - t0
     te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
     if world > 1:
@@ -298,8 +321,8 @@ def run_ours(args):
             "energy_j_per_image": energy,
             "clocks": clocks,
             "e2e": {"value": e2e_val, "unit": "images/s", "h2d_bytes_per_step": sum(x.numel() * 2 for x in xh.values()),
-                    "d2h_bytes_per_step": sum(l.numel() * 4 for l in lh.values()),
-                    "api": "SlimNet / slim_forward_chain with pinned-host input copy + logits read-back per step"},
+                    "d2h_bytes_per_step": sum(l[0].numel() * 4 for l in lh.values()),
+                    "api": "slim_forward_chain with a pinned-host input copy (double-buffered on a copy stream) + logits read-back every step; L2 flushed every step (inside the wall-clock)"},
             "cpu_baseline": cpu,
         }
         print(json.dumps(line))
