@@ -34,20 +34,23 @@ using namespace ptx;
 namespace {
 
 constexpr int kHaloEpiWarps = 16;   // four per TMEM lane quarter: the epilogue is latency bound
-constexpr int kHaloEpiThreads = kHaloEpiWarps * 32;
 constexpr int kHaloThreads = (4 + kHaloEpiWarps) * 32;   // warps 0 A, 1 MMA, 2 B, 3 residual, 4..19 epilogue
+// compact variant (narrow layers): 8 epilogue warps, <= 85 registers, <= ~110 KB smem and <= 256 TMEM
+// columns, so two CTAs -- of this kernel or of a concurrent width instance's -- share an SM
+constexpr int kHaloThreadsSmall = (4 + 8) * 32;
 
 // kNarrow: runtime channel-chunk geometry (16/32-channel boxes); false folds 64-channel / 128-B rows.
 // kVar: 0 = plain / residual epilogue, 1 = + projection shortcut, 2 = + fused average pool,
 // 3 = stride-2 conv (parity planes), 4 = three shifted halo boxes (no kw accumulators), see below
 // (compile-time, so the common variant carries none of the other two's code)
-template <bool kNarrow, int kVar>
-__global__ void __launch_bounds__(kHaloThreads, 1)
+template <bool kNarrow, int kVar, bool kSmall = false>
+__global__ void __launch_bounds__(kSmall ? kHaloThreadsSmall : kHaloThreads, kSmall ? 2 : 1)
     conv_halo_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmRes, const __grid_constant__ CUtensorMap tmOut,
                      const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUtensorMap tmB1,
                      const HaloArgs a) {
     extern __shared__ uint8_t smem_raw[];
+    constexpr int EPIW = kSmall ? 8 : kHaloEpiWarps, EPIT = EPIW * 32;   // epilogue warps / threads
     const int CK = kNarrow ? a.ck : kChunk, RBK = kNarrow ? a.rbk : 128;
     const int CO_CHUNK = kNarrow ? a.co_chunk : kChunk, RBO = kNarrow ? a.rbo : 128;
     // 1 KiB alignment without leaving the shared address space (LDS/STS, not generic LD/ST)
@@ -112,9 +115,9 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
         }
         for (int i = 0; i < 4; ++i) {
             mbar_init(t_full(i), 1);
-            mbar_init(t_empty(i), kHaloEpiThreads / n_grp);
+            mbar_init(t_empty(i), EPIT / n_grp);
             mbar_init(r_full(i), 1);
-            mbar_init(r_empty(i), kHaloEpiThreads / n_grp);
+            mbar_init(r_empty(i), EPIT / n_grp);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         prefetch_tmap(&tmA);
@@ -540,11 +543,11 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
         // stages, residual slots, a staging buffer and a named barrier of its own, so n_grp tiles'
         // epilogues overlap; inside a group the 4/n_grp warps of a lane quarter split the columns.
         const int q = warp & 3;
-        const int quad = (warp - kEpiWarp0) >> 2;          // 0..3
-        const int cw = 4 / n_grp;                           // column ways per group
+        const int quad = (warp - kEpiWarp0) >> 2;          // 0 .. EPIW/4 - 1
+        const int cw = (EPIW / 4) / n_grp;                  // column ways per group
         const int grp = quad / cw;
         const int g0 = quad % cw, gstep = cw;
-        const int gthreads = kHaloEpiThreads / n_grp;
+        const int gthreads = EPIT / n_grp;
         const int row = q * 32 + lane;
         // TMA swizzle of the staging tile (rbo-byte rows): 16-B piece q of this row lives at q ^ row_x
         const int co_shift = CO_CHUNK == 16 ? 4 : (CO_CHUNK == 32 ? 5 : 6);
@@ -748,6 +751,8 @@ cudaError_t launch_conv_halo(const HaloArgs &a, const CUtensorMap &tmA, const CU
                                   conv_halo_kernel<false, 3>, conv_halo_kernel<false, 4>, conv_halo_kernel<false, 5>},
                                  {conv_halo_kernel<true, 0>, conv_halo_kernel<true, 1>, conv_halo_kernel<true, 2>,
                                   conv_halo_kernel<true, 3>, conv_halo_kernel<true, 4>, conv_halo_kernel<true, 5>}};
+    static const Fn small_fns[4] = {conv_halo_kernel<true, 0, true>, conv_halo_kernel<true, 1, true>,
+                                    conv_halo_kernel<true, 2, true>, conv_halo_kernel<true, 3, true>};
     static bool attr_set = false;
     if (!attr_set) {
         for (int m = 0; m < 2; ++m)
@@ -756,11 +761,16 @@ cudaError_t launch_conv_halo(const HaloArgs &a, const CUtensorMap &tmA, const CU
                 if (e != cudaSuccess) return e;
                 cudaFuncSetAttribute(fns[m][v], cudaFuncAttributePreferredSharedMemoryCarveout, 100);
             }
+        for (int v = 0; v < 4; ++v) {
+            cudaError_t e = cudaFuncSetAttribute(small_fns[v], cudaFuncAttributeMaxDynamicSharedMemorySize, 113 * 1024);
+            if (e != cudaSuccess) return e;
+            cudaFuncSetAttribute(small_fns[v], cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        }
         attr_set = true;
     }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(kHaloThreads);
+    cfg.blockDim = dim3(a.small ? kHaloThreadsSmall : kHaloThreads);
     cfg.dynamicSmemBytes = conv_halo_smem_bytes(a);
     cfg.stream = stream;
     cudaLaunchAttribute attr[1];
@@ -770,6 +780,10 @@ cudaError_t launch_conv_halo(const HaloArgs &a, const CUtensorMap &tmA, const CU
     cfg.numAttrs = 1;
     const bool narrow = a.ck != kChunk || a.co_chunk != kChunk;
     const int var = a.stride2 ? 3 : (a.x3 == 1 ? 4 : (a.x3 == 2 ? 5 : (a.epi == EPI_BN_PROJ_RELU ? 1 : (a.pool_out ? 2 : 0))));
+    if (a.small) {
+        if (var > 3) return cudaErrorInvalidValue;
+        return cudaLaunchKernelEx(&cfg, small_fns[var], tmA, tmB, tmRes, tmOut, tmA1, tmB1, a);
+    }
     return cudaLaunchKernelEx(&cfg, fns[narrow ? 1 : 0][var], tmA, tmB, tmRes, tmOut, tmA1, tmB1, a);
 }
 

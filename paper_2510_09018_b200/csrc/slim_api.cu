@@ -336,7 +336,7 @@ void conv_work(const slim_config &c, const ConvCall &cc, int ri, int B, int Ho, 
 
 // Stride-1 3x3 conv with one halo load per channel chunk (kernels_halo.cu).  Returns
 // SLIM_EUNSUPPORTED (nothing launched) when the layer does not fit its constraints.
-slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, int ri, int B) {
+slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, int ri, int B, bool allow_small = true) {
     static const bool disabled = getenv("SLIM_NO_HALO") != nullptr;
     const slim_config &c = ctx->cfg;
     DevLayer &L = *cc.L;
@@ -406,10 +406,16 @@ slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, i
     a.n_tiles = nt;
     a.c_out = c_out;
     a.c_in = cc.c_in;
-    // 64-channel boxes unless SLIM_HALO_NARROW (16/32-channel boxes measured no faster here)
+    // compact variant for narrow layers (c_out <= 32, c_in <= 64; opt-in SLIM_HALO_SMALL=1): exact
+    // 16/32-channel boxes, <= 256 TMEM columns and ~110 KB of smem so two CTAs share an SM.  Measured:
+    // -13 % on seg 0 at r <= 0.5 for one width alone, but the concurrent 4-width step loses 4 %: a
+    // compact CTA parked on an SM holds off the full-SM CTAs of the wide instances' kernels
+    static const int small_env = getenv("SLIM_HALO_SMALL") ? atoi(getenv("SLIM_HALO_SMALL")) : 0;
+    bool small = allow_small && small_env != 0 && c_out <= 32 && cc.c_in <= 64 && !cc.pool_out;
+    // 64-channel boxes unless SLIM_HALO_NARROW or the compact variant (16/32-channel boxes)
     static const bool halo_narrow = getenv("SLIM_HALO_NARROW") != nullptr;
-    auto hch = [&](int ch) { return halo_narrow ? chunk_ch(ch) : kChunk; };
-    a.ck = hch(cc.c_in);
+    auto hch = [&](int ch) { return (halo_narrow || small) ? chunk_ch(ch) : kChunk; };
+    a.ck = proj ? kChunk : hch(cc.c_in);
     a.rbk = 2 * a.ck;
     a.n_chunks = (cc.c_in + a.ck - 1) / a.ck;
     a.co_chunk = narrow_out ? a.n_tile : hch(a.n_tile);
@@ -425,7 +431,7 @@ slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, i
     // single-chunk layers (seg 0); measured 15% slower there (3x A traffic, N=64 MMAs): SLIM_HALO_X3=1
     static const int x3_env = getenv("SLIM_HALO_X3") ? atoi(getenv("SLIM_HALO_X3")) : -1;
     // x2 (two boxes, two accumulators, 2/3 of the TMEM reads): SLIM_HALO_X3=2, measured 5% slower at seg 0
-    const bool xbox_ok = !s2 && !proj && !cc.pool_out && cc.c_in <= kChunk && nt == 1 && 9 * a.n_tile * 128 <= 100 * 1024 &&
+    const bool xbox_ok = !small && !s2 && !proj && !cc.pool_out && cc.c_in <= kChunk && nt == 1 && 9 * a.n_tile * 128 <= 100 * 1024 &&
                          2 * a.n_tile <= 256;   // (weights stationary)
     const int xmode = !xbox_ok ? 0 : (x3_env >= 0 ? x3_env : 0);   // both measured slower than kw accumulators
     const bool x3 = xmode == 1, x2 = xmode == 2;
@@ -448,7 +454,10 @@ slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, i
     // up to four accumulator stages (narrow layers): the MMA runs further ahead of the epilogue,
     // whose per-tile latency chain (not its work) bounds narrow widths
     static const int max_stages = getenv("SLIM_HALO_STAGES") ? atoi(getenv("SLIM_HALO_STAGES")) : 4;
-    a.acc_stages = (4 * a.stage_cols <= 512 && max_stages >= 4) ? 4 : (2 * a.stage_cols <= 512 && max_stages >= 2 ? 2 : 1);
+    const int tmem_max = small ? 256 : 512;
+    a.acc_stages = (4 * a.stage_cols <= tmem_max && max_stages >= 4) ? 4
+                                                                      : (2 * a.stage_cols <= tmem_max && max_stages >= 2 ? 2 : 1);
+    if (a.stage_cols > tmem_max) small = false;   // (cannot happen for c_out <= 64)
     int cols = a.acc_stages * a.stage_cols, tc = 32;
     while (tc < cols) tc <<= 1;
     a.tmem_cols = tc;
@@ -468,10 +477,9 @@ slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, i
     const size_t chunk = static_cast<size_t>(a.n_out_chunks) * 128 * a.rbo;
     static const bool one_group = getenv("SLIM_HALO_EPI1") != nullptr;
     a.epi_groups = one_group ? 1 : a.acc_stages;
-    // narrow layers (exact 16/32-channel boxes): two CTAs per SM (smem and 2x256 TMEM columns fit)
-    // (two CTAs per SM for narrow layers measured slower: SLIM_HALO_TWO=1 to try)
-    static const bool two_cta = getenv("SLIM_HALO_TWO") != nullptr;
-    const bool two = two_cta && a.n_tile <= 32 && a.ck <= 32;
+    if (small && a.epi_groups > 2) a.epi_groups = 2;   // 8 epilogue warps: one or two tile groups
+    a.small = small ? 1 : 0;
+    const bool two = small;
     const size_t budget = two ? 110 * 1024 : 226 * 1024;
     auto fixed0 = [&]() {
         return 1024 + chunk * a.epi_groups + (proj ? 16 : 8) * static_cast<size_t>(c_out) + 8 * 32 + 16;
@@ -480,7 +488,7 @@ slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, i
     const uint32_t all_w = r1k(static_cast<uint32_t>(a.n_chunks) * 9u * a.n_tile * a.rbk);
     // residual slots: a multiple of the tile groups (each slot serves one group, parity waits)
     a.res_slots = (cc.epi == EPI_BN_ADD_RELU) ? std::max(2, a.epi_groups) : 0;
-    a.stationary = (nt == 1 && all_w <= 100 * 1024) ? 1 : 0;
+    a.stationary = (nt == 1 && all_w <= (small ? 48u : 100u) * 1024) ? 1 : 0;
     if (a.stationary) {
         a.b_bytes = all_w;
         a.sb = 1;
@@ -499,7 +507,7 @@ slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, i
                     continue;
                 }
                 if (a.res_slots == 2) { a.res_slots = 1; continue; }
-                return SLIM_EUNSUPPORTED;
+                return small ? conv_halo_bf16(ctx, st, cc, ri, B, false) : SLIM_EUNSUPPORTED;
             }
             left -= a.b_bytes;
             a.sa = static_cast<int>(left / a.a_slot);
@@ -512,7 +520,7 @@ slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, i
                     continue;
                 }
                 if (a.res_slots == 2) { a.res_slots = 1; continue; }
-                return SLIM_EUNSUPPORTED;
+                return small ? conv_halo_bf16(ctx, st, cc, ri, B, false) : SLIM_EUNSUPPORTED;
             }
             a.sa = 2;
             left -= 2 * a.a_slot;

@@ -99,6 +99,7 @@ struct HaloArgs {
     int c_in_p, n_chunks_p;   // projection input channels and 64-channel chunks
     float *pool_out;          // fused average pool -> fp32 [B][c_out] (rows == 4, row_px == 32), else nullptr
     int stride2;              // stride-2 conv: input [B, 2H, 2W, c_in] as parity planes (tmA even rows, tmA1 odd)
+    int small;                // compact variant: 8 epilogue warps, two CTAs per SM (narrow layers)
     int x3;                   // 1: three kw-shifted halo boxes per chunk, one accumulator; 2: two boxes, two
                               // accumulators (a_bytes = one box)
     int stationary;           // all weights resident in smem (one B slot of n_chunks*9 taps)

@@ -383,6 +383,7 @@ def test_splitk_cluster_path_parity():
     "SLIM_HALO_STAGES=1 SLIM_HALO_EPI1=1",  # one accumulator stage, one epilogue group
     "SLIM_HALO_NARROW=1",                  # 16/32-channel operand boxes
     "SLIM_NPROD=1",                        # one TMA producer in the per-tap kernel
+    "SLIM_HALO_SMALL=1",                   # compact two-CTA-per-SM variant for narrow layers
 ])
 def test_kernel_variant_parity(env):
     """Every kernel variant / fallback a runtime switch can select computes the same network:
