@@ -8,7 +8,8 @@ It is the plain definition of the batched forward pass of the segmented
 SlimResNet at a runtime-chosen width, in float64:
 
 * convolution: `oracle.c` (direct sum, fixed kh,kw,ci order; O2),
-* everything else: numpy float64, one line per formula.
+* everything else: numpy float64, one line per formula,
+* the GroupNorm variant: `groupnorm`, `Model(norm="gn")`.
 
 Citations: P:n = /root/reference/PAPER.md line n.  The paper fixes none of the
 architecture; the readings used here (ResNet-18-CIFAR, per-width BN selected by
@@ -37,6 +38,11 @@ _lib = None
 # Width set W and BN epsilon (reading #6, PyTorch default).  Kept here,
 # not imported from the CUDA side.
 BN_EPS = 1e-5
+# GroupNorm variant ("Group Normalization instead of Batch Normalization"; SURVEY
+# §8(f) NEXT-1).  Group size is unstated in the paper: reading R16 fixes
+# 16 consecutive channels per group, so every width c(r, C) (a multiple of 16) holds
+# whole groups and a group means the same channels at every width.
+GN_GROUP_CHANNELS = 16
 
 
 def build(force: bool = False) -> str:
@@ -118,6 +124,28 @@ def batchnorm(y: np.ndarray, stats: dict, eps: float = BN_EPS) -> np.ndarray:
     return (y - mu) / np.sqrt(var + eps) * gamma + beta
 
 
+def groupnorm(y: np.ndarray, params: dict, group_channels: int = GN_GROUP_CHANNELS,
+              eps: float = BN_EPS) -> np.ndarray:
+    """GN (Wu & He's definition, inference = training: no running statistics).
+
+    Per image n and group g of `group_channels` consecutive channels:
+    mu = mean of y[n, :, :, g], var = mean of (y - mu)^2 over the same H*W*group_channels
+    values (biased), z = (y - mu) / sqrt(var + eps) * gamma[c] + beta[c].
+    params: dict with gamma, beta (per channel of this width; mean/var are not used).
+    """
+    B, H, W, c = y.shape
+    assert c % group_channels == 0, "active channels must hold whole groups (reading R16)"
+    G = c // group_channels
+    yg = y.reshape(B, H, W, G, group_channels)
+    mu = yg.mean(axis=(1, 2, 4), keepdims=True)
+    var = ((yg - mu) ** 2).mean(axis=(1, 2, 4), keepdims=True)
+    z = ((yg - mu) / np.sqrt(var + eps)).reshape(B, H, W, c)
+    gamma = np.asarray(params["gamma"], np.float64)[:c]
+    beta = np.asarray(params["beta"], np.float64)[:c]
+    assert gamma.shape[0] == c, "GN affine shorter than the active channel count"
+    return z * gamma + beta
+
+
 def relu(z: np.ndarray) -> np.ndarray:
     """O4: max(z, 0)."""
     return np.maximum(z, 0.0)
@@ -133,13 +161,17 @@ class Model:
     """
 
     def __init__(self, weights: dict, bn: dict, widths=(0.25, 0.5, 0.75, 1.0),
-                 base=(64, 128, 256, 512), blocks=(2, 2, 2, 2), eps: float = BN_EPS):
+                 base=(64, 128, 256, 512), blocks=(2, 2, 2, 2), eps: float = BN_EPS,
+                 norm: str = "bn", group_channels: int = GN_GROUP_CHANNELS):
         self.w = {k: np.ascontiguousarray(v, dtype=np.float64) for k, v in weights.items()}
         self.bn = bn
         self.widths = tuple(float(r) for r in widths)
         self.base = tuple(base)
         self.blocks = tuple(blocks)
         self.eps = eps
+        assert norm in ("bn", "gn")
+        self.norm = norm                  # "bn": O3 switchable BN (NS); "gn": GroupNorm
+        self.group_channels = group_channels
 
     def width_index(self, r: float) -> int:
         for i, q in enumerate(self.widths):
@@ -148,11 +180,15 @@ class Model:
         raise ValueError(f"width {r} not in the slimming set {self.widths}")
 
     def conv_bn(self, x, name, r, stride, pad, bn_width=None):
-        """conv (O2) at output width c(r, Cout) followed by BN_{name, width r} (O3)."""
+        """conv (O2) at output width c(r, Cout) followed by BN_{name, width r} (O3),
+        or by GN with that width's affine (gamma, beta) when norm == "gn"."""
         w = self.w[name]
         c_out = channels(r, w.shape[0])
         y = conv2d(x, w, c_out, stride, pad)
-        return batchnorm(y, self.bn[name][self.width_index(r if bn_width is None else bn_width)], self.eps)
+        params = self.bn[name][self.width_index(r if bn_width is None else bn_width)]
+        if self.norm == "gn":
+            return groupnorm(y, params, self.group_channels, self.eps)
+        return batchnorm(y, params, self.eps)
 
     # O5 BasicBlock
     def basic_block(self, x, s, b, r, bn_width=None):

@@ -26,9 +26,16 @@ def _bn(y, st, eps):
                         training=False, eps=eps)
 
 
+def _gn(y, st, eps, group_channels=16):
+    c = y.shape[1]
+    t = lambda a: torch.as_tensor(a[:c]).double()
+    return F.group_norm(y, c // group_channels, t(st["gamma"]), t(st["beta"]), eps=eps)
+
+
 def segment(weights, bn, widths, s, x_nchw, r_prev, r, base=(64, 128, 256, 512), blocks=(2, 2, 2, 2),
-            eps=1e-5, head=True):
+            eps=1e-5, head=True, norm="bn"):
     wi = [abs(q - r) < 1e-6 for q in widths].index(True)
+    _bn = _gn if norm == "gn" else globals()["_bn"]
     C = active_channels(r, base[s])
     h = x_nchw
     if s == 0:
