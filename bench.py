@@ -58,12 +58,12 @@ def _cores():
 
 
 # ------------------------------------------------------------------ CPU oracle legs
-def oracle_throughput(target_s: float = 15.0, batch_per_width: int | None = None):
+def oracle_throughput(target_s: float = 15.0, batch_per_width: int | None = None, norm: str = "bn"):
     """The fp64 oracle as it stands on this host's cores: images/s on a bounded sample of CFG2
     (equal images per width, like the GPU step)."""
     import oracle
     import synth
-    m = oracle.Model(synth.make_weights(), synth.make_bn())
+    m = oracle.Model(synth.make_weights(), synth.make_bn(), norm=norm)
     x = synth.make_images(128, offset=1)
     if batch_per_width is None:   # size the sample to ~target_s of CPU work
         t0 = time.perf_counter()
@@ -87,7 +87,7 @@ def run_reference(args):
         return 0
     import oracle
     import synth
-    m = oracle.Model(synth.make_weights(), synth.make_bn())
+    m = oracle.Model(synth.make_weights(), synth.make_bn(), norm=args.norm)
     x = synth.make_images(128, offset=1)
     step = lambda k: [m.chain(x[k % 128:k % 128 + 1], (r,) * 4) for r in WIDTHS]
     for k in range(args.warmup):
@@ -104,7 +104,7 @@ def run_reference(args):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": "CFG2: full SlimResNet chain (4 segments + pool/FC, 100 classes) at each width "
                                "r in {0.25,0.5,0.75,1.0}; reference step = 1 image per width", "batch": 1,
-                   "image": [32, 32, 3], "widths": list(WIDTHS)},
+                   "image": [32, 32, 3], "widths": list(WIDTHS), "norm": args.norm},
         "cpu_baseline": {"value": value, "unit": "images/s", "cores": _cores(), "kind": "oracle",
                          "sample": f"{args.steps} steps x 1 image per width of the CFG2 chain"},
         "e2e": {"value": value, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -134,7 +134,7 @@ def run_ours(args):
 
     B = args.batch
     weights, bn = synth.make_weights(), synth.make_bn()
-    net = slim.SlimNet(weights, bn, device=local, max_batch=max(B, 16))
+    net = slim.SlimNet(weights, bn, device=local, max_batch=max(B, 16), norm=args.norm)
     if not args.no_graph:
         slim.slim_set_graph_mode(net.ctx, True)
     stream = torch.cuda.current_stream(dev)
@@ -301,14 +301,14 @@ def run_ours(args):
     e2e_val = world * imgs_per_step * KE / float(te.item())
 
     if rank == 0:
-        cpu = oracle_throughput(args.cpu_seconds) if (world == 1 and not args.no_cpu) else None
+        cpu = oracle_throughput(args.cpu_seconds, norm=args.norm) if (world == 1 and not args.no_cpu) else None
         line = {
             "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world, "steps": K,
             "warmup": args.warmup, "ms_per_step": total_max_ms / K, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded N(0,1) images, random-init weights)",
             "config": {"workload": "CFG2: full SlimResNet chain (4 segments + pool/FC, 100 classes) at each width "
                                    "r in {0.25,0.5,0.75,1.0}, batch 128 per width, 1 step = 4 x 128 images",
-                       "batch": B, "image": [32, 32, 3], "widths": list(WIDTHS),
+                       "batch": B, "image": [32, 32, 3], "widths": list(WIDTHS), "norm": args.norm,
                        "parallelism": f"dp{world} (independent per-GPU batches)",
                        "l2": "flushed (256 MiB write) before every timed step", "graphs": not args.no_graph,
                        "instances": "sequential" if args.sequential else
@@ -435,7 +435,7 @@ def run_points(args):
     points = [(8, 0.25, "seg0")] if args.workload == "cfg1" else \
         [(B, r, "chain") for B in (1, 2, 4, 8, 16, 32, 64, 128, 256, 512, 1024, 2048, 4096) for r in WIDTHS]
     bmax = max(p[0] for p in points)
-    net = slim.SlimNet(synth.make_weights(), synth.make_bn(), device=local, max_batch=bmax)
+    net = slim.SlimNet(synth.make_weights(), synth.make_bn(), device=local, max_batch=bmax, norm=args.norm)
     slim.slim_set_graph_mode(net.ctx, True)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     xall = torch.from_numpy(synth.make_images(bmax, offset=300)).to(torch.bfloat16).cuda()
@@ -515,6 +515,8 @@ def main(argv=None):
     ap.add_argument("--requests", type=int, default=1024, help="stream: requests per rank per step")
     ap.add_argument("--bmax", type=int, default=256, help="stream: B_max of the key batching")
     ap.add_argument("--policy", default="random", help="stream: routing policy (random | slim | table_rr)")
+    ap.add_argument("--norm", choices=("bn", "gn"), default="bn",
+                    help="bn = switchable BatchNorm (north_star, default); gn = GroupNorm variant (P:148, NEXT-1)")
     args = ap.parse_args(argv)
     assert args.warmup >= 0 and args.steps >= 1
     if args.impl == "reference":

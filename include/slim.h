@@ -67,6 +67,15 @@ typedef enum {
 
 typedef enum { SLIM_BF16 = 0, SLIM_FP32 = 1 } slim_dtype;
 
+/* Normalisation after every conv.  SLIM_NORM_BN: switchable inference BatchNorm per
+ * width (north_star; folded into the conv epilogue).  SLIM_NORM_GN: GroupNorm, what the
+ * paper's model uses ("Group Normalization instead of Batch Normalization to avoid
+ * cross-width statistics drift"): statistics per
+ * (image, group of gn_group_channels consecutive channels) over H*W*gn_group_channels
+ * values, biased variance, bn_eps; affine gamma/beta per (layer, width) (slim_bn's
+ * mean/var are not read and may be NULL).  DESIGN.md reading R16. */
+typedef enum { SLIM_NORM_BN = 0, SLIM_NORM_GN = 1 } slim_norm;
+
 /* Network configuration (reading D1 = CIFAR ResNet-18). */
 typedef struct {
     int n_widths;              /* |W|, 1..8 */
@@ -79,6 +88,9 @@ typedef struct {
     int max_batch;             /* B_max: bounds every batch; sizes the internal workspace */
     float bn_eps;              /* BatchNorm epsilon, 1e-5 */
     slim_dtype dtype;          /* SLIM_BF16 (default) or SLIM_FP32 */
+    slim_norm norm;            /* SLIM_NORM_BN (default) or SLIM_NORM_GN */
+    int gn_group_channels;     /* GN group size, default 16; a multiple of 8 dividing every c(r, C_s),
+                                  else slim_create returns SLIM_EUNSUPPORTED */
 } slim_config;
 
 /* Host pointers to ONE segment's full-width weights, fp32 values (copied at load).
@@ -200,6 +212,62 @@ SLIM_API slim_status slim_gather(slim_ctx *ctx, const void *src, const uint32_t 
 SLIM_API slim_status slim_scatter(slim_ctx *ctx, const void *src, const uint32_t *idx, int n, size_t row_bytes,
                                   void *dst, size_t dst_stride, void *stream);
 
+/* ---- Algorithm 1: greedy segment-slim scheduler (host) ----
+ * A per-server decision engine: FIFO queue of requests keyed (s, w_req, w_prev), batch
+ * formation from the head key (l.3-4), FINDFREEBESTFIT (l.5, l.11-12: free instance of
+ * segment s with the smallest width >= w_req), CANLOAD (l.7, l.13-20: VRAM cap M_max and
+ * utilisation gate U_blk), the opportunistic scale-up of P:49 (up to N_new instances of
+ * key k when its queue holds >= Q_th requests, else one; each guarded by CANLOAD),
+ * requeue-to-front on failure (l.9) and UNLOADERLOOP (l.21-25: non-busy instances idle
+ * >= t_idle are removed).  Host only, no CUDA calls, thread-safe (one mutex).  An
+ * "instance" is an execution slot (the caller gives each one a CUDA stream); its
+ * bytes are slim_segment_bytes(cfg, s, w, w), and VRAM_used = vram_external (passed by
+ * the caller) + the bytes of the live instances (reading R17). */
+typedef struct {
+    int B_max;                 /* batch limit */
+    double M_max_bytes;        /* VRAM cap M_max (bytes) */
+    float U_blk;               /* utilisation block threshold, fraction in [0, 1] */
+    double t_idle_s;           /* idle-unload time t_idle (s) */
+    int Q_th;                  /* scale trigger: key-k queue length that scales up by N_new */
+    int N_new;                 /* scale cap: instances added per scale-up */
+} slim_sched_knobs;
+typedef struct slim_sched slim_sched;
+typedef enum { SLIM_ACT_IDLE = 0, SLIM_ACT_RUN = 1, SLIM_ACT_REQUEUE = 2 } slim_sched_act_kind;
+typedef struct {
+    int kind;                  /* slim_sched_act_kind: IDLE = queue empty; REQUEUE = no instance (l.9) */
+    int inst;                  /* RUN: instance id (busy until slim_sched_complete) */
+    int seg;                   /* the batch key (s, w_req, w_prev) (w_prev = 0 for seg 0) */
+    float w_req, w_prev;
+    float inst_w;              /* RUN: the instance's width (>= w_req; compute follows w_req, R9) */
+    int batch;                 /* RUN: requests taken; their slots/ids are written in FIFO order */
+    int n_loaded;              /* instances created by this call (CANLOAD passed) */
+} slim_sched_action;
+typedef struct {
+    int id, seg;
+    float w;
+    int busy;
+    double t_last;
+    size_t bytes;
+} slim_instance;
+/* Defaults: B_max 256, M_max 64e9 B (the paper's 64 GB devices), U_blk 0.95,
+ * t_idle 1 s, Q_th 512, N_new 2 (the paper gives no values; all knobs). */
+SLIM_API void slim_sched_default_knobs(slim_sched_knobs *k);
+SLIM_API slim_status slim_sched_create(const slim_config *cfg, const slim_sched_knobs *knobs, slim_sched **out);
+SLIM_API void slim_sched_destroy(slim_sched *s);
+/* Append n requests (key validated against cfg's widths; SLIM_EINVAL leaves Q unchanged). */
+SLIM_API slim_status slim_sched_enqueue(slim_sched *s, const slim_request *reqs, int n, double t_enq);
+/* One LOOP iteration at time `now` (s).  util: latest utilisation sample in [0,1], or < 0
+ * for none (l.18 "u != empty").  slots (and ids if non-NULL) must hold B_max entries. */
+SLIM_API slim_status slim_sched_next(slim_sched *s, double now, float util, size_t vram_external,
+                                     slim_sched_action *act, uint32_t *slots, uint64_t *ids);
+/* RUNBATCH finished on instance inst: busy = false, t_last = now. */
+SLIM_API slim_status slim_sched_complete(slim_sched *s, int inst, double now);
+/* UNLOADERLOOP pass: removes idle instances, writes up to max_removed ids, returns the count. */
+SLIM_API int slim_sched_unload_idle(slim_sched *s, double now, int *removed, int max_removed);
+SLIM_API int slim_sched_queue_len(const slim_sched *s);
+/* Copies up to max_out instance records; returns the number of live instances. */
+SLIM_API int slim_sched_instances(const slim_sched *s, slim_instance *out, int max_out);
+
 /* ---- execution modes and profiling ------------------------------------- */
 
 /* Graph mode (default off): slim_forward_ws / slim_forward_chain capture their
@@ -215,7 +283,8 @@ SLIM_API slim_status slim_set_graph_mode(slim_ctx *ctx, int enable);
  * residual / projection input read once, output written once).  Graph replay
  * is bypassed while profiling.  begin() allocates the events (at most
  * max_launches records); end() synchronises and returns the records. */
-typedef enum { SLIM_K_STEM = 0, SLIM_K_CONV_UMMA = 1, SLIM_K_HEAD = 2, SLIM_K_GATHER = 3, SLIM_K_CONV_F32 = 4 } slim_kernel_kind;
+typedef enum { SLIM_K_STEM = 0, SLIM_K_CONV_UMMA = 1, SLIM_K_HEAD = 2, SLIM_K_GATHER = 3, SLIM_K_CONV_F32 = 4,
+               SLIM_K_GN = 5 /* GroupNorm apply (SLIM_NORM_GN) */ } slim_kernel_kind;
 typedef struct {
     int kind;                  /* slim_kernel_kind */
     int seg, layer;            /* segment, manifest index of the conv (stem = 0 in seg 0; head/gather: -1) */

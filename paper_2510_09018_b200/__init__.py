@@ -21,13 +21,14 @@ __all__ = [
     "slim_load_segment", "slim_unload_segment", "slim_segment_bytes", "slim_forward", "slim_forward_ws",
     "slim_forward_workspace_bytes", "slim_chain_workspace_bytes", "slim_forward_chain", "slim_pack",
     "slim_launch", "slim_gather", "slim_scatter", "slim_last_error", "slim_launch_count", "slim_channels", "SlimNet",
-    "manifest", "LIB_PATH",
+    "manifest", "LIB_PATH", "Scheduler",
 ]
 
 LIB_PATH = os.environ.get("SLIM_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libslim.so")
 
 SLIM_OK, SLIM_EINVAL, SLIM_ENOTLOADED, SLIM_ENOMEM, SLIM_ECUDA, SLIM_EUNSUPPORTED = 0, -1, -2, -3, -4, -5
 SLIM_BF16, SLIM_FP32 = 0, 1
+SLIM_NORM_BN, SLIM_NORM_GN = 0, 1
 
 
 class SlimError(RuntimeError):
@@ -44,7 +45,7 @@ class slim_config(ctypes.Structure):
     _fields_ = [("n_widths", ctypes.c_int), ("widths", ctypes.c_float * 8), ("blocks_per_seg", ctypes.c_int * 4),
                 ("base_channels", ctypes.c_int * 4), ("in_channels", ctypes.c_int), ("num_classes", ctypes.c_int),
                 ("image_hw", ctypes.c_int), ("max_batch", ctypes.c_int), ("bn_eps", ctypes.c_float),
-                ("dtype", ctypes.c_int)]
+                ("dtype", ctypes.c_int), ("norm", ctypes.c_int), ("gn_group_channels", ctypes.c_int)]
 
 
 class slim_seg_weights(ctypes.Structure):
@@ -72,13 +73,31 @@ class slim_profile_record(ctypes.Structure):
                 ("bytes", ctypes.c_double), ("ms", ctypes.c_float)]
 
 
-KERNEL_KINDS = {0: "stem", 1: "conv_umma", 2: "head", 3: "gather", 4: "conv_f32"}
+KERNEL_KINDS = {0: "stem", 1: "conv_umma", 2: "head", 3: "gather", 4: "conv_f32", 5: "gn"}
 
 
 class slim_launch_desc(ctypes.Structure):
     _fields_ = [("seg", ctypes.c_int), ("r_prev", ctypes.c_float), ("r", ctypes.c_float), ("batch", ctypes.c_int),
                 ("first", ctypes.c_int)]
 
+
+class slim_sched_knobs(ctypes.Structure):
+    _fields_ = [("B_max", ctypes.c_int), ("M_max_bytes", ctypes.c_double), ("U_blk", ctypes.c_float),
+                ("t_idle_s", ctypes.c_double), ("Q_th", ctypes.c_int), ("N_new", ctypes.c_int)]
+
+
+class slim_sched_action(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int), ("inst", ctypes.c_int), ("seg", ctypes.c_int), ("w_req", ctypes.c_float),
+                ("w_prev", ctypes.c_float), ("inst_w", ctypes.c_float), ("batch", ctypes.c_int),
+                ("n_loaded", ctypes.c_int)]
+
+
+class slim_instance(ctypes.Structure):
+    _fields_ = [("id", ctypes.c_int), ("seg", ctypes.c_int), ("w", ctypes.c_float), ("busy", ctypes.c_int),
+                ("t_last", ctypes.c_double), ("bytes", ctypes.c_size_t)]
+
+
+SLIM_ACT_IDLE, SLIM_ACT_RUN, SLIM_ACT_REQUEUE = 0, 1, 2
 
 _lib = None
 _VP, _SZ, _I, _F = ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_float
@@ -122,6 +141,17 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "slim_set_graph_mode": (_I, [_VP, _I]),
         "slim_profile_begin": (_I, [_VP, _I]),
         "slim_profile_end": (_I, [_VP, ctypes.POINTER(slim_profile_record), _I, ctypes.POINTER(_I)]),
+        "slim_sched_default_knobs": (None, [ctypes.POINTER(slim_sched_knobs)]),
+        "slim_sched_create": (_I, [ctypes.POINTER(slim_config), ctypes.POINTER(slim_sched_knobs),
+                                   ctypes.POINTER(_VP)]),
+        "slim_sched_destroy": (None, [_VP]),
+        "slim_sched_enqueue": (_I, [_VP, ctypes.POINTER(slim_request), _I, ctypes.c_double]),
+        "slim_sched_next": (_I, [_VP, ctypes.c_double, _F, _SZ, ctypes.POINTER(slim_sched_action),
+                                 ctypes.POINTER(ctypes.c_uint32), ctypes.POINTER(ctypes.c_uint64)]),
+        "slim_sched_complete": (_I, [_VP, _I, ctypes.c_double]),
+        "slim_sched_unload_idle": (_I, [_VP, ctypes.c_double, ctypes.POINTER(_I), _I]),
+        "slim_sched_queue_len": (_I, [_VP]),
+        "slim_sched_instances": (_I, [_VP, ctypes.POINTER(slim_instance), _I]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -136,7 +166,9 @@ EXPORTED = ("slim_create", "slim_destroy", "slim_default_config", "slim_load_seg
             "slim_forward_ws", "slim_chain_workspace_bytes", "slim_forward_chain", "slim_pack", "slim_launch",
             "slim_gather", "slim_scatter", "slim_last_error", "slim_last_error_msg", "slim_status_str", "slim_version",
             "slim_launch_count", "slim_num_sms", "slim_channels", "slim_set_graph_mode", "slim_profile_begin",
-            "slim_profile_end")
+            "slim_profile_end", "slim_sched_default_knobs", "slim_sched_create", "slim_sched_destroy",
+            "slim_sched_enqueue", "slim_sched_next", "slim_sched_complete", "slim_sched_unload_idle",
+            "slim_sched_queue_len", "slim_sched_instances")
 
 
 # ------------------------------------------------------------------ marshalling helpers
@@ -180,6 +212,8 @@ def default_config(**kw) -> slim_config:
                 getattr(cfg, k)[i] = c
         elif k == "dtype":
             cfg.dtype = {"bf16": SLIM_BF16, "fp32": SLIM_FP32}.get(v, v)
+        elif k == "norm":
+            cfg.norm = {"bn": SLIM_NORM_BN, "gn": SLIM_NORM_GN}.get(v, v)
         else:
             setattr(cfg, k, v)
     return cfg
@@ -209,7 +243,8 @@ def slim_destroy(ctx):
 
 
 def slim_load_segment(ctx, seg: int, conv_w: list, bn_per_width: list, fc_w=None, fc_b=None):
-    """conv_w: fp32 host arrays in manifest order; bn_per_width: [width][layer] dicts(gamma,beta,mean,var)."""
+    """conv_w: fp32 host arrays in manifest order; bn_per_width: [width][layer] dicts(gamma,beta,mean,var)
+    (GroupNorm mode reads gamma/beta only; mean/var may be absent)."""
     lib = load_library()
     keep = []
     w = slim_seg_weights()
@@ -227,9 +262,10 @@ def slim_load_segment(ctx, seg: int, conv_w: list, bn_per_width: list, fc_w=None
     for wi, layers in enumerate(bn_per_width):
         arr = (slim_bn * len(layers))()
         for li, st in enumerate(layers):
-            vals = [np.ascontiguousarray(st[k], dtype=np.float32) for k in ("gamma", "beta", "mean", "var")]
-            keep += vals
-            arr[li] = slim_bn(*[v.ctypes.data for v in vals])
+            vals = [np.ascontiguousarray(st[k], dtype=np.float32) if st.get(k) is not None else None
+                    for k in ("gamma", "beta", "mean", "var")]
+            keep += [v for v in vals if v is not None]
+            arr[li] = slim_bn(*[v.ctypes.data if v is not None else None for v in vals])
         keep.append(arr)
         sets[wi] = slim_bn_set(ctypes.cast(arr, ctypes.POINTER(slim_bn)), len(layers))
     _check(ctx, lib.slim_load_segment(ctx, seg, ctypes.byref(w), sets))
@@ -327,6 +363,74 @@ def slim_profile_end(ctx, max_out: int = 1 << 20):
     _check(ctx, lib.slim_profile_end(ctx, recs, n.value, ctypes.byref(n)))
     return [dict(kind=KERNEL_KINDS.get(r.kind, r.kind), seg=r.seg, layer=r.layer, batch=r.batch, r_prev=r.r_prev,
                  r=r.r, flops=r.flops, bytes=r.bytes, ms=r.ms) for r in recs[:n.value]]
+
+
+# ------------------------------------------------------------------ Alg. 1 scheduler (host)
+class Scheduler:
+    """Marshalling wrapper of the native Alg. 1 decision engine (slim_sched_*, include/slim.h).
+
+    requests: iterables of (id, seg, w_req, w_prev, slot).  next() returns a dict
+    (kind, inst, seg, w_req, w_prev, inst_w, batch, n_loaded, slots, ids)."""
+
+    KIND = {SLIM_ACT_IDLE: "idle", SLIM_ACT_RUN: "run", SLIM_ACT_REQUEUE: "requeue"}
+
+    def __init__(self, cfg: slim_config, **knobs):
+        lib = load_library()
+        self.k = slim_sched_knobs()
+        lib.slim_sched_default_knobs(ctypes.byref(self.k))
+        for name, v in knobs.items():
+            setattr(self.k, name, v)
+        h = ctypes.c_void_p()
+        _check(None, lib.slim_sched_create(ctypes.byref(cfg), ctypes.byref(self.k), ctypes.byref(h)))
+        self.h = h.value
+        self._slots = (ctypes.c_uint32 * self.k.B_max)()
+        self._ids = (ctypes.c_uint64 * self.k.B_max)()
+
+    def enqueue(self, requests, t_enq: float = 0.0):
+        reqs = list(requests)
+        q = (slim_request * max(len(reqs), 1))()
+        for i, (rid, seg, wr, wp, slot) in enumerate(reqs):
+            q[i] = slim_request(rid, seg, wr, wp, slot)
+        _check(None, load_library().slim_sched_enqueue(self.h, q, len(reqs), t_enq))
+
+    def next(self, now: float, util: float = -1.0, vram_external: int = 0) -> dict:
+        act = slim_sched_action()
+        _check(None, load_library().slim_sched_next(self.h, now, util, vram_external, ctypes.byref(act),
+                                                    self._slots, self._ids))
+        n = act.batch if act.kind == SLIM_ACT_RUN else 0
+        return dict(kind=self.KIND[act.kind], inst=act.inst, seg=act.seg, w_req=act.w_req, w_prev=act.w_prev,
+                    inst_w=act.inst_w, batch=act.batch, n_loaded=act.n_loaded,
+                    slots=np.frombuffer(self._slots, np.uint32, n).copy(),
+                    ids=np.frombuffer(self._ids, np.uint64, n).copy())
+
+    def complete(self, inst: int, now: float):
+        _check(None, load_library().slim_sched_complete(self.h, inst, now))
+
+    def unload_idle(self, now: float):
+        buf = (ctypes.c_int * 256)()
+        n = load_library().slim_sched_unload_idle(self.h, now, buf, 256)
+        return list(buf[:min(n, 256)])
+
+    def queue_len(self) -> int:
+        return load_library().slim_sched_queue_len(self.h)
+
+    def instances(self):
+        lib = load_library()
+        n = lib.slim_sched_instances(self.h, None, 0)
+        buf = (slim_instance * max(n, 1))()
+        lib.slim_sched_instances(self.h, buf, n)
+        return [dict(id=i.id, seg=i.seg, w=i.w, busy=bool(i.busy), t_last=i.t_last, bytes=i.bytes) for i in buf[:n]]
+
+    def close(self):
+        if self.h:
+            load_library().slim_sched_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 # ------------------------------------------------------------------ convenience

@@ -1,0 +1,253 @@
+// kernels_gn.cu -- GroupNorm (+ shortcut) (+ ReLU) for the GroupNorm variant of the network.
+//
+// "We employ Group Normalization instead of Batch Normalization to avoid
+// cross-width statistics drift".  Reading R16: groups of `cpg` (16) consecutive
+// channels; statistics per (image, group) over H*W*cpg values; biased variance; eps.
+//
+// The convs run with an identity epilogue and no ReLU (relu_lo = -inf) and store the raw
+// pre-norm output y; this kernel then computes, per (image n, group g),
+//   mu = mean(y[n, :, :, g]),  var = mean((y - mu)^2)          (two passes, fp32)
+// and writes  out = act( (y - mu) * rsqrt(var + eps) * gamma + beta
+//                        [ + (yp - mu_p) * rsqrt(var_p + eps) * gamma_p + beta_p ]   (projection shortcut)
+//                        [ + res ] )                                                  (identity shortcut)
+// act = ReLU or identity.  out may alias y (each element is read and written by the same
+// thread in the last pass, after both statistics passes).
+//
+// Layout: NHWC, dense; a CTA owns gpc whole groups of one image (gpc*cpg contiguous
+// channels per pixel) and reads them as 16-byte vectors: thread t always handles the
+// same vector slot v = t % V of the pixel row, pixels t / V, t / V + k, ... (k = threads / V),
+// so its partial sums belong to one group; the partials are reduced in a fixed order
+// (warp butterflies + a per-warp sum, see group_sums): deterministic and independent of B.
+// HBM-bound: y is read once (held in registers, kGnPPT pixels x 16 B per thread), the shortcut
+// once, out written once.
+#include "slim_internal.h"
+
+#include <cuda_bf16.h>
+
+namespace slim {
+namespace {
+
+// 16-byte vectors are kept packed in registers (uint4: 8 bf16 or 4 fp32) and unpacked on use
+template <typename T>
+__device__ __forceinline__ uint4 ld16(const T *p) { return *reinterpret_cast<const uint4 *>(p); }
+__device__ __forceinline__ void unpack(const uint4 &q, uint16_t, float *v) {
+    const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        v[2 * i] = __uint_as_float(w[i] << 16);
+        v[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
+    }
+}
+__device__ __forceinline__ void unpack(const uint4 &q, float, float *v) {
+    v[0] = __uint_as_float(q.x);
+    v[1] = __uint_as_float(q.y);
+    v[2] = __uint_as_float(q.z);
+    v[3] = __uint_as_float(q.w);
+}
+__device__ __forceinline__ uint32_t pack2(float a, float b) {
+    const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);   // RNE
+    return *reinterpret_cast<const uint32_t *>(&h);
+}
+__device__ __forceinline__ void store_vec(uint16_t *p, const float *v) {
+    *reinterpret_cast<uint4 *>(p) = make_uint4(pack2(v[0], v[1]), pack2(v[2], v[3]), pack2(v[4], v[5]), pack2(v[6], v[7]));
+}
+__device__ __forceinline__ void store_vec(float *p, const float *v) {
+    *reinterpret_cast<float4 *>(p) = make_float4(v[0], v[1], v[2], v[3]);
+}
+
+constexpr int kGnMaxThreads = 512;
+constexpr int kGnPPT = 8;       // pixels per thread: the CTA's slice lives in registers (y read once)
+constexpr int kGnMaxCh = 512;   // channels per CTA slice
+
+// Per-(local group) totals of one partial pair per thread, in a fixed order (deterministic,
+// independent of B).  Thread t holds vector slot v = t % V (group v / vpg) of pixel lane t / V.
+// Fast path (V < 32, whole warps): butterfly over the group's vpg slots and over the warp's
+// pixel lanes (offsets V .. 16), one partial per (warp, group) in smem, summed over warps.
+// Otherwise every thread's partial goes to smem and thread g sums its group's k*vpg partials.
+__device__ __forceinline__ void group_sums(float x0, float x1, int V, int vpg, int k, int gpc, float2 *part,
+                                           float *out0, float *out1) {
+    const int t = threadIdx.x, lane = t & 31, nw = blockDim.x >> 5;
+    if (V < 32 && (blockDim.x & 31) == 0) {
+        for (int o = 1; o < vpg; o <<= 1) {
+            x0 += __shfl_xor_sync(0xffffffffu, x0, o);
+            x1 += __shfl_xor_sync(0xffffffffu, x1, o);
+        }
+        for (int o = V; o < 32; o <<= 1) {
+            x0 += __shfl_xor_sync(0xffffffffu, x0, o);
+            x1 += __shfl_xor_sync(0xffffffffu, x1, o);
+        }
+        if (lane < V && lane % vpg == 0) part[(t >> 5) * gpc + lane / vpg] = make_float2(x0, x1);
+        __syncthreads();
+        if (t < gpc) {
+            float2 s = make_float2(0.f, 0.f);
+            for (int w = 0; w < nw; ++w) {
+                s.x += part[w * gpc + t].x;
+                s.y += part[w * gpc + t].y;
+            }
+            out0[t] = s.x;
+            out1[t] = s.y;
+        }
+    } else {
+        part[t] = make_float2(x0, x1);
+        __syncthreads();
+        if (t < gpc) {
+            float2 s = make_float2(0.f, 0.f);
+            for (int m = 0; m < k; ++m)
+                for (int j = 0; j < vpg; ++j) {
+                    s.x += part[m * V + t * vpg + j].x;
+                    s.y += part[m * V + t * vpg + j].y;
+                }
+            out0[t] = s.x;
+            out1[t] = s.y;
+        }
+    }
+    __syncthreads();
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kGnMaxThreads, 1) gn_kernel(const GnArgs a) {
+    constexpr int VE = 16 / sizeof(T);   // elements per 16-byte vector
+    __shared__ float2 part[kGnMaxThreads];
+    __shared__ float gsum[2][kGnMaxCh / 8];
+    __shared__ float stat[2][2][kGnMaxCh / 8];          // [y|yp][mean|rstd][local group]
+    __shared__ float coef[2][2][kGnMaxCh];              // [y|yp][A|Bc] per channel of the slice
+    const int n = blockIdx.y;
+    const int ch0 = blockIdx.x * a.gpc * a.cpg;         // first channel of this CTA's slice
+    const int V = a.gpc * a.cpg / VE, vpg = a.cpg / VE;
+    const int t = threadIdx.x, v = t % V, k = blockDim.x / V;
+    const bool two = a.yp != nullptr;
+    const size_t img = static_cast<size_t>(n) * a.HW * a.C;
+    const size_t base = img + ch0 + v * VE;
+    const float inv_cnt = 1.f / (static_cast<float>(a.HW) * a.cpg);
+    const int p0 = t / V;
+
+    // programmatic dependent launch: the index math above overlaps the producing conv's tail;
+    // dependents may start their prologue now (their own wait covers this grid's completion)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+
+    // the slice into registers: pixels p0, p0 + k, ... (< kGnPPT of them), all loads in flight
+    uint4 q0[kGnPPT], q1[kGnPPT];
+#pragma unroll
+    for (int j = 0; j < kGnPPT; ++j) {
+        const int p = p0 + j * k;
+        q0[j] = q1[j] = make_uint4(0u, 0u, 0u, 0u);
+        if (p < a.HW) {
+            q0[j] = ld16(static_cast<const T *>(a.y) + base + static_cast<size_t>(p) * a.C);
+            if (two) q1[j] = ld16(static_cast<const T *>(a.yp) + base + static_cast<size_t>(p) * a.C);
+        }
+    }
+    // pass 1: sums -> means
+    float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+    for (int j = 0; j < kGnPPT; ++j)
+        if (p0 + j * k < a.HW) {
+            float x0[VE], x1[VE];
+            unpack(q0[j], T(), x0);
+            unpack(q1[j], T(), x1);
+#pragma unroll
+            for (int i = 0; i < VE; ++i) {
+                s0 += x0[i];
+                if (two) s1 += x1[i];
+            }
+        }
+    group_sums(s0, s1, V, vpg, k, a.gpc, part, gsum[0], gsum[1]);
+    const int lg = v / vpg;
+    const float mu0 = gsum[0][lg] * inv_cnt, mu1 = gsum[1][lg] * inv_cnt;
+    if (t < a.gpc) {
+        stat[0][0][t] = gsum[0][t] * inv_cnt;
+        stat[1][0][t] = gsum[1][t] * inv_cnt;
+    }
+    // pass 2 (registers): sum of squared deviations -> rstd
+    s0 = 0.f;
+    s1 = 0.f;
+#pragma unroll
+    for (int j = 0; j < kGnPPT; ++j)
+        if (p0 + j * k < a.HW) {
+            float x0[VE], x1[VE];
+            unpack(q0[j], T(), x0);
+            unpack(q1[j], T(), x1);
+#pragma unroll
+            for (int i = 0; i < VE; ++i) {
+                s0 = fmaf(x0[i] - mu0, x0[i] - mu0, s0);
+                if (two) s1 = fmaf(x1[i] - mu1, x1[i] - mu1, s1);
+            }
+        }
+    __syncthreads();   // every thread has read gsum (means) before it is overwritten
+    group_sums(s0, s1, V, vpg, k, a.gpc, part, gsum[0], gsum[1]);
+    if (t < a.gpc) {
+        stat[0][1][t] = rsqrtf(gsum[0][t] * inv_cnt + a.eps);
+        stat[1][1][t] = rsqrtf(gsum[1][t] * inv_cnt + a.eps);
+    }
+    __syncthreads();
+    // per-channel affine of the slice in smem: z = y * A + Bc, A = rstd*gamma, Bc = beta - mu*A
+    for (int c = t; c < a.gpc * a.cpg; c += blockDim.x) {
+        const int g = c / a.cpg;
+        const float A = stat[0][1][g] * a.gamma[ch0 + c];
+        coef[0][0][c] = A;
+        coef[0][1][c] = fmaf(-stat[0][0][g], A, a.beta[ch0 + c]);
+        if (two) {
+            const float Ap = stat[1][1][g] * a.gamma_p[ch0 + c];
+            coef[1][0][c] = Ap;
+            coef[1][1][c] = fmaf(-stat[1][0][g], Ap, a.beta_p[ch0 + c]);
+        }
+    }
+    __syncthreads();
+    const float *A0 = coef[0][0] + v * VE, *B0 = coef[0][1] + v * VE, *A1 = coef[1][0] + v * VE,
+                *B1 = coef[1][1] + v * VE;
+    // pass 3: apply (+ shortcut) (+ ReLU); out may alias y (every y element is already in registers)
+#pragma unroll
+    for (int j = 0; j < kGnPPT; ++j) {
+        const int p = p0 + j * k;
+        if (p >= a.HW) continue;
+        float z[VE], x0[VE], x1[VE], r[VE];
+        unpack(q0[j], T(), x0);
+        unpack(q1[j], T(), x1);
+        unpack(a.res ? ld16(static_cast<const T *>(a.res) + base + static_cast<size_t>(p) * a.C) : make_uint4(0u, 0u, 0u, 0u),
+               T(), r);
+#pragma unroll
+        for (int i = 0; i < VE; ++i) {
+            z[i] = fmaf(x0[i], A0[i], B0[i]);
+            if (two) z[i] += fmaf(x1[i], A1[i], B1[i]);
+            if (a.res) z[i] += r[i];
+            z[i] = fmaxf(z[i], a.relu_lo);
+        }
+        store_vec(static_cast<T *>(a.out) + base + static_cast<size_t>(p) * a.C, z);
+    }
+}
+
+}  // namespace
+
+// Pixel lanes per vector slot: k = HW / kGnPPT (each thread holds kGnPPT pixels).
+static int gn_lanes(int HW) { return HW > kGnPPT ? (HW + kGnPPT - 1) / kGnPPT : 1; }
+
+int gn_groups_per_cta(int /*B*/, int HW, int C, int cpg, int /*num_sms*/) {
+    // independent of B (batch independence is bit-exact): widen the slice while it divides
+    // G and the CTA stays <= 512 threads (vpg = cpg/8 vectors per group in bf16, cpg/4 in fp32;
+    // sized for fp32 so both modes pick the same slice)
+    const int G = C / cpg, k = gn_lanes(HW), vpg = cpg / 4;
+    int gpc = 1;
+    while (G % (2 * gpc) == 0 && 2 * gpc * vpg * k <= kGnMaxThreads && 2 * gpc * cpg <= kGnMaxCh) gpc *= 2;
+    return gpc;
+}
+
+cudaError_t launch_gn(const GnArgs &a, bool fp32, cudaStream_t s, bool pdl) {
+    const int VE = fp32 ? 4 : 8;
+    if (a.cpg % VE || a.C % (a.gpc * a.cpg) || a.gpc * a.cpg > kGnMaxCh || a.HW < 1) return cudaErrorInvalidValue;
+    const int V = a.gpc * a.cpg / VE;
+    int k = 1;   // power-of-two pixel lanes per vector slot, every thread holds <= kGnPPT pixels
+    while (k < gn_lanes(a.HW)) k *= 2;
+    if (V * k > kGnMaxThreads || (a.HW + k - 1) / k > kGnPPT) return cudaErrorInvalidValue;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(a.C / (a.gpc * a.cpg), a.B);
+    cfg.blockDim = dim3(V * k);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return fp32 ? cudaLaunchKernelEx(&cfg, gn_kernel<float>, a) : cudaLaunchKernelEx(&cfg, gn_kernel<uint16_t>, a);
+}
+
+}  // namespace slim

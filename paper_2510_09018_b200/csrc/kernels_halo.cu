@@ -671,7 +671,7 @@ __global__ void __launch_bounds__(kSmall ? kHaloThreadsSmall : kHaloThreads, kSm
                     // (lanes of one image are W consecutive lanes), park it per (row = lane quarter,
                     // image, channel) in the staging tile; rows are summed below in fixed order
 #pragma unroll
-                    for (int i = 0; i < 16; ++i) f[i] = fmaxf(f[i], 0.f);
+                    for (int i = 0; i < 16; ++i) f[i] = fmaxf(f[i], a.relu_lo);
                     for (int o = 1; o < a.W; o <<= 1) {
 #pragma unroll
                         for (int i = 0; i < 16; ++i) f[i] += __shfl_xor_sync(0xffffffffu, f[i], o);
@@ -686,7 +686,7 @@ __global__ void __launch_bounds__(kSmall ? kHaloThreadsSmall : kHaloThreads, kSm
                 }
                 uint32_t o[8];
 #pragma unroll
-                for (int i = 0; i < 8; ++i) o[i] = pack_bf16(fmaxf(f[2 * i], 0.f), fmaxf(f[2 * i + 1], 0.f));
+                for (int i = 0; i < 8; ++i) o[i] = pack_bf16(fmaxf(f[2 * i], a.relu_lo), fmaxf(f[2 * i + 1], a.relu_lo));
                 *reinterpret_cast<uint4 *>(pOutG + off0) = make_uint4(o[0], o[1], o[2], o[3]);
                 *reinterpret_cast<uint4 *>(pOutG + off1) = make_uint4(o[4], o[5], o[6], o[7]);
             }

@@ -38,7 +38,8 @@ constexpr int kMaxStemW = 64, kMaxStemC = 4, kMaxStemCout = 64;
 template <typename TIn, typename TOut>
 __global__ void __launch_bounds__(kStemThreads)
     stem_kernel(const TIn *__restrict__ in, const float *__restrict__ w, int cin_full, const float *__restrict__ scale,
-                const float *__restrict__ shift, TOut *__restrict__ out, int H, int W, int cimg, int c0) {
+                const float *__restrict__ shift, TOut *__restrict__ out, int H, int W, int cimg, int c0,
+                float relu_lo) {
     __shared__ float s_in[(kStemRows + 2) * (kMaxStemW + 2) * kMaxStemC];
     __shared__ float s_w[kMaxStemCout * 9 * kMaxStemC];
     const int n = blockIdx.y;
@@ -76,7 +77,7 @@ __global__ void __launch_bounds__(kStemThreads)
         const size_t o = ((static_cast<size_t>(n) * H + h0 + r) * W + col) * c0 + g * 8;
         float y[8];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) y[j] = fmaxf(fmaf(acc[j], scale[g * 8 + j], shift[g * 8 + j]), 0.f);
+        for (int j = 0; j < 8; ++j) y[j] = fmaxf(fmaf(acc[j], scale[g * 8 + j], shift[g * 8 + j]), relu_lo);
         if constexpr (sizeof(TOut) == 2) {
             uint4 v = make_uint4(pack2(y[0], y[1]), pack2(y[2], y[3]), pack2(y[4], y[5]), pack2(y[6], y[7]));
             *reinterpret_cast<uint4 *>(out + o) = v;
@@ -314,7 +315,7 @@ __global__ void __launch_bounds__(kF32Threads) conv_f32_kernel(const ConvF32Args
             float f = fmaf(acc[i][j], a.scale0[c], a.shift0[c]);
             if (a.epi == EPI_BN_PROJ_RELU) f += fmaf(acc1[i][j], a.scale1[c], a.shift1[c]);
             if (a.epi == EPI_BN_ADD_RELU) f += a.res[o + c];
-            a.out[o + c] = fmaxf(f, 0.f);
+            a.out[o + c] = fmaxf(f, a.relu_lo);
         }
     }
 }
@@ -322,17 +323,19 @@ __global__ void __launch_bounds__(kF32Threads) conv_f32_kernel(const ConvF32Args
 }  // namespace
 
 cudaError_t launch_stem_bf16(const uint16_t *in, const float *w, int cin_full, const float *scale, const float *shift,
-                             uint16_t *out, int B, int H, int W, int cimg, int c0, cudaStream_t s) {
+                             uint16_t *out, int B, int H, int W, int cimg, int c0, cudaStream_t s,
+                             float relu_lo) {
     if (W > kMaxStemW || cimg > kMaxStemC || c0 > kMaxStemCout || c0 % 8) return cudaErrorInvalidValue;
     dim3 grid((H + kStemRows - 1) / kStemRows, B);
-    stem_kernel<uint16_t, uint16_t><<<grid, kStemThreads, 0, s>>>(in, w, cin_full, scale, shift, out, H, W, cimg, c0);
+    stem_kernel<uint16_t, uint16_t><<<grid, kStemThreads, 0, s>>>(in, w, cin_full, scale, shift, out, H, W, cimg, c0, relu_lo);
     return cudaGetLastError();
 }
 cudaError_t launch_stem_f32(const float *in, const float *w, int cin_full, const float *scale, const float *shift,
-                            float *out, int B, int H, int W, int cimg, int c0, cudaStream_t s) {
+                            float *out, int B, int H, int W, int cimg, int c0, cudaStream_t s,
+                            float relu_lo) {
     if (W > kMaxStemW || cimg > kMaxStemC || c0 > kMaxStemCout || c0 % 8) return cudaErrorInvalidValue;
     dim3 grid((H + kStemRows - 1) / kStemRows, B);
-    stem_kernel<float, float><<<grid, kStemThreads, 0, s>>>(in, w, cin_full, scale, shift, out, H, W, cimg, c0);
+    stem_kernel<float, float><<<grid, kStemThreads, 0, s>>>(in, w, cin_full, scale, shift, out, H, W, cimg, c0, relu_lo);
     return cudaGetLastError();
 }
 template <typename... KArgs, typename... Args>

@@ -290,7 +290,7 @@ __global__ void __launch_bounds__(kSplitThreads, 1)
                 }
             }
 #pragma unroll
-            for (int i = 0; i < 16; ++i) f[i] = fmaxf(f[i], 0.f);
+            for (int i = 0; i < 16; ++i) f[i] = fmaxf(f[i], a.relu_lo);
             if (a.pool_out) {
 #pragma unroll
                 for (int o = 1; o < 32; o <<= 1) {

@@ -205,7 +205,7 @@ __global__ void __launch_bounds__(kStemThreads, 1)
                 float f[16];
 #pragma unroll
                 for (int i = 0; i < 16; ++i)
-                    f[i] = fmaxf(fmaf(__uint_as_float(v[i]), sBN[g * 16 + i], sBN[64 + g * 16 + i]), 0.f);
+                    f[i] = fmaxf(fmaf(__uint_as_float(v[i]), sBN[g * 16 + i], sBN[64 + g * 16 + i]), a.relu_lo);
                 const int q16 = g * 2;
                 *reinterpret_cast<uint4 *>(rowp + ((q16 ^ sw) << 4)) =
                     make_uint4(pack_bf16(f[0], f[1]), pack_bf16(f[2], f[3]), pack_bf16(f[4], f[5]), pack_bf16(f[6], f[7]));

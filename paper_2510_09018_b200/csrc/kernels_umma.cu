@@ -375,7 +375,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
                     }
                 }
 #pragma unroll
-                for (int i = 0; i < 16; ++i) f[i] = fmaxf(f[i], 0.f);
+                for (int i = 0; i < 16; ++i) f[i] = fmaxf(f[i], a.relu_lo);
                 if (a.pool_out) {
                     // rows of one image are P consecutive lanes (P | 32): butterfly over them
 #pragma unroll

@@ -40,6 +40,8 @@ struct DevLayer {
     void *w = nullptr;                       // full-width KRSC, bf16 (BF16 mode) or fp32; stem: fp32
     float *scale[kMaxW] = {};                // folded BN per width, length c(width, cout)
     float *shift[kMaxW] = {};
+    float *gn_gamma[kMaxW] = {};             // GroupNorm mode: affine per width (scale/shift are then the identity)
+    float *gn_beta[kMaxW] = {};
     CUtensorMap tm[kMaxW][kMaxW][17];        // weight tensor map per (r_prev idx, r idx, n_tile/16)
     bool tm_ok[kMaxW][kMaxW][17] = {};
     CUtensorMap tmh[kMaxW][9][2];            // halo-kernel weight maps per (r idx, n_tile/16 - 1 (<=128), taps 3|9)
@@ -312,6 +314,7 @@ struct ConvCall {
     void *out = nullptr;
     float *pool_out = nullptr;               // fused global average pool (fp32 [B][c_out]) instead of `out`
     int epi = EPI_BN_RELU;
+    float relu_lo = 0.f;                     // -inf: no ReLU (GroupNorm mode: raw pre-norm output)
 };
 
 // Algorithmic work: 2*MACs of the sliced conv(s); bytes = input(s),
@@ -373,6 +376,7 @@ slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, i
     // fused pool: one image row per TMEM lane quarter (the 4x4 images of the last segment)
     if (cc.pool_out && (a.tile_imgs == 1 || a.row_px != 32 || a.rows != 4)) return SLIM_EUNSUPPORTED;
     a.pool_out = cc.pool_out;
+    a.relu_lo = cc.relu_lo;
     // N tile <= 128: three accumulators of it must fit the 512 TMEM columns
     // (128-channel layers: two N tiles of 64 keep two accumulator stages + the fused N=192 MMA,
     // measured faster than one tile of 128; 96 channels cannot split into 64-channel tiles)
@@ -649,6 +653,7 @@ slim_status conv_splitk_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc,
         a.shift1 = cc.Lp->shift[ri];
     }
     a.pool_out = cc.pool_out;
+    a.relu_lo = cc.relu_lo;
     if (a.pool_out && (P > 32 || 32 % P || a.tile_imgs == 1)) return SLIM_EUNSUPPORTED;
     a.stage_bytes = 16384u + static_cast<uint32_t>(nt) * 128u;
     int tc = 32;
@@ -838,6 +843,7 @@ slim_status conv_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, int ri
     a.n_out_chunks = static_cast<uint32_t>((a.n_tile + a.co_chunk - 1) / a.co_chunk);
     a.res_slots = a.n_out_chunks <= 2 ? 2 : 1;
     a.pool_out = cc.pool_out;
+    a.relu_lo = cc.relu_lo;
     if (a.pool_out && (P > 32 || 32 % P || (a.tile_imgs == 1 && P != kTileM)))
         return fail(ctx, SLIM_EUNSUPPORTED, "fused pool needs Ho*Wo dividing 32");
     // pipeline depth: two CTAs per SM for very narrow tiles, one otherwise; 2..8 stages
@@ -949,6 +955,7 @@ slim_status conv_f32(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, int ri,
     a.res = static_cast<const float *>(cc.res);
     a.out = static_cast<float *>(cc.out);
     a.epi = cc.epi;
+    a.relu_lo = cc.relu_lo;
     double flops, bytes;
     conv_work(c, cc, ri, B, a.Ho, a.Wo, &flops, &bytes);
     LaunchProf prof(ctx, st);
@@ -987,6 +994,39 @@ slim_status validate_fwd(slim_ctx *ctx, int seg, float r_prev, float r, int batc
 }
 
 // The segment schedule (O5/O6 in SURVEY §8(c)); all buffers validated by the caller.
+// GroupNorm mode (reading R16): out = act(GN(y) [+ GN_p(yp)] [+ res]) over [B, H, H, C].
+slim_status gn_apply(slim_ctx *ctx, cudaStream_t st, int seg, int layer, const DevLayer &L, const DevLayer *Lp,
+                     int ri, int B, int H, int C, const void *y, const void *yp, const void *res, void *out, bool relu) {
+    const slim_config &c = ctx->cfg;
+    GnArgs g{};
+    g.y = y;
+    g.yp = yp;
+    g.res = res;
+    g.gamma = L.gn_gamma[ri];
+    g.beta = L.gn_beta[ri];
+    if (yp) {
+        g.gamma_p = Lp->gn_gamma[ri];
+        g.beta_p = Lp->gn_beta[ri];
+    }
+    g.out = out;
+    g.B = B;
+    g.HW = H * H;
+    g.C = C;
+    g.cpg = c.gn_group_channels;
+    g.gpc = gn_groups_per_cta(B, g.HW, C, g.cpg, ctx->num_sms);
+    g.eps = c.bn_eps;
+    g.relu_lo = relu ? 0.f : -INFINITY;
+    const double eb = static_cast<double>(elem_bytes(c));
+    const double n = static_cast<double>(B) * H * H * C;
+    const double flops = 8.0 * n * (yp ? 2 : 1);   // 2 statistics passes + apply, per input tensor
+    const double bytes = eb * n * (2 + (yp ? 1 : 0) + (res ? 1 : 0)) + 8.0 * C * (yp ? 2 : 1);
+    LaunchProf prof(ctx, st);
+    const cudaError_t e = launch_gn(g, c.dtype == SLIM_FP32, st, ctx->pdl && !ctx->prof_on);
+    prof.done(SLIM_K_GN, seg, layer, c.widths[ri], c.widths[ri], B, flops, bytes);
+    if (e != cudaSuccess) return fail(ctx, SLIM_ECUDA, "gn launch: %s", cudaGetErrorString(e));
+    return SLIM_OK;
+}
+
 slim_status run_segment(slim_ctx *ctx, int seg, int ri_prev, int ri, int B, const void *in, void *out, void *ws,
                         cudaStream_t st) {
     const slim_config &c = ctx->cfg;
@@ -995,6 +1035,8 @@ slim_status run_segment(slim_ctx *ctx, int seg, int ri_prev, int ri, int B, cons
     const double eb = static_cast<double>(elem_bytes(c));
     const float r = c.widths[ri];
     const int H = seg_hw(c, seg);
+    const bool gn = c.norm == SLIM_NORM_GN;
+    const float relu_lo = gn ? -INFINITY : 0.f;   // GN: convs store the raw pre-norm output
     const int C = slim_channels(r, c.base_channels[seg]);
     const size_t buf = round256(act_bytes(c, seg, r, B));
     char *bufs[3] = {static_cast<char *>(ws), static_cast<char *>(ws) + buf, static_cast<char *>(ws) + 2 * buf};
@@ -1024,6 +1066,7 @@ slim_status run_segment(slim_ctx *ctx, int seg, int ri_prev, int ri, int B, cons
             sa.m_tiles = B * (H / sa.tile_rows);
             sa.tmem_cols = C <= 16 ? 64 : 128;   // two accumulator stages of round32(C) columns
             sa.trace = ctx->trace;
+            sa.relu_lo = relu_lo;
             if (ctx->trace) cudaMemsetAsync(ctx->trace + 3584, 0, 512 * sizeof(unsigned long long), st);
             CUtensorMap tIn, tOut;
             {   // the image as flat rows: (W*cimg, H, B), box = the tile's rows plus the 3x3 halo
@@ -1047,10 +1090,14 @@ slim_status run_segment(slim_ctx *ctx, int seg, int ri_prev, int ri, int B, cons
             LaunchProf prof(ctx, st);
             e = launch_stem_f32(static_cast<const float *>(in), static_cast<const float *>(Ls.w), Ls.sh.cin,
                                 Ls.scale[ri], Ls.shift[ri], reinterpret_cast<float *>(bufs[0]), B, H, H,
-                                c.in_channels, C, st);
+                                c.in_channels, C, st, relu_lo);
             prof.done(SLIM_K_STEM, 0, 0, r, r, B, flops, bytes);
         }
         if (e != cudaSuccess) return fail(ctx, SLIM_ECUDA, "stem launch: %s", cudaGetErrorString(e));
+        if (gn) {   // h = ReLU(GN(stem(x))), in place
+            const slim_status gs = gn_apply(ctx, st, 0, 0, Ls, nullptr, ri, B, H, C, bufs[0], nullptr, nullptr, bufs[0], true);
+            if (gs) return gs;
+        }
         cur = bufs[0];
         curH = H;
         curC = C;
@@ -1079,7 +1126,7 @@ slim_status run_segment(slim_ctx *ctx, int seg, int ri_prev, int ri, int B, cons
         c1.epi = EPI_BN_RELU;
         // the network's last conv pools in its epilogue (BF16 mode): the segment-3 output
         // never goes to memory; the head is then the FC alone
-        const bool fuse_pool = bf && seg == 3 && b == nb - 1 && H * H <= 32 && 32 % (H * H) == 0;
+        const bool fuse_pool = !gn && bf && seg == 3 && b == nb - 1 && H * H <= 32 && 32 % (H * H) == 0;
         ConvCall c2;   // out = relu(BN2(conv3x3(t)) + shortcut)
         c2.seg = seg;
         c2.layer = bi.c2;
@@ -1102,6 +1149,46 @@ slim_status run_segment(slim_ctx *ctx, int seg, int ri_prev, int ri, int B, cons
             c2.epi = EPI_BN_ADD_RELU;
             c2.res = cur;
         }
+        if (gn) {
+            // t = ReLU(GN1(conv1(x))): conv writes raw into T, GN in place.  u = conv2(t) raw into dst;
+            // the projection (raw) reuses T once conv2 has read it; then dst = ReLU(GN2(u) + shortcut).
+            c1.relu_lo = relu_lo;
+            slim_status s1 = bf ? conv_bf16(ctx, st, c1, ri, B) : conv_f32(ctx, st, c1, ri, B);
+            if (s1) return s1;
+            s1 = gn_apply(ctx, st, seg, bi.c1, S.L[bi.c1], nullptr, ri, B, H, C, T, nullptr, nullptr, T, true);
+            if (s1) return s1;
+            ConvCall u = c2;
+            u.epi = EPI_BN_RELU;
+            u.relu_lo = relu_lo;
+            u.res = nullptr;
+            u.Lp = nullptr;
+            s1 = bf ? conv_bf16(ctx, st, u, ri, B) : conv_f32(ctx, st, u, ri, B);
+            if (s1) return s1;
+            const void *yp = nullptr;
+            if (down) {
+                ConvCall p;   // 1x1 stride-2 projection, raw
+                p.seg = seg;
+                p.layer = bi.sc;
+                p.L = &S.L[bi.sc];
+                p.ri_in = ri_in;
+                p.x = cur;
+                p.H = p.W = curH;
+                p.c_in = curC;
+                p.out = T;
+                p.epi = EPI_BN_RELU;
+                p.relu_lo = relu_lo;
+                s1 = bf ? conv_bf16(ctx, st, p, ri, B) : conv_f32(ctx, st, p, ri, B);
+                if (s1) return s1;
+                yp = T;
+            }
+            s1 = gn_apply(ctx, st, seg, bi.c2, S.L[bi.c2], down ? &S.L[bi.sc] : nullptr, ri, B, H, C, dst, yp,
+                          down ? nullptr : cur, dst, true);
+            if (s1) return s1;
+            cur = dst;
+            curH = H;
+            curC = C;
+            continue;
+        }
         slim_status s1 = bf ? conv_bf16(ctx, st, c1, ri, B) : conv_f32(ctx, st, c1, ri, B);
         if (s1) return s1;
         slim_status s2 = bf ? conv_bf16(ctx, st, c2, ri, B) : conv_f32(ctx, st, c2, ri, B);
@@ -1112,7 +1199,7 @@ slim_status run_segment(slim_ctx *ctx, int seg, int ri_prev, int ri, int B, cons
     }
     if (seg == 3) {
         const double K = c.num_classes;
-        const bool pooled = bf && H * H <= 32 && 32 % (H * H) == 0;   // see fuse_pool above
+        const bool pooled = !gn && bf && H * H <= 32 && 32 % (H * H) == 0;   // see fuse_pool above
         const double flops = 2.0 * B * C * K + (pooled ? 0.0 : static_cast<double>(B) * H * H * C);
         const double bytes = (pooled ? 4.0 * B * C : eb * B * H * H * C) + 4.0 * K * (C + 1) + 4.0 * B * K;
         LaunchProf prof(ctx, st);
@@ -1179,6 +1266,8 @@ void free_segment(DevSegment &S) {
         for (int i = 0; i < kMaxW; ++i) {
             cudaFree(L.scale[i]);
             cudaFree(L.shift[i]);
+            cudaFree(L.gn_gamma[i]);
+            cudaFree(L.gn_beta[i]);
         }
         L = DevLayer{};
     }
@@ -1224,6 +1313,8 @@ void slim_default_config(slim_config *cfg) {
     cfg->max_batch = 4096;
     cfg->bn_eps = 1e-5f;
     cfg->dtype = SLIM_BF16;
+    cfg->norm = SLIM_NORM_BN;
+    cfg->gn_group_channels = 16;
 }
 
 slim_status slim_create(int device, const slim_config *cfg, slim_ctx **out) {
@@ -1240,6 +1331,13 @@ slim_status slim_create(int device, const slim_config *cfg, slim_ctx **out) {
         !(c.bn_eps > 0.f) || (c.dtype != SLIM_BF16 && c.dtype != SLIM_FP32))
         return SLIM_EINVAL;
     if (c.image_hw < 16 || c.image_hw % 8) return SLIM_EUNSUPPORTED;
+    if (c.norm != SLIM_NORM_BN && c.norm != SLIM_NORM_GN) return SLIM_EINVAL;
+    if (c.norm == SLIM_NORM_GN) {   // groups must tile every active width (reading R16) and the 16-B vectors
+        if (c.gn_group_channels < 8 || c.gn_group_channels % 8) return SLIM_EUNSUPPORTED;
+        for (int s = 0; s < 4; ++s)
+            for (int i = 0; i < c.n_widths; ++i)
+                if (slim_channels(c.widths[i], c.base_channels[s]) % c.gn_group_channels) return SLIM_EUNSUPPORTED;
+    }
     // BF16 stem/conv tiling: a 128-pixel tile is whole image rows and the stem's halo rows are 16-B multiples
     if (c.dtype == SLIM_BF16 && (c.image_hw > 32 || (c.image_hw * c.in_channels) % 8)) return SLIM_EUNSUPPORTED;
     for (int s = 0; s < 4; ++s) {
@@ -1319,7 +1417,8 @@ slim_status slim_load_segment(slim_ctx *ctx, int seg, const slim_seg_weights *w,
             return fail(ctx, SLIM_EINVAL, "load: BN set %d has %d layers, expected %d", i, bn[i].n_layers, n);
         for (int l = 0; l < n; ++l) {
             const slim_bn &b = bn[i].per_layer[l];
-            if (!b.gamma || !b.beta || !b.mean || !b.var) return fail(ctx, SLIM_EINVAL, "load: BN arrays NULL");
+            if (!b.gamma || !b.beta || (c.norm == SLIM_NORM_BN && (!b.mean || !b.var)))
+                return fail(ctx, SLIM_EINVAL, "load: BN arrays NULL");
         }
     }
     cudaSetDevice(ctx->device);
@@ -1357,12 +1456,20 @@ slim_status slim_load_segment(slim_ctx *ctx, int seg, const slim_seg_weights *w,
             CUDA_TRY(ctx, cudaMalloc(&L.w, cnt * 2));
             CUDA_TRY(ctx, cudaMemcpy(L.w, h.data(), cnt * 2, cudaMemcpyHostToDevice));
         }
-        // switchable BN, folded per width in fp64: s = gamma/sqrt(var+eps), t = beta - mean*s
+        // switchable BN, folded per width in fp64: s = gamma/sqrt(var+eps), t = beta - mean*s.
+        // GN: the conv epilogue is the identity (s = 1, t = 0); gamma/beta go to the GN kernel.
         for (int i = 0; i < c.n_widths; ++i) {
             const int ch = slim_channels(c.widths[i], L.sh.cout);
             const slim_bn &b = bn[i].per_layer[l];
-            std::vector<float> sc(ch), sh(ch);
-            for (int k = 0; k < ch; ++k) {
+            std::vector<float> sc(ch, 1.f), sh(ch, 0.f);
+            if (c.norm == SLIM_NORM_GN) {
+                std::vector<float> g(b.gamma, b.gamma + ch), be(b.beta, b.beta + ch);
+                CUDA_TRY(ctx, cudaMalloc(&L.gn_gamma[i], ch * 4));
+                CUDA_TRY(ctx, cudaMalloc(&L.gn_beta[i], ch * 4));
+                CUDA_TRY(ctx, cudaMemcpy(L.gn_gamma[i], g.data(), ch * 4, cudaMemcpyHostToDevice));
+                CUDA_TRY(ctx, cudaMemcpy(L.gn_beta[i], be.data(), ch * 4, cudaMemcpyHostToDevice));
+            }
+            for (int k = 0; k < ch && c.norm == SLIM_NORM_BN; ++k) {
                 const double s = static_cast<double>(b.gamma[k]) /
                                  std::sqrt(static_cast<double>(b.var[k]) + static_cast<double>(c.bn_eps));
                 sc[k] = static_cast<float>(s);

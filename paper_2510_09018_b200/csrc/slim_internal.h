@@ -59,6 +59,7 @@ struct ConvArgs {
     float *pool_out;          // nullptr = normal store
     int debug;                // diagnostics only (env SLIM_CONV_DEBUG): 1 = no TMA loads, 2 = no MMAs
     unsigned long long *trace;   // diagnostics only (env SLIM_CONV_TRACE): per-CTA %globaltimer stamps
+    float relu_lo;            // output = max(v, relu_lo): 0 = ReLU; -inf = raw (GroupNorm mode, pre-norm output)
 };
 
 size_t conv_umma_smem_bytes(const ConvArgs &a);
@@ -80,6 +81,7 @@ struct SplitArgs {
     uint32_t stage_bytes;     // A 16 KiB + B n_tile*128 B; the drained stages hold the DSMEM receive buffer
     int n_prod, tmem_cols;
     float *pool_out;
+    float relu_lo;            // 0 = ReLU, -inf = raw pre-norm output (GroupNorm mode)
 };
 size_t conv_splitk_smem_bytes(const SplitArgs &a);
 size_t conv_splitk_recv_bytes(const SplitArgs &a);
@@ -116,6 +118,7 @@ struct HaloArgs {
     int epi_groups;           // 2: epilogue warps 4-7 / 8-11 take even / odd tiles; 1: they split columns
     int debug;
     unsigned long long *trace;
+    float relu_lo;            // 0 = ReLU, -inf = raw pre-norm output (GroupNorm mode)
 };
 size_t conv_halo_smem_bytes(const HaloArgs &a);
 cudaError_t launch_conv_halo(const HaloArgs &a, const CUtensorMap &tmA, const CUtensorMap &tmB,
@@ -136,6 +139,7 @@ struct StemArgs {
     int B, H, W, cimg, c0;
     int tile_rows, m_tiles, tmem_cols;
     unsigned long long *trace;     // diagnostics only (SLIM_CONV_TRACE): CTA 0 role x tile %globaltimer stamps
+    float relu_lo;                 // 0 = ReLU, -inf = raw pre-norm output (GroupNorm mode)
 };
 // (kernels_stem.cu) tmIn: the image as a 3-D map (W*cimg, H, B), box (W*cimg, tile_rows+2, 1), no swizzle
 cudaError_t launch_stem_umma(const StemArgs &a, const CUtensorMap &tmIn, const CUtensorMap &tmOut, int grid,
@@ -144,7 +148,7 @@ cudaError_t launch_stem_umma(const StemArgs &a, const CUtensorMap &tmIn, const C
 // ---- CUDA-core kernels (kernels_simt.cu) ------------------------------------
 cudaError_t launch_stem_bf16(const uint16_t *in, const float *w, int cin_full, const float *scale,
                              const float *shift, uint16_t *out, int B, int H, int W, int cimg, int c0,
-                             cudaStream_t s);
+                             cudaStream_t s, float relu_lo = 0.f);
 cudaError_t launch_head_bf16(const uint16_t *in, const float *fc_w, const float *fc_b, float *logits,
                              int B, int P, int c3, int c3_full, int K, cudaStream_t s, bool pdl);
 // FC head on pooled fp32 features [B][c3] (pool fused into the last conv)
@@ -168,12 +172,27 @@ struct ConvF32Args {
     const float *scale0, *shift0, *scale1, *shift1;
     float *out; int Ho, Wo, c_out;
     int epi;
+    float relu_lo;                               // 0 = ReLU, -inf = raw pre-norm output (GroupNorm mode)
 };
 cudaError_t launch_conv_f32(const ConvF32Args &a, cudaStream_t s);
 cudaError_t launch_stem_f32(const float *in, const float *w, int cin_full, const float *scale,
                             const float *shift, float *out, int B, int H, int W, int cimg, int c0,
-                            cudaStream_t s);
+                            cudaStream_t s, float relu_lo = 0.f);
 cudaError_t launch_head_f32(const float *in, const float *fc_w, const float *fc_b, float *logits,
                             int B, int P, int c3, int c3_full, int K, cudaStream_t s, bool pdl);
+
+// ---- GroupNorm variant (kernels_gn.cu, reading R16) ---------------
+struct GnArgs {
+    const void *y;                 // raw conv output [B][HW][C] (bf16 or fp32)
+    const void *yp;                // raw projection-shortcut output (same shape) or nullptr
+    const void *res;               // identity residual (same shape) or nullptr
+    const float *gamma, *beta;     // GN affine of this width, C entries
+    const float *gamma_p, *beta_p; // the shortcut's GN affine (yp != nullptr)
+    void *out;                     // may alias y
+    int B, HW, C, cpg, gpc;        // cpg channels per group; gpc groups per CTA (divides C/cpg)
+    float eps, relu_lo;            // relu_lo 0 = ReLU, -inf = none
+};
+int gn_groups_per_cta(int B, int HW, int C, int cpg, int num_sms);
+cudaError_t launch_gn(const GnArgs &a, bool fp32, cudaStream_t s, bool pdl);
 
 }  // namespace slim

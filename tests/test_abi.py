@@ -69,3 +69,16 @@ def test_segment_bytes_scales_like_w_squared():
     b5 = slim.slim_segment_bytes(cfg, 2, 0.5, 0.5)
     assert 0.24 < b5 / b1 < 0.26
     assert slim.slim_segment_bytes(cfg, 2, 0.3, 0.5) == 0          # width outside the set
+
+
+def test_groupnorm_config_validation():
+    """GN groups must tile every active width (reading R16): rejected before any device call."""
+    lib = slim.load_library()
+    h = ctypes.c_void_p()
+    for g in (24, 4, 12):
+        cfg = slim.default_config(norm="gn", gn_group_channels=g)
+        assert lib.slim_create(0, ctypes.byref(cfg), ctypes.byref(h)) == slim.SLIM_EUNSUPPORTED
+    cfg = slim.default_config(norm=7)
+    assert lib.slim_create(0, ctypes.byref(cfg), ctypes.byref(h)) == slim.SLIM_EINVAL
+    cfg = slim.default_config()
+    assert cfg.norm == slim.SLIM_NORM_BN and cfg.gn_group_channels == 16

@@ -1,0 +1,135 @@
+"""GPU parity of the GroupNorm variant ("Group Normalization instead of Batch
+Normalization"; reading R16: 16 channels per group)
+through the C-ABI (slim_config.norm = SLIM_NORM_GN) against the fp64 oracle
+(oracle.Model(norm="gn")).  Same tolerance rule as tests/test_gpu_parity.py:
+per image max|GPU - oracle| <= tau * max|oracle|, tau 2e-2 (bf16), 1e-4 (FP32 mode).
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+import paper_2510_09018_b200 as slim
+
+pytestmark = pytest.mark.gpu
+
+TAU_BF16 = 2e-2
+TAU_FP32 = 1e-4
+W4 = synth.WIDTHS
+
+
+def _dev(a, dtype=torch.bfloat16):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).to(dtype).cuda()
+
+
+@pytest.fixture(scope="module")
+def params():
+    return synth.make_weights(), synth.make_bn()
+
+
+@pytest.fixture(scope="module")
+def net(params):
+    n = slim.SlimNet(*params, max_batch=256, norm="gn")
+    yield n
+    n.close()
+
+
+@pytest.fixture(scope="module")
+def ref(params):
+    return oracle.Model(*params, norm="gn")
+
+
+def _seg_input(seg, r_prev, B, seed):
+    if seg == 0:
+        return synth.make_images(B, offset=seed)
+    H = 32 >> (seg - 1)
+    C = synth.active_channels(r_prev, synth.BASE_CHANNELS[seg - 1])
+    g = np.random.default_rng(2000 + seed)
+    return synth.round_bf16(np.abs(g.standard_normal((B, H, H, C), dtype=np.float32)))
+
+
+def _check(got, exp, tau, what):
+    err = oracle.per_image_rel_err(got, exp)
+    assert np.isfinite(got).all(), f"{what}: non-finite output"
+    assert err.max() <= tau, f"{what}: worst per-image rel err {err.max():.3e} > {tau}"
+    return err
+
+
+@pytest.mark.parametrize("r", W4)
+def test_gn_segment0(net, ref, r):
+    x = _seg_input(0, None, 9, 0)
+    got = net.forward(0, _dev(x), r, r).float().cpu().numpy()
+    _check(got, ref.segment(0, x, None, r), TAU_BF16, f"GN seg0 r={r}")
+
+
+@pytest.mark.parametrize("seg", [1, 2, 3])
+@pytest.mark.parametrize("r_prev,r", [(0.25, 0.25), (1.0, 1.0), (0.5, 0.75), (0.75, 0.25), (0.25, 1.0)])
+def test_gn_segment(net, ref, seg, r_prev, r):
+    x = _seg_input(seg, r_prev, 9, seg)
+    got = net.forward(seg, _dev(x), r_prev, r).float().cpu().numpy()
+    _check(got, ref.segment(seg, x, r_prev, r), TAU_BF16, f"GN seg{seg} ({r_prev}->{r})")
+
+
+@pytest.mark.parametrize("tup", synth.TABLE_TUPLES)
+def test_gn_chain_table_tuples(net, ref, tup):
+    x = synth.make_images(9, offset=21)
+    got = net.forward_chain(_dev(x), tup).cpu().numpy()
+    exp = ref.chain(x, tup)
+    _check(got, exp, TAU_BF16, f"GN chain {tup}")
+    # argmax agrees wherever the oracle's top-2 margin exceeds the tolerance band
+    top2 = np.sort(exp, 1)[:, -2:]
+    band = 2 * TAU_BF16 * np.abs(exp).max(1)
+    assert ((got.argmax(1) == exp.argmax(1)) | (top2[:, 1] - top2[:, 0] < band)).all()
+
+
+@pytest.mark.parametrize("r", W4)
+def test_gn_chain_bench_batch_sampled(net, ref, r):
+    """B=128 (the bench configuration); 4 sampled images checked one by one (GN has no cross-image term)."""
+    x = synth.make_images(128, offset=5)
+    got = net.forward_chain(_dev(x), (r,) * 4).cpu().numpy()
+    idx = [0, 37, 90, 127]
+    _check(got[idx], ref.chain(x[idx], (r,) * 4), TAU_BF16, f"GN chain r={r} B=128")
+
+
+def test_gn_batch_independence_bitwise(net):
+    x = synth.make_images(130, offset=8)
+    tup = (0.5, 1.0, 0.25, 0.75)
+    full = net.forward_chain(_dev(x), tup).cpu().numpy()
+    for B in (1, 7):
+        part = net.forward_chain(_dev(x[:B]), tup).cpu().numpy()
+        np.testing.assert_array_equal(part, full[:B])
+
+
+def test_gn_differs_from_bn(params):
+    """Negative control: the GN context really normalises per group (BN context differs)."""
+    x = synth.make_images(4, offset=2)
+    with_gn = slim.SlimNet(*params, max_batch=8, norm="gn")
+    with_bn = slim.SlimNet(*params, max_batch=8)
+    a = with_gn.forward_chain(_dev(x), (1.0,) * 4).cpu().numpy()
+    b = with_bn.forward_chain(_dev(x), (1.0,) * 4).cpu().numpy()
+    with_gn.close()
+    with_bn.close()
+    assert np.abs(a - b).max() > 1e-2
+
+
+@pytest.mark.parametrize("tup", [(1.0, 0.75, 0.5, 0.25), (0.25, 0.5, 0.75, 1.0)])
+def test_gn_fp32_mode(params, tup):
+    net32 = slim.SlimNet(*params, max_batch=16, norm="gn", dtype="fp32")
+    x = synth.make_images(5, offset=13)
+    got = net32.forward_chain(_dev(x, torch.float32), tup).cpu().numpy()
+    net32.close()
+    _check(got, oracle.Model(*params, norm="gn").chain(x, tup), TAU_FP32, f"GN fp32 chain {tup}")
+
+
+def test_gn_graph_replay_equals_eager(params):
+    x = _dev(synth.make_images(16, offset=4))
+    tup = (0.75, 0.25, 1.0, 0.5)
+    n = slim.SlimNet(*params, max_batch=16, norm="gn")
+    eager = n.forward_chain(x, tup).clone()
+    slim.slim_set_graph_mode(n.ctx, True)
+    g1 = n.forward_chain(x, tup).clone()
+    g2 = n.forward_chain(x, tup).clone()
+    n.close()
+    torch.testing.assert_close(g1, eager, rtol=0, atol=0)
+    torch.testing.assert_close(g2, eager, rtol=0, atol=0)

@@ -16,7 +16,7 @@ import paper_2510_09018_b200 as slim  # noqa: E402
 B = int(sys.argv[1]) if len(sys.argv) > 1 else 128
 N = int(sys.argv[2]) if len(sys.argv) > 2 else 200
 graph = os.environ.get("GRAPH", "1") == "1"
-net = slim.SlimNet(synth.make_weights(), synth.make_bn(), max_batch=B)
+net = slim.SlimNet(synth.make_weights(), synth.make_bn(), max_batch=B, norm=sys.argv[3] if len(sys.argv) > 3 else "bn")
 slim.slim_set_graph_mode(net.ctx, graph)
 x = torch.from_numpy(synth.make_images(B)).to(torch.bfloat16).cuda()
 st = torch.cuda.current_stream()
