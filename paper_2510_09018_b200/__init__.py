@@ -445,16 +445,27 @@ class SlimNet:
         self.cfg = default_config(**cfg_kw)
         self.ctx = slim_create(device, self.cfg)
         self.widths = tuple(self.cfg.widths[i] for i in range(self.cfg.n_widths))
-        blocks = tuple(self.cfg.blocks_per_seg)
+        self._host = (weights, bn)   # host copy: Alg. 1's offloaded segments reload from here
         for s in segments:
-            names = manifest(s, blocks)
-            conv = [weights[n] for n in names]
-            bn_sets = [[bn[n][wi] for n in names] for wi in range(self.cfg.n_widths)]
-            if s == 3:
-                slim_load_segment(self.ctx, s, conv, bn_sets, weights["fc_w"], weights["fc_b"])
-            else:
-                slim_load_segment(self.ctx, s, conv, bn_sets)
+            self.load_segment(s)
         self._ws = {}
+
+    def load_segment(self, s: int):
+        """(Re)load segment s from the host copy (slim_load_segment copies to the device)."""
+        weights, bn = self._host
+        names = manifest(s, tuple(self.cfg.blocks_per_seg))
+        conv = [weights[n] for n in names]
+        bn_sets = [[bn[n][wi] for n in names] for wi in range(self.cfg.n_widths)]
+        if s == 3:
+            slim_load_segment(self.ctx, s, conv, bn_sets, weights["fc_w"], weights["fc_b"])
+        else:
+            slim_load_segment(self.ctx, s, conv, bn_sets)
+
+    def unload_segment(self, s: int):
+        slim_unload_segment(self.ctx, s)
+
+    def segment_loaded(self, s: int) -> bool:
+        return bool(load_library().slim_segment_loaded(self.ctx, s))
 
     @property
     def act_dtype(self):
