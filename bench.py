@@ -360,14 +360,29 @@ def run_stream(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     slim_build.build()
-    net = slim.SlimNet(synth.make_weights(), synth.make_bn(), device=local, max_batch=args.bmax)
-    slim.slim_set_graph_mode(net.ctx, True)
+    net = slim.SlimNet(synth.make_weights(), synth.make_bn(), device=local, max_batch=args.bmax, norm=args.norm)
+    greedy = args.executor == "greedy"
+    slim.slim_set_graph_mode(net.ctx, True)   # Alg. 1: one graph per (key, batch size, instance buffers), reused across steps
     n_total = args.requests * world
     devs, tups, grps = router.route(n_total, world, args.policy)
     mine = router.shard(devs, rank)
     tuples = np.asarray([router.TABLE_TUPLES[t] for t in tups[mine]], np.float32)
     x = torch.from_numpy(synth.make_images(len(mine), offset=200 + rank)).to(torch.bfloat16).to(dev)
-    ex = StreamExecutor(net, n_max=len(mine), B_max=args.bmax, device=dev)
+    if greedy:   # Alg. 1: native scheduler decisions, instances on their own CUDA streams
+        from paper_2510_09018_b200.executor import GreedyExecutor
+        gx = GreedyExecutor(net, n_max=len(mine), B_max=args.bmax, Q_th=args.q_th, N_new=args.n_new)
+
+        class _Adapter:
+            last_batches = [[]]
+
+            def run(self, x, tuples, stream=None):
+                gx.stats["batch_sizes"] = []
+                out = gx.run(x, tuples)
+                self.last_batches = [gx.stats["batch_sizes"]]
+                return out
+        ex = _Adapter()
+    else:
+        ex = StreamExecutor(net, n_max=len(mine), B_max=args.bmax, device=dev)
     telem = TelemetryExchange(device=dev) if world > 1 else None
     stream = torch.cuda.current_stream(dev)
     for _ in range(args.warmup):
@@ -406,7 +421,8 @@ def run_stream(args):
             "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": f"{'CFG5' if world > 1 else 'CFG4'}: mixed-width request stream "
                                    f"(width tuples of Tables I-II), greedy (segment, w_req, w_prev) batching, "
-                                   f"B_max={args.bmax}, routing={args.policy}",
+                                   f"B_max={args.bmax}, routing={args.policy}, executor={args.executor}"
+                                   + (f" (Alg. 1: Q_th={args.q_th}, N_new={args.n_new})" if greedy else ""),
                        "requests_per_rank": args.requests, "parallelism": f"dp{world} routed"},
             "batches_per_step_rank0": len(batches), "mean_batch_rank0": float(np.mean(batches)),
             "gpu_launches": slim.slim_launch_count(net.ctx) - l0, "energy_j_per_image": energy, "clocks": clocks,
@@ -515,6 +531,11 @@ def main(argv=None):
     ap.add_argument("--requests", type=int, default=1024, help="stream: requests per rank per step")
     ap.add_argument("--bmax", type=int, default=256, help="stream: B_max of the key batching")
     ap.add_argument("--policy", default="random", help="stream: routing policy (random | slim | table_rr)")
+    ap.add_argument("--executor", choices=("stream", "greedy"), default="stream",
+                    help="stream: whole-stream packing per segment (graph replay); greedy: Alg. 1 executor "
+                         "(native scheduler, per-instance streams)")
+    ap.add_argument("--q-th", type=int, default=512, help="greedy: Alg. 1 scale trigger Q_th")
+    ap.add_argument("--n-new", type=int, default=2, help="greedy: Alg. 1 scale cap N_new")
     ap.add_argument("--norm", choices=("bn", "gn"), default="bn",
                     help="bn = switchable BatchNorm (north_star, default); gn = GroupNorm variant (P:148, NEXT-1)")
     args = ap.parse_args(argv)

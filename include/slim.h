@@ -79,7 +79,8 @@ typedef enum { SLIM_NORM_BN = 0, SLIM_NORM_GN = 1 } slim_norm;
 /* Network configuration (reading D1 = CIFAR ResNet-18). */
 typedef struct {
     int n_widths;              /* |W|, 1..8 */
-    float widths[8];           /* sorted ascending, each in (0,1]; default {0.25,0.5,0.75,1.0} */
+    float widths[8];           /* sorted ascending, each in (0,1]; default {0.25,0.5,0.75,1.0};
+                                  any values (universal widths, see slim_act_channels) */
     int blocks_per_seg[4];     /* BasicBlocks per segment, default {2,2,2,2} (1..4 each) */
     int base_channels[4];      /* full-width channels C_s, default {64,128,256,512} */
     int in_channels;           /* image channels, 3 (never sliced) */
@@ -306,6 +307,12 @@ SLIM_API uint64_t slim_launch_count(const slim_ctx *ctx);
 /* Number of SMs of the context's device and the active-channel rule c(r, C). */
 SLIM_API int slim_num_sms(const slim_ctx *ctx);
 SLIM_API int slim_channels(float r, int C);
+/* Universal widths ("universally slimmable"): any width in (0, 1]
+ * may be configured.  Activations of width r carry c_act(r, C) = slim_act_channels(r, C)
+ * channels per pixel: c(r, C) rounded up to a multiple of 16, and above 128 to a multiple of
+ * 64 (the kernels' tile granules).  Channels c .. c_act-1 are exact zeros on output and are
+ * ignored (multiply zero) on input.  For the paper's width set c_act == c. */
+SLIM_API int slim_act_channels(float r, int C);
 
 #ifdef __cplusplus
 }

@@ -20,7 +20,8 @@ __all__ = [
     "SlimError", "load_library", "slim_config", "default_config", "slim_create", "slim_destroy",
     "slim_load_segment", "slim_unload_segment", "slim_segment_bytes", "slim_forward", "slim_forward_ws",
     "slim_forward_workspace_bytes", "slim_chain_workspace_bytes", "slim_forward_chain", "slim_pack",
-    "slim_launch", "slim_gather", "slim_scatter", "slim_last_error", "slim_launch_count", "slim_channels", "SlimNet",
+    "slim_launch", "slim_gather", "slim_scatter", "slim_last_error", "slim_launch_count", "slim_channels",
+    "slim_act_channels", "SlimNet",
     "manifest", "LIB_PATH", "Scheduler",
 ]
 
@@ -138,6 +139,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "slim_launch_count": (ctypes.c_uint64, [_VP]),
         "slim_num_sms": (_I, [_VP]),
         "slim_channels": (_I, [_F, _I]),
+        "slim_act_channels": (_I, [_F, _I]),
         "slim_set_graph_mode": (_I, [_VP, _I]),
         "slim_profile_begin": (_I, [_VP, _I]),
         "slim_profile_end": (_I, [_VP, ctypes.POINTER(slim_profile_record), _I, ctypes.POINTER(_I)]),
@@ -165,7 +167,7 @@ EXPORTED = ("slim_create", "slim_destroy", "slim_default_config", "slim_load_seg
             "slim_segment_loaded", "slim_segment_bytes", "slim_forward", "slim_forward_workspace_bytes",
             "slim_forward_ws", "slim_chain_workspace_bytes", "slim_forward_chain", "slim_pack", "slim_launch",
             "slim_gather", "slim_scatter", "slim_last_error", "slim_last_error_msg", "slim_status_str", "slim_version",
-            "slim_launch_count", "slim_num_sms", "slim_channels", "slim_set_graph_mode", "slim_profile_begin",
+            "slim_launch_count", "slim_num_sms", "slim_channels", "slim_act_channels", "slim_set_graph_mode", "slim_profile_begin",
             "slim_profile_end", "slim_sched_default_knobs", "slim_sched_create", "slim_sched_destroy",
             "slim_sched_enqueue", "slim_sched_next", "slim_sched_complete", "slim_sched_unload_idle",
             "slim_sched_queue_len", "slim_sched_instances")
@@ -346,6 +348,11 @@ def slim_channels(r: float, C: int) -> int:
     return load_library().slim_channels(r, C)
 
 
+def slim_act_channels(r: float, C: int) -> int:
+    """Channels an activation of width r carries (c(r, C) padded to the kernel granule; extra ones are 0)."""
+    return load_library().slim_act_channels(r, C)
+
+
 def slim_set_graph_mode(ctx, enable: bool):
     _check(ctx, load_library().slim_set_graph_mode(ctx, int(bool(enable))))
 
@@ -499,7 +506,7 @@ class SlimNet:
         if seg == 3:
             return (B, self.cfg.num_classes)
         H = self.cfg.image_hw >> seg
-        return (B, H, H, slim_channels(r, self.cfg.base_channels[seg]))
+        return (B, H, H, slim_act_channels(r, self.cfg.base_channels[seg]))
 
     def forward(self, seg, x, r_prev, r, out=None, stream=None):
         import torch

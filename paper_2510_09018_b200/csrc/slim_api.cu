@@ -96,6 +96,18 @@ extern "C" int slim_channels(float r, int C) {
     return static_cast<int>(std::ceil(static_cast<double>(r) * C - 1e-9));
 }
 
+// Universal widths ("universally slimmable"): activations and kernels
+// use c_act(r, C) >= c(r, C) channels -- c rounded up to a multiple of 16 (the UMMA N / K-block
+// granule) and, above 128, to a multiple of 64 (the N tiles of the conv kernels) -- and channels
+// c .. c_act-1 are EXACT zeros: their folded BN scale/shift (GN: identity scale, gamma, beta) are
+// zero, so conv outputs there are 0*acc + 0, and as inputs they multiply weights by zero.  For the
+// paper's width set every c is already such a value (c_act == c).
+extern "C" int slim_act_channels(float r, int C) {
+    const int c = slim_channels(r, C);
+    const int p16 = (c + 15) / 16 * 16;
+    return p16 <= 128 ? p16 : (c + 63) / 64 * 64;
+}
+
 namespace {
 
 slim_status fail(slim_ctx *ctx, slim_status s, const char *fmt, ...) __attribute__((format(printf, 3, 4)));
@@ -151,7 +163,7 @@ BlockIdx block_layers(const slim_config &c, int s, int b) {
 
 size_t act_bytes(const slim_config &c, int s, float r, int B) {
     const int H = seg_hw(c, s);
-    return static_cast<size_t>(B) * H * H * slim_channels(r, c.base_channels[s]) * elem_bytes(c);
+    return static_cast<size_t>(B) * H * H * slim_act_channels(r, c.base_channels[s]) * elem_bytes(c);
 }
 size_t seg_ws_bytes(const slim_config &c, int s, float r, int B) { return 3 * round256(act_bytes(c, s, r, B)); }
 
@@ -354,7 +366,7 @@ slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, i
     const int H = s2 ? cc.H / 2 : cc.H, W = s2 ? cc.W / 2 : cc.W;   // output size
     static const bool no_small = getenv("SLIM_HALO_NO_SMALL") != nullptr;   // A/B: small images via per-tap conv
     if (W > 32 || 32 % W) return SLIM_EUNSUPPORTED;
-    const int c_out = slim_channels(c.widths[ri], L.sh.cout);
+    const int c_out = slim_act_channels(c.widths[ri], L.sh.cout);
     HaloArgs a{};
     a.B = B;
     a.H = H;
@@ -604,7 +616,7 @@ slim_status conv_splitk_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc,
     if (disabled) return SLIM_EUNSUPPORTED;
     const int k = L.sh.k, s = L.sh.stride, pad = k / 2;
     const int Ho = (cc.H + 2 * pad - k) / s + 1, Wo = (cc.W + 2 * pad - k) / s + 1;
-    const int c_out = slim_channels(c.widths[ri], L.sh.cout);
+    const int c_out = slim_act_channels(c.widths[ri], L.sh.cout);
     const int P = Ho * Wo;
     SplitArgs a{};
     a.B = B;
@@ -770,7 +782,7 @@ slim_status conv_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, int ri
     DevLayer &L = *cc.L;
     const int k = L.sh.k, s = L.sh.stride, pad = k / 2;
     const int Ho = (cc.H + 2 * pad - k) / s + 1, Wo = (cc.W + 2 * pad - k) / s + 1;
-    const int c_out = slim_channels(c.widths[ri], L.sh.cout);
+    const int c_out = slim_act_channels(c.widths[ri], L.sh.cout);
     ConvArgs a{};
     a.B = B;
     a.Ho = Ho;
@@ -938,7 +950,7 @@ slim_status conv_f32(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, int ri,
     a.pad = pad;
     a.Ho = (cc.H + 2 * pad - k) / s + 1;
     a.Wo = (cc.W + 2 * pad - k) / s + 1;
-    a.c_out = slim_channels(c.widths[ri], L.sh.cout);
+    a.c_out = slim_act_channels(c.widths[ri], L.sh.cout);
     a.scale0 = L.scale[ri];
     a.shift0 = L.shift[ri];
     if (cc.epi == EPI_BN_PROJ_RELU) {
@@ -1037,12 +1049,12 @@ slim_status run_segment(slim_ctx *ctx, int seg, int ri_prev, int ri, int B, cons
     const int H = seg_hw(c, seg);
     const bool gn = c.norm == SLIM_NORM_GN;
     const float relu_lo = gn ? -INFINITY : 0.f;   // GN: convs store the raw pre-norm output
-    const int C = slim_channels(r, c.base_channels[seg]);
+    const int C = slim_act_channels(r, c.base_channels[seg]);
     const size_t buf = round256(act_bytes(c, seg, r, B));
     char *bufs[3] = {static_cast<char *>(ws), static_cast<char *>(ws) + buf, static_cast<char *>(ws) + 2 * buf};
     const void *cur = in;
     int curH = (seg == 0) ? H : (H * 2);
-    int curC = (seg == 0) ? c.in_channels : slim_channels(c.widths[ri_prev], c.base_channels[seg - 1]);
+    int curC = (seg == 0) ? c.in_channels : slim_act_channels(c.widths[ri_prev], c.base_channels[seg - 1]);
     if (seg == 0) {
         DevLayer &Ls = S.L[0];
         const double pix = static_cast<double>(B) * H * H;
@@ -1343,10 +1355,10 @@ slim_status slim_create(int device, const slim_config *cfg, slim_ctx **out) {
     for (int s = 0; s < 4; ++s) {
         if (c.blocks_per_seg[s] < 1 || c.blocks_per_seg[s] > 4) return SLIM_EINVAL;
         if (c.base_channels[s] < 16 || c.base_channels[s] > 1024) return SLIM_EINVAL;
-        for (int i = 0; i < c.n_widths; ++i) {   // kernels need channel prefixes in multiples of 16
-            const int ch = slim_channels(c.widths[i], c.base_channels[s]);
-            if (ch % 16) return SLIM_EUNSUPPORTED;
-            if (s == 0 && ch > 64) return SLIM_EUNSUPPORTED;   // stem kernel holds <= 64 output channels
+        for (int i = 0; i < c.n_widths; ++i) {   // kernel channel counts (padded, see slim_act_channels)
+            const int ch = slim_act_channels(c.widths[i], c.base_channels[s]);
+            if (ch > c.base_channels[s]) return SLIM_EUNSUPPORTED;   // the padding must stay inside the weights
+            if (s == 0 && ch > 64) return SLIM_EUNSUPPORTED;         // stem kernel holds <= 64 output channels
         }
     }
     slim_ctx *ctx = new slim_ctx();
@@ -1458,16 +1470,21 @@ slim_status slim_load_segment(slim_ctx *ctx, int seg, const slim_seg_weights *w,
         }
         // switchable BN, folded per width in fp64: s = gamma/sqrt(var+eps), t = beta - mean*s.
         // GN: the conv epilogue is the identity (s = 1, t = 0); gamma/beta go to the GN kernel.
+        // Channels ch .. cp-1 (universal-width padding) get scale = shift = 0 (GN: gamma = beta = 0).
         for (int i = 0; i < c.n_widths; ++i) {
             const int ch = slim_channels(c.widths[i], L.sh.cout);
+            const int cp = slim_act_channels(c.widths[i], L.sh.cout);
             const slim_bn &b = bn[i].per_layer[l];
-            std::vector<float> sc(ch, 1.f), sh(ch, 0.f);
+            std::vector<float> sc(cp, 0.f), sh(cp, 0.f);
+            for (int k = 0; k < ch; ++k) sc[k] = 1.f;
             if (c.norm == SLIM_NORM_GN) {
-                std::vector<float> g(b.gamma, b.gamma + ch), be(b.beta, b.beta + ch);
-                CUDA_TRY(ctx, cudaMalloc(&L.gn_gamma[i], ch * 4));
-                CUDA_TRY(ctx, cudaMalloc(&L.gn_beta[i], ch * 4));
-                CUDA_TRY(ctx, cudaMemcpy(L.gn_gamma[i], g.data(), ch * 4, cudaMemcpyHostToDevice));
-                CUDA_TRY(ctx, cudaMemcpy(L.gn_beta[i], be.data(), ch * 4, cudaMemcpyHostToDevice));
+                std::vector<float> g(cp, 0.f), be(cp, 0.f);
+                std::copy(b.gamma, b.gamma + ch, g.begin());
+                std::copy(b.beta, b.beta + ch, be.begin());
+                CUDA_TRY(ctx, cudaMalloc(&L.gn_gamma[i], cp * 4));
+                CUDA_TRY(ctx, cudaMalloc(&L.gn_beta[i], cp * 4));
+                CUDA_TRY(ctx, cudaMemcpy(L.gn_gamma[i], g.data(), cp * 4, cudaMemcpyHostToDevice));
+                CUDA_TRY(ctx, cudaMemcpy(L.gn_beta[i], be.data(), cp * 4, cudaMemcpyHostToDevice));
             }
             for (int k = 0; k < ch && c.norm == SLIM_NORM_BN; ++k) {
                 const double s = static_cast<double>(b.gamma[k]) /
@@ -1475,10 +1492,10 @@ slim_status slim_load_segment(slim_ctx *ctx, int seg, const slim_seg_weights *w,
                 sc[k] = static_cast<float>(s);
                 sh[k] = static_cast<float>(static_cast<double>(b.beta[k]) - static_cast<double>(b.mean[k]) * s);
             }
-            CUDA_TRY(ctx, cudaMalloc(&L.scale[i], ch * 4));
-            CUDA_TRY(ctx, cudaMalloc(&L.shift[i], ch * 4));
-            CUDA_TRY(ctx, cudaMemcpy(L.scale[i], sc.data(), ch * 4, cudaMemcpyHostToDevice));
-            CUDA_TRY(ctx, cudaMemcpy(L.shift[i], sh.data(), ch * 4, cudaMemcpyHostToDevice));
+            CUDA_TRY(ctx, cudaMalloc(&L.scale[i], cp * 4));
+            CUDA_TRY(ctx, cudaMalloc(&L.shift[i], cp * 4));
+            CUDA_TRY(ctx, cudaMemcpy(L.scale[i], sc.data(), cp * 4, cudaMemcpyHostToDevice));
+            CUDA_TRY(ctx, cudaMemcpy(L.shift[i], sh.data(), cp * 4, cudaMemcpyHostToDevice));
         }
     }
     if (seg == 3) {
@@ -1662,7 +1679,7 @@ slim_status slim_launch(slim_ctx *ctx, const slim_launch_desc *d, const uint32_t
     if (s) return s;
     const slim_config &c = ctx->cfg;
     const int Hin = d->seg == 0 ? c.image_hw : seg_hw(c, d->seg - 1);
-    const int Cin = d->seg == 0 ? c.in_channels : slim_channels(d->r_prev, c.base_channels[d->seg - 1]);
+    const int Cin = d->seg == 0 ? c.in_channels : slim_act_channels(d->r_prev, c.base_channels[d->seg - 1]);
     const size_t row = static_cast<size_t>(Hin) * Hin * Cin * elem_bytes(c);
     const void *in = pool;
     if (slots) {

@@ -24,7 +24,7 @@ import time
 import numpy as np
 import torch
 
-from . import Scheduler, SlimNet, slim_channels, slim_forward_workspace_bytes, slim_launch, slim_scatter
+from . import Scheduler, SlimNet, slim_act_channels, slim_forward_workspace_bytes, slim_launch, slim_scatter
 
 
 class _Instance:
@@ -56,7 +56,7 @@ class GreedyExecutor:
         self.row_elems = [hw * hw * cfg.in_channels]
         for s in range(1, 4):
             h = hw >> (s - 1)
-            self.row_elems.append(h * h * slim_channels(wmax, cfg.base_channels[s - 1]))
+            self.row_elems.append(h * h * slim_act_channels(wmax, cfg.base_channels[s - 1]))
         self.out_elems = max(max(self.row_elems[1:]), cfg.num_classes * 4 // self.eb)
         self.wsb = max(slim_forward_workspace_bytes(net.ctx, s, wmax, wmax, B_max) for s in range(4))
         self.pools = [None] + [torch.empty(n_max * self.row_elems[s], dtype=self.adt, device=self.dev)
@@ -85,7 +85,7 @@ class GreedyExecutor:
             slim_launch(ctx, d, I.slots_d, pool, self.row_elems[s] * self.eb, I.slab, I.out, I.ws, self.wsb, st)
             if s < 3:
                 h = hw >> s
-                row = h * h * slim_channels(act["w_req"], cfg.base_channels[s]) * self.eb
+                row = h * h * slim_act_channels(act["w_req"], cfg.base_channels[s]) * self.eb
                 slim_scatter(ctx, I.out, I.slots_d, b, row, self.pools[s + 1], self.row_elems[s + 1] * self.eb, st)
             else:
                 slim_scatter(ctx, I.out, I.slots_d, b, cfg.num_classes * 4, self.logits, cfg.num_classes * 4, st)

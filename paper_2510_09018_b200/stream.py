@@ -21,7 +21,7 @@ from __future__ import annotations
 import numpy as np
 import torch
 
-from . import SlimNet, slim_channels, slim_forward_workspace_bytes, slim_launch, slim_pack, slim_scatter
+from . import SlimNet, slim_act_channels, slim_forward_workspace_bytes, slim_launch, slim_pack, slim_scatter
 
 
 class StreamExecutor:
@@ -40,7 +40,7 @@ class StreamExecutor:
         self.row_elems = [hw * hw * cfg.in_channels]
         for s in range(1, 4):
             h = hw >> (s - 1)
-            self.row_elems.append(h * h * slim_channels(wmax, cfg.base_channels[s - 1]))
+            self.row_elems.append(h * h * slim_act_channels(wmax, cfg.base_channels[s - 1]))
         self.pools = [None] + [torch.empty(n_max * self.row_elems[s], dtype=self.adt, device=self.dev)
                                for s in range(1, 4)]
         self.logits = torch.empty(n_max, cfg.num_classes, dtype=torch.float32, device=self.dev)
@@ -90,7 +90,7 @@ class StreamExecutor:
                 slim_launch(self.net.ctx, d, idx, pool, pool_row, self.slab, self.out, self.ws, self.wsb, st)
                 if s < 3:
                     h = hw >> s
-                    row = h * h * slim_channels(d["r"], cfg.base_channels[s]) * self.eb
+                    row = h * h * slim_act_channels(d["r"], cfg.base_channels[s]) * self.eb
                     slim_scatter(self.net.ctx, self.out, idx, b, row, self.pools[s + 1],
                                  self.row_elems[s + 1] * self.eb, st)
                 else:
