@@ -425,6 +425,81 @@ def run_stream(args):
                                    + (f" (Alg. 1: Q_th={args.q_th}, N_new={args.n_new})" if greedy else ""),
                        "requests_per_rank": args.requests, "parallelism": f"dp{world} routed"},
             "batches_per_step_rank0": len(batches), "mean_batch_rank0": float(np.mean(batches)),
+            **({"alg1_host_s_per_step": {k: gx.stats[k] / (args.steps + args.warmup)
+                                         for k in ("t_next", "t_launch", "t_wait")},
+                "alg1_instances": len(gx.sched.instances())} if greedy else {}),
+            "gpu_launches": slim.slim_launch_count(net.ctx) - l0, "energy_j_per_image": energy, "clocks": clocks,
+        }))
+    net.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def run_handoff(args):
+    """NEXT-2: the mixed-width stream with per-SEGMENT routing (handoff.plan_segments): every
+    rank runs the segments routed to it and hands activations to the next segment's rank with
+    one all_to_all_single per segment boundary (NCCL over NVLink).  N=1: no exchange."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import synth
+    import paper_2510_09018_b200 as slim
+    from paper_2510_09018_b200 import build as slim_build
+    from paper_2510_09018_b200 import handoff, router
+    from paper_2510_09018_b200.telemetry import NvmlSampler
+
+    world, rank, local = _dist()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    slim_build.build()
+    net = slim.SlimNet(synth.make_weights(), synth.make_bn(), device=local, max_batch=args.bmax, norm=args.norm)
+    slim.slim_set_graph_mode(net.ctx, True)
+    n = args.requests * world                      # weak scaling: requests per rank fixed
+    g = np.random.Generator(np.random.PCG64([2510_09018, 5]))
+    tuples = np.asarray(router.TABLE_TUPLES, np.float32)[g.integers(0, len(router.TABLE_TUPLES), n)]
+    plan = handoff.plan_segments(n, world, args.seg_policy)
+    x = torch.from_numpy(synth.make_images(n, offset=300)).to(torch.bfloat16).to(dev)
+    ex = handoff.HandoffExecutor(net, n, rank, world, B_max=args.bmax)
+    for _ in range(args.warmup):
+        ex.run(x, tuples, plan)
+    torch.cuda.synchronize()
+    sampler = NvmlSampler(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    l0 = slim.slim_launch_count(net.ctx)
+    e0 = sampler.energy_mj()
+    sampler.start()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(args.steps):
+        ex.run(x, tuples, plan)
+    b.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    sampler.stop()
+    e1 = sampler.energy_mj()
+    t = torch.tensor([a.elapsed_time(b)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    value = n * args.steps / (float(t.item()) / 1e3)
+    clocks, energy = _clock_energy_json(sampler, e0, e1, args.requests * args.steps)
+    moved = int((plan[:, 1:] != plan[:, :-1]).sum())
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": float(t.item()) / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": f"NEXT-2: mixed-width request stream routed per segment ({args.seg_policy}), "
+                                   f"activation hand-off by all_to_all_single between segments, B_max={args.bmax}",
+                       "requests_per_rank": args.requests, "parallelism": f"dp{world} segment-routed"},
+            "handoffs_per_step": moved, "handoff_bytes_per_step": int(sum(
+                ex.row_elems[s + 1] * ex.eb * int((plan[:, s] != plan[:, s + 1]).sum()) for s in range(3))),
             "gpu_launches": slim.slim_launch_count(net.ctx) - l0, "energy_j_per_image": energy, "clocks": clocks,
         }))
     net.close()
@@ -525,12 +600,13 @@ def main(argv=None):
     ap.add_argument("--profile-steps", type=int, default=50)
     ap.add_argument("--e2e-steps", type=int, default=200)
     ap.add_argument("--json-out", default=None)
-    ap.add_argument("--workload", choices=("cfg2", "cfg1", "sweep", "stream"), default="cfg2",
+    ap.add_argument("--workload", choices=("cfg2", "cfg1", "sweep", "stream", "handoff"), default="cfg2",
                     help="cfg2 (default, BASELINE configs[1]); cfg1 = seg0 r=0.25 B=8; sweep = CFG3 batch sweep "
                          "(one JSON line per point); stream = CFG4/CFG5 mixed-width routed request stream")
     ap.add_argument("--requests", type=int, default=1024, help="stream: requests per rank per step")
     ap.add_argument("--bmax", type=int, default=256, help="stream: B_max of the key batching")
     ap.add_argument("--policy", default="random", help="stream: routing policy (random | slim | table_rr)")
+    ap.add_argument("--seg-policy", default="random", help="handoff: per-segment routing (random | pipeline | sticky)")
     ap.add_argument("--executor", choices=("stream", "greedy"), default="stream",
                     help="stream: whole-stream packing per segment (graph replay); greedy: Alg. 1 executor "
                          "(native scheduler, per-instance streams)")
@@ -544,6 +620,8 @@ def main(argv=None):
         return run_reference(args)
     if args.workload == "stream":
         return run_stream(args)
+    if args.workload == "handoff":
+        return run_handoff(args)
     if args.workload in ("cfg1", "sweep"):
         return run_points(args)
     return run_ours(args)

@@ -63,7 +63,8 @@ class GreedyExecutor:
                                for s in range(1, 4)]
         self.logits = torch.empty(n_max, cfg.num_classes, dtype=torch.float32, device=self.dev)
         self.inst = {}            # instance id -> _Instance (buffers + stream)
-        self.stats = dict(batches=0, loads=0, requeues=0, unloaded=0, seg_reloads=0, batch_sizes=[])
+        self.stats = dict(batches=0, loads=0, requeues=0, unloaded=0, seg_reloads=0, batch_sizes=[], t_next=0.0,
+                          t_launch=0.0, t_wait=0.0)
 
     # --------------------------------------------------------------- RUNBATCH
     def _run(self, act, images, tuples):
@@ -96,14 +97,11 @@ class GreedyExecutor:
 
     def _reap(self, now, tuples, block: bool) -> int:
         """Release instances whose batch finished; re-enqueue their requests for the next segment."""
-        done = []
-        for iid in list(self.pending):
-            if self.inst[iid].event.query():
-                done.append(iid)
-        if not done and block and self.pending:
-            iid = next(iter(self.pending))          # oldest batch
-            self.inst[iid].event.synchronize()
-            done.append(iid)
+        t0 = time.perf_counter()
+        done = [iid for iid in self.pending if self.inst[iid].event.query()]
+        while not done and block and self.pending:   # wait for whichever batch finishes first
+            done = [iid for iid in self.pending if self.inst[iid].event.query()]
+        self.stats["t_wait"] += time.perf_counter() - t0
         finished = 0
         for iid in done:
             s, ids = self.pending.pop(iid)
@@ -154,9 +152,12 @@ class GreedyExecutor:
         while finished < n:
             now = clock()
             act = self.sched.next(now, self.util_fn(), self.vram_fn())
+            self.stats["t_next"] += clock() - now
             self.stats["loads"] += act["n_loaded"]
             if act["kind"] == "run":
+                t1 = clock()
                 self._run(act, images, tuples)
+                self.stats["t_launch"] += clock() - t1
                 finished += self._reap(clock(), tuples, block=False)
                 continue
             if act["kind"] == "requeue":
