@@ -58,26 +58,27 @@ def _cores():
 
 
 # ------------------------------------------------------------------ CPU oracle legs
-def oracle_throughput(target_s: float = 15.0, batch_per_width: int | None = None, norm: str = "bn"):
+def oracle_throughput(target_s: float = 15.0, batch_per_width: int | None = None, norm: str = "bn",
+                      widths=WIDTHS):
     """The fp64 oracle as it stands on this host's cores: images/s on a bounded sample of CFG2
     (equal images per width, like the GPU step)."""
     import oracle
     import synth
-    m = oracle.Model(synth.make_weights(), synth.make_bn(), norm=norm)
+    m = oracle.Model(synth.make_weights(), synth.make_bn(widths=widths), norm=norm, widths=widths)
     x = synth.make_images(128, offset=1)
     if batch_per_width is None:   # size the sample to ~target_s of CPU work
         t0 = time.perf_counter()
-        for r in WIDTHS:
+        for r in widths:
             m.chain(x[:1], (r,) * 4)
         t1 = time.perf_counter() - t0
         batch_per_width = max(1, min(128, int(target_s / max(t1, 1e-3))))
     t0 = time.perf_counter()
-    for r in WIDTHS:
+    for r in widths:
         m.chain(x[:batch_per_width], (r,) * 4)
     dt = time.perf_counter() - t0
-    n = batch_per_width * len(WIDTHS)
+    n = batch_per_width * len(widths)
     return dict(value=n / dt, unit="images/s", cores=_cores(), kind="oracle",
-                sample=f"{batch_per_width} images x {len(WIDTHS)} widths of the CFG2 chain (fp64 C oracle, "
+                sample=f"{batch_per_width} images x {len(widths)} widths of the CFG2 chain (fp64 C oracle, "
                        f"OpenMP over rows), {dt:.1f} s")
 
 
@@ -133,8 +134,9 @@ def run_ours(args):
     slim_build.build()
 
     B = args.batch
-    weights, bn = synth.make_weights(), synth.make_bn()
-    net = slim.SlimNet(weights, bn, device=local, max_batch=max(B, 16), norm=args.norm)
+    WIDTHS = tuple(args.widths)   # default: the paper's set; other values exercise universal widths (NEXT-4)
+    weights, bn = synth.make_weights(), synth.make_bn(widths=WIDTHS)
+    net = slim.SlimNet(weights, bn, device=local, max_batch=max(B, 16), norm=args.norm, widths=WIDTHS)
     if not args.no_graph:
         slim.slim_set_graph_mode(net.ctx, True)
     stream = torch.cuda.current_stream(dev)
@@ -301,18 +303,20 @@ def run_ours(args):
     e2e_val = world * imgs_per_step * KE / float(te.item())
 
     if rank == 0:
-        cpu = oracle_throughput(args.cpu_seconds, norm=args.norm) if (world == 1 and not args.no_cpu) else None
+        cpu = oracle_throughput(args.cpu_seconds, norm=args.norm, widths=WIDTHS) if (world == 1 and not args.no_cpu) \
+            else None
         line = {
             "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world, "steps": K,
             "warmup": args.warmup, "ms_per_step": total_max_ms / K, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded N(0,1) images, random-init weights)",
             "config": {"workload": "CFG2: full SlimResNet chain (4 segments + pool/FC, 100 classes) at each width "
-                                   "r in {0.25,0.5,0.75,1.0}, batch 128 per width, 1 step = 4 x 128 images",
+                                   f"r in {{{','.join(f'{r:g}' for r in WIDTHS)}}}, batch {B} per width, "
+                                   f"1 step = {len(WIDTHS)} x {B} images",
                        "batch": B, "image": [32, 32, 3], "widths": list(WIDTHS), "norm": args.norm,
                        "parallelism": f"dp{world} (independent per-GPU batches)",
                        "l2": "flushed (256 MiB write) before every timed step", "graphs": not args.no_graph,
                        "instances": "sequential" if args.sequential else
-                                    "4 width instances, one CUDA stream each, run concurrently"},
+                                    f"{len(WIDTHS)} width instances, one CUDA stream each, run concurrently"},
             "per_width_images_per_s": per_width,
             "per_width_ms_per_batch": {str(r): width_ms[i] / KW for i, r in enumerate(WIDTHS)},
             "roofline": roof,
@@ -362,13 +366,25 @@ def run_stream(args):
     slim_build.build()
     net = slim.SlimNet(synth.make_weights(), synth.make_bn(), device=local, max_batch=args.bmax, norm=args.norm)
     greedy = args.executor == "greedy"
+    native = args.executor == "native"
     slim.slim_set_graph_mode(net.ctx, True)   # Alg. 1: one graph per (key, batch size, instance buffers), reused across steps
     n_total = args.requests * world
     devs, tups, grps = router.route(n_total, world, args.policy)
     mine = router.shard(devs, rank)
     tuples = np.asarray([router.TABLE_TUPLES[t] for t in tups[mine]], np.float32)
     x = torch.from_numpy(synth.make_images(len(mine), offset=200 + rank)).to(torch.bfloat16).to(dev)
-    if greedy:   # Alg. 1: native scheduler decisions, instances on their own CUDA streams
+    if native:   # Alg. 1 with the LOOP itself in C++ (slim_exec_*)
+        nx = slim.NativeExecutor(net, n_max=len(mine), B_max=args.bmax, Q_th=args.q_th, N_new=args.n_new)
+
+        class _NAdapter:
+            last_batches = [[]]
+
+            def run(self, x, tuples, stream=None):
+                out = nx.run(x, tuples)
+                self.last_batches = [[0] * nx.stats["batches"]]
+                return out
+        ex = _NAdapter()
+    elif greedy:   # Alg. 1: native scheduler decisions, instances on their own CUDA streams
         from paper_2510_09018_b200.executor import GreedyExecutor
         gx = GreedyExecutor(net, n_max=len(mine), B_max=args.bmax, Q_th=args.q_th, N_new=args.n_new)
 
@@ -422,9 +438,10 @@ def run_stream(args):
             "config": {"workload": f"{'CFG5' if world > 1 else 'CFG4'}: mixed-width request stream "
                                    f"(width tuples of Tables I-II), greedy (segment, w_req, w_prev) batching, "
                                    f"B_max={args.bmax}, routing={args.policy}, executor={args.executor}"
-                                   + (f" (Alg. 1: Q_th={args.q_th}, N_new={args.n_new})" if greedy else ""),
+                                   + (f" (Alg. 1: Q_th={args.q_th}, N_new={args.n_new})" if greedy or native else ""),
                        "requests_per_rank": args.requests, "parallelism": f"dp{world} routed"},
-            "batches_per_step_rank0": len(batches), "mean_batch_rank0": float(np.mean(batches)),
+            "batches_per_step_rank0": len(batches),
+            "mean_batch_rank0": float(len(mine) * 4 / len(batches)) if native else float(np.mean(batches)),
             **({"alg1_host_s_per_step": {k: gx.stats[k] / (args.steps + args.warmup)
                                          for k in ("t_next", "t_launch", "t_wait")},
                 "alg1_instances": len(gx.sched.instances())} if greedy else {}),
@@ -606,8 +623,10 @@ def main(argv=None):
     ap.add_argument("--requests", type=int, default=1024, help="stream: requests per rank per step")
     ap.add_argument("--bmax", type=int, default=256, help="stream: B_max of the key batching")
     ap.add_argument("--policy", default="random", help="stream: routing policy (random | slim | table_rr)")
+    ap.add_argument("--widths", type=float, nargs="+", default=list(WIDTHS),
+                    help="cfg2: width set (default the paper's {.25,.5,.75,1}; others = universal widths, NEXT-4)")
     ap.add_argument("--seg-policy", default="random", help="handoff: per-segment routing (random | pipeline | sticky)")
-    ap.add_argument("--executor", choices=("stream", "greedy"), default="stream",
+    ap.add_argument("--executor", choices=("stream", "greedy", "native"), default="stream",
                     help="stream: whole-stream packing per segment (graph replay); greedy: Alg. 1 executor "
                          "(native scheduler, per-instance streams)")
     ap.add_argument("--q-th", type=int, default=512, help="greedy: Alg. 1 scale trigger Q_th")

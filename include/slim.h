@@ -269,6 +269,27 @@ SLIM_API int slim_sched_queue_len(const slim_sched *s);
 /* Copies up to max_out instance records; returns the number of live instances. */
 SLIM_API int slim_sched_instances(const slim_sched *s, slim_instance *out, int max_out);
 
+/* ---- native Alg. 1 executor (one GPU) ------------------------------------------------
+ * Drives the scheduler's LOOP in C++: each RUN decision copies the batch's slots to the
+ * device and runs slim_launch (gather + segment) and slim_scatter (outputs -> the next
+ * segment's request pool, or the logits) on the instance's own CUDA stream; finished
+ * batches (event polling) release their instance and re-enqueue their requests with key
+ * (s+1, w_{s+1}, w_s); idle instances are unloaded (their buffers are recycled).
+ * create: allocates the per-segment request pools for n_max requests; the scheduler
+ * (B_max <= cfg.max_batch) stays owned by the caller.  run: images = device
+ * [n][H][W][in_channels]; tuples = HOST float [n][4] (the width of each segment, each in
+ * cfg.widths); logits = device fp32 [n][num_classes]; vram_external as in slim_sched_next;
+ * the call returns when every request is done (stream: ordered before the first read). */
+typedef struct slim_exec slim_exec;
+typedef struct {
+    int batches, loads, requeues, unloaded;
+    double seconds;            /* host wall time of the loop */
+} slim_exec_stats;
+SLIM_API slim_status slim_exec_create(slim_ctx *ctx, slim_sched *sched, int n_max, int B_max, slim_exec **out);
+SLIM_API void slim_exec_destroy(slim_exec *x);
+SLIM_API slim_status slim_exec_run(slim_exec *x, const void *images, const float *tuples, int n, float *logits,
+                                   size_t vram_external, slim_exec_stats *stats, void *stream);
+
 /* ---- execution modes and profiling ------------------------------------- */
 
 /* Graph mode (default off): slim_forward_ws / slim_forward_chain capture their

@@ -22,7 +22,7 @@ __all__ = [
     "slim_forward_workspace_bytes", "slim_chain_workspace_bytes", "slim_forward_chain", "slim_pack",
     "slim_launch", "slim_gather", "slim_scatter", "slim_last_error", "slim_launch_count", "slim_channels",
     "slim_act_channels", "SlimNet",
-    "manifest", "LIB_PATH", "Scheduler",
+    "manifest", "LIB_PATH", "Scheduler", "NativeExecutor",
 ]
 
 LIB_PATH = os.environ.get("SLIM_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libslim.so")
@@ -98,6 +98,11 @@ class slim_instance(ctypes.Structure):
                 ("t_last", ctypes.c_double), ("bytes", ctypes.c_size_t)]
 
 
+class slim_exec_stats(ctypes.Structure):
+    _fields_ = [("batches", ctypes.c_int), ("loads", ctypes.c_int), ("requeues", ctypes.c_int),
+                ("unloaded", ctypes.c_int), ("seconds", ctypes.c_double)]
+
+
 SLIM_ACT_IDLE, SLIM_ACT_RUN, SLIM_ACT_REQUEUE = 0, 1, 2
 
 _lib = None
@@ -154,6 +159,9 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "slim_sched_unload_idle": (_I, [_VP, ctypes.c_double, ctypes.POINTER(_I), _I]),
         "slim_sched_queue_len": (_I, [_VP]),
         "slim_sched_instances": (_I, [_VP, ctypes.POINTER(slim_instance), _I]),
+        "slim_exec_create": (_I, [_VP, _VP, _I, _I, ctypes.POINTER(_VP)]),
+        "slim_exec_destroy": (None, [_VP]),
+        "slim_exec_run": (_I, [_VP, _VP, ctypes.POINTER(_F), _I, _VP, _SZ, ctypes.POINTER(slim_exec_stats), _VP]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -170,7 +178,7 @@ EXPORTED = ("slim_create", "slim_destroy", "slim_default_config", "slim_load_seg
             "slim_launch_count", "slim_num_sms", "slim_channels", "slim_act_channels", "slim_set_graph_mode", "slim_profile_begin",
             "slim_profile_end", "slim_sched_default_knobs", "slim_sched_create", "slim_sched_destroy",
             "slim_sched_enqueue", "slim_sched_next", "slim_sched_complete", "slim_sched_unload_idle",
-            "slim_sched_queue_len", "slim_sched_instances")
+            "slim_sched_queue_len", "slim_sched_instances", "slim_exec_create", "slim_exec_destroy", "slim_exec_run")
 
 
 # ------------------------------------------------------------------ marshalling helpers
@@ -432,6 +440,46 @@ class Scheduler:
         if self.h:
             load_library().slim_sched_destroy(self.h)
             self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class NativeExecutor:
+    """Marshalling wrapper of the native Alg. 1 executor (slim_exec_*): the LOOP runs in C++."""
+
+    def __init__(self, net, n_max: int, B_max: int = 256, **knobs):
+        self.net = net
+        self.sched = Scheduler(net.cfg, B_max=B_max, **knobs)
+        h = ctypes.c_void_p()
+        _check(net.ctx, load_library().slim_exec_create(net.ctx, self.sched.h, n_max, B_max, ctypes.byref(h)))
+        self.h = h.value
+        self.n_max = n_max
+        self.stats = {}
+
+    def run(self, images, tuples, logits=None, vram_external: int = 0, stream=None):
+        """images: device [n,H,W,C]; tuples: [n,4] widths.  Returns fp32 logits [n, classes]."""
+        import torch
+        t = np.ascontiguousarray(np.asarray(tuples, np.float32))
+        n = t.shape[0]
+        if logits is None:
+            logits = torch.empty(n, self.net.cfg.num_classes, dtype=torch.float32, device=images.device)
+        st = slim_exec_stats()
+        _check(self.net.ctx, load_library().slim_exec_run(
+            self.h, _ptr(images), t.ctypes.data_as(ctypes.POINTER(ctypes.c_float)), n, _ptr(logits), vram_external,
+            ctypes.byref(st), _stream(stream)))
+        self.stats = dict(batches=st.batches, loads=st.loads, requeues=st.requeues, unloaded=st.unloaded,
+                          seconds=st.seconds)
+        return logits
+
+    def close(self):
+        if self.h:
+            load_library().slim_exec_destroy(self.h)
+            self.h = None
+        self.sched.close()
 
     def __del__(self):
         try:

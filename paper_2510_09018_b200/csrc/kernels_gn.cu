@@ -104,8 +104,14 @@ __device__ __forceinline__ void group_sums(float x0, float x1, int V, int vpg, i
     __syncthreads();
 }
 
+// Threads per CTA: bf16 <= 256 (3 CTAs per SM resident), fp32 <= 512 (its vectors hold 4 values).
 template <typename T>
-__global__ void __launch_bounds__(kGnMaxThreads, 1) gn_kernel(const GnArgs a) {
+constexpr int gn_max_threads() { return sizeof(T) == 2 ? 256 : kGnMaxThreads; }
+
+// TWO: a second raw input (the projection shortcut) -- a template flag so the common case
+// keeps half the registers (more CTAs resident: the kernel is a short latency chain).
+template <typename T, bool TWO>
+__global__ void __launch_bounds__(gn_max_threads<T>(), sizeof(T) == 2 ? (TWO ? 2 : 3) : 1) gn_kernel(const GnArgs a) {
     constexpr int VE = 16 / sizeof(T);   // elements per 16-byte vector
     __shared__ float2 part[kGnMaxThreads];
     __shared__ float gsum[2][kGnMaxCh / 8];
@@ -115,7 +121,7 @@ __global__ void __launch_bounds__(kGnMaxThreads, 1) gn_kernel(const GnArgs a) {
     const int ch0 = blockIdx.x * a.gpc * a.cpg;         // first channel of this CTA's slice
     const int V = a.gpc * a.cpg / VE, vpg = a.cpg / VE;
     const int t = threadIdx.x, v = t % V, k = blockDim.x / V;
-    const bool two = a.yp != nullptr;
+    constexpr bool two = TWO;
     const size_t img = static_cast<size_t>(n) * a.HW * a.C;
     const size_t base = img + ch0 + v * VE;
     const float inv_cnt = 1.f / (static_cast<float>(a.HW) * a.cpg);
@@ -127,14 +133,15 @@ __global__ void __launch_bounds__(kGnMaxThreads, 1) gn_kernel(const GnArgs a) {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
     // the slice into registers: pixels p0, p0 + k, ... (< kGnPPT of them), all loads in flight
-    uint4 q0[kGnPPT], q1[kGnPPT];
+    uint4 q0[kGnPPT], q1[TWO ? kGnPPT : 1];
 #pragma unroll
     for (int j = 0; j < kGnPPT; ++j) {
         const int p = p0 + j * k;
-        q0[j] = q1[j] = make_uint4(0u, 0u, 0u, 0u);
+        q0[j] = make_uint4(0u, 0u, 0u, 0u);
+        if (TWO) q1[TWO ? j : 0] = make_uint4(0u, 0u, 0u, 0u);
         if (p < a.HW) {
             q0[j] = ld16(static_cast<const T *>(a.y) + base + static_cast<size_t>(p) * a.C);
-            if (two) q1[j] = ld16(static_cast<const T *>(a.yp) + base + static_cast<size_t>(p) * a.C);
+            if (TWO) q1[TWO ? j : 0] = ld16(static_cast<const T *>(a.yp) + base + static_cast<size_t>(p) * a.C);
         }
     }
     // pass 1: sums -> means
@@ -144,7 +151,7 @@ __global__ void __launch_bounds__(kGnMaxThreads, 1) gn_kernel(const GnArgs a) {
         if (p0 + j * k < a.HW) {
             float x0[VE], x1[VE];
             unpack(q0[j], T(), x0);
-            unpack(q1[j], T(), x1);
+            if (TWO) unpack(q1[TWO ? j : 0], T(), x1);
 #pragma unroll
             for (int i = 0; i < VE; ++i) {
                 s0 += x0[i];
@@ -166,7 +173,7 @@ __global__ void __launch_bounds__(kGnMaxThreads, 1) gn_kernel(const GnArgs a) {
         if (p0 + j * k < a.HW) {
             float x0[VE], x1[VE];
             unpack(q0[j], T(), x0);
-            unpack(q1[j], T(), x1);
+            if (TWO) unpack(q1[TWO ? j : 0], T(), x1);
 #pragma unroll
             for (int i = 0; i < VE; ++i) {
                 s0 = fmaf(x0[i] - mu0, x0[i] - mu0, s0);
@@ -202,7 +209,7 @@ __global__ void __launch_bounds__(kGnMaxThreads, 1) gn_kernel(const GnArgs a) {
         if (p >= a.HW) continue;
         float z[VE], x0[VE], x1[VE], r[VE];
         unpack(q0[j], T(), x0);
-        unpack(q1[j], T(), x1);
+        if (TWO) unpack(q1[TWO ? j : 0], T(), x1);
         unpack(a.res ? ld16(static_cast<const T *>(a.res) + base + static_cast<size_t>(p) * a.C) : make_uint4(0u, 0u, 0u, 0u),
                T(), r);
 #pragma unroll
@@ -221,13 +228,13 @@ __global__ void __launch_bounds__(kGnMaxThreads, 1) gn_kernel(const GnArgs a) {
 // Pixel lanes per vector slot: k = HW / kGnPPT (each thread holds kGnPPT pixels).
 static int gn_lanes(int HW) { return HW > kGnPPT ? (HW + kGnPPT - 1) / kGnPPT : 1; }
 
-int gn_groups_per_cta(int /*B*/, int HW, int C, int cpg, int /*num_sms*/) {
+int gn_groups_per_cta(int /*B*/, int HW, int C, int cpg, bool fp32) {
     // independent of B (batch independence is bit-exact): widen the slice while it divides
-    // G and the CTA stays <= 512 threads (vpg = cpg/8 vectors per group in bf16, cpg/4 in fp32;
-    // sized for fp32 so both modes pick the same slice)
-    const int G = C / cpg, k = gn_lanes(HW), vpg = cpg / 4;
+    // G and the CTA stays within its thread budget (vpg = cpg/8 vectors per group in bf16, cpg/4 in fp32)
+    const int G = C / cpg, k = gn_lanes(HW), vpg = cpg / (fp32 ? 4 : 8);
+    const int maxt = fp32 ? gn_max_threads<float>() : gn_max_threads<uint16_t>();
     int gpc = 1;
-    while (G % (2 * gpc) == 0 && 2 * gpc * vpg * k <= kGnMaxThreads && 2 * gpc * cpg <= kGnMaxCh) gpc *= 2;
+    while (G % (2 * gpc) == 0 && 2 * gpc * vpg * k <= maxt && 2 * gpc * cpg <= kGnMaxCh) gpc *= 2;
     return gpc;
 }
 
@@ -237,7 +244,8 @@ cudaError_t launch_gn(const GnArgs &a, bool fp32, cudaStream_t s, bool pdl) {
     const int V = a.gpc * a.cpg / VE;
     int k = 1;   // power-of-two pixel lanes per vector slot, every thread holds <= kGnPPT pixels
     while (k < gn_lanes(a.HW)) k *= 2;
-    if (V * k > kGnMaxThreads || (a.HW + k - 1) / k > kGnPPT) return cudaErrorInvalidValue;
+    if (V * k > (fp32 ? gn_max_threads<float>() : gn_max_threads<uint16_t>()) || (a.HW + k - 1) / k > kGnPPT)
+        return cudaErrorInvalidValue;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(a.C / (a.gpc * a.cpg), a.B);
     cfg.blockDim = dim3(V * k);
@@ -247,7 +255,9 @@ cudaError_t launch_gn(const GnArgs &a, bool fp32, cudaStream_t s, bool pdl) {
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = pdl ? 1 : 0;
-    return fp32 ? cudaLaunchKernelEx(&cfg, gn_kernel<float>, a) : cudaLaunchKernelEx(&cfg, gn_kernel<uint16_t>, a);
+    if (a.yp)
+        return fp32 ? cudaLaunchKernelEx(&cfg, gn_kernel<float, true>, a) : cudaLaunchKernelEx(&cfg, gn_kernel<uint16_t, true>, a);
+    return fp32 ? cudaLaunchKernelEx(&cfg, gn_kernel<float, false>, a) : cudaLaunchKernelEx(&cfg, gn_kernel<uint16_t, false>, a);
 }
 
 }  // namespace slim

@@ -89,6 +89,10 @@ struct slim_ctx {
     unsigned long long *trace = nullptr;   // diagnostics: SLIM_CONV_TRACE -> per-CTA timestamps of the last conv
 };
 
+namespace slim {
+const slim_config *ctx_config(const slim_ctx *ctx) { return &ctx->cfg; }
+}  // namespace slim
+
 extern "C" int slim_channels(float r, int C) {
     // c(r, C) = ceil(r*C) (north_star); integer form for r = k/4 (exact for the width set of P:148)
     const double q = static_cast<double>(r) * 4.0;
@@ -1025,7 +1029,7 @@ slim_status gn_apply(slim_ctx *ctx, cudaStream_t st, int seg, int layer, const D
     g.HW = H * H;
     g.C = C;
     g.cpg = c.gn_group_channels;
-    g.gpc = gn_groups_per_cta(B, g.HW, C, g.cpg, ctx->num_sms);
+    g.gpc = gn_groups_per_cta(B, g.HW, C, g.cpg, c.dtype == SLIM_FP32);
     g.eps = c.bn_eps;
     g.relu_lo = relu ? 0.f : -INFINITY;
     const double eb = static_cast<double>(elem_bytes(c));

@@ -86,22 +86,47 @@ class HandoffExecutor:
         self.ws = torch.empty(self.wsb, dtype=torch.uint8, device=self.dev)
         self.stats = dict(sent_rows=0, recv_rows=0, batches=0)
 
-    def _idx(self, a):
+    def _plan(self, tuples: np.ndarray, dev: np.ndarray):
+        """Key batching of all four segments and every exchange list (host), with ONE host-to-device
+        copy of all slot arrays; cached while (tuples, plan) repeat."""
+        key = (hash(tuples.tobytes()), hash(dev.tobytes()))
+        if getattr(self, "_pkey", None) == key:
+            return self._pc
+        parts, segs, off = [], [], 0
+
+        def add(a):
+            nonlocal off
+            parts.append(np.asarray(a, np.int32))
+            off += len(a)
+            return off - len(a), len(a)
+        for s in range(4):
+            mine = np.nonzero(dev[:, s] == self.rank)[0]
+            batches = []
+            if len(mine):
+                reqs = [(int(i), s, float(tuples[i, s]), float(tuples[i, s - 1]) if s else 0.0, int(i)) for i in mine]
+                descs, order = slim_pack(self.cfg, reqs, self.B_max)
+                batches = [(d, add(mine[order[d["first"]:d["first"] + d["batch"]]])) for d in descs]
+            ex = None
+            if s < 3 and self.world > 1:
+                send, recv = exchange_lists(dev, s, self.rank, self.world)
+                ex = (add(np.concatenate(send)), [len(x) for x in send], add(np.concatenate(recv)), [len(x) for x in recv])
+            segs.append((batches, ex))
         import torch
-        return torch.as_tensor(np.ascontiguousarray(a, np.int32)).to(self.dev, non_blocking=False)
+        host = torch.from_numpy(np.concatenate(parts) if parts else np.zeros(1, np.int32))
+        self._slots_d = host.to(self.dev)
+        self._pkey, self._pc = key, segs
+        return segs
+
+    def _sl(self, span):
+        return self._slots_d[span[0]:span[0] + span[1]]
 
     def compute(self, s: int, images, tuples: np.ndarray, dev: np.ndarray, stream=None):
         """Run segment s for the requests routed to this rank (key batching + RUNBATCH)."""
-        mine = np.nonzero(dev[:, s] == self.rank)[0]
-        if not len(mine):
-            return
         cfg, hw = self.cfg, self.cfg.image_hw
-        reqs = [(int(i), s, float(tuples[i, s]), float(tuples[i, s - 1]) if s else 0.0, int(i)) for i in mine]
-        descs, order = slim_pack(cfg, reqs, self.B_max)
         pool = images if s == 0 else self.pools[s]
-        for d in descs:
-            b, first = d["batch"], d["first"]
-            slots = self._idx(mine[order[first:first + b]])
+        for d, span in self._plan(np.asarray(tuples, np.float32), dev)[s][0]:
+            b = d["batch"]
+            slots = self._sl(span)
             slim_launch(self.net.ctx, d, slots, pool, self.row_elems[s] * self.eb, self.slab, self.out, self.ws,
                         self.wsb, stream)
             if s < 3:
@@ -116,22 +141,22 @@ class HandoffExecutor:
     def pack(self, s: int, dev: np.ndarray, stream=None):
         """Send buffer (uint8) of the rows leaving after segment s, and its per-destination byte counts."""
         import torch
-        send, recv = exchange_lists(dev, s, self.rank, self.world)
+        send_span, send_n, _, recv_n = self._pc[s][1]
         row = self.row_elems[s + 1] * self.eb
-        ids = np.concatenate(send) if sum(len(x) for x in send) else np.zeros(0, np.int64)
-        buf = torch.empty(max(len(ids), 1) * row, dtype=torch.uint8, device=self.dev)
-        if len(ids):
-            slim_gather(self.net.ctx, self.pools[s + 1], self._idx(ids), len(ids), row, buf, stream)
-        self.stats["sent_rows"] += len(ids)
-        return buf[:len(ids) * row], [len(x) * row for x in send], [len(x) * row for x in recv]
+        n = send_span[1]
+        buf = torch.empty(max(n, 1) * row, dtype=torch.uint8, device=self.dev)
+        if n:
+            slim_gather(self.net.ctx, self.pools[s + 1], self._sl(send_span), n, row, buf, stream)
+        self.stats["sent_rows"] += n
+        return buf[:n * row], [c * row for c in send_n], [c * row for c in recv_n]
 
     def unpack(self, s: int, dev: np.ndarray, recv_buf, stream=None):
-        _, recv = exchange_lists(dev, s, self.rank, self.world)
-        ids = np.concatenate(recv) if sum(len(x) for x in recv) else np.zeros(0, np.int64)
-        if len(ids):
+        _, _, recv_span, _ = self._pc[s][1]
+        n = recv_span[1]
+        if n:
             row = self.row_elems[s + 1] * self.eb
-            slim_scatter(self.net.ctx, recv_buf, self._idx(ids), len(ids), row, self.pools[s + 1], row, stream)
-        self.stats["recv_rows"] += len(ids)
+            slim_scatter(self.net.ctx, recv_buf, self._sl(recv_span), n, row, self.pools[s + 1], row, stream)
+        self.stats["recv_rows"] += n
 
     def run(self, images, tuples, dev: np.ndarray, transport=None, stream=None):
         """All four segments with the hand-offs between them (collective transport).  Returns the
@@ -141,7 +166,7 @@ class HandoffExecutor:
         tuples = np.asarray(tuples, np.float32)
         for s in range(4):
             self.compute(s, images, tuples, dev, stream)
-            if s < 3:
+            if s < 3 and self.world > 1:
                 send_buf, sb, rb = self.pack(s, dev, stream)
                 recv_buf = torch.empty(max(sum(rb), 1), dtype=torch.uint8, device=self.dev)
                 torch.cuda.current_stream(self.dev).synchronize()   # rows packed before the collective reads them

@@ -62,3 +62,26 @@ def test_executor_vram_cap_serialises_and_offload_reloads(net):
     torch.testing.assert_close(got, _expected(net, x, tuples), rtol=0, atol=0)
     assert ex.stats["unloaded"] > 0 and ex.stats["seg_reloads"] > 0
     assert torch.cuda.memory_allocated() >= base
+
+
+@pytest.mark.parametrize("B_max,Q_th,N_new", [(32, 64, 2), (5, 3, 4), (256, 512, 1)])
+def test_native_executor_matches_per_request_chain(net, B_max, Q_th, N_new):
+    x, tuples = _stream(300, 17)
+    ex = slim.NativeExecutor(net, n_max=300, B_max=B_max, Q_th=Q_th, N_new=N_new)
+    got = ex.run(x, tuples).clone()
+    got2 = ex.run(x, tuples).clone()          # instances persist across runs
+    ex.close()
+    exp = _expected(net, x, tuples)
+    torch.testing.assert_close(got, exp, rtol=0, atol=0)
+    torch.testing.assert_close(got2, exp, rtol=0, atol=0)
+
+
+def test_native_executor_vram_cap_and_unload(net):
+    x, tuples = _stream(100, 3)
+    big = max(slim.slim_segment_bytes(net.cfg, s, 1.0, 1.0) for s in range(4))
+    ex = slim.NativeExecutor(net, n_max=100, B_max=16, t_idle_s=0.0, M_max_bytes=float(1.2 * big))
+    got = ex.run(x, tuples).clone()
+    st = ex.stats
+    ex.close()
+    torch.testing.assert_close(got, _expected(net, x, tuples), rtol=0, atol=0)
+    assert st["unloaded"] > 0 and st["batches"] >= 4

@@ -20,8 +20,9 @@ def main():
     ap.add_argument("--widths", type=float, nargs="+", default=[1.0])
     ap.add_argument("--batch", type=int, default=128)
     ap.add_argument("--reps", type=int, default=1)
+    ap.add_argument("--norm", default="bn")
     a = ap.parse_args()
-    net = slim.SlimNet(synth.make_weights(), synth.make_bn(), max_batch=a.batch)
+    net = slim.SlimNet(synth.make_weights(), synth.make_bn(), max_batch=a.batch, norm=a.norm)
     x = torch.from_numpy(synth.make_images(a.batch)).to(torch.bfloat16).cuda()
     for _ in range(a.reps):
         for r in a.widths:
