@@ -6,12 +6,13 @@
 //
 // The convs run with an identity epilogue and no ReLU (relu_lo = -inf) and store the raw
 // pre-norm output y; this kernel then computes, per (image n, group g),
-//   mu = mean(y[n, :, :, g]),  var = mean((y - mu)^2)          (two passes, fp32)
+//   mu = mean(y[n, :, :, g]),  var = mean((y - mu)^2)          (fp32; one pass over registers in the
+//                                                              shifted-data form, see the kernel)
 // and writes  out = act( (y - mu) * rsqrt(var + eps) * gamma + beta
 //                        [ + (yp - mu_p) * rsqrt(var_p + eps) * gamma_p + beta_p ]   (projection shortcut)
 //                        [ + res ] )                                                  (identity shortcut)
 // act = ReLU or identity.  out may alias y (each element is read and written by the same
-// thread in the last pass, after both statistics passes).
+// thread, after the statistics).
 //
 // Layout: NHWC, dense; a CTA owns gpc whole groups of one image (gpc*cpg contiguous
 // channels per pixel) and reads them as 16-byte vectors: thread t always handles the
@@ -144,30 +145,23 @@ __global__ void __launch_bounds__(gn_max_threads<T>(), sizeof(T) == 2 ? (TWO ? 2
             if (TWO) q1[TWO ? j : 0] = ld16(static_cast<const T *>(a.yp) + base + static_cast<size_t>(p) * a.C);
         }
     }
-    // pass 1: sums -> means
-    float s0 = 0.f, s1 = 0.f;
-#pragma unroll
-    for (int j = 0; j < kGnPPT; ++j)
-        if (p0 + j * k < a.HW) {
-            float x0[VE], x1[VE];
-            unpack(q0[j], T(), x0);
-            if (TWO) unpack(q1[TWO ? j : 0], T(), x1);
-#pragma unroll
-            for (int i = 0; i < VE; ++i) {
-                s0 += x0[i];
-                if (two) s1 += x1[i];
-            }
-        }
-    group_sums(s0, s1, V, vpg, k, a.gpc, part, gsum[0], gsum[1]);
+    // statistics in ONE register pass, shifted by a sample of the group (the group's first value
+    // in this image, K): mean = K + S1/N, var = S2/N - (S1/N)^2 with S1 = sum(x - K),
+    // S2 = sum((x - K)^2) -- K lies within a few sigma of the mean, so the subtraction does not
+    // cancel (the shifted-data form of the textbook variance).  Fixed-order reductions.
     const int lg = v / vpg;
-    const float mu0 = gsum[0][lg] * inv_cnt, mu1 = gsum[1][lg] * inv_cnt;
-    if (t < a.gpc) {
-        stat[0][0][t] = gsum[0][t] * inv_cnt;
-        stat[1][0][t] = gsum[1][t] * inv_cnt;
+    const size_t gfirst = img + ch0 + static_cast<size_t>(lg) * a.cpg;   // pixel 0, first channel of the group
+    float K0, K1 = 0.f;
+    {
+        float kv[VE];
+        unpack(ld16(static_cast<const T *>(a.y) + gfirst), T(), kv);
+        K0 = kv[0];
+        if (TWO) {
+            unpack(ld16(static_cast<const T *>(a.yp) + gfirst), T(), kv);
+            K1 = kv[0];
+        }
     }
-    // pass 2 (registers): sum of squared deviations -> rstd
-    s0 = 0.f;
-    s1 = 0.f;
+    float s0 = 0.f, q0s = 0.f, s1 = 0.f, q1s = 0.f;
 #pragma unroll
     for (int j = 0; j < kGnPPT; ++j)
         if (p0 + j * k < a.HW) {
@@ -176,15 +170,34 @@ __global__ void __launch_bounds__(gn_max_threads<T>(), sizeof(T) == 2 ? (TWO ? 2
             if (TWO) unpack(q1[TWO ? j : 0], T(), x1);
 #pragma unroll
             for (int i = 0; i < VE; ++i) {
-                s0 = fmaf(x0[i] - mu0, x0[i] - mu0, s0);
-                if (two) s1 = fmaf(x1[i] - mu1, x1[i] - mu1, s1);
+                const float d0 = x0[i] - K0;
+                s0 += d0;
+                q0s = fmaf(d0, d0, q0s);
+                if (TWO) {
+                    const float d1 = x1[i] - K1;
+                    s1 += d1;
+                    q1s = fmaf(d1, d1, q1s);
+                }
             }
         }
-    __syncthreads();   // every thread has read gsum (means) before it is overwritten
-    group_sums(s0, s1, V, vpg, k, a.gpc, part, gsum[0], gsum[1]);
-    if (t < a.gpc) {
-        stat[0][1][t] = rsqrtf(gsum[0][t] * inv_cnt + a.eps);
-        stat[1][1][t] = rsqrtf(gsum[1][t] * inv_cnt + a.eps);
+    group_sums(s0, q0s, V, vpg, k, a.gpc, part, gsum[0], gsum[1]);
+    if (t < a.gpc) {   // K of local group t: its first value (every thread of group t loaded the same one)
+        float kv[VE];
+        unpack(ld16(static_cast<const T *>(a.y) + img + ch0 + static_cast<size_t>(t) * a.cpg), T(), kv);
+        const float m = gsum[0][t] * inv_cnt;
+        stat[0][0][t] = kv[0] + m;
+        stat[0][1][t] = rsqrtf(fmaxf(fmaf(-m, m, gsum[1][t] * inv_cnt), 0.f) + a.eps);
+    }
+    if (TWO) {
+        __syncthreads();   // gsum is reused
+        group_sums(s1, q1s, V, vpg, k, a.gpc, part, gsum[0], gsum[1]);
+        if (t < a.gpc) {
+            float kv[VE];
+            unpack(ld16(static_cast<const T *>(a.yp) + img + ch0 + static_cast<size_t>(t) * a.cpg), T(), kv);
+            const float m = gsum[0][t] * inv_cnt;
+            stat[1][0][t] = kv[0] + m;
+            stat[1][1][t] = rsqrtf(fmaxf(fmaf(-m, m, gsum[1][t] * inv_cnt), 0.f) + a.eps);
+        }
     }
     __syncthreads();
     // per-channel affine of the slice in smem: z = y * A + Bc, A = rstd*gamma, Bc = beta - mu*A

@@ -1,0 +1,7 @@
+mkdir -p gpurun_out
+timeout 600 python -m pytest tests/test_gpu_gn.py -x -q > gpurun_out/t12.log 2>&1; echo tests=$?
+tail -4 gpurun_out/t12.log
+timeout 600 python bench.py --norm gn --steps 300 --no-cpu > gpurun_out/bench_gn.json 2> gpurun_out/bench_gn.err; echo gn=$?
+python -c "
+import json;d=json.loads(open('gpurun_out/bench_gn.json').read().strip().splitlines()[-1]);print(d['value'],d['per_width_images_per_s'],d['kernel_time_by_kind_ms_per_step'])"
+python tools/micro.py 128 200 gn > gpurun_out/micro_gn.txt 2>&1; cat gpurun_out/micro_gn.txt
