@@ -136,11 +136,13 @@ def run_ours(args):
     B = args.batch
     WIDTHS = tuple(args.widths)   # default: the paper's set; other values exercise universal widths (NEXT-4)
     weights, bn = synth.make_weights(), synth.make_bn(widths=WIDTHS)
-    net = slim.SlimNet(weights, bn, device=local, max_batch=max(B, 16), norm=args.norm, widths=WIDTHS)
+    net = slim.SlimNet(weights, bn, device=local, max_batch=max(B, 16), norm=args.norm, widths=WIDTHS,
+                       dtype=args.dtype)
+    adt = torch.bfloat16 if args.dtype == "bf16" else torch.float32
     if not args.no_graph:
         slim.slim_set_graph_mode(net.ctx, True)
     stream = torch.cuda.current_stream(dev)
-    xs = {r: torch.from_numpy(synth.make_images(B, offset=100 + rank * 8 + i)).to(torch.bfloat16).to(dev)
+    xs = {r: torch.from_numpy(synth.make_images(B, offset=100 + rank * 8 + i)).to(adt).to(dev)
           for i, r in enumerate(WIDTHS)}
     logits = {r: torch.empty(B, 100, dtype=torch.float32, device=dev) for r in WIDTHS}
     wsb = max(slim.slim_chain_workspace_bytes(net.ctx, (r,) * 4, B) for r in WIDTHS)
@@ -228,6 +230,10 @@ def run_ours(args):
             chain(r, stream)
     recs = slim.slim_profile_end(net.ctx)
     peaks = _peaks()
+    if args.dtype == "fp32":
+        # FP32 mode runs on the CUDA cores (FFMA): peak = 148 SMs x 128 FP32 lanes x 2 FLOP x 1.965 GHz
+        # (B200 unit counts and the max SM clock of this pool) -- an ALU roofline
+        peaks = dict(peaks, bf16=148 * 128 * 2 * 1.965e9 / 1e12, src="derived (FFMA lanes x clock)")
     by_kind = {}
     for rc in recs:
         d = by_kind.setdefault(rc["kind"], dict(ms=0.0, flops=0.0, bytes=0.0, n=0, roof_ms=0.0))
@@ -243,7 +249,8 @@ def run_ours(args):
     hbm_time = D["bytes"] / (peaks["hbm"] * 1e9)
     if tensor_time >= hbm_time:
         achieved = D["flops"] / (D["ms"] / 1e3) / 1e12
-        roof = {"bound": "tensor", "achieved": achieved, "peak": peaks["bf16"], "unit": "TFLOP/s",
+        roof = {"bound": "tensor" if args.dtype == "bf16" else "alu", "achieved": achieved, "peak": peaks["bf16"],
+                "unit": "TFLOP/s",
                 "frac": achieved / peaks["bf16"]}
     else:
         achieved = D["bytes"] / (D["ms"] / 1e3) / 1e9
@@ -251,10 +258,10 @@ def run_ours(args):
                 "frac": achieved / peaks["hbm"]}
     roof.update({
         "kernel": dom, "launches_profiled": D["n"], "share_of_kernel_time": D["ms"] / kern_ms,
-        "peak_source": peaks["src"] + ", bf16 burst",
+        "peak_source": peaks["src"] + (", bf16 burst" if args.dtype == "bf16" else ""),
         "per_layer_roofline_frac": D["roof_ms"] / D["ms"],
         "algorithmic_flops_per_launch": D["flops"] / D["n"], "algorithmic_bytes_per_launch": D["bytes"] / D["n"],
-        "traffic": _ncu_traffic(),
+        "traffic": _ncu_traffic() if args.dtype == "bf16" else None,
     })
 
     # ---------------- e2e through the public API with host buffers
@@ -308,7 +315,8 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world, "steps": K,
             "warmup": args.warmup, "ms_per_step": total_max_ms / K, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded N(0,1) images, random-init weights)",
+            "vs_baseline": None, "dtype": args.dtype if args.dtype == "bf16" else "f32",
+            "data": "synthetic (seeded N(0,1) images, random-init weights)",
             "config": {"workload": "CFG2: full SlimResNet chain (4 segments + pool/FC, 100 classes) at each width "
                                    f"r in {{{','.join(f'{r:g}' for r in WIDTHS)}}}, batch {B} per width, "
                                    f"1 step = {len(WIDTHS)} x {B} images",
@@ -623,6 +631,8 @@ def main(argv=None):
     ap.add_argument("--requests", type=int, default=1024, help="stream: requests per rank per step")
     ap.add_argument("--bmax", type=int, default=256, help="stream: B_max of the key batching")
     ap.add_argument("--policy", default="random", help="stream: routing policy (random | slim | table_rr)")
+    ap.add_argument("--dtype", choices=("bf16", "fp32"), default="bf16",
+                    help="cfg2: bf16 storage + fp32 accumulate (tcgen05, default) or the FP32/TF32-off mode (SIMT FFMA)")
     ap.add_argument("--widths", type=float, nargs="+", default=list(WIDTHS),
                     help="cfg2: width set (default the paper's {.25,.5,.75,1}; others = universal widths, NEXT-4)")
     ap.add_argument("--seg-policy", default="random", help="handoff: per-segment routing (random | pipeline | sticky)")
