@@ -320,6 +320,137 @@ __global__ void __launch_bounds__(kF32Threads) conv_f32_kernel(const ConvF32Args
     }
 }
 
+// FP32 implicit GEMM: CTA tile 128 output pixels x 64 output channels, K in steps of
+// 16 input channels of one tap, double-buffered through shared memory (A stored k-major so a
+// thread reads its 8 pixels as two float4, B as one float4 of 4 channels); each thread owns an
+// 8 x 4 register tile (32 FFMA per 3 LDS.128).  Same fused epilogues as conv_f32_kernel.
+constexpr int kGM = 128, kGN = 64, kGK = 16, kGThreads = 256;
+
+struct GemmTile {   // per-thread loader / compute coordinates of conv_f32_gemm_kernel
+    int tx, ty, lp, lc, lb, lbc, pn, poh, pw, gco;
+    bool pok, cok;
+};
+
+// acc += the GEMM of one conv part (K = k*k*cin in steps of 16 channels of one tap)
+__device__ __forceinline__ void f32_gemm_part(const GemmTile &g, const float *__restrict__ x, const float *__restrict__ w,
+                                              int H, int W, int cin, int k, int st, int pad, int cin_full,
+                                              float (*As)[kGK][kGM + 4], float (*Bs)[kGK][kGN + 4], float (&acc)[8][4]) {
+    const int csteps = cin / kGK, steps = k * k * csteps;
+    float4 ra0, ra1, rb;
+    auto load = [&](int s) {
+        const int tap = s / csteps, c0 = (s - tap * csteps) * kGK, kh = tap / k, kw = tap - kh * k;
+        const int ih = st * g.poh + kh - pad, iw = st * g.pw + kw - pad;
+        const bool ok = g.pok && ih >= 0 && ih < H && iw >= 0 && iw < W;
+        const float *xp = x + ((static_cast<size_t>(g.pn) * H + (ok ? ih : 0)) * W + (ok ? iw : 0)) * cin + c0 + g.lc;
+        ra0 = ok ? __ldg(reinterpret_cast<const float4 *>(xp)) : make_float4(0.f, 0.f, 0.f, 0.f);
+        ra1 = ok ? __ldg(reinterpret_cast<const float4 *>(xp + 4)) : make_float4(0.f, 0.f, 0.f, 0.f);
+        const float *wp = w + ((static_cast<size_t>(g.cok ? g.gco : 0) * k + kh) * k + kw) * cin_full + c0 + g.lbc;
+        rb = g.cok ? __ldg(reinterpret_cast<const float4 *>(wp)) : make_float4(0.f, 0.f, 0.f, 0.f);
+    };
+    auto store = [&](int b) {
+        As[b][g.lc + 0][g.lp] = ra0.x;
+        As[b][g.lc + 1][g.lp] = ra0.y;
+        As[b][g.lc + 2][g.lp] = ra0.z;
+        As[b][g.lc + 3][g.lp] = ra0.w;
+        As[b][g.lc + 4][g.lp] = ra1.x;
+        As[b][g.lc + 5][g.lp] = ra1.y;
+        As[b][g.lc + 6][g.lp] = ra1.z;
+        As[b][g.lc + 7][g.lp] = ra1.w;
+        Bs[b][g.lbc + 0][g.lb] = rb.x;
+        Bs[b][g.lbc + 1][g.lb] = rb.y;
+        Bs[b][g.lbc + 2][g.lb] = rb.z;
+        Bs[b][g.lbc + 3][g.lb] = rb.w;
+    };
+    __syncthreads();   // a previous part's last tile has been consumed
+    load(0);
+    store(0);
+    __syncthreads();
+#pragma unroll 1
+    for (int s = 0; s < steps; ++s) {
+        const int b = s & 1;
+        if (s + 1 < steps) load(s + 1);
+#pragma unroll
+        for (int kk = 0; kk < kGK; ++kk) {
+            const float4 a0 = *reinterpret_cast<const float4 *>(&As[b][kk][g.tx * 8]);
+            const float4 a1 = *reinterpret_cast<const float4 *>(&As[b][kk][g.tx * 8 + 4]);
+            const float4 bv = *reinterpret_cast<const float4 *>(&Bs[b][kk][g.ty * 4]);
+            const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+            const float bw[4] = {bv.x, bv.y, bv.z, bv.w};
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], bw[j], acc[i][j]);
+        }
+        if (s + 1 < steps) store(b ^ 1);
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(kGThreads) conv_f32_gemm_kernel(const ConvF32Args a) {
+    __shared__ __align__(16) float As[2][kGK][kGM + 4];
+    __shared__ __align__(16) float Bs[2][kGK][kGN + 4];
+    const int tid = threadIdx.x;
+    const long m0 = static_cast<long>(blockIdx.x) * kGM;
+    const int n0 = blockIdx.y * kGN;
+    const long npix = static_cast<long>(a.B) * a.Ho * a.Wo;
+    GemmTile g;
+    g.tx = tid & 15;          // compute: pixels tx*8 .. +7, channels ty*4 .. +3
+    g.ty = tid >> 4;
+    g.lp = tid >> 1;          // A loader: pixel lp, channels lc .. lc+7 of the 16-channel step
+    g.lc = (tid & 1) * 8;
+    g.lb = tid >> 2;          // B loader: channel lb, ci lbc .. lbc+3
+    g.lbc = (tid & 3) * 4;
+    const long gp = m0 + g.lp;
+    g.pok = gp < npix;
+    const long gpp = g.pok ? gp : 0;
+    g.pn = static_cast<int>(gpp / (a.Ho * a.Wo));
+    g.poh = static_cast<int>((gpp / a.Wo) % a.Ho);
+    g.pw = static_cast<int>(gpp % a.Wo);
+    g.gco = n0 + g.lb;
+    g.cok = g.gco < a.c_out;
+    const int tx = g.tx, ty = g.ty;
+    float acc0[8][4], acc1[8][4];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc0[i][j] = acc1[i][j] = 0.f;
+    const int nparts = a.epi == EPI_BN_PROJ_RELU ? 2 : 1;
+    f32_gemm_part(g, a.x, a.w, a.H, a.W, a.c_in, a.k, a.stride, a.pad, a.cin_full, As, Bs, acc0);
+    if (nparts == 2) f32_gemm_part(g, a.x1, a.w1, a.H1, a.W1, a.c_in1, 1, a.stride1, 0, a.cin1_full, As, Bs, acc1);
+    const int c = n0 + ty * 4;
+    if (c >= a.c_out) return;   // c_out is a multiple of 16: a thread's 4 channels are all valid or none
+    const float4 s0 = *reinterpret_cast<const float4 *>(a.scale0 + c), t0 = *reinterpret_cast<const float4 *>(a.shift0 + c);
+    float4 s1 = make_float4(0.f, 0.f, 0.f, 0.f), t1 = s1;
+    if (nparts == 2) {
+        s1 = *reinterpret_cast<const float4 *>(a.scale1 + c);
+        t1 = *reinterpret_cast<const float4 *>(a.shift1 + c);
+    }
+    const float sc0[4] = {s0.x, s0.y, s0.z, s0.w}, sh0[4] = {t0.x, t0.y, t0.z, t0.w};
+    const float sc1[4] = {s1.x, s1.y, s1.z, s1.w}, sh1[4] = {t1.x, t1.y, t1.z, t1.w};
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const long p = m0 + tx * 8 + i;
+        if (p >= npix) break;
+        const size_t o = static_cast<size_t>(p) * a.c_out + c;
+        float r[4] = {0.f, 0.f, 0.f, 0.f};
+        if (a.epi == EPI_BN_ADD_RELU) {
+            const float4 rv = *reinterpret_cast<const float4 *>(a.res + o);
+            r[0] = rv.x;
+            r[1] = rv.y;
+            r[2] = rv.z;
+            r[3] = rv.w;
+        }
+        float f[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            f[j] = fmaf(acc0[i][j], sc0[j], sh0[j]);
+            if (nparts == 2) f[j] += fmaf(acc1[i][j], sc1[j], sh1[j]);
+            f[j] = fmaxf(f[j] + r[j], a.relu_lo);
+        }
+        *reinterpret_cast<float4 *>(a.out + o) = make_float4(f[0], f[1], f[2], f[3]);
+    }
+}
+
 }  // namespace
 
 cudaError_t launch_stem_bf16(const uint16_t *in, const float *w, int cin_full, const float *scale, const float *shift,
@@ -397,6 +528,12 @@ cudaError_t launch_scatter(const void *src, const uint32_t *idx, int n, size_t r
 }
 cudaError_t launch_conv_f32(const ConvF32Args &a, cudaStream_t s) {
     const long npix = static_cast<long>(a.B) * a.Ho * a.Wo;
+    static const bool direct = getenv("SLIM_F32_DIRECT") != nullptr;   // A/B: the direct-conv kernel
+    if (!direct && a.c_in % kGK == 0 && (a.epi != EPI_BN_PROJ_RELU || a.c_in1 % kGK == 0) && a.c_out % 16 == 0) {
+        dim3 grid(static_cast<unsigned>((npix + kGM - 1) / kGM), (a.c_out + kGN - 1) / kGN);
+        conv_f32_gemm_kernel<<<grid, kGThreads, 0, s>>>(a);
+        return cudaGetLastError();
+    }
     dim3 grid(static_cast<unsigned>((npix + 63) / 64), (a.c_out + 31) / 32);
     conv_f32_kernel<<<grid, kF32Threads, 0, s>>>(a);
     return cudaGetLastError();
