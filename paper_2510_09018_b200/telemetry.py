@@ -132,16 +132,27 @@ class TelemetryExchange:
         self.send = torch.zeros(RECORD_LEN, dtype=torch.float32, device=self.device)
         self.recv = torch.zeros(self.world * RECORD_LEN, dtype=torch.float32, device=self.device)
         self.stream = torch.cuda.Stream(device=self.device) if str(self.device).startswith("cuda") else None
+        # pinned staging ring: a pageable H2D copy would block the host until the side stream (which
+        # waits for the step) reaches it, serialising the host's launches with the GPU every tick
+        self._ring = [torch.zeros(RECORD_LEN, dtype=torch.float32).pin_memory() for _ in range(4)] \
+            if self.stream is not None else None
+        self._ev = [torch.cuda.Event() for _ in range(4)] if self.stream is not None else None
+        self._k = 0
 
     def tick(self, record: np.ndarray, wait: bool = False):
         """Start the all-gather of this rank's record; returns a handle (or the gathered [world, 8] array)."""
         import torch
         rec = torch.from_numpy(np.asarray(record, np.float32))
         if self.stream is not None:
+            i = self._k % len(self._ring)
+            self._k += 1
+            self._ev[i].synchronize()          # the copy that last read this staging buffer is done
+            self._ring[i].copy_(rec)
             cur = torch.cuda.current_stream(self.device)
             self.stream.wait_stream(cur)
             with torch.cuda.stream(self.stream):
-                self.send.copy_(rec, non_blocking=True)
+                self.send.copy_(self._ring[i], non_blocking=True)
+                self._ev[i].record(self.stream)
                 work = self.dist.all_gather_into_tensor(self.recv, self.send, group=self.group, async_op=True)
         else:
             self.send.copy_(rec)
