@@ -1,6 +1,6 @@
 """Per-launch device times of the bench chain (slim_profile_*, CUDA events per launch, no PDL).
 
-    python tools/layer_times.py [B] [reps] [bn|gn]
+    python tools/layer_times.py [B] [reps] [bn|gn] [bf16|fp32]
 """
 import os
 import sys
@@ -17,8 +17,9 @@ import paper_2510_09018_b200 as slim  # noqa: E402
 B = int(sys.argv[1]) if len(sys.argv) > 1 else 128
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 20
 norm = sys.argv[3] if len(sys.argv) > 3 else "bn"
-net = slim.SlimNet(synth.make_weights(), synth.make_bn(), max_batch=B, norm=norm)
-x = torch.from_numpy(synth.make_images(B)).to(torch.bfloat16).cuda()
+dtype = sys.argv[4] if len(sys.argv) > 4 else "bf16"
+net = slim.SlimNet(synth.make_weights(), synth.make_bn(), max_batch=B, norm=norm, dtype=dtype)
+x = torch.from_numpy(synth.make_images(B)).to(torch.bfloat16 if dtype == "bf16" else torch.float32).cuda()
 for r in (0.25, 0.5, 0.75, 1.0):
     for _ in range(5):
         net.forward_chain(x, (r,) * 4)
