@@ -43,6 +43,21 @@ def _peaks():
     return dict(hbm=6650.0, bf16=1590.0, bf16_sus=1400.0, src="fallback (B200_PROFILING.md)")
 
 
+def sm_shares(widths, spec: str):
+    """Per-width SM shares for the concurrent width instances (slim_set_sm_share).  auto: share(r) =
+    0.1 + 0.45 r, clamped to (0, 1] (fitted to the B=128 sweep in profiles/r01_sm_share_sweep.txt:
+    0.21 / 0.33 / 0.44 / 0.55 of the SMs for r = .25 / .5 / .75 / 1 -- the shares overlap, their sum is
+    1.5; 1.18-1.20 M images/s vs 0.88 M with every kernel on all SMs); none: every width may use all
+    SMs; else a comma list, one share per width."""
+    if spec == "none":
+        return {r: 1.0 for r in widths}
+    if spec == "auto":
+        return {r: min(1.0, max(0.05, 0.1 + 0.45 * r)) for r in widths}
+    vals = [float(v) for v in spec.split(",")]
+    assert len(vals) == len(widths), "--sm-share needs one value per width"
+    return dict(zip(widths, vals))
+
+
 def _dist():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -166,6 +181,13 @@ def run_ours(args):
         for r in WIDTHS:
             stream.wait_stream(streams[r])
 
+    shares = sm_shares(WIDTHS, "none" if args.sequential else args.sm_share)
+
+    def set_shares(sh):
+        for r in WIDTHS:
+            slim.slim_set_sm_share(net.ctx, r, sh[r])
+
+    set_shares(shares)
     for _ in range(args.warmup):
         flush.zero_()
         step()
@@ -207,10 +229,12 @@ def run_ours(args):
     clocks = sampler.summary()
     energy = ((e1 - e0) / 1e3 / (imgs_per_step * K)) if (e0 is not None and e1 is not None) else None
 
-    # ---------------- per-width images/s: each width's chain alone (L2 flushed before it)
+    # ---------------- per-width images/s: each width's chain alone (L2 flushed before it), on all SMs
+    set_shares({r: 1.0 for r in WIDTHS})
     KW = max(1, min(K, args.profile_steps * 4))
     width_ms = []
     for r in WIDTHS:
+        chain(r, stream)   # (re)capture the graph outside the timed events
         evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(KW)]
         for k in range(KW):
             flush.zero_()
@@ -263,6 +287,11 @@ def run_ours(args):
         "algorithmic_flops_per_launch": D["flops"] / D["n"], "algorithmic_bytes_per_launch": D["bytes"] / D["n"],
         "traffic": _ncu_traffic() if args.dtype == "bf16" else None,
     })
+    # the concurrent step as a whole: all algorithmic FLOPs of a step / the device-timed step
+    step_flops = sum(rc["flops"] for rc in recs) / KP
+    roof["step_aggregate"] = {"tflops": step_flops / (total_max_ms / K / 1e3) / 1e12,
+                              "frac": step_flops / (total_max_ms / K / 1e3) / 1e12 / peaks["bf16"],
+                              "note": "all kernels of a step (concurrent width instances on SM shares) / step time"}
 
     # ---------------- e2e through the public API with host buffers
     # Every step copies its images from pinned host memory and reads its logits back.  As a
@@ -275,6 +304,7 @@ def run_ours(args):
     ev_ready = {r: [torch.cuda.Event(), torch.cuda.Event()] for r in WIDTHS}
     ev_free = {r: [torch.cuda.Event(), torch.cuda.Event()] for r in WIDTHS}
     KE = max(1, min(K, args.e2e_steps))
+    set_shares(shares)
     for _ in range(2):   # warm both input buffers' graphs
         for r in WIDTHS:
             for b in range(2):
@@ -324,7 +354,8 @@ def run_ours(args):
                        "parallelism": f"dp{world} (independent per-GPU batches)",
                        "l2": "flushed (256 MiB write) before every timed step", "graphs": not args.no_graph,
                        "instances": "sequential" if args.sequential else
-                                    f"{len(WIDTHS)} width instances, one CUDA stream each, run concurrently"},
+                                    f"{len(WIDTHS)} width instances, one CUDA stream each, run concurrently",
+                       "sm_share": {str(r): v for r, v in shares.items()}},
             "per_width_images_per_s": per_width,
             "per_width_ms_per_batch": {str(r): width_ms[i] / KW for i, r in enumerate(WIDTHS)},
             "roofline": roof,
@@ -631,6 +662,8 @@ def main(argv=None):
     ap.add_argument("--requests", type=int, default=1024, help="stream: requests per rank per step")
     ap.add_argument("--bmax", type=int, default=256, help="stream: B_max of the key batching")
     ap.add_argument("--policy", default="random", help="stream: routing policy (random | slim | table_rr)")
+    ap.add_argument("--sm-share", default="auto",
+                    help="cfg2: SM shares of the concurrent width instances (auto | none | comma list per width)")
     ap.add_argument("--dtype", choices=("bf16", "fp32"), default="bf16",
                     help="cfg2: bf16 storage + fp32 accumulate (tcgen05, default) or the FP32/TF32-off mode (SIMT FFMA)")
     ap.add_argument("--widths", type=float, nargs="+", default=list(WIDTHS),

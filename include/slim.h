@@ -299,6 +299,14 @@ SLIM_API slim_status slim_exec_run(slim_exec *x, const void *images, const float
  * bake in the buffer addresses; loading/unloading a segment drops them. */
 SLIM_API slim_status slim_set_graph_mode(slim_ctx *ctx, int enable);
 
+/* SM partitioning for concurrent width instances: every persistent kernel this context launches
+ * for width r uses at most round(share * num_SMs) CTAs (share in (0,1]; default 1 = all SMs).
+ * At small batches the kernels are latency chains that each occupy every SM with one CTA, so
+ * instances of different widths on different streams serialise kernel by kernel; disjoint SM
+ * shares let them run side by side.  Synchronises the device and drops the
+ * captured graphs.  SLIM_EINVAL if r is not a configured width or share is outside (0,1]. */
+SLIM_API slim_status slim_set_sm_share(slim_ctx *ctx, float r, float share);
+
 /* Per-launch profiling: while on, every kernel launch is bracketed by CUDA
  * events on its stream and described by its algorithmic work (SURVEY §8(d):
  * sliced FLOPs = 2*MACs; bytes = layer-materialised traffic: input, weights,

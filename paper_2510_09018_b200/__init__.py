@@ -146,6 +146,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "slim_channels": (_I, [_F, _I]),
         "slim_act_channels": (_I, [_F, _I]),
         "slim_set_graph_mode": (_I, [_VP, _I]),
+        "slim_set_sm_share": (_I, [_VP, _F, _F]),
         "slim_profile_begin": (_I, [_VP, _I]),
         "slim_profile_end": (_I, [_VP, ctypes.POINTER(slim_profile_record), _I, ctypes.POINTER(_I)]),
         "slim_sched_default_knobs": (None, [ctypes.POINTER(slim_sched_knobs)]),
@@ -175,7 +176,7 @@ EXPORTED = ("slim_create", "slim_destroy", "slim_default_config", "slim_load_seg
             "slim_segment_loaded", "slim_segment_bytes", "slim_forward", "slim_forward_workspace_bytes",
             "slim_forward_ws", "slim_chain_workspace_bytes", "slim_forward_chain", "slim_pack", "slim_launch",
             "slim_gather", "slim_scatter", "slim_last_error", "slim_last_error_msg", "slim_status_str", "slim_version",
-            "slim_launch_count", "slim_num_sms", "slim_channels", "slim_act_channels", "slim_set_graph_mode", "slim_profile_begin",
+            "slim_launch_count", "slim_num_sms", "slim_channels", "slim_act_channels", "slim_set_graph_mode", "slim_set_sm_share", "slim_profile_begin",
             "slim_profile_end", "slim_sched_default_knobs", "slim_sched_create", "slim_sched_destroy",
             "slim_sched_enqueue", "slim_sched_next", "slim_sched_complete", "slim_sched_unload_idle",
             "slim_sched_queue_len", "slim_sched_instances", "slim_exec_create", "slim_exec_destroy", "slim_exec_run")
@@ -363,6 +364,10 @@ def slim_act_channels(r: float, C: int) -> int:
 
 def slim_set_graph_mode(ctx, enable: bool):
     _check(ctx, load_library().slim_set_graph_mode(ctx, int(bool(enable))))
+
+
+def slim_set_sm_share(ctx, r: float, share: float):
+    _check(ctx, load_library().slim_set_sm_share(ctx, r, share))
 
 
 def slim_profile_begin(ctx, max_launches: int):

@@ -87,6 +87,7 @@ struct slim_ctx {
     std::mutex graph_mu;
     std::unordered_map<std::string, GraphEntry> graphs;
     unsigned long long *trace = nullptr;   // diagnostics: SLIM_CONV_TRACE -> per-CTA timestamps of the last conv
+    float sm_share[8] = {1.f, 1.f, 1.f, 1.f, 1.f, 1.f, 1.f, 1.f};   // per width: persistent-grid cap / num_SMs
 };
 
 namespace slim {
@@ -353,6 +354,28 @@ void conv_work(const slim_config &c, const ConvCall &cc, int ri, int B, int Ho, 
     *bytes = b;
 }
 
+// SM partitioning between concurrent width instances (slim_set_sm_share): the persistent grids of a
+// width's kernels are capped at share * num_SMs, so the latency-bound kernels of several width
+// instances running on their own streams occupy disjoint SM sets instead of each taking all SMs and
+// serialising at kernel granularity.  SLIM_GRID_CAP="f0,f1,..." (per width index) overrides for A/B.
+int grid_cap(const slim_ctx *ctx, int ri, int grid) {
+    static float env_frac[kMaxW] = {0};
+    static const bool env_set = [] {
+        const char *e = getenv("SLIM_GRID_CAP");
+        if (!e || !*e) return false;
+        for (int i = 0; i < kMaxW; ++i) env_frac[i] = 1.f;
+        for (int i = 0; e && *e && i < kMaxW; ++i) {
+            env_frac[i] = static_cast<float>(atof(e));
+            e = strchr(e, ',');
+            if (e) ++e;
+        }
+        return true;
+    }();
+    const float f = env_set ? env_frac[ri] : ctx->sm_share[ri];
+    const int cap = static_cast<int>(f * ctx->num_sms + 0.5f);
+    return (cap >= 1 && cap < grid) ? cap : grid;
+}
+
 // Stride-1 3x3 conv with one halo load per channel chunk (kernels_halo.cu).  Returns
 // SLIM_EUNSUPPORTED (nothing launched) when the layer does not fit its constraints.
 slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, int ri, int B, bool allow_small = true) {
@@ -587,6 +610,7 @@ slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, i
     const int total = a.m_tiles * a.n_tiles;
     int grid = ctx->num_sms * (two ? 2 : 1);
     if (grid > total) grid = total;
+    grid = grid_cap(ctx, ri, grid);
     double flops, bytes;
     conv_work(c, cc, ri, B, H, W, &flops, &bytes);
     if (ctx->trace) cudaMemsetAsync(ctx->trace, 0, 3584 * sizeof(unsigned long long), st);   // diagnostics (stem: 3584..)
@@ -908,6 +932,7 @@ slim_status conv_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, int ri
     const int total = a.m_tiles * a.n_tiles;
     int grid = ctx->num_sms * per_sm;
     if (grid > total) grid = total;
+    grid = grid_cap(ctx, ri, grid);
     // A-tile multicast: a cluster of mc CTAs (<= 8, dividing n_tiles) shares each M tile
     static const bool no_mc = getenv("SLIM_NO_MC") != nullptr;
     a.mc = 1;
@@ -1099,6 +1124,7 @@ slim_status run_segment(slim_ctx *ctx, int seg, int ri_prev, int ri, int B, cons
             // persistent: one CTA per SM, halo fetch / im2col / MMA / store of consecutive tiles overlap
             int grid = ctx->num_sms;
             if (grid > sa.m_tiles) grid = sa.m_tiles;
+            grid = grid_cap(ctx, ri, grid);
             LaunchProf prof(ctx, st);
             e = launch_stem_umma(sa, tIn, tOut, grid, st, ctx->pdl && !ctx->prof_on);
             prof.done(SLIM_K_STEM, 0, 0, r, r, B, flops, bytes);
@@ -1698,6 +1724,17 @@ slim_status slim_launch(slim_ctx *ctx, const slim_launch_desc *d, const uint32_t
         in = slab;
     }
     return slim_forward_ws(ctx, d->seg, d->r_prev, d->r, d->batch, in, out, ws, ws_bytes, stream);
+}
+
+slim_status slim_set_sm_share(slim_ctx *ctx, float r, float share) {
+    if (!ctx) return SLIM_EINVAL;
+    const int ri = width_index(ctx->cfg, r);
+    if (ri < 0 || !(share > 0.f && share <= 1.f)) return fail(ctx, SLIM_EINVAL, "sm_share: bad width or share");
+    cudaSetDevice(ctx->device);
+    cudaDeviceSynchronize();   // captured graphs bake the grid sizes: drop them once nothing is in flight
+    clear_graphs(ctx);
+    ctx->sm_share[ri] = share;
+    return SLIM_OK;
 }
 
 slim_status slim_set_graph_mode(slim_ctx *ctx, int enable) {

@@ -411,3 +411,24 @@ def test_kernel_variant_parity(env):
                          cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     assert out.returncode == 0, out.stderr[-2000:]
     assert float(out.stdout.strip().splitlines()[-1]) <= TAU_BF16, env
+
+
+def test_sm_share_is_bit_exact(params):
+    """SM partitioning (slim_set_sm_share) only changes which CTA computes which tile: bit-exact."""
+    w, bn = params
+    n = slim.SlimNet(w, bn, max_batch=64)
+    x = _dev(synth.make_images(64, offset=31))
+    tup = (0.25, 1.0, 0.5, 0.75)
+    full = n.forward_chain(x, tup).clone()
+    for r, sh in ((0.25, 0.05), (1.0, 0.2), (0.5, 0.33), (0.75, 0.6)):
+        slim.slim_set_sm_share(n.ctx, r, sh)
+    slim.slim_set_graph_mode(n.ctx, True)
+    part = n.forward_chain(x, tup).clone()
+    part2 = n.forward_chain(x, tup).clone()
+    with pytest.raises(slim.SlimError):
+        slim.slim_set_sm_share(n.ctx, 0.3, 0.5)
+    with pytest.raises(slim.SlimError):
+        slim.slim_set_sm_share(n.ctx, 0.5, 0.0)
+    n.close()
+    torch.testing.assert_close(part, full, rtol=0, atol=0)
+    torch.testing.assert_close(part2, full, rtol=0, atol=0)
