@@ -439,7 +439,11 @@ def run_stream(args):
                 return out
         ex = _Adapter()
     else:
-        ex = StreamExecutor(net, n_max=len(mine), B_max=args.bmax, device=dev)
+        ex = StreamExecutor(net, n_max=len(mine), B_max=args.bmax, device=dev, lanes=args.lanes)
+        if args.lanes > 1:   # one lane per width: partition the SMs by width as in cfg2
+            cw = tuple(net.cfg.widths[i] for i in range(net.cfg.n_widths))
+            for r, sh in sm_shares(cw, args.sm_share).items():
+                slim.slim_set_sm_share(net.ctx, r, sh)
     telem = TelemetryExchange(device=dev) if world > 1 else None
     stream = torch.cuda.current_stream(dev)
     for _ in range(args.warmup):
@@ -479,6 +483,7 @@ def run_stream(args):
             "config": {"workload": f"{'CFG5' if world > 1 else 'CFG4'}: mixed-width request stream "
                                    f"(width tuples of Tables I-II), greedy (segment, w_req, w_prev) batching, "
                                    f"B_max={args.bmax}, routing={args.policy}, executor={args.executor}"
+                                   + (f", lanes={args.lanes}" if not (greedy or native) else "")
                                    + (f" (Alg. 1: Q_th={args.q_th}, N_new={args.n_new})" if greedy or native else ""),
                        "requests_per_rank": args.requests, "parallelism": f"dp{world} routed"},
             "batches_per_step_rank0": len(batches),
@@ -674,6 +679,7 @@ def main(argv=None):
     ap.add_argument("--executor", choices=("stream", "greedy", "native"), default="stream",
                     help="stream: whole-stream packing per segment (graph replay); greedy: Alg. 1 executor "
                          "(native scheduler, per-instance streams)")
+    ap.add_argument("--lanes", type=int, default=4, help="stream: concurrent lanes (streams) per segment, one per width")
     ap.add_argument("--q-th", type=int, default=512, help="greedy: Alg. 1 scale trigger Q_th")
     ap.add_argument("--n-new", type=int, default=2, help="greedy: Alg. 1 scale cap N_new")
     ap.add_argument("--norm", choices=("bn", "gn"), default="bn",

@@ -118,20 +118,24 @@ __global__ void __launch_bounds__(gn_max_threads<T>(), sizeof(T) == 2 ? (TWO ? 2
     __shared__ float gsum[2][kGnMaxCh / 8];
     __shared__ float stat[2][2][kGnMaxCh / 8];          // [y|yp][mean|rstd][local group]
     __shared__ float coef[2][2][kGnMaxCh];              // [y|yp][A|Bc] per channel of the slice
-    const int n = blockIdx.y;
-    const int ch0 = blockIdx.x * a.gpc * a.cpg;         // first channel of this CTA's slice
     const int V = a.gpc * a.cpg / VE, vpg = a.cpg / VE;
     const int t = threadIdx.x, v = t % V, k = blockDim.x / V;
     constexpr bool two = TWO;
-    const size_t img = static_cast<size_t>(n) * a.HW * a.C;
-    const size_t base = img + ch0 + v * VE;
     const float inv_cnt = 1.f / (static_cast<float>(a.HW) * a.cpg);
     const int p0 = t / V;
+    const int slices = a.C / (a.gpc * a.cpg);
 
     // programmatic dependent launch: the index math above overlaps the producing conv's tail;
     // dependents may start their prologue now (their own wait covers this grid's completion)
     asm volatile("griddepcontrol.wait;" ::: "memory");
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+
+    // persistent over (image, slice) items: the grid may be capped (SM share of this width)
+    for (int item = blockIdx.x; item < a.B * slices; item += gridDim.x) {
+    const int n = item / slices;
+    const int ch0 = (item - n * slices) * a.gpc * a.cpg;   // first channel of this CTA's slice
+    const size_t img = static_cast<size_t>(n) * a.HW * a.C;
+    const size_t base = img + ch0 + v * VE;
 
     // the slice into registers: pixels p0, p0 + k, ... (< kGnPPT of them), all loads in flight
     uint4 q0[kGnPPT], q1[TWO ? kGnPPT : 1];
@@ -234,6 +238,7 @@ __global__ void __launch_bounds__(gn_max_threads<T>(), sizeof(T) == 2 ? (TWO ? 2
         }
         store_vec(static_cast<T *>(a.out) + base + static_cast<size_t>(p) * a.C, z);
     }
+    }   // items
 }
 
 }  // namespace
@@ -260,7 +265,8 @@ cudaError_t launch_gn(const GnArgs &a, bool fp32, cudaStream_t s, bool pdl) {
     if (V * k > (fp32 ? gn_max_threads<float>() : gn_max_threads<uint16_t>()) || (a.HW + k - 1) / k > kGnPPT)
         return cudaErrorInvalidValue;
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(a.C / (a.gpc * a.cpg), a.B);
+    const int items = a.B * (a.C / (a.gpc * a.cpg));
+    cfg.gridDim = dim3(a.max_ctas > 0 && a.max_ctas < items ? a.max_ctas : items);
     cfg.blockDim = dim3(V * k);
     cfg.stream = s;
     cudaLaunchAttribute attr[1];

@@ -358,7 +358,7 @@ void conv_work(const slim_config &c, const ConvCall &cc, int ri, int B, int Ho, 
 // width's kernels are capped at share * num_SMs, so the latency-bound kernels of several width
 // instances running on their own streams occupy disjoint SM sets instead of each taking all SMs and
 // serialising at kernel granularity.  SLIM_GRID_CAP="f0,f1,..." (per width index) overrides for A/B.
-int grid_cap(const slim_ctx *ctx, int ri, int grid) {
+int grid_cap(const slim_ctx *ctx, int ri, int grid, int seg = -1) {
     static float env_frac[kMaxW] = {0};
     static const bool env_set = [] {
         const char *e = getenv("SLIM_GRID_CAP");
@@ -371,7 +371,19 @@ int grid_cap(const slim_ctx *ctx, int ri, int grid) {
         }
         return true;
     }();
-    const float f = env_set ? env_frac[ri] : ctx->sm_share[ri];
+    float f = env_set ? env_frac[ri] : ctx->sm_share[ri];
+    static float seg_scale[4] = {1.f, 1.f, 1.f, 1.f};   // experiment: SLIM_SEG_CAP_SCALE="a,b,c,d"
+    static const bool seg_parsed = [] {
+        const char *e = getenv("SLIM_SEG_CAP_SCALE");
+        for (int i = 0; e && *e && i < 4; ++i) {
+            seg_scale[i] = static_cast<float>(atof(e));
+            e = strchr(e, ',');
+            if (e) ++e;
+        }
+        return true;
+    }();
+    (void)seg_parsed;
+    if (seg >= 0 && seg < 4 && f < 1.f) f = f * seg_scale[seg] < 1.f ? f * seg_scale[seg] : 1.f;
     const int cap = static_cast<int>(f * ctx->num_sms + 0.5f);
     return (cap >= 1 && cap < grid) ? cap : grid;
 }
@@ -610,7 +622,7 @@ slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, i
     const int total = a.m_tiles * a.n_tiles;
     int grid = ctx->num_sms * (two ? 2 : 1);
     if (grid > total) grid = total;
-    grid = grid_cap(ctx, ri, grid);
+    grid = grid_cap(ctx, ri, grid, cc.seg);
     double flops, bytes;
     conv_work(c, cc, ri, B, H, W, &flops, &bytes);
     if (ctx->trace) cudaMemsetAsync(ctx->trace, 0, 3584 * sizeof(unsigned long long), st);   // diagnostics (stem: 3584..)
@@ -932,7 +944,7 @@ slim_status conv_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, int ri
     const int total = a.m_tiles * a.n_tiles;
     int grid = ctx->num_sms * per_sm;
     if (grid > total) grid = total;
-    grid = grid_cap(ctx, ri, grid);
+    grid = grid_cap(ctx, ri, grid, cc.seg);
     // A-tile multicast: a cluster of mc CTAs (<= 8, dividing n_tiles) shares each M tile
     static const bool no_mc = getenv("SLIM_NO_MC") != nullptr;
     a.mc = 1;
@@ -1057,6 +1069,11 @@ slim_status gn_apply(slim_ctx *ctx, cudaStream_t st, int seg, int layer, const D
     g.gpc = gn_groups_per_cta(B, g.HW, C, g.cpg, c.dtype == SLIM_FP32);
     g.eps = c.bn_eps;
     g.relu_lo = relu ? 0.f : -INFINITY;
+    {   // SM share of this width: gn_mult CTAs per SM of the share (persistent over items); 0 = uncapped
+        static const int gn_mult = getenv("SLIM_GN_CAP_MULT") ? atoi(getenv("SLIM_GN_CAP_MULT")) : 0;   // measured: uncapped 716k, x3 699k, x6 717k
+        const int cap = grid_cap(ctx, ri, 1 << 30, seg);
+        g.max_ctas = (gn_mult > 0 && cap < (1 << 30)) ? gn_mult * cap : 0;
+    }
     const double eb = static_cast<double>(elem_bytes(c));
     const double n = static_cast<double>(B) * H * H * C;
     const double flops = 8.0 * n * (yp ? 2 : 1);   // 2 statistics passes + apply, per input tensor
@@ -1124,7 +1141,7 @@ slim_status run_segment(slim_ctx *ctx, int seg, int ri_prev, int ri, int B, cons
             // persistent: one CTA per SM, halo fetch / im2col / MMA / store of consecutive tiles overlap
             int grid = ctx->num_sms;
             if (grid > sa.m_tiles) grid = sa.m_tiles;
-            grid = grid_cap(ctx, ri, grid);
+            grid = grid_cap(ctx, ri, grid, 0);
             LaunchProf prof(ctx, st);
             e = launch_stem_umma(sa, tIn, tOut, grid, st, ctx->pdl && !ctx->prof_on);
             prof.done(SLIM_K_STEM, 0, 0, r, r, B, flops, bytes);

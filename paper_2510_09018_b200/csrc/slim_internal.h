@@ -191,6 +191,7 @@ struct GnArgs {
     void *out;                     // may alias y
     int B, HW, C, cpg, gpc;        // cpg channels per group; gpc groups per CTA (divides C/cpg)
     float eps, relu_lo;            // relu_lo 0 = ReLU, -inf = none
+    int max_ctas;                  // persistent-grid cap (0 = one CTA per (image, slice))
 };
 int gn_groups_per_cta(int B, int HW, int C, int cpg, bool fp32);
 cudaError_t launch_gn(const GnArgs &a, bool fp32, cudaStream_t s, bool pdl);

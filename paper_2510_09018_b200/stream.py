@@ -25,7 +25,7 @@ from . import SlimNet, slim_act_channels, slim_forward_workspace_bytes, slim_lau
 
 
 class StreamExecutor:
-    def __init__(self, net: SlimNet, n_max: int, B_max: int = 256, device=None):
+    def __init__(self, net: SlimNet, n_max: int, B_max: int = 256, device=None, lanes: int = 1):
         self.net = net
         self.cfg = net.cfg
         self.n_max = n_max
@@ -44,11 +44,18 @@ class StreamExecutor:
         self.pools = [None] + [torch.empty(n_max * self.row_elems[s], dtype=self.adt, device=self.dev)
                                for s in range(1, 4)]
         self.logits = torch.empty(n_max, cfg.num_classes, dtype=torch.float32, device=self.dev)
-        self.slab = torch.empty(B_max * max(self.row_elems), dtype=self.adt, device=self.dev)
+        # lanes: batches of one segment with different keys are independent -- with lanes > 1 they
+        # run concurrently on their own streams (one lane per width; the context's per-width SM
+        # shares keep them side by side), joined before the next segment reads the pools
+        self.lanes = max(1, int(lanes))
         out_elems = max(max(self.row_elems[1:]), cfg.num_classes * 4 // self.eb)
-        self.out = torch.empty(B_max * out_elems, dtype=self.adt, device=self.dev)
         self.wsb = max(slim_forward_workspace_bytes(net.ctx, s, wmax, wmax, B_max) for s in range(4))
-        self.ws = torch.empty(self.wsb, dtype=torch.uint8, device=self.dev)
+        self.lane_buf = [(torch.empty(B_max * max(self.row_elems), dtype=self.adt, device=self.dev),
+                          torch.empty(B_max * out_elems, dtype=self.adt, device=self.dev),
+                          torch.empty(self.wsb, dtype=torch.uint8, device=self.dev)) for _ in range(self.lanes)]
+        self.slab, self.out, self.ws = self.lane_buf[0]
+        self.lane_streams = [torch.cuda.Stream(device=self.dev) for _ in range(self.lanes)] if self.lanes > 1 else []
+        self.widths = [cfg.widths[i] for i in range(cfg.n_widths)]
         self.order_h = torch.empty(4 * n_max, dtype=torch.int32).pin_memory()
         self.order_d = torch.empty(4 * n_max, dtype=torch.int32, device=self.dev)
         self._plan_key = None
@@ -84,16 +91,27 @@ class StreamExecutor:
             pool = images if s == 0 else self.pools[s]
             pool_row = self.row_elems[s] * self.eb
             base = s * n
+            if self.lanes > 1:   # fork: every lane starts after the previous segment's scatters
+                fork = torch.cuda.Event()
+                fork.record(st)
+                for ls in self.lane_streams:
+                    ls.wait_event(fork)
             for d in descs:
                 b, first = d["batch"], d["first"]
                 idx = self.order_d[base + first: base + first + b]
-                slim_launch(self.net.ctx, d, idx, pool, pool_row, self.slab, self.out, self.ws, self.wsb, st)
+                lane = self.widths.index(min(self.widths, key=lambda w: abs(w - d["r"]))) % self.lanes
+                slab, out, ws = self.lane_buf[lane]
+                ls = self.lane_streams[lane] if self.lanes > 1 else st
+                slim_launch(self.net.ctx, d, idx, pool, pool_row, slab, out, ws, self.wsb, ls)
                 if s < 3:
                     h = hw >> s
                     row = h * h * slim_act_channels(d["r"], cfg.base_channels[s]) * self.eb
-                    slim_scatter(self.net.ctx, self.out, idx, b, row, self.pools[s + 1],
-                                 self.row_elems[s + 1] * self.eb, st)
+                    slim_scatter(self.net.ctx, out, idx, b, row, self.pools[s + 1],
+                                 self.row_elems[s + 1] * self.eb, ls)
                 else:
-                    slim_scatter(self.net.ctx, self.out, idx, b, cfg.num_classes * 4, self.logits,
-                                 cfg.num_classes * 4, st)
+                    slim_scatter(self.net.ctx, out, idx, b, cfg.num_classes * 4, self.logits,
+                                 cfg.num_classes * 4, ls)
+            if self.lanes > 1:   # join before the next segment gathers from the pools
+                for ls in self.lane_streams:
+                    st.wait_stream(ls)
         return self.logits[:n]

@@ -301,16 +301,18 @@ def test_fp32_segment_parity(net32, ref, seg, r_prev, r):
 
 
 # ------------------------------------------------------------------ request stream (CFG4)
-def test_stream_executor_matches_per_request_chain(net):
+@pytest.mark.parametrize("lanes", [1, 4])
+def test_stream_executor_matches_per_request_chain(net, lanes):
     """Mixed-width stream: key batching per segment + gather/scatter; each request's logits are
-    bitwise the chain of its own tuple (batch independence makes grouping invisible)."""
+    bitwise the chain of its own tuple (batch independence makes grouping invisible); lanes = 4
+    runs a segment's batches concurrently on one stream per width."""
     from paper_2510_09018_b200.stream import StreamExecutor
     from paper_2510_09018_b200.router import TABLE_TUPLES
     rng = np.random.default_rng(21)
     n = 61
     tup = np.asarray([TABLE_TUPLES[i] for i in rng.integers(0, len(TABLE_TUPLES), n)], np.float32)
     x = synth.make_images(n, offset=21)
-    ex = StreamExecutor(net, n_max=64, B_max=8)
+    ex = StreamExecutor(net, n_max=64, B_max=8, lanes=lanes)
     got = ex.run(_dev(x), tup).clone()
     torch.cuda.synchronize()
     assert max(max(b) for b in ex.last_batches) <= 8
