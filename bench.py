@@ -406,9 +406,12 @@ def run_stream(args):
     net = slim.SlimNet(synth.make_weights(), synth.make_bn(), device=local, max_batch=args.bmax, norm=args.norm)
     greedy = args.executor == "greedy"
     native = args.executor == "native"
-    # (SM shares are not applied here: measured 361 k -> 236 k images/s for the native Alg. 1 loop,
-    # whose instances are mostly of the same width at a time)
-    slim.slim_set_graph_mode(net.ctx, True)   # Alg. 1: one graph per (key, batch size, instance buffers), reused across steps
+    if (greedy or native) and args.alg1_shares:   # opt-in: partition the SMs by width as in cfg2
+        for r, sh in sm_shares(tuple(net.cfg.widths[i] for i in range(net.cfg.n_widths)), args.sm_share).items():
+            slim.slim_set_sm_share(net.ctx, r, sh)
+    # Alg. 1 executors: eager launches by default -- their batches land on whichever instance is free, so
+    # (key, batch size, instance buffers) combinations keep changing and graph capture would dominate
+    slim.slim_set_graph_mode(net.ctx, not (greedy or native) or args.alg1_graphs)
     n_total = args.requests * world
     devs, tups, grps = router.route(n_total, world, args.policy)
     mine = router.shard(devs, rank)
@@ -526,7 +529,10 @@ def run_handoff(args):
     tuples = np.asarray(router.TABLE_TUPLES, np.float32)[g.integers(0, len(router.TABLE_TUPLES), n)]
     plan = handoff.plan_segments(n, world, args.seg_policy)
     x = torch.from_numpy(synth.make_images(n, offset=300)).to(torch.bfloat16).to(dev)
-    ex = handoff.HandoffExecutor(net, n, rank, world, B_max=args.bmax)
+    ex = handoff.HandoffExecutor(net, n, rank, world, B_max=args.bmax, lanes=args.lanes)
+    if args.lanes > 1:
+        for r, sh in sm_shares(tuple(net.cfg.widths[i] for i in range(net.cfg.n_widths)), args.sm_share).items():
+            slim.slim_set_sm_share(net.ctx, r, sh)
     for _ in range(args.warmup):
         ex.run(x, tuples, plan)
     torch.cuda.synchronize()
@@ -680,6 +686,8 @@ def main(argv=None):
                     help="stream: whole-stream packing per segment (graph replay); greedy: Alg. 1 executor "
                          "(native scheduler, per-instance streams)")
     ap.add_argument("--lanes", type=int, default=4, help="stream: concurrent lanes (streams) per segment, one per width")
+    ap.add_argument("--alg1-graphs", action="store_true", help="greedy/native: CUDA-graph replay per batch shape")
+    ap.add_argument("--alg1-shares", action="store_true", help="greedy/native: per-width SM shares (--sm-share)")
     ap.add_argument("--q-th", type=int, default=512, help="greedy: Alg. 1 scale trigger Q_th")
     ap.add_argument("--n-new", type=int, default=2, help="greedy: Alg. 1 scale cap N_new")
     ap.add_argument("--norm", choices=("bn", "gn"), default="bn",

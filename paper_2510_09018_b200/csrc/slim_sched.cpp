@@ -31,6 +31,15 @@ namespace {
 struct QEntry {
     slim_request r;
     double t_enq;
+    int64_t seq;   // global FIFO position (requeued batches get positions before every other entry)
+};
+
+// The FIFO queue Q, held as one FIFO per key (there are at most 4 + 16*3 keys): the head key is
+// the key whose oldest entry has the smallest sequence number, so a LOOP step costs O(keys + B)
+// instead of a pass over the whole queue; global FIFO order is the sequence order.
+struct KeyQ {
+    slim_request key;
+    std::deque<QEntry> q;
 };
 
 struct Inst {
@@ -59,7 +68,15 @@ struct slim_sched {
     slim_config cfg{};
     slim_sched_knobs k{};
     std::mutex mu;
-    std::deque<QEntry> q;
+    std::vector<KeyQ> keys;
+    int64_t next_seq = 0, front_seq = -1;
+    size_t total = 0;
+    KeyQ &key_queue(const slim_request &r) {
+        for (KeyQ &k : keys)
+            if (key_eq(k.key, r)) return k;
+        keys.push_back(KeyQ{r, {}});
+        return keys.back();
+    }
     std::vector<Inst> inst;
     int next_id = 0;
     size_t live_bytes() const {
@@ -122,7 +139,10 @@ slim_status slim_sched_enqueue(slim_sched *s, const slim_request *reqs, int n, d
             return SLIM_EINVAL;
     }
     std::lock_guard<std::mutex> g(s->mu);
-    for (int i = 0; i < n; ++i) s->q.push_back(QEntry{reqs[i], t_enq});
+    for (int i = 0; i < n; ++i) {
+        s->key_queue(reqs[i]).q.push_back(QEntry{reqs[i], t_enq, s->next_seq++});
+        ++s->total;
+    }
     return SLIM_OK;
 }
 
@@ -132,24 +152,17 @@ slim_status slim_sched_next(slim_sched *s, double now, float util, size_t vram_e
     std::lock_guard<std::mutex> g(s->mu);
     std::memset(act, 0, sizeof *act);
     act->inst = -1;
-    if (s->q.empty()) {   // l.3 "wait until Q non-empty": the caller waits
+    if (s->total == 0) {   // l.3 "wait until Q non-empty": the caller waits
         act->kind = SLIM_ACT_IDLE;
         return SLIM_OK;
     }
-    // l.3-4: head key, batch of up to B_max requests with that key (FIFO order kept)
-    const slim_request head = s->q.front().r;
-    std::vector<QEntry> batch, rest;
-    int key_count = 0;
-    for (const QEntry &e : s->q) {
-        if (key_eq(e.r, head)) {
-            ++key_count;
-            if (static_cast<int>(batch.size()) < s->k.B_max) {
-                batch.push_back(e);
-                continue;
-            }
-        }
-        rest.push_back(e);
-    }
+    // l.3-4: head key = the key of the oldest request; batch = its first B_max requests (FIFO order)
+    KeyQ *hq = nullptr;
+    for (KeyQ &k : s->keys)
+        if (!k.q.empty() && (!hq || k.q.front().seq < hq->q.front().seq)) hq = &k;
+    const slim_request head = hq->q.front().r;
+    const int key_count = static_cast<int>(hq->q.size());
+    const int nb = key_count < s->k.B_max ? key_count : s->k.B_max;
     act->seg = head.seg;
     act->w_req = head.w_req;
     act->w_prev = head.seg ? head.w_prev : 0.f;
@@ -168,11 +181,11 @@ slim_status slim_sched_next(slim_sched *s, double now, float util, size_t vram_e
         if (act->n_loaded) bi = static_cast<int>(s->inst.size()) - act->n_loaded;   // first new instance
     }
     if (bi < 0) {   // l.8-9: requeue B to the front of Q (batch order, then the rest)
-        s->q.clear();
-        for (const QEntry &e : batch) s->q.push_back(e);
-        for (const QEntry &e : rest) s->q.push_back(e);
+        const int64_t base = s->front_seq - nb + 1;
+        for (int i = 0; i < nb; ++i) hq->q[i].seq = base + i;
+        s->front_seq = base - 1;
         act->kind = SLIM_ACT_REQUEUE;
-        act->batch = static_cast<int>(batch.size());
+        act->batch = nb;
         return SLIM_OK;
     }
     // l.10: mark busy, hand the batch to the caller (RUNBATCH)
@@ -182,12 +195,14 @@ slim_status slim_sched_next(slim_sched *s, double now, float util, size_t vram_e
     act->kind = SLIM_ACT_RUN;
     act->inst = I.id;
     act->inst_w = I.w;
-    act->batch = static_cast<int>(batch.size());
-    for (size_t i = 0; i < batch.size(); ++i) {
-        slots[i] = batch[i].r.slot;
-        if (ids) ids[i] = batch[i].r.id;
+    act->batch = nb;
+    for (int i = 0; i < nb; ++i) {
+        const QEntry &e = hq->q.front();
+        slots[i] = e.r.slot;
+        if (ids) ids[i] = e.r.id;
+        hq->q.pop_front();
     }
-    s->q.assign(rest.begin(), rest.end());
+    s->total -= nb;
     return SLIM_OK;
 }
 
@@ -224,7 +239,7 @@ int slim_sched_unload_idle(slim_sched *s, double now, int *removed, int max_remo
 int slim_sched_queue_len(const slim_sched *s) {
     if (!s) return -1;
     std::lock_guard<std::mutex> g(const_cast<slim_sched *>(s)->mu);
-    return static_cast<int>(s->q.size());
+    return static_cast<int>(s->total);
 }
 
 int slim_sched_instances(const slim_sched *s, slim_instance *out, int max_out) {

@@ -66,7 +66,7 @@ class CollectiveTransport:
 class HandoffExecutor:
     """One rank's share of a segment-routed request stream on its GPU."""
 
-    def __init__(self, net, n_max: int, rank: int, world: int, B_max: int = 256):
+    def __init__(self, net, n_max: int, rank: int, world: int, B_max: int = 256, lanes: int = 1):
         import torch
         self.net, self.cfg, self.n_max, self.rank, self.world, self.B_max = net, net.cfg, n_max, rank, world, B_max
         cfg = self.cfg
@@ -79,11 +79,15 @@ class HandoffExecutor:
         self.pools = [None] + [torch.zeros(n_max * self.row_elems[s], dtype=self.adt, device=self.dev)
                                for s in range(1, 4)]
         self.logits = torch.zeros(n_max, cfg.num_classes, dtype=torch.float32, device=self.dev)
-        self.slab = torch.empty(B_max * max(self.row_elems), dtype=self.adt, device=self.dev)
-        self.out = torch.empty(B_max * max(max(self.row_elems[1:]), cfg.num_classes * 4 // self.eb),
-                               dtype=self.adt, device=self.dev)
         self.wsb = max(slim_forward_workspace_bytes(net.ctx, s, wmax, wmax, B_max) for s in range(4))
-        self.ws = torch.empty(self.wsb, dtype=torch.uint8, device=self.dev)
+        # lanes (as in stream.StreamExecutor): a segment's key batches on one stream per width
+        self.lanes = max(1, int(lanes))
+        self.lane_buf = [(torch.empty(B_max * max(self.row_elems), dtype=self.adt, device=self.dev),
+                          torch.empty(B_max * max(max(self.row_elems[1:]), cfg.num_classes * 4 // self.eb),
+                                      dtype=self.adt, device=self.dev),
+                          torch.empty(self.wsb, dtype=torch.uint8, device=self.dev)) for _ in range(self.lanes)]
+        self.lane_streams = [torch.cuda.Stream(device=self.dev) for _ in range(self.lanes)] if self.lanes > 1 else []
+        self.widths = [cfg.widths[i] for i in range(cfg.n_widths)]
         self.stats = dict(sent_rows=0, recv_rows=0, batches=0)
 
     def _plan(self, tuples: np.ndarray, dev: np.ndarray):
@@ -122,21 +126,31 @@ class HandoffExecutor:
 
     def compute(self, s: int, images, tuples: np.ndarray, dev: np.ndarray, stream=None):
         """Run segment s for the requests routed to this rank (key batching + RUNBATCH)."""
+        import torch
         cfg, hw = self.cfg, self.cfg.image_hw
         pool = images if s == 0 else self.pools[s]
+        main = stream if stream is not None else torch.cuda.current_stream(self.dev)
+        if self.lanes > 1:
+            fork = torch.cuda.Event()
+            fork.record(main)
+            for ls in self.lane_streams:
+                ls.wait_event(fork)
         for d, span in self._plan(np.asarray(tuples, np.float32), dev)[s][0]:
             b = d["batch"]
             slots = self._sl(span)
-            slim_launch(self.net.ctx, d, slots, pool, self.row_elems[s] * self.eb, self.slab, self.out, self.ws,
-                        self.wsb, stream)
+            lane = self.widths.index(min(self.widths, key=lambda w: abs(w - d["r"]))) % self.lanes
+            slab, out, ws = self.lane_buf[lane]
+            ls = self.lane_streams[lane] if self.lanes > 1 else main
+            slim_launch(self.net.ctx, d, slots, pool, self.row_elems[s] * self.eb, slab, out, ws, self.wsb, ls)
             if s < 3:
                 row = (hw >> s) ** 2 * slim_act_channels(d["r"], cfg.base_channels[s]) * self.eb
-                slim_scatter(self.net.ctx, self.out, slots, b, row, self.pools[s + 1], self.row_elems[s + 1] * self.eb,
-                             stream)
+                slim_scatter(self.net.ctx, out, slots, b, row, self.pools[s + 1], self.row_elems[s + 1] * self.eb, ls)
             else:
-                slim_scatter(self.net.ctx, self.out, slots, b, cfg.num_classes * 4, self.logits, cfg.num_classes * 4,
-                             stream)
+                slim_scatter(self.net.ctx, out, slots, b, cfg.num_classes * 4, self.logits, cfg.num_classes * 4, ls)
             self.stats["batches"] += 1
+        if self.lanes > 1:
+            for ls in self.lane_streams:
+                main.wait_stream(ls)
 
     def pack(self, s: int, dev: np.ndarray, stream=None):
         """Send buffer (uint8) of the rows leaving after segment s, and its per-destination byte counts."""

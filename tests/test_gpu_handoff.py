@@ -21,14 +21,15 @@ def net():
     n.close()
 
 
-@pytest.mark.parametrize("world,policy", [(2, "random"), (3, "random"), (2, "pipeline"), (4, "sticky")])
-def test_handoff_matches_chain(net, world, policy):
+@pytest.mark.parametrize("world,policy,lanes", [(2, "random", 1), (3, "random", 4), (2, "pipeline", 1),
+                                               (4, "sticky", 4)])
+def test_handoff_matches_chain(net, world, policy, lanes):
     n = 150
     g = np.random.default_rng(world)
     tuples = np.asarray(synth.TABLE_TUPLES, np.float32)[g.integers(0, 8, n)]
     x = torch.from_numpy(synth.make_images(n, offset=world)).to(torch.bfloat16).cuda()
     dev = handoff.plan_segments(n, world, policy, seed=world)
-    exs = [handoff.HandoffExecutor(net, n, r, world, B_max=64) for r in range(world)]
+    exs = [handoff.HandoffExecutor(net, n, r, world, B_max=64, lanes=lanes) for r in range(world)]
     got = handoff.run_local(exs, x, tuples, dev)
     exp = torch.empty_like(got)
     for t in {tuple(map(float, r)) for r in tuples}:

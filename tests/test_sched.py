@@ -207,7 +207,7 @@ class RefAlg1:
         return gone
 
 
-@pytest.mark.parametrize("seed", [1, 2, 3])
+@pytest.mark.parametrize("seed", [1, 2, 3, 4, 5, 6, 7, 8])
 def test_randomized_equivalence_with_alg1_transcription(cfg, seed):
     g = np.random.default_rng(seed)
     knobs = dict(B_max=int(g.integers(1, 6)), M_max_bytes=float(g.uniform(2e6, 4e7)), U_blk=0.8, t_idle_s=0.5,
