@@ -502,6 +502,66 @@ def run_stream(args):
     return 0
 
 
+def run_poisson(args):
+    """CFG4 latency variant (SPEC Poisson arrivals): an open-loop Poisson request
+    stream at --rate requests/s through the native Alg. 1 executor.  Reports completed
+    images/s and per-request latency percentiles (arrival -> segment-3 batch complete)."""
+    import numpy as np
+    import torch
+
+    import synth
+    import paper_2510_09018_b200 as slim
+    from paper_2510_09018_b200 import build as slim_build
+    from paper_2510_09018_b200 import router
+    from paper_2510_09018_b200.telemetry import NvmlSampler
+
+    world, rank, local = _dist()
+    if rank != 0:
+        return 0
+    torch.cuda.set_device(local)
+    slim_build.build()
+    net = slim.SlimNet(synth.make_weights(), synth.make_bn(), device=local, max_batch=args.bmax, norm=args.norm)
+    n = args.requests
+    g = np.random.Generator(np.random.PCG64([2510_09018, 5]))      # request-stream substream (+5)
+    tuples = np.asarray(router.TABLE_TUPLES, np.float32)[g.integers(0, len(router.TABLE_TUPLES), n)]
+    arrivals = np.cumsum(g.exponential(1.0 / args.rate, n))
+    x = torch.from_numpy(synth.make_images(n, offset=400)).to(torch.bfloat16).cuda()
+    slim.slim_set_graph_mode(net.ctx, args.alg1_graphs)
+    ex = slim.NativeExecutor(net, n_max=n, B_max=args.bmax, Q_th=args.q_th, N_new=args.n_new,
+                             M_max_bytes=args.m_max_gb * 1e9)
+    for _ in range(args.warmup):
+        ex.run(x, tuples, arrivals=arrivals)
+    sampler = NvmlSampler(local)
+    e0 = sampler.energy_mj()
+    sampler.start()
+    lat, spans, batches = [], [], 0
+    for _ in range(args.steps):
+        ex.run(x, tuples, arrivals=arrivals)
+        lat.append(ex.latency.copy())
+        spans.append(float(ex.done.max()))
+        batches += ex.stats["batches"]
+    sampler.stop()
+    e1 = sampler.energy_mj()
+    lat = np.concatenate(lat) * 1e3
+    clocks, energy = _clock_energy_json(sampler, e0, e1, n * args.steps)
+    print(json.dumps({
+        "metric": METRIC, "value": n * args.steps / sum(spans), "unit": "images/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * sum(spans) / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": f"CFG4 latency variant: open-loop Poisson arrivals at {args.rate:g} requests/s, width "
+                               f"tuples uniform over Tables I-II, native Alg. 1 executor, B_max={args.bmax}",
+                   "requests_per_step": n, "graphs": args.alg1_graphs, "M_max_GB": args.m_max_gb},
+        "offered_rate": args.rate,
+        "latency_ms": {"p50": float(np.percentile(lat, 50)), "p95": float(np.percentile(lat, 95)),
+                       "p99": float(np.percentile(lat, 99)), "mean": float(lat.mean())},
+        "mean_batch": 4.0 * n * args.steps / max(batches, 1),
+        "gpu_launches": None, "energy_j_per_image": energy, "clocks": clocks,
+    }))
+    ex.close()
+    net.close()
+    return 0
+
+
 def run_handoff(args):
     """NEXT-2: the mixed-width stream with per-SEGMENT routing (handoff.plan_segments): every
     rank runs the segments routed to it and hands activations to the next segment's rank with
@@ -669,7 +729,7 @@ def main(argv=None):
     ap.add_argument("--profile-steps", type=int, default=50)
     ap.add_argument("--e2e-steps", type=int, default=200)
     ap.add_argument("--json-out", default=None)
-    ap.add_argument("--workload", choices=("cfg2", "cfg1", "sweep", "stream", "handoff"), default="cfg2",
+    ap.add_argument("--workload", choices=("cfg2", "cfg1", "sweep", "stream", "handoff", "poisson"), default="cfg2",
                     help="cfg2 (default, BASELINE configs[1]); cfg1 = seg0 r=0.25 B=8; sweep = CFG3 batch sweep "
                          "(one JSON line per point); stream = CFG4/CFG5 mixed-width routed request stream")
     ap.add_argument("--requests", type=int, default=1024, help="stream: requests per rank per step")
@@ -685,6 +745,9 @@ def main(argv=None):
     ap.add_argument("--executor", choices=("stream", "greedy", "native"), default="stream",
                     help="stream: whole-stream packing per segment (graph replay); greedy: Alg. 1 executor "
                          "(native scheduler, per-instance streams)")
+    ap.add_argument("--rate", type=float, default=300_000.0, help="poisson: offered load, requests/s")
+    ap.add_argument("--m-max-gb", type=float, default=8.0,
+                    help="poisson: Alg. 1 VRAM cap M_max (GB) -- bounds the instances the executor scales up to")
     ap.add_argument("--lanes", type=int, default=4, help="stream: concurrent lanes (streams) per segment, one per width")
     ap.add_argument("--alg1-graphs", action="store_true", help="greedy/native: CUDA-graph replay per batch shape")
     ap.add_argument("--alg1-shares", action="store_true", help="greedy/native: per-width SM shares (--sm-share)")
@@ -700,6 +763,8 @@ def main(argv=None):
         return run_stream(args)
     if args.workload == "handoff":
         return run_handoff(args)
+    if args.workload == "poisson":
+        return run_poisson(args)
     if args.workload in ("cfg1", "sweep"):
         return run_points(args)
     return run_ours(args)

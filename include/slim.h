@@ -278,8 +278,12 @@ SLIM_API int slim_sched_instances(const slim_sched *s, slim_instance *out, int m
  * create: allocates the per-segment request pools for n_max requests; the scheduler
  * (B_max <= cfg.max_batch) stays owned by the caller.  run: images = device
  * [n][H][W][in_channels]; tuples = HOST float [n][4] (the width of each segment, each in
- * cfg.widths); logits = device fp32 [n][num_classes]; vram_external as in slim_sched_next;
- * the call returns when every request is done (stream: ordered before the first read). */
+ * cfg.widths); logits = device fp32 [n][num_classes]; vram_external as in slim_sched_next, to which
+ * the executor adds the buffers of its live instances (slab, out, workspace: M_max bounds scale-up);
+ * the call returns when every request is done (stream: ordered before the first read).
+ * arrival_s (host, n, ascending, may be NULL): open loop -- request i enters the queue once the
+ * loop's clock (s since the call began) reaches arrival_s[i]; NULL = all at t = 0 (closed loop).
+ * done_s (host, n, may be NULL): the clock when request i's segment-3 batch was seen complete. */
 typedef struct slim_exec slim_exec;
 typedef struct {
     int batches, loads, requeues, unloaded;
@@ -288,7 +292,8 @@ typedef struct {
 SLIM_API slim_status slim_exec_create(slim_ctx *ctx, slim_sched *sched, int n_max, int B_max, slim_exec **out);
 SLIM_API void slim_exec_destroy(slim_exec *x);
 SLIM_API slim_status slim_exec_run(slim_exec *x, const void *images, const float *tuples, int n, float *logits,
-                                   size_t vram_external, slim_exec_stats *stats, void *stream);
+                                   size_t vram_external, slim_exec_stats *stats, void *stream,
+                                   const double *arrival_s, double *done_s);
 
 /* ---- execution modes and profiling ------------------------------------- */
 

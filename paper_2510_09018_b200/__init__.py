@@ -162,7 +162,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "slim_sched_instances": (_I, [_VP, ctypes.POINTER(slim_instance), _I]),
         "slim_exec_create": (_I, [_VP, _VP, _I, _I, ctypes.POINTER(_VP)]),
         "slim_exec_destroy": (None, [_VP]),
-        "slim_exec_run": (_I, [_VP, _VP, ctypes.POINTER(_F), _I, _VP, _SZ, ctypes.POINTER(slim_exec_stats), _VP]),
+        "slim_exec_run": (_I, [_VP, _VP, ctypes.POINTER(_F), _I, _VP, _SZ, ctypes.POINTER(slim_exec_stats), _VP,
+                               ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -465,17 +466,24 @@ class NativeExecutor:
         self.n_max = n_max
         self.stats = {}
 
-    def run(self, images, tuples, logits=None, vram_external: int = 0, stream=None):
-        """images: device [n,H,W,C]; tuples: [n,4] widths.  Returns fp32 logits [n, classes]."""
+    def run(self, images, tuples, logits=None, vram_external: int = 0, stream=None, arrivals=None):
+        """images: device [n,H,W,C]; tuples: [n,4] widths.  Returns fp32 logits [n, classes].
+        arrivals: optional ascending arrival times (s) -- open loop; then self.done holds each
+        request's completion time (s, same clock) and self.latency = done - arrivals."""
         import torch
         t = np.ascontiguousarray(np.asarray(tuples, np.float32))
         n = t.shape[0]
         if logits is None:
             logits = torch.empty(n, self.net.cfg.num_classes, dtype=torch.float32, device=images.device)
         st = slim_exec_stats()
+        dp = ctypes.POINTER(ctypes.c_double)
+        arr = None if arrivals is None else np.ascontiguousarray(np.asarray(arrivals, np.float64))
+        done = np.zeros(n, np.float64)
         _check(self.net.ctx, load_library().slim_exec_run(
             self.h, _ptr(images), t.ctypes.data_as(ctypes.POINTER(ctypes.c_float)), n, _ptr(logits), vram_external,
-            ctypes.byref(st), _stream(stream)))
+            ctypes.byref(st), _stream(stream), None if arr is None else arr.ctypes.data_as(dp), done.ctypes.data_as(dp)))
+        self.done = done
+        self.latency = done - (arr if arr is not None else 0.0)
         self.stats = dict(batches=st.batches, loads=st.loads, requeues=st.requeues, unloaded=st.unloaded,
                           seconds=st.seconds)
         return logits

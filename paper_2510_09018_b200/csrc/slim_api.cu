@@ -88,6 +88,8 @@ struct slim_ctx {
     std::unordered_map<std::string, GraphEntry> graphs;
     unsigned long long *trace = nullptr;   // diagnostics: SLIM_CONV_TRACE -> per-CTA timestamps of the last conv
     float sm_share[8] = {1.f, 1.f, 1.f, 1.f, 1.f, 1.f, 1.f, 1.f};   // per width: persistent-grid cap / num_SMs
+    std::mutex tm_mu;                                        // encoded tensor-map cache (encode_map)
+    std::unordered_map<std::string, CUtensorMap> tm_cache;
 };
 
 namespace slim {
@@ -224,13 +226,39 @@ CUtensorMapSwizzle swizzle_for(int box_c) {   // box inner bytes = 2*box_c = the
     return box_c == 16 ? CU_TENSOR_MAP_SWIZZLE_32B : (box_c == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B);
 }
 
+// Encoded tensor maps are cached by their full argument list (eager launches re-encode the same
+// activation maps for every call on the same buffers; the cache takes that host cost off the
+// launch path of the executors).
 bool encode_map(slim_ctx *ctx, CUtensorMap *tm, const void *ptr, int rank, const cuuint64_t *dims,
                 const cuuint64_t *strides, const cuuint32_t *box, const cuuint32_t *es, bool swizzle = true) {
+    uint64_t key[1 + 1 + 5 + 4 + 5 + 5 + 1] = {};
+    key[0] = reinterpret_cast<uintptr_t>(ptr);
+    key[1] = static_cast<uint64_t>(rank);
+    for (int i = 0; i < rank; ++i) {
+        key[2 + i] = dims[i];
+        key[11 + i] = box[i];
+        key[16 + i] = es[i];
+    }
+    for (int i = 0; i + 1 < rank; ++i) key[7 + i] = strides[i];
+    key[21] = swizzle;
+    const std::string k(reinterpret_cast<const char *>(key), sizeof key);
+    {
+        std::lock_guard<std::mutex> g(ctx->tm_mu);
+        auto it = ctx->tm_cache.find(k);
+        if (it != ctx->tm_cache.end()) {
+            *tm = it->second;
+            return true;
+        }
+    }
     CUresult r = ctx->encode(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void *>(ptr), dims, strides, box,
                              es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                              swizzle ? swizzle_for(static_cast<int>(box[0])) : CU_TENSOR_MAP_SWIZZLE_NONE,
                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    return r == CUDA_SUCCESS;
+    if (r != CUDA_SUCCESS) return false;
+    std::lock_guard<std::mutex> g(ctx->tm_mu);
+    if (ctx->tm_cache.size() > 8192) ctx->tm_cache.clear();
+    ctx->tm_cache.emplace(k, *tm);
+    return true;
 }
 
 // Activation NHWC [B][H][W][C] bf16 as a 4-D map (C, W, H, B); box (box_c, bw, bh, bn), traversal

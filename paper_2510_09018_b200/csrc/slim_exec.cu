@@ -49,7 +49,7 @@ struct slim_exec {
     slim_sched *sched = nullptr;
     slim_config cfg{};
     int n_max = 0, B_max = 0;
-    size_t eb = 2, row_bytes[4] = {}, out_bytes = 0, wsb = 0;
+    size_t eb = 2, row_bytes[4] = {}, out_bytes = 0, wsb = 0, pool_bytes = 0;
     void *pools[4] = {};                       // pools[1..3]: per-request input rows of segments 1..3
     std::vector<Res *> free_res;
     std::unordered_map<int, Res *> inst_res;
@@ -109,6 +109,7 @@ slim_status slim_exec_create(slim_ctx *ctx, slim_sched *sched, int n_max, int B_
         const size_t b = slim_forward_workspace_bytes(ctx, s, wmax, wmax, B_max);
         x->wsb = b > x->wsb ? b : x->wsb;
     }
+    for (int s = 1; s < 4; ++s) x->pool_bytes += static_cast<size_t>(n_max) * x->row_bytes[s];
     for (int s = 1; s < 4; ++s)
         if (cudaMalloc(&x->pools[s], static_cast<size_t>(n_max) * x->row_bytes[s]) != cudaSuccess) {
             cudaGetLastError();
@@ -137,20 +138,30 @@ void slim_exec_destroy(slim_exec *x) {
 }
 
 slim_status slim_exec_run(slim_exec *x, const void *images, const float *tuples, int n, float *logits,
-                          size_t vram_external, slim_exec_stats *stats, void *stream) {
+                          size_t vram_external, slim_exec_stats *stats, void *stream, const double *arrival_s,
+                          double *done_s) {
     if (!x || !images || !tuples || !logits || n < 1 || n > x->n_max) return SLIM_EINVAL;
+    if (arrival_s)
+        for (int i = 1; i < n; ++i)
+            if (arrival_s[i] < arrival_s[i - 1]) return SLIM_EINVAL;   // arrivals in request order
     const slim_config &c = x->cfg;
     slim_exec_stats st{};
     // the inputs are ordered before the instance streams read them
     if (cudaStreamSynchronize(static_cast<cudaStream_t>(stream)) != cudaSuccess) return SLIM_ECUDA;
     const auto t0 = std::chrono::steady_clock::now();
     auto now = [&]() { return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count(); };
-    {
-        std::vector<slim_request> q(n);
-        for (int i = 0; i < n; ++i) q[i] = slim_request{static_cast<uint64_t>(i), 0, tuples[4 * i], 0.f, static_cast<uint32_t>(i)};
-        const slim_status s = slim_sched_enqueue(x->sched, q.data(), n, 0.0);
-        if (s) return s;
-    }
+    // open loop: request i enters Q (key (0, w_0)) once now >= arrival_s[i]; closed loop: all at t = 0
+    int admitted = 0;
+    std::vector<slim_request> arrive;
+    auto admit = [&](double t) -> slim_status {
+        arrive.clear();
+        while (admitted < n && (!arrival_s || arrival_s[admitted] <= t)) {
+            const int i = admitted++;
+            arrive.push_back(slim_request{static_cast<uint64_t>(i), 0, tuples[4 * i], 0.f, static_cast<uint32_t>(i)});
+        }
+        return arrive.empty() ? SLIM_OK : slim_sched_enqueue(x->sched, arrive.data(), static_cast<int>(arrive.size()), t);
+    };
+    auto arrival_due = [&]() { return admitted < n && arrival_s[admitted] <= now(); };
     std::vector<Pending> pending;
     std::vector<uint32_t> slots(x->B_max);
     std::vector<uint64_t> ids(x->B_max);
@@ -158,8 +169,13 @@ slim_status slim_exec_run(slim_exec *x, const void *images, const float *tuples,
     std::vector<slim_request> next_q;
     int finished = 0;
     while (finished < n) {
+        if (slim_status sa = admit(now())) return sa;
         slim_sched_action act;
-        slim_status s = slim_sched_next(x->sched, now(), -1.f, vram_external, &act, slots.data(), ids.data());
+        // VRAM_used for CANLOAD (l.14): the caller's figure + the buffers of the live instances (slab,
+        // out, workspace each), so M_max bounds the scale-up; buffers parked in the free list are reused
+        // by the next instance without a new allocation and are not counted
+        const size_t res_bytes = x->inst_res.size() * (2 * x->B_max * x->out_bytes + x->wsb);
+        slim_status s = slim_sched_next(x->sched, now(), -1.f, vram_external + res_bytes, &act, slots.data(), ids.data());
         if (s) return s;
         st.loads += act.n_loaded;
         if (act.kind == SLIM_ACT_RUN) {
@@ -201,7 +217,12 @@ slim_status slim_exec_run(slim_exec *x, const void *images, const float *tuples,
         }
         if (act.kind == SLIM_ACT_REQUEUE) st.requeues += 1;
         if (pending.empty()) {   // nothing in flight: only the unloader can free capacity
-            if (act.kind == SLIM_ACT_IDLE) return SLIM_EINVAL;   // queue empty with requests unfinished: cannot happen
+            if (act.kind == SLIM_ACT_IDLE) {
+                if (admitted >= n) return SLIM_EINVAL;   // queue empty with requests unfinished: cannot happen
+                while (!arrival_due()) {
+                }   // open loop: idle until the next arrival
+                continue;
+            }
             const int k = slim_sched_unload_idle(x->sched, now(), removed.data(), static_cast<int>(removed.size()));
             for (int i = 0; i < k && i < static_cast<int>(removed.size()); ++i) {
                 auto it = x->inst_res.find(removed[i]);
@@ -218,8 +239,9 @@ slim_status slim_exec_run(slim_exec *x, const void *images, const float *tuples,
             }
             continue;
         }
-        // wait for whichever in-flight batch finishes first, then release every finished batch
+        // wait for whichever in-flight batch finishes first (or a new arrival), then release the finished
         for (bool any = false; !any;) {
+            if (arrival_s && arrival_due()) break;
             for (const Pending &p : pending) {
                 const cudaError_t e = cudaEventQuery(p.res->event);
                 if (e == cudaSuccess) {
@@ -246,6 +268,8 @@ slim_status slim_exec_run(slim_exec *x, const void *images, const float *tuples,
                 if ((s = slim_sched_enqueue(x->sched, next_q.data(), static_cast<int>(next_q.size()), t))) return s;
             } else {
                 finished += p.batch;
+                if (done_s)
+                    for (uint64_t id : p.ids) done_s[id] = t;
             }
         }
         const int k = slim_sched_unload_idle(x->sched, now(), removed.data(), static_cast<int>(removed.size()));

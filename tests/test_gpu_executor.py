@@ -79,9 +79,29 @@ def test_native_executor_matches_per_request_chain(net, B_max, Q_th, N_new):
 def test_native_executor_vram_cap_and_unload(net):
     x, tuples = _stream(100, 3)
     big = max(slim.slim_segment_bytes(net.cfg, s, 1.0, 1.0) for s in range(4))
-    ex = slim.NativeExecutor(net, n_max=100, B_max=16, t_idle_s=0.0, M_max_bytes=float(1.2 * big))
+    # one instance's buffers: slab + out (16 rows of the widest activation row) + the widest workspace
+    per_inst = 2 * 16 * 32 * 32 * 64 * 2 + max(slim.slim_forward_workspace_bytes(net.ctx, s, 1.0, 1.0, 16)
+                                               for s in range(4))
+    ex = slim.NativeExecutor(net, n_max=100, B_max=16, t_idle_s=0.0, M_max_bytes=float(1.2 * (big + per_inst)))
     got = ex.run(x, tuples).clone()
     st = ex.stats
     ex.close()
     torch.testing.assert_close(got, _expected(net, x, tuples), rtol=0, atol=0)
     assert st["unloaded"] > 0 and st["batches"] >= 4
+
+
+def test_native_executor_open_loop_arrivals(net):
+    """Open loop (Poisson arrivals): same bits as the closed loop; every request completes after it
+    arrives, and requests arriving late cannot finish before they arrive."""
+    x, tuples = _stream(200, 23)
+    g = np.random.default_rng(4)
+    arrivals = np.cumsum(g.exponential(1.0 / 50_000.0, 200))       # ~4 ms trace
+    ex = slim.NativeExecutor(net, n_max=200, B_max=32)
+    got = ex.run(x, tuples, arrivals=arrivals).clone()
+    lat, done = ex.latency.copy(), ex.done.copy()
+    with pytest.raises(slim.SlimError):
+        ex.run(x, tuples, arrivals=arrivals[::-1].copy())          # arrivals must be ascending
+    ex.close()
+    torch.testing.assert_close(got, _expected(net, x, tuples), rtol=0, atol=0)
+    assert (lat > 0).all() and (done >= arrivals).all()
+    assert done.max() >= arrivals[-1]

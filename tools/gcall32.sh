@@ -1,0 +1,6 @@
+timeout 600 python -m pytest tests/test_gpu_executor.py -x -q 2>&1 | tail -2
+for rate in 100000 300000 500000 1000000; do
+timeout 300 python bench.py --workload poisson --rate $rate --requests 4096 --steps 5 --warmup 2 > /tmp/p.json 2>/tmp/p.err
+python -c "
+import json;d=json.loads(open('/tmp/p.json').read().strip().splitlines()[-1]);print('rate $rate', round(d['value']), d['latency_ms'], round(d['mean_batch'],1))" || tail -3 /tmp/p.err
+done
