@@ -451,6 +451,102 @@ __global__ void __launch_bounds__(kGThreads) conv_f32_gemm_kernel(const ConvF32A
     }
 }
 
+// Wider variant for layers without a projection: CTA tile 256 pixels x 64 channels, 8 x 8 register
+// tile per thread (64 FFMA per 4 LDS.128).
+constexpr int kWM = 256;
+__global__ void __launch_bounds__(kGThreads, 1) conv_f32_gemm256_kernel(const ConvF32Args a) {
+    __shared__ __align__(16) float As[2][kGK][kWM + 4];
+    __shared__ __align__(16) float Bs[2][kGK][kGN + 4];
+    const int tid = threadIdx.x;
+    const int tx = tid & 31, ty = tid >> 5;       // compute: pixels tx*8 .. +7, channels ty*8 .. +7
+    const long m0 = static_cast<long>(blockIdx.x) * kWM;
+    const int n0 = blockIdx.y * kGN;
+    const long npix = static_cast<long>(a.B) * a.Ho * a.Wo;
+    const long gp = m0 + tid;                      // A loader: one pixel, 16 channels
+    const bool pok = gp < npix;
+    const long gpp = pok ? gp : 0;
+    const int pn = static_cast<int>(gpp / (a.Ho * a.Wo)), poh = static_cast<int>((gpp / a.Wo) % a.Ho),
+              pw = static_cast<int>(gpp % a.Wo);
+    const int lb = tid >> 2, lbc = (tid & 3) * 4;  // B loader: channel lb, ci lbc .. +3
+    const int gco = n0 + lb;
+    const bool cok = gco < a.c_out;
+    const int H = a.H, W = a.W, cin = a.c_in, k = a.k, st = a.stride, pad = a.pad;
+    const int csteps = cin / kGK, steps = k * k * csteps;
+    float acc[8][8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+    float4 ra[4], rb;
+    auto load = [&](int s) {
+        const int tap = s / csteps, c0 = (s - tap * csteps) * kGK, kh = tap / k, kw = tap - kh * k;
+        const int ih = st * poh + kh - pad, iw = st * pw + kw - pad;
+        const bool ok = pok && ih >= 0 && ih < H && iw >= 0 && iw < W;
+        const float *xp = a.x + ((static_cast<size_t>(pn) * H + (ok ? ih : 0)) * W + (ok ? iw : 0)) * cin + c0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            ra[q] = ok ? __ldg(reinterpret_cast<const float4 *>(xp) + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+        const float *wp = a.w + ((static_cast<size_t>(cok ? gco : 0) * k + kh) * k + kw) * a.cin_full + c0 + lbc;
+        rb = cok ? __ldg(reinterpret_cast<const float4 *>(wp)) : make_float4(0.f, 0.f, 0.f, 0.f);
+    };
+    auto store = [&](int b) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            As[b][4 * q + 0][tid] = ra[q].x;
+            As[b][4 * q + 1][tid] = ra[q].y;
+            As[b][4 * q + 2][tid] = ra[q].z;
+            As[b][4 * q + 3][tid] = ra[q].w;
+        }
+        Bs[b][lbc + 0][lb] = rb.x;
+        Bs[b][lbc + 1][lb] = rb.y;
+        Bs[b][lbc + 2][lb] = rb.z;
+        Bs[b][lbc + 3][lb] = rb.w;
+    };
+    load(0);
+    store(0);
+    __syncthreads();
+#pragma unroll 1
+    for (int s = 0; s < steps; ++s) {
+        const int b = s & 1;
+        if (s + 1 < steps) load(s + 1);
+#pragma unroll
+        for (int kk = 0; kk < kGK; ++kk) {
+            const float4 a0 = *reinterpret_cast<const float4 *>(&As[b][kk][tx * 8]);
+            const float4 a1 = *reinterpret_cast<const float4 *>(&As[b][kk][tx * 8 + 4]);
+            const float4 b0 = *reinterpret_cast<const float4 *>(&Bs[b][kk][ty * 8]);
+            const float4 b1 = *reinterpret_cast<const float4 *>(&Bs[b][kk][ty * 8 + 4]);
+            const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+            const float bw[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+#pragma unroll
+                for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(av[i], bw[j], acc[i][j]);
+        }
+        if (s + 1 < steps) store(b ^ 1);
+        __syncthreads();
+    }
+    const int c = n0 + ty * 8;
+    if (c >= a.c_out) return;   // c_out is a multiple of 16: a thread's 8 channels are all valid or none
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const long p = m0 + tx * 8 + i;
+        if (p >= npix) break;
+        const size_t o = static_cast<size_t>(p) * a.c_out + c;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            float f[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int cc = c + 4 * h + j;
+                f[j] = fmaf(acc[i][4 * h + j], a.scale0[cc], a.shift0[cc]);
+                if (a.epi == EPI_BN_ADD_RELU) f[j] += a.res[o + 4 * h + j];
+                f[j] = fmaxf(f[j], a.relu_lo);
+            }
+            *reinterpret_cast<float4 *>(a.out + o + 4 * h) = make_float4(f[0], f[1], f[2], f[3]);
+        }
+    }
+}
+
 }  // namespace
 
 cudaError_t launch_stem_bf16(const uint16_t *in, const float *w, int cin_full, const float *scale, const float *shift,
@@ -529,6 +625,13 @@ cudaError_t launch_scatter(const void *src, const uint32_t *idx, int n, size_t r
 cudaError_t launch_conv_f32(const ConvF32Args &a, cudaStream_t s) {
     const long npix = static_cast<long>(a.B) * a.Ho * a.Wo;
     static const bool direct = getenv("SLIM_F32_DIRECT") != nullptr;   // A/B: the direct-conv kernel
+    static const bool narrow = getenv("SLIM_F32_GEMM128") != nullptr;   // A/B: the 128 x 64 tile only
+    if (!direct && !narrow && a.c_in % kGK == 0 && a.epi != EPI_BN_PROJ_RELU && a.c_out % 16 == 0 &&
+        npix >= 148L * kWM) {
+        dim3 grid(static_cast<unsigned>((npix + kWM - 1) / kWM), (a.c_out + kGN - 1) / kGN);
+        conv_f32_gemm256_kernel<<<grid, kGThreads, 0, s>>>(a);
+        return cudaGetLastError();
+    }
     if (!direct && a.c_in % kGK == 0 && (a.epi != EPI_BN_PROJ_RELU || a.c_in1 % kGK == 0) && a.c_out % 16 == 0) {
         dim3 grid(static_cast<unsigned>((npix + kGM - 1) / kGM), (a.c_out + kGN - 1) / kGN);
         conv_f32_gemm_kernel<<<grid, kGThreads, 0, s>>>(a);
