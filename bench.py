@@ -287,6 +287,12 @@ def run_ours(args):
         "algorithmic_flops_per_launch": D["flops"] / D["n"], "algorithmic_bytes_per_launch": D["bytes"] / D["n"],
         "traffic": _ncu_traffic() if args.dtype == "bf16" else None,
     })
+    # every kernel kind against its own roofline (per-launch algorithmic work / event-timed duration)
+    roof["by_kind"] = {k: {"launches": d["n"], "tflops": d["flops"] / (d["ms"] / 1e3) / 1e12,
+                           "gbs": d["bytes"] / (d["ms"] / 1e3) / 1e9,
+                           "frac_tensor": d["flops"] / (d["ms"] / 1e3) / 1e12 / peaks["bf16"],
+                           "frac_hbm": d["bytes"] / (d["ms"] / 1e3) / 1e9 / peaks["hbm"],
+                           "per_layer_roofline_frac": d["roof_ms"] / d["ms"]} for k, d in by_kind.items()}
     # the concurrent step as a whole: all algorithmic FLOPs of a step / the device-timed step
     step_flops = sum(rc["flops"] for rc in recs) / KP
     roof["step_aggregate"] = {"tflops": step_flops / (total_max_ms / K / 1e3) / 1e12,

@@ -189,6 +189,10 @@ def test_error_paths(net):
         slim.slim_forward(net.ctx, 0, 0.25, 0.25, 10_000, x, x)   # B > B_max
     with pytest.raises(slim.SlimError, match="EINVAL"):
         slim.slim_forward(net.ctx, 4, 0.25, 0.25, 2, x, x)        # seg out of range
+    with pytest.raises(slim.SlimError, match="EINVAL"):
+        slim.slim_forward(net.ctx, 0, 0.25, 0.25, 0, x, x)        # empty batch
+    with pytest.raises(slim.SlimError, match="EINVAL"):
+        slim.slim_forward(net.ctx, 0, 0.25, 0.25, 2, x.view(torch.uint8)[1:].data_ptr(), x)   # misaligned
     assert slim.slim_last_error(net.ctx) == 0
 
 
@@ -434,3 +438,24 @@ def test_sm_share_is_bit_exact(params):
     n.close()
     torch.testing.assert_close(part, full, rtol=0, atol=0)
     torch.testing.assert_close(part2, full, rtol=0, atol=0)
+
+
+@pytest.mark.parametrize("r", [0.25, 1.0])
+def test_max_batch_4096(params, ref, r):
+    """CFG3's largest batch (B = 4096, the default B_max): 48 sampled images against the oracle, and
+    512 sampled images bit-identical to the same images run as a batch of 512 (batch independence
+    carries the oracle check to every image)."""
+    w, bn = params
+    n = slim.SlimNet(w, bn)                       # default config: B_max = 4096
+    B = 4096
+    x = synth.make_images(B, offset=77)
+    xd = _dev(x)
+    got = n.forward_chain(xd, (r,) * 4)
+    g = np.random.default_rng(int(r * 100))
+    idx = np.sort(g.choice(B, 512, replace=False))
+    sub = n.forward_chain(xd[torch.from_numpy(idx).cuda()].contiguous(), (r,) * 4)
+    torch.testing.assert_close(got[torch.from_numpy(idx).cuda()], sub, rtol=0, atol=0)
+    pick = idx[:48]
+    _check(got[torch.from_numpy(pick).cuda()].cpu().numpy(), ref.chain(x[pick], (r,) * 4), TAU_BF16,
+           f"B=4096 r={r}")
+    n.close()
