@@ -478,12 +478,14 @@ slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, i
         nt = c_out / splitn;
         narrow_out = true;
     }
-    if (!no_fill && a.m_tiles * nt * 10 < ctx->num_sms * 8 && !cc.pool_out)
+    // (the SMs to fill are this width's share when instances are partitioned, slim_set_sm_share)
+    const int fill_sms = grid_cap(ctx, ri, ctx->num_sms, cc.seg);
+    if (!no_fill && a.m_tiles * nt * 10 < fill_sms * 8 && !cc.pool_out)
         for (int n2 : {32, 16}) {
-            if (n2 >= c_out / nt || c_out % n2 || a.m_tiles * (c_out / n2) > ctx->num_sms) continue;   // one wave
+            if (n2 >= c_out / nt || c_out % n2 || a.m_tiles * (c_out / n2) > fill_sms) continue;   // one wave
             nt = c_out / n2;
             narrow_out = true;
-            if (a.m_tiles * nt * 10 >= ctx->num_sms * 8) break;
+            if (a.m_tiles * nt * 10 >= fill_sms * 8) break;
         }
     a.n_tile = c_out / nt;
     a.n_tiles = nt;
