@@ -45,14 +45,14 @@ def _peaks():
 
 def sm_shares(widths, spec: str):
     """Per-width SM shares for the concurrent width instances (slim_set_sm_share).  auto: share(r) =
-    0.1 + 0.45 r, clamped to (0, 1] (fitted to the B=128 sweep in profiles/r01_sm_share_sweep.txt:
-    0.21 / 0.33 / 0.44 / 0.55 of the SMs for r = .25 / .5 / .75 / 1 -- the shares overlap, their sum is
-    1.5; 1.18-1.20 M images/s vs 0.88 M with every kernel on all SMs); none: every width may use all
+    0.1 + 0.4 r, clamped to (0, 1] (fitted to the B=128 sweeps in profiles/r01_sm_share_sweep.txt:
+    0.2 / 0.3 / 0.4 / 0.5 of the SMs for r = .25 / .5 / .75 / 1 -- the shares overlap, their sum is
+    1.4; ~1.24 M images/s vs 0.88 M with every kernel on all SMs); none: every width may use all
     SMs; else a comma list, one share per width."""
     if spec == "none":
         return {r: 1.0 for r in widths}
     if spec == "auto":
-        return {r: min(1.0, max(0.05, 0.1 + 0.45 * r)) for r in widths}
+        return {r: min(1.0, max(0.05, 0.1 + 0.4 * r)) for r in widths}
     vals = [float(v) for v in spec.split(",")]
     assert len(vals) == len(widths), "--sm-share needs one value per width"
     return dict(zip(widths, vals))
