@@ -219,7 +219,12 @@ __global__ void __launch_bounds__(gn_max_threads<T>(), sizeof(T) == 2 ? (TWO ? 2
     __syncthreads();
     const float *A0 = coef[0][0] + v * VE, *B0 = coef[0][1] + v * VE, *A1 = coef[1][0] + v * VE,
                 *B1 = coef[1][1] + v * VE;
-    // pass 3: apply (+ shortcut) (+ ReLU); out may alias y (every y element is already in registers)
+    // pass 3: apply (+ shortcut) (+ ReLU); out may alias y (every y element is already in registers).
+    // pool_out (the network's last GN): the average pool of the result instead of its store --
+    // per-thread channel sums, then a fixed-order sum over the k pixel lanes (deterministic)
+    float zs[VE];
+#pragma unroll
+    for (int i = 0; i < VE; ++i) zs[i] = 0.f;
 #pragma unroll
     for (int j = 0; j < kGnPPT; ++j) {
         const int p = p0 + j * k;
@@ -235,8 +240,23 @@ __global__ void __launch_bounds__(gn_max_threads<T>(), sizeof(T) == 2 ? (TWO ? 2
             if (two) z[i] += fmaf(x1[i], A1[i], B1[i]);
             if (a.res) z[i] += r[i];
             z[i] = fmaxf(z[i], a.relu_lo);
+            zs[i] += z[i];
         }
-        store_vec(static_cast<T *>(a.out) + base + static_cast<size_t>(p) * a.C, z);
+        if (!a.pool_out) store_vec(static_cast<T *>(a.out) + base + static_cast<size_t>(p) * a.C, z);
+    }
+    if (a.pool_out) {
+        float *red = &coef[0][0][0];   // blockDim * VE <= 2048 floats = the coef array (all reads done below)
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < VE; ++i) red[t * VE + i] = zs[i];
+        __syncthreads();
+        for (int cl = t; cl < V * VE; cl += blockDim.x) {   // local channel cl = slot * VE + element
+            const int slot = cl / VE, e = cl - slot * VE;
+            float sum = 0.f;
+            for (int m = 0; m < k; ++m) sum += red[(m * V + slot) * VE + e];
+            a.pool_out[static_cast<size_t>(n) * a.C + ch0 + cl] = sum / static_cast<float>(a.HW);
+        }
+        __syncthreads();   // red (= coef) is rewritten by the next item
     }
     }   // items
 }

@@ -1079,7 +1079,8 @@ slim_status validate_fwd(slim_ctx *ctx, int seg, float r_prev, float r, int batc
 // The segment schedule (O5/O6 in SURVEY §8(c)); all buffers validated by the caller.
 // GroupNorm mode (reading R16): out = act(GN(y) [+ GN_p(yp)] [+ res]) over [B, H, H, C].
 slim_status gn_apply(slim_ctx *ctx, cudaStream_t st, int seg, int layer, const DevLayer &L, const DevLayer *Lp,
-                     int ri, int B, int H, int C, const void *y, const void *yp, const void *res, void *out, bool relu) {
+                     int ri, int B, int H, int C, const void *y, const void *yp, const void *res, void *out, bool relu,
+                     float *pool_out = nullptr) {
     const slim_config &c = ctx->cfg;
     GnArgs g{};
     g.y = y;
@@ -1099,6 +1100,7 @@ slim_status gn_apply(slim_ctx *ctx, cudaStream_t st, int seg, int layer, const D
     g.gpc = gn_groups_per_cta(B, g.HW, C, g.cpg, c.dtype == SLIM_FP32);
     g.eps = c.bn_eps;
     g.relu_lo = relu ? 0.f : -INFINITY;
+    g.pool_out = pool_out;   // the network's last GN: average pool fp32 [B][C] instead of the activation
     {   // SM share of this width: gn_mult CTAs per SM of the share (persistent over items); 0 = uncapped
         static const int gn_mult = getenv("SLIM_GN_CAP_MULT") ? atoi(getenv("SLIM_GN_CAP_MULT")) : 0;   // measured: uncapped 716k, x3 699k, x6 717k
         const int cap = grid_cap(ctx, ri, 1 << 30, seg);
@@ -1125,6 +1127,7 @@ slim_status run_segment(slim_ctx *ctx, int seg, int ri_prev, int ri, int B, cons
     const int H = seg_hw(c, seg);
     const bool gn = c.norm == SLIM_NORM_GN;
     const float relu_lo = gn ? -INFINITY : 0.f;   // GN: convs store the raw pre-norm output
+    float *gn_pooled = nullptr;                    // GN: the last GN's fused average pool (fp32 [B][C])
     const int C = slim_act_channels(r, c.base_channels[seg]);
     const size_t buf = round256(act_bytes(c, seg, r, B));
     char *bufs[3] = {static_cast<char *>(ws), static_cast<char *>(ws) + buf, static_cast<char *>(ws) + 2 * buf};
@@ -1270,8 +1273,15 @@ slim_status run_segment(slim_ctx *ctx, int seg, int ri_prev, int ri, int B, cons
                 if (s1) return s1;
                 yp = T;
             }
+            // the network's last GN pools in place of its store (the head is then the FC alone); the
+            // pooled fp32 [B][C] goes to a buffer this GN does not read: T (free unless it holds the
+            // projection), else the block input if it is a workspace buffer (never the caller's `in`)
+            if (seg == 3 && b == nb - 1) {
+                void *pb = !down ? static_cast<void *>(T) : (cur != in ? const_cast<void *>(cur) : nullptr);
+                gn_pooled = static_cast<float *>(pb);
+            }
             s1 = gn_apply(ctx, st, seg, bi.c2, S.L[bi.c2], down ? &S.L[bi.sc] : nullptr, ri, B, H, C, dst, yp,
-                          down ? nullptr : cur, dst, true);
+                          down ? nullptr : cur, dst, true, gn_pooled);
             if (s1) return s1;
             cur = dst;
             curH = H;
@@ -1288,7 +1298,8 @@ slim_status run_segment(slim_ctx *ctx, int seg, int ri_prev, int ri, int B, cons
     }
     if (seg == 3) {
         const double K = c.num_classes;
-        const bool pooled = !gn && bf && H * H <= 32 && 32 % (H * H) == 0;   // see fuse_pool above
+        const bool pooled = gn ? gn_pooled != nullptr : (bf && H * H <= 32 && 32 % (H * H) == 0);   // fuse_pool
+        if (gn_pooled) cur = gn_pooled;
         const double flops = 2.0 * B * C * K + (pooled ? 0.0 : static_cast<double>(B) * H * H * C);
         const double bytes = (pooled ? 4.0 * B * C : eb * B * H * H * C) + 4.0 * K * (C + 1) + 4.0 * B * K;
         LaunchProf prof(ctx, st);

@@ -192,6 +192,7 @@ struct GnArgs {
     int B, HW, C, cpg, gpc;        // cpg channels per group; gpc groups per CTA (divides C/cpg)
     float eps, relu_lo;            // relu_lo 0 = ReLU, -inf = none
     int max_ctas;                  // persistent-grid cap (0 = one CTA per (image, slice))
+    float *pool_out;               // != nullptr: write the average pool fp32 [B][C] instead of out
 };
 int gn_groups_per_cta(int B, int HW, int C, int cpg, bool fp32);
 cudaError_t launch_gn(const GnArgs &a, bool fp32, cudaStream_t s, bool pdl);

@@ -133,3 +133,22 @@ def test_gn_graph_replay_equals_eager(params):
     n.close()
     torch.testing.assert_close(g1, eager, rtol=0, atol=0)
     torch.testing.assert_close(g2, eager, rtol=0, atol=0)
+
+
+@pytest.mark.parametrize("blocks", [(1, 1, 1, 1), (2, 1, 1, 3)])
+def test_gn_other_depths_pool_paths(blocks):
+    """Depths where the last block of segment 3 is (or is not) the down-sampling block: the fused
+    average pool of the last GN lands in a free workspace buffer (chain), and the unfused head runs
+    when the only candidate is the caller's input (slim_forward of segment 3)."""
+    w = synth.make_weights(blocks=blocks)
+    bn = synth.make_bn(blocks=blocks)
+    n = slim.SlimNet(w, bn, max_batch=16, norm="gn", blocks_per_seg=blocks)
+    ref = oracle.Model(w, bn, blocks=blocks, norm="gn")
+    x = synth.make_images(9, offset=41)
+    tup = (0.5, 1.0, 0.25, 0.75)
+    got = n.forward_chain(_dev(x), tup).cpu().numpy()
+    _check(got, ref.chain(x, tup), TAU_BF16, f"GN chain blocks={blocks}")
+    h = _seg_input(3, 0.25, 5, 3)
+    got3 = n.forward(3, _dev(h), 0.25, 0.75).cpu().numpy()
+    _check(got3, ref.segment(3, h, 0.25, 0.75), TAU_BF16, f"GN seg3 blocks={blocks}")
+    n.close()
