@@ -165,7 +165,12 @@ def run_ours(args):
     # instances of a step serve their batches concurrently (Alg. 1 runs every loaded
     # instance independently); --sequential runs them one after another
     wss = {r: torch.empty(wsb, dtype=torch.uint8, device=dev) for r in WIDTHS}
-    streams = {r: (stream if args.sequential else torch.cuda.Stream(device=dev)) for r in WIDTHS}
+    # --stream-priority wide: the wider (longer) chains' streams get higher CUDA priority
+    prio = {r: 0 for r in WIDTHS}
+    if args.stream_priority == "wide":
+        for i, r in enumerate(sorted(WIDTHS, reverse=True)):
+            prio[r] = -max(0, 2 - i)
+    streams = {r: (stream if args.sequential else torch.cuda.Stream(device=dev, priority=prio[r])) for r in WIDTHS}
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
     telem = TelemetryExchange(device=dev) if world > 1 else None
 
@@ -287,6 +292,7 @@ def run_ours(args):
         "algorithmic_flops_per_launch": D["flops"] / D["n"], "algorithmic_bytes_per_launch": D["bytes"] / D["n"],
         "traffic": _ncu_traffic() if args.dtype == "bf16" else None,
     })
+    roof["tensor_pipe_pct_ncu"] = _ncu_tensor_pipe() if args.dtype == "bf16" else None
     # every kernel kind against its own roofline (per-launch algorithmic work / event-timed duration)
     roof["by_kind"] = {k: {"launches": d["n"], "tflops": d["flops"] / (d["ms"] / 1e3) / 1e12,
                            "gbs": d["bytes"] / (d["ms"] / 1e3) / 1e9,
@@ -721,6 +727,23 @@ def _ncu_traffic():
         return None
 
 
+def _ncu_tensor_pipe():
+    """Tensor-pipe activity of the conv kernels from the committed ncu --set full summaries (the
+    metric's "tensor-pipe % of peak"): mean over the captured conv launches, % of elapsed and of
+    active cycles (sm__pipe_tensor_cycles_active / sm__pipe_tc_cycles_active)."""
+    out = {}
+    for key, f in (("b128_all_widths", "r01_ncu_chain.json"), ("b1024_r1", "r01_ncu_b1024_r1.json")):
+        p = os.path.join(ROOT, "profiles", f)
+        try:
+            L = [r for r in json.load(open(p))["launches"] if "conv" in r["kernel"]]
+            out[key] = {"pct_of_peak_elapsed": sum(r.get("tensor_pct", 0.0) for r in L) / len(L),
+                        "pct_of_peak_active": sum(r.get("tc_pipe_pct_active", 0.0) for r in L) / len(L),
+                        "launches": len(L), "source": f"profiles/{f}"}
+        except Exception:
+            pass
+    return out or None
+
+
 def main(argv=None):
     ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
     ap.add_argument("--gpus", type=int, default=1)
@@ -741,6 +764,8 @@ def main(argv=None):
     ap.add_argument("--requests", type=int, default=1024, help="stream: requests per rank per step")
     ap.add_argument("--bmax", type=int, default=256, help="stream: B_max of the key batching")
     ap.add_argument("--policy", default="random", help="stream: routing policy (random | slim | table_rr)")
+    ap.add_argument("--stream-priority", choices=("none", "wide"), default="none",
+                    help="cfg2: CUDA stream priorities of the width instances")
     ap.add_argument("--sm-share", default="auto",
                     help="cfg2: SM shares of the concurrent width instances (auto | none | comma list per width)")
     ap.add_argument("--dtype", choices=("bf16", "fp32"), default="bf16",

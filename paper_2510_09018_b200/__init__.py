@@ -532,6 +532,11 @@ class SlimNet:
     def unload_segment(self, s: int):
         slim_unload_segment(self.ctx, s)
 
+    def set_sm_shares(self, shares: dict):
+        """{width: share of the SMs} for concurrent width instances (slim_set_sm_share)."""
+        for r, sh in shares.items():
+            slim_set_sm_share(self.ctx, r, sh)
+
     def segment_loaded(self, s: int) -> bool:
         return bool(load_library().slim_segment_loaded(self.ctx, s))
 
