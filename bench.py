@@ -167,8 +167,8 @@ def run_ours(args):
     wss = {r: torch.empty(wsb, dtype=torch.uint8, device=dev) for r in WIDTHS}
     # --stream-priority wide: the wider (longer) chains' streams get higher CUDA priority
     prio = {r: 0 for r in WIDTHS}
-    if args.stream_priority == "wide":
-        for i, r in enumerate(sorted(WIDTHS, reverse=True)):
+    if args.stream_priority in ("wide", "narrow"):
+        for i, r in enumerate(sorted(WIDTHS, reverse=args.stream_priority == "wide")):
             prio[r] = -max(0, 2 - i)
     streams = {r: (stream if args.sequential else torch.cuda.Stream(device=dev, priority=prio[r])) for r in WIDTHS}
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
@@ -764,7 +764,7 @@ def main(argv=None):
     ap.add_argument("--requests", type=int, default=1024, help="stream: requests per rank per step")
     ap.add_argument("--bmax", type=int, default=256, help="stream: B_max of the key batching")
     ap.add_argument("--policy", default="random", help="stream: routing policy (random | slim | table_rr)")
-    ap.add_argument("--stream-priority", choices=("none", "wide"), default="none",
+    ap.add_argument("--stream-priority", choices=("none", "wide", "narrow"), default="none",
                     help="cfg2: CUDA stream priorities of the width instances")
     ap.add_argument("--sm-share", default="auto",
                     help="cfg2: SM shares of the concurrent width instances (auto | none | comma list per width)")

@@ -1,4 +1,4 @@
-for p in none wide none wide; do
+for p in narrow none narrow; do
   timeout 300 python bench.py --steps 300 --no-cpu --e2e-steps 20 --profile-steps 5 --stream-priority $p > /tmp/b.json 2>/tmp/b.err
   python -c "
 import json;d=json.loads(open('/tmp/b.json').read().strip().splitlines()[-1]);print('prio=$p', round(d['value']))" || tail -2 /tmp/b.err
