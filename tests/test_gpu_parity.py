@@ -459,3 +459,4 @@ def test_max_batch_4096(params, ref, r):
     _check(got[torch.from_numpy(pick).cuda()].cpu().numpy(), ref.chain(x[pick], (r,) * 4), TAU_BF16,
            f"B=4096 r={r}")
     n.close()
+
