@@ -177,10 +177,12 @@ def run_ours(args):
     def chain(r, st=None):
         slim.slim_forward_chain(net.ctx, (r,) * 4, B, xs[r], logits[r], wss[r], wsb, st if st is not None else streams[r])
 
+    order = sorted(WIDTHS, reverse=args.launch_order == "desc")
+
     def step():
         fork = torch.cuda.Event()
         fork.record(stream)
-        for r in WIDTHS:
+        for r in order:
             streams[r].wait_event(fork)
             chain(r)
         for r in WIDTHS:
@@ -764,6 +766,8 @@ def main(argv=None):
     ap.add_argument("--requests", type=int, default=1024, help="stream: requests per rank per step")
     ap.add_argument("--bmax", type=int, default=256, help="stream: B_max of the key batching")
     ap.add_argument("--policy", default="random", help="stream: routing policy (random | slim | table_rr)")
+    ap.add_argument("--launch-order", choices=("asc", "desc"), default="asc",
+                    help="cfg2: order in which the width instances are enqueued each step")
     ap.add_argument("--stream-priority", choices=("none", "wide", "narrow"), default="none",
                     help="cfg2: CUDA stream priorities of the width instances")
     ap.add_argument("--sm-share", default="auto",
