@@ -457,7 +457,9 @@ def run_stream(args):
         ex = _Adapter()
     else:
         ex = StreamExecutor(net, n_max=len(mine), B_max=args.bmax, device=dev, lanes=args.lanes)
-        if args.lanes > 1:   # one lane per width: partition the SMs by width as in cfg2
+        # one lane per width: partition the SMs by width as in cfg2 -- only when the stream mixes
+        # widths (a single-width stream, e.g. the "slim" policy, keeps every SM for its one lane)
+        if args.lanes > 1 and len(np.unique(tuples)) > 1:
             cw = tuple(net.cfg.widths[i] for i in range(net.cfg.n_widths))
             for r, sh in sm_shares(cw, args.sm_share).items():
                 slim.slim_set_sm_share(net.ctx, r, sh)
@@ -704,6 +706,28 @@ def run_points(args):
         b.record(st)
         torch.cuda.synchronize()
         us = a.elapsed_time(b) / reps * 1e3
+        floor = {}
+        if kind == "seg0":   # CFG1: the launch floor -- a CUDA graph of as many empty-ish kernels
+            t1 = torch.zeros(1, device="cuda")
+            g = torch.cuda.CUDAGraph()
+            cs = torch.cuda.Stream()
+            with torch.cuda.stream(cs):
+                t1.add_(1)
+                torch.cuda.synchronize()
+                with torch.cuda.graph(g, stream=cs):
+                    for _ in range(len(recs)):
+                        t1.add_(1)
+            for _ in range(3):
+                g.replay()
+            torch.cuda.synchronize()
+            a.record()
+            for _ in range(reps):
+                g.replay()
+            b.record()
+            torch.cuda.synchronize()
+            fl = a.elapsed_time(b) / reps * 1e3
+            floor = {"launch_floor_us": fl, "ratio_to_launch_floor": us / fl,
+                     "launch_floor": f"CUDA graph of {len(recs)} one-element torch kernels, same replay count"}
         print(json.dumps({
             "metric": METRIC, "value": B / us * 1e6, "unit": "images/s", "n_gpus": 1, "steps": reps,
             "warmup": max(3, args.warmup), "ms_per_step": us / 1e3, "higher_is_better": True, "scaling": "weak",
@@ -712,7 +736,7 @@ def run_points(args):
                                     else "CFG3: full chain batch sweep"), "batch": B, "width": r,
                        "l2": "flushed once before the timed replays (steady-state L2 reuse across replays)"},
             "us_per_call": us, "tflops": flops / (us * 1e-6) / 1e12,
-            "per_layer_roofline_frac": roof_s / (us * 1e-6), "gpu_launches_per_call": len(recs),
+            "per_layer_roofline_frac": roof_s / (us * 1e-6), "gpu_launches_per_call": len(recs), **floor,
         }), flush=True)
     net.close()
     return 0
