@@ -188,7 +188,7 @@ def run_ours(args):
         for r in WIDTHS:
             stream.wait_stream(streams[r])
 
-    shares = sm_shares(WIDTHS, "none" if args.sequential else args.sm_share)
+    shares = sm_shares(WIDTHS, "none" if (args.sequential or len(WIDTHS) == 1) else args.sm_share)
 
     def set_shares(sh):
         for r in WIDTHS:
@@ -606,7 +606,7 @@ def run_handoff(args):
     plan = handoff.plan_segments(n, world, args.seg_policy)
     x = torch.from_numpy(synth.make_images(n, offset=300)).to(torch.bfloat16).to(dev)
     ex = handoff.HandoffExecutor(net, n, rank, world, B_max=args.bmax, lanes=args.lanes)
-    if args.lanes > 1:
+    if args.lanes > 1 and len(np.unique(tuples)) > 1:
         for r, sh in sm_shares(tuple(net.cfg.widths[i] for i in range(net.cfg.n_widths)), args.sm_share).items():
             slim.slim_set_sm_share(net.ctx, r, sh)
     for _ in range(args.warmup):
