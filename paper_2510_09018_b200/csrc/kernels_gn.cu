@@ -112,7 +112,7 @@ constexpr int gn_max_threads() { return sizeof(T) == 2 ? 256 : kGnMaxThreads; }
 // TWO: a second raw input (the projection shortcut) -- a template flag so the common case
 // keeps half the registers (more CTAs resident: the kernel is a short latency chain).
 template <typename T, bool TWO>
-__global__ void __launch_bounds__(gn_max_threads<T>(), sizeof(T) == 2 ? (TWO ? 2 : 3) : 1) gn_kernel(const GnArgs a) {
+__global__ void __launch_bounds__(gn_max_threads<T>(), sizeof(T) == 2 ? (TWO ? 2 : 4) : 1) gn_kernel(const GnArgs a) {
     constexpr int VE = 16 / sizeof(T);   // elements per 16-byte vector
     __shared__ float2 part[kGnMaxThreads];
     __shared__ float gsum[2][kGnMaxCh / 8];
