@@ -375,6 +375,8 @@ def run_ours(args):
             "roofline": roof,
             "kernel_time_by_kind_ms_per_step": {k: v["ms"] / KP for k, v in by_kind.items()},
             "gpu_launches": launches,
+            **({"telemetry_allgather_us_mean": 1e3 * float(np.mean(telem.gather_ms)),
+                "telemetry_ticks_timed": len(telem.gather_ms)} if telem and telem.gather_ms else {}),
             "energy_j_per_image": energy,
             "clocks": clocks,
             "e2e": {"value": e2e_val, "unit": "images/s", "h2d_bytes_per_step": sum(x.numel() * 2 for x in xh.values()),

@@ -138,6 +138,10 @@ class TelemetryExchange:
             if self.stream is not None else None
         self._ev = [torch.cuda.Event() for _ in range(4)] if self.stream is not None else None
         self._k = 0
+        # device time of each all-gather on the side stream (CFG5 "telemetry all-gather overhead")
+        self._t = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(4)] \
+            if self.stream is not None else None
+        self.gather_ms = []
 
     def tick(self, record: np.ndarray, wait: bool = False):
         """Start the all-gather of this rank's record; returns a handle (or the gathered [world, 8] array)."""
@@ -150,10 +154,17 @@ class TelemetryExchange:
             self._ring[i].copy_(rec)
             cur = torch.cuda.current_stream(self.device)
             self.stream.wait_stream(cur)
+            if self._k > len(self._t):   # the timing events of slot i were recorded 4 ticks ago
+                ta, tb = self._t[i]
+                tb.synchronize()
+                self.gather_ms.append(ta.elapsed_time(tb))
             with torch.cuda.stream(self.stream):
                 self.send.copy_(self._ring[i], non_blocking=True)
                 self._ev[i].record(self.stream)
+                self._t[i][0].record(self.stream)
                 work = self.dist.all_gather_into_tensor(self.recv, self.send, group=self.group, async_op=True)
+                work.wait()   # NCCL: the side stream (not the host) waits for the collective
+                self._t[i][1].record(self.stream)
         else:
             self.send.copy_(rec)
             work = self.dist.all_gather_into_tensor(self.recv, self.send, group=self.group, async_op=True)

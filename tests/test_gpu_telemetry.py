@@ -43,5 +43,9 @@ def test_nccl_telemetry_ticks_are_async():
         torch.cuda.synchronize()
         assert ex.gathered()[0][0] == 42.0
         assert dt < 0.02, f"tick blocked the host for {dt * 1e3:.1f} ms"
+        for _ in range(6):
+            ex.tick(pack_record(queue_len=1.0))
+        torch.cuda.synchronize()
+        assert len(ex.gather_ms) >= 3 and all(t > 0 for t in ex.gather_ms)   # device time per all-gather
     finally:
         dist.destroy_process_group()
