@@ -386,12 +386,12 @@ __device__ __forceinline__ void f32_gemm_part(const GemmTile &g, const float *__
     }
 }
 
-__global__ void __launch_bounds__(kGThreads) conv_f32_gemm_kernel(const ConvF32Args a) {
+__device__ __forceinline__ void conv_f32_gemm_tile(const ConvF32Args &a, int bx, int by) {
     __shared__ __align__(16) float As[2][kGK][kGM + 4];
     __shared__ __align__(16) float Bs[2][kGK][kGN + 4];
     const int tid = threadIdx.x;
-    const long m0 = static_cast<long>(blockIdx.x) * kGM;
-    const int n0 = blockIdx.y * kGN;
+    const long m0 = static_cast<long>(bx) * kGM;
+    const int n0 = by * kGN;
     const long npix = static_cast<long>(a.B) * a.Ho * a.Wo;
     GemmTile g;
     g.tx = tid & 15;          // compute: pixels tx*8 .. +7, channels ty*4 .. +3
@@ -451,16 +451,24 @@ __global__ void __launch_bounds__(kGThreads) conv_f32_gemm_kernel(const ConvF32A
     }
 }
 
+// persistent over (M tile, N tile): the grid may be capped (SM share of the width, max_ctas)
+__global__ void __launch_bounds__(kGThreads) conv_f32_gemm_kernel(const ConvF32Args a, int gx, int gy) {
+    for (int t = blockIdx.x; t < gx * gy; t += gridDim.x) {
+        conv_f32_gemm_tile(a, t % gx, t / gx);
+        __syncthreads();
+    }
+}
+
 // Wider variant for layers without a projection: CTA tile 256 pixels x 64 channels, 8 x 8 register
 // tile per thread (64 FFMA per 4 LDS.128).
 constexpr int kWM = 256;
-__global__ void __launch_bounds__(kGThreads, 1) conv_f32_gemm256_kernel(const ConvF32Args a) {
+__device__ __forceinline__ void conv_f32_gemm256_tile(const ConvF32Args &a, int bx, int by) {
     __shared__ __align__(16) float As[2][kGK][kWM + 4];
     __shared__ __align__(16) float Bs[2][kGK][kGN + 4];
     const int tid = threadIdx.x;
     const int tx = tid & 31, ty = tid >> 5;       // compute: pixels tx*8 .. +7, channels ty*8 .. +7
-    const long m0 = static_cast<long>(blockIdx.x) * kWM;
-    const int n0 = blockIdx.y * kGN;
+    const long m0 = static_cast<long>(bx) * kWM;
+    const int n0 = by * kGN;
     const long npix = static_cast<long>(a.B) * a.Ho * a.Wo;
     const long gp = m0 + tid;                      // A loader: one pixel, 16 channels
     const bool pok = gp < npix;
@@ -547,6 +555,13 @@ __global__ void __launch_bounds__(kGThreads, 1) conv_f32_gemm256_kernel(const Co
     }
 }
 
+__global__ void __launch_bounds__(kGThreads, 1) conv_f32_gemm256_kernel(const ConvF32Args a, int gx, int gy) {
+    for (int t = blockIdx.x; t < gx * gy; t += gridDim.x) {
+        conv_f32_gemm256_tile(a, t % gx, t / gx);
+        __syncthreads();
+    }
+}
+
 }  // namespace
 
 cudaError_t launch_stem_bf16(const uint16_t *in, const float *w, int cin_full, const float *scale, const float *shift,
@@ -628,13 +643,15 @@ cudaError_t launch_conv_f32(const ConvF32Args &a, cudaStream_t s) {
     static const bool narrow = getenv("SLIM_F32_GEMM128") != nullptr;   // A/B: the 128 x 64 tile only
     if (!direct && !narrow && a.c_in % kGK == 0 && a.epi != EPI_BN_PROJ_RELU && a.c_out % 16 == 0 &&
         npix >= 148L * kWM) {
-        dim3 grid(static_cast<unsigned>((npix + kWM - 1) / kWM), (a.c_out + kGN - 1) / kGN);
-        conv_f32_gemm256_kernel<<<grid, kGThreads, 0, s>>>(a);
+        const int gx = static_cast<int>((npix + kWM - 1) / kWM), gy = (a.c_out + kGN - 1) / kGN;
+        const int grid = (a.max_ctas > 0 && a.max_ctas < gx * gy) ? a.max_ctas : gx * gy;
+        conv_f32_gemm256_kernel<<<grid, kGThreads, 0, s>>>(a, gx, gy);
         return cudaGetLastError();
     }
     if (!direct && a.c_in % kGK == 0 && (a.epi != EPI_BN_PROJ_RELU || a.c_in1 % kGK == 0) && a.c_out % 16 == 0) {
-        dim3 grid(static_cast<unsigned>((npix + kGM - 1) / kGM), (a.c_out + kGN - 1) / kGN);
-        conv_f32_gemm_kernel<<<grid, kGThreads, 0, s>>>(a);
+        const int gx = static_cast<int>((npix + kGM - 1) / kGM), gy = (a.c_out + kGN - 1) / kGN;
+        const int grid = (a.max_ctas > 0 && a.max_ctas < gx * gy) ? a.max_ctas : gx * gy;
+        conv_f32_gemm_kernel<<<grid, kGThreads, 0, s>>>(a, gx, gy);
         return cudaGetLastError();
     }
     dim3 grid(static_cast<unsigned>((npix + 63) / 64), (a.c_out + 31) / 32);

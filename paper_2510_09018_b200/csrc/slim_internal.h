@@ -173,6 +173,7 @@ struct ConvF32Args {
     float *out; int Ho, Wo, c_out;
     int epi;
     float relu_lo;                               // 0 = ReLU, -inf = raw pre-norm output (GroupNorm mode)
+    int max_ctas;                                // persistent-grid cap of the GEMM kernels (0 = one CTA per tile)
 };
 cudaError_t launch_conv_f32(const ConvF32Args &a, cudaStream_t s);
 cudaError_t launch_stem_f32(const float *in, const float *w, int cin_full, const float *scale,
