@@ -80,13 +80,14 @@ def oracle_throughput(target_s: float = 15.0, batch_per_width: int | None = None
     import oracle
     import synth
     m = oracle.Model(synth.make_weights(), synth.make_bn(widths=widths), norm=norm, widths=widths)
-    x = synth.make_images(128, offset=1)
-    if batch_per_width is None:   # size the sample to ~target_s of CPU work
+    x = synth.make_images(384, offset=1)
+    if batch_per_width is None:   # size the sample to ~target_s of CPU work (10-30 s of the oracle)
+        m.chain(x[:1], (widths[0],) * 4)   # warm-up (library load, thread pool)
         t0 = time.perf_counter()
         for r in widths:
-            m.chain(x[:1], (r,) * 4)
-        t1 = time.perf_counter() - t0
-        batch_per_width = max(1, min(128, int(target_s / max(t1, 1e-3))))
+            m.chain(x[:2], (r,) * 4)
+        t1 = (time.perf_counter() - t0) / 2
+        batch_per_width = max(1, min(384, int(target_s / max(t1, 1e-3))))
     t0 = time.perf_counter()
     for r in widths:
         m.chain(x[:batch_per_width], (r,) * 4)
