@@ -135,10 +135,16 @@ class HandoffExecutor:
             fork.record(main)
             for ls in self.lane_streams:
                 ls.wait_event(fork)
+        per_width = {}
         for d, span in self._plan(np.asarray(tuples, np.float32), dev)[s][0]:
             b = d["batch"]
             slots = self._sl(span)
-            lane = self.widths.index(min(self.widths, key=lambda w: abs(w - d["r"]))) % self.lanes
+            # lane = width index, plus (lanes > widths) a rotation over the width's batches (as in stream.py)
+            wi = self.widths.index(min(self.widths, key=lambda w: abs(w - d["r"])))
+            j = per_width.get(wi, 0)
+            per_width[wi] = j + 1
+            nw = len(self.widths)
+            lane = (wi + nw * (j % max(1, self.lanes // nw))) % self.lanes
             slab, out, ws = self.lane_buf[lane]
             ls = self.lane_streams[lane] if self.lanes > 1 else main
             slim_launch(self.net.ctx, d, slots, pool, self.row_elems[s] * self.eb, slab, out, ws, self.wsb, ls)

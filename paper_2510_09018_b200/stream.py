@@ -96,10 +96,16 @@ class StreamExecutor:
                 fork.record(st)
                 for ls in self.lane_streams:
                     ls.wait_event(fork)
+            per_width = {}
             for d in descs:
                 b, first = d["batch"], d["first"]
                 idx = self.order_d[base + first: base + first + b]
-                lane = self.widths.index(min(self.widths, key=lambda w: abs(w - d["r"]))) % self.lanes
+                # lane = width index, plus (lanes > widths) a rotation over the width's batches of this segment
+                wi = self.widths.index(min(self.widths, key=lambda w: abs(w - d["r"])))
+                j = per_width.get(wi, 0)
+                per_width[wi] = j + 1
+                nw = len(self.widths)
+                lane = (wi + nw * (j % max(1, self.lanes // nw))) % self.lanes
                 slab, out, ws = self.lane_buf[lane]
                 ls = self.lane_streams[lane] if self.lanes > 1 else st
                 slim_launch(self.net.ctx, d, idx, pool, pool_row, slab, out, ws, self.wsb, ls)

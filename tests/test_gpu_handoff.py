@@ -22,7 +22,7 @@ def net():
 
 
 @pytest.mark.parametrize("world,policy,lanes", [(2, "random", 1), (3, "random", 4), (2, "pipeline", 1),
-                                               (4, "sticky", 4)])
+                                               (4, "sticky", 8)])
 def test_handoff_matches_chain(net, world, policy, lanes):
     n = 150
     g = np.random.default_rng(world)

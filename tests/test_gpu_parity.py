@@ -305,7 +305,7 @@ def test_fp32_segment_parity(net32, ref, seg, r_prev, r):
 
 
 # ------------------------------------------------------------------ request stream (CFG4)
-@pytest.mark.parametrize("lanes", [1, 4])
+@pytest.mark.parametrize("lanes", [1, 4, 8])
 def test_stream_executor_matches_per_request_chain(net, lanes):
     """Mixed-width stream: key batching per segment + gather/scatter; each request's logits are
     bitwise the chain of its own tuple (batch independence makes grouping invisible); lanes = 4
