@@ -130,6 +130,84 @@ def run_reference(args):
     return 0
 
 
+class Cfg2Step:
+    """The CFG2 step bench.py times (BASELINE configs[1]): one full-chain forward of a B-image batch at
+    every width, the width instances on their own CUDA streams (concurrently, on per-width SM shares),
+    CUDA-graph replay.  tests/test_gpu_bench_step.py builds the same object from bench.py's default
+    arguments and checks its logits against the oracle."""
+
+    def __init__(self, args, dev, rank: int = 0):
+        import torch
+
+        import synth
+        import paper_2510_09018_b200 as slim
+        self.slim = slim
+        self.B = B = args.batch
+        self.widths = WIDTHS = tuple(args.widths)   # default: the paper's set; others = universal widths (NEXT-4)
+        weights, bn = synth.make_weights(), synth.make_bn(widths=WIDTHS)
+        self.net = net = slim.SlimNet(weights, bn, device=dev.index, max_batch=max(B, 16), norm=args.norm,
+                                      widths=WIDTHS, dtype=args.dtype)
+        adt = torch.bfloat16 if args.dtype == "bf16" else torch.float32
+        if not args.no_graph:
+            slim.slim_set_graph_mode(net.ctx, True)
+        self.stream = stream = torch.cuda.current_stream(dev)
+        self.image_offsets = {r: 100 + rank * 8 + i for i, r in enumerate(WIDTHS)}
+        self.xs = {r: torch.from_numpy(synth.make_images(B, offset=self.image_offsets[r])).to(adt).to(dev)
+                   for r in WIDTHS}
+        self.logits = {r: torch.empty(B, 100, dtype=torch.float32, device=dev) for r in WIDTHS}
+        self.wsb = max(slim.slim_chain_workspace_bytes(net.ctx, (r,) * 4, B) for r in WIDTHS)
+        # one workspace and one stream per width instance: the four (segment-chain, width)
+        # instances of a step serve their batches concurrently (Alg. 1 runs every loaded
+        # instance independently, P:49/P:69); --sequential runs them one after another
+        self.wss = {r: torch.empty(self.wsb, dtype=torch.uint8, device=dev) for r in WIDTHS}
+        # --stream-priority wide: the wider (longer) chains' streams get higher CUDA priority
+        prio = {r: 0 for r in WIDTHS}
+        if args.stream_priority in ("wide", "narrow"):
+            for i, r in enumerate(sorted(WIDTHS, reverse=args.stream_priority == "wide")):
+                prio[r] = -max(0, 2 - i)
+        self.streams = {r: (stream if args.sequential else torch.cuda.Stream(device=dev, priority=prio[r]))
+                        for r in WIDTHS}
+        self.order = sorted(WIDTHS, reverse=args.launch_order == "desc")
+        # FP32 mode: the SIMT GEMMs are compute-bound on every SM -- shares measured 5 % slower
+        self.shares = sm_shares(WIDTHS, "none" if (args.sequential or len(WIDTHS) == 1 or args.dtype == "fp32")
+                                else args.sm_share)
+        self.set_shares(self.shares)
+
+    def chain(self, r, st=None):
+        self.slim.slim_forward_chain(self.net.ctx, (r,) * 4, self.B, self.xs[r], self.logits[r], self.wss[r],
+                                     self.wsb, st if st is not None else self.streams[r])
+
+    def step(self):
+        import torch
+        fork = torch.cuda.Event()
+        fork.record(self.stream)
+        for r in self.order:
+            self.streams[r].wait_event(fork)
+            self.chain(r)
+        for r in self.widths:
+            self.stream.wait_stream(self.streams[r])
+
+    def set_shares(self, sh):
+        for r in self.widths:
+            self.slim.slim_set_sm_share(self.net.ctx, r, sh[r])
+
+
+def _init_nccl(dev):
+    """NCCL process group over NVLink, one rank per GPU; returns a record proving the communicator
+    spans every rank (an all-reduce of ones == world size)."""
+    import torch
+    import torch.distributed as dist
+    dist.init_process_group("nccl", device_id=dev)
+    one = torch.ones(1, device=dev)
+    dist.all_reduce(one)
+    torch.cuda.synchronize(dev)
+    rec = {"backend": dist.get_backend(), "world": dist.get_world_size(), "rank": dist.get_rank(),
+           "allreduce_ones": int(one.item()), "nccl_version": ".".join(map(str, torch.cuda.nccl.version()))}
+    rec["comm_nranks_ok"] = rec["allreduce_ones"] == rec["world"]
+    print(f"[rank {rec['rank']}] NCCL communicator up: {rec}", file=sys.stderr, flush=True)
+    return rec
+
+
 # ------------------------------------------------------------------ GPU arm
 def run_ours(args):
     import numpy as np
@@ -146,56 +224,15 @@ def run_ours(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        _init_nccl(dev)
     slim_build.build()
 
-    B = args.batch
-    WIDTHS = tuple(args.widths)   # default: the paper's set; other values exercise universal widths (NEXT-4)
-    weights, bn = synth.make_weights(), synth.make_bn(widths=WIDTHS)
-    net = slim.SlimNet(weights, bn, device=local, max_batch=max(B, 16), norm=args.norm, widths=WIDTHS,
-                       dtype=args.dtype)
-    adt = torch.bfloat16 if args.dtype == "bf16" else torch.float32
-    if not args.no_graph:
-        slim.slim_set_graph_mode(net.ctx, True)
-    stream = torch.cuda.current_stream(dev)
-    xs = {r: torch.from_numpy(synth.make_images(B, offset=100 + rank * 8 + i)).to(adt).to(dev)
-          for i, r in enumerate(WIDTHS)}
-    logits = {r: torch.empty(B, 100, dtype=torch.float32, device=dev) for r in WIDTHS}
-    wsb = max(slim.slim_chain_workspace_bytes(net.ctx, (r,) * 4, B) for r in WIDTHS)
-    # one workspace and one stream per width instance: the four (segment-chain, width)
-    # instances of a step serve their batches concurrently (Alg. 1 runs every loaded
-    # instance independently); --sequential runs them one after another
-    wss = {r: torch.empty(wsb, dtype=torch.uint8, device=dev) for r in WIDTHS}
-    # --stream-priority wide: the wider (longer) chains' streams get higher CUDA priority
-    prio = {r: 0 for r in WIDTHS}
-    if args.stream_priority in ("wide", "narrow"):
-        for i, r in enumerate(sorted(WIDTHS, reverse=args.stream_priority == "wide")):
-            prio[r] = -max(0, 2 - i)
-    streams = {r: (stream if args.sequential else torch.cuda.Stream(device=dev, priority=prio[r])) for r in WIDTHS}
+    cfg2 = Cfg2Step(args, dev, rank)
+    B, WIDTHS, net, xs, logits = cfg2.B, cfg2.widths, cfg2.net, cfg2.xs, cfg2.logits
+    stream, streams, wss, wsb = cfg2.stream, cfg2.streams, cfg2.wss, cfg2.wsb
+    chain, step, shares, set_shares = cfg2.chain, cfg2.step, cfg2.shares, cfg2.set_shares
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
     telem = TelemetryExchange(device=dev) if world > 1 else None
-
-    def chain(r, st=None):
-        slim.slim_forward_chain(net.ctx, (r,) * 4, B, xs[r], logits[r], wss[r], wsb, st if st is not None else streams[r])
-
-    order = sorted(WIDTHS, reverse=args.launch_order == "desc")
-
-    def step():
-        fork = torch.cuda.Event()
-        fork.record(stream)
-        for r in order:
-            streams[r].wait_event(fork)
-            chain(r)
-        for r in WIDTHS:
-            stream.wait_stream(streams[r])
-
-    # FP32 mode: the SIMT GEMMs are compute-bound on every SM -- shares measured 5 % slower
-    shares = sm_shares(WIDTHS, "none" if (args.sequential or len(WIDTHS) == 1 or args.dtype == "fp32")
-                       else args.sm_share)
-
-    def set_shares(sh):
-        for r in WIDTHS:
-            slim.slim_set_sm_share(net.ctx, r, sh[r])
 
     set_shares(shares)
     for _ in range(args.warmup):
@@ -775,7 +812,7 @@ def _ncu_tensor_pipe():
     return out or None
 
 
-def main(argv=None):
+def build_parser():
     ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=1000)
@@ -821,6 +858,11 @@ def main(argv=None):
     ap.add_argument("--n-new", type=int, default=2, help="greedy: Alg. 1 scale cap N_new")
     ap.add_argument("--norm", choices=("bn", "gn"), default="bn",
                     help="bn = switchable BatchNorm (north_star, default); gn = GroupNorm variant (P:148, NEXT-1)")
+    return ap
+
+
+def main(argv=None):
+    ap = build_parser()
     args = ap.parse_args(argv)
     assert args.warmup >= 0 and args.steps >= 1
     if args.impl == "reference":

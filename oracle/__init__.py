@@ -46,10 +46,10 @@ GN_GROUP_CHANNELS = 16
 
 
 def build(force: bool = False) -> str:
-    """Compile oracle.c with gcc (-O2, strict IEEE: no -ffast-math) -> liboracle.so."""
+    """Compile oracle.c with gcc (-O3, strict IEEE: no -ffast-math, no FMA contraction) -> liboracle.so."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
         tmp = _LIB + f".tmp{os.getpid()}"
-        subprocess.check_call(["gcc", "-O2", "-fopenmp", "-fPIC", "-shared", "-fno-fast-math",
+        subprocess.check_call(["gcc", "-O3", "-fopenmp", "-fPIC", "-shared", "-fno-fast-math",
                                "-ffp-contract=off", "-o", tmp, _SRC])
         os.replace(tmp, _LIB)
     return _LIB
@@ -65,6 +65,8 @@ def _load():
             L = ctypes.c_long
             lib.oracle_conv2d.argtypes = [dp, L, L, L, L, dp, L, L, L, L, L, L, dp]
             lib.oracle_conv2d.restype = ctypes.c_int
+            lib.oracle_conv2d_plain.argtypes = [dp, L, L, L, L, dp, L, L, L, L, L, L, dp]
+            lib.oracle_conv2d_plain.restype = ctypes.c_int
             lib.oracle_out_size.argtypes = [L, L, L, L]
             lib.oracle_out_size.restype = L
             _lib = lib
@@ -88,11 +90,13 @@ def channels(r: float, C: int) -> int:
 
 
 # ---------------------------------------------------------------- O2 conv
-def conv2d(x: np.ndarray, w: np.ndarray, c_out: int, stride: int, pad: int) -> np.ndarray:
+def conv2d(x: np.ndarray, w: np.ndarray, c_out: int, stride: int, pad: int, plain: bool = False) -> np.ndarray:
     """O2: width-sliced convolution of dense NHWC x with the full KRSC tensor w.
 
     x: [B,H,W,c_in] (c_in = x.shape[-1] active channels); w: [Cout_full,k,k,Cin_full].
     Reads w[:c_out, :, :, :c_in] only.  Returns float64 [B,Ho,Wo,c_out].
+    plain=True runs the one-output-at-a-time loop nest (oracle_conv2d_plain); the default
+    runs the same sums vectorised across outputs -- bitwise equal (pinned).
     """
     lib = _load()
     x = np.ascontiguousarray(x, dtype=np.float64)
@@ -105,8 +109,8 @@ def conv2d(x: np.ndarray, w: np.ndarray, c_out: int, stride: int, pad: int) -> n
     y = np.empty((B, Ho, Wo, c_out), dtype=np.float64)
     if B == 0:
         return y
-    rc = lib.oracle_conv2d(_ptr(x), B, H, W, c_in, _ptr(w), cout_full, k, cin_full, c_out,
-                           stride, pad, _ptr(y))
+    fn = lib.oracle_conv2d_plain if plain else lib.oracle_conv2d
+    rc = fn(_ptr(x), B, H, W, c_in, _ptr(w), cout_full, k, cin_full, c_out, stride, pad, _ptr(y))
     if rc != 0:
         raise ValueError("oracle_conv2d: bad arguments")
     return y
@@ -121,7 +125,11 @@ def batchnorm(y: np.ndarray, stats: dict, eps: float = BN_EPS) -> np.ndarray:
     gamma = np.asarray(stats["gamma"], np.float64)[:c]
     beta = np.asarray(stats["beta"], np.float64)[:c]
     assert mu.shape[0] == c, "BN statistics shorter than the active channel count"
-    return (y - mu) / np.sqrt(var + eps) * gamma + beta
+    z = y - mu                       # the formula above, evaluated left to right in place
+    z /= np.sqrt(var + eps)
+    z *= gamma
+    z += beta
+    return z
 
 
 def groupnorm(y: np.ndarray, params: dict, group_channels: int = GN_GROUP_CHANNELS,
@@ -181,14 +189,44 @@ class Model:
 
     def conv_bn(self, x, name, r, stride, pad, bn_width=None):
         """conv (O2) at output width c(r, Cout) followed by BN_{name, width r} (O3),
-        or by GN with that width's affine (gamma, beta) when norm == "gn"."""
+        or by GN with that width's affine (gamma, beta) when norm == "gn".
+        During O10 calibration (`calibrate_bn`) the BN statistics of this (layer, width)
+        are first set from this batch."""
         w = self.w[name]
         c_out = channels(r, w.shape[0])
         y = conv2d(x, w, c_out, stride, pad)
-        params = self.bn[name][self.width_index(r if bn_width is None else bn_width)]
+        wi = self.width_index(r if bn_width is None else bn_width)
+        if getattr(self, "_calibrating", False):
+            self.bn[name][wi] = batch_statistics(y, self.bn[name][wi])
+        params = self.bn[name][wi]
         if self.norm == "gn":
             return groupnorm(y, params, self.group_channels, self.eps)
         return batchnorm(y, params, self.eps)
+
+    # O10 fixture utility: BN calibration
+    def calibrate_bn(self, x, r_per_seg) -> dict:
+        """O10: run the chain O1-O8 on the calibration set x at the width
+        tuple r_per_seg with *batch-statistics* BN, layer by layer in forward order: each
+        BN's running mean / biased variance are set from its own input batch (`batch_statistics`)
+        before it is applied, so every later layer sees the already-calibrated earlier ones.
+        Returns the new BN dict (a copy; entries of the widths the tuple uses are replaced,
+        rounded to float32 as the C-ABI stores them; gamma and beta are kept).  self.bn is
+        left unchanged.  Fixture utility, not part of the forward pass."""
+        assert self.norm == "bn", "O10 calibrates BatchNorm statistics"
+        saved = self.bn
+        self.bn = {k: [dict(e) for e in v] for k, v in saved.items()}
+        self._calibrating = True
+        try:
+            self.chain(x, r_per_seg, head=False)
+            out = self.bn
+        finally:
+            self._calibrating = False
+            self.bn = saved
+        return out
+
+    def features(self, x, r_per_seg):
+        """Pooled features p[n, c] = (1/16) sum_{h,w<4} h[n,h,w,c] after segment 3 (O7's first line)."""
+        return self.chain(x, r_per_seg, head=False).mean(axis=(1, 2))
 
     # O5 BasicBlock
     def basic_block(self, x, s, b, r, bn_width=None):
@@ -234,6 +272,45 @@ class Model:
         for s in range(1, 4):
             h = self.segment(s, h, r_per_seg[s - 1], r_per_seg[s], head=head)
         return h
+
+
+def batch_statistics(y: np.ndarray, stats: dict) -> dict:
+    """O10 step for one BN: per-channel mean and BIASED variance of y over (N, H, W), rounded to
+    float32 (the stored running statistics); gamma and beta are copied unchanged."""
+    mean = y.mean(axis=(0, 1, 2))
+    var = ((y - mean) ** 2).mean(axis=(0, 1, 2))
+    return dict(gamma=stats["gamma"], beta=stats["beta"], mean=mean.astype(np.float32), var=var.astype(np.float32))
+
+
+def ncm_head(features: np.ndarray, num_classes: int, c_full: int, scale: float = 4.0):
+    """Nearest-class-mean head of the D2 fixture: from the pooled features
+    f_k [num_classes, c3] of the 100 clean class prototypes,
+
+        m = mean_k f_k,  W[k, :c3] = scale * (f_k - m) / ||f_k - m||_2,  W[k, c3:] = 0,
+        b[k] = -sum_c m[c] * W[k, c],
+
+    so logits(p) = W (p - m): a cosine classifier around the mean prototype.  W and b are
+    rounded to bf16 (W first; b from the rounded W) so both sides read identical values.
+    Returns (W [num_classes, c_full] float32, b [num_classes] float32)."""
+    f = np.asarray(features, np.float64)
+    assert f.shape[0] == num_classes
+    c3 = f.shape[1]
+    m = f.mean(axis=0)
+    d = f - m
+    u = d / np.sqrt((d * d).sum(axis=1, keepdims=True))
+    W = np.zeros((num_classes, c_full), np.float64)
+    W[:, :c3] = scale * u
+    W = _round_bf16(W)
+    b = _round_bf16(-(W[:, :c3] * m[None, :]).sum(axis=1))
+    return W.astype(np.float32), b.astype(np.float32)
+
+
+def _round_bf16(a: np.ndarray) -> np.ndarray:
+    """float64 -> nearest float32 -> nearest bf16 (round-to-nearest-even), returned as float64."""
+    f = np.ascontiguousarray(a, dtype=np.float32)
+    bits = f.view(np.uint32).astype(np.uint64)
+    out = ((bits + 0x7FFF + ((bits >> 16) & 1)) >> 16) << 16
+    return out.astype(np.uint32).view(np.float32).astype(np.float64)
 
 
 def per_image_rel_err(got: np.ndarray, ref: np.ndarray) -> np.ndarray:

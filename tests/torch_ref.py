@@ -26,6 +26,14 @@ def _bn(y, st, eps):
                         training=False, eps=eps)
 
 
+def _bn_batch(y, st, eps):
+    """Training-mode BN: normalises with this batch's per-channel statistics (biased variance)
+    -- the library's statement of what O10's calibrated statistics must reproduce."""
+    c = y.shape[1]
+    t = lambda a: torch.as_tensor(a[:c]).double()
+    return F.batch_norm(y, None, None, t(st["gamma"]), t(st["beta"]), training=True, eps=eps)
+
+
 def _gn(y, st, eps, group_channels=16):
     c = y.shape[1]
     t = lambda a: torch.as_tensor(a[:c]).double()
@@ -35,7 +43,7 @@ def _gn(y, st, eps, group_channels=16):
 def segment(weights, bn, widths, s, x_nchw, r_prev, r, base=(64, 128, 256, 512), blocks=(2, 2, 2, 2),
             eps=1e-5, head=True, norm="bn"):
     wi = [abs(q - r) < 1e-6 for q in widths].index(True)
-    _bn = _gn if norm == "gn" else globals()["_bn"]
+    _bn = {"gn": _gn, "bn_batch": _bn_batch}.get(norm, globals()["_bn"])
     C = active_channels(r, base[s])
     h = x_nchw
     if s == 0:
