@@ -73,57 +73,104 @@ def _cores():
 
 
 # ------------------------------------------------------------------ CPU oracle legs
-def oracle_throughput(target_s: float = 15.0, batch_per_width: int | None = None, norm: str = "bn",
-                      widths=WIDTHS):
-    """The fp64 oracle as it stands on this host's cores: images/s on a bounded sample of CFG2
-    (equal images per width, like the GPU step)."""
+def _cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def oracle_protocol(norm: str = "bn", widths=WIDTHS, budget_s: float = 30.0):
+    """SURVEY §8(d) "Oracle beside it": the fp64 oracle (oracle/, as it stands) on this host, on the
+    same workload definitions, all threads and 1 thread; CPU model and thread counts recorded.
+
+    * CFG2 = CFG3 at B = 128: the full chain per width, all threads (the line's cpu_baseline value
+      blends the four widths like the GPU step: 4 x 128 images / total seconds);
+    * CFG3 at B in {1, 8} per width, all threads;
+    * CFG2 per width single-threaded (a 4-image sample per width -- CPU cost is linear in B);
+    * CFG1 exactly (segment 0, r = 0.25, B = 8), all threads and 1 thread.
+    The oracle computes in fp64 (reading R15; the north_star names an FP32 oracle)."""
     import oracle
     import synth
     m = oracle.Model(synth.make_weights(), synth.make_bn(widths=widths), norm=norm, widths=widths)
-    x = synth.make_images(384, offset=1)
-    if batch_per_width is None:   # size the sample to ~target_s of CPU work (10-30 s of the oracle)
-        m.chain(x[:1], (widths[0],) * 4)   # warm-up (library load, thread pool)
+    x = synth.make_images(128, offset=1)
+    nthr = oracle.max_threads()
+    m.chain(x[:1], (widths[0],) * 4)                    # warm-up: library load, thread pool
+    t_start = time.perf_counter()
+
+    def timed(fn):
         t0 = time.perf_counter()
+        fn()
+        return time.perf_counter() - t0
+
+    out = {"cpu_model": _cpu_model(), "threads_all": nthr, "precision": "fp64 (reading R15; NS names FP32)"}
+    cfg3 = {}
+    for B in (1, 8, 128):
         for r in widths:
-            m.chain(x[:2], (r,) * 4)
-        t1 = (time.perf_counter() - t0) / 2
-        batch_per_width = max(1, min(384, int(target_s / max(t1, 1e-3))))
-    t0 = time.perf_counter()
-    for r in widths:
-        m.chain(x[:batch_per_width], (r,) * 4)
-    dt = time.perf_counter() - t0
-    n = batch_per_width * len(widths)
-    return dict(value=n / dt, unit="images/s", cores=_cores(), kind="oracle",
-                sample=f"{batch_per_width} images x {len(widths)} widths of the CFG2 chain (fp64 C oracle, "
-                       f"OpenMP over rows), {dt:.1f} s")
+            if time.perf_counter() - t_start > budget_s and B == 128:
+                break
+            dt = timed(lambda: m.chain(x[:B], (r,) * 4))
+            cfg3[f"B{B}_r{r:g}"] = B / dt
+    out["cfg3_images_per_s_all_threads"] = cfg3
+    full = [r for r in widths if f"B128_r{r:g}" in cfg3]
+    out["cfg2_images_per_s_all_threads"] = {str(r): cfg3[f"B128_r{r:g}"] for r in full}
+    seconds = sum(128 / cfg3[f"B128_r{r:g}"] for r in full)
+    out["cfg2_blended_images_per_s"] = 128 * len(full) / seconds if full else None
+    out["cfg1_us_all_threads"] = 1e6 * min(timed(lambda: m.segment(0, x[:8], None, 0.25)) for _ in range(3))
+    oracle.set_num_threads(1)
+    try:
+        out["cfg1_us_1_thread"] = 1e6 * timed(lambda: m.segment(0, x[:8], None, 0.25))
+        out["cfg2_images_per_s_1_thread"] = {str(r): 4 / timed(lambda: m.chain(x[:4], (r,) * 4)) for r in widths}
+    finally:
+        oracle.set_num_threads(nthr)
+    out["seconds"] = time.perf_counter() - t_start
+    return out
+
+
+def oracle_throughput(norm: str = "bn", widths=WIDTHS, budget_s: float = 30.0):
+    """cpu_baseline of the bench line: the protocol above; value = CFG2 blended over the widths."""
+    p = oracle_protocol(norm, widths, budget_s)
+    return dict(value=p["cfg2_blended_images_per_s"], unit="images/s", cores=p["threads_all"], kind="oracle",
+                sample=f"CFG2: the full chain at B=128 for each width (all {p['threads_all']} threads of "
+                       f"{p['cpu_model']}), fp64 C oracle; {p['seconds']:.1f} s incl. the rest of the protocol",
+                protocol=p)
 
 
 def run_reference(args):
+    """--impl reference: the oracle as it stands, on this arm's config/metric/unit; each step = a bounded
+    sample of CFG2 (args.ref_batch images per width through the full chain), all host threads."""
     world, rank, _ = _dist()
     if rank != 0:
         return 0
     import oracle
     import synth
     m = oracle.Model(synth.make_weights(), synth.make_bn(), norm=args.norm)
+    nb = args.ref_batch
     x = synth.make_images(128, offset=1)
-    step = lambda k: [m.chain(x[k % 128:k % 128 + 1], (r,) * 4) for r in WIDTHS]
+    step = lambda k: [m.chain(x[(k * nb) % 128:(k * nb) % 128 + nb], (r,) * 4) for r in WIDTHS]
     for k in range(args.warmup):
         step(k)
     t0 = time.perf_counter()
     for k in range(args.steps):
         step(k)
     dt = time.perf_counter() - t0
-    imgs = len(WIDTHS) * args.steps
+    imgs = nb * len(WIDTHS) * args.steps
     value = imgs / dt
+    cores = oracle.max_threads()
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": 0,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": "CFG2: full SlimResNet chain (4 segments + pool/FC, 100 classes) at each width "
-                               "r in {0.25,0.5,0.75,1.0}; reference step = 1 image per width", "batch": 1,
+                               f"r in {{0.25,0.5,0.75,1.0}}; reference step = {nb} images per width", "batch": nb,
                    "image": [32, 32, 3], "widths": list(WIDTHS), "norm": args.norm},
-        "cpu_baseline": {"value": value, "unit": "images/s", "cores": _cores(), "kind": "oracle",
-                         "sample": f"{args.steps} steps x 1 image per width of the CFG2 chain"},
+        "cpu_baseline": {"value": value, "unit": "images/s", "cores": cores, "kind": "oracle",
+                         "cpu_model": _cpu_model(),
+                         "sample": f"{args.steps} steps x {nb} images per width of the CFG2 chain (fp64)"},
         "e2e": {"value": value, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
@@ -177,13 +224,19 @@ class Cfg2Step:
         self.slim.slim_forward_chain(self.net.ctx, (r,) * 4, self.B, self.xs[r], self.logits[r], self.wss[r],
                                      self.wsb, st if st is not None else self.streams[r])
 
-    def step(self):
+    def step(self, events=None):
+        """One step; events: optional {r: (start, end)} CUDA events recorded around each width's chain
+        on that width's stream."""
         import torch
         fork = torch.cuda.Event()
         fork.record(self.stream)
         for r in self.order:
             self.streams[r].wait_event(fork)
+            if events is not None:
+                events[r][0].record(self.streams[r])
             self.chain(r)
+            if events is not None:
+                events[r][1].record(self.streams[r])
         for r in self.widths:
             self.stream.wait_stream(self.streams[r])
 
@@ -214,17 +267,15 @@ def run_ours(args):
     import torch
     import torch.distributed as dist
 
-    import synth
     import paper_2510_09018_b200 as slim
     from paper_2510_09018_b200 import build as slim_build
-    from paper_2510_09018_b200.telemetry import NvmlSampler, TelemetryExchange, pack_record
+    from paper_2510_09018_b200.telemetry import NvmlSampler, TelemetryExchange, TelemetrySource
 
     world, rank, local = _dist()
     assert torch.cuda.is_available(), "bench.py (ours) needs a GPU; the oracle arm is --impl reference"
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
-        _init_nccl(dev)
+    nccl = _init_nccl(dev) if world > 1 else None
     slim_build.build()
 
     cfg2 = Cfg2Step(args, dev, rank)
@@ -232,38 +283,55 @@ def run_ours(args):
     stream, streams, wss, wsb = cfg2.stream, cfg2.streams, cfg2.wss, cfg2.wsb
     chain, step, shares, set_shares = cfg2.chain, cfg2.step, cfg2.shares, cfg2.set_shares
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
+    sampler = NvmlSampler(local)
     telem = TelemetryExchange(device=dev) if world > 1 else None
+    tsrc = TelemetrySource(sampler, rank)
+    imgs_per_step = B * len(WIDTHS)
+    last_ms = [0.0]
+
+    def tick(k, ev):
+        """Router tick after step k: this rank's record (NVML power / util / energy from the sampler
+        thread, latency of the newest completed step) all-gathered over NCCL on a side stream."""
+        if telem is None:
+            return
+        for j in range(k, max(-1, k - 4), -1):           # newest step whose end event has completed
+            if ev[j][1].query():
+                last_ms[0] = ev[j][0].elapsed_time(ev[j][1])
+                break
+        telem.tick(tsrc.record(queue_len=0.0, mean_latency_s=last_ms[0] / 1e3, completed=(k + 1) * imgs_per_step))
 
     set_shares(shares)
-    for _ in range(args.warmup):
+    sampler.start()
+    wev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(max(4, args.warmup))]
+    for k in range(args.warmup):
         flush.zero_()
+        wev[k % 4][0].record(stream)
         step()
-        if telem:
-            telem.tick(pack_record(rank=rank))
+        wev[k % 4][1].record(stream)
+        tick(k % 4, wev) if telem else None
     torch.cuda.synchronize()
 
-    # ---------------- timed region
+    # ---------------- timed region: K steps, events on the launching stream; per-width events on the
+    # width instances' own streams (the per-width numbers of the timed mode)
     K = args.steps
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
-    sampler = NvmlSampler(local)
+    evw = [{r: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for r in WIDTHS}
+           for _ in range(K)]
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     launches0 = slim.slim_launch_count(net.ctx)
-    e0 = sampler.energy_mj()
-    sampler.start()
+    ns0 = len(sampler.samples)
     for k in range(K):
         flush.zero_()
         ev[k][0].record(stream)
-        step()
+        step(evw[k])
         ev[k][1].record(stream)
-        if telem:
-            telem.tick(pack_record(rank=rank, completed=(k + 1) * B * len(WIDTHS)))
+        tick(k, ev)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    sampler.stop()
-    e1 = sampler.energy_mj()
+    timed_samples = len(sampler.samples) - ns0
     launches = slim.slim_launch_count(net.ctx) - launches0
     step_ms = [a.elapsed_time(b) for a, b in ev]
     total_ms = sum(step_ms)
@@ -271,15 +339,43 @@ def run_ours(args):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_max_ms = float(t.item())
-    imgs_per_step = B * len(WIDTHS)
     value = world * imgs_per_step * K / (total_max_ms / 1e3)
-    clocks = sampler.summary()
-    energy = ((e1 - e0) / 1e3 / (imgs_per_step * K)) if (e0 is not None and e1 is not None) else None
+    in_step_ms = {r: float(np.mean([e[r][0].elapsed_time(e[r][1]) for e in evw])) for r in WIDTHS}
 
-    # ---------------- per-width images/s: each width's chain alone (L2 flushed before it), on all SMs
+    # ---------------- energy (Eq. 7's E_t = P * L): the same step, L2 flush included, in a loop
+    # of >= args.energy_seconds; NVML total-energy counter delta / images.  Clocks sampled throughout.
+    torch.cuda.synchronize()
+    e0 = sampler.energy_mj()
+    t0 = time.perf_counter()
+    n_energy = 0
+    while True:
+        for _ in range(50):
+            flush.zero_()
+            step()
+        n_energy += 50
+        if n_energy % 500 == 0:
+            torch.cuda.synchronize()
+            if time.perf_counter() - t0 >= args.energy_seconds:
+                break
+    torch.cuda.synchronize()
+    energy_s = time.perf_counter() - t0
+    e1 = sampler.energy_mj()
+    sampler.stop()
+    clocks = sampler.summary()
+    clocks["samples_timed_region"] = timed_samples
+    clocks["note"] = (f"sampled every {sampler.period * 1e3:.0f} ms over warm-up, the timed region and the "
+                      f"{energy_s:.1f} s energy loop of the same step")
+    energy = ({"j_per_image": (e1 - e0) / 1e3 / (imgs_per_step * n_energy), "seconds": energy_s,
+               "images": imgs_per_step * n_energy, "mean_power_w": (e1 - e0) / 1e3 / energy_s,
+               "images_per_s_in_loop": imgs_per_step * n_energy / energy_s,
+               "method": "nvmlDeviceGetTotalEnergyConsumption delta over the loop (host wall clock)"}
+              if (e0 is not None and e1 is not None and e1 > e0) else None)
+
+    # ---------------- per-width: each width's chain alone (L2 flushed before it), on all SMs, graph replay
+    # with PDL -- the same kernels as the step without the other instances
     set_shares({r: 1.0 for r in WIDTHS})
-    KW = max(1, min(K, args.profile_steps * 4))
-    width_ms = []
+    KW = max(3, min(K, args.profile_steps * 4))
+    width_ms = {}
     for r in WIDTHS:
         chain(r, stream)   # (re)capture the graph outside the timed events
         evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(KW)]
@@ -289,12 +385,12 @@ def run_ours(args):
             chain(r, stream)
             evs[k][1].record(stream)
         torch.cuda.synchronize()
-        width_ms.append(sum(x.elapsed_time(y) for x, y in evs))
-    per_width = {str(r): B * KW / (width_ms[i] / 1e3) for i, r in enumerate(WIDTHS)}
+        width_ms[r] = sum(x.elapsed_time(y) for x, y in evs) / KW
 
-    # ---------------- profiled replay (per-launch CUDA events, no graph) for the roofline object
-    KP = min(K, args.profile_steps)
-    slim.slim_profile_begin(net.ctx, KP * 80 + 16)
+    # ---------------- per-launch records (eager, an event pair around every launch, PDL off): the
+    # algorithmic FLOPs/bytes of every kernel and its standalone duration -> the kernels' shares
+    KP = max(1, min(K, args.profile_steps))
+    slim.slim_profile_begin(net.ctx, KP * 80 * len(WIDTHS) + 16)
     for _ in range(KP):
         flush.zero_()
         for r in WIDTHS:
@@ -304,48 +400,65 @@ def run_ours(args):
     if args.dtype == "fp32":
         # FP32 mode runs on the CUDA cores (FFMA): peak = 148 SMs x 128 FP32 lanes x 2 FLOP x 1.965 GHz
         # (B200 unit counts and the max SM clock of this pool) -- an ALU roofline
-        peaks = dict(peaks, bf16=148 * 128 * 2 * 1.965e9 / 1e12, src="derived (FFMA lanes x clock)")
-    by_kind = {}
+        peaks = dict(peaks, bf16=148 * 128 * 2 * 1.965e9 / 1e12, bf16_sus=None, src="derived (FFMA lanes x clock)")
+    P_tc, P_hbm = peaks["bf16"] * 1e12, peaks["hbm"] * 1e9
+    by_kind, by_width = {}, {}
     for rc in recs:
-        d = by_kind.setdefault(rc["kind"], dict(ms=0.0, flops=0.0, bytes=0.0, n=0, roof_ms=0.0))
-        d["ms"] += rc["ms"]
-        d["flops"] += rc["flops"]
-        d["bytes"] += rc["bytes"]
-        d["n"] += 1
-        d["roof_ms"] += max(rc["flops"] / (peaks["bf16"] * 1e12), rc["bytes"] / (peaks["hbm"] * 1e9)) * 1e3
+        roof = max(rc["flops"] / P_tc, rc["bytes"] / P_hbm) * 1e3
+        for key, tab in ((rc["kind"], by_kind), (rc["r"], by_width)):
+            d = tab.setdefault(key, dict(ms=0.0, flops=0.0, bytes=0.0, n=0, roof_ms=0.0))
+            d["ms"] += rc["ms"]
+            d["flops"] += rc["flops"]
+            d["bytes"] += rc["bytes"]
+            d["n"] += 1
+            d["roof_ms"] += roof
     kern_ms = sum(d["ms"] for d in by_kind.values())
     dom = max(by_kind, key=lambda k: by_kind[k]["ms"])
     D = by_kind[dom]
-    tensor_time = D["flops"] / (peaks["bf16"] * 1e12)
-    hbm_time = D["bytes"] / (peaks["hbm"] * 1e9)
-    if tensor_time >= hbm_time:
-        achieved = D["flops"] / (D["ms"] / 1e3) / 1e12
-        roof = {"bound": "tensor" if args.dtype == "bf16" else "alu", "achieved": achieved, "peak": peaks["bf16"],
-                "unit": "TFLOP/s",
-                "frac": achieved / peaks["bf16"]}
-    else:
-        achieved = D["bytes"] / (D["ms"] / 1e3) / 1e9
-        roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm"], "unit": "GB/s",
-                "frac": achieved / peaks["hbm"]}
-    roof.update({
-        "kernel": dom, "launches_profiled": D["n"], "share_of_kernel_time": D["ms"] / kern_ms,
-        "peak_source": peaks["src"] + (", bf16 burst" if args.dtype == "bf16" else ""),
+    step_ms_mean = total_max_ms / K
+    share = D["ms"] / kern_ms
+    conv_flops_step = D["flops"] / KP
+    # dominant kernel in the TIMED step: its algorithmic FLOPs per step / (step time x its share of the
+    # kernel time); launches per step from the same records
+    achieved = conv_flops_step / (step_ms_mean * share / 1e3) / 1e12
+    bound = "tensor" if args.dtype == "bf16" else "alu"
+    roof = {"bound": bound, "achieved": achieved, "peak": peaks["bf16"], "unit": "TFLOP/s",
+            "frac": achieved / peaks["bf16"],
+            "traffic": _ncu_traffic() if args.dtype == "bf16" else None,
+            "kernel": f"{dom} (every tcgen05 conv launch of the step)" if args.dtype == "bf16" else dom,
+            "how": "achieved = the dominant kernel's algorithmic FLOPs per step / (ms_per_step x its share of "
+                   "the summed kernel time); share from the per-launch records (events around each launch), "
+                   "to agree with the ncu launch list's share (profiles/)",
+            "share_of_kernel_time": share, "launches_per_step": D["n"] / KP,
+            "algorithmic_flops_per_launch": D["flops"] / D["n"], "algorithmic_bytes_per_launch": D["bytes"] / D["n"],
+            "peak_source": peaks["src"] + (", bf16 burst" if args.dtype == "bf16" else "")}
+    if peaks.get("bf16_sus"):
+        roof["frac_vs_sustained_peak"] = achieved / peaks["bf16_sus"]
+    roof["step_aggregate"] = {"tflops": sum(r_["flops"] for r_ in recs) / KP / (step_ms_mean / 1e3) / 1e12,
+                              "note": "all algorithmic FLOPs of a step (every kernel) / the device-timed step"}
+    roof["step_aggregate"]["frac"] = roof["step_aggregate"]["tflops"] / peaks["bf16"]
+    roof["standalone_per_launch"] = {
+        "tflops": D["flops"] / (D["ms"] / 1e3) / 1e12, "frac": D["flops"] / (D["ms"] / 1e3) / 1e12 / peaks["bf16"],
         "per_layer_roofline_frac": D["roof_ms"] / D["ms"],
-        "algorithmic_flops_per_launch": D["flops"] / D["n"], "algorithmic_bytes_per_launch": D["bytes"] / D["n"],
-        "traffic": _ncu_traffic() if args.dtype == "bf16" else None,
-    })
+        "note": "each launch timed alone (eager, PDL off, events around it): latency-chain view of B=128 kernels"}
     roof["tensor_pipe_pct_ncu"] = _ncu_tensor_pipe() if args.dtype == "bf16" else None
-    # every kernel kind against its own roofline (per-launch algorithmic work / event-timed duration)
-    roof["by_kind"] = {k: {"launches": d["n"], "tflops": d["flops"] / (d["ms"] / 1e3) / 1e12,
-                           "gbs": d["bytes"] / (d["ms"] / 1e3) / 1e9,
-                           "frac_tensor": d["flops"] / (d["ms"] / 1e3) / 1e12 / peaks["bf16"],
-                           "frac_hbm": d["bytes"] / (d["ms"] / 1e3) / 1e9 / peaks["hbm"],
-                           "per_layer_roofline_frac": d["roof_ms"] / d["ms"]} for k, d in by_kind.items()}
-    # the concurrent step as a whole: all algorithmic FLOPs of a step / the device-timed step
-    step_flops = sum(rc["flops"] for rc in recs) / KP
-    roof["step_aggregate"] = {"tflops": step_flops / (total_max_ms / K / 1e3) / 1e12,
-                              "frac": step_flops / (total_max_ms / K / 1e3) / 1e12 / peaks["bf16"],
-                              "note": "all kernels of a step (concurrent width instances on SM shares) / step time"}
+    roof["by_kind_standalone"] = {k: {"launches_per_step": d["n"] / KP, "ms_per_step": d["ms"] / KP,
+                                      "tflops": d["flops"] / (d["ms"] / 1e3) / 1e12,
+                                      "gbs": d["bytes"] / (d["ms"] / 1e3) / 1e9,
+                                      "per_layer_roofline_frac": d["roof_ms"] / d["ms"]} for k, d in by_kind.items()}
+    # per width: images/s in the timed (concurrent) step and alone, and the fraction of the per-layer
+    # roofline (sum over launches of max(F/P_tc, bytes/P_hbm) / measured time)
+    per_width = {}
+    for r in WIDTHS:
+        d = by_width.get(r, by_width.get(float(np.float32(r))))
+        roof_ms = d["roof_ms"] / KP if d else None
+        per_width[str(r)] = {
+            "images_per_s_in_step": B / (in_step_ms[r] / 1e3), "ms_in_step": in_step_ms[r],
+            "per_layer_roofline_frac_in_step": roof_ms / in_step_ms[r] if roof_ms else None,
+            "images_per_s_alone": B / (width_ms[r] / 1e3), "ms_alone": width_ms[r],
+            "per_layer_roofline_frac_alone": roof_ms / width_ms[r] if roof_ms else None,
+            "per_layer_roofline_ms": roof_ms, "gflop_per_batch": d["flops"] / KP / 1e9 if d else None,
+            "tflops_alone": d["flops"] / KP / (width_ms[r] / 1e3) / 1e12 if d else None}
 
     # ---------------- e2e through the public API with host buffers
     # Every step copies its images from pinned host memory and reads its logits back.  As a
@@ -392,10 +505,11 @@ def run_ours(args):
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_val = world * imgs_per_step * KE / float(te.item())
+    gathered = telem.gathered().tolist() if telem else None
 
     if rank == 0:
-        cpu = oracle_throughput(args.cpu_seconds, norm=args.norm, widths=WIDTHS) if (world == 1 and not args.no_cpu) \
-            else None
+        cpu = oracle_throughput(norm=args.norm, widths=WIDTHS, budget_s=args.cpu_seconds) \
+            if (world == 1 and not args.no_cpu) else None
         line = {
             "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world, "steps": K,
             "warmup": args.warmup, "ms_per_step": total_max_ms / K, "higher_is_better": True, "scaling": "weak",
@@ -410,14 +524,16 @@ def run_ours(args):
                        "instances": "sequential" if args.sequential else
                                     f"{len(WIDTHS)} width instances, one CUDA stream each, run concurrently",
                        "sm_share": {str(r): v for r, v in shares.items()}},
-            "per_width_images_per_s": per_width,
-            "per_width_ms_per_batch": {str(r): width_ms[i] / KW for i, r in enumerate(WIDTHS)},
+            "per_width": per_width,
+            "per_width_images_per_s": {k: v["images_per_s_in_step"] for k, v in per_width.items()},
             "roofline": roof,
-            "kernel_time_by_kind_ms_per_step": {k: v["ms"] / KP for k, v in by_kind.items()},
+            "kernel_time_by_kind_ms_per_step_standalone": {k: v["ms"] / KP for k, v in by_kind.items()},
             "gpu_launches": launches,
-            **({"telemetry_allgather_us_mean": 1e3 * float(np.mean(telem.gather_ms)),
-                "telemetry_ticks_timed": len(telem.gather_ms)} if telem and telem.gather_ms else {}),
-            "energy_j_per_image": energy,
+            **({"nccl": nccl, "telemetry_allgather_us_mean": 1e3 * float(np.mean(telem.gather_ms))
+                if telem.gather_ms else None, "telemetry_ticks_timed": len(telem.gather_ms),
+                "telemetry_last_gathered": gathered} if telem else {}),
+            "energy_j_per_image": energy["j_per_image"] if energy else None,
+            "energy": energy,
             "clocks": clocks,
             "e2e": {"value": e2e_val, "unit": "images/s", "h2d_bytes_per_step": sum(x.numel() * 2 for x in xh.values()),
                     "d2h_bytes_per_step": sum(l[0].numel() * 4 for l in lh.values()),
@@ -441,7 +557,12 @@ def _clock_energy_json(sampler, e0, e1, n_images):
 
 def run_stream(args):
     """CFG4 (N=1) / CFG5 (torchrun N>1): the mixed-width request stream through the key packer,
-    gather, segment forwards and scatter; requests routed to ranks by a replicated policy."""
+    gather, segment forwards and scatter; requests routed to ranks by a replicated policy.
+
+    Every step routes a FRESH stream of --requests x N requests (the policy's draw for that step;
+    --repeat-stream replays step 0's), so the router and the packer (slim_pack on all four segments)
+    run inside the timed region.  --policy ppo_frozen routes with the frozen factored PPO policy on the
+    telemetry all-gathered two ticks earlier (fixed lag: identical on every rank, no GPU wait)."""
     import numpy as np
     import torch
     import torch.distributed as dist
@@ -451,13 +572,12 @@ def run_stream(args):
     from paper_2510_09018_b200 import build as slim_build
     from paper_2510_09018_b200 import router
     from paper_2510_09018_b200.stream import StreamExecutor
-    from paper_2510_09018_b200.telemetry import NvmlSampler, TelemetryExchange, pack_record
+    from paper_2510_09018_b200.telemetry import NvmlSampler, TelemetryExchange, TelemetrySource
 
     world, rank, local = _dist()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+    nccl = _init_nccl(dev) if world > 1 else None
     slim_build.build()
     net = slim.SlimNet(synth.make_weights(), synth.make_bn(), device=local, max_batch=args.bmax, norm=args.norm)
     greedy = args.executor == "greedy"
@@ -469,15 +589,14 @@ def run_stream(args):
     # (key, batch size, instance buffers) combinations keep changing and graph capture would dominate
     slim.slim_set_graph_mode(net.ctx, not (greedy or native) or args.alg1_graphs)
     n_total = args.requests * world
-    devs, tups, grps = router.route(n_total, world, args.policy)
-    mine = router.shard(devs, rank)
-    tuples = np.asarray([router.TABLE_TUPLES[t] for t in tups[mine]], np.float32)
-    x = torch.from_numpy(synth.make_images(len(mine), offset=200 + rank)).to(torch.bfloat16).to(dev)
+    n_max = n_total                                   # a rank may receive up to the whole stream
+    x = torch.from_numpy(synth.make_images(n_max, offset=200 + rank)).to(torch.bfloat16).to(dev)
     if native:   # Alg. 1 with the LOOP itself in C++ (slim_exec_*)
-        nx = slim.NativeExecutor(net, n_max=len(mine), B_max=args.bmax, Q_th=args.q_th, N_new=args.n_new)
+        nx = slim.NativeExecutor(net, n_max=n_max, B_max=args.bmax, Q_th=args.q_th, N_new=args.n_new)
 
         class _NAdapter:
             last_batches = [[]]
+            pack_s = []
 
             def run(self, x, tuples, stream=None):
                 out = nx.run(x, tuples)
@@ -486,10 +605,11 @@ def run_stream(args):
         ex = _NAdapter()
     elif greedy:   # Alg. 1: native scheduler decisions, instances on their own CUDA streams
         from paper_2510_09018_b200.executor import GreedyExecutor
-        gx = GreedyExecutor(net, n_max=len(mine), B_max=args.bmax, Q_th=args.q_th, N_new=args.n_new)
+        gx = GreedyExecutor(net, n_max=n_max, B_max=args.bmax, Q_th=args.q_th, N_new=args.n_new)
 
         class _Adapter:
             last_batches = [[]]
+            pack_s = []
 
             def run(self, x, tuples, stream=None):
                 gx.stats["batch_sizes"] = []
@@ -498,31 +618,61 @@ def run_stream(args):
                 return out
         ex = _Adapter()
     else:
-        ex = StreamExecutor(net, n_max=len(mine), B_max=args.bmax, device=dev, lanes=args.lanes)
-        # one lane per width: partition the SMs by width as in cfg2 -- only when the stream mixes
-        # widths (a single-width stream, e.g. the "slim" policy, keeps every SM for its one lane)
-        if args.lanes > 1 and len(np.unique(tuples)) > 1:
+        ex = StreamExecutor(net, n_max=n_max, B_max=args.bmax, device=dev, lanes=args.lanes)
+        ex.cache_plans = args.repeat_stream
+        # one lane per width: partition the SMs by width as in cfg2 -- unless the policy routes a
+        # single width (the "slim" policy keeps every SM for its one lane)
+        if args.lanes > 1 and args.policy != "slim":
             cw = tuple(net.cfg.widths[i] for i in range(net.cfg.n_widths))
             for r, sh in sm_shares(cw, args.sm_share).items():
                 slim.slim_set_sm_share(net.ctx, r, sh)
-    telem = TelemetryExchange(device=dev) if world > 1 else None
-    stream = torch.cuda.current_stream(dev)
-    for _ in range(args.warmup):
-        ex.run(x, tuples, stream)
-    torch.cuda.synchronize()
     sampler = NvmlSampler(local)
+    telem = TelemetryExchange(device=dev) if world > 1 else None
+    tsrc = TelemetrySource(sampler, rank)
+    stream = torch.cuda.current_stream(dev)
+    LAG = 2
+
+    def routed(k):
+        """This rank's requests of step k: (tuples [m, 4], m) -- identical decisions on every rank."""
+        kk = 0 if args.repeat_stream else k
+        if args.policy == "ppo_frozen":
+            if telem is not None and telem.ticks() > LAG - 1:
+                rec = telem.records(telem.ticks() - LAG)
+            else:
+                rec = np.zeros((world, 8), np.float32)
+            devs, tups, _ = router.route_frozen(n_total, world, rec, t=kk, c_done=float(k * n_total))
+        else:
+            devs, tups, _ = router.route(n_total, world, args.policy, seed=2510_09018 + kk)
+        mine = router.shard(devs, rank)
+        return np.asarray(router.TABLE_TUPLES, np.float32)[tups[mine]], len(mine)
+
+    done = [0]
+
+    def one_step(k):
+        tuples, m = routed(k)
+        ex.run(x[:m], tuples, stream)
+        done[0] += m
+        if telem:
+            telem.tick(tsrc.record(queue_len=float(n_total - m), completed=float(done[0])))
+        return m
+
+    sampler.start()
+    for k in range(args.warmup):
+        one_step(k)
+    torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     l0 = slim.slim_launch_count(net.ctx)
     e0 = sampler.energy_mj()
-    sampler.start()
+    n_pack0 = len(getattr(ex, "pack_s", []))
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record(stream)
+    mine_total = 0
+    batches = []
     for k in range(args.steps):
-        ex.run(x, tuples, stream)
-        if telem:
-            telem.tick(pack_record(rank=rank, completed=(k + 1) * len(mine)))
+        mine_total += one_step(args.warmup + k)
+        batches += [bb for seg in ex.last_batches for bb in seg]
     b.record(stream)
     torch.cuda.synchronize()
     if world > 1:
@@ -534,8 +684,9 @@ def run_stream(args):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     value = n_total * args.steps / (float(t.item()) / 1e3)
-    clocks, energy = _clock_energy_json(sampler, e0, e1, len(mine) * args.steps)
-    batches = [b for seg in ex.last_batches for b in seg]
+    clocks, energy = _clock_energy_json(sampler, e0, e1, max(mine_total, 1))
+    pack = getattr(ex, "pack_s", [])[n_pack0:]
+    n_desc = len(batches)
     if rank == 0:
         print(json.dumps({
             "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps,
@@ -546,12 +697,20 @@ def run_stream(args):
                                    f"B_max={args.bmax}, routing={args.policy}, executor={args.executor}"
                                    + (f", lanes={args.lanes}" if not (greedy or native) else "")
                                    + (f" (Alg. 1: Q_th={args.q_th}, N_new={args.n_new})" if greedy or native else ""),
-                       "requests_per_rank": args.requests, "parallelism": f"dp{world} routed"},
-            "batches_per_step_rank0": len(batches),
-            "mean_batch_rank0": float(len(mine) * 4 / len(batches)) if native else float(np.mean(batches)),
+                       "requests_per_rank": args.requests, "parallelism": f"dp{world} routed",
+                       "stream": "replayed (step 0's routing every step)" if args.repeat_stream else
+                                 "fresh routing + packing every step (inside the timed region)"},
+            "batches_per_step_rank0": n_desc / args.steps,
+            "mean_batch_rank0": (float(mine_total * 4 / max(1, sum(len(s) for s in ex.last_batches) * args.steps))
+                                 if native else float(np.mean(batches)) if batches else None),
+            "packer_host_us": ({"per_step": 1e6 * float(np.mean(pack)), "per_batch": 1e6 * float(np.sum(pack)) /
+                                max(1, n_desc), "note": "slim_pack on all four segments + marshalling, host"}
+                               if pack else None),
             **({"alg1_host_s_per_step": {k: gx.stats[k] / (args.steps + args.warmup)
                                          for k in ("t_next", "t_launch", "t_wait")},
                 "alg1_instances": len(gx.sched.instances())} if greedy else {}),
+            **({"nccl": nccl, "telemetry_allgather_us_mean": 1e3 * float(np.mean(telem.gather_ms))
+                if telem.gather_ms else None} if telem else {}),
             "gpu_launches": slim.slim_launch_count(net.ctx) - l0, "energy_j_per_image": energy, "clocks": clocks,
         }))
     net.close()
@@ -822,16 +981,22 @@ def build_parser():
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--sequential", action="store_true", help="run the 4 width instances one after another")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
-    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--cpu-seconds", type=float, default=30.0, help="cpu_baseline: time budget of the oracle protocol")
+    ap.add_argument("--ref-batch", type=int, default=8, help="--impl reference: images per width per step")
     ap.add_argument("--profile-steps", type=int, default=50)
     ap.add_argument("--e2e-steps", type=int, default=200)
+    ap.add_argument("--energy-seconds", type=float, default=2.0, help="cfg2: length of the NVML energy loop (>= 1 s)")
     ap.add_argument("--json-out", default=None)
-    ap.add_argument("--workload", choices=("cfg2", "cfg1", "sweep", "stream", "handoff", "poisson"), default="cfg2",
+    ap.add_argument("--workload", choices=("cfg2", "cfg1", "sweep", "stream", "handoff", "poisson", "env"),
+                    default="cfg2",
                     help="cfg2 (default, BASELINE configs[1]); cfg1 = seg0 r=0.25 B=8; sweep = CFG3 batch sweep "
                          "(one JSON line per point); stream = CFG4/CFG5 mixed-width routed request stream")
     ap.add_argument("--requests", type=int, default=1024, help="stream: requests per rank per step")
     ap.add_argument("--bmax", type=int, default=256, help="stream: B_max of the key batching")
-    ap.add_argument("--policy", default="random", help="stream: routing policy (random | slim | table_rr)")
+    ap.add_argument("--policy", default="random",
+                    help="stream: routing policy (random | slim | table_rr | ppo_frozen)")
+    ap.add_argument("--repeat-stream", action="store_true",
+                    help="stream: replay step 0's routing every step (packer plan cached) instead of a fresh stream")
     ap.add_argument("--launch-order", choices=("asc", "desc"), default="asc",
                     help="cfg2: order in which the width instances are enqueued each step")
     ap.add_argument("--stream-priority", choices=("none", "wide", "narrow"), default="none",
@@ -861,9 +1026,55 @@ def build_parser():
     return ap
 
 
+def launcher_cmd(argv, n: int, port: int):
+    """The torchrun command bench.py re-executes itself under for --gpus N > 1 (one process per GPU,
+    rendezvous on 127.0.0.1), as the driver's own launch does."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+            "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *argv]
+
+
+def _free_port() -> int:
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def run_env(args):
+    """Diagnostic workload: each rank reports the launcher environment (and, with world > 1, a gloo
+    all-gather of the ranks proves the group spans them).  No GPU needed."""
+    world, rank, local = _dist()
+    rec = {"rank": rank, "local_rank": local, "world_size": world, "gpus_arg": args.gpus,
+           "master_addr": os.environ.get("MASTER_ADDR"), "pid": os.getpid()}
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        dist.init_process_group("gloo")
+        t = torch.tensor([rank], dtype=torch.int64)
+        got = [torch.zeros_like(t) for _ in range(world)]
+        dist.all_gather(got, t)
+        rec["gathered_ranks"] = [int(x) for x in got]
+        dist.destroy_process_group()
+    os.write(1, ("ENV " + json.dumps(rec) + "\n").encode())   # one write: ranks share the pipe
+    return 0
+
+
 def main(argv=None):
     ap = build_parser()
-    args = ap.parse_args(argv)
+    raw = list(sys.argv[1:] if argv is None else argv)
+    args = ap.parse_args(raw)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # `bench.py --gpus N` run directly: re-execute under torchrun with N ranks (the driver launches
+        # N>1 through torchrun itself, which sets WORLD_SIZE and lands in the branch below)
+        import subprocess
+        return subprocess.call(launcher_cmd(raw, args.gpus, _free_port()))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.impl != "reference" and world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world} (one rank per GPU)")
+    if args.workload == "env":
+        return run_env(args)
     assert args.warmup >= 0 and args.steps >= 1
     if args.impl == "reference":
         return run_reference(args)

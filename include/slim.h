@@ -266,6 +266,8 @@ SLIM_API slim_status slim_sched_complete(slim_sched *s, int inst, double now);
 /* UNLOADERLOOP pass: removes idle instances, writes up to max_removed ids, returns the count. */
 SLIM_API int slim_sched_unload_idle(slim_sched *s, double now, int *removed, int max_removed);
 SLIM_API int slim_sched_queue_len(const slim_sched *s);
+/* The scheduler's batch cap (knobs.B_max): the most slots/ids one slim_sched_next writes. */
+SLIM_API int slim_sched_b_max(const slim_sched *s);
 /* Copies up to max_out instance records; returns the number of live instances. */
 SLIM_API int slim_sched_instances(const slim_sched *s, slim_instance *out, int max_out);
 
@@ -276,7 +278,8 @@ SLIM_API int slim_sched_instances(const slim_sched *s, slim_instance *out, int m
  * batches (event polling) release their instance and re-enqueue their requests with key
  * (s+1, w_{s+1}, w_s); idle instances are unloaded (their buffers are recycled).
  * create: allocates the per-segment request pools for n_max requests; the scheduler
- * (B_max <= cfg.max_batch) stays owned by the caller.  run: images = device
+ * stays owned by the caller; SLIM_EINVAL unless slim_sched_b_max(sched) <= B_max <= cfg.max_batch
+ * (every buffer is sized for B_max requests per batch).  run: images = device
  * [n][H][W][in_channels]; tuples = HOST float [n][4] (the width of each segment, each in
  * cfg.widths); logits = device fp32 [n][num_classes]; vram_external as in slim_sched_next, to which
  * the executor adds the buffers of its live instances (slab, out, workspace: M_max bounds scale-up);

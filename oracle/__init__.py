@@ -67,10 +67,22 @@ def _load():
             lib.oracle_conv2d.restype = ctypes.c_int
             lib.oracle_conv2d_plain.argtypes = [dp, L, L, L, L, dp, L, L, L, L, L, L, dp]
             lib.oracle_conv2d_plain.restype = ctypes.c_int
+            lib.oracle_set_num_threads.argtypes = [ctypes.c_int]
+            lib.oracle_set_num_threads.restype = None
+            lib.oracle_max_threads.restype = ctypes.c_int
             lib.oracle_out_size.argtypes = [L, L, L, L]
             lib.oracle_out_size.restype = L
             _lib = lib
     return _lib
+
+
+def set_num_threads(n: int) -> None:
+    """OpenMP threads of the conv loops (results do not depend on it: one sequential sum per output)."""
+    _load().oracle_set_num_threads(int(n))
+
+
+def max_threads() -> int:
+    return _load().oracle_max_threads()
 
 
 def _ptr(a):

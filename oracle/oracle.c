@@ -38,10 +38,15 @@
  *                         the plain form (tests/test_oracle_pins.py pins this); it
  *                         only makes the >= 4096-image argmax checks affordable.
  */
+#include <omp.h>
 #include <stddef.h>
 #include <stdlib.h>
 
 int oracle_version(void) { return 2; }
+
+/* Thread count of the OpenMP loops (bench.py's cpu_baseline times 1 thread and all threads). */
+void oracle_set_num_threads(int n) { omp_set_num_threads(n > 0 ? n : 1); }
+int oracle_max_threads(void) { return omp_get_max_threads(); }
 
 /* Output spatial size of a k x k, stride s, padding p convolution (O2). */
 long oracle_out_size(long h_in, long k, long s, long p) { return (h_in + 2 * p - k) / s + 1; }

@@ -20,7 +20,7 @@ __all__ = [
     "SlimError", "load_library", "slim_config", "default_config", "slim_create", "slim_destroy",
     "slim_load_segment", "slim_unload_segment", "slim_segment_bytes", "slim_forward", "slim_forward_ws",
     "slim_forward_workspace_bytes", "slim_chain_workspace_bytes", "slim_forward_chain", "slim_pack",
-    "slim_launch", "slim_gather", "slim_scatter", "slim_last_error", "slim_launch_count", "slim_channels",
+    "slim_pack_arrays", "slim_launch", "slim_gather", "slim_scatter", "slim_last_error", "slim_launch_count", "slim_channels",
     "slim_act_channels", "SlimNet",
     "manifest", "LIB_PATH", "Scheduler", "NativeExecutor",
 ]
@@ -159,6 +159,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "slim_sched_complete": (_I, [_VP, _I, ctypes.c_double]),
         "slim_sched_unload_idle": (_I, [_VP, ctypes.c_double, ctypes.POINTER(_I), _I]),
         "slim_sched_queue_len": (_I, [_VP]),
+        "slim_sched_b_max": (_I, [_VP]),
         "slim_sched_instances": (_I, [_VP, ctypes.POINTER(slim_instance), _I]),
         "slim_exec_create": (_I, [_VP, _VP, _I, _I, ctypes.POINTER(_VP)]),
         "slim_exec_destroy": (None, [_VP]),
@@ -180,7 +181,7 @@ EXPORTED = ("slim_create", "slim_destroy", "slim_default_config", "slim_load_seg
             "slim_launch_count", "slim_num_sms", "slim_channels", "slim_act_channels", "slim_set_graph_mode", "slim_set_sm_share", "slim_profile_begin",
             "slim_profile_end", "slim_sched_default_knobs", "slim_sched_create", "slim_sched_destroy",
             "slim_sched_enqueue", "slim_sched_next", "slim_sched_complete", "slim_sched_unload_idle",
-            "slim_sched_queue_len", "slim_sched_instances", "slim_exec_create", "slim_exec_destroy", "slim_exec_run")
+            "slim_sched_queue_len", "slim_sched_b_max", "slim_sched_instances", "slim_exec_create", "slim_exec_destroy", "slim_exec_run")
 
 
 # ------------------------------------------------------------------ marshalling helpers
@@ -329,6 +330,33 @@ def slim_pack(cfg: slim_config, requests, B_max: int):
     _check(None, load_library().slim_pack(ctypes.byref(cfg), q, n, B_max, descs, max(n, 1), ctypes.byref(nd), order))
     out = [dict(seg=d.seg, r_prev=d.r_prev, r=d.r, batch=d.batch, first=d.first) for d in descs[:nd.value]]
     return out, np.frombuffer(order, dtype=np.uint32, count=n).copy()
+
+
+# numpy mirror of slim_request (include/slim.h): marshal a whole request array without a Python loop
+_REQ_DTYPE = np.dtype({"names": ["id", "seg", "w_req", "w_prev", "slot"],
+                       "formats": [np.uint64, np.int32, np.float32, np.float32, np.uint32],
+                       "offsets": [0, 8, 12, 16, 20], "itemsize": ctypes.sizeof(slim_request)})
+
+
+def slim_pack_arrays(cfg: slim_config, seg: int, w_req, w_prev, B_max: int, ids=None, slots=None):
+    """slim_pack on arrays (one segment): request i = (id ids[i] (default i), seg, w_req[i], w_prev[i],
+    slot slots[i] (default i)).  Marshalling only, vectorised.  Returns (descs list, order ndarray)."""
+    w_req = np.asarray(w_req, np.float32)
+    n = w_req.shape[0]
+    q = np.zeros(max(n, 1), _REQ_DTYPE)
+    q["id"][:n] = np.arange(n) if ids is None else ids
+    q["seg"][:n] = seg
+    q["w_req"][:n] = w_req
+    q["w_prev"][:n] = np.asarray(w_prev, np.float32) if seg else 0.0
+    q["slot"][:n] = np.arange(n) if slots is None else slots
+    descs = (slim_launch_desc * max(n, 1))()
+    order = np.zeros(max(n, 1), np.uint32)
+    nd = ctypes.c_int()
+    _check(None, load_library().slim_pack(ctypes.byref(cfg), q.ctypes.data_as(ctypes.POINTER(slim_request)), n,
+                                          B_max, descs, max(n, 1), ctypes.byref(nd),
+                                          order.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32))))
+    out = [dict(seg=d.seg, r_prev=d.r_prev, r=d.r, batch=d.batch, first=d.first) for d in descs[:nd.value]]
+    return out, order[:n]
 
 
 def slim_launch(ctx, desc: dict, slots, pool, pool_row_bytes, slab, out, ws, ws_bytes, stream=None):

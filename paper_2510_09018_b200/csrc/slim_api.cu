@@ -1039,9 +1039,10 @@ slim_status conv_f32(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, int ri,
     a.out = static_cast<float *>(cc.out);
     a.epi = cc.epi;
     a.relu_lo = cc.relu_lo;
-    {   // SM share of this width: 2 resident GEMM CTAs per SM of the share (persistent over tiles)
-        const int cap = grid_cap(ctx, ri, 1 << 30, cc.seg);
-        a.max_ctas = cap < (1 << 30) ? 2 * cap : 0;
+    {   // SM share of this width (< 1, or SLIM_GRID_CAP): 2 resident GEMM CTAs per SM of the share,
+        // persistent over tiles; at the full share: one CTA per tile (max_ctas = 0)
+        const int cap = grid_cap(ctx, ri, ctx->num_sms, cc.seg);
+        a.max_ctas = cap < ctx->num_sms ? 2 * cap : 0;
     }
     double flops, bytes;
     conv_work(c, cc, ri, B, a.Ho, a.Wo, &flops, &bytes);

@@ -87,7 +87,8 @@ slim_status slim_exec_create(slim_ctx *ctx, slim_sched *sched, int n_max, int B_
     x->sched = sched;
     x->cfg = *slim::ctx_config(ctx);
     const slim_config &c = x->cfg;
-    if (B_max > c.max_batch) {
+    // slim_sched_next writes up to the scheduler's B_max slots/ids into buffers sized for B_max
+    if (B_max > c.max_batch || slim_sched_b_max(sched) > B_max) {
         delete x;
         return SLIM_EINVAL;
     }

@@ -236,6 +236,8 @@ int slim_sched_unload_idle(slim_sched *s, double now, int *removed, int max_remo
     return n;
 }
 
+int slim_sched_b_max(const slim_sched *s) { return s ? s->k.B_max : 0; }
+
 int slim_sched_queue_len(const slim_sched *s) {
     if (!s) return -1;
     std::lock_guard<std::mutex> g(const_cast<slim_sched *>(s)->mu);

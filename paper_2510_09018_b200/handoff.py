@@ -189,7 +189,8 @@ class HandoffExecutor:
             if s < 3 and self.world > 1:
                 send_buf, sb, rb = self.pack(s, dev, stream)
                 recv_buf = torch.empty(max(sum(rb), 1), dtype=torch.uint8, device=self.dev)
-                torch.cuda.current_stream(self.dev).synchronize()   # rows packed before the collective reads them
+                # rows packed (on the stream compute/pack used) before the collective reads them
+                (stream if stream is not None else torch.cuda.current_stream(self.dev)).synchronize()
                 transport.exchange(send_buf, sb, recv_buf[:sum(rb)], rb)
                 self.unpack(s, dev, recv_buf, stream)
         return self.logits

@@ -11,8 +11,14 @@ needs is a *replicated, deterministic* routing decision so that every rank of th
 * ``slim``     -- every request at the slimmest tuple (0.25)^4, round-robin devices
                   (the behaviour the "overfit" PPO converged to, Table IV).
 * ``table_rr`` -- round-robin devices, width tuples cycling through Tables I-II.
+* ``ppo_frozen`` -- the factored policy itself (Eqs. 1-6, `ppo_router.FrozenRouter`, frozen seeded
+                  weights): each action a = (server, width, group g) takes the next g requests of the
+                  FIFO; the state (Eq. 1) is built from the telemetry all-gathered one tick earlier,
+                  with each server's queue length advanced by what this tick already assigned to it
+                  (`route_frozen`).
 
-All ranks call `route()` with the same seed and obtain identical assignments.
+All ranks call `route()` / `route_frozen()` with the same seed (and the same gathered telemetry) and
+obtain identical assignments.
 """
 from __future__ import annotations
 
@@ -25,7 +31,9 @@ TABLE_TUPLES = (
 )
 # micro-batch group sizes G for the factored action (knob; the paper gives no values)
 GROUPS = (16, 64, 256)
-POLICIES = ("random", "slim", "table_rr")
+POLICIES = ("random", "slim", "table_rr", "ppo_frozen")
+# uniform tuple (w, w, w, w) of a width the frozen policy picks -> its index in TABLE_TUPLES
+_UNIFORM = {0.25: 0, 0.5: 1, 0.75: 2, 1.0: 3}
 
 
 def route(n: int, world: int, policy: str = "random", seed: int = 2510_09018):
@@ -33,6 +41,8 @@ def route(n: int, world: int, policy: str = "random", seed: int = 2510_09018):
 
     Deterministic in (n, world, policy, seed): identical on every rank.
     """
+    if policy == "ppo_frozen":     # no telemetry yet: the state of an idle cluster at t = 0
+        return route_frozen(n, world, np.zeros((world, 8), np.float32), 0, seed=seed)
     if policy not in POLICIES:
         raise ValueError(f"unknown policy {policy!r}; one of {POLICIES}")
     g = np.random.Generator(np.random.PCG64([seed, 77]))
@@ -54,3 +64,36 @@ def route(n: int, world: int, policy: str = "random", seed: int = 2510_09018):
 def shard(dev: np.ndarray, rank: int) -> np.ndarray:
     """Indices of the requests this rank executes."""
     return np.nonzero(dev == rank)[0]
+
+
+_FROZEN = {}
+
+
+def route_frozen(n: int, world: int, records, t: int, c_done: float = 0.0, seed: int = 2510_09018):
+    """Route n FIFO requests with the frozen factored PPO router (Eqs. 1-6).
+
+    records: the all-gathered telemetry float32[world, 8] of the previous tick (telemetry.FIELDS).
+    Repeatedly: s = Eq. 1 state (q_fifo = requests still unrouted, c_done, per server (q_i + routed_i,
+    P_i, U_i)); a = (srv, w, g) ~ pi~(.|s) at step t (Eqs. 4-5); the next g requests go to srv at the
+    uniform tuple (w, w, w, w).  The sampling RNG is seeded by (seed, t): deterministic in
+    (n, world, records, t), hence identical on every rank that holds the same gathered records.
+    Returns (device[n], tuple_index[n], group[n]) like `route`."""
+    from .ppo_router import FrozenRouter, state_vector
+    if world not in _FROZEN:
+        _FROZEN[world] = FrozenRouter(FrozenRouter.init(world, seed=seed), groups=GROUPS)
+    fr = _FROZEN[world]
+    rec = np.asarray(records, np.float64).reshape(world, -1)
+    g = np.random.Generator(np.random.PCG64([seed, 78, int(t)]))
+    dev = np.empty(n, np.int64)
+    tup = np.empty(n, np.int64)
+    grp = np.empty(n, np.int64)
+    routed = np.zeros(world)
+    i = 0
+    while i < n:
+        s = state_vector(n - i, c_done, [(rec[k, 0] + routed[k], rec[k, 1], rec[k, 2]) for k in range(world)])
+        srv, w, gsz, _ = fr.act(s, t, g)
+        j = min(n, i + gsz)
+        dev[i:j], tup[i:j], grp[i:j] = srv, _UNIFORM[w], gsz
+        routed[srv] += j - i
+        i = j
+    return dev, tup, grp

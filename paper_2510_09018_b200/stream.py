@@ -18,10 +18,12 @@ for n_max requests; graph mode caches one CUDA graph per (group shape, buffers).
 """
 from __future__ import annotations
 
+import time
+
 import numpy as np
 import torch
 
-from . import SlimNet, slim_act_channels, slim_forward_workspace_bytes, slim_launch, slim_pack, slim_scatter
+from . import SlimNet, slim_act_channels, slim_forward_workspace_bytes, slim_launch, slim_pack_arrays, slim_scatter
 
 
 class StreamExecutor:
@@ -56,25 +58,42 @@ class StreamExecutor:
         self.slab, self.out, self.ws = self.lane_buf[0]
         self.lane_streams = [torch.cuda.Stream(device=self.dev) for _ in range(self.lanes)] if self.lanes > 1 else []
         self.widths = [cfg.widths[i] for i in range(cfg.n_widths)]
-        self.order_h = torch.empty(4 * n_max, dtype=torch.int32).pin_memory()
+        # two pinned staging buffers for the per-segment request orders, used alternately: a buffer is
+        # rewritten only after the H2D copy that last read it (enqueued on the run's stream) is done
+        self.order_h = [torch.empty(4 * n_max, dtype=torch.int32).pin_memory() for _ in range(2)]
+        self._order_ev = [None, None]
+        self._buf = 0
         self.order_d = torch.empty(4 * n_max, dtype=torch.int32, device=self.dev)
         self._plan_key = None
         self.last_batches = []
+        self.cache_plans = True     # False: pack every call (a fresh request stream each step)
+        self.pack_s = []            # host seconds of each packing (slim_pack on all four segments)
 
-    def _plan(self, tuples: np.ndarray):
-        """Pack all four segments (host only; cached for a repeated stream)."""
+    def _plan(self, tuples: np.ndarray, st):
+        """Pack all four segments (host only) and stage the request orders to the device on `st`.
+        Cached for a repeated stream unless cache_plans is False."""
         key = (tuples.shape[0], hash(tuples.tobytes()))
-        if key == self._plan_key:
+        if self.cache_plans and key == self._plan_key:
             return self._plan_cache
         n = tuples.shape[0]
+        t0 = time.perf_counter()
         plan = []
         for s in range(4):
-            reqs = [(i, s, float(tuples[i, s]), float(tuples[i, s - 1]) if s else 0.0, i) for i in range(n)]
-            descs, order = slim_pack(self.cfg, reqs, self.B_max)
+            descs, order = slim_pack_arrays(self.cfg, s, tuples[:, s], tuples[:, s - 1] if s else None, self.B_max)
             plan.append((descs, order.astype(np.int32)))
+        self.pack_s.append(time.perf_counter() - t0)
         self._plan_key, self._plan_cache = key, plan
-        self.order_h[:4 * n].view(4, n).copy_(torch.from_numpy(np.stack([p[1] for p in plan])))
-        self.order_d[:4 * n].copy_(self.order_h[:4 * n], non_blocking=True)
+        b = self._buf
+        self._buf ^= 1
+        if self._order_ev[b] is not None:
+            self._order_ev[b].synchronize()        # the copy that last read order_h[b] has run
+        oh = self.order_h[b]
+        oh[:4 * n].view(4, n).copy_(torch.from_numpy(np.stack([p[1] for p in plan])))
+        with torch.cuda.stream(st):               # ordered before the lanes forked from st read order_d
+            self.order_d[:4 * n].copy_(oh[:4 * n], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(st)
+        self._order_ev[b] = ev
         self.last_batches = [[d["batch"] for d in p[0]] for p in plan]
         return plan
 
@@ -83,8 +102,8 @@ class StreamExecutor:
         Returns the logits [n, classes] (a view into the executor's buffer)."""
         n = images.shape[0]
         assert n <= self.n_max and tuples.shape == (n, 4)
-        plan = self._plan(np.asarray(tuples, np.float32))
         st = stream if stream is not None else torch.cuda.current_stream(self.dev)
+        plan = self._plan(np.asarray(tuples, np.float32), st)
         hw, cfg = self.cfg.image_hw, self.cfg
         for s in range(4):
             descs, _ = plan[s]

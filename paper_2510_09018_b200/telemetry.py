@@ -78,10 +78,18 @@ class NvmlSampler:
             reasons = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
         except Exception:
             reasons = nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+        try:
+            energy_mj = nv.nvmlDeviceGetTotalEnergyConsumption(h)
+        except Exception:
+            energy_mj = None
         return dict(t=time.time(), sm=nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM),
                     power_w=nv.nvmlDeviceGetPowerUsage(h) / 1000.0,
                     util=nv.nvmlDeviceGetUtilizationRates(h).gpu / 100.0, reasons=int(reasons),
-                    mem_gb=nv.nvmlDeviceGetMemoryInfo(h).used / 2 ** 30)
+                    mem_gb=nv.nvmlDeviceGetMemoryInfo(h).used / 2 ** 30, energy_mj=energy_mj)
+
+    def latest(self):
+        """The most recent background sample (None before the first); no NVML call on the caller."""
+        return self.samples[-1] if self.samples else None
 
     def _run(self):
         while not self._stop.is_set():
@@ -119,6 +127,29 @@ class NvmlSampler:
                 "samples": len(self.samples), "power_w_max": max(s["power_w"] for s in self.samples)}
 
 
+class TelemetrySource:
+    """Fills this rank's float32[8] record (FIELDS) for a router tick from the background NVML
+    sampler's latest sample -- power (W), utilisation (fraction), VRAM (GB), energy (J) since the
+    previous tick -- plus what the executor knows: queue length, mean latency (s), completed requests.
+    The tick itself makes no NVML call (the sampler thread does, every period_s)."""
+
+    def __init__(self, sampler: "NvmlSampler", rank: int):
+        self.sampler, self.rank = sampler, rank
+        self._e_prev = None
+
+    def record(self, queue_len: float = 0.0, mean_latency_s: float = 0.0, completed: float = 0.0) -> np.ndarray:
+        s = self.sampler.latest() if self.sampler is not None else None
+        if s is None:
+            return pack_record(queue_len=queue_len, mean_latency_s=mean_latency_s, completed=completed, rank=self.rank)
+        e = s.get("energy_mj")
+        de = 0.0 if (e is None or self._e_prev is None) else (e - self._e_prev) / 1e3
+        if e is not None:
+            self._e_prev = e
+        return pack_record(queue_len=queue_len, power_w=s["power_w"], util=s["util"],
+                           mean_latency_s=mean_latency_s, energy_j=de, completed=completed,
+                           vram_gb=s["mem_gb"], rank=self.rank)
+
+
 class TelemetryExchange:
     """One all_gather_into_tensor of float32[8] per rank per router tick."""
 
@@ -137,6 +168,15 @@ class TelemetryExchange:
         self._ring = [torch.zeros(RECORD_LEN, dtype=torch.float32).pin_memory() for _ in range(4)] \
             if self.stream is not None else None
         self._ev = [torch.cuda.Event() for _ in range(4)] if self.stream is not None else None
+        # per-tick result ring: tick i gathers into recv_ring[i % 4] and copies it to a pinned host buffer;
+        # records(i) waits for that copy only (a fixed lag, so every rank reads the same tick's state)
+        if self.stream is not None:
+            self._recv_ring = [torch.zeros(self.world * RECORD_LEN, dtype=torch.float32, device=self.device)
+                               for _ in range(4)]
+            self._host_ring = [torch.zeros(self.world * RECORD_LEN, dtype=torch.float32).pin_memory()
+                               for _ in range(4)]
+            self._hev = [torch.cuda.Event() for _ in range(4)]
+        self._cpu_hist = {}
         self._k = 0
         # device time of each all-gather on the side stream (CFG5 "telemetry all-gather overhead")
         self._t = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(4)] \
@@ -158,6 +198,7 @@ class TelemetryExchange:
                 ta, tb = self._t[i]
                 tb.synchronize()
                 self.gather_ms.append(ta.elapsed_time(tb))
+            self.recv = self._recv_ring[i]
             with torch.cuda.stream(self.stream):
                 self.send.copy_(self._ring[i], non_blocking=True)
                 self._ev[i].record(self.stream)
@@ -165,15 +206,35 @@ class TelemetryExchange:
                 work = self.dist.all_gather_into_tensor(self.recv, self.send, group=self.group, async_op=True)
                 work.wait()   # NCCL: the side stream (not the host) waits for the collective
                 self._t[i][1].record(self.stream)
+                self._host_ring[i].copy_(self.recv, non_blocking=True)
+                self._hev[i].record(self.stream)
         else:
             self.send.copy_(rec)
             work = self.dist.all_gather_into_tensor(self.recv, self.send, group=self.group, async_op=True)
+            work.wait()
+            self._cpu_hist[self._k] = self.recv.clone()
+            self._cpu_hist.pop(self._k - 8, None)
+            self._k += 1
         if wait:
             work.wait()
             if self.stream is not None:
                 self.stream.synchronize()
             return self.recv.view(self.world, RECORD_LEN).cpu().numpy()
         return work
+
+    def ticks(self) -> int:
+        """Number of ticks started so far (tick indices 0 .. ticks()-1)."""
+        return self._k
+
+    def records(self, tick: int) -> np.ndarray:
+        """The [world, 8] records all-gathered at tick `tick` (one of the last 4; waits only for that
+        tick's copy).  Reading a fixed number of ticks back keeps every rank on the same state."""
+        if self.stream is not None:
+            assert self._k - 4 <= tick < self._k, "tick outside the 4-entry ring"
+            i = tick % 4
+            self._hev[i].synchronize()
+            return self._host_ring[i].view(self.world, RECORD_LEN).numpy().copy()
+        return self._cpu_hist[tick].view(self.world, RECORD_LEN).numpy().copy()
 
     def gathered(self) -> np.ndarray:
         if self.stream is not None:

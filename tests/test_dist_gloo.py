@@ -41,6 +41,18 @@ def _worker(rank, world, port, q):
         ex = TelemetryExchange(device="cpu")
         g = ex.tick(pack_record(queue_len=rank + 1, power_w=100.0 * (rank + 1), util=0.5 * rank, rank=rank), wait=True)
         out["telemetry"] = g.tolist()
+        # 3. frozen PPO routing on the gathered state (one tick late): identical on both ranks, and
+        #    it reads the state (a different gathered record routes differently)
+        def _hash(a):
+            h = torch.tensor([int(np.bitwise_xor.reduce(a[0] * 1000003 + a[1] * 31 + a[2]))], dtype=torch.int64)
+            hs = [torch.zeros_like(h) for _ in range(world)]
+            dist.all_gather(hs, h)
+            return [int(x) for x in hs]
+        rt = router.route_frozen(2000, world, g, t=3)
+        out["frozen_hashes"] = _hash(rt)
+        busy = g.copy(); busy[0, 0] += 5000.0                    # rank 0's queue much longer
+        out["frozen_differs"] = not np.array_equal(router.route_frozen(2000, world, busy, t=3)[0], rt[0])
+        out["frozen_counts"] = np.bincount(rt[0], minlength=world).tolist()
         q.put((rank, out))
     finally:
         dist.destroy_process_group()
@@ -78,6 +90,16 @@ def test_telemetry_allgather_layout(gloo_results):
         assert g.shape == (2, RECORD_LEN)
         assert list(g[:, 0]) == [1.0, 2.0] and list(g[:, 1]) == [100.0, 200.0]
         assert list(g[:, 7]) == [0.0, 1.0]
+
+
+def test_frozen_policy_routing_replicated(gloo_results):
+    """--policy ppo_frozen: both ranks derive the same assignment from the all-gathered telemetry."""
+    for r in (0, 1):
+        h = gloo_results[r]["frozen_hashes"]
+        assert h[0] == h[1]
+        assert gloo_results[r]["frozen_differs"]
+        assert sum(gloo_results[r]["frozen_counts"]) == 2000
+    assert gloo_results[0]["frozen_hashes"] == gloo_results[1]["frozen_hashes"]
 
 
 def test_util_variance_spec_example():

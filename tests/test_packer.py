@@ -71,3 +71,19 @@ def test_random_streams_property():
             queue = [i for i in queue if i not in batch]
         got = [order[d["first"]:d["first"] + d["batch"]].tolist() for d in descs]
         assert got == ref
+
+
+@pytest.mark.parametrize("seg", [0, 1, 3])
+def test_pack_arrays_equals_pack(seg):
+    """The vectorised marshalling (slim_pack_arrays) hands the packer the same requests."""
+    g = np.random.default_rng(seg)
+    W = (0.25, 0.5, 0.75, 1.0)
+    n = 300
+    wr = np.asarray(W)[g.integers(0, 4, n)]
+    wp = np.asarray(W)[g.integers(0, 4, n)]
+    reqs = [(i, seg, float(wr[i]), float(wp[i]) if seg else 0.0, i) for i in range(n)]
+    d1, o1 = slim.slim_pack(cfg(), reqs, 64)
+    d2, o2 = slim.slim_pack_arrays(cfg(), seg, wr, wp if seg else None, 64)
+    assert d1 == d2 and np.array_equal(o1, o2)
+    d3, o3 = slim.slim_pack_arrays(cfg(), seg, wr[:0], wp[:0], 64)
+    assert d3 == [] and o3.shape == (0,)
