@@ -325,7 +325,7 @@ def run_ours(args):
     for k in range(K):
         flush.zero_()
         ev[k][0].record(stream)
-        step(evw[k])
+        step(evw[k] if args.width_events else None)
         ev[k][1].record(stream)
         tick(k, ev)
     torch.cuda.synchronize()
@@ -340,7 +340,8 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_max_ms = float(t.item())
     value = world * imgs_per_step * K / (total_max_ms / 1e3)
-    in_step_ms = {r: float(np.mean([e[r][0].elapsed_time(e[r][1]) for e in evw])) for r in WIDTHS}
+    in_step_ms = ({r: float(np.mean([e[r][0].elapsed_time(e[r][1]) for e in evw])) for r in WIDTHS}
+                  if args.width_events else None)
 
     # ---------------- energy (Eq. 7's E_t = P * L): the same step, L2 flush included, in a loop
     # of >= args.energy_seconds; NVML total-energy counter delta / images.  Clocks sampled throughout.
@@ -452,13 +453,14 @@ def run_ours(args):
     for r in WIDTHS:
         d = by_width.get(r, by_width.get(float(np.float32(r))))
         roof_ms = d["roof_ms"] / KP if d else None
-        per_width[str(r)] = {
+        per_width[str(r)] = {} if in_step_ms is None else {
             "images_per_s_in_step": B / (in_step_ms[r] / 1e3), "ms_in_step": in_step_ms[r],
-            "per_layer_roofline_frac_in_step": roof_ms / in_step_ms[r] if roof_ms else None,
+            "per_layer_roofline_frac_in_step": roof_ms / in_step_ms[r] if roof_ms else None}
+        per_width[str(r)].update({
             "images_per_s_alone": B / (width_ms[r] / 1e3), "ms_alone": width_ms[r],
             "per_layer_roofline_frac_alone": roof_ms / width_ms[r] if roof_ms else None,
             "per_layer_roofline_ms": roof_ms, "gflop_per_batch": d["flops"] / KP / 1e9 if d else None,
-            "tflops_alone": d["flops"] / KP / (width_ms[r] / 1e3) / 1e12 if d else None}
+            "tflops_alone": d["flops"] / KP / (width_ms[r] / 1e3) / 1e12 if d else None})
 
     # ---------------- e2e through the public API with host buffers
     # Every step copies its images from pinned host memory and reads its logits back.  As a
@@ -525,7 +527,8 @@ def run_ours(args):
                                     f"{len(WIDTHS)} width instances, one CUDA stream each, run concurrently",
                        "sm_share": {str(r): v for r, v in shares.items()}},
             "per_width": per_width,
-            "per_width_images_per_s": {k: v["images_per_s_in_step"] for k, v in per_width.items()},
+            "per_width_images_per_s": {k: v.get("images_per_s_in_step", v["images_per_s_alone"])
+                                       for k, v in per_width.items()},
             "roofline": roof,
             "kernel_time_by_kind_ms_per_step_standalone": {k: v["ms"] / KP for k, v in by_kind.items()},
             "gpu_launches": launches,
@@ -587,7 +590,11 @@ def run_stream(args):
             slim.slim_set_sm_share(net.ctx, r, sh)
     # Alg. 1 executors: eager launches by default -- their batches land on whichever instance is free, so
     # (key, batch size, instance buffers) combinations keep changing and graph capture would dominate
-    slim.slim_set_graph_mode(net.ctx, not (greedy or native) or args.alg1_graphs)
+    # stream executor: CUDA graphs pay off only when batch shapes repeat (--repeat-stream); a fresh
+    # stream changes every key's batch size each step, so eager launches (no per-step capture)
+    graphs = args.alg1_graphs if (greedy or native) else (
+        args.repeat_stream if args.stream_graphs == "auto" else args.stream_graphs == "on")
+    slim.slim_set_graph_mode(net.ctx, graphs)
     n_total = args.requests * world
     n_max = n_total                                   # a rank may receive up to the whole stream
     x = torch.from_numpy(synth.make_images(n_max, offset=200 + rank)).to(torch.bfloat16).to(dev)
@@ -677,14 +684,27 @@ def run_stream(args):
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    sampler.stop()
-    e1 = sampler.energy_mj()
     ms = a.elapsed_time(b)
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     value = n_total * args.steps / (float(t.item()) / 1e3)
-    clocks, energy = _clock_energy_json(sampler, e0, e1, max(mine_total, 1))
+    # energy: the same steps continued for >= --energy-seconds (NVML counter delta / this rank's images)
+    e0 = sampler.energy_mj()
+    t0 = time.perf_counter()
+    n_e = 0
+    k = args.warmup + args.steps
+    while True:
+        n_e += one_step(k)
+        k += 1
+        if k % 8 == 0:
+            torch.cuda.synchronize()
+            if time.perf_counter() - t0 >= args.energy_seconds:
+                break
+    torch.cuda.synchronize()
+    sampler.stop()
+    e1 = sampler.energy_mj()
+    clocks, energy = _clock_energy_json(sampler, e0, e1, max(n_e, 1))
     pack = getattr(ex, "pack_s", [])[n_pack0:]
     n_desc = len(batches)
     if rank == 0:
@@ -699,7 +719,8 @@ def run_stream(args):
                                    + (f" (Alg. 1: Q_th={args.q_th}, N_new={args.n_new})" if greedy or native else ""),
                        "requests_per_rank": args.requests, "parallelism": f"dp{world} routed",
                        "stream": "replayed (step 0's routing every step)" if args.repeat_stream else
-                                 "fresh routing + packing every step (inside the timed region)"},
+                                 "fresh routing + packing every step (inside the timed region)",
+                       "graphs": graphs},
             "batches_per_step_rank0": n_desc / args.steps,
             "mean_batch_rank0": (float(mine_total * 4 / max(1, sum(len(s) for s in ex.last_batches) * args.steps))
                                  if native else float(np.mean(batches)) if batches else None),
@@ -985,6 +1006,9 @@ def build_parser():
     ap.add_argument("--ref-batch", type=int, default=8, help="--impl reference: images per width per step")
     ap.add_argument("--profile-steps", type=int, default=50)
     ap.add_argument("--e2e-steps", type=int, default=200)
+    ap.add_argument("--width-events", type=int, default=1,
+                    help="cfg2: record CUDA events around each width's chain inside the timed step (per-width "
+                         "time in the concurrent step); 0 = off")
     ap.add_argument("--energy-seconds", type=float, default=2.0, help="cfg2: length of the NVML energy loop (>= 1 s)")
     ap.add_argument("--json-out", default=None)
     ap.add_argument("--workload", choices=("cfg2", "cfg1", "sweep", "stream", "handoff", "poisson", "env"),
@@ -995,6 +1019,8 @@ def build_parser():
     ap.add_argument("--bmax", type=int, default=256, help="stream: B_max of the key batching")
     ap.add_argument("--policy", default="random",
                     help="stream: routing policy (random | slim | table_rr | ppo_frozen)")
+    ap.add_argument("--stream-graphs", choices=("auto", "on", "off"), default="auto",
+                    help="stream: CUDA-graph replay per batch shape (auto: only with --repeat-stream)")
     ap.add_argument("--repeat-stream", action="store_true",
                     help="stream: replay step 0's routing every step (packer plan cached) instead of a fresh stream")
     ap.add_argument("--launch-order", choices=("asc", "desc"), default="asc",
