@@ -322,7 +322,8 @@ SLIM_API slim_status slim_set_sm_share(slim_ctx *ctx, float r, float share);
  * is bypassed while profiling.  begin() allocates the events (at most
  * max_launches records); end() synchronises and returns the records. */
 typedef enum { SLIM_K_STEM = 0, SLIM_K_CONV_UMMA = 1, SLIM_K_HEAD = 2, SLIM_K_GATHER = 3, SLIM_K_CONV_F32 = 4,
-               SLIM_K_GN = 5 /* GroupNorm apply (SLIM_NORM_GN) */ } slim_kernel_kind;
+               SLIM_K_GN = 5 /* GroupNorm apply (SLIM_NORM_GN) */,
+               SLIM_K_SEG_FUSED = 6 /* a whole segment in one kernel (narrow widths) */ } slim_kernel_kind;
 typedef struct {
     int kind;                  /* slim_kernel_kind */
     int seg, layer;            /* segment, manifest index of the conv (stem = 0 in seg 0; head/gather: -1) */

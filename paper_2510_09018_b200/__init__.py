@@ -74,7 +74,7 @@ class slim_profile_record(ctypes.Structure):
                 ("bytes", ctypes.c_double), ("ms", ctypes.c_float)]
 
 
-KERNEL_KINDS = {0: "stem", 1: "conv_umma", 2: "head", 3: "gather", 4: "conv_f32", 5: "gn"}
+KERNEL_KINDS = {0: "stem", 1: "conv_umma", 2: "head", 3: "gather", 4: "conv_f32", 5: "gn", 6: "seg_fused"}
 
 
 class slim_launch_desc(ctypes.Structure):

@@ -55,6 +55,7 @@ struct DevSegment {
     bool loaded = false;
     int n_conv = 0;
     DevLayer L[kMaxLayers];
+    void *fimg[kMaxW][kMaxW] = {};           // fused-segment weight image per (r_prev idx, r idx) (seg >= 1)
     float *fc_w = nullptr, *fc_b = nullptr;
 };
 
@@ -1139,6 +1140,78 @@ slim_status run_segment(slim_ctx *ctx, int seg, int ri_prev, int ri, int B, cons
     const void *cur = in;
     int curH = (seg == 0) ? H : (H * 2);
     int curC = (seg == 0) ? c.in_channels : slim_act_channels(c.widths[ri_prev], c.base_channels[seg - 1]);
+    // segment 0 at a narrow width: stem + both blocks in one kernel, activations in shared memory
+    // (kernels_fused.cu; bit-identical to the per-layer kernels below).  SLIM_NO_FUSED=1: per-layer path.
+    static const bool no_fused = getenv("SLIM_NO_FUSED") != nullptr;
+    if (seg == 0 && bf && !gn && !no_fused && (C == 16 || C == 32) && C == slim_channels(r, c.base_channels[0]) &&
+        H == 32 && c.in_channels == 3 && c.blocks_per_seg[0] == 2 && S.L[1].sh.cin % 8 == 0) {
+        FusedSeg0Args fa{};
+        fa.in = static_cast<const uint16_t *>(in);
+        fa.out = static_cast<uint16_t *>(out);
+        fa.B = B;
+        fa.c0 = C;
+        fa.cin_full = S.L[1].sh.cin;
+        for (int l = 0; l < 4; ++l) fa.w[l] = static_cast<const uint16_t *>(S.L[1 + l].w);
+        fa.stem_b = S.L[0].stem_b;
+        fa.trace = ctx->trace ? ctx->trace + 8192 : nullptr;
+        for (int l = 0; l < 5; ++l) {
+            fa.scale[l] = S.L[l].scale[ri];
+            fa.shift[l] = S.L[l].shift[ri];
+        }
+        const double pix = static_cast<double>(B) * H * H;
+        const double flops = 2.0 * pix * C * 9 * (c.in_channels + 4.0 * C);
+        const double bytes = eb * pix * (c.in_channels + C) + 2.0 * 4 * 9 * C * C + 2.0 * 64 * C + 40.0 * C;
+        int grid = std::min(B, ctx->num_sms);
+        grid = grid_cap(ctx, ri, grid, 0);
+        LaunchProf prof(ctx, st);
+        const cudaError_t e = launch_seg0_fused(fa, grid, st, ctx->pdl && !ctx->prof_on);
+        prof.done(SLIM_K_SEG_FUSED, 0, 0, r, r, B, flops, bytes);
+        if (e != cudaSuccess) return fail(ctx, SLIM_ECUDA, "fused segment-0 launch: %s", cudaGetErrorString(e));
+        return SLIM_OK;
+    }
+    // segments 1-3 at a narrow width: both blocks in one kernel (kernels_fused.cu) where it measured faster
+    // than the per-layer kernels at B = 8 and 128 (profiles/r02_fused_micro.txt): segment 1 at C <= 64
+    // (r <= 0.5), segment 2 at C <= 64 (r = 0.25); segment 3 (8-image units, 16 CTAs at B = 128, ~1 MB of
+    // weights streamed per unit) stays per-layer.  SLIM_FUSED_SEGS (bit s = segment s) overrides; the
+    // (r_prev, r) weight image must exist (the kernel's working set fits in shared memory).
+    static const int fused_env = getenv("SLIM_FUSED_SEGS") ? atoi(getenv("SLIM_FUSED_SEGS")) : -1;
+    const bool fused_on = fused_env >= 0 ? ((fused_env >> seg) & 1) != 0 : (seg == 1 || (seg == 2 && C <= 64));
+    if (seg > 0 && bf && !gn && !no_fused && fused_on && S.fimg[ri_prev][ri]) {
+        FusedSegArgs fa{};
+        fa.in = static_cast<const uint16_t *>(in);
+        fa.B = B;
+        fa.CI = curC;
+        fa.wimg = static_cast<const uint8_t *>(S.fimg[ri_prev][ri]);
+        const bool last = seg == 3;
+        float *pooled = nullptr;
+        if (last) pooled = reinterpret_cast<float *>(bufs[0]);   // fp32 [B][C] for the FC
+        else fa.out = static_cast<uint16_t *>(out);
+        fa.pool_out = pooled;
+        for (int l = 0; l < 5; ++l) {
+            fa.scale[l] = S.L[l].scale[ri];
+            fa.shift[l] = S.L[l].shift[ri];
+        }
+        const int G = seg == 1 ? 1 : (seg == 2 ? 2 : 8);
+        const double pix = static_cast<double>(B) * H * H;
+        const double flops = 2.0 * pix * C * (9.0 * curC + 27.0 * C + curC);
+        const double bytes = eb * (static_cast<double>(B) * 4 * H * H * curC + (last ? 2.0 * B * C : pix * C)) +
+                             static_cast<double>(segn_fused_image_bytes(C, curC));
+        int grid = std::min((B + G - 1) / G, ctx->num_sms);
+        grid = grid_cap(ctx, ri, grid, seg);
+        LaunchProf prof(ctx, st);
+        const cudaError_t e = launch_segn_fused(fa, seg, C, grid, st, ctx->pdl && !ctx->prof_on);
+        prof.done(SLIM_K_SEG_FUSED, seg, 0, c.widths[ri_prev], r, B, flops, bytes);
+        if (e != cudaSuccess) return fail(ctx, SLIM_ECUDA, "fused segment-%d launch: %s", seg, cudaGetErrorString(e));
+        if (last) {   // the head: FC on the pooled features
+            const double K = c.num_classes;
+            LaunchProf prof2(ctx, st);
+            const cudaError_t e2 = launch_fc_f32(pooled, S.fc_w, S.fc_b, static_cast<float *>(out), B, C,
+                                                 c.base_channels[3], c.num_classes, st, ctx->pdl && !ctx->prof_on);
+            prof2.done(SLIM_K_HEAD, 3, -1, r, r, B, 2.0 * B * C * K, 4.0 * B * C + 4.0 * K * (C + 1) + 4.0 * B * K);
+            if (e2 != cudaSuccess) return fail(ctx, SLIM_ECUDA, "head launch: %s", cudaGetErrorString(e2));
+        }
+        return SLIM_OK;
+    }
     if (seg == 0) {
         DevLayer &Ls = S.L[0];
         const double pix = static_cast<double>(B) * H * H;
@@ -1378,6 +1451,8 @@ void free_segment(DevSegment &S) {
     }
     cudaFree(S.fc_w);
     cudaFree(S.fc_b);
+    for (int i = 0; i < kMaxW; ++i)
+        for (int j = 0; j < kMaxW; ++j) cudaFree(S.fimg[i][j]);
     S = DevSegment{};
 }
 
@@ -1597,6 +1672,24 @@ slim_status slim_load_segment(slim_ctx *ctx, int seg, const slim_seg_weights *w,
         CUDA_TRY(ctx, cudaMalloc(&S.fc_b, c.num_classes * 4));
         CUDA_TRY(ctx, cudaMemcpy(S.fc_w, w->fc_w, fw * 4, cudaMemcpyHostToDevice));
         CUDA_TRY(ctx, cudaMemcpy(S.fc_b, w->fc_b, c.num_classes * 4, cudaMemcpyHostToDevice));
+    }
+    // fused-segment weight images (segments 1-3, narrow widths; kernels_fused.cu) for every (r_prev, r)
+    // pair the fused kernel supports: built once here, so no first-use repack lands inside a graph capture
+    if (seg > 0 && c.dtype == SLIM_BF16 && c.norm == SLIM_NORM_BN && c.blocks_per_seg[seg] == 2) {
+        for (int ri = 0; ri < c.n_widths; ++ri) {
+            const int C = slim_channels(c.widths[ri], c.base_channels[seg]);
+            if (C != slim_act_channels(c.widths[ri], c.base_channels[seg])) continue;
+            for (int rp = 0; rp < c.n_widths; ++rp) {
+                const int CI = slim_act_channels(c.widths[rp], c.base_channels[seg - 1]);
+                if (!segn_fused_smem_bytes(seg, C, CI)) continue;
+                const size_t nb = segn_fused_image_bytes(C, CI);
+                CUDA_TRY(ctx, cudaMalloc(&S.fimg[rp][ri], nb));
+                CUDA_TRY(ctx, cudaMemset(S.fimg[rp][ri], 0, nb));
+                CUDA_TRY(ctx, build_segn_fused_image(S.fimg[rp][ri], S.L[0].w, S.L[1].w, S.L[2].w, S.L[3].w, S.L[4].w,
+                                                     C, CI, S.L[0].sh.cin, S.L[1].sh.cin, nullptr));
+            }
+        }
+        CUDA_TRY(ctx, cudaDeviceSynchronize());
     }
     S.loaded = true;
     return SLIM_OK;

@@ -145,6 +145,37 @@ struct StemArgs {
 cudaError_t launch_stem_umma(const StemArgs &a, const CUtensorMap &tmIn, const CUtensorMap &tmOut, int grid,
                              cudaStream_t stream, bool pdl);
 
+// ---- segment 0 as one kernel for the narrow widths (kernels_fused.cu) ----------------------
+// stem + two BasicBlocks, one image per CTA, activations resident in shared memory; c0 = 16 | 32
+struct FusedSeg0Args {
+    const uint16_t *in;            // images [B][32][32][3] bf16
+    uint16_t *out;                 // segment output [B][32][32][c0] bf16
+    int B, c0, cin_full;           // cin_full: the convs' full input width (weight row stride)
+    const uint16_t *w[4];          // the four convs' full-width KRSC bf16 weights (manifest order)
+    const void *stem_b;            // the stem's SW128 B image (64 rows x 128 B, K = 27 zero-padded)
+    const float *scale[5], *shift[5];   // folded BN of stem + four convs at this width, c0 entries
+    unsigned long long *trace;     // diagnostics only (SLIM_CONV_TRACE): CTA 0 phase %globaltimer stamps
+};
+size_t seg0_fused_smem_bytes(int c0);
+
+// segments 1-3 as one kernel for the narrow widths (kernels_fused.cu): units of G images (seg 1: 1, 2: 2,
+// 3: 8), activations in shared memory, weights streamed from a pre-swizzled image (build_segn_fused_image)
+struct FusedSegArgs {
+    const uint16_t *in;            // previous segment's output [B][2H][2W][CI] bf16
+    uint16_t *out;                 // [B][H][W][C] bf16 (segments 1, 2)
+    float *pool_out;               // segment 3: fp32 [B][C] average pool (the FC follows), else nullptr
+    int B, CI;
+    const uint8_t *wimg;           // the weight image of this (segment, r_prev, r)
+    const float *scale[5], *shift[5];   // folded BN: b0c1, b0c2, projection, b1c1, b1c2 (C entries)
+    uint32_t smem_budget;          // dynamic smem the launch reserved (the ring takes what is left)
+};
+size_t segn_fused_smem_bytes(int seg, int C, int CI);   // 0 = unsupported / does not fit
+size_t segn_fused_image_bytes(int C, int CI);
+cudaError_t build_segn_fused_image(void *img, const void *w0, const void *w1, const void *wp, const void *w3,
+                                   const void *w4, int C, int CI, int cin0_full, int cf_full, cudaStream_t st);
+cudaError_t launch_segn_fused(const FusedSegArgs &a, int seg, int C, int grid, cudaStream_t stream, bool pdl);
+cudaError_t launch_seg0_fused(const FusedSeg0Args &a, int grid, cudaStream_t stream, bool pdl);
+
 // ---- CUDA-core kernels (kernels_simt.cu) ------------------------------------
 cudaError_t launch_stem_bf16(const uint16_t *in, const float *w, int cin_full, const float *scale,
                              const float *shift, uint16_t *out, int B, int H, int W, int cimg, int c0,

@@ -252,7 +252,8 @@ def test_graph_mode_bitwise_and_launch_count(params):
     c0 = slim.slim_launch_count(n.ctx)
     n.forward_chain(x, tup)
     per_chain = slim.slim_launch_count(n.ctx) - c0
-    assert per_chain == 1 + 4 + 4 * 3 + 1          # stem + 2 convs x 8 blocks + head
+    # segment 0 at r = 0.25 is one fused kernel (stem + both blocks); then 2 convs x 6 blocks + head
+    assert per_chain == 1 + 4 * 3 + 1
     slim.slim_set_graph_mode(n.ctx, True)
     logits = torch.empty_like(a)
     for _ in range(3):
@@ -460,3 +461,82 @@ def test_max_batch_4096(params, ref, r):
            f"B=4096 r={r}")
     n.close()
 
+
+
+@pytest.mark.parametrize("B", [1, 8, 130])
+def test_fused_segment0_bitwise_equals_per_layer(B):
+    """Segment 0 at the narrow widths runs as one fused kernel (kernels_fused.cu); the same arithmetic
+    as the per-layer stem + halo convs (SLIM_NO_FUSED=1), bit for bit, and within tolerance of the oracle."""
+    import subprocess, sys, os
+    code = (
+        "import sys, numpy as np, torch, synth, paper_2510_09018_b200 as slim\n"
+        "w, bn = synth.make_weights(), synth.make_bn()\n"
+        f"B = {B}\n"
+        "net = slim.SlimNet(w, bn, max_batch=max(B, 16))\n"
+        "x = torch.from_numpy(synth.make_images(B, offset=61)).to(torch.bfloat16).cuda()\n"
+        "outs = [net.forward(0, x, r, r).view(torch.int16).cpu().numpy() for r in (0.25, 0.5)]\n"
+        "logits = net.forward_chain(x, (0.25, 0.5, 0.25, 0.5)).cpu().numpy()\n"
+        "np.savez(sys.argv[1], o0=outs[0], o1=outs[1], logits=logits)\n"
+    )
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    import tempfile
+    with tempfile.TemporaryDirectory() as d:
+        res = {}
+        for name, extra in (("fused", {}), ("layers", {"SLIM_NO_FUSED": "1"})):
+            out = subprocess.run([sys.executable, "-c", code, os.path.join(d, name + ".npz")],
+                                 env=dict(os.environ, **extra), capture_output=True, text=True, timeout=300, cwd=root)
+            assert out.returncode == 0, out.stderr[-2000:]
+            res[name] = np.load(os.path.join(d, name + ".npz"))
+        for k in ("o0", "o1", "logits"):
+            assert np.array_equal(res["fused"][k], res["layers"][k]), k
+    x = synth.make_images(B, offset=61)
+    ref = oracle.Model(synth.make_weights(), synth.make_bn())
+    exp = ref.segment(0, x[:4], None, 0.25)
+    got = res["fused"]["o0"][:4].astype(np.int32).astype(np.uint32) << 16
+    _check(got.view(np.float32), exp, TAU_BF16, "fused seg0 r=0.25")
+
+
+@pytest.mark.parametrize("seg", [1, 2, 3])
+def test_fused_segments_bitwise_equal_per_layer(seg):
+    """Segments 1-3 at the narrow widths as one fused kernel (kernels_fused.cu, forced on for every
+    segment with SLIM_FUSED_SEGS=14): bit-identical to the per-layer halo kernels (SLIM_NO_FUSED=1) for
+    every (r_prev, r) the fused kernel takes, ragged unit counts included, and within tolerance of the
+    oracle."""
+    import subprocess, sys, os, tempfile
+    code = (
+        "import sys, numpy as np, torch, synth, paper_2510_09018_b200 as slim\n"
+        "w, bn = synth.make_weights(), synth.make_bn()\n"
+        f"seg = {seg}\n"
+        "net = slim.SlimNet(w, bn, max_batch=64)\n"
+        "res = {}\n"
+        "for B in (1, 9, 64):\n"
+        "    H = 32 >> (seg - 1)\n"
+        "    for rp in synth.WIDTHS:\n"
+        "        C = synth.active_channels(rp, synth.BASE_CHANNELS[seg - 1])\n"
+        "        g = np.random.default_rng(700 + seg + B)\n"
+        "        x = synth.round_bf16(np.abs(g.standard_normal((B, H, H, C), dtype=np.float32)))\n"
+        "        xd = torch.from_numpy(x).to(torch.bfloat16).cuda()\n"
+        "        for r in (0.25, 0.5):\n"
+        "            o = net.forward(seg, xd, rp, r)\n"
+        "            res[f'{B}_{rp}_{r}'] = (o.view(torch.int16) if o.dtype == torch.bfloat16 else o.view(torch.int32)).cpu().numpy()\n"
+        "np.savez(sys.argv[1], **res)\n"
+    )
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    with tempfile.TemporaryDirectory() as d:
+        out = {}
+        for name, extra in (("fused", {"SLIM_FUSED_SEGS": "14"}), ("layers", {"SLIM_NO_FUSED": "1"})):
+            p = subprocess.run([sys.executable, "-c", code, os.path.join(d, name + ".npz")],
+                               env=dict(os.environ, **extra), capture_output=True, text=True, timeout=600, cwd=root)
+            assert p.returncode == 0, p.stderr[-3000:]
+            out[name] = dict(np.load(os.path.join(d, name + ".npz")))
+        bad = [k for k in out["fused"] if not np.array_equal(out["fused"][k], out["layers"][k])]
+        assert not bad, f"fused != per-layer for {bad[:8]} ({len(bad)} of {len(out['fused'])})"
+    # the fused result against the oracle (one configuration per segment)
+    ref = oracle.Model(synth.make_weights(), synth.make_bn())
+    H = 32 >> (seg - 1)
+    C = synth.active_channels(0.5, synth.BASE_CHANNELS[seg - 1])
+    g = np.random.default_rng(700 + seg + 9)
+    x = synth.round_bf16(np.abs(g.standard_normal((9, H, H, C), dtype=np.float32)))
+    got = out["fused"]["9_0.5_0.25"]
+    got = got.view(np.float32) if seg == 3 else (got.astype(np.int32).astype(np.uint32) << 16).view(np.float32)
+    _check(got[:3], ref.segment(seg, x[:3], 0.5, 0.25), TAU_BF16, f"fused seg{seg}")
