@@ -366,13 +366,17 @@ namespace {
 // =====================================================================================================
 // Segments 1-3 as ONE kernel for the narrow widths: block 0 (3x3 stride-2 conv + BN + ReLU; 3x3 conv +
 // BN + 1x1 stride-2 projection + BN + ReLU) and block 1 (two 3x3 convs, identity shortcut), segment 3
-// ending in the fused global average pool.  One CTA takes a UNIT of G images (G*H*W = 128 or 256 output
-// pixels: segment 1 H=16 G=1, segment 2 H=8 G=2, segment 3 H=4 G=8) through all four layers with every
-// activation in shared memory; weights stream through a ring of slabs (one 1-D bulk copy each, from a
-// pre-swizzled image built at load, slim_api.cu build_fused_image), in exactly the order the MMAs use
-// them.  Bit-identical to the per-layer halo kernels: the same MMAs in the same K order (stride-2:
-// kh 0, 2, 1 with [kw0 | kw2] on the odd-column plane and kw1 on the even one; stride 1: chunk outer,
-// kh, 16-channel steps), the same epilogue arithmetic.
+// ending in the fused global average pool.  A cluster of P CTAs takes a UNIT of G images (G*H*W = 128
+// or 256 output pixels: segment 1 H=16 G=1, segment 2 H=8 G=2, segment 3 H=4 G=8) through all four
+// layers with every activation in shared memory; CTA p of the cluster computes output channels
+// [p*R, (p+1)*R), R = C/P, and writes them into the activation buffers of every CTA of the cluster
+// (DSMEM), so each CTA holds the whole layer output as the next layer's A operand; a layer boundary is
+// a local barrier plus one remote mbarrier arrive per peer.  Weights stream through a ring of slabs (one
+// 1-D bulk copy each, from a pre-swizzled per-rank image built at load, build_segn_fused_image) in
+// exactly the order the MMAs use them.  Bit-identical to the per-layer halo kernels: the same MMAs in
+// the same K order (stride 2: kh 0, 2, 1 with [kw0 | kw2] on the odd-column plane and kw1 on the even
+// one; stride 1: chunk outer, kh, 16-channel steps; an output column's sum does not depend on how the
+// N dimension is split), the same epilogue arithmetic.
 //
 // Activation layout: a "halo row" = RP = G*W pixels ordered (image n, column w); a buffer holds H+2
 // halo rows (zero rows 0 and H+1), channels in chunks of <= 64 (K-major, swizzle span = 2*chunk B).
@@ -385,42 +389,61 @@ namespace {
 constexpr int kFnEpiWarps = 16;
 constexpr int kFnThreads = (kFnEpiWarps + 2) * 32;   // warps 0-15 epilogue / loaders, 16 MMA, 17 weight producer
 
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void st_cluster_v4(uint32_t addr, uint4 v) {
+    asm volatile("st.shared::cluster.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z),
+                 "r"(v.w)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t remote_bar) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote_bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint32_t bar, uint32_t parity) {
+    uint32_t ok = 0;
+    while (!ok)
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(ok)
+            : "r"(bar), "r"(parity)
+            : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_cluster() {
+    asm volatile("fence.proxy.async.shared::cluster;" ::: "memory");
+}
+
 struct FnGeom {
-    // runtime sizes (bytes) of the smem regions for one (C, CI, H, G)
     uint32_t rb_i, nch_i, rb_c, nch_c, rp;
     uint32_t plane_odd, plane_even;       // one parity plane (all input chunks)
-    uint32_t act;                         // T or X (all output chunks)
+    uint32_t act;                         // T or X (all C channels)
     uint32_t slot, n_slots;
-    uint32_t planes, t, x, ring, bn, stage, bars, total;
+    uint32_t planes, t, x, ring, bn, bars, total;
 };
 __host__ __device__ inline uint32_t fn_al(uint32_t v) { return (v + 1023u) & ~1023u; }
-__host__ __device__ inline FnGeom fn_geom(int C, int CI, int H, int G, bool tap_mode) {
+__host__ __device__ inline int fn_ck(int c) { return c <= 16 ? 16 : (c <= 32 ? 32 : 64); }
+// smem layout for full width C, R = C/P rows per CTA, input width CI; the weight ring takes what the
+// budget leaves (up to 6 slots)
+__host__ __device__ inline FnGeom fn_layout(int C, int R, int CI, int H, int G, uint32_t budget) {
     FnGeom g;
-    const int ck_i = CI <= 16 ? 16 : (CI <= 32 ? 32 : 64), ck_c = C <= 16 ? 16 : (C <= 32 ? 32 : 64);
-    g.rb_i = 2u * ck_i;
+    g.rb_i = 2u * fn_ck(CI);
     g.nch_i = (CI + 63) / 64;
-    g.rb_c = 2u * ck_c;
+    g.rb_c = 2u * fn_ck(C);
     g.nch_c = (C + 63) / 64;
     g.rp = static_cast<uint32_t>(G * H);                          // W == H
     g.plane_odd = fn_al(g.nch_i * (H + 1) * g.rp * g.rb_i);
     g.plane_even = fn_al(g.nch_i * H * g.rp * g.rb_i);
     g.act = fn_al(g.nch_c * (H + 2) * g.rp * g.rb_c);
-    const uint32_t taps = tap_mode ? 1u : 3u;
-    uint32_t s = taps * C * (g.rb_i > g.rb_c ? g.rb_i : g.rb_c);
-    g.slot = fn_al(s);
+    const uint32_t taps = 3 * R > 256 ? 1u : 3u;
+    g.slot = fn_al(taps * R * (g.rb_i > g.rb_c ? g.rb_i : g.rb_c));
     g.planes = 0;
     g.t = g.planes + 2 * g.plane_odd + 2 * g.plane_even;
     g.x = g.t + g.act;
     g.ring = g.x + g.act;
-    g.n_slots = 0;   // filled by the caller (fn_layout) from the remaining budget
-    g.bn = 0;
-    g.stage = 0;
-    g.bars = 0;
-    g.total = g.ring;
-    return g;
-}
-__host__ __device__ inline FnGeom fn_layout(int C, int CI, int H, int G, bool tap_mode, uint32_t budget) {
-    FnGeom g = fn_geom(C, CI, H, G, tap_mode);
     const uint32_t tail = 5u * 2u * C * 4u + 64u * 8u + 16u;   // BN vectors, barriers, tmem slot
     uint32_t ns = 0;
     while (ns < 6 && g.ring + (ns + 1) * g.slot + tail <= budget) ++ns;
@@ -431,20 +454,21 @@ __host__ __device__ inline FnGeom fn_layout(int C, int CI, int H, int G, bool ta
     return g;
 }
 
-template <int C, int H, int G>
+template <int C, int H, int G, int P>
 __global__ void __launch_bounds__(kFnThreads, 1) segn_fused_kernel(const FusedSegArgs a) {
     constexpr int W = H, RP = G * W, NPIX = G * H * W, NT = NPIX / 128, TR = 128 / RP;
-    constexpr bool TAPM = 3 * C > 256;                       // one tap per slab / MMA (C = 128)
-    constexpr int NG = C / 16;                               // 16-channel groups
-    constexpr int SC = 4 * C;                                // TMEM columns per tile stage: 3 kw accs + projection
+    constexpr int R = C / P;                                 // output channels of this CTA
+    constexpr bool TAPM = 3 * R > 256;                       // one tap per slab / MMA
+    constexpr int NG = R / 16;                               // 16-channel groups of this CTA
+    constexpr int SC = 4 * R;                                // TMEM columns per tile stage: 3 kw accs + projection
     static_assert(NT * SC <= 512, "TMEM");
     const int CI = a.CI;
-    const FnGeom Gm = fn_layout(C, CI, H, G, TAPM, a.smem_budget);
+    const FnGeom Gm = fn_layout(C, R, CI, H, G, a.smem_budget);
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     const uint32_t s0 = smem_u32(smem);
     const uint32_t sPl = s0 + Gm.planes, sT = s0 + Gm.t, sX = s0 + Gm.x, sRing = s0 + Gm.ring;
-    // plane p = py*2 + px (0: even/even, 1: even/odd, 2: odd/even, 3: odd/odd)
+    // plane (py, px): even-row planes first (px = 0, 1), then odd-row planes
     auto plane_base = [&](int py, int px) -> uint32_t {
         return (py ? 2 * Gm.plane_even + px * Gm.plane_odd : px * Gm.plane_even);
     };
@@ -453,10 +477,23 @@ __global__ void __launch_bounds__(kFnThreads, 1) segn_fused_kernel(const FusedSe
     auto w_full = [&](int i) { return bar0 + 8u * i; };
     auto w_empty = [&](int i) { return bar0 + 8u * (8 + i); };
     auto t_full = [&](int t) { return bar0 + 8u * (16 + t); };
+    const uint32_t peer_done = bar0 + 8u * 24;               // P-1 remote arrivals per layer
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + Gm.bars + 64 * 8);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint32_t rbi = Gm.rb_i, rbc = Gm.rb_c, nchi = Gm.nch_i;
     const int n_units = (a.B + G - 1) / G;
+    const uint32_t rank = P > 1 ? cluster_ctarank() : 0;
+    const int unit0 = blockIdx.x / P, unit_step = gridDim.x / P;
+    // diagnostics: CTA 0, thread 0 (epilogue) stamps [0..15], the MMA warp's lane 0 [16..31], producer [32..47]
+    unsigned long long *tr = (a.trace && blockIdx.x == 0) ? a.trace : nullptr;
+    int ntr = 0, ntm = 16, ntp = 32;
+#define FN_STAMP()                                                                      \
+    do {                                                                                \
+        if (tr && tid == 0 && ntr < 16) tr[ntr++] = gtimer();                           \
+        if (tr && warp == kFnEpiWarps && lane == 0 && ntm < 32) tr[ntm++] = gtimer();   \
+        if (tr && warp == kFnEpiWarps + 1 && lane == 0 && ntp < 48) tr[ntp++] = gtimer(); \
+    } while (0)
+    FN_STAMP();
 
     // ---- prologue (static data only: before the PDL wait)
     for (int i = tid; i < 5 * C; i += kFnThreads) {
@@ -465,8 +502,8 @@ __global__ void __launch_bounds__(kFnThreads, 1) segn_fused_kernel(const FusedSe
         sBN[l * 2 * C + C + c] = a.shift[l][c];
     }
     // zero rows: odd-row planes' row 0, T and X rows 0 and H+1 (never written afterwards)
-    for (int py = 1, px = 0; px < 2; ++px) {
-        const uint32_t base = Gm.planes + plane_base(py, px);
+    for (int px = 0; px < 2; ++px) {
+        const uint32_t base = Gm.planes + plane_base(1, px);
         for (uint32_t ch = 0; ch < nchi; ++ch)
             for (int i = tid; i < RP * static_cast<int>(rbi) / 16; i += kFnThreads)
                 reinterpret_cast<uint4 *>(smem + base + ch * (H + 1) * RP * rbi)[i] = make_uint4(0, 0, 0, 0);
@@ -483,6 +520,7 @@ __global__ void __launch_bounds__(kFnThreads, 1) segn_fused_kernel(const FusedSe
             mbar_init(w_empty(i), 1);
             mbar_init(t_full(i), 1);
         }
+        mbar_init(peer_done, P > 1 ? P - 1 : 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == kFnEpiWarps) {
@@ -493,34 +531,37 @@ __global__ void __launch_bounds__(kFnThreads, 1) segn_fused_kernel(const FusedSe
     }
     fence_proxy_async();
     tc_fence_before();
-    __syncthreads();
+    if (P > 1)
+        cluster_sync_all();   // every CTA's barriers are initialised before any remote arrive / store
+    else
+        __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    FN_STAMP();
 
-    // slab sequence of one unit (identical for producer and MMA issuer): returns bytes of slab k, or 0
-    // past the end.  L1: (ch_i, kh in 0,2,1) x [3 taps | tap]; L2: (ch_c, kh) x taps, then projection
-    // (ch_i); L3, L4: (ch_c, kh) x taps.
+    // slab sequence of one unit (identical for producer and MMA issuer): L1: (ch_i, kh in 0,2,1) x
+    // [3 taps | tap]; L2: (ch_c, kh) x taps, then the projection (ch_i); L3, L4: (ch_c, kh) x taps
     const int tps = TAPM ? 3 : 1;                            // slabs per (chunk, kh)
     const int n_l1 = nchi * 3 * tps, n_l2 = Gm.nch_c * 3 * tps, n_p = nchi;
     const int n_slabs = n_l1 + n_l2 + n_p + 2 * n_l2;
     auto slab_bytes = [&](int k) -> uint32_t {
         const uint32_t taps = TAPM ? 1u : 3u;
-        if (k < n_l1) return taps * C * rbi;
+        if (k < n_l1) return taps * R * rbi;
         k -= n_l1;
-        if (k < n_l2) return taps * C * rbc;
+        if (k < n_l2) return taps * R * rbc;
         k -= n_l2;
-        if (k < n_p) return static_cast<uint32_t>(C) * rbi;
-        return taps * C * rbc;
+        if (k < n_p) return static_cast<uint32_t>(R) * rbi;
+        return taps * R * rbc;
     };
 
     if (warp == kFnEpiWarps + 1) {
-        // ===================== weight producer: slabs in consumption order, every unit ==============
+        // ===================== weight producer: this rank's slabs in consumption order, every unit ======
         pdl_launch_dependents();
         if (lane == 0) {
             int s = 0;
             uint32_t ph = 0;
-            for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
-                const uint8_t *src = a.wimg;
+            for (int u = unit0; u < n_units; u += unit_step) {
+                const uint8_t *src = a.wimg + static_cast<size_t>(rank) * a.wimg_rank_bytes;
                 for (int k = 0; k < n_slabs; ++k) {
                     const uint32_t by = slab_bytes(k);
                     mbar_wait(w_empty(s), ph ^ 1);
@@ -531,368 +572,449 @@ __global__ void __launch_bounds__(kFnThreads, 1) segn_fused_kernel(const FusedSe
                         s = 0;
                         ph ^= 1;
                     }
+                    if ((k & 3) == 3) FN_STAMP();
                 }
             }
         }
-        return;   // (no CTA-wide barrier below involves this warp)
-    }
-    pdl_wait();
-    pdl_launch_dependents();
+    } else {
+        pdl_wait();
+        pdl_launch_dependents();
+        FN_STAMP();
 
-    const int q = warp & 3, sub = warp >> 2;                 // epilogue: TMEM lane quarter, column way
-    const int m = q * 32 + lane;                             // row within a tile
-    const int wcol = m % W;                                  // pixel column (W divides 32)
-    const float mL = wcol > 0 ? 1.f : 0.f, mR = wcol < W - 1 ? 1.f : 0.f;
-    const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
-    int ws = 0;                                              // MMA: weight ring position
-    uint32_t wph = 0;
-    uint32_t layer_uses = 0;                                 // t_full phase counter (one completion per layer)
-    constexpr uint32_t kBarThreads = (kFnEpiWarps + 1) * 32;
+        const int q = warp & 3, sub = warp >> 2;             // epilogue: TMEM lane quarter, column way
+        const int m = q * 32 + lane;                         // row within a tile
+        const int wcol = m % W;                              // pixel column (W divides 32)
+        const float mL = wcol > 0 ? 1.f : 0.f, mR = wcol < W - 1 ? 1.f : 0.f;
+        const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
+        int ws = 0;                                          // MMA: weight ring position
+        uint32_t wph = 0;
+        uint32_t layers_done = 0;                            // layers completed by this CTA (t_full / peer phases)
+        constexpr uint32_t kBarThreads = (kFnEpiWarps + 1) * 32;
 
-    for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
-        // ---- the unit's input -> four parity planes (16-B pieces; images past B are zeros)
-        if (warp < kFnEpiWarps) {
-            const int per_px = CI / 8;                       // 16-B pieces per input pixel
-            const int total = G * (2 * H) * (2 * W) * per_px;
-            for (int i = tid; i < total; i += kFnEpiWarps * 32) {
-                const int j = i % per_px, p = i / per_px;
-                const int x = p % (2 * W), y = (p / (2 * W)) % (2 * H), n = p / (4 * H * W);
-                const int img = u * G + n;
-                uint4 v = make_uint4(0, 0, 0, 0);
-                if (img < a.B)
-                    v = *reinterpret_cast<const uint4 *>(a.in + ((static_cast<size_t>(img) * 2 * H + y) * 2 * W + x) * CI +
-                                                         j * 8);
-                const int py = y & 1, px = x & 1;
-                const int row = py ? (y + 1) / 2 : y / 2, col = px ? (x - 1) / 2 : x / 2;
-                const int ch = (j * 8) / 64, jj = j % (static_cast<int>(rbi) / 16);
-                const uint32_t rows = py ? (H + 1) : H;
-                const uint32_t off = Gm.planes + plane_base(py, px) + ch * rows * RP * rbi +
-                                     swz_off(row * RP + n * W + col, jj, rbi);
-                *reinterpret_cast<uint4 *>(smem + off) = v;
-            }
-            fence_proxy_async();
-        }
-        named_bar_sync(1, kBarThreads);
-        tc_fence_after();
-        for (int l = 1; l <= 4; ++l) {
-            if (warp == kFnEpiWarps) {
-                // ===================== MMA issuer ========================================================
-                const uint32_t src = (l == 2 || l == 4) ? sT : sX;   // L2, L4 read T; L3 reads X
-                auto next_slab = [&]() -> uint64_t {
-                    mbar_wait(w_full(ws), wph);
-                    tc_fence_after();
-                    return static_cast<uint64_t>(sRing + ws * Gm.slot);
-                };
-                auto release_slab = [&]() {
-                    if (elect_one()) umma_commit(w_empty(ws));
-                    __syncwarp();
-                    if (++ws == static_cast<int>(Gm.n_slots)) {
-                        ws = 0;
-                        wph ^= 1;
-                    }
-                };
-                if (l == 1) {
-                    // stride-2 conv from the parity planes: kh order 0, 2, 1
-                    const uint32_t idesc1 = umma_idesc_bf16(kTileM, C), idesc2 = umma_idesc_bf16(kTileM, 2 * C);
-                    for (uint32_t ch = 0; ch < nchi; ++ch) {
-                        const int nk = min(static_cast<int>(rbi) / 32, (CI - static_cast<int>(ch) * 64 + 15) >> 4);
-                        for (int o = 0; o < 3; ++o) {
-                            const int kh = o == 0 ? 0 : (o == 1 ? 2 : 1);
-                            const int py = kh == 1 ? 0 : 1, roff = kh == 2 ? 1 : 0;
-                            const uint32_t rows = py ? (H + 1) : H;
-                            for (int j = 0; j < (TAPM ? 3 : 1); ++j) {
-                                const uint32_t sb = static_cast<uint32_t>(next_slab());
-                                if (elect_one()) {
-                                    for (int t = 0; t < NT; ++t) {
-                                        const uint32_t acc = tmem + t * SC;
-                                        const uint32_t aoff = ch * rows * RP * rbi + (t * TR + roff) * RP * rbi;
-                                        const uint64_t aod = umma_desc_kmajor(sPl + plane_base(py, 1) + aoff, rbi);
-                                        const uint64_t aev = umma_desc_kmajor(sPl + plane_base(py, 0) + aoff, rbi);
-                                        const uint64_t bd = umma_desc_kmajor(sb, rbi);
-                                        for (int kk = 0; kk < nk; ++kk) {
-                                            const uint32_t accum = (ch | kh | kk) != 0;
-                                            if (!TAPM) {   // slab taps [kw0 | kw2 | kw1]
-                                                umma_bf16(acc, aod + 2 * kk, bd + 2 * kk, idesc2, accum);
-                                                umma_bf16(acc + 2 * C, aev + 2 * kk, bd + ((2u * C * rbi) >> 4) + 2 * kk,
-                                                          idesc1, accum);
-                                            } else if (j < 2) {   // tap kw0 -> acc0, kw2 -> acc1 (odd columns)
-                                                umma_bf16(acc + j * C, aod + 2 * kk, bd + 2 * kk, idesc1, accum);
-                                            } else {              // kw1 -> acc2 (even columns)
-                                                umma_bf16(acc + 2 * C, aev + 2 * kk, bd + 2 * kk, idesc1, accum);
-                                            }
-                                        }
-                                    }
-                                }
-                                __syncwarp();
-                                release_slab();
-                            }
-                        }
-                    }
-                } else {
-                    const uint32_t idesc3 = umma_idesc_bf16(kTileM, TAPM ? C : 3 * C), idesc1 = umma_idesc_bf16(kTileM, C);
-                    for (uint32_t ch = 0; ch < Gm.nch_c; ++ch) {
-                        const int nk = min(static_cast<int>(rbc) / 32, (C - static_cast<int>(ch) * 64 + 15) >> 4);
-                        for (int kh = 0; kh < 3; ++kh) {
-                            for (int j = 0; j < (TAPM ? 3 : 1); ++j) {
-                                const uint32_t sb = static_cast<uint32_t>(next_slab());
-                                if (elect_one()) {
-                                    for (int t = 0; t < NT; ++t) {
-                                        const uint32_t acc = tmem + t * SC + (TAPM ? j * C : 0);
-                                        const uint64_t ad = umma_desc_kmajor(
-                                            src + ch * (H + 2) * RP * rbc + (t * TR + kh) * RP * rbc, rbc);
-                                        const uint64_t bd = umma_desc_kmajor(sb, rbc);
-                                        for (int kk = 0; kk < nk; ++kk)
-                                            umma_bf16(acc, ad + 2 * kk, bd + 2 * kk, idesc3, (ch | kh | kk) != 0);
-                                    }
-                                }
-                                __syncwarp();
-                                release_slab();
-                            }
-                        }
-                    }
-                    if (l == 2) {   // 1x1 stride-2 projection from the even/even plane -> 4th accumulator
-                        for (uint32_t cp = 0; cp < nchi; ++cp) {
-                            const int nk = min(static_cast<int>(rbi) / 32, (CI - static_cast<int>(cp) * 64 + 15) >> 4);
-                            const uint32_t sb = static_cast<uint32_t>(next_slab());
-                            if (elect_one()) {
-                                for (int t = 0; t < NT; ++t) {
-                                    const uint64_t ad = umma_desc_kmajor(
-                                        sPl + plane_base(0, 0) + cp * H * RP * rbi + t * TR * RP * rbi, rbi);
-                                    const uint64_t bd = umma_desc_kmajor(sb, rbi);
-                                    for (int kk = 0; kk < nk; ++kk)
-                                        umma_bf16(tmem + t * SC + 3 * C, ad + 2 * kk, bd + 2 * kk, idesc1, (cp | kk) != 0);
-                                }
-                            }
-                            __syncwarp();
-                            release_slab();
-                        }
-                    }
-                }
-                if (elect_one())
-                    for (int t = 0; t < NT; ++t) umma_commit(t_full(t));
-                __syncwarp();
-            } else {
-                // ===================== epilogue: items (tile, 16-channel group) over the 4 column ways =====
-                const int bn_l = l == 1 ? 0 : (l == 2 ? 1 : l);   // scale/shift slots: b0c1, b0c2, sc, b1c1, b1c2
-                const float *sc = sBN + bn_l * 2 * C, *sh = sc + C;
-                const float *sc1 = sBN + 2 * 2 * C, *sh1 = sc1 + C;
-                const uint32_t dstb = (l == 2) ? Gm.x : Gm.t;     // L1, L3 -> T; L2 -> X; L4 -> global
-                const bool pool = a.pool_out != nullptr && l == 4;
-                // L4 pool partials: the even-row planes (dead after L2's projection; no zero rows to keep)
-                float *stage = reinterpret_cast<float *>(smem + Gm.planes);
-                for (int it = sub; it < NT * NG; it += 4) {
-                    const int t = it / NG, gi = it % NG;
-                    mbar_wait(t_full(t), layer_uses & 1);
-                    tc_fence_after();
-                    const int hr = t * TR + m / RP, pix = m % RP, n = pix / W;   // halo row (output h), image in unit
-                    uint32_t v0[16], v1[16], v2[16];
-                    const uint32_t col = tmem + lane_off + t * SC + gi * 16;
-                    tmem_ld16(col, v0);
-                    tmem_ld16(col + C, v1);
-                    tmem_ld16(col + 2 * C, v2);
-                    tmem_wait_ld();
-                    reg_fence16(v0);
-                    reg_fence16(v1);
-                    reg_fence16(v2);
-                    float f[16];
-                    if (l == 1) {   // acc [kw0 | kw2 | kw1]: kw0[w-1] + kw2[w] + kw1[w] (scalar, as the halo kernel)
+        for (int u = unit0; u < n_units; u += unit_step) {
+            // ---- the unit's input -> four parity planes (16-B pieces; images past B are zeros)
+            if (warp < kFnEpiWarps) {
+                const int per_px = CI / 8;                   // 16-B pieces per input pixel
+                const int total = G * (2 * H) * (2 * W) * per_px;
+                constexpr int kU = 8;                        // loads in flight per thread before the stores
+                for (int i0 = tid; i0 < total; i0 += kU * kFnEpiWarps * 32) {
+                    uint4 v[kU];
 #pragma unroll
-                        for (int i = 0; i < 16; ++i) {
-                            const float left = __shfl_up_sync(0xffffffffu, __uint_as_float(v0[i]), 1);
-                            const float y = fmaf(mL, left, __uint_as_float(v1[i]) + __uint_as_float(v2[i]));
-                            f[i] = fmaf(y, sc[gi * 16 + i], sh[gi * 16 + i]);
-                        }
-                    } else {
-                        const unsigned long long mL2 = f2pk(mL, mL), mR2 = f2pk(mR, mR);
-#pragma unroll
-                        for (int i = 0; i < 16; i += 2) {
-                            const float l0 = __shfl_up_sync(0xffffffffu, __uint_as_float(v0[i]), 1);
-                            const float l1 = __shfl_up_sync(0xffffffffu, __uint_as_float(v0[i + 1]), 1);
-                            const float r0 = __shfl_down_sync(0xffffffffu, __uint_as_float(v2[i]), 1);
-                            const float r1 = __shfl_down_sync(0xffffffffu, __uint_as_float(v2[i + 1]), 1);
-                            const unsigned long long y = ffma2(
-                                mR2, f2pk(r0, r1),
-                                ffma2(mL2, f2pk(l0, l1), f2pk(__uint_as_float(v1[i]), __uint_as_float(v1[i + 1]))));
-                            const int c = gi * 16 + i;
-                            f2upk(ffma2(y, f2pk(sc[c], sc[c + 1]), f2pk(sh[c], sh[c + 1])), f[i], f[i + 1]);
-                        }
+                    for (int k = 0; k < kU; ++k) {
+                        const int i = i0 + k * kFnEpiWarps * 32;
+                        const int j = i % per_px, p = i / per_px;
+                        const int img = u * G + p / (4 * H * W);
+                        v[k] = make_uint4(0, 0, 0, 0);
+                        if (i < total && img < a.B)
+                            v[k] = *reinterpret_cast<const uint4 *>(a.in + (static_cast<size_t>(u * G) * 4 * H * W + p) * CI +
+                                                                    j * 8);
                     }
-                    if (l == 2) {   // + s_sc * proj + t_sc
-                        tmem_ld16(col + 3 * C, v0);
-                        tmem_wait_ld();
-                        reg_fence16(v0);
 #pragma unroll
-                        for (int i = 0; i < 16; i += 2) {
-                            const int c = gi * 16 + i;
-                            const unsigned long long pr =
-                                ffma2(f2pk(__uint_as_float(v0[i]), __uint_as_float(v0[i + 1])), f2pk(sc1[c], sc1[c + 1]),
-                                      f2pk(sh1[c], sh1[c + 1]));
-                            f2upk(fadd2(f2pk(f[i], f[i + 1]), pr), f[i], f[i + 1]);
-                        }
-                    }
-                    // this pixel in the activation buffers: halo row hr+1, chunk gi*16/64
-                    const uint32_t chk = (gi * 16) / 64, pc = ((gi * 16) % 64) / 8, pcs = rbc / 16;
-                    const uint32_t brow = (hr + 1) * RP + pix;
-                    const uint32_t o0 = chk * (H + 2) * RP * rbc + swz_off(brow, pc % pcs, rbc);
-                    const uint32_t o1 = chk * (H + 2) * RP * rbc + swz_off(brow, (pc + 1) % pcs, rbc);
-                    if (l == 4) {   // + the block input (X, this pixel)
-                        const uint4 r0 = *reinterpret_cast<const uint4 *>(smem + Gm.x + o0);
-                        const uint4 r1 = *reinterpret_cast<const uint4 *>(smem + Gm.x + o1);
-                        const uint32_t rr[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
-#pragma unroll
-                        for (int i = 0; i < 8; ++i)
-                            f2upk(fadd2(f2pk(f[2 * i], f[2 * i + 1]), f2pk(bf16_lo(rr[i]), bf16_hi(rr[i]))), f[2 * i],
-                                  f[2 * i + 1]);
-                    }
-                    if (pool) {
-                        // fused global average pool, as the halo kernel: the W pixels of an image row summed
-                        // across lanes, parked per (row, image, channel); rows summed below in fixed order
-#pragma unroll
-                        for (int i = 0; i < 16; ++i) f[i] = fmaxf(f[i], 0.f);
-                        for (int o = 1; o < W; o <<= 1) {
-#pragma unroll
-                            for (int i = 0; i < 16; ++i) f[i] += __shfl_xor_sync(0xffffffffu, f[i], o);
-                        }
-                        if (wcol == 0) {
-                            float4 *dstp = reinterpret_cast<float4 *>(stage + (hr * G + n) * C + gi * 16);
-#pragma unroll
-                            for (int i = 0; i < 4; ++i) dstp[i] = make_float4(f[4 * i], f[4 * i + 1], f[4 * i + 2], f[4 * i + 3]);
-                        }
-                        continue;
-                    }
-                    uint32_t o[8];
-#pragma unroll
-                    for (int i = 0; i < 8; ++i) o[i] = pack_bf16(fmaxf(f[2 * i], 0.f), fmaxf(f[2 * i + 1], 0.f));
-                    const uint4 q0 = make_uint4(o[0], o[1], o[2], o[3]), q1 = make_uint4(o[4], o[5], o[6], o[7]);
-                    if (l == 4) {
-                        const int img = u * G + n;
-                        if (img < a.B) {
-                            uint4 *gp = reinterpret_cast<uint4 *>(
-                                a.out + ((static_cast<size_t>(img) * H + hr) * W + wcol) * C + gi * 16);
-                            gp[0] = q0;
-                            gp[1] = q1;
-                        }
-                    } else {
-                        *reinterpret_cast<uint4 *>(smem + dstb + o0) = q0;
-                        *reinterpret_cast<uint4 *>(smem + dstb + o1) = q1;
+                    for (int k = 0; k < kU; ++k) {
+                        const int i = i0 + k * kFnEpiWarps * 32;
+                        if (i >= total) break;
+                        const int j = i % per_px, p = i / per_px;
+                        const int x = p % (2 * W), y = (p / (2 * W)) % (2 * H), n = p / (4 * H * W);
+                        const int py = y & 1, px = x & 1;
+                        const int row = py ? (y + 1) / 2 : y / 2, col = px ? (x - 1) / 2 : x / 2;
+                        const int ch = (j * 8) / 64, jj = j % (static_cast<int>(rbi) / 16);
+                        const uint32_t rows = py ? (H + 1) : H;
+                        const uint32_t off = Gm.planes + plane_base(py, px) + ch * rows * RP * rbi +
+                                             swz_off(row * RP + n * W + col, jj, rbi);
+                        *reinterpret_cast<uint4 *>(smem + off) = v[k];
                     }
                 }
                 fence_proxy_async();
-                tc_fence_before();
-                if (pool) {   // rows summed in order h = 0..H-1, times 1/(H*W)
-                    named_bar_sync(2, kFnEpiWarps * 32);
-                    const float inv = 1.f / static_cast<float>(H * W);
-                    for (int idx = tid; idx < G * C; idx += kFnEpiWarps * 32) {
-                        float sum = 0.f;
-                        for (int h = 0; h < H; ++h) sum += stage[h * G * C + idx];
-                        const int img = u * G + idx / C;
-                        if (img < a.B) a.pool_out[static_cast<size_t>(img) * C + idx % C] = sum * inv;
-                    }
-                }
             }
-            ++layer_uses;
             named_bar_sync(1, kBarThreads);
             tc_fence_after();
+            FN_STAMP();
+            for (int l = 1; l <= 4; ++l) {
+                if (warp == kFnEpiWarps) {
+                    // ===================== MMA issuer ====================================================
+                    // the previous layer's outputs of every peer are in this CTA's buffers (and the peers
+                    // are done reading the buffer this layer's epilogue will write into theirs)
+                    if (P > 1 && layers_done > 0) mbar_wait_cluster(peer_done, (layers_done - 1) & 1);
+                    tc_fence_after();
+                    const uint32_t src = (l == 2 || l == 4) ? sT : sX;   // L2, L4 read T; L3 reads X
+                    auto next_slab = [&]() -> uint32_t {
+                        mbar_wait(w_full(ws), wph);
+                        tc_fence_after();
+                        return sRing + ws * Gm.slot;
+                    };
+                    auto release_slab = [&]() {
+                        if (elect_one()) umma_commit(w_empty(ws));
+                        __syncwarp();
+                        if (++ws == static_cast<int>(Gm.n_slots)) {
+                            ws = 0;
+                            wph ^= 1;
+                        }
+                    };
+                    if (l == 1) {
+                        // stride-2 conv from the parity planes: kh order 0, 2, 1
+                        const uint32_t idesc1 = umma_idesc_bf16(kTileM, R), idesc2 = umma_idesc_bf16(kTileM, 2 * R);
+                        for (uint32_t ch = 0; ch < nchi; ++ch) {
+                            const int nk = min(static_cast<int>(rbi) / 32, (CI - static_cast<int>(ch) * 64 + 15) >> 4);
+                            for (int o = 0; o < 3; ++o) {
+                                const int kh = o == 0 ? 0 : (o == 1 ? 2 : 1);
+                                const int py = kh == 1 ? 0 : 1, roff = kh == 2 ? 1 : 0;
+                                const uint32_t rows = py ? (H + 1) : H;
+                                for (int j = 0; j < (TAPM ? 3 : 1); ++j) {
+                                    const uint32_t sb = next_slab();
+                                    if (elect_one()) {
+                                        for (int t = 0; t < NT; ++t) {
+                                            const uint32_t acc = tmem + t * SC;
+                                            const uint32_t aoff = ch * rows * RP * rbi + (t * TR + roff) * RP * rbi;
+                                            const uint64_t aod = umma_desc_kmajor(sPl + plane_base(py, 1) + aoff, rbi);
+                                            const uint64_t aev = umma_desc_kmajor(sPl + plane_base(py, 0) + aoff, rbi);
+                                            const uint64_t bd = umma_desc_kmajor(sb, rbi);
+                                            for (int kk = 0; kk < nk; ++kk) {
+                                                const uint32_t accum = (ch | kh | kk) != 0;
+                                                if (!TAPM) {   // slab taps [kw0 | kw2 | kw1]
+                                                    umma_bf16(acc, aod + 2 * kk, bd + 2 * kk, idesc2, accum);
+                                                    umma_bf16(acc + 2 * R, aev + 2 * kk,
+                                                              bd + ((2u * R * rbi) >> 4) + 2 * kk, idesc1, accum);
+                                                } else if (j < 2) {   // tap kw0 -> acc0, kw2 -> acc1 (odd columns)
+                                                    umma_bf16(acc + j * R, aod + 2 * kk, bd + 2 * kk, idesc1, accum);
+                                                } else {              // kw1 -> acc2 (even columns)
+                                                    umma_bf16(acc + 2 * R, aev + 2 * kk, bd + 2 * kk, idesc1, accum);
+                                                }
+                                            }
+                                        }
+                                    }
+                                    __syncwarp();
+                                    release_slab();
+                                }
+                            }
+                        }
+                    } else {
+                        const uint32_t idesc3 = umma_idesc_bf16(kTileM, TAPM ? R : 3 * R),
+                                       idesc1 = umma_idesc_bf16(kTileM, R);
+                        for (uint32_t ch = 0; ch < Gm.nch_c; ++ch) {
+                            const int nk = min(static_cast<int>(rbc) / 32, (C - static_cast<int>(ch) * 64 + 15) >> 4);
+                            for (int kh = 0; kh < 3; ++kh) {
+                                for (int j = 0; j < (TAPM ? 3 : 1); ++j) {
+                                    const uint32_t sb = next_slab();
+                                    if (elect_one()) {
+                                        for (int t = 0; t < NT; ++t) {
+                                            const uint32_t acc = tmem + t * SC + (TAPM ? j * R : 0);
+                                            const uint64_t ad = umma_desc_kmajor(
+                                                src + ch * (H + 2) * RP * rbc + (t * TR + kh) * RP * rbc, rbc);
+                                            const uint64_t bd = umma_desc_kmajor(sb, rbc);
+                                            for (int kk = 0; kk < nk; ++kk)
+                                                umma_bf16(acc, ad + 2 * kk, bd + 2 * kk, idesc3, (ch | kh | kk) != 0);
+                                        }
+                                    }
+                                    __syncwarp();
+                                    release_slab();
+                                }
+                            }
+                        }
+                        if (l == 2) {   // 1x1 stride-2 projection from the even/even plane -> 4th accumulator
+                            for (uint32_t cp = 0; cp < nchi; ++cp) {
+                                const int nk =
+                                    min(static_cast<int>(rbi) / 32, (CI - static_cast<int>(cp) * 64 + 15) >> 4);
+                                const uint32_t sb = next_slab();
+                                if (elect_one()) {
+                                    for (int t = 0; t < NT; ++t) {
+                                        const uint64_t ad = umma_desc_kmajor(
+                                            sPl + plane_base(0, 0) + cp * H * RP * rbi + t * TR * RP * rbi, rbi);
+                                        const uint64_t bd = umma_desc_kmajor(sb, rbi);
+                                        for (int kk = 0; kk < nk; ++kk)
+                                            umma_bf16(tmem + t * SC + 3 * R, ad + 2 * kk, bd + 2 * kk, idesc1,
+                                                      (cp | kk) != 0);
+                                    }
+                                }
+                                __syncwarp();
+                                release_slab();
+                            }
+                        }
+                    }
+                    if (elect_one())
+                        for (int t = 0; t < NT; ++t) umma_commit(t_full(t));
+                    __syncwarp();
+                    FN_STAMP();
+                } else {
+                    // ===================== epilogue: items (tile, 16-channel group) over the 4 column ways ==
+                    const int bn_l = l == 1 ? 0 : (l == 2 ? 1 : l);   // BN slots: b0c1, b0c2, sc, b1c1, b1c2
+                    const float *sc = sBN + bn_l * 2 * C, *sh = sc + C;
+                    const float *sc1 = sBN + 2 * 2 * C, *sh1 = sc1 + C;
+                    const uint32_t dstb = (l == 2) ? Gm.x : Gm.t;     // L1, L3 -> T; L2 -> X; L4 -> global
+                    const bool pool = a.pool_out != nullptr && l == 4;
+                    // L4 pool partials: the even-row planes (dead after L2's projection; no zero rows to keep)
+                    float *stage = reinterpret_cast<float *>(smem + Gm.planes);
+                    for (int it = sub; it < NT * NG; it += 4) {
+                        const int t = it / NG, gi = it % NG;
+                        mbar_wait(t_full(t), layers_done & 1);
+                        tc_fence_after();
+                        const int hr = t * TR + m / RP, pix = m % RP, n = pix / W;   // output row, image in unit
+                        const int cg = static_cast<int>(rank) * R + gi * 16;         // first global channel
+                        uint32_t v0[16], v1[16], v2[16];
+                        const uint32_t col = tmem + lane_off + t * SC + gi * 16;
+                        tmem_ld16(col, v0);
+                        tmem_ld16(col + R, v1);
+                        tmem_ld16(col + 2 * R, v2);
+                        tmem_wait_ld();
+                        reg_fence16(v0);
+                        reg_fence16(v1);
+                        reg_fence16(v2);
+                        float f[16];
+                        if (l == 1) {   // acc [kw0 | kw2 | kw1]: kw0[w-1] + kw2[w] + kw1[w] (scalar, as the halo kernel)
+#pragma unroll
+                            for (int i = 0; i < 16; ++i) {
+                                const float left = __shfl_up_sync(0xffffffffu, __uint_as_float(v0[i]), 1);
+                                const float y = fmaf(mL, left, __uint_as_float(v1[i]) + __uint_as_float(v2[i]));
+                                f[i] = fmaf(y, sc[cg + i], sh[cg + i]);
+                            }
+                        } else {
+                            const unsigned long long mL2 = f2pk(mL, mL), mR2 = f2pk(mR, mR);
+#pragma unroll
+                            for (int i = 0; i < 16; i += 2) {
+                                const float l0 = __shfl_up_sync(0xffffffffu, __uint_as_float(v0[i]), 1);
+                                const float l1 = __shfl_up_sync(0xffffffffu, __uint_as_float(v0[i + 1]), 1);
+                                const float r0 = __shfl_down_sync(0xffffffffu, __uint_as_float(v2[i]), 1);
+                                const float r1 = __shfl_down_sync(0xffffffffu, __uint_as_float(v2[i + 1]), 1);
+                                const unsigned long long y = ffma2(
+                                    mR2, f2pk(r0, r1),
+                                    ffma2(mL2, f2pk(l0, l1), f2pk(__uint_as_float(v1[i]), __uint_as_float(v1[i + 1]))));
+                                const int c = cg + i;
+                                f2upk(ffma2(y, f2pk(sc[c], sc[c + 1]), f2pk(sh[c], sh[c + 1])), f[i], f[i + 1]);
+                            }
+                        }
+                        if (l == 2) {   // + s_sc * proj + t_sc
+                            tmem_ld16(col + 3 * R, v0);
+                            tmem_wait_ld();
+                            reg_fence16(v0);
+#pragma unroll
+                            for (int i = 0; i < 16; i += 2) {
+                                const int c = cg + i;
+                                const unsigned long long pr =
+                                    ffma2(f2pk(__uint_as_float(v0[i]), __uint_as_float(v0[i + 1])),
+                                          f2pk(sc1[c], sc1[c + 1]), f2pk(sh1[c], sh1[c + 1]));
+                                f2upk(fadd2(f2pk(f[i], f[i + 1]), pr), f[i], f[i + 1]);
+                            }
+                        }
+                        // this pixel in the activation buffers: halo row hr+1, chunk cg/64
+                        const uint32_t chk = cg / 64, pc = (cg % 64) / 8;
+                        const uint32_t brow = (hr + 1) * RP + pix;
+                        const uint32_t o0 = chk * (H + 2) * RP * rbc + swz_off(brow, pc, rbc);
+                        const uint32_t o1 = chk * (H + 2) * RP * rbc + swz_off(brow, pc + 1, rbc);
+                        if (l == 4) {   // + the block input (X, this pixel)
+                            const uint4 r0 = *reinterpret_cast<const uint4 *>(smem + Gm.x + o0);
+                            const uint4 r1 = *reinterpret_cast<const uint4 *>(smem + Gm.x + o1);
+                            const uint32_t rr[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+#pragma unroll
+                            for (int i = 0; i < 8; ++i)
+                                f2upk(fadd2(f2pk(f[2 * i], f[2 * i + 1]), f2pk(bf16_lo(rr[i]), bf16_hi(rr[i]))),
+                                      f[2 * i], f[2 * i + 1]);
+                        }
+                        if (pool) {
+                            // fused global average pool, as the halo kernel: the W pixels of an image row summed
+                            // across lanes, parked per (row, image, channel); rows summed below in fixed order
+#pragma unroll
+                            for (int i = 0; i < 16; ++i) f[i] = fmaxf(f[i], 0.f);
+                            for (int o = 1; o < W; o <<= 1) {
+#pragma unroll
+                                for (int i = 0; i < 16; ++i) f[i] += __shfl_xor_sync(0xffffffffu, f[i], o);
+                            }
+                            if (wcol == 0) {
+                                float4 *dstp = reinterpret_cast<float4 *>(stage + (hr * G + n) * R + gi * 16);
+#pragma unroll
+                                for (int i = 0; i < 4; ++i)
+                                    dstp[i] = make_float4(f[4 * i], f[4 * i + 1], f[4 * i + 2], f[4 * i + 3]);
+                            }
+                            continue;
+                        }
+                        uint32_t o[8];
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) o[i] = pack_bf16(fmaxf(f[2 * i], 0.f), fmaxf(f[2 * i + 1], 0.f));
+                        const uint4 q0 = make_uint4(o[0], o[1], o[2], o[3]), q1 = make_uint4(o[4], o[5], o[6], o[7]);
+                        if (l == 4) {
+                            const int img = u * G + n;
+                            if (img < a.B) {
+                                uint4 *gp = reinterpret_cast<uint4 *>(
+                                    a.out + ((static_cast<size_t>(img) * H + hr) * W + wcol) * C + cg);
+                                gp[0] = q0;
+                                gp[1] = q1;
+                            }
+                        } else {
+                            *reinterpret_cast<uint4 *>(smem + dstb + o0) = q0;
+                            *reinterpret_cast<uint4 *>(smem + dstb + o1) = q1;
+#pragma unroll
+                            for (int pr = 1; pr < P; ++pr) {   // the same slice into every peer's buffer
+                                const uint32_t peer = (rank + pr) % P;
+                                st_cluster_v4(mapa_shared(s0 + dstb + o0, peer), q0);
+                                st_cluster_v4(mapa_shared(s0 + dstb + o1, peer), q1);
+                            }
+                        }
+                    }
+                    if (P > 1)
+                        fence_proxy_async_cluster();
+                    else
+                        fence_proxy_async();
+                    tc_fence_before();
+                    if (pool) {   // rows summed in order h = 0..H-1, times 1/(H*W)
+                        named_bar_sync(2, kFnEpiWarps * 32);
+                        const float inv = 1.f / static_cast<float>(H * W);
+                        for (int idx = tid; idx < G * R; idx += kFnEpiWarps * 32) {
+                            float sum = 0.f;
+                            for (int h = 0; h < H; ++h) sum += stage[h * G * R + idx];
+                            const int img = u * G + idx / R;
+                            if (img < a.B)
+                                a.pool_out[static_cast<size_t>(img) * C + rank * R + idx % R] = sum * inv;
+                        }
+                    }
+                }
+                ++layers_done;
+                if (warp < kFnEpiWarps) FN_STAMP();
+                named_bar_sync(1, kBarThreads);
+                tc_fence_after();
+                if (P > 1 && tid == 0) {   // this CTA's slice of the layer is in every peer's buffers
+#pragma unroll
+                    for (int pr = 1; pr < P; ++pr) mbar_arrive_remote(mapa_shared(peer_done, (rank + pr) % P));
+                }
+            }
         }
     }
     tc_fence_before();
-    named_bar_sync(1, kBarThreads);
+    if (P > 1)
+        cluster_sync_all();   // no CTA exits while a peer may still write into it or arrive on its barrier
+    else
+        __syncthreads();
     if (warp == kFnEpiWarps) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512) : "memory");
     }
 }
 
+int fn_geom_seg(int seg, int *H, int *G) {
+    *H = 32 >> seg;
+    *G = seg == 1 ? 1 : (seg == 2 ? 2 : 8);
+    return 0;
+}
+
 }  // namespace
+
+// cluster size of the fused segment kernel for (seg, C): output channels split over P CTAs where a single
+// CTA would be weight-streaming / MMA bound (8-image segment-3 units; segment 2 at C = 128)
+int segn_fused_cluster(int seg, int C) {
+    if (seg == 3) return C >= 128 ? 4 : 2;
+    if (seg == 2 && C >= 128) return 2;
+    return 1;
+}
 
 // smem the fused segment-s kernel needs for (C, CI) at segment s (0 if unsupported); >= 2 ring slots
 size_t segn_fused_smem_bytes(int seg, int C, int CI) {
-    const int H = 32 >> seg, G = seg == 1 ? 1 : (seg == 2 ? 2 : 8);
     if (!(seg >= 1 && seg <= 3) || (C != 32 && C != 64 && C != 128) || CI % 16 != 0 || CI > 128) return 0;
     if (seg == 1 && C == 128) return 0;
-    if (G * H * H / 128 * 4 * C > 512) return 0;
-    const FnGeom g = fn_layout(C, CI, H, G, 3 * C > 256, 227u * 1024u - 1024u);
+    int H, G;
+    fn_geom_seg(seg, &H, &G);
+    const int P = segn_fused_cluster(seg, C), R = C / P;
+    if (G * H * H / 128 * 4 * R > 512) return 0;
+    const FnGeom g = fn_layout(C, R, CI, H, G, 227u * 1024u - 1024u);
     if (g.n_slots < 2) return 0;
     return 1024 + g.total;
 }
 
-// bytes of the fused weight image for (seg, C, CI) and its slab sequence (build order = consumption order)
-size_t segn_fused_image_bytes(int C, int CI) {
-    const bool tapm = 3 * C > 256;
-    const int ck_i = CI <= 16 ? 16 : (CI <= 32 ? 32 : 64), ck_c = C <= 16 ? 16 : (C <= 32 ? 32 : 64);
+// bytes of one rank's weight image (R = C/P output rows) for (C, CI): slabs in consumption order
+size_t segn_fused_rank_image_bytes(int seg, int C, int CI) {
+    const int R = C / segn_fused_cluster(seg, C);
+    const int ck_i = fn_ck(CI), ck_c = fn_ck(C);
     const size_t nchi = (CI + 63) / 64, nchc = (C + 63) / 64;
-    (void)tapm;
-    return static_cast<size_t>(C) * (9 * nchi * 2 * ck_i + 3 * 9 * nchc * 2 * ck_c + nchi * 2 * ck_i);
+    return static_cast<size_t>(R) * (9 * nchi * 2 * ck_i + 3 * 9 * nchc * 2 * ck_c + nchi * 2 * ck_i);
+}
+size_t segn_fused_image_bytes(int seg, int C, int CI) {
+    return segn_fused_cluster(seg, C) * segn_fused_rank_image_bytes(seg, C, CI);
 }
 
-cudaError_t launch_segn_fused(const FusedSegArgs &a, int seg, int C, int grid, cudaStream_t stream, bool pdl) {
+cudaError_t launch_segn_fused(const FusedSegArgs &a, int seg, int C, int units_grid, cudaStream_t stream, bool pdl) {
     using Fn = void (*)(FusedSegArgs);
     Fn fn = nullptr;
-    if (seg == 1 && C == 32) fn = segn_fused_kernel<32, 16, 1>;
-    if (seg == 1 && C == 64) fn = segn_fused_kernel<64, 16, 1>;
-    if (seg == 2 && C == 64) fn = segn_fused_kernel<64, 8, 2>;
-    if (seg == 2 && C == 128) fn = segn_fused_kernel<128, 8, 2>;
-    if (seg == 3 && C == 64) fn = segn_fused_kernel<64, 4, 8>;
-    if (seg == 3 && C == 128) fn = segn_fused_kernel<128, 4, 8>;
+    if (seg == 1 && C == 32) fn = segn_fused_kernel<32, 16, 1, 1>;
+    if (seg == 1 && C == 64) fn = segn_fused_kernel<64, 16, 1, 1>;
+    if (seg == 2 && C == 64) fn = segn_fused_kernel<64, 8, 2, 1>;
+    if (seg == 2 && C == 128) fn = segn_fused_kernel<128, 8, 2, 2>;
+    if (seg == 3 && C == 64) fn = segn_fused_kernel<64, 4, 8, 2>;
+    if (seg == 3 && C == 128) fn = segn_fused_kernel<128, 4, 8, 4>;
     if (!fn) return cudaErrorInvalidValue;
     const size_t smem = segn_fused_smem_bytes(seg, C, a.CI);
     if (!smem) return cudaErrorInvalidValue;
+    const int P = segn_fused_cluster(seg, C);
     FusedSegArgs args = a;
     args.smem_budget = 227u * 1024u - 1024u;   // the same budget segn_fused_smem_bytes laid the ring out for
+    args.wimg_rank_bytes = segn_fused_rank_image_bytes(seg, C, a.CI);
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(grid);
+    cfg.gridDim = dim3(units_grid * P);
     cfg.blockDim = dim3(kFnThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = P;
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     return cudaLaunchKernelEx(&cfg, fn, args);
 }
 
-// Builds the fused weight image of one (segment, r_prev, r): the slabs of b0c1, b0c2, the projection,
-// b1c1, b1c2 in consumption order, each [taps][C rows][row bytes] K-major and swizzled exactly as the
-// kernel's ring slot expects (swizzle row index relative to the 1 KiB-aligned slab start).
+// Builds the fused weight image of one (segment, r_prev, r): per rank p (output rows [p*R, (p+1)*R)),
+// the slabs of b0c1, b0c2, the projection, b1c1, b1c2 in consumption order, each [taps][R rows][row
+// bytes] K-major and swizzled exactly as the kernel's ring slot expects (swizzle row index relative to
+// the 1 KiB-aligned slab start).
 namespace {
 __global__ void fused_image_kernel(uint8_t *img, const uint16_t *w0, const uint16_t *w1, const uint16_t *wp,
-                                   const uint16_t *w3, const uint16_t *w4, int C, int CI, int cin0_full, int cf_full) {
-    const bool tapm = 3 * C > 256;
-    const int ck_i = CI <= 16 ? 16 : (CI <= 32 ? 32 : 64), ck_c = C <= 16 ? 16 : (C <= 32 ? 32 : 64);
-    const int rbi = 2 * ck_i, rbc = 2 * ck_c;
+                                   const uint16_t *w3, const uint16_t *w4, int C, int R, int co_off, int CI,
+                                   int cin0_full, int cf_full) {
+    const bool tapm = 3 * R > 256;
+    const int rbi = 2 * fn_ck(CI), rbc = 2 * fn_ck(C);
     const int nchi = (CI + 63) / 64, nchc = (C + 63) / 64;
-    // enumerate slabs; each thread handles 16-B pieces of all slabs (grid-stride over a flat index space)
-    const long total_pieces = static_cast<long>(C) * (9 * nchi * rbi + 3 * 9 * nchc * rbc + nchi * rbi) / 16;
+    const long l1 = static_cast<long>(9) * nchi * R * rbi / 16;   // pieces of L1
+    const long l2 = static_cast<long>(9) * nchc * R * rbc / 16;   // pieces of one stride-1 conv
+    const long lp = static_cast<long>(nchi) * R * rbi / 16;       // pieces of the projection
+    const long total_pieces = l1 + lp + 3 * l2;
     for (long gi = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; gi < total_pieces;
          gi += static_cast<long>(gridDim.x) * blockDim.x) {
         long rem = gi;
-        size_t off = 0;   // slab start (bytes)
-        // L1: ch, kh in (0,2,1), taps (0,2,1) [x C rows x rbi]
-        const long l1 = static_cast<long>(9) * nchi * C * rbi / 16;
-        const long l2 = static_cast<long>(9) * nchc * C * rbc / 16;
-        const long lp = static_cast<long>(nchi) * C * rbi / 16;
+        size_t off;
         const uint16_t *w;
-        int kidx, cin_full, rb, ch, kh, kw, row_in_slab, piece, slab_taps;
-        if (rem < l1) {
-            const int per_kh = 3 * C * rbi / 16;   // pieces per (ch, kh) group
+        int cin_full, cin_act, taps_k, rb, ch, kh, kw, row_in_slab, piece;
+        if (rem < l1) {   // L1: groups (ch, kh in 0,2,1), taps kw 0,2,1
+            const int per_kh = 3 * R * rbi / 16;
             const int grp = static_cast<int>(rem / per_kh), r2 = static_cast<int>(rem % per_kh);
             ch = grp / 3;
             const int o = grp % 3;
             kh = o == 0 ? 0 : (o == 1 ? 2 : 1);
-            const int tap_i = r2 / (C * rbi / 16), r3 = r2 % (C * rbi / 16);
+            const int tap_i = r2 / (R * rbi / 16), r3 = r2 % (R * rbi / 16);
             kw = tap_i == 0 ? 0 : (tap_i == 1 ? 2 : 1);
-            row_in_slab = (tapm ? 0 : tap_i * C) + r3 / (rbi / 16);
+            row_in_slab = (tapm ? 0 : tap_i * R) + r3 / (rbi / 16);
             piece = r3 % (rbi / 16);
-            off = static_cast<size_t>(grp) * 3 * C * rbi + (tapm ? static_cast<size_t>(tap_i) * C * rbi : 0);
-            slab_taps = tapm ? 1 : 3;
+            off = static_cast<size_t>(grp) * 3 * R * rbi + (tapm ? static_cast<size_t>(tap_i) * R * rbi : 0);
             w = w0;
             cin_full = cin0_full;
+            cin_act = CI;
+            taps_k = 9;
             rb = rbi;
-            kidx = kh * 3 + kw;
-        } else if ((rem -= l1) < l2 || (rem >= l2 + lp && rem < l2 + lp + 2 * l2)) {
+        } else if (rem - l1 >= l2 && rem - l1 < l2 + lp) {   // projection: chunks, R rows x rbi
+            rem -= l1 + l2;
+            const int per = R * rbi / 16;
+            ch = static_cast<int>(rem / per);
+            const int r3 = static_cast<int>(rem % per);
+            row_in_slab = r3 / (rbi / 16);
+            piece = r3 % (rbi / 16);
+            off = static_cast<size_t>(l1 + l2) * 16 + static_cast<size_t>(ch) * R * rbi;
+            w = wp;
+            cin_full = cin0_full;
+            cin_act = CI;
+            taps_k = 1;
+            rb = rbi;
+            kh = kw = 0;
+        } else {          // stride-1 convs b0c2 (after L1), b1c1, b1c2 (after the projection)
+            rem -= l1;
             int layer;
             size_t base;
             if (rem < l2) {
@@ -904,55 +1026,45 @@ __global__ void fused_image_kernel(uint8_t *img, const uint16_t *w0, const uint1
                 if (layer == 4) rem -= l2;
                 base = static_cast<size_t>(l1 + l2 + lp + (layer == 4 ? l2 : 0)) * 16;
             }
-            const int per_kh = 3 * C * rbc / 16;
+            const int per_kh = 3 * R * rbc / 16;
             const int grp = static_cast<int>(rem / per_kh), r2 = static_cast<int>(rem % per_kh);
             ch = grp / 3;
             kh = grp % 3;
-            const int tap_i = r2 / (C * rbc / 16), r3 = r2 % (C * rbc / 16);
+            const int tap_i = r2 / (R * rbc / 16), r3 = r2 % (R * rbc / 16);
             kw = tap_i;
-            row_in_slab = (tapm ? 0 : tap_i * C) + r3 / (rbc / 16);
+            row_in_slab = (tapm ? 0 : tap_i * R) + r3 / (rbc / 16);
             piece = r3 % (rbc / 16);
-            off = base + static_cast<size_t>(grp) * 3 * C * rbc + (tapm ? static_cast<size_t>(tap_i) * C * rbc : 0);
-            slab_taps = tapm ? 1 : 3;
+            off = base + static_cast<size_t>(grp) * 3 * R * rbc + (tapm ? static_cast<size_t>(tap_i) * R * rbc : 0);
             w = layer == 1 ? w1 : (layer == 3 ? w3 : w4);
             cin_full = cf_full;
+            cin_act = C;
+            taps_k = 9;
             rb = rbc;
-            kidx = kh * 3 + kw;
-        } else {   // projection: ch, C rows x rbi (1x1 kernel)
-            rem -= l2;
-            const int per = C * rbi / 16;
-            ch = static_cast<int>(rem / per);
-            const int r3 = static_cast<int>(rem % per);
-            row_in_slab = r3 / (rbi / 16);
-            piece = r3 % (rbi / 16);
-            off = static_cast<size_t>(l1 + l2) * 16 + static_cast<size_t>(ch) * C * rbi;
-            slab_taps = 1;
-            w = wp;
-            cin_full = cin0_full;
-            rb = rbi;
-            kidx = 0;
-            kh = kw = 0;
         }
-        (void)slab_taps;
-        const int co = row_in_slab % C;
+        const int co = co_off + row_in_slab % R;
         const int ci0 = ch * 64 + piece * 8;
-        const int taps_k = (w == wp) ? 1 : 9;
-        const int cin_act = (w == w0 || w == wp) ? CI : C;
         uint4 v = make_uint4(0, 0, 0, 0);
         if (ci0 < cin_act)   // channels past the active input width are never multiplied (K steps stop there)
-            v = *reinterpret_cast<const uint4 *>(w + (static_cast<size_t>(co) * taps_k + kidx) * cin_full + ci0);
+            v = *reinterpret_cast<const uint4 *>(w + (static_cast<size_t>(co) * taps_k + (kh * 3 + kw) * (taps_k == 9)) *
+                                                         cin_full + ci0);
         *reinterpret_cast<uint4 *>(img + off + swz_off(row_in_slab, piece, rb)) = v;
     }
 }
 }  // namespace
 
 cudaError_t build_segn_fused_image(void *img, const void *w0, const void *w1, const void *wp, const void *w3,
-                                   const void *w4, int C, int CI, int cin0_full, int cf_full, cudaStream_t st) {
-    fused_image_kernel<<<64, 256, 0, st>>>(static_cast<uint8_t *>(img), static_cast<const uint16_t *>(w0),
-                                           static_cast<const uint16_t *>(w1), static_cast<const uint16_t *>(wp),
-                                           static_cast<const uint16_t *>(w3), static_cast<const uint16_t *>(w4), C, CI,
-                                           cin0_full, cf_full);
-    return cudaGetLastError();
+                                   const void *w4, int seg, int C, int CI, int cin0_full, int cf_full, cudaStream_t st) {
+    const int P = segn_fused_cluster(seg, C), R = C / P;
+    const size_t per = segn_fused_rank_image_bytes(seg, C, CI);
+    for (int p = 0; p < P; ++p) {
+        fused_image_kernel<<<64, 256, 0, st>>>(static_cast<uint8_t *>(img) + p * per, static_cast<const uint16_t *>(w0),
+                                               static_cast<const uint16_t *>(w1), static_cast<const uint16_t *>(wp),
+                                               static_cast<const uint16_t *>(w3), static_cast<const uint16_t *>(w4), C,
+                                               R, p * R, CI, cin0_full, cf_full);
+        const cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
 }
 
 }  // namespace slim

@@ -1169,19 +1169,19 @@ slim_status run_segment(slim_ctx *ctx, int seg, int ri_prev, int ri, int B, cons
         if (e != cudaSuccess) return fail(ctx, SLIM_ECUDA, "fused segment-0 launch: %s", cudaGetErrorString(e));
         return SLIM_OK;
     }
-    // segments 1-3 at a narrow width: both blocks in one kernel (kernels_fused.cu) where it measured faster
-    // than the per-layer kernels at B = 8 and 128 (profiles/r02_fused_micro.txt): segment 1 at C <= 64
-    // (r <= 0.5), segment 2 at C <= 64 (r = 0.25); segment 3 (8-image units, 16 CTAs at B = 128, ~1 MB of
-    // weights streamed per unit) stays per-layer.  SLIM_FUSED_SEGS (bit s = segment s) overrides; the
-    // (r_prev, r) weight image must exist (the kernel's working set fits in shared memory).
-    static const int fused_env = getenv("SLIM_FUSED_SEGS") ? atoi(getenv("SLIM_FUSED_SEGS")) : -1;
-    const bool fused_on = fused_env >= 0 ? ((fused_env >> seg) & 1) != 0 : (seg == 1 || (seg == 2 && C <= 64));
+    // segments 1-3 at a narrow width: both blocks in one kernel (kernels_fused.cu) wherever the (r_prev, r)
+    // working set fits in shared memory (the weight image then exists): measured faster than the per-layer
+    // kernels at B = 8 and 128 for every such case (profiles/r02_fused_micro.txt).  SLIM_FUSED_SEGS (bit s =
+    // segment s) restricts it (A/B).
+    static const int fused_env = getenv("SLIM_FUSED_SEGS") ? atoi(getenv("SLIM_FUSED_SEGS")) : 0xE;
+    const bool fused_on = ((fused_env >> seg) & 1) != 0;
     if (seg > 0 && bf && !gn && !no_fused && fused_on && S.fimg[ri_prev][ri]) {
         FusedSegArgs fa{};
         fa.in = static_cast<const uint16_t *>(in);
         fa.B = B;
         fa.CI = curC;
         fa.wimg = static_cast<const uint8_t *>(S.fimg[ri_prev][ri]);
+        fa.trace = ctx->trace ? ctx->trace + 8192 + 64 : nullptr;
         const bool last = seg == 3;
         float *pooled = nullptr;
         if (last) pooled = reinterpret_cast<float *>(bufs[0]);   // fp32 [B][C] for the FC
@@ -1195,9 +1195,10 @@ slim_status run_segment(slim_ctx *ctx, int seg, int ri_prev, int ri, int B, cons
         const double pix = static_cast<double>(B) * H * H;
         const double flops = 2.0 * pix * C * (9.0 * curC + 27.0 * C + curC);
         const double bytes = eb * (static_cast<double>(B) * 4 * H * H * curC + (last ? 2.0 * B * C : pix * C)) +
-                             static_cast<double>(segn_fused_image_bytes(C, curC));
-        int grid = std::min((B + G - 1) / G, ctx->num_sms);
-        grid = grid_cap(ctx, ri, grid, seg);
+                             static_cast<double>(segn_fused_image_bytes(seg, C, curC));
+        const int P = segn_fused_cluster(seg, C);
+        int grid = std::min((B + G - 1) / G, ctx->num_sms / P);   // clusters (units in flight)
+        grid = std::max(1, grid_cap(ctx, ri, grid * P, seg) / P);
         LaunchProf prof(ctx, st);
         const cudaError_t e = launch_segn_fused(fa, seg, C, grid, st, ctx->pdl && !ctx->prof_on);
         prof.done(SLIM_K_SEG_FUSED, seg, 0, c.widths[ri_prev], r, B, flops, bytes);
@@ -1682,11 +1683,11 @@ slim_status slim_load_segment(slim_ctx *ctx, int seg, const slim_seg_weights *w,
             for (int rp = 0; rp < c.n_widths; ++rp) {
                 const int CI = slim_act_channels(c.widths[rp], c.base_channels[seg - 1]);
                 if (!segn_fused_smem_bytes(seg, C, CI)) continue;
-                const size_t nb = segn_fused_image_bytes(C, CI);
+                const size_t nb = segn_fused_image_bytes(seg, C, CI);
                 CUDA_TRY(ctx, cudaMalloc(&S.fimg[rp][ri], nb));
                 CUDA_TRY(ctx, cudaMemset(S.fimg[rp][ri], 0, nb));
                 CUDA_TRY(ctx, build_segn_fused_image(S.fimg[rp][ri], S.L[0].w, S.L[1].w, S.L[2].w, S.L[3].w, S.L[4].w,
-                                                     C, CI, S.L[0].sh.cin, S.L[1].sh.cin, nullptr));
+                                                     seg, C, CI, S.L[0].sh.cin, S.L[1].sh.cin, nullptr));
             }
         }
         CUDA_TRY(ctx, cudaDeviceSynchronize());
