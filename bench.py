@@ -325,7 +325,7 @@ def run_ours(args):
     for k in range(K):
         flush.zero_()
         ev[k][0].record(stream)
-        step(evw[k] if args.width_events else None)
+        step()
         ev[k][1].record(stream)
         tick(k, ev)
     torch.cuda.synchronize()
@@ -340,8 +340,15 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_max_ms = float(t.item())
     value = world * imgs_per_step * K / (total_max_ms / 1e3)
-    in_step_ms = ({r: float(np.mean([e[r][0].elapsed_time(e[r][1]) for e in evw])) for r in WIDTHS}
-                  if args.width_events else None)
+    # per-width time inside the concurrent step: the same step again (outside the timed region, events on
+    # each width's stream around its chain; recording them costs ~6 % of the step, so not in the timed loop)
+    in_step_ms = None
+    if args.width_events:
+        for k in range(K):
+            flush.zero_()
+            step(evw[k])
+        torch.cuda.synchronize()
+        in_step_ms = {r: float(np.mean([e[r][0].elapsed_time(e[r][1]) for e in evw])) for r in WIDTHS}
 
     # ---------------- energy (Eq. 7's E_t = P * L): the same step, L2 flush included, in a loop
     # of >= args.energy_seconds; NVML total-energy counter delta / images.  Clocks sampled throughout.
@@ -349,7 +356,7 @@ def run_ours(args):
     e0 = sampler.energy_mj()
     t0 = time.perf_counter()
     n_energy = 0
-    while True:
+    while args.energy_seconds > 0:
         for _ in range(50):
             flush.zero_()
             step()
@@ -370,7 +377,7 @@ def run_ours(args):
                "images": imgs_per_step * n_energy, "mean_power_w": (e1 - e0) / 1e3 / energy_s,
                "images_per_s_in_loop": imgs_per_step * n_energy / energy_s,
                "method": "nvmlDeviceGetTotalEnergyConsumption delta over the loop (host wall clock)"}
-              if (e0 is not None and e1 is not None and e1 > e0) else None)
+              if (e0 is not None and e1 is not None and e1 > e0 and n_energy > 0) else None)
 
     # ---------------- per-width: each width's chain alone (L2 flushed before it), on all SMs, graph replay
     # with PDL -- the same kernels as the step without the other instances
@@ -694,7 +701,7 @@ def run_stream(args):
     t0 = time.perf_counter()
     n_e = 0
     k = args.warmup + args.steps
-    while True:
+    while args.energy_seconds > 0:
         n_e += one_step(k)
         k += 1
         if k % 8 == 0:
@@ -704,7 +711,7 @@ def run_stream(args):
     torch.cuda.synchronize()
     sampler.stop()
     e1 = sampler.energy_mj()
-    clocks, energy = _clock_energy_json(sampler, e0, e1, max(n_e, 1))
+    clocks, energy = _clock_energy_json(sampler, e0, e1, max(n_e, 1)) if n_e else (sampler.summary(), None)
     pack = getattr(ex, "pack_s", [])[n_pack0:]
     n_desc = len(batches)
     if rank == 0:
