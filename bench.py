@@ -987,7 +987,7 @@ def _ncu_tensor_pipe():
     metric's "tensor-pipe % of peak"): mean over the captured conv launches, % of elapsed and of
     active cycles (sm__pipe_tensor_cycles_active / sm__pipe_tc_cycles_active)."""
     out = {}
-    for key, f in (("b128_all_widths", "r01_ncu_chain.json"), ("b1024_r1", "r01_ncu_b1024_r1.json")):
+    for key, f in (("b128_all_widths", "r02_ncu_chain_b128.json"), ("b1024_r1", "r02_ncu_b1024_r1.json")):
         p = os.path.join(ROOT, "profiles", f)
         try:
             L = [r for r in json.load(open(p))["launches"] if "conv" in r["kernel"]]

@@ -1174,7 +1174,15 @@ slim_status run_segment(slim_ctx *ctx, int seg, int ri_prev, int ri, int B, cons
     // kernels at B = 8 and 128 for every such case (profiles/r02_fused_micro.txt).  SLIM_FUSED_SEGS (bit s =
     // segment s) restricts it (A/B).
     static const int fused_env = getenv("SLIM_FUSED_SEGS") ? atoi(getenv("SLIM_FUSED_SEGS")) : 0xE;
-    const bool fused_on = ((fused_env >> seg) & 1) != 0;
+    // While the width's instance shares the GPU with concurrent instances (SM share < 1, the CFG2 step),
+    // segments 1-3 take the per-layer kernels: a fused unit is a long per-CTA latency chain that holds its
+    // SMs (large smem) for most of the step and starves the wide instances' kernels -- measured 1.07 M
+    // (fused, capped to the share) / 1.12 M (fused, uncapped) vs 1.27 M images/s (per-layer) for the
+    // 4-width step (tools/gpu_runs/r02_ab_fused2.sh).  SLIM_FUSED_PART (A/B): 0 = that (default),
+    // 1 = fused and capped to the share, 2 = fused and uncapped.
+    static const int fused_part = getenv("SLIM_FUSED_PART") ? atoi(getenv("SLIM_FUSED_PART")) : 0;
+    const bool partitioned = grid_cap(ctx, ri, ctx->num_sms, seg) < ctx->num_sms;
+    const bool fused_on = ((fused_env >> seg) & 1) != 0 && !(partitioned && fused_part == 0);
     if (seg > 0 && bf && !gn && !no_fused && fused_on && S.fimg[ri_prev][ri]) {
         FusedSegArgs fa{};
         fa.in = static_cast<const uint16_t *>(in);
@@ -1198,7 +1206,7 @@ slim_status run_segment(slim_ctx *ctx, int seg, int ri_prev, int ri, int B, cons
                              static_cast<double>(segn_fused_image_bytes(seg, C, curC));
         const int P = segn_fused_cluster(seg, C);
         int grid = std::min((B + G - 1) / G, ctx->num_sms / P);   // clusters (units in flight)
-        grid = std::max(1, grid_cap(ctx, ri, grid * P, seg) / P);
+        if (fused_part != 2) grid = std::max(1, grid_cap(ctx, ri, grid * P, seg) / P);
         LaunchProf prof(ctx, st);
         const cudaError_t e = launch_segn_fused(fa, seg, C, grid, st, ctx->pdl && !ctx->prof_on);
         prof.done(SLIM_K_SEG_FUSED, seg, 0, c.widths[ri_prev], r, B, flops, bytes);

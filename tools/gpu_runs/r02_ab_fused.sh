@@ -1,0 +1,4 @@
+for i in 1 2; do
+for env in "X=1" "SLIM_NO_FUSED=1" "SLIM_FUSED_SEGS=0" "SLIM_FUSED_SEGS=2"; do
+  env $env python bench.py --steps 300 --warmup 20 --no-cpu --energy-seconds 0 --width-events 0 --e2e-steps 1 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('$env', round(d['value']), round(d['ms_per_step']*1e3,1), 'us')"
+done; done
