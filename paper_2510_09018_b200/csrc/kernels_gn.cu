@@ -261,7 +261,105 @@ __global__ void __launch_bounds__(gn_max_threads<T>(), sizeof(T) == 2 ? (TWO ? 2
     }   // items
 }
 
+// GN apply from the producing conv's statistics partials (kernels_halo.cu, HaloArgs::gn_part): each thread
+// takes 8 channels (one 16-B vector, half of a 16-channel group) of one pixel; it merges the image's
+// per-tile partials of its group (Chan's pairwise update, fixed tile order -> deterministic, the same
+// for every pixel of the image), then out = act(y*A + Bc [+ res]) with A = rstd*gamma, Bc = beta - mean*A.
+// pool_out: per (image, 8 channels) the average over the image's pixels instead of the store.
+// The coefficients of a whole image (C channels) are built once per CTA in smem: thread c merges the
+// image's tiles_per_img partials of channel c's group (Chan's pairwise update, fixed tile order: the same
+// for every pixel) -> A = rstd*gamma, Bc = beta - mean*A.
+constexpr int kGnpThreads = 256;
+constexpr int kGnpMaxC = 512;
+__device__ __forceinline__ void gn_part_image_coef(const GnPartArgs &a, int n, float *sA, float *sB) {
+    const int G = a.C / 16;
+    for (int c = threadIdx.x; c < a.C; c += blockDim.x) {
+        const float2 *p = a.part + static_cast<size_t>(n) * a.tiles_per_img * G + c / 16;
+        float mean = p[0].x, m2 = p[0].y, cnt = a.part_count;
+        for (int t = 1; t < a.tiles_per_img; ++t) {
+            const float2 q = p[static_cast<size_t>(t) * G];
+            const float nb = a.part_count, tot = cnt + nb;
+            const float d = q.x - mean;
+            mean = fmaf(d, nb / tot, mean);
+            m2 = (m2 + q.y) + d * d * (cnt * nb / tot);
+            cnt = tot;
+        }
+        const float rstd = rsqrtf(fmaxf(m2 / cnt, 0.f) + a.eps);
+        const float A = rstd * a.gamma[c];
+        sA[c] = A;
+        sB[c] = fmaf(-mean, A, a.beta[c]);
+    }
+}
+
+// grid: (pixel chunks of one image) x images; pool_out: one CTA per image
+__global__ void __launch_bounds__(kGnpThreads) gn_apply_part_kernel(const GnPartArgs a, int px_per_cta) {
+    __shared__ float sA[kGnpMaxC], sB[kGnpMaxC];
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    const int V = a.C / 8;
+    const int chunks = a.pool_out ? 1 : (a.HW + px_per_cta - 1) / px_per_cta;
+    for (int item = blockIdx.x; item < a.B * chunks; item += gridDim.x) {
+        const int n = item / chunks, ck = item - n * chunks;
+        __syncthreads();   // the previous item's readers of sA / sB are done
+        gn_part_image_coef(a, n, sA, sB);
+        __syncthreads();
+        if (a.pool_out) {   // thread per 8 channels: the image's pixels summed in order, then / HW
+            for (int v = threadIdx.x; v < V; v += blockDim.x) {
+                const int c8 = v * 8;
+                float acc[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) acc[k] = 0.f;
+                for (int p = 0; p < a.HW; ++p) {
+                    const size_t o = (static_cast<size_t>(n) * a.HW + p) * a.C + c8;
+                    float y[8], r[8];
+                    unpack(ld16(a.y + o), uint16_t(), y);
+                    unpack(a.res ? ld16(a.res + o) : make_uint4(0u, 0u, 0u, 0u), uint16_t(), r);
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) acc[k] += fmaxf(fmaf(y[k], sA[c8 + k], sB[c8 + k]) + r[k], a.relu_lo);
+                }
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                    a.pool_out[static_cast<size_t>(n) * a.C + c8 + k] = acc[k] / static_cast<float>(a.HW);
+            }
+            continue;
+        }
+        const int p0 = ck * px_per_cta, p1 = min(a.HW, p0 + px_per_cta);
+        const long lo = static_cast<long>(p0) * V, hi = static_cast<long>(p1) * V;
+        const size_t img = static_cast<size_t>(n) * a.HW * a.C;
+        for (long i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+            const int c8 = static_cast<int>(i % V) * 8;
+            const size_t o = img + static_cast<size_t>(i) * 8;
+            float y[8], r[8], z[8];
+            unpack(ld16(a.y + o), uint16_t(), y);
+            unpack(a.res ? ld16(a.res + o) : make_uint4(0u, 0u, 0u, 0u), uint16_t(), r);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) z[k] = fmaxf(fmaf(y[k], sA[c8 + k], sB[c8 + k]) + r[k], a.relu_lo);
+            store_vec(a.out + o, z);
+        }
+    }
+}
+
 }  // namespace
+
+cudaError_t launch_gn_apply_part(const GnPartArgs &a, cudaStream_t s, bool pdl) {
+    if (a.C % 16 || a.C > kGnpMaxC || a.B < 1 || a.HW < 1 || a.tiles_per_img < 1) return cudaErrorInvalidValue;
+    // pixel chunk per CTA: about 2048 16-B vectors (8 per thread)
+    int px = 2048 / (a.C / 8);
+    if (px < 1) px = 1;
+    if (px > a.HW) px = a.HW;
+    const long items = a.pool_out ? a.B : static_cast<long>(a.B) * ((a.HW + px - 1) / px);
+    const long cap = a.max_ctas > 0 ? a.max_ctas : 148L * 8;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(static_cast<unsigned>(items < cap ? items : cap));
+    cfg.blockDim = dim3(kGnpThreads);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, gn_apply_part_kernel, a, px);
+}
 
 // Pixel lanes per vector slot: k = HW / kGnPPT (each thread holds kGnPPT pixels).
 static int gn_lanes(int HW) { return HW > kGnPPT ? (HW + kGnPPT - 1) / kGnPPT : 1; }

@@ -97,6 +97,9 @@ __global__ void __launch_bounds__(kSmall ? kHaloThreadsSmall : kHaloThreads, kSm
     auto r_full = [&](int i) { return bar0 + 8u * (24 + i); };
     auto r_empty = [&](int i) { return bar0 + 8u * (28 + i); };
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 32);
+    // GroupNorm statistics partials (a.gn_part): [tile group][16-ch group of the tile][lane quarter][image]
+    float4 *sGN = reinterpret_cast<float4 *>((reinterpret_cast<uintptr_t>(tmem_slot + 4) + 15) & ~uintptr_t(15));
+    const int gn_ng = a.n_tile / 16, gn_ni = a.tile_imgs;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int total = a.m_tiles * a.n_tiles;
@@ -689,6 +692,32 @@ __global__ void __launch_bounds__(kSmall ? kHaloThreadsSmall : kHaloThreads, kSm
                 for (int i = 0; i < 8; ++i) o[i] = pack_bf16(fmaxf(f[2 * i], a.relu_lo), fmaxf(f[2 * i + 1], a.relu_lo));
                 *reinterpret_cast<uint4 *>(pOutG + off0) = make_uint4(o[0], o[1], o[2], o[3]);
                 *reinterpret_cast<uint4 *>(pOutG + off1) = make_uint4(o[4], o[5], o[6], o[7]);
+                if (a.gn_part) {
+                    // GN statistics of the stored values: this thread's 16 (one pixel, one 16-channel group),
+                    // shifted by K = lane 0's first value (a sample of the same layer: keeps the sums of
+                    // squares from cancelling), summed over the lanes of the same image (fixed butterfly),
+                    // parked per (quarter, image) with K; the quarters are merged below
+                    const float K = __shfl_sync(0xffffffffu, bf16_lo(o[0]), 0);
+                    const unsigned long long K2 = f2pk(-K, -K);
+                    unsigned long long s1 = 0ull, s2 = 0ull;
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        const unsigned long long d = fadd2(f2pk(bf16_lo(o[i]), bf16_hi(o[i])), K2);
+                        s1 = fadd2(s1, d);
+                        s2 = ffma2(d, d, s2);
+                    }
+                    float a1, b1, a2, b2;
+                    f2upk(s1, a1, b1);
+                    f2upk(s2, a2, b2);
+                    float S1 = a1 + b1, S2 = a2 + b2;
+                    for (int ofs = 1; ofs < 32; ofs <<= 1) {
+                        if (ofs >= a.W && ofs < a.row_px) continue;   // would mix images of the tile
+                        S1 += __shfl_xor_sync(0xffffffffu, S1, ofs);
+                        S2 += __shfl_xor_sync(0xffffffffu, S2, ofs);
+                    }
+                    if (lane < a.row_px && lane % a.W == 0)
+                        sGN[((grp * gn_ng + g) * 4 + q) * gn_ni + lane / a.W] = make_float4(K, S1, S2, 0.f);
+                }
             }
             tc_fence_before();
             mbar_arrive(t_empty(as));
@@ -711,6 +740,34 @@ __global__ void __launch_bounds__(kSmall ? kHaloThreadsSmall : kHaloThreads, kSm
             }
             fence_proxy_async();
             named_bar_sync(1 + grp, gthreads);
+            if (a.gn_part) {   // merge the four lane quarters (equal counts, fixed order) -> global
+                const int tig = ((quad - grp * cw) * 4 + q) * 32 + lane;
+                const int ni_tile = a.tile_imgs;
+                for (int idx = tig; idx < gn_ng * ni_tile; idx += gthreads) {
+                    const int gg = idx / ni_tile, im = idx - gg * ni_tile;
+                    const float4 *pq = sGN + ((grp * gn_ng + gg) * 4) * gn_ni + im;
+                    const float cq = 16.f * 32.f * static_cast<float>(a.W) / static_cast<float>(a.row_px);   // per partial
+                    auto quarter = [&](const float4 v) {   // (K, S1, S2) -> (mean, M2) over cq values
+                        const float m = v.y / cq;
+                        return make_float2(v.x + m, fmaf(-v.y, m, v.z));
+                    };
+                    auto merge = [](float2 x, float2 y, float c) {   // two partials of c values each
+                        const float d = y.x - x.x;
+                        return make_float2((x.x + y.x) * 0.5f, (x.y + y.y) + d * d * (c * 0.5f));
+                    };
+                    const float2 tot = merge(merge(quarter(pq[0]), quarter(pq[gn_ni]), cq),
+                                             merge(quarter(pq[2 * gn_ni]), quarter(pq[3 * gn_ni]), cq), 2.f * cq);
+                    int nimg, ti;
+                    if (ni_tile == 1) {
+                        nimg = mt / tiles_per_img;
+                        ti = mt - nimg * tiles_per_img;
+                    } else {
+                        nimg = mt * ni_tile + im;
+                        ti = 0;
+                    }
+                    if (nimg < a.B) a.gn_part[(static_cast<size_t>(nimg) * tiles_per_img + ti) * (a.c_out / 16) + co0 / 16 + gg] = tot;
+                }
+            }
             if (leader && !(a.debug & 4)) {
                 TD(2, ti, 3);
                 for (uint32_t j = 0; j < a.n_out_chunks; ++j)
@@ -740,7 +797,8 @@ size_t conv_halo_smem_bytes(const HaloArgs &a) {
     const int n_res = (a.epi == EPI_BN_ADD_RELU) ? a.res_slots : 0;
     return 1024 + static_cast<size_t>(a.sa) * a.a_slot + static_cast<size_t>(a.sb) * a.b_bytes +
            chunk * (a.epi_groups + n_res) +
-           (a.epi == EPI_BN_PROJ_RELU ? 16 : 8) * static_cast<size_t>(a.c_out) + 8 * 32 + 16;
+           (a.epi == EPI_BN_PROJ_RELU ? 16 : 8) * static_cast<size_t>(a.c_out) + 8 * 32 + 16 +
+           (a.gn_part ? static_cast<size_t>(a.epi_groups) * (a.n_tile / 16) * 4 * a.tile_imgs * 16 + 16 : 0);
 }
 
 cudaError_t launch_conv_halo(const HaloArgs &a, const CUtensorMap &tmA, const CUtensorMap &tmB,

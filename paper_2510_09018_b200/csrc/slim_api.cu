@@ -173,7 +173,15 @@ size_t act_bytes(const slim_config &c, int s, float r, int B) {
     const int H = seg_hw(c, s);
     return static_cast<size_t>(B) * H * H * slim_act_channels(r, c.base_channels[s]) * elem_bytes(c);
 }
-size_t seg_ws_bytes(const slim_config &c, int s, float r, int B) { return 3 * round256(act_bytes(c, s, r, B)); }
+// GroupNorm mode: statistics partials of one layer, (mean, M2) per (image, 128-pixel tile, 16-channel group)
+size_t gn_part_bytes(const slim_config &c, int s, float r, int B) {
+    if (c.norm != SLIM_NORM_GN || c.dtype != SLIM_BF16) return 0;
+    const int H = seg_hw(c, s), tiles = H * H >= 128 ? H * H / 128 : 1;
+    return round256(static_cast<size_t>(B) * tiles * (slim_act_channels(r, c.base_channels[s]) / 16 + 1) * 8);
+}
+size_t seg_ws_bytes(const slim_config &c, int s, float r, int B) {
+    return 3 * round256(act_bytes(c, s, r, B)) + gn_part_bytes(c, s, r, B);
+}
 
 uint16_t f2bf(float f) {   // round-to-nearest-even (NaN kept NaN)
     uint32_t u;
@@ -361,6 +369,9 @@ struct ConvCall {
     float *pool_out = nullptr;               // fused global average pool (fp32 [B][c_out]) instead of `out`
     int epi = EPI_BN_RELU;
     float relu_lo = 0.f;                     // -inf: no ReLU (GroupNorm mode: raw pre-norm output)
+    float2 *gn_part = nullptr;               // GroupNorm mode: where the conv may write statistics partials
+    mutable bool gn_stats = false;           // set when the launched kernel wrote them (halo path)
+    mutable int gn_tiles_per_img = 0;        // their tiling (partials per image per group)
 };
 
 // Algorithmic work: 2*MACs of the sliced conv(s); bytes = input(s),
@@ -524,6 +535,7 @@ slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, i
     if (x3 || x2) {
         a.x3 = xmode;
         a.kw_fuse = 1;
+        a.gn_part = nullptr;   // (the x3 / x2 epilogues do not compute GN statistics)
     }
     if (s2) {   // [acc_kw0 | acc_kw2 | acc_kw1] adjacent; kw 0 and 2 as one N = 2n MMA
         if (2 * a.n_tile > 256) return SLIM_EUNSUPPORTED;
@@ -567,8 +579,16 @@ slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, i
     a.small = small ? 1 : 0;
     const bool two = small;
     const size_t budget = two ? 110 * 1024 : 226 * 1024;
+    // GroupNorm statistics partials (GN mode, plain / stride-2 variants): smem for the per-quarter merge.
+    // Opt-in (SLIM_GN_PART=1): measured slower than the separate GN reduction kernel -- the statistics
+    // add ~22 % to the epilogue-bound conv (seg 0 r=1: 18.8 -> 23.0 us standalone) while the elementwise
+    // apply costs the same launch as the reduction kernel it replaces (GN CFG2 step 663 k vs 716 k images/s,
+    // tools/gpu_runs/r02_gnpart.sh); kept as the measured alternative.
+    static const bool no_gn_part = getenv("SLIM_GN_PART") == nullptr || getenv("SLIM_GN_NO_PART") != nullptr;
+    a.gn_part = (cc.gn_part && !no_gn_part && !proj && !cc.pool_out && !small && !a.x3) ? cc.gn_part : nullptr;
     auto fixed0 = [&]() {
-        return 1024 + chunk * a.epi_groups + (proj ? 16 : 8) * static_cast<size_t>(c_out) + 8 * 32 + 16;
+        return 1024 + chunk * a.epi_groups + (proj ? 16 : 8) * static_cast<size_t>(c_out) + 8 * 32 + 16 +
+               (a.gn_part ? static_cast<size_t>(a.epi_groups) * (a.n_tile / 16) * 4 * a.tile_imgs * 16 + 16 : 0);
     };
     auto r1k = [](uint32_t x) { return (x + 1023u) & ~1023u; };
     const uint32_t all_w = r1k(static_cast<uint32_t>(a.n_chunks) * 9u * a.n_tile * a.rbk);
@@ -671,6 +691,10 @@ slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, i
     if (e != cudaSuccess)
         return fail(ctx, SLIM_ECUDA, "conv_halo launch (grid %d, smem %zu): %s", grid, conv_halo_smem_bytes(a),
                     cudaGetErrorString(e));
+    if (a.gn_part && !a.x3) {
+        cc.gn_stats = true;
+        cc.gn_tiles_per_img = a.tiles_per_img;
+    }
     return SLIM_OK;
 }
 
@@ -1123,6 +1147,40 @@ slim_status gn_apply(slim_ctx *ctx, cudaStream_t st, int seg, int layer, const D
     return SLIM_OK;
 }
 
+// GroupNorm mode, fast path: the conv wrote statistics partials (ConvCall::gn_stats); apply elementwise.
+slim_status gn_apply_part(slim_ctx *ctx, cudaStream_t st, int seg, int layer, const DevLayer &L, int ri, int B, int H,
+                          int C, const void *y, const float2 *part, int tiles_per_img, const void *res, void *out,
+                          float *pool_out = nullptr) {
+    const slim_config &c = ctx->cfg;
+    GnPartArgs g{};
+    g.y = static_cast<const uint16_t *>(y);
+    g.part = part;
+    g.res = static_cast<const uint16_t *>(res);
+    g.gamma = L.gn_gamma[ri];
+    g.beta = L.gn_beta[ri];
+    g.out = static_cast<uint16_t *>(out);
+    g.pool_out = pool_out;
+    g.B = B;
+    g.HW = H * H;
+    g.C = C;
+    g.tiles_per_img = tiles_per_img;
+    g.part_count = static_cast<float>(g.HW / tiles_per_img * 16);
+    g.eps = c.bn_eps;
+    g.relu_lo = 0.f;
+    {
+        const int cap = grid_cap(ctx, ri, ctx->num_sms, seg);
+        g.max_ctas = cap < ctx->num_sms ? 8 * cap : 0;
+    }
+    const double n = static_cast<double>(B) * H * H * C;
+    const double flops = 4.0 * n;
+    const double bytes = 2.0 * n * (2 + (res ? 1 : 0)) + 8.0 * C;
+    LaunchProf prof(ctx, st);
+    const cudaError_t e = launch_gn_apply_part(g, st, ctx->pdl && !ctx->prof_on);
+    prof.done(SLIM_K_GN, seg, layer, c.widths[ri], c.widths[ri], B, flops, bytes);
+    if (e != cudaSuccess) return fail(ctx, SLIM_ECUDA, "gn apply launch: %s", cudaGetErrorString(e));
+    return SLIM_OK;
+}
+
 slim_status run_segment(slim_ctx *ctx, int seg, int ri_prev, int ri, int B, const void *in, void *out, void *ws,
                         cudaStream_t st) {
     const slim_config &c = ctx->cfg;
@@ -1331,16 +1389,24 @@ slim_status run_segment(slim_ctx *ctx, int seg, int ri_prev, int ri, int B, cons
         if (gn) {
             // t = ReLU(GN1(conv1(x))): conv writes raw into T, GN in place.  u = conv2(t) raw into dst;
             // the projection (raw) reuses T once conv2 has read it; then dst = ReLU(GN2(u) + shortcut).
+            // Where the conv is the halo kernel it also writes the GroupNorm statistics partials (part),
+            // and the GN is an elementwise pass over them (gn_apply_part) instead of a reduction kernel.
+            float2 *part = bf ? reinterpret_cast<float2 *>(static_cast<char *>(ws) + 3 * buf) : nullptr;
             c1.relu_lo = relu_lo;
+            c1.gn_part = part;
             slim_status s1 = bf ? conv_bf16(ctx, st, c1, ri, B) : conv_f32(ctx, st, c1, ri, B);
             if (s1) return s1;
-            s1 = gn_apply(ctx, st, seg, bi.c1, S.L[bi.c1], nullptr, ri, B, H, C, T, nullptr, nullptr, T, true);
+            s1 = c1.gn_stats ? gn_apply_part(ctx, st, seg, bi.c1, S.L[bi.c1], ri, B, H, C, T, part, c1.gn_tiles_per_img,
+                                             nullptr, T)
+                             : gn_apply(ctx, st, seg, bi.c1, S.L[bi.c1], nullptr, ri, B, H, C, T, nullptr, nullptr, T, true);
             if (s1) return s1;
             ConvCall u = c2;
             u.epi = EPI_BN_RELU;
             u.relu_lo = relu_lo;
             u.res = nullptr;
             u.Lp = nullptr;
+            u.pool_out = nullptr;
+            u.gn_part = down ? nullptr : part;   // (a down block's GN pairs u with the projection's GN)
             s1 = bf ? conv_bf16(ctx, st, u, ri, B) : conv_f32(ctx, st, u, ri, B);
             if (s1) return s1;
             const void *yp = nullptr;
@@ -1367,8 +1433,10 @@ slim_status run_segment(slim_ctx *ctx, int seg, int ri_prev, int ri, int B, cons
                 void *pb = !down ? static_cast<void *>(T) : (cur != in ? const_cast<void *>(cur) : nullptr);
                 gn_pooled = static_cast<float *>(pb);
             }
-            s1 = gn_apply(ctx, st, seg, bi.c2, S.L[bi.c2], down ? &S.L[bi.sc] : nullptr, ri, B, H, C, dst, yp,
-                          down ? nullptr : cur, dst, true, gn_pooled);
+            s1 = u.gn_stats ? gn_apply_part(ctx, st, seg, bi.c2, S.L[bi.c2], ri, B, H, C, dst, part, u.gn_tiles_per_img,
+                                            cur, dst, gn_pooled)
+                            : gn_apply(ctx, st, seg, bi.c2, S.L[bi.c2], down ? &S.L[bi.sc] : nullptr, ri, B, H, C, dst, yp,
+                                       down ? nullptr : cur, dst, true, gn_pooled);
             if (s1) return s1;
             cur = dst;
             curH = H;

@@ -119,6 +119,10 @@ struct HaloArgs {
     int debug;
     unsigned long long *trace;
     float relu_lo;            // 0 = ReLU, -inf = raw pre-norm output (GroupNorm mode)
+    // GroupNorm mode: per-(image, tile, 16-channel group) statistics of the stored (bf16) raw output,
+    // (mean, M2) over the tile's pixels of that image, at gn_part[(n*tiles_per_img + ti)*(c_out/16) + g];
+    // nullptr = off.  The GN apply kernel then merges them (launch_gn_apply_part).
+    float2 *gn_part;
 };
 size_t conv_halo_smem_bytes(const HaloArgs &a);
 cudaError_t launch_conv_halo(const HaloArgs &a, const CUtensorMap &tmA, const CUtensorMap &tmB,
@@ -232,5 +236,20 @@ struct GnArgs {
 };
 int gn_groups_per_cta(int B, int HW, int C, int cpg, bool fp32);
 cudaError_t launch_gn(const GnArgs &a, bool fp32, cudaStream_t s, bool pdl);
+// GN apply from statistics partials the producing conv wrote (HaloArgs::gn_part): no reduction over
+// the image here -- an elementwise pass: out = act(GN(y) [+ res]) (bf16), or the average pool.
+struct GnPartArgs {
+    const uint16_t *y;             // raw conv output [B][HW][C] bf16
+    const float2 *part;            // (mean, M2) per (image, tile, 16-channel group), tiles_per_img per image
+    const uint16_t *res;           // identity residual or nullptr
+    const float *gamma, *beta;     // GN affine, C entries
+    uint16_t *out;                 // may alias y
+    float *pool_out;               // != nullptr: fp32 [B][C] average pool instead of out
+    int B, HW, C, tiles_per_img;
+    float part_count;              // values per partial (pixels of the image in one tile x 16)
+    float eps, relu_lo;
+    int max_ctas;
+};
+cudaError_t launch_gn_apply_part(const GnPartArgs &a, cudaStream_t s, bool pdl);
 
 }  // namespace slim

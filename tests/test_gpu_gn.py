@@ -152,3 +152,29 @@ def test_gn_other_depths_pool_paths(blocks):
     got3 = n.forward(3, _dev(h), 0.25, 0.75).cpu().numpy()
     _check(got3, ref.segment(3, h, 0.25, 0.75), TAU_BF16, f"GN seg3 blocks={blocks}")
     n.close()
+
+
+def test_gn_statistics_partials_path_parity():
+    """The opt-in GroupNorm path (SLIM_GN_PART=1): the halo conv writes per-(image, tile, group) statistics
+    partials and the GN becomes an elementwise pass over them -- same network within tolerance of the
+    oracle, bitwise batch independent."""
+    import os, subprocess, sys
+    code = (
+        "import numpy as np, torch, synth, oracle, paper_2510_09018_b200 as slim\n"
+        "w, bn = synth.make_weights(), synth.make_bn()\n"
+        "net = slim.SlimNet(w, bn, max_batch=64, norm='gn')\n"
+        "ref = oracle.Model(w, bn, norm='gn')\n"
+        "x = synth.make_images(20, offset=37)\n"
+        "xd = torch.from_numpy(x).to(torch.bfloat16).cuda()\n"
+        "worst = 0.0\n"
+        "for t in ((1.0, 1.0, 1.0, 1.0), (0.25, 0.75, 0.5, 1.0), (0.5, 0.5, 0.25, 0.25)):\n"
+        "    got = net.forward_chain(xd, t)\n"
+        "    sub = net.forward_chain(xd[3:7].contiguous(), t)\n"
+        "    assert torch.equal(got[3:7], sub)\n"
+        "    worst = max(worst, float(oracle.per_image_rel_err(got[:3].cpu().numpy(), ref.chain(x[:3], t)).max()))\n"
+        "print(worst)\n"
+    )
+    out = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, SLIM_GN_PART="1"), capture_output=True,
+                         text=True, timeout=600, cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert float(out.stdout.strip().splitlines()[-1]) <= 2e-2
