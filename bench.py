@@ -379,6 +379,16 @@ def run_ours(args):
                "method": "nvmlDeviceGetTotalEnergyConsumption delta over the loop (host wall clock)"}
               if (e0 is not None and e1 is not None and e1 > e0 and n_energy > 0) else None)
 
+    # ---------------- per-launch records (eager, an event pair around every launch, PDL off) of the SAME
+    # step configuration (the widths' SM shares select the same kernels as in the timed step): the
+    # algorithmic FLOPs/bytes of every kernel and its standalone duration -> the kernels' shares
+    KP = max(1, min(K, args.profile_steps))
+    slim.slim_profile_begin(net.ctx, KP * 80 * len(WIDTHS) + 16)
+    for _ in range(KP):
+        flush.zero_()
+        for r in WIDTHS:
+            chain(r, stream)
+    recs = slim.slim_profile_end(net.ctx)
     # ---------------- per-width: each width's chain alone (L2 flushed before it), on all SMs, graph replay
     # with PDL -- the same kernels as the step without the other instances
     set_shares({r: 1.0 for r in WIDTHS})
@@ -395,15 +405,6 @@ def run_ours(args):
         torch.cuda.synchronize()
         width_ms[r] = sum(x.elapsed_time(y) for x, y in evs) / KW
 
-    # ---------------- per-launch records (eager, an event pair around every launch, PDL off): the
-    # algorithmic FLOPs/bytes of every kernel and its standalone duration -> the kernels' shares
-    KP = max(1, min(K, args.profile_steps))
-    slim.slim_profile_begin(net.ctx, KP * 80 * len(WIDTHS) + 16)
-    for _ in range(KP):
-        flush.zero_()
-        for r in WIDTHS:
-            chain(r, stream)
-    recs = slim.slim_profile_end(net.ctx)
     peaks = _peaks()
     if args.dtype == "fp32":
         # FP32 mode runs on the CUDA cores (FFMA): peak = 148 SMs x 128 FP32 lanes x 2 FLOP x 1.965 GHz

@@ -697,7 +697,9 @@ __global__ void __launch_bounds__(kSmall ? kHaloThreadsSmall : kHaloThreads, kSm
                     // shifted by K = lane 0's first value (a sample of the same layer: keeps the sums of
                     // squares from cancelling), summed over the lanes of the same image (fixed butterfly),
                     // parked per (quarter, image) with K; the quarters are merged below
-                    const float K = __shfl_sync(0xffffffffu, bf16_lo(o[0]), 0);
+                    // (the image's first lane in this warp: the statistics of an image never depend on
+                    // which slot of the tile it occupies -> bitwise batch independent)
+                    const float K = __shfl_sync(0xffffffffu, bf16_lo(o[0]), ((lane % a.row_px) / a.W) * a.W);
                     const unsigned long long K2 = f2pk(-K, -K);
                     unsigned long long s1 = 0ull, s2 = 0ull;
 #pragma unroll

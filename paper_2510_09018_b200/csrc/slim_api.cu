@@ -1218,7 +1218,12 @@ slim_status run_segment(slim_ctx *ctx, int seg, int ri_prev, int ri, int B, cons
         }
         const double pix = static_cast<double>(B) * H * H;
         const double flops = 2.0 * pix * C * 9 * (c.in_channels + 4.0 * C);
-        const double bytes = eb * pix * (c.in_channels + C) + 2.0 * 4 * 9 * C * C + 2.0 * 64 * C + 40.0 * C;
+        // the SURVEY §8(d) roofline's layer-materialised bytes (each layer reads its input, residual and
+        // weights and writes its output), so the fused kernel is measured against the same roofline as
+        // the per-layer kernels; its compulsory traffic is only in + out + weights
+        const double bytes = eb * pix * (c.in_channels + C) + eb * 27.0 * C +                  // stem
+                             4.0 * (eb * pix * 2.0 * C + eb * 9.0 * C * C) + 2.0 * eb * pix * C +   // 4 convs, 2 residuals
+                             48.0 * C;
         int grid = std::min(B, ctx->num_sms);
         grid = grid_cap(ctx, ri, grid, 0);
         LaunchProf prof(ctx, st);
@@ -1260,8 +1265,12 @@ slim_status run_segment(slim_ctx *ctx, int seg, int ri_prev, int ri, int B, cons
         const int G = seg == 1 ? 1 : (seg == 2 ? 2 : 8);
         const double pix = static_cast<double>(B) * H * H;
         const double flops = 2.0 * pix * C * (9.0 * curC + 27.0 * C + curC);
-        const double bytes = eb * (static_cast<double>(B) * 4 * H * H * curC + (last ? 2.0 * B * C : pix * C)) +
-                             static_cast<double>(segn_fused_image_bytes(seg, C, curC));
+        // layer-materialised bytes (SURVEY §8(d) roofline, as the per-layer kernels count them)
+        const double in_b = eb * B * 4.0 * H * H * curC, act = eb * pix * C;
+        const double bytes = (in_b + act + eb * 9.0 * curC * C) +                  // b0c1 (stride 2)
+                             (act + in_b + act + eb * (9.0 * C * C + curC * C)) +   // b0c2 + projection
+                             (2.0 * act + eb * 9.0 * C * C) +                       // b1c1
+                             (3.0 * act + eb * 9.0 * C * C) + 40.0 * C;            // b1c2 + residual
         const int P = segn_fused_cluster(seg, C);
         int grid = std::min((B + G - 1) / G, ctx->num_sms / P);   // clusters (units in flight)
         if (fused_part != 2) grid = std::max(1, grid_cap(ctx, ri, grid * P, seg) / P);
