@@ -38,43 +38,66 @@ constexpr int kFsImg = 32;                  // H = W = 32 (CIFAR-shaped input)
 constexpr int kFsTiles = 8;                 // 1024 pixels / 128
 constexpr int kFsImgBytes = kFsImg * kFsImg * 3 * 2;
 
+__device__ __forceinline__ uint32_t fs_mapa(uint32_t addr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void fs_st_cluster(uint32_t addr, uint4 v) {
+    asm volatile("st.shared::cluster.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z),
+                 "r"(v.w)
+                 : "memory");
+}
+
+// P CTAs per image (a cluster): CTA p owns image rows [4*TPC*p, 4*TPC*(p+1)), TPC = 8/P tiles of 4 rows;
+// its activation buffers hold those rows plus one halo row above and below (LR = 4*TPC + 2 rows): at the
+// image border the zero padding, inside the image the neighbour CTA's boundary row, which the neighbour's
+// epilogue writes there through DSMEM before the layer barrier (P = 1: the whole image, 34 rows).
 struct FsLayout {
-    uint32_t rb, act, x, t, wc, ws, img, bn, bars, total;
+    uint32_t rb, act, x, t, wc, ws, img, sa, bn, bars, total;
 };
-__host__ __device__ inline FsLayout fs_layout(int c0) {
+__host__ __device__ inline FsLayout fs_layout(int c0, int P) {
     FsLayout L;
+    const uint32_t tpc = 8u / P, lr = 4u * tpc + 2u;
     L.rb = 2u * c0;
-    L.act = 34u * 32u * L.rb;
+    L.act = (lr * 32u * L.rb + 1023u) & ~1023u;
     L.x = 0;
     L.t = L.x + L.act;
     L.wc = L.t + L.act;
     L.ws = (L.wc + 4u * 9u * c0 * L.rb + 1023u) & ~1023u;
     L.img = L.ws + ((static_cast<uint32_t>(c0) * 64u + 1023u) & ~1023u);
-    L.bn = L.img + kFsImgBytes;
+    // stem im2col A slots (8 KiB each): inside T between its halo rows when T is large enough (P = 1)
+    const uint32_t slots = tpc < 4 ? tpc : 4;
+    L.sa = (P == 1) ? L.t + 32u * L.rb : ((L.img + kFsImgBytes + 1023u) & ~1023u);
+    L.bn = (P == 1) ? L.img + kFsImgBytes : L.sa + slots * 8192u;
     L.bars = L.bn + 5u * 2u * 32u * 4u;
     L.total = L.bars + 2u * kFsTiles * 8u + 16u;
     return L;
 }
 
-template <int C0>
+template <int C0, int P>
 __global__ void __launch_bounds__(kFsThreads, 1) seg0_fused_kernel(const FusedSeg0Args a) {
     constexpr int RB = 2 * C0, NG = C0 / 16;                 // row bytes, 16-channel groups
     constexpr int SC = C0 == 16 ? 64 : 128;                  // TMEM columns per tile stage (>= 3*C0)
     constexpr int S = 512 / SC;                              // stages: 8 | 4
     constexpr int PCS = RB / 16;                             // 16-B pieces per pixel row
+    constexpr int TPC = kFsTiles / P, LR = 4 * TPC + 2;      // tiles / local rows per CTA
+    constexpr int ROUND = TPC < 4 ? TPC : 4;                 // stem tiles per round (A slots)
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-    const FsLayout Lo = fs_layout(C0);
+    const FsLayout Lo = fs_layout(C0, P);
     uint8_t *pX = smem + Lo.x, *pT = smem + Lo.t, *pWc = smem + Lo.wc, *pWs = smem + Lo.ws;
-    uint8_t *pImg = smem + Lo.img;
+    uint8_t *pImg = smem + Lo.img, *pA = smem + Lo.sa;
     float *sBN = reinterpret_cast<float *>(smem + Lo.bn);   // [layer 0..4][scale 32 | shift 32]
     const uint32_t bar0 = smem_u32(smem + Lo.bars);
     auto t_full = [&](int s) { return bar0 + 8u * s; };
     auto t_empty = [&](int s) { return bar0 + 8u * (kFsTiles + s); };
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + Lo.bars + 2 * kFsTiles * 8);
     const uint32_t sX = smem_u32(pX), sT = smem_u32(pT), sWc = smem_u32(pWc), sWs = smem_u32(pWs);
-    const uint32_t sA = sT + 32u * RB;                       // stem A slots: inside T, past its zero row
+    const uint32_t sA = smem_u32(pA);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const uint32_t rank = P > 1 ? cluster_ctarank() : 0;
+    const int h_base = 4 * TPC * static_cast<int>(rank);   // first image row of this CTA
     // diagnostics: CTA 0, thread 0 (epilogue warp 0) stamps [0..15], the MMA warp's lane 0 [16..31]
     unsigned long long *tr = (a.trace && blockIdx.x == 0) ? a.trace : nullptr;
     int ntr = 0, ntm = 16;
@@ -84,21 +107,50 @@ __global__ void __launch_bounds__(kFsThreads, 1) seg0_fused_kernel(const FusedSe
         if (tr && warp == kFsEpiWarps && lane == 0 && ntm < 32) tr[ntm++] = gtimer(); \
     } while (0)
     FS_STAMP();
+    // layer barrier: the CTA, or the whole cluster (halo rows written into the neighbours)
+    auto layer_sync = [&]() {
+        if (P > 1) {
+            asm volatile("fence.proxy.async.shared::cluster;" ::: "memory");
+            tc_fence_before();
+            cluster_sync_all();
+        } else {
+            fence_proxy_async();
+            tc_fence_before();
+            __syncthreads();
+        }
+        tc_fence_after();
+    };
 
     // ---- prologue: nothing here is produced by the previous kernel (before the PDL wait)
-    for (int i = tid; i < 32 * RB / 16; i += kFsThreads) {   // zero rows of X and T (never written again)
+    for (int i = tid; i < 32 * RB / 16; i += kFsThreads) {   // zero rows at the image border (never written)
         const uint4 z = make_uint4(0, 0, 0, 0);
-        reinterpret_cast<uint4 *>(pX)[i] = z;
-        reinterpret_cast<uint4 *>(pX + 33 * 32 * RB)[i] = z;
-        reinterpret_cast<uint4 *>(pT)[i] = z;
-        reinterpret_cast<uint4 *>(pT + 33 * 32 * RB)[i] = z;
+        if (rank == 0) {
+            reinterpret_cast<uint4 *>(pX)[i] = z;
+            reinterpret_cast<uint4 *>(pT)[i] = z;
+        }
+        if (rank == P - 1) {
+            reinterpret_cast<uint4 *>(pX + (LR - 1) * 32 * RB)[i] = z;
+            reinterpret_cast<uint4 *>(pT + (LR - 1) * 32 * RB)[i] = z;
+        }
     }
-    // conv weights: row (l*9 + tap)*C0 + co holds w_l[co][tap][0..C0) (K-major, swizzled)
-    for (int i = tid; i < 4 * 9 * C0 * PCS; i += kFsThreads) {
-        const int j = i % PCS, row = i / PCS;
-        const int co = row % C0, lt = row / C0, tap = lt % 9, l = lt / 9;
-        const uint4 v = *reinterpret_cast<const uint4 *>(a.w[l] + (static_cast<size_t>(co) * 9 + tap) * a.cin_full + j * 8);
-        *reinterpret_cast<uint4 *>(pWc + swz_off(row, j, RB)) = v;
+    // conv weights: row (l*9 + tap)*C0 + co holds w_l[co][tap][0..C0) (K-major, swizzled); all of a thread's
+    // loads are issued before its stores (one global round trip instead of one per piece)
+    {
+        constexpr int NP = 4 * 9 * C0 * PCS, PER = (NP + kFsThreads - 1) / kFsThreads;
+        uint4 v[PER];
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const int i = tid + k * kFsThreads;
+            const int j = i % PCS, row = i / PCS;
+            const int co = row % C0, lt = row / C0, tap = lt % 9, l = lt / 9;
+            if (i < NP)
+                v[k] = *reinterpret_cast<const uint4 *>(a.w[l] + (static_cast<size_t>(co) * 9 + tap) * a.cin_full + j * 8);
+        }
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const int i = tid + k * kFsThreads;
+            if (i < NP) *reinterpret_cast<uint4 *>(pWc + swz_off(i / PCS, i % PCS, RB)) = v[k];
+        }
     }
     // stem weights: the SW128 B image built at load (128-B rows, K = 64 padded) -> SW64 rows (K = 32)
     for (int i = tid; i < C0 * 4; i += kFsThreads) {
@@ -127,7 +179,10 @@ __global__ void __launch_bounds__(kFsThreads, 1) seg0_fused_kernel(const FusedSe
     }
     fence_proxy_async();   // generic-proxy weight / zero-row writes -> visible to the tensor core
     tc_fence_before();
-    __syncthreads();
+    if (P > 1)
+        cluster_sync_all();
+    else
+        __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     FS_STAMP();
@@ -136,12 +191,28 @@ __global__ void __launch_bounds__(kFsThreads, 1) seg0_fused_kernel(const FusedSe
     FS_STAMP();
 
     const int g = warp >> 2, q = warp & 3;                   // epilogue tile group, TMEM lane quarter
-    const int row = q * 32 + lane;                           // tile row = image row 4t+q, column = lane
+    const int row = q * 32 + lane;                           // tile row = local tile row q, column = lane
     const uint32_t lane_addr = tmem + (static_cast<uint32_t>(q * 32) << 16);
     const float mL = lane > 0 ? 1.f : 0.f, mR = lane < 31 ? 1.f : 0.f;   // conv zero padding in W
     uint32_t u = 0;                                          // tile counter: stage u % S, phase u / S
+    // an output of local tile t, quarter q: local buffer row lr = 4t + q + 1; the boundary rows also go to
+    // the neighbour's halo row (DSMEM)
+    auto store_act = [&](uint8_t *buf, int t, int piece, uint4 v) {
+        const int lr = 4 * t + q + 1;
+        const uint32_t off = static_cast<uint32_t>(buf - smem) + swz_off(lr * 32 + lane, piece, RB);
+        *reinterpret_cast<uint4 *>(smem + off) = v;
+        if (P > 1) {
+            if (lr == 1 && rank > 0)   // first row -> the upper neighbour's bottom halo row
+                fs_st_cluster(fs_mapa(smem_u32(smem) + static_cast<uint32_t>(buf - smem) +
+                                          swz_off((LR - 1) * 32 + lane, piece, RB), rank - 1), v);
+            if (lr == LR - 2 && rank < P - 1)   // last row -> the lower neighbour's top halo row
+                fs_st_cluster(fs_mapa(smem_u32(smem) + static_cast<uint32_t>(buf - smem) + swz_off(lane, piece, RB),
+                                      rank + 1),
+                              v);
+        }
+    };
 
-    for (int img = blockIdx.x; img < a.B; img += gridDim.x) {
+    for (int img = blockIdx.x / P; img < a.B; img += gridDim.x / P) {
         // ---- the image -> smem (6 KiB, coalesced 16-B loads)
         {
             const uint4 *src = reinterpret_cast<const uint4 *>(a.in + static_cast<size_t>(img) * kFsImg * kFsImg * 3);
@@ -149,10 +220,10 @@ __global__ void __launch_bounds__(kFsThreads, 1) seg0_fused_kernel(const FusedSe
         }
         __syncthreads();
         FS_STAMP();
-        // ---- stem: conv3x3 3 -> C0 + BN + ReLU -> X; two rounds of four tiles (A slots 0..3)
-        for (int rnd = 0; rnd < 2; ++rnd) {
-            if (warp < kFsEpiWarps) {   // im2col: one output pixel (A row) per thread, K = (kh*3+kw)*3+ci
-                const int t = 4 * rnd + g, h = 4 * t + q;
+        // ---- stem: conv3x3 3 -> C0 + BN + ReLU -> X; rounds of up to four tiles (A slots 0..3)
+        for (int rnd = 0; rnd * ROUND < TPC; ++rnd) {
+            if (warp < kFsEpiWarps && g < ROUND) {   // im2col: one output pixel (A row) per thread
+                const int t = ROUND * rnd + g, h = h_base + 4 * t + q;
                 const uint16_t *im = reinterpret_cast<const uint16_t *>(pImg);
                 uint32_t packed[16];
 #pragma unroll
@@ -171,7 +242,7 @@ __global__ void __launch_bounds__(kFsThreads, 1) seg0_fused_kernel(const FusedSe
                             packed[k >> 1] |= (k & 1) ? (b << 16) : b;
                         }
                     }
-                uint8_t *dst = pT + 32 * RB + g * 8192;
+                uint8_t *dst = pA + g * 8192;
 #pragma unroll
                 for (int j = 0; j < 4; ++j)
                     *reinterpret_cast<uint4 *>(dst + swz_off(row, j, 64)) =
@@ -183,7 +254,7 @@ __global__ void __launch_bounds__(kFsThreads, 1) seg0_fused_kernel(const FusedSe
                 tc_fence_after();
                 const uint32_t idesc = umma_idesc_bf16(kTileM, C0);
                 const uint64_t bd = umma_desc_kmajor(sWs, 64);
-                for (int gg = 0; gg < 4; ++gg) {
+                for (int gg = 0; gg < ROUND; ++gg) {
                     const uint32_t uu = u + gg, s = uu % S;
                     if (uu >= static_cast<uint32_t>(S)) mbar_wait(t_empty(s), ((uu / S) - 1) & 1);
                     tc_fence_after();
@@ -195,12 +266,11 @@ __global__ void __launch_bounds__(kFsThreads, 1) seg0_fused_kernel(const FusedSe
                     }
                     __syncwarp();
                 }
-            } else {   // stem epilogue of tile 4*rnd + g -> X
-                const int t = 4 * rnd + g;
+            } else if (g < ROUND) {   // stem epilogue of tile ROUND*rnd + g -> X
+                const int t = ROUND * rnd + g;
                 const uint32_t uu = u + g, s = uu % S;
                 mbar_wait(t_full(s), (uu / S) & 1);
                 tc_fence_after();
-                const uint32_t R = 32u + static_cast<uint32_t>(t * 128 + row);   // padded pixel row in X
 #pragma unroll
                 for (int gi = 0; gi < NG; ++gi) {
                     uint32_t v[16];
@@ -214,27 +284,24 @@ __global__ void __launch_bounds__(kFsThreads, 1) seg0_fused_kernel(const FusedSe
                         o[i] = pack_bf16(fmaxf(fmaf(__uint_as_float(v[2 * i]), sBN[c], sBN[32 + c]), 0.f),
                                          fmaxf(fmaf(__uint_as_float(v[2 * i + 1]), sBN[c + 1], sBN[32 + c + 1]), 0.f));
                     }
-                    *reinterpret_cast<uint4 *>(pX + swz_off(R, 2 * gi, RB)) = make_uint4(o[0], o[1], o[2], o[3]);
-                    *reinterpret_cast<uint4 *>(pX + swz_off(R, 2 * gi + 1, RB)) = make_uint4(o[4], o[5], o[6], o[7]);
+                    store_act(pX, t, 2 * gi, make_uint4(o[0], o[1], o[2], o[3]));
+                    store_act(pX, t, 2 * gi + 1, make_uint4(o[4], o[5], o[6], o[7]));
                 }
                 tc_fence_before();
                 mbar_arrive(t_empty(s));
             }
-            u += 4;
+            u += ROUND;
             __syncthreads();   // this round's A slots consumed (each group waited for its MMA) before rebuild
             FS_STAMP();
         }
-        fence_proxy_async();
-        tc_fence_before();
-        __syncthreads();
-        tc_fence_after();
+        layer_sync();
         // ---- the two BasicBlocks: l = 0: X -> T, 1: T -> X (+ X), 2: X -> T, 3: T -> X (+ X) / global
         for (int l = 0; l < 4; ++l) {
             const uint32_t src = (l & 1) ? sT : sX;
             uint8_t *dst = (l & 1) ? pX : pT;
             if (warp == kFsEpiWarps) {
                 const uint32_t idesc = umma_idesc_bf16(kTileM, 3 * C0);
-                for (int t = 0; t < kFsTiles; ++t) {
+                for (int t = 0; t < TPC; ++t) {
                     const uint32_t uu = u + t, s = uu % S;
                     if (uu >= static_cast<uint32_t>(S)) mbar_wait(t_empty(s), ((uu / S) - 1) & 1);
                     tc_fence_after();
@@ -255,12 +322,12 @@ __global__ void __launch_bounds__(kFsThreads, 1) seg0_fused_kernel(const FusedSe
             } else {
                 const float *sc = sBN + (l + 1) * 64, *sh = sc + 32;
                 const bool res = (l & 1) != 0, last = l == 3;
-                for (int t = g; t < kFsTiles; t += 4) {
+                for (int t = g; t < TPC; t += 4) {
                     const uint32_t uu = u + t, s = uu % S;
                     mbar_wait(t_full(s), (uu / S) & 1);
                     tc_fence_after();
-                    const uint32_t R = 32u + static_cast<uint32_t>(t * 128 + row);
-                    const int h = 4 * t + q;
+                    const uint32_t R = static_cast<uint32_t>((4 * t + q + 1) * 32 + lane);   // local buffer row
+                    const int h = h_base + 4 * t + q;
 #pragma unroll
                     for (int gi = 0; gi < NG; ++gi) {
                         uint32_t v0[16], v1[16], v2[16];
@@ -306,24 +373,24 @@ __global__ void __launch_bounds__(kFsThreads, 1) seg0_fused_kernel(const FusedSe
                             gp[0] = o0;
                             gp[1] = o1;
                         } else {
-                            *reinterpret_cast<uint4 *>(p0) = o0;
-                            *reinterpret_cast<uint4 *>(p1) = o1;
+                            store_act(dst, t, 2 * gi, o0);
+                            store_act(dst, t, 2 * gi + 1, o1);
                         }
                     }
                     tc_fence_before();
                     mbar_arrive(t_empty(s));
                 }
-                fence_proxy_async();
             }
-            u += kFsTiles;
-            tc_fence_before();
-            __syncthreads();
-            tc_fence_after();
+            u += TPC;
+            layer_sync();
             FS_STAMP();
         }
     }
     tc_fence_before();
-    __syncthreads();
+    if (P > 1)
+        cluster_sync_all();
+    else
+        __syncthreads();
     if (warp == kFsEpiWarps) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512) : "memory");
@@ -332,32 +399,31 @@ __global__ void __launch_bounds__(kFsThreads, 1) seg0_fused_kernel(const FusedSe
 
 }  // namespace
 
-size_t seg0_fused_smem_bytes(int c0) { return 1024 + fs_layout(c0).total; }
+size_t seg0_fused_smem_bytes(int c0, int P) { return 1024 + fs_layout(c0, P).total; }
 
 cudaError_t launch_seg0_fused(const FusedSeg0Args &a, int grid, cudaStream_t stream, bool pdl) {
     if (a.c0 != 16 && a.c0 != 32) return cudaErrorInvalidValue;
+    const int P = a.cluster == 8 ? 8 : 1;
     using Fn = void (*)(FusedSeg0Args);
-    const Fn fn = a.c0 == 16 ? seg0_fused_kernel<16> : seg0_fused_kernel<32>;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(seg0_fused_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             static_cast<int>(seg0_fused_smem_bytes(16)));
-        if (e != cudaSuccess) return e;
-        e = cudaFuncSetAttribute(seg0_fused_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(seg0_fused_smem_bytes(32)));
-        if (e != cudaSuccess) return e;
-        attr_set = true;
-    }
+    const Fn fn = P == 8 ? (a.c0 == 16 ? seg0_fused_kernel<16, 8> : seg0_fused_kernel<32, 8>)
+                         : (a.c0 == 16 ? seg0_fused_kernel<16, 1> : seg0_fused_kernel<32, 1>);
+    const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               static_cast<int>(seg0_fused_smem_bytes(a.c0, P)));
+    if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(grid);
+    cfg.gridDim = dim3(grid * P);
     cfg.blockDim = dim3(kFsThreads);
-    cfg.dynamicSmemBytes = seg0_fused_smem_bytes(a.c0);
+    cfg.dynamicSmemBytes = seg0_fused_smem_bytes(a.c0, P);
     cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = P;
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     return cudaLaunchKernelEx(&cfg, fn, a);
 }
 

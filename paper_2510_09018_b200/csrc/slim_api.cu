@@ -1224,8 +1224,15 @@ slim_status run_segment(slim_ctx *ctx, int seg, int ri_prev, int ri, int B, cons
         const double bytes = eb * pix * (c.in_channels + C) + eb * 27.0 * C +                  // stem
                              4.0 * (eb * pix * 2.0 * C + eb * 9.0 * C * C) + 2.0 * eb * pix * C +   // 4 convs, 2 residuals
                              48.0 * C;
-        int grid = std::min(B, ctx->num_sms);
-        grid = grid_cap(ctx, ri, grid, 0);
+        // small batches: a cluster of 8 CTAs per image (one 4-row tile each, halo rows through DSMEM) --
+        // a layer is then one tile's MMA + epilogue instead of eight; one CTA per image once 8 B CTAs no
+        // longer fit the SMs (or the width shares the GPU).  Batch-independent either way (same
+        // arithmetic).  SLIM_SEG0_CLUSTER=0/8 forces.
+        static const int cl_env = getenv("SLIM_SEG0_CLUSTER") ? atoi(getenv("SLIM_SEG0_CLUSTER")) : -1;
+        const int cap_sms = grid_cap(ctx, ri, ctx->num_sms, 0);
+        fa.cluster = cl_env >= 0 ? (cl_env == 8 ? 8 : 1) : (8 * B <= cap_sms && cap_sms == ctx->num_sms ? 8 : 1);
+        int grid = std::min(B, ctx->num_sms / fa.cluster);
+        if (fa.cluster == 1) grid = grid_cap(ctx, ri, grid, 0);
         LaunchProf prof(ctx, st);
         const cudaError_t e = launch_seg0_fused(fa, grid, st, ctx->pdl && !ctx->prof_on);
         prof.done(SLIM_K_SEG_FUSED, 0, 0, r, r, B, flops, bytes);

@@ -159,8 +159,9 @@ struct FusedSeg0Args {
     const void *stem_b;            // the stem's SW128 B image (64 rows x 128 B, K = 27 zero-padded)
     const float *scale[5], *shift[5];   // folded BN of stem + four convs at this width, c0 entries
     unsigned long long *trace;     // diagnostics only (SLIM_CONV_TRACE): CTA 0 phase %globaltimer stamps
+    int cluster;                   // CTAs per image: 1 (whole image per CTA) or 8 (one 4-row tile each, DSMEM halo)
 };
-size_t seg0_fused_smem_bytes(int c0);
+size_t seg0_fused_smem_bytes(int c0, int P);
 
 // segments 1-3 as one kernel for the narrow widths (kernels_fused.cu): units of G images (seg 1: 1, 2: 2,
 // 3: 8), activations in shared memory, weights streamed from a pre-swizzled image (build_segn_fused_image)
