@@ -54,7 +54,7 @@ __device__ __forceinline__ void fs_st_cluster(uint32_t addr, uint4 v) {
 // image border the zero padding, inside the image the neighbour CTA's boundary row, which the neighbour's
 // epilogue writes there through DSMEM before the layer barrier (P = 1: the whole image, 34 rows).
 struct FsLayout {
-    uint32_t rb, act, x, t, wc, ws, img, sa, bn, bars, total;
+    uint32_t rb, act, x, t, wc, ws, img, sa, bn, bars, gn, total;
 };
 __host__ __device__ inline FsLayout fs_layout(int c0, int P) {
     FsLayout L;
@@ -71,11 +71,12 @@ __host__ __device__ inline FsLayout fs_layout(int c0, int P) {
     L.sa = (P == 1) ? L.t + 32u * L.rb : ((L.img + kFsImgBytes + 1023u) & ~1023u);
     L.bn = (P == 1) ? L.img + kFsImgBytes : L.sa + slots * 8192u;
     L.bars = L.bn + 5u * 2u * 32u * 4u;
-    L.total = L.bars + 2u * kFsTiles * 8u + 16u;
+    L.gn = (L.bars + 2u * kFsTiles * 8u + 16u + 15u) & ~15u;   // GroupNorm: partials + coefficients
+    L.total = L.gn + 1024u + 256u;
     return L;
 }
 
-template <int C0, int P>
+template <int C0, int P, bool GN>
 __global__ void __launch_bounds__(kFsThreads, 1) seg0_fused_kernel(const FusedSeg0Args a) {
     constexpr int RB = 2 * C0, NG = C0 / 16;                 // row bytes, 16-channel groups
     constexpr int SC = C0 == 16 ? 64 : 128;                  // TMEM columns per tile stage (>= 3*C0)
@@ -212,6 +213,86 @@ __global__ void __launch_bounds__(kFsThreads, 1) seg0_fused_kernel(const FusedSe
         }
     };
 
+    // GroupNorm (GN): two passes per layer over the same (recomputed) accumulators -- pass 1 the per-(image,
+    // 16-channel group) statistics of the fp32 raw output (per thread (mean, M2) of its 16 values, merged
+    // with equal counts in one fixed tree: 32 lanes -> 4 lane quarters -> tiles; a cluster merges its CTAs'
+    // tile partials in the same tree, so P = 1 and P = 8 agree bit for bit), pass 2 the normalisation
+    // y * A + Bc (A = rstd * gamma, Bc = beta - mean * A) in the epilogue that BatchNorm uses.
+    float2 *sPart = reinterpret_cast<float2 *>(smem + Lo.gn);          // [tile][quarter][group] (count 512)
+    float2 *sClu = sPart + kFsTiles * 4 * NG;                           // [rank][group] tile partials (P > 1)
+    float *sCoef = reinterpret_cast<float *>(sClu + 8 * NG);            // [A 32 | Bc 32]
+    auto merge2 = [](float2 x, float2 y, float c) {   // two partials of c values each
+        const float d = y.x - x.x;
+        return make_float2((x.x + y.x) * 0.5f, (x.y + y.y) + d * d * (c * 0.5f));
+    };
+    // per-thread statistics of 16 values, merged over the warp (all 32 lanes: one image row, one group)
+    auto warp_stats = [&](const float (&y)[16], int t, int gi) {
+        float mu = 0.f;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) mu += y[i];
+        mu *= (1.f / 16.f);
+        float m2 = 0.f;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) m2 = fmaf(y[i] - mu, y[i] - mu, m2);
+        float cnt = 16.f;
+        for (int ofs = 1; ofs < 32; ofs <<= 1) {
+            const float mo = __shfl_xor_sync(0xffffffffu, mu, ofs), qo = __shfl_xor_sync(0xffffffffu, m2, ofs);
+            const float d = mo - mu;
+            m2 = (m2 + qo) + d * d * (cnt * 0.5f);
+            mu = (mu + mo) * 0.5f;
+            cnt *= 2.f;
+        }
+        if (lane == 0) sPart[(t * 4 + q) * NG + gi] = make_float2(mu, m2);
+    };
+    // after pass 1: the image's statistics per group -> coefficients (layer lgn's gamma / beta in sBN)
+    auto gn_finish = [&](int lgn) {
+        __syncthreads();
+        if (tid < NG) {
+            float2 tp[TPC];
+#pragma unroll
+            for (int t = 0; t < TPC; ++t) {
+                const float2 *pq = sPart + (t * 4) * NG + tid;
+                tp[t] = merge2(merge2(pq[0], pq[NG], 512.f), merge2(pq[2 * NG], pq[3 * NG], 512.f), 1024.f);
+            }
+            if (P > 1) {   // this CTA's tile partial into every CTA's rank slot
+                for (int pr = 0; pr < P; ++pr)
+                    asm volatile("st.shared::cluster.v2.f32 [%0], {%1, %2};" ::"r"(fs_mapa(
+                                     smem_u32(sClu + static_cast<int>(rank) * NG + tid), pr)),
+                                 "f"(tp[0].x), "f"(tp[0].y)
+                                 : "memory");
+            } else {
+#pragma unroll
+                for (int t = 0; t < TPC; ++t) sClu[t * NG + tid] = tp[t];
+            }
+        }
+        if (P > 1) cluster_sync_all();
+        else __syncthreads();
+        if (tid < NG) {   // fixed pairwise tree over the 8 tile partials (2048 values each)
+            float2 v[8];
+#pragma unroll
+            for (int t = 0; t < 8; ++t) v[t] = sClu[t * NG + tid];
+            float c = 2048.f;
+#pragma unroll
+            for (int w = 8; w > 1; w >>= 1) {
+#pragma unroll
+                for (int t = 0; t < w / 2; ++t) v[t] = merge2(v[2 * t], v[2 * t + 1], c);
+                c *= 2.f;
+            }
+            const float rstd = rsqrtf(fmaxf(v[0].y * (1.f / 16384.f), 0.f) + a.eps);
+            sCoef[64 + tid * 2] = v[0].x;
+            sCoef[64 + tid * 2 + 1] = rstd;
+        }
+        __syncthreads();
+        if (tid < C0) {
+            const float mean = sCoef[64 + (tid / 16) * 2], rstd = sCoef[64 + (tid / 16) * 2 + 1];
+            const float A = rstd * sBN[lgn * 64 + tid];
+            sCoef[tid] = A;
+            sCoef[32 + tid] = fmaf(-mean, A, sBN[lgn * 64 + 32 + tid]);
+        }
+        __syncthreads();
+    };
+    constexpr int NPASS = GN ? 2 : 1;
+
     for (int img = blockIdx.x / P; img < a.B; img += gridDim.x / P) {
         // ---- the image -> smem (6 KiB, coalesced 16-B loads)
         {
@@ -220,168 +301,202 @@ __global__ void __launch_bounds__(kFsThreads, 1) seg0_fused_kernel(const FusedSe
         }
         __syncthreads();
         FS_STAMP();
-        // ---- stem: conv3x3 3 -> C0 + BN + ReLU -> X; rounds of up to four tiles (A slots 0..3)
-        for (int rnd = 0; rnd * ROUND < TPC; ++rnd) {
-            if (warp < kFsEpiWarps && g < ROUND) {   // im2col: one output pixel (A row) per thread
-                const int t = ROUND * rnd + g, h = h_base + 4 * t + q;
-                const uint16_t *im = reinterpret_cast<const uint16_t *>(pImg);
-                uint32_t packed[16];
+        // ---- stem: conv3x3 3 -> C0 + norm + ReLU -> X; rounds of up to four tiles (A slots 0..3)
+        for (int pass = 2 - NPASS + 1; pass <= 2; ++pass) {
+            const float *cA = GN ? sCoef : sBN, *cB = GN ? sCoef + 32 : sBN + 32;
+            for (int rnd = 0; rnd * ROUND < TPC; ++rnd) {
+                if (warp < kFsEpiWarps && g < ROUND) {   // im2col: one output pixel (A row) per thread
+                    const int t = ROUND * rnd + g, h = h_base + 4 * t + q;
+                    const uint16_t *im = reinterpret_cast<const uint16_t *>(pImg);
+                    uint32_t packed[16];
 #pragma unroll
-                for (int j = 0; j < 16; ++j) packed[j] = 0;
+                    for (int j = 0; j < 16; ++j) packed[j] = 0;
 #pragma unroll
-                for (int kh = 0; kh < 3; ++kh)
+                    for (int kh = 0; kh < 3; ++kh)
 #pragma unroll
-                    for (int kw = 0; kw < 3; ++kw) {
-                        const int ih = h + kh - 1, iw = lane + kw - 1;
-                        const bool ok = ih >= 0 && ih < kFsImg && iw >= 0 && iw < kFsImg;
-                        const uint16_t *px = im + (ih * kFsImg + iw) * 3;
+                        for (int kw = 0; kw < 3; ++kw) {
+                            const int ih = h + kh - 1, iw = lane + kw - 1;
+                            const bool ok = ih >= 0 && ih < kFsImg && iw >= 0 && iw < kFsImg;
+                            const uint16_t *px = im + (ih * kFsImg + iw) * 3;
 #pragma unroll
-                        for (int ci = 0; ci < 3; ++ci) {
-                            const int k = (kh * 3 + kw) * 3 + ci;
-                            const uint32_t b = ok ? static_cast<uint32_t>(px[ci]) : 0u;
-                            packed[k >> 1] |= (k & 1) ? (b << 16) : b;
+                            for (int ci = 0; ci < 3; ++ci) {
+                                const int k = (kh * 3 + kw) * 3 + ci;
+                                const uint32_t b = ok ? static_cast<uint32_t>(px[ci]) : 0u;
+                                packed[k >> 1] |= (k & 1) ? (b << 16) : b;
+                            }
                         }
-                    }
-                uint8_t *dst = pA + g * 8192;
+                    uint8_t *dst = pA + g * 8192;
 #pragma unroll
-                for (int j = 0; j < 4; ++j)
-                    *reinterpret_cast<uint4 *>(dst + swz_off(row, j, 64)) =
-                        make_uint4(packed[4 * j], packed[4 * j + 1], packed[4 * j + 2], packed[4 * j + 3]);
-                fence_proxy_async();
-            }
-            __syncthreads();
-            if (warp == kFsEpiWarps) {
-                tc_fence_after();
-                const uint32_t idesc = umma_idesc_bf16(kTileM, C0);
-                const uint64_t bd = umma_desc_kmajor(sWs, 64);
-                for (int gg = 0; gg < ROUND; ++gg) {
-                    const uint32_t uu = u + gg, s = uu % S;
-                    if (uu >= static_cast<uint32_t>(S)) mbar_wait(t_empty(s), ((uu / S) - 1) & 1);
+                    for (int j = 0; j < 4; ++j)
+                        *reinterpret_cast<uint4 *>(dst + swz_off(row, j, 64)) =
+                            make_uint4(packed[4 * j], packed[4 * j + 1], packed[4 * j + 2], packed[4 * j + 3]);
+                    fence_proxy_async();
+                }
+                __syncthreads();
+                if (warp == kFsEpiWarps) {
                     tc_fence_after();
-                    if (elect_one()) {
-                        const uint64_t ad = umma_desc_kmajor(sA + gg * 8192, 64);
-                        umma_bf16(tmem + s * SC, ad, bd, idesc, 0u);
-                        umma_bf16(tmem + s * SC, ad + 2, bd + 2, idesc, 1u);
-                        umma_commit(t_full(s));
+                    const uint32_t idesc = umma_idesc_bf16(kTileM, C0);
+                    const uint64_t bd = umma_desc_kmajor(sWs, 64);
+                    for (int gg = 0; gg < ROUND; ++gg) {
+                        const uint32_t uu = u + gg, s = uu % S;
+                        if (uu >= static_cast<uint32_t>(S)) mbar_wait(t_empty(s), ((uu / S) - 1) & 1);
+                        tc_fence_after();
+                        if (elect_one()) {
+                            const uint64_t ad = umma_desc_kmajor(sA + gg * 8192, 64);
+                            umma_bf16(tmem + s * SC, ad, bd, idesc, 0u);
+                            umma_bf16(tmem + s * SC, ad + 2, bd + 2, idesc, 1u);
+                            umma_commit(t_full(s));
+                        }
+                        __syncwarp();
                     }
-                    __syncwarp();
-                }
-            } else if (g < ROUND) {   // stem epilogue of tile ROUND*rnd + g -> X
-                const int t = ROUND * rnd + g;
-                const uint32_t uu = u + g, s = uu % S;
-                mbar_wait(t_full(s), (uu / S) & 1);
-                tc_fence_after();
+                } else if (g < ROUND) {   // stem epilogue of tile ROUND*rnd + g
+                    const int t = ROUND * rnd + g;
+                    const uint32_t uu = u + g, s = uu % S;
+                    mbar_wait(t_full(s), (uu / S) & 1);
+                    tc_fence_after();
 #pragma unroll
-                for (int gi = 0; gi < NG; ++gi) {
-                    uint32_t v[16];
-                    tmem_ld16(lane_addr + s * SC + gi * 16, v);
-                    tmem_wait_ld();
-                    reg_fence16(v);
-                    uint32_t o[8];
+                    for (int gi = 0; gi < NG; ++gi) {
+                        uint32_t v[16];
+                        tmem_ld16(lane_addr + s * SC + gi * 16, v);
+                        tmem_wait_ld();
+                        reg_fence16(v);
+                        if (GN && pass == 1) {
+                            float y[16];
 #pragma unroll
-                    for (int i = 0; i < 8; ++i) {
-                        const int c = gi * 16 + 2 * i;
-                        o[i] = pack_bf16(fmaxf(fmaf(__uint_as_float(v[2 * i]), sBN[c], sBN[32 + c]), 0.f),
-                                         fmaxf(fmaf(__uint_as_float(v[2 * i + 1]), sBN[c + 1], sBN[32 + c + 1]), 0.f));
+                            for (int i = 0; i < 16; ++i) y[i] = __uint_as_float(v[i]);
+                            warp_stats(y, t, gi);
+                            continue;
+                        }
+                        uint32_t o[8];
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) {
+                            const int c = gi * 16 + 2 * i;
+                            o[i] = pack_bf16(fmaxf(fmaf(__uint_as_float(v[2 * i]), cA[c], cB[c]), 0.f),
+                                             fmaxf(fmaf(__uint_as_float(v[2 * i + 1]), cA[c + 1], cB[c + 1]), 0.f));
+                        }
+                        store_act(pX, t, 2 * gi, make_uint4(o[0], o[1], o[2], o[3]));
+                        store_act(pX, t, 2 * gi + 1, make_uint4(o[4], o[5], o[6], o[7]));
                     }
-                    store_act(pX, t, 2 * gi, make_uint4(o[0], o[1], o[2], o[3]));
-                    store_act(pX, t, 2 * gi + 1, make_uint4(o[4], o[5], o[6], o[7]));
+                    tc_fence_before();
+                    mbar_arrive(t_empty(s));
                 }
-                tc_fence_before();
-                mbar_arrive(t_empty(s));
+                u += ROUND;
+                __syncthreads();   // this round's A slots consumed (each group waited for its MMA) before rebuild
+                FS_STAMP();
             }
-            u += ROUND;
-            __syncthreads();   // this round's A slots consumed (each group waited for its MMA) before rebuild
-            FS_STAMP();
+            if (GN && pass == 1) gn_finish(0);
         }
         layer_sync();
         // ---- the two BasicBlocks: l = 0: X -> T, 1: T -> X (+ X), 2: X -> T, 3: T -> X (+ X) / global
         for (int l = 0; l < 4; ++l) {
             const uint32_t src = (l & 1) ? sT : sX;
             uint8_t *dst = (l & 1) ? pX : pT;
-            if (warp == kFsEpiWarps) {
-                const uint32_t idesc = umma_idesc_bf16(kTileM, 3 * C0);
-                for (int t = 0; t < TPC; ++t) {
-                    const uint32_t uu = u + t, s = uu % S;
-                    if (uu >= static_cast<uint32_t>(S)) mbar_wait(t_empty(s), ((uu / S) - 1) & 1);
-                    tc_fence_after();
-                    if (elect_one()) {
+            for (int pass = 2 - NPASS + 1; pass <= 2; ++pass) {
+                if (warp == kFsEpiWarps) {
+                    const uint32_t idesc = umma_idesc_bf16(kTileM, 3 * C0);
+                    for (int t = 0; t < TPC; ++t) {
+                        const uint32_t uu = u + t, s = uu % S;
+                        if (uu >= static_cast<uint32_t>(S)) mbar_wait(t_empty(s), ((uu / S) - 1) & 1);
+                        tc_fence_after();
+                        if (elect_one()) {
 #pragma unroll
-                        for (int kh = 0; kh < 3; ++kh) {
-                            const uint64_t ad = umma_desc_kmajor(src + static_cast<uint32_t>((4 * t + kh) * 32 * RB), RB);
-                            const uint64_t bd =
-                                umma_desc_kmajor(sWc + static_cast<uint32_t>((l * 9 + kh * 3) * C0 * RB), RB);
+                            for (int kh = 0; kh < 3; ++kh) {
+                                const uint64_t ad =
+                                    umma_desc_kmajor(src + static_cast<uint32_t>((4 * t + kh) * 32 * RB), RB);
+                                const uint64_t bd =
+                                    umma_desc_kmajor(sWc + static_cast<uint32_t>((l * 9 + kh * 3) * C0 * RB), RB);
 #pragma unroll
-                            for (int kk = 0; kk < C0 / 16; ++kk)
-                                umma_bf16(tmem + s * SC, ad + 2 * kk, bd + 2 * kk, idesc, (kh | kk) != 0);
+                                for (int kk = 0; kk < C0 / 16; ++kk)
+                                    umma_bf16(tmem + s * SC, ad + 2 * kk, bd + 2 * kk, idesc, (kh | kk) != 0);
+                            }
+                            umma_commit(t_full(s));
                         }
-                        umma_commit(t_full(s));
+                        __syncwarp();
                     }
-                    __syncwarp();
+                } else {
+                    const float *sc = GN ? sCoef : sBN + (l + 1) * 64, *sh = sc + 32;
+                    const bool res = (l & 1) != 0, last = l == 3;
+                    for (int t = g; t < TPC; t += 4) {
+                        const uint32_t uu = u + t, s = uu % S;
+                        mbar_wait(t_full(s), (uu / S) & 1);
+                        tc_fence_after();
+                        const uint32_t R = static_cast<uint32_t>((4 * t + q + 1) * 32 + lane);   // local buffer row
+                        const int h = h_base + 4 * t + q;
+#pragma unroll
+                        for (int gi = 0; gi < NG; ++gi) {
+                            uint32_t v0[16], v1[16], v2[16];
+                            const uint32_t col = lane_addr + s * SC + gi * 16;
+                            tmem_ld16(col, v0);
+                            tmem_ld16(col + C0, v1);
+                            tmem_ld16(col + 2 * C0, v2);
+                            tmem_wait_ld();
+                            reg_fence16(v0);
+                            reg_fence16(v1);
+                            reg_fence16(v2);
+                            float f[16];
+                            const unsigned long long mL2 = f2pk(mL, mL), mR2 = f2pk(mR, mR);
+                            if (GN && pass == 1) {   // raw output (acc0[w-1] + acc1[w] + acc2[w+1]) -> statistics
+#pragma unroll
+                                for (int i = 0; i < 16; i += 2) {
+                                    const float l0 = __shfl_up_sync(0xffffffffu, __uint_as_float(v0[i]), 1);
+                                    const float l1 = __shfl_up_sync(0xffffffffu, __uint_as_float(v0[i + 1]), 1);
+                                    const float r0 = __shfl_down_sync(0xffffffffu, __uint_as_float(v2[i]), 1);
+                                    const float r1 = __shfl_down_sync(0xffffffffu, __uint_as_float(v2[i + 1]), 1);
+                                    f2upk(ffma2(mR2, f2pk(r0, r1),
+                                                ffma2(mL2, f2pk(l0, l1),
+                                                      f2pk(__uint_as_float(v1[i]), __uint_as_float(v1[i + 1])))),
+                                          f[i], f[i + 1]);
+                                }
+                                warp_stats(f, t, gi);
+                                continue;
+                            }
+#pragma unroll
+                            for (int i = 0; i < 16; i += 2) {   // out[w] = acc0[w-1] + acc1[w] + acc2[w+1], then norm
+                                const float l0 = __shfl_up_sync(0xffffffffu, __uint_as_float(v0[i]), 1);
+                                const float l1 = __shfl_up_sync(0xffffffffu, __uint_as_float(v0[i + 1]), 1);
+                                const float r0 = __shfl_down_sync(0xffffffffu, __uint_as_float(v2[i]), 1);
+                                const float r1 = __shfl_down_sync(0xffffffffu, __uint_as_float(v2[i + 1]), 1);
+                                const unsigned long long y = ffma2(
+                                    mR2, f2pk(r0, r1),
+                                    ffma2(mL2, f2pk(l0, l1), f2pk(__uint_as_float(v1[i]), __uint_as_float(v1[i + 1]))));
+                                const int c = gi * 16 + i;
+                                f2upk(ffma2(y, f2pk(sc[c], sc[c + 1]), f2pk(sh[c], sh[c + 1])), f[i], f[i + 1]);
+                            }
+                            uint8_t *p0 = dst + swz_off(R, 2 * gi, RB), *p1 = dst + swz_off(R, 2 * gi + 1, RB);
+                            if (res) {   // + the block input (in place: this thread's own pixel and channels)
+                                const uint4 r0 = *reinterpret_cast<const uint4 *>(p0);
+                                const uint4 r1 = *reinterpret_cast<const uint4 *>(p1);
+                                const uint32_t rr[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+#pragma unroll
+                                for (int i = 0; i < 8; ++i)
+                                    f2upk(fadd2(f2pk(f[2 * i], f[2 * i + 1]), f2pk(bf16_lo(rr[i]), bf16_hi(rr[i]))),
+                                          f[2 * i], f[2 * i + 1]);
+                            }
+                            uint32_t o[8];
+#pragma unroll
+                            for (int i = 0; i < 8; ++i) o[i] = pack_bf16(fmaxf(f[2 * i], 0.f), fmaxf(f[2 * i + 1], 0.f));
+                            const uint4 o0 = make_uint4(o[0], o[1], o[2], o[3]), o1 = make_uint4(o[4], o[5], o[6], o[7]);
+                            if (last) {   // segment output [B][32][32][C0]
+                                uint4 *gp = reinterpret_cast<uint4 *>(
+                                    a.out + ((static_cast<size_t>(img) * kFsImg + h) * kFsImg + lane) * C0 + gi * 16);
+                                gp[0] = o0;
+                                gp[1] = o1;
+                            } else {
+                                store_act(dst, t, 2 * gi, o0);
+                                store_act(dst, t, 2 * gi + 1, o1);
+                            }
+                        }
+                        tc_fence_before();
+                        mbar_arrive(t_empty(s));
+                    }
                 }
-            } else {
-                const float *sc = sBN + (l + 1) * 64, *sh = sc + 32;
-                const bool res = (l & 1) != 0, last = l == 3;
-                for (int t = g; t < TPC; t += 4) {
-                    const uint32_t uu = u + t, s = uu % S;
-                    mbar_wait(t_full(s), (uu / S) & 1);
-                    tc_fence_after();
-                    const uint32_t R = static_cast<uint32_t>((4 * t + q + 1) * 32 + lane);   // local buffer row
-                    const int h = h_base + 4 * t + q;
-#pragma unroll
-                    for (int gi = 0; gi < NG; ++gi) {
-                        uint32_t v0[16], v1[16], v2[16];
-                        const uint32_t col = lane_addr + s * SC + gi * 16;
-                        tmem_ld16(col, v0);
-                        tmem_ld16(col + C0, v1);
-                        tmem_ld16(col + 2 * C0, v2);
-                        tmem_wait_ld();
-                        reg_fence16(v0);
-                        reg_fence16(v1);
-                        reg_fence16(v2);
-                        float f[16];
-                        const unsigned long long mL2 = f2pk(mL, mL), mR2 = f2pk(mR, mR);
-#pragma unroll
-                        for (int i = 0; i < 16; i += 2) {   // out[w] = acc0[w-1] + acc1[w] + acc2[w+1], then BN
-                            const float l0 = __shfl_up_sync(0xffffffffu, __uint_as_float(v0[i]), 1);
-                            const float l1 = __shfl_up_sync(0xffffffffu, __uint_as_float(v0[i + 1]), 1);
-                            const float r0 = __shfl_down_sync(0xffffffffu, __uint_as_float(v2[i]), 1);
-                            const float r1 = __shfl_down_sync(0xffffffffu, __uint_as_float(v2[i + 1]), 1);
-                            const unsigned long long y = ffma2(
-                                mR2, f2pk(r0, r1),
-                                ffma2(mL2, f2pk(l0, l1), f2pk(__uint_as_float(v1[i]), __uint_as_float(v1[i + 1]))));
-                            const int c = gi * 16 + i;
-                            f2upk(ffma2(y, f2pk(sc[c], sc[c + 1]), f2pk(sh[c], sh[c + 1])), f[i], f[i + 1]);
-                        }
-                        uint8_t *p0 = dst + swz_off(R, 2 * gi, RB), *p1 = dst + swz_off(R, 2 * gi + 1, RB);
-                        if (res) {   // + the block input (in place: this thread's own pixel and channels)
-                            const uint4 r0 = *reinterpret_cast<const uint4 *>(p0);
-                            const uint4 r1 = *reinterpret_cast<const uint4 *>(p1);
-                            const uint32_t rr[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
-#pragma unroll
-                            for (int i = 0; i < 8; ++i)
-                                f2upk(fadd2(f2pk(f[2 * i], f[2 * i + 1]), f2pk(bf16_lo(rr[i]), bf16_hi(rr[i]))),
-                                      f[2 * i], f[2 * i + 1]);
-                        }
-                        uint32_t o[8];
-#pragma unroll
-                        for (int i = 0; i < 8; ++i) o[i] = pack_bf16(fmaxf(f[2 * i], 0.f), fmaxf(f[2 * i + 1], 0.f));
-                        const uint4 o0 = make_uint4(o[0], o[1], o[2], o[3]), o1 = make_uint4(o[4], o[5], o[6], o[7]);
-                        if (last) {   // segment output [B][32][32][C0]
-                            uint4 *gp = reinterpret_cast<uint4 *>(
-                                a.out + ((static_cast<size_t>(img) * kFsImg + h) * kFsImg + lane) * C0 + gi * 16);
-                            gp[0] = o0;
-                            gp[1] = o1;
-                        } else {
-                            store_act(dst, t, 2 * gi, o0);
-                            store_act(dst, t, 2 * gi + 1, o1);
-                        }
-                    }
+                u += TPC;
+                if (GN && pass == 1) {
                     tc_fence_before();
-                    mbar_arrive(t_empty(s));
+                    gn_finish(l + 1);
+                    tc_fence_after();
                 }
             }
-            u += TPC;
             layer_sync();
             FS_STAMP();
         }
@@ -405,8 +520,11 @@ cudaError_t launch_seg0_fused(const FusedSeg0Args &a, int grid, cudaStream_t str
     if (a.c0 != 16 && a.c0 != 32) return cudaErrorInvalidValue;
     const int P = a.cluster == 8 ? 8 : 1;
     using Fn = void (*)(FusedSeg0Args);
-    const Fn fn = P == 8 ? (a.c0 == 16 ? seg0_fused_kernel<16, 8> : seg0_fused_kernel<32, 8>)
-                         : (a.c0 == 16 ? seg0_fused_kernel<16, 1> : seg0_fused_kernel<32, 1>);
+    const Fn fns[2][2][2] = {{{seg0_fused_kernel<16, 1, false>, seg0_fused_kernel<16, 1, true>},
+                              {seg0_fused_kernel<16, 8, false>, seg0_fused_kernel<16, 8, true>}},
+                             {{seg0_fused_kernel<32, 1, false>, seg0_fused_kernel<32, 1, true>},
+                              {seg0_fused_kernel<32, 8, false>, seg0_fused_kernel<32, 8, true>}}};
+    const Fn fn = fns[a.c0 == 32][P == 8][a.gn ? 1 : 0];
     const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                static_cast<int>(seg0_fused_smem_bytes(a.c0, P)));
     if (e != cudaSuccess) return e;

@@ -1201,8 +1201,15 @@ slim_status run_segment(slim_ctx *ctx, int seg, int ri_prev, int ri, int B, cons
     // segment 0 at a narrow width: stem + both blocks in one kernel, activations in shared memory
     // (kernels_fused.cu; bit-identical to the per-layer kernels below).  SLIM_NO_FUSED=1: per-layer path.
     static const bool no_fused = getenv("SLIM_NO_FUSED") != nullptr;
-    if (seg == 0 && bf && !gn && !no_fused && (C == 16 || C == 32) && C == slim_channels(r, c.base_channels[0]) &&
-        H == 32 && c.in_channels == 3 && c.blocks_per_seg[0] == 2 && S.L[1].sh.cin % 8 == 0) {
+    // GroupNorm: fused too (two-pass statistics in the kernel), but only while the width has the GPU to
+    // itself -- under SM partitioning the two-pass kernel holds its SMs long enough to slow the concurrent
+    // step (GN CFG2 668 k vs 707 k images/s, tools/gpu_runs/r02_gnfused.sh)
+    static const bool no_fused_gn = getenv("SLIM_NO_FUSED_GN") != nullptr;
+    const bool seg0_partitioned = grid_cap(ctx, ri, ctx->num_sms, 0) < ctx->num_sms;
+    if (seg == 0 && bf && (!gn || (!no_fused_gn && c.gn_group_channels == 16 && !seg0_partitioned)) && !no_fused &&
+        (C == 16 || C == 32) &&
+        C == slim_channels(r, c.base_channels[0]) && H == 32 && c.in_channels == 3 && c.blocks_per_seg[0] == 2 &&
+        S.L[1].sh.cin % 8 == 0) {
         FusedSeg0Args fa{};
         fa.in = static_cast<const uint16_t *>(in);
         fa.out = static_cast<uint16_t *>(out);
@@ -1212,9 +1219,11 @@ slim_status run_segment(slim_ctx *ctx, int seg, int ri_prev, int ri, int B, cons
         for (int l = 0; l < 4; ++l) fa.w[l] = static_cast<const uint16_t *>(S.L[1 + l].w);
         fa.stem_b = S.L[0].stem_b;
         fa.trace = ctx->trace ? ctx->trace + 8192 : nullptr;
+        fa.gn = gn ? 1 : 0;   // GroupNorm: the kernel's two-pass statistics; scale/shift carry gamma/beta
+        fa.eps = c.bn_eps;
         for (int l = 0; l < 5; ++l) {
-            fa.scale[l] = S.L[l].scale[ri];
-            fa.shift[l] = S.L[l].shift[ri];
+            fa.scale[l] = gn ? S.L[l].gn_gamma[ri] : S.L[l].scale[ri];
+            fa.shift[l] = gn ? S.L[l].gn_beta[ri] : S.L[l].shift[ri];
         }
         const double pix = static_cast<double>(B) * H * H;
         const double flops = 2.0 * pix * C * 9 * (c.in_channels + 4.0 * C);

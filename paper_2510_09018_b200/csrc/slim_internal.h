@@ -160,6 +160,8 @@ struct FusedSeg0Args {
     const float *scale[5], *shift[5];   // folded BN of stem + four convs at this width, c0 entries
     unsigned long long *trace;     // diagnostics only (SLIM_CONV_TRACE): CTA 0 phase %globaltimer stamps
     int cluster;                   // CTAs per image: 1 (whole image per CTA) or 8 (one 4-row tile each, DSMEM halo)
+    int gn;                        // GroupNorm (16-channel groups): scale / shift carry gamma / beta
+    float eps;
 };
 size_t seg0_fused_smem_bytes(int c0, int P);
 

@@ -178,3 +178,36 @@ def test_gn_statistics_partials_path_parity():
                          text=True, timeout=600, cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     assert out.returncode == 0, out.stderr[-2000:]
     assert float(out.stdout.strip().splitlines()[-1]) <= 2e-2
+
+
+def test_fused_segment0_gn_parity_and_cluster_bitwise():
+    """GroupNorm inside the fused segment-0 kernel (two-pass statistics over the fp32 raw output, one
+    fixed merge tree): within tolerance of the oracle for r = 0.25 / 0.5, and the 8-CTA cluster variant
+    (small batches) bit-identical to the one-CTA-per-image variant."""
+    import os, subprocess, sys, tempfile
+    code = (
+        "import sys, numpy as np, torch, synth, paper_2510_09018_b200 as slim\n"
+        "w, bn = synth.make_weights(), synth.make_bn()\n"
+        "net = slim.SlimNet(w, bn, max_batch=16, norm='gn')\n"
+        "x = torch.from_numpy(synth.make_images(9, offset=71)).to(torch.bfloat16).cuda()\n"
+        "o = [net.forward(0, x, r, r).view(torch.int16).cpu().numpy() for r in (0.25, 0.5)]\n"
+        "np.savez(sys.argv[1], o0=o[0], o1=o[1])\n"
+    )
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    with tempfile.TemporaryDirectory() as d:
+        res = {}
+        for name, cl in (("p8", "8"), ("p1", "0")):
+            out = subprocess.run([sys.executable, "-c", code, os.path.join(d, name + ".npz")],
+                                 env=dict(os.environ, SLIM_SEG0_CLUSTER=cl), capture_output=True, text=True,
+                                 timeout=300, cwd=root)
+            assert out.returncode == 0, out.stderr[-2000:]
+            res[name] = np.load(os.path.join(d, name + ".npz"))
+        for k in ("o0", "o1"):
+            assert np.array_equal(res["p8"][k], res["p1"][k]), k
+    w, bn = synth.make_weights(), synth.make_bn()
+    ref = oracle.Model(w, bn, norm="gn")
+    x = synth.make_images(9, offset=71)
+    for k, r in (("o0", 0.25), ("o1", 0.5)):
+        got = (res["p8"][k].astype(np.int32).astype(np.uint32) << 16).view(np.float32)
+        err = oracle.per_image_rel_err(got[:3], ref.segment(0, x[:3], None, r))
+        assert err.max() <= 2e-2, (r, err.max())
