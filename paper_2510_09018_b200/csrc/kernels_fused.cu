@@ -606,13 +606,13 @@ struct FnGeom {
     uint32_t plane_odd, plane_even;       // one parity plane (all input chunks)
     uint32_t act;                         // T or X (all C channels)
     uint32_t slot, n_slots;
-    uint32_t planes, t, x, ring, bn, bars, total;
+    uint32_t planes, t, x, ring, bn, bars, gn, total;
 };
 __host__ __device__ inline uint32_t fn_al(uint32_t v) { return (v + 1023u) & ~1023u; }
 __host__ __device__ inline int fn_ck(int c) { return c <= 16 ? 16 : (c <= 32 ? 32 : 64); }
 // smem layout for full width C, R = C/P rows per CTA, input width CI; the weight ring takes what the
 // budget leaves (up to 6 slots)
-__host__ __device__ inline FnGeom fn_layout(int C, int R, int CI, int H, int G, uint32_t budget) {
+__host__ __device__ inline FnGeom fn_layout(int C, int R, int CI, int H, int G, uint32_t budget, bool gn = false) {
     FnGeom g;
     g.rb_i = 2u * fn_ck(CI);
     g.nch_i = (CI + 63) / 64;
@@ -628,17 +628,19 @@ __host__ __device__ inline FnGeom fn_layout(int C, int R, int CI, int H, int G, 
     g.t = g.planes + 2 * g.plane_odd + 2 * g.plane_even;
     g.x = g.t + g.act;
     g.ring = g.x + g.act;
-    const uint32_t tail = 5u * 2u * C * 4u + 64u * 8u + 16u;   // BN vectors, barriers, tmem slot
+    const uint32_t gnb = gn ? 6144u : 0u;                      // GroupNorm partials + per-image coefficients
+    const uint32_t tail = 5u * 2u * C * 4u + 64u * 8u + 16u + gnb;   // BN / GN vectors, barriers, tmem slot
     uint32_t ns = 0;
     while (ns < 6 && g.ring + (ns + 1) * g.slot + tail <= budget) ++ns;
     g.n_slots = ns;
     g.bn = g.ring + ns * g.slot;
     g.bars = g.bn + 5u * 2u * C * 4u;
-    g.total = g.bars + 64u * 8u + 16u;
+    g.gn = g.bars + 64u * 8u + 16u;
+    g.total = g.gn + gnb;
     return g;
 }
 
-template <int C, int H, int G, int P>
+template <int C, int H, int G, int P, bool GN>
 __global__ void __launch_bounds__(kFnThreads, 1) segn_fused_kernel(const FusedSegArgs a) {
     constexpr int W = H, RP = G * W, NPIX = G * H * W, NT = NPIX / 128, TR = 128 / RP;
     constexpr int R = C / P;                                 // output channels of this CTA
@@ -647,7 +649,7 @@ __global__ void __launch_bounds__(kFnThreads, 1) segn_fused_kernel(const FusedSe
     constexpr int SC = 4 * R;                                // TMEM columns per tile stage: 3 kw accs + projection
     static_assert(NT * SC <= 512, "TMEM");
     const int CI = a.CI;
-    const FnGeom Gm = fn_layout(C, R, CI, H, G, a.smem_budget);
+    const FnGeom Gm = fn_layout(C, R, CI, H, G, a.smem_budget, GN);
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     const uint32_t s0 = smem_u32(smem);
@@ -927,9 +929,79 @@ __global__ void __launch_bounds__(kFnThreads, 1) segn_fused_kernel(const FusedSe
                     const bool pool = a.pool_out != nullptr && l == 4;
                     // L4 pool partials: the even-row planes (dead after L2's projection; no zero rows to keep)
                     float *stage = reinterpret_cast<float *>(smem + Gm.planes);
+                    // GroupNorm: pass 1 the statistics per (image of the unit, 16-channel group) of the fp32 raw
+                    // outputs (u; and the projection p at L2) -- per thread (mean, M2) of 16 values, merged with
+                    // equal counts over the lanes of the same image, then over (tile, lane quarter) in a fixed
+                    // tree -- pass 2 the normalisation with per-(image, channel) coefficients.  The accumulators
+                    // stay in TMEM between the passes (a unit's tiles never share a stage).
+                    constexpr int SLOTS = RP / W;                                   // images per warp row
+                    const float leaf_cnt = 16.f * 32.f * W / RP;
+                    float2 *gPart = reinterpret_cast<float2 *>(smem + Gm.gn);      // [which][t][q][gi][slot]
+                    float *gCoef = reinterpret_cast<float *>(gPart + 2 * NT * 4 * NG * SLOTS);   // [which][A|B][n][cl]
+                    auto gpart = [&](int which, int t, int qq, int gi_, int slot) -> float2 & {
+                        return gPart[(((which * NT + t) * 4 + qq) * NG + gi_) * SLOTS + slot];
+                    };
+                    auto stats16 = [&](const float (&y)[16], int which, int t, int gi_) {
+                        float mu = 0.f;
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) mu += y[i];
+                        mu *= (1.f / 16.f);
+                        float m2 = 0.f;
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) m2 = fmaf(y[i] - mu, y[i] - mu, m2);
+                        float cnt = 16.f;
+                        for (int ofs = 1; ofs < 32; ofs <<= 1) {
+                            if (ofs >= W && ofs < RP) continue;   // would mix images
+                            const float mo = __shfl_xor_sync(0xffffffffu, mu, ofs), qo = __shfl_xor_sync(0xffffffffu, m2, ofs);
+                            const float d = mo - mu;
+                            m2 = (m2 + qo) + d * d * (cnt * 0.5f);
+                            mu = (mu + mo) * 0.5f;
+                            cnt *= 2.f;
+                        }
+                        if (lane < RP && lane % W == 0) gpart(which, t, q, gi_, lane / W) = make_float2(mu, m2);
+                    };
+                    for (int pass = GN ? 1 : 2; pass <= 2; ++pass) {
+                    if (GN && pass == 2) {   // pass-1 partials -> per (image, channel) coefficients
+                        named_bar_sync(2, kFnEpiWarps * 32);
+                        const int nwhich = l == 2 ? 2 : 1;
+                        for (int idx = tid; idx < nwhich * G * NG; idx += kFnEpiWarps * 32) {
+                            const int which = idx / (G * NG), n = (idx / NG) % G, gi_ = idx % NG;
+                            float2 lv[2 * NT];
+                            float c = leaf_cnt;
+#pragma unroll
+                            for (int t = 0; t < NT; ++t) {   // quarters pairwise, then the tiles
+                                const float2 a0 = gpart(which, t, 0, gi_, n), a1 = gpart(which, t, 1, gi_, n);
+                                const float2 a2 = gpart(which, t, 2, gi_, n), a3 = gpart(which, t, 3, gi_, n);
+                                auto mg = [](float2 x, float2 y, float cc) {
+                                    const float d = y.x - x.x;
+                                    return make_float2((x.x + y.x) * 0.5f, (x.y + y.y) + d * d * (cc * 0.5f));
+                                };
+                                lv[t] = mg(mg(a0, a1, c), mg(a2, a3, c), 2.f * c);
+                            }
+                            float2 tot = lv[0];
+                            float cc = 4.f * c;
+                            for (int t = 1; t < NT; ++t) {   // NT <= 2
+                                const float d = lv[t].x - tot.x;
+                                tot = make_float2((tot.x + lv[t].x) * 0.5f, (tot.y + lv[t].y) + d * d * (cc * 0.5f));
+                                cc *= 2.f;
+                            }
+                            const float rstd = rsqrtf(fmaxf(tot.y / cc, 0.f) + a.eps);
+                            const int bl = which ? 2 : bn_l;   // gamma / beta slots (projection: slot 2)
+                            for (int i = 0; i < 16; ++i) {
+                                const int cl = gi_ * 16 + i, cgl = static_cast<int>(rank) * R + cl;
+                                const float A = rstd * sBN[bl * 2 * C + cgl];
+                                gCoef[((which * 2 + 0) * G + n) * R + cl] = A;
+                                gCoef[((which * 2 + 1) * G + n) * R + cl] = fmaf(-tot.x, A, sBN[bl * 2 * C + C + cgl]);
+                            }
+                        }
+                        named_bar_sync(2, kFnEpiWarps * 32);
+                    }
                     for (int it = sub; it < NT * NG; it += 4) {
                         const int t = it / NG, gi = it % NG;
-                        mbar_wait(t_full(t), layers_done & 1);
+                        if (pass == 2 || !GN) {   // (pass 1 already waited for this layer's accumulators)
+                            if (!GN) mbar_wait(t_full(t), layers_done & 1);
+                        }
+                        if (GN && pass == 1) mbar_wait(t_full(t), layers_done & 1);
                         tc_fence_after();
                         const int hr = t * TR + m / RP, pix = m % RP, n = pix / W;   // output row, image in unit
                         const int cg = static_cast<int>(rank) * R + gi * 16;         // first global channel
@@ -943,12 +1015,47 @@ __global__ void __launch_bounds__(kFnThreads, 1) segn_fused_kernel(const FusedSe
                         reg_fence16(v1);
                         reg_fence16(v2);
                         float f[16];
+                        // normalisation coefficients: BN per channel, or GN per (image, channel) (pass 2)
+                        const float *ca = GN ? gCoef + (0 * G + n) * R + gi * 16 - cg : sc;
+                        const float *cb = GN ? gCoef + (1 * G + n) * R + gi * 16 - cg : sh;
+                        if (GN && pass == 1) {   // raw outputs -> statistics
+                            if (l == 1) {
+#pragma unroll
+                                for (int i = 0; i < 16; ++i) {
+                                    const float left = __shfl_up_sync(0xffffffffu, __uint_as_float(v0[i]), 1);
+                                    f[i] = fmaf(mL, left, __uint_as_float(v1[i]) + __uint_as_float(v2[i]));
+                                }
+                            } else {
+                                const unsigned long long mL2 = f2pk(mL, mL), mR2 = f2pk(mR, mR);
+#pragma unroll
+                                for (int i = 0; i < 16; i += 2) {
+                                    const float l0 = __shfl_up_sync(0xffffffffu, __uint_as_float(v0[i]), 1);
+                                    const float l1 = __shfl_up_sync(0xffffffffu, __uint_as_float(v0[i + 1]), 1);
+                                    const float r0 = __shfl_down_sync(0xffffffffu, __uint_as_float(v2[i]), 1);
+                                    const float r1 = __shfl_down_sync(0xffffffffu, __uint_as_float(v2[i + 1]), 1);
+                                    f2upk(ffma2(mR2, f2pk(r0, r1),
+                                                ffma2(mL2, f2pk(l0, l1),
+                                                      f2pk(__uint_as_float(v1[i]), __uint_as_float(v1[i + 1])))),
+                                          f[i], f[i + 1]);
+                                }
+                            }
+                            stats16(f, 0, t, gi);
+                            if (l == 2) {   // the projection's raw output
+                                tmem_ld16(col + 3 * R, v0);
+                                tmem_wait_ld();
+                                reg_fence16(v0);
+#pragma unroll
+                                for (int i = 0; i < 16; ++i) f[i] = __uint_as_float(v0[i]);
+                                stats16(f, 1, t, gi);
+                            }
+                            continue;
+                        }
                         if (l == 1) {   // acc [kw0 | kw2 | kw1]: kw0[w-1] + kw2[w] + kw1[w] (scalar, as the halo kernel)
 #pragma unroll
                             for (int i = 0; i < 16; ++i) {
                                 const float left = __shfl_up_sync(0xffffffffu, __uint_as_float(v0[i]), 1);
                                 const float y = fmaf(mL, left, __uint_as_float(v1[i]) + __uint_as_float(v2[i]));
-                                f[i] = fmaf(y, sc[cg + i], sh[cg + i]);
+                                f[i] = fmaf(y, ca[cg + i], cb[cg + i]);
                             }
                         } else {
                             const unsigned long long mL2 = f2pk(mL, mL), mR2 = f2pk(mR, mR);
@@ -962,10 +1069,12 @@ __global__ void __launch_bounds__(kFnThreads, 1) segn_fused_kernel(const FusedSe
                                     mR2, f2pk(r0, r1),
                                     ffma2(mL2, f2pk(l0, l1), f2pk(__uint_as_float(v1[i]), __uint_as_float(v1[i + 1]))));
                                 const int c = cg + i;
-                                f2upk(ffma2(y, f2pk(sc[c], sc[c + 1]), f2pk(sh[c], sh[c + 1])), f[i], f[i + 1]);
+                                f2upk(ffma2(y, f2pk(ca[c], ca[c + 1]), f2pk(cb[c], cb[c + 1])), f[i], f[i + 1]);
                             }
                         }
-                        if (l == 2) {   // + s_sc * proj + t_sc
+                        if (l == 2) {   // + s_sc * proj + t_sc (GN: the projection's own GN)
+                            const float *pa = GN ? gCoef + (2 * G + n) * R + gi * 16 - cg : sc1;
+                            const float *pb = GN ? gCoef + (3 * G + n) * R + gi * 16 - cg : sh1;
                             tmem_ld16(col + 3 * R, v0);
                             tmem_wait_ld();
                             reg_fence16(v0);
@@ -974,7 +1083,7 @@ __global__ void __launch_bounds__(kFnThreads, 1) segn_fused_kernel(const FusedSe
                                 const int c = cg + i;
                                 const unsigned long long pr =
                                     ffma2(f2pk(__uint_as_float(v0[i]), __uint_as_float(v0[i + 1])),
-                                          f2pk(sc1[c], sc1[c + 1]), f2pk(sh1[c], sh1[c + 1]));
+                                          f2pk(pa[c], pa[c + 1]), f2pk(pb[c], pb[c + 1]));
                                 f2upk(fadd2(f2pk(f[i], f[i + 1]), pr), f[i], f[i + 1]);
                             }
                         }
@@ -1032,6 +1141,7 @@ __global__ void __launch_bounds__(kFnThreads, 1) segn_fused_kernel(const FusedSe
                             }
                         }
                     }
+                    }   // passes
                     if (P > 1)
                         fence_proxy_async_cluster();
                     else
@@ -1088,14 +1198,14 @@ int segn_fused_cluster(int seg, int C) {
 }
 
 // smem the fused segment-s kernel needs for (C, CI) at segment s (0 if unsupported); >= 2 ring slots
-size_t segn_fused_smem_bytes(int seg, int C, int CI) {
+size_t segn_fused_smem_bytes(int seg, int C, int CI, bool gn) {
     if (!(seg >= 1 && seg <= 3) || (C != 32 && C != 64 && C != 128) || CI % 16 != 0 || CI > 128) return 0;
     if (seg == 1 && C == 128) return 0;
     int H, G;
     fn_geom_seg(seg, &H, &G);
     const int P = segn_fused_cluster(seg, C), R = C / P;
     if (G * H * H / 128 * 4 * R > 512) return 0;
-    const FnGeom g = fn_layout(C, R, CI, H, G, 227u * 1024u - 1024u);
+    const FnGeom g = fn_layout(C, R, CI, H, G, 227u * 1024u - 1024u, gn);
     if (g.n_slots < 2) return 0;
     return 1024 + g.total;
 }
@@ -1114,14 +1224,18 @@ size_t segn_fused_image_bytes(int seg, int C, int CI) {
 cudaError_t launch_segn_fused(const FusedSegArgs &a, int seg, int C, int units_grid, cudaStream_t stream, bool pdl) {
     using Fn = void (*)(FusedSegArgs);
     Fn fn = nullptr;
-    if (seg == 1 && C == 32) fn = segn_fused_kernel<32, 16, 1, 1>;
-    if (seg == 1 && C == 64) fn = segn_fused_kernel<64, 16, 1, 1>;
-    if (seg == 2 && C == 64) fn = segn_fused_kernel<64, 8, 2, 1>;
-    if (seg == 2 && C == 128) fn = segn_fused_kernel<128, 8, 2, 2>;
-    if (seg == 3 && C == 64) fn = segn_fused_kernel<64, 4, 8, 2>;
-    if (seg == 3 && C == 128) fn = segn_fused_kernel<128, 4, 8, 4>;
+    const bool gn = a.gn != 0;
+#define SEGN_PICK(S_, C_, H_, G_, P_) \
+    if (seg == S_ && C == C_) fn = gn ? segn_fused_kernel<C_, H_, G_, P_, true> : segn_fused_kernel<C_, H_, G_, P_, false>;
+    SEGN_PICK(1, 32, 16, 1, 1)
+    SEGN_PICK(1, 64, 16, 1, 1)
+    SEGN_PICK(2, 64, 8, 2, 1)
+    SEGN_PICK(2, 128, 8, 2, 2)
+    SEGN_PICK(3, 64, 4, 8, 2)
+    SEGN_PICK(3, 128, 4, 8, 4)
+#undef SEGN_PICK
     if (!fn) return cudaErrorInvalidValue;
-    const size_t smem = segn_fused_smem_bytes(seg, C, a.CI);
+    const size_t smem = segn_fused_smem_bytes(seg, C, a.CI, gn);
     if (!smem) return cudaErrorInvalidValue;
     const int P = segn_fused_cluster(seg, C);
     FusedSegArgs args = a;

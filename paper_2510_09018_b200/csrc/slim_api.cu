@@ -1262,7 +1262,8 @@ slim_status run_segment(slim_ctx *ctx, int seg, int ri_prev, int ri, int B, cons
     static const int fused_part = getenv("SLIM_FUSED_PART") ? atoi(getenv("SLIM_FUSED_PART")) : 0;
     const bool partitioned = grid_cap(ctx, ri, ctx->num_sms, seg) < ctx->num_sms;
     const bool fused_on = ((fused_env >> seg) & 1) != 0 && !(partitioned && fused_part == 0);
-    if (seg > 0 && bf && !gn && !no_fused && fused_on && S.fimg[ri_prev][ri]) {
+    // GroupNorm: the kernel's two-pass statistics (per image and 16-channel group), same condition
+    if (seg > 0 && bf && (!gn || !no_fused_gn) && !no_fused && fused_on && S.fimg[ri_prev][ri]) {
         FusedSegArgs fa{};
         fa.in = static_cast<const uint16_t *>(in);
         fa.B = B;
@@ -1274,9 +1275,11 @@ slim_status run_segment(slim_ctx *ctx, int seg, int ri_prev, int ri, int B, cons
         if (last) pooled = reinterpret_cast<float *>(bufs[0]);   // fp32 [B][C] for the FC
         else fa.out = static_cast<uint16_t *>(out);
         fa.pool_out = pooled;
+        fa.gn = gn ? 1 : 0;
+        fa.eps = c.bn_eps;
         for (int l = 0; l < 5; ++l) {
-            fa.scale[l] = S.L[l].scale[ri];
-            fa.shift[l] = S.L[l].shift[ri];
+            fa.scale[l] = gn ? S.L[l].gn_gamma[ri] : S.L[l].scale[ri];
+            fa.shift[l] = gn ? S.L[l].gn_beta[ri] : S.L[l].shift[ri];
         }
         const int G = seg == 1 ? 1 : (seg == 2 ? 2 : 8);
         const double pix = static_cast<double>(B) * H * H;
@@ -1777,13 +1780,14 @@ slim_status slim_load_segment(slim_ctx *ctx, int seg, const slim_seg_weights *w,
     }
     // fused-segment weight images (segments 1-3, narrow widths; kernels_fused.cu) for every (r_prev, r)
     // pair the fused kernel supports: built once here, so no first-use repack lands inside a graph capture
-    if (seg > 0 && c.dtype == SLIM_BF16 && c.norm == SLIM_NORM_BN && c.blocks_per_seg[seg] == 2) {
+    if (seg > 0 && c.dtype == SLIM_BF16 && c.blocks_per_seg[seg] == 2 &&
+        (c.norm == SLIM_NORM_BN || c.gn_group_channels == 16)) {
         for (int ri = 0; ri < c.n_widths; ++ri) {
             const int C = slim_channels(c.widths[ri], c.base_channels[seg]);
             if (C != slim_act_channels(c.widths[ri], c.base_channels[seg])) continue;
             for (int rp = 0; rp < c.n_widths; ++rp) {
                 const int CI = slim_act_channels(c.widths[rp], c.base_channels[seg - 1]);
-                if (!segn_fused_smem_bytes(seg, C, CI)) continue;
+                if (!segn_fused_smem_bytes(seg, C, CI, c.norm == SLIM_NORM_GN)) continue;
                 const size_t nb = segn_fused_image_bytes(seg, C, CI);
                 CUDA_TRY(ctx, cudaMalloc(&S.fimg[rp][ri], nb));
                 CUDA_TRY(ctx, cudaMemset(S.fimg[rp][ri], 0, nb));

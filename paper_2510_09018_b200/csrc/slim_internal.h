@@ -176,10 +176,12 @@ struct FusedSegArgs {
     const float *scale[5], *shift[5];   // folded BN: b0c1, b0c2, projection, b1c1, b1c2 (C entries)
     uint32_t smem_budget;          // dynamic smem the launch reserved (the ring takes what is left)
     size_t wimg_rank_bytes;        // one cluster rank's part of the image (set by launch_segn_fused)
+    int gn;                        // GroupNorm (16-channel groups): scale / shift carry gamma / beta
+    float eps;
     unsigned long long *trace;     // diagnostics only (SLIM_CONV_TRACE): CTA 0 phase %globaltimer stamps
 };
 int segn_fused_cluster(int seg, int C);                 // CTAs per unit (output channels split over them)
-size_t segn_fused_smem_bytes(int seg, int C, int CI);   // 0 = unsupported / does not fit
+size_t segn_fused_smem_bytes(int seg, int C, int CI, bool gn = false);   // 0 = unsupported / does not fit
 size_t segn_fused_image_bytes(int seg, int C, int CI);
 cudaError_t build_segn_fused_image(void *img, const void *w0, const void *w1, const void *wp, const void *w3,
                                    const void *w4, int seg, int C, int CI, int cin0_full, int cf_full, cudaStream_t st);

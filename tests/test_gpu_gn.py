@@ -211,3 +211,29 @@ def test_fused_segment0_gn_parity_and_cluster_bitwise():
         got = (res["p8"][k].astype(np.int32).astype(np.uint32) << 16).view(np.float32)
         err = oracle.per_image_rel_err(got[:3], ref.segment(0, x[:3], None, r))
         assert err.max() <= 2e-2, (r, err.max())
+
+
+@pytest.mark.parametrize("seg", [1, 2, 3])
+def test_fused_segments_gn_parity(seg):
+    """GroupNorm inside the fused segment-1..3 kernels (statistics per image of the unit, channel slices over
+    the cluster): every (r_prev, r) the fused kernel takes against the oracle, ragged unit counts, and
+    bitwise batch independence (an image's statistics never depend on its slot in the unit)."""
+    w, bn = synth.make_weights(), synth.make_bn()
+    net = slim.SlimNet(w, bn, max_batch=16, norm="gn")
+    ref = oracle.Model(w, bn, norm="gn")
+    H = 32 >> (seg - 1)
+    worst = 0.0
+    for rp in synth.WIDTHS:
+        C = synth.active_channels(rp, synth.BASE_CHANNELS[seg - 1])
+        g = np.random.default_rng(900 + seg)
+        x = synth.round_bf16(np.abs(g.standard_normal((11, H, H, C), dtype=np.float32)))
+        xd = torch.from_numpy(x).to(torch.bfloat16).cuda()
+        for r in (0.25, 0.5):
+            got = net.forward(seg, xd, rp, r)
+            sub = net.forward(seg, xd[3:6].contiguous(), rp, r)
+            assert torch.equal(got[3:6], sub), (rp, r)
+            gotn = got.float().cpu().numpy()
+            err = oracle.per_image_rel_err(gotn[[0, 4, 10]], ref.segment(seg, x[[0, 4, 10]], rp, r))
+            worst = max(worst, float(err.max()))
+    net.close()
+    assert worst <= 2e-2, worst
