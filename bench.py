@@ -245,19 +245,31 @@ class Cfg2Step:
             self.slim.slim_set_sm_share(self.net.ctx, r, sh[r])
 
 
+_BACKEND = {"name": "nccl"}
+
+
+def _coll_dev(dev):
+    """Device of tensors handed to collectives: the GPU for NCCL, the host for gloo."""
+    return dev if _BACKEND["name"] == "nccl" else "cpu"
+
+
 def _init_nccl(dev):
-    """NCCL process group over NVLink, one rank per GPU; returns a record proving the communicator
+    """Process group (NCCL over NVLink, one rank per GPU; `--dist-backend gloo` is the functional check
+    for several ranks sharing a GPU -- NCCL refuses that); returns a record proving the communicator
     spans every rank (an all-reduce of ones == world size)."""
     import torch
     import torch.distributed as dist
-    dist.init_process_group("nccl", device_id=dev)
-    one = torch.ones(1, device=dev)
+    if _BACKEND["name"] == "nccl":
+        dist.init_process_group("nccl", device_id=dev)
+    else:
+        dist.init_process_group("gloo")
+    one = torch.ones(1, device=_coll_dev(dev))
     dist.all_reduce(one)
     torch.cuda.synchronize(dev)
     rec = {"backend": dist.get_backend(), "world": dist.get_world_size(), "rank": dist.get_rank(),
            "allreduce_ones": int(one.item()), "nccl_version": ".".join(map(str, torch.cuda.nccl.version()))}
     rec["comm_nranks_ok"] = rec["allreduce_ones"] == rec["world"]
-    print(f"[rank {rec['rank']}] NCCL communicator up: {rec}", file=sys.stderr, flush=True)
+    print(f"[rank {rec['rank']}] process group up: {rec}", file=sys.stderr, flush=True)
     return rec
 
 
@@ -273,6 +285,7 @@ def run_ours(args):
 
     world, rank, local = _dist()
     assert torch.cuda.is_available(), "bench.py (ours) needs a GPU; the oracle arm is --impl reference"
+    local = local % torch.cuda.device_count()   # (gloo functional check: several ranks on one GPU)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     nccl = _init_nccl(dev) if world > 1 else None
@@ -284,7 +297,7 @@ def run_ours(args):
     chain, step, shares, set_shares = cfg2.chain, cfg2.step, cfg2.shares, cfg2.set_shares
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
     sampler = NvmlSampler(local)
-    telem = TelemetryExchange(device=dev) if world > 1 else None
+    telem = TelemetryExchange(device=_coll_dev(dev)) if world > 1 else None
     tsrc = TelemetrySource(sampler, rank)
     imgs_per_step = B * len(WIDTHS)
     last_ms = [0.0]
@@ -335,7 +348,7 @@ def run_ours(args):
     launches = slim.slim_launch_count(net.ctx) - launches0
     step_ms = [a.elapsed_time(b) for a, b in ev]
     total_ms = sum(step_ms)
-    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    t = torch.tensor([total_ms], dtype=torch.float64, device=_coll_dev(dev))
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_max_ms = float(t.item())
@@ -511,7 +524,7 @@ def run_ours(args):
         streams[r].synchronize()
         cstreams[r].synchronize()
     e2e_s = time.perf_counter() - t0
-    te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+    te = torch.tensor([e2e_s], dtype=torch.float64, device=_coll_dev(dev))
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_val = world * imgs_per_step * KE / float(te.item())
@@ -586,6 +599,7 @@ def run_stream(args):
     from paper_2510_09018_b200.telemetry import NvmlSampler, TelemetryExchange, TelemetrySource
 
     world, rank, local = _dist()
+    local = local % torch.cuda.device_count()   # (gloo functional check: several ranks on one GPU)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     nccl = _init_nccl(dev) if world > 1 else None
@@ -642,7 +656,7 @@ def run_stream(args):
             for r, sh in sm_shares(cw, args.sm_share).items():
                 slim.slim_set_sm_share(net.ctx, r, sh)
     sampler = NvmlSampler(local)
-    telem = TelemetryExchange(device=dev) if world > 1 else None
+    telem = TelemetryExchange(device=_coll_dev(dev)) if world > 1 else None
     tsrc = TelemetrySource(sampler, rank)
     stream = torch.cuda.current_stream(dev)
     LAG = 2
@@ -693,7 +707,7 @@ def run_stream(args):
     if world > 1:
         dist.barrier()
     ms = a.elapsed_time(b)
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    t = torch.tensor([ms], dtype=torch.float64, device=_coll_dev(dev))
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     value = n_total * args.steps / (float(t.item()) / 1e3)
@@ -823,6 +837,7 @@ def run_handoff(args):
     from paper_2510_09018_b200.telemetry import NvmlSampler
 
     world, rank, local = _dist()
+    local = local % torch.cuda.device_count()   # (gloo functional check: several ranks on one GPU)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
@@ -859,7 +874,7 @@ def run_handoff(args):
         dist.barrier()
     sampler.stop()
     e1 = sampler.energy_mj()
-    t = torch.tensor([a.elapsed_time(b)], dtype=torch.float64, device=dev)
+    t = torch.tensor([a.elapsed_time(b)], dtype=torch.float64, device=_coll_dev(dev))
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     value = n * args.steps / (float(t.item()) / 1e3)
@@ -1003,6 +1018,9 @@ def _ncu_tensor_pipe():
 def build_parser():
     ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
     ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--dist-backend", choices=("nccl", "gloo"), default="nccl",
+                    help="N > 1: nccl (one rank per GPU); gloo = functional check of the multi-rank path with "
+                         "several ranks sharing a GPU (not a scaling measurement)")
     ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
@@ -1099,6 +1117,7 @@ def main(argv=None):
     ap = build_parser()
     raw = list(sys.argv[1:] if argv is None else argv)
     args = ap.parse_args(raw)
+    _BACKEND["name"] = args.dist_backend
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         # `bench.py --gpus N` run directly: re-execute under torchrun with N ranks (the driver launches
         # N>1 through torchrun itself, which sets WORLD_SIZE and lands in the branch below)
