@@ -998,10 +998,8 @@ __global__ void __launch_bounds__(kFnThreads, 1) segn_fused_kernel(const FusedSe
                     }
                     for (int it = sub; it < NT * NG; it += 4) {
                         const int t = it / NG, gi = it % NG;
-                        if (pass == 2 || !GN) {   // (pass 1 already waited for this layer's accumulators)
-                            if (!GN) mbar_wait(t_full(t), layers_done & 1);
-                        }
-                        if (GN && pass == 1) mbar_wait(t_full(t), layers_done & 1);
+                        // (GN pass 2 reads the accumulators pass 1 already waited for)
+                        if (!GN || pass == 1) mbar_wait(t_full(t), layers_done & 1);
                         tc_fence_after();
                         const int hr = t * TR + m / RP, pix = m % RP, n = pix / W;   // output row, image in unit
                         const int cg = static_cast<int>(rank) * R + gi * 16;         // first global channel
