@@ -595,7 +595,7 @@ def run_stream(args):
     import paper_2510_09018_b200 as slim
     from paper_2510_09018_b200 import build as slim_build
     from paper_2510_09018_b200 import router
-    from paper_2510_09018_b200.stream import StreamExecutor
+    from paper_2510_09018_b200.stream import NativeStreamExecutor, StreamExecutor
     from paper_2510_09018_b200.telemetry import NvmlSampler, TelemetryExchange, TelemetrySource
 
     world, rank, local = _dist()
@@ -647,8 +647,13 @@ def run_stream(args):
                 return out
         ex = _Adapter()
     else:
-        ex = StreamExecutor(net, n_max=n_max, B_max=args.bmax, device=dev, lanes=args.lanes)
-        ex.cache_plans = args.repeat_stream
+        if args.lanes is None:   # the Python sequencer is host-bound on a fresh stream: extra lanes cost host time
+            args.lanes = 1 if (args.stream_impl == "python" and not args.repeat_stream) else 8
+        if args.stream_impl == "native":   # pack + enqueue in libslim (slim_stream_run)
+            ex = NativeStreamExecutor(net, n_max=n_max, B_max=args.bmax, device=dev, lanes=args.lanes)
+        else:
+            ex = StreamExecutor(net, n_max=n_max, B_max=args.bmax, device=dev, lanes=args.lanes)
+            ex.cache_plans = args.repeat_stream
         # one lane per width: partition the SMs by width as in cfg2 -- unless the policy routes a
         # single width (the "slim" policy keeps every SM for its one lane)
         if args.lanes > 1 and args.policy != "slim":
@@ -699,9 +704,16 @@ def run_stream(args):
     a.record(stream)
     mine_total = 0
     batches = []
+    n_batches = 0
+    host_s = []
     for k in range(args.steps):
         mine_total += one_step(args.warmup + k)
-        batches += [bb for seg in ex.last_batches for bb in seg]
+        if isinstance(ex, NativeStreamExecutor):
+            n_batches += ex.last_n_batches
+            host_s.append(ex.host_s[-1])
+        else:
+            batches += [bb for seg in ex.last_batches for bb in seg]
+            n_batches += sum(len(seg) for seg in ex.last_batches)
     b.record(stream)
     torch.cuda.synchronize()
     if world > 1:
@@ -728,7 +740,7 @@ def run_stream(args):
     e1 = sampler.energy_mj()
     clocks, energy = _clock_energy_json(sampler, e0, e1, max(n_e, 1)) if n_e else (sampler.summary(), None)
     pack = getattr(ex, "pack_s", [])[n_pack0:]
-    n_desc = len(batches)
+    n_desc = n_batches
     if rank == 0:
         print(json.dumps({
             "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps,
@@ -737,18 +749,19 @@ def run_stream(args):
             "config": {"workload": f"{'CFG5' if world > 1 else 'CFG4'}: mixed-width request stream "
                                    f"(width tuples of Tables I-II), greedy (segment, w_req, w_prev) batching, "
                                    f"B_max={args.bmax}, routing={args.policy}, executor={args.executor}"
-                                   + (f", lanes={args.lanes}" if not (greedy or native) else "")
+                                   + (f", lanes={args.lanes}, sequencer={args.stream_impl}"
+                                      if not (greedy or native) else "")
                                    + (f" (Alg. 1: Q_th={args.q_th}, N_new={args.n_new})" if greedy or native else ""),
                        "requests_per_rank": args.requests, "parallelism": f"dp{world} routed",
                        "stream": "replayed (step 0's routing every step)" if args.repeat_stream else
                                  "fresh routing + packing every step (inside the timed region)",
                        "graphs": graphs},
             "batches_per_step_rank0": n_desc / args.steps,
-            "mean_batch_rank0": (float(mine_total * 4 / max(1, sum(len(s) for s in ex.last_batches) * args.steps))
-                                 if native else float(np.mean(batches)) if batches else None),
+            "mean_batch_rank0": (float(mine_total * 4 / max(1, n_desc)) if n_desc else None),
             "packer_host_us": ({"per_step": 1e6 * float(np.mean(pack)), "per_batch": 1e6 * float(np.sum(pack)) /
                                 max(1, n_desc), "note": "slim_pack on all four segments + marshalling, host"}
                                if pack else None),
+            **({"sequencer_host_us_per_step": 1e6 * float(np.mean(host_s))} if host_s else {}),
             **({"alg1_host_s_per_step": {k: gx.stats[k] / (args.steps + args.warmup)
                                          for k in ("t_next", "t_launch", "t_wait")},
                 "alg1_instances": len(gx.sched.instances())} if greedy else {}),
@@ -850,6 +863,8 @@ def run_handoff(args):
     tuples = np.asarray(router.TABLE_TUPLES, np.float32)[g.integers(0, len(router.TABLE_TUPLES), n)]
     plan = handoff.plan_segments(n, world, args.seg_policy)
     x = torch.from_numpy(synth.make_images(n, offset=300)).to(torch.bfloat16).to(dev)
+    if args.lanes is None:
+        args.lanes = 8
     ex = handoff.HandoffExecutor(net, n, rank, world, B_max=args.bmax, lanes=args.lanes)
     if args.lanes > 1 and len(np.unique(tuples)) > 1:
         for r, sh in sm_shares(tuple(net.cfg.widths[i] for i in range(net.cfg.n_widths)), args.sm_share).items():
@@ -1066,9 +1081,11 @@ def build_parser():
     ap.add_argument("--rate", type=float, default=300_000.0, help="poisson: offered load, requests/s")
     ap.add_argument("--m-max-gb", type=float, default=8.0,
                     help="poisson: Alg. 1 VRAM cap M_max (GB) -- bounds the instances the executor scales up to")
-    ap.add_argument("--lanes", type=int, default=8,
+    ap.add_argument("--lanes", type=int, default=None,
                     help="stream/handoff: concurrent lanes (streams) per segment: one per width, times lanes/widths "
-                         "rotating over a width's batches (4 -> 926 k, 8 -> 1.05-1.08 M images/s)")
+                         "rotating over a width's batches (default 8; 1 for the Python sequencer on a fresh stream)")
+    ap.add_argument("--stream-impl", choices=("native", "python"), default="native",
+                    help="stream executor: native = slim_stream_run (pack + enqueue in libslim); python = stream.py")
     ap.add_argument("--alg1-graphs", action="store_true", help="greedy/native: CUDA-graph replay per batch shape")
     ap.add_argument("--alg1-shares", action="store_true", help="greedy/native: per-width SM shares (--sm-share)")
     ap.add_argument("--q-th", type=int, default=512, help="greedy: Alg. 1 scale trigger Q_th")

@@ -298,6 +298,36 @@ SLIM_API slim_status slim_exec_run(slim_exec *x, const void *images, const float
                                    size_t vram_external, slim_exec_stats *stats, void *stream,
                                    const double *arrival_s, double *done_s);
 
+/* ---- native request-stream executor (CFG4; Alg. 1 l.3-4 + l.10) ----------------
+ * One call runs a whole request stream through the four segments with the key batching of
+ * slim_pack (FIFO head key, up to B_max equal keys, per segment with key (s, w_s, w_{s-1}))
+ * and, per batch, slim_launch (gather + segment kernels) and slim_scatter (outputs -> the
+ * next segment's request pool, or the logits).  All four packings are done on the host
+ * first (they depend only on the tuples); the four request orders go to the device in ONE
+ * H2D copy from a double-buffered pinned staging area.  lanes > 1: the batches of one
+ * segment run on `lanes` streams (lane = width index, plus a rotation over a width's batches
+ * when lanes > widths), forked from and joined back to the caller's stream around each
+ * segment; the per-width SM shares of slim_set_sm_share keep them side by side.
+ * create: allocates the pools for n_max requests and per-lane slab/out/workspace buffers for
+ * B_max rows (SLIM_EINVAL unless 1 <= B_max <= cfg.max_batch, 1 <= lanes <= 16).
+ * run: images = device [n][H][W][in_channels] (activation dtype); tuples = HOST float [n][4]
+ * (each in cfg.widths, else SLIM_EINVAL before any launch); logits = device fp32
+ * [n][num_classes].  Asynchronous: everything is ordered on `stream` (and after what was
+ * enqueued on it before the call); the call returns after enqueueing.  The host blocks only
+ * when a staging buffer is still being read by the copy of the call before the previous one.
+ * stats (may be NULL): batches, kernels launched, host seconds spent packing and in the call. */
+typedef struct slim_stream slim_stream;
+typedef struct {
+    int batches;               /* packed batches over the four segments */
+    int launches;              /* kernels this call launched (gather, segment kernels, scatter) */
+    double pack_seconds;       /* host: the four slim_pack calls */
+    double host_seconds;       /* host: the whole call (pack + staging + enqueueing) */
+} slim_stream_stats;
+SLIM_API slim_status slim_stream_create(slim_ctx *ctx, int n_max, int B_max, int lanes, slim_stream **out);
+SLIM_API void slim_stream_destroy(slim_stream *x);
+SLIM_API slim_status slim_stream_run(slim_stream *x, const void *images, const float *tuples, int n, float *logits,
+                                     void *stream, slim_stream_stats *stats);
+
 /* ---- execution modes and profiling ------------------------------------- */
 
 /* Graph mode (default off): slim_forward_ws / slim_forward_chain capture their

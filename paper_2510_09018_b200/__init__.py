@@ -98,6 +98,11 @@ class slim_instance(ctypes.Structure):
                 ("t_last", ctypes.c_double), ("bytes", ctypes.c_size_t)]
 
 
+class slim_stream_stats(ctypes.Structure):
+    _fields_ = [("batches", ctypes.c_int), ("launches", ctypes.c_int), ("pack_seconds", ctypes.c_double),
+                ("host_seconds", ctypes.c_double)]
+
+
 class slim_exec_stats(ctypes.Structure):
     _fields_ = [("batches", ctypes.c_int), ("loads", ctypes.c_int), ("requeues", ctypes.c_int),
                 ("unloaded", ctypes.c_int), ("seconds", ctypes.c_double)]
@@ -165,6 +170,9 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "slim_exec_destroy": (None, [_VP]),
         "slim_exec_run": (_I, [_VP, _VP, ctypes.POINTER(_F), _I, _VP, _SZ, ctypes.POINTER(slim_exec_stats), _VP,
                                ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]),
+        "slim_stream_create": (_I, [_VP, _I, _I, _I, ctypes.POINTER(_VP)]),
+        "slim_stream_destroy": (None, [_VP]),
+        "slim_stream_run": (_I, [_VP, _VP, ctypes.POINTER(_F), _I, _VP, _VP, ctypes.POINTER(slim_stream_stats)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -181,7 +189,8 @@ EXPORTED = ("slim_create", "slim_destroy", "slim_default_config", "slim_load_seg
             "slim_launch_count", "slim_num_sms", "slim_channels", "slim_act_channels", "slim_set_graph_mode", "slim_set_sm_share", "slim_profile_begin",
             "slim_profile_end", "slim_sched_default_knobs", "slim_sched_create", "slim_sched_destroy",
             "slim_sched_enqueue", "slim_sched_next", "slim_sched_complete", "slim_sched_unload_idle",
-            "slim_sched_queue_len", "slim_sched_b_max", "slim_sched_instances", "slim_exec_create", "slim_exec_destroy", "slim_exec_run")
+            "slim_sched_queue_len", "slim_sched_b_max", "slim_sched_instances", "slim_exec_create", "slim_exec_destroy", "slim_exec_run",
+            "slim_stream_create", "slim_stream_destroy", "slim_stream_run")
 
 
 # ------------------------------------------------------------------ marshalling helpers

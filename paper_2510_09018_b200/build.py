@@ -11,7 +11,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libslim.so")
-SOURCES = ["kernels_fused.cu", "kernels_umma.cu", "kernels_halo.cu", "kernels_stem.cu", "kernels_splitk.cu", "kernels_simt.cu", "kernels_gn.cu", "slim_api.cu", "slim_sched.cpp", "slim_exec.cu"]
+SOURCES = ["kernels_fused.cu", "kernels_umma.cu", "kernels_halo.cu", "kernels_stem.cu", "kernels_splitk.cu", "kernels_simt.cu", "kernels_gn.cu", "slim_api.cu", "slim_sched.cpp", "slim_exec.cu", "slim_stream.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden", "--expt-relaxed-constexpr"]

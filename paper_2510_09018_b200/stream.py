@@ -140,3 +140,48 @@ class StreamExecutor:
                 for ls in self.lane_streams:
                     st.wait_stream(ls)
         return self.logits[:n]
+
+
+class NativeStreamExecutor:
+    """The same request-stream sequencing as StreamExecutor, run by libslim (slim_stream_*): one
+    C-ABI call per stream packs the four segments, stages the request orders and enqueues every
+    gather / segment / scatter launch.  Marshalling only; same buffers and lane rule."""
+
+    def __init__(self, net: SlimNet, n_max: int, B_max: int = 256, device=None, lanes: int = 1):
+        import ctypes
+        from . import _check, load_library
+        self.net, self.cfg, self.n_max, self.B_max = net, net.cfg, n_max, B_max
+        self.dev = torch.device(device if device is not None else f"cuda:{torch.cuda.current_device()}")
+        self.lanes = max(1, int(lanes))
+        h = ctypes.c_void_p()
+        _check(net.ctx, load_library().slim_stream_create(net.ctx, n_max, B_max, self.lanes, ctypes.byref(h)))
+        self.h = h.value
+        self.logits = torch.empty(n_max, self.cfg.num_classes, dtype=torch.float32, device=self.dev)
+        self.pack_s, self.host_s, self.last_launches, self.last_n_batches = [], [], 0, 0
+
+    def run(self, images: torch.Tensor, tuples: np.ndarray, stream=None) -> torch.Tensor:
+        import ctypes
+        from . import _check, _stream, load_library, slim_stream_stats
+        t = np.ascontiguousarray(np.asarray(tuples, np.float32))
+        n = t.shape[0]
+        assert n <= self.n_max and t.shape == (n, 4)
+        st = slim_stream_stats()
+        _check(self.net.ctx, load_library().slim_stream_run(
+            self.h, images.data_ptr(), t.ctypes.data_as(ctypes.POINTER(ctypes.c_float)), n, self.logits.data_ptr(),
+            _stream(stream if stream is not None else torch.cuda.current_stream(self.dev)), ctypes.byref(st)))
+        self.pack_s.append(st.pack_seconds)
+        self.host_s.append(st.host_seconds)
+        self.last_launches, self.last_n_batches = st.launches, st.batches
+        return self.logits[:n]
+
+    def close(self):
+        if self.h:
+            from . import load_library
+            load_library().slim_stream_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -82,3 +82,13 @@ def test_groupnorm_config_validation():
     assert lib.slim_create(0, ctypes.byref(cfg), ctypes.byref(h)) == slim.SLIM_EINVAL
     cfg = slim.default_config()
     assert cfg.norm == slim.SLIM_NORM_BN and cfg.gn_group_channels == 16
+
+
+def test_stream_executor_rejects_bad_arguments_without_gpu():
+    """slim_stream_*: argument checks come before any CUDA call (NULL context / handle)."""
+    lib = slim.load_library()
+    h = ctypes.c_void_p(1)
+    assert lib.slim_stream_create(None, 16, 8, 1, ctypes.byref(h)) == -1 and h.value is None
+    assert lib.slim_stream_create(None, 16, 8, 1, None) == -1
+    assert lib.slim_stream_run(None, None, None, 4, None, None, None) == -1
+    lib.slim_stream_destroy(None)

@@ -327,6 +327,39 @@ def test_stream_executor_matches_per_request_chain(net, lanes):
         assert torch.equal(got[idx], ref_l), t
 
 
+@pytest.mark.parametrize("lanes", [1, 8])
+def test_native_stream_executor_matches_python_and_chain(net, lanes):
+    """slim_stream_run (the C++ sequencer) on three consecutive fresh streams (the staging buffers
+    alternate and are reused): bitwise the Python executor's logits and each tuple's own chain;
+    n = 1 and a single-key stream are the degenerate cases."""
+    from paper_2510_09018_b200.stream import NativeStreamExecutor, StreamExecutor
+    from paper_2510_09018_b200.router import TABLE_TUPLES
+    nx = NativeStreamExecutor(net, n_max=64, B_max=8, lanes=lanes)
+    px = StreamExecutor(net, n_max=64, B_max=8, lanes=lanes)
+    px.cache_plans = False
+    for seed, n in ((22, 61), (23, 64), (24, 1)):
+        rng = np.random.default_rng(seed)
+        tup = np.asarray([TABLE_TUPLES[i] for i in rng.integers(0, len(TABLE_TUPLES), n)], np.float32)
+        x = _dev(synth.make_images(n, offset=seed))
+        got = nx.run(x, tup).clone()
+        want = px.run(x, tup).clone()
+        torch.cuda.synchronize()
+        assert torch.equal(got, want), (seed, n)
+        assert nx.last_n_batches == sum(len(b) for b in px.last_batches)
+        for t in set(map(tuple, tup.tolist())):
+            idx = [i for i in range(n) if tuple(tup[i].tolist()) == t]
+            assert torch.equal(got[idx], net.forward_chain(x[idx], t)), t
+    tup = np.tile(np.asarray([[0.5, 0.25, 1.0, 0.75]], np.float32), (40, 1))
+    x = _dev(synth.make_images(40, offset=25))
+    got = nx.run(x, tup).clone()
+    torch.cuda.synchronize()
+    assert nx.last_n_batches == 4 * 5                     # 40 requests, B_max 8, one key per segment
+    assert torch.equal(got, net.forward_chain(x, (0.5, 0.25, 1.0, 0.75)))
+    with pytest.raises(slim.SlimError):                  # a width outside cfg.widths: rejected before any launch
+        nx.run(x, np.full((40, 4), 0.3, np.float32))
+    nx.close()
+
+
 def test_cluster_multicast_path_parity(params, ref):
     """The A-tile multicast variant (cluster of CTAs sharing an M tile; off by default, SLIM_MC_MAX)
     computes the same results: run it through a subprocess with the env var set."""
