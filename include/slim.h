@@ -315,7 +315,8 @@ SLIM_API slim_status slim_exec_run(slim_exec *x, const void *images, const float
  * [n][num_classes].  Asynchronous: everything is ordered on `stream` (and after what was
  * enqueued on it before the call); the call returns after enqueueing.  The host blocks only
  * when a staging buffer is still being read by the copy of the call before the previous one.
- * stats (may be NULL): batches, kernels launched, host seconds spent packing and in the call. */
+ * stats (may be NULL): batches, kernels launched, host seconds spent packing and in the whole call
+ * (incl. any wait for the staging buffer). */
 typedef struct slim_stream slim_stream;
 typedef struct {
     int batches;               /* packed batches over the four segments */

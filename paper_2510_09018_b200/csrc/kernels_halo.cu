@@ -48,7 +48,7 @@ __global__ void __launch_bounds__(kSmall ? kHaloThreadsSmall : kHaloThreads, kSm
     conv_halo_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmRes, const __grid_constant__ CUtensorMap tmOut,
                      const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUtensorMap tmB1,
-                     const HaloArgs a) {
+                     const __grid_constant__ CUtensorMap tmBh, const HaloArgs a) {
     extern __shared__ uint8_t smem_raw[];
     constexpr int EPIW = kSmall ? 8 : kHaloEpiWarps, EPIT = EPIW * 32;   // epilogue warps / threads
     const int CK = kNarrow ? a.ck : kChunk, RBK = kNarrow ? a.rbk : 128;
@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(kSmall ? kHaloThreadsSmall : kHaloThreads, kSm
             mbar_init(a_full(i), 1);
             mbar_init(a_empty(i), 1);
             mbar_init(b_full(i), 1);
-            mbar_init(b_empty(i), 1);
+            mbar_init(b_empty(i), a.bmc);   // B multicast: every CTA of the cluster frees the slot
         }
         for (int i = 0; i < 4; ++i) {
             mbar_init(t_full(i), 1);
@@ -144,6 +144,8 @@ __global__ void __launch_bounds__(kSmall ? kHaloThreadsSmall : kHaloThreads, kSm
     }
     // weight-stationary B does not depend on the previous kernel: start it before the PDL wait
     __syncthreads();
+    const uint16_t bmask = static_cast<uint16_t>((1u << a.bmc) - 1u);
+    if (a.bmc > 1) cluster_sync_all();   // every CTA's barriers exist before a peer multicasts / commits into them
     if (a.stationary && warp == 2 && lane == 0) {
         // exact box bytes (the slot itself is rounded up to 1 KiB)
         mbar_expect_tx(b_full(0), static_cast<uint32_t>(a.n_chunks) * 9u * a.n_tile * RBK);
@@ -269,14 +271,23 @@ __global__ void __launch_bounds__(kSmall ? kHaloThreadsSmall : kHaloThreads, kSm
         if (lane == 0 && !a.stationary) {
             int s = 0;
             uint32_t ph = 0;
+            // multicast: this CTA's share of each stage = rows [rank*hrows, +hrows) of every tap block
+            const int hrows = a.n_tile / a.bmc;
+            const uint32_t rank = a.bmc > 1 ? cluster_ctarank() : 0u;
+            const uint32_t tapb = static_cast<uint32_t>(a.n_tile) * RBK, hoff = rank * hrows * RBK;
             for (int t = blockIdx.x; t < total; t += gridDim.x) {
                 const int co0 = (t / a.m_tiles) * a.n_tile;
                 for (int ch = 0; ch < a.n_chunks; ++ch)
                     for (int kq = 0; kq < 3; ++kq) {
                         const int kh = s2 ? (kq == 0 ? 0 : (kq == 1 ? 2 : 1)) : kq;   // s2 consumes kh 0, 2, 1
                         mbar_wait(b_empty(s), ph ^ 1);
-                        mbar_expect_tx(b_full(s), 3u * a.n_tile * RBK);
-                        if (!s2) {
+                        mbar_expect_tx(b_full(s), 3u * a.n_tile * RBK);   // all bmc shares land in every CTA
+                        if (a.bmc > 1) {   // tap blocks in the consumer's order (s2: kw = 0, 2, 1)
+                            for (int j = 0; j < 3; ++j)
+                                tma_load_3d_mc(sB + s * a.b_bytes + j * tapb + hoff, &tmBh, b_full(s), ch * CK,
+                                               co0 + static_cast<int>(rank) * hrows,
+                                               kh * 3 + (s2 ? (j == 0 ? 0 : (j == 1 ? 2 : 1)) : j), bmask);
+                        } else if (!s2) {
                             tma_load_3d(sB + s * a.b_bytes, &tmB, b_full(s), ch * CK, co0, kh * 3);
                         } else {   // one-tap boxes in the order kw = 0, 2, 1
                             const uint32_t tapb = static_cast<uint32_t>(a.n_tile) * RBK;
@@ -354,7 +365,10 @@ __global__ void __launch_bounds__(kSmall ? kHaloThreadsSmall : kHaloThreads, kSm
                                 }
                                 __syncwarp();
                                 if (!a.stationary) {
-                                    if (elect_one()) umma_commit(b_empty(bs));
+                                    if (elect_one()) {
+                                        if (a.bmc > 1) umma_commit_mc(b_empty(bs), bmask);
+                                        else umma_commit(b_empty(bs));
+                                    }
                                     __syncwarp();
                                     if (++bs == a.sb) {
                                         bs = 0;
@@ -488,7 +502,8 @@ __global__ void __launch_bounds__(kSmall ? kHaloThreadsSmall : kHaloThreads, kSm
                                                 umma_bf16(acc + kw * accs, adk + 2 * kk, bd + kw * tap16 + 2 * kk,
                                                           kw ? idesc_r : idesc, (ch | kh | kk) != 0);
                                 }
-                                umma_commit(b_empty(bs));
+                                if (a.bmc > 1) umma_commit_mc(b_empty(bs), bmask);   // frees the slot cluster-wide
+                                else umma_commit(b_empty(bs));
                             }
                             __syncwarp();
                             if (++bs == a.sb) {
@@ -784,6 +799,7 @@ __global__ void __launch_bounds__(kSmall ? kHaloThreadsSmall : kHaloThreads, kSm
 
     tc_fence_before();
     __syncthreads();
+    if (a.bmc > 1) cluster_sync_all();   // no CTA leaves while a peer may still multicast / commit into it
     if (warp == 1) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(a.tmem_cols)
@@ -805,8 +821,9 @@ size_t conv_halo_smem_bytes(const HaloArgs &a) {
 
 cudaError_t launch_conv_halo(const HaloArgs &a, const CUtensorMap &tmA, const CUtensorMap &tmB,
                              const CUtensorMap &tmRes, const CUtensorMap &tmOut, const CUtensorMap &tmA1,
-                             const CUtensorMap &tmB1, int grid, cudaStream_t stream, bool pdl) {
-    using Fn = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, HaloArgs);
+                             const CUtensorMap &tmB1, const CUtensorMap &tmBh, int grid, cudaStream_t stream, bool pdl) {
+    using Fn = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap,
+                        HaloArgs);
     static const Fn fns[2][6] = {{conv_halo_kernel<false, 0>, conv_halo_kernel<false, 1>, conv_halo_kernel<false, 2>,
                                   conv_halo_kernel<false, 3>, conv_halo_kernel<false, 4>, conv_halo_kernel<false, 5>},
                                  {conv_halo_kernel<true, 0>, conv_halo_kernel<true, 1>, conv_halo_kernel<true, 2>,
@@ -833,18 +850,23 @@ cudaError_t launch_conv_halo(const HaloArgs &a, const CUtensorMap &tmA, const CU
     cfg.blockDim = dim3(a.small ? kHaloThreadsSmall : kHaloThreads);
     cfg.dynamicSmemBytes = conv_halo_smem_bytes(a);
     cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = a.bmc;
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = a.bmc > 1 ? 2 : 1;
+    if (a.bmc > 1 && (grid % a.bmc || a.m_tiles % a.bmc || a.stationary || a.small)) return cudaErrorInvalidValue;
     const bool narrow = a.ck != kChunk || a.co_chunk != kChunk;
     const int var = a.stride2 ? 3 : (a.x3 == 1 ? 4 : (a.x3 == 2 ? 5 : (a.epi == EPI_BN_PROJ_RELU ? 1 : (a.pool_out ? 2 : 0))));
     if (a.small) {
         if (var > 3) return cudaErrorInvalidValue;
-        return cudaLaunchKernelEx(&cfg, small_fns[var], tmA, tmB, tmRes, tmOut, tmA1, tmB1, a);
+        return cudaLaunchKernelEx(&cfg, small_fns[var], tmA, tmB, tmRes, tmOut, tmA1, tmB1, tmBh, a);
     }
-    return cudaLaunchKernelEx(&cfg, fns[narrow ? 1 : 0][var], tmA, tmB, tmRes, tmOut, tmA1, tmB1, a);
+    return cudaLaunchKernelEx(&cfg, fns[narrow ? 1 : 0][var], tmA, tmB, tmRes, tmOut, tmA1, tmB1, tmBh, a);
 }
 
 }  // namespace slim

@@ -674,6 +674,21 @@ slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, i
     int grid = ctx->num_sms * (two ? 2 : 1);
     if (grid > total) grid = total;
     grid = grid_cap(ctx, ri, grid, cc.seg);
+    // streamed weights: clusters of bmc CTAs on consecutive M tiles of one N tile share each B stage
+    // (TMA multicast) -- the weight bytes one launch pulls from L2 drop by bmc.  Opt-in (SLIM_HALO_BMC=2|4):
+    // bit-identical, but measured no faster (B=1024 r=1 seg 2/3 convs 84/80 us either way; B=128 chains
+    // +4 %, bmc 4 up to 2x slower: the cluster's CTAs advance in lock step, profiles/r02_bmc_multicast.txt),
+    // so the L2->SM weight stream is not what bounds these convs
+    static const int bmc_env = getenv("SLIM_HALO_BMC") ? atoi(getenv("SLIM_HALO_BMC")) : 1;
+    a.bmc = 1;
+    CUtensorMap tBh = tA;
+    if ((bmc_env == 2 || bmc_env == 4) && !a.stationary && !small && !a.x3 && a.m_tiles % bmc_env == 0 &&
+        (a.n_tile / bmc_env) % 8 == 0 && grid >= bmc_env) {
+        if (!encode_w_taps(ctx, &tBh, L, cc.c_in, c_out, a.n_tile / bmc_env, 1, a.ck))
+            return fail(ctx, SLIM_ECUDA, "cuTensorMapEncodeTiled(halo W share) failed");
+        a.bmc = bmc_env;
+        grid -= grid % bmc_env;
+    }
     double flops, bytes;
     conv_work(c, cc, ri, B, H, W, &flops, &bytes);
     if (ctx->trace) cudaMemsetAsync(ctx->trace, 0, 3584 * sizeof(unsigned long long), st);   // diagnostics (stem: 3584..)
@@ -686,7 +701,7 @@ slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, i
         if (!encode_w(ctx, &tB1, *cc.Lp, cc.c_in_p, c_out, a.n_tile, kChunk))
             return fail(ctx, SLIM_ECUDA, "cuTensorMapEncodeTiled(halo proj W) failed");
     }
-    cudaError_t e = launch_conv_halo(a, tA, *tB, tRes, tOut, tA1, tB1, grid, st, ctx->pdl && !ctx->prof_on);
+    cudaError_t e = launch_conv_halo(a, tA, *tB, tRes, tOut, tA1, tB1, tBh, grid, st, ctx->pdl && !ctx->prof_on);
     prof.done(SLIM_K_CONV_UMMA, cc.seg, cc.layer, c.widths[cc.ri_in], c.widths[ri], B, flops, bytes);
     if (e != cudaSuccess)
         return fail(ctx, SLIM_ECUDA, "conv_halo launch (grid %d, smem %zu): %s", grid, conv_halo_smem_bytes(a),
@@ -1902,32 +1917,38 @@ slim_status slim_pack(const slim_config *cfg, const slim_request *q, int n, int 
     if (!cfg || n < 0 || B_max < 1 || !n_descs || (n > 0 && (!q || !descs || !order))) return SLIM_EINVAL;
     *n_descs = 0;
     const slim_config &c = *cfg;
-    // key -> FIFO of request indices; a key is (seg, w_req idx, w_prev idx)
-    std::unordered_map<int, std::vector<int>> buckets;
-    std::vector<int> key_of(n);
+    // key -> FIFO of request indices; a key is (seg, w_req idx, w_prev idx).  Buckets are one
+    // flat array grouped by key (counting sort, stable: FIFO order inside a key).
+    constexpr int kKeys = 4 * kMaxW * kMaxW;
+    std::vector<int> key_of(n), bucket(n);
+    int start[kKeys + 1] = {}, head[kKeys];
     for (int i = 0; i < n; ++i) {
         const int wr = width_index(c, q[i].w_req);
         const int wp = q[i].seg == 0 ? 0 : width_index(c, q[i].w_prev);
         if (q[i].seg < 0 || q[i].seg > 3 || wr < 0 || wp < 0) return SLIM_EINVAL;
         key_of[i] = (q[i].seg * kMaxW + wr) * kMaxW + wp;
-        buckets[key_of[i]].push_back(i);
+        start[key_of[i] + 1]++;
     }
-    std::unordered_map<int, size_t> head;   // consumed prefix of each bucket
+    for (int k = 0; k < kKeys; ++k) {
+        start[k + 1] += start[k];
+        head[k] = start[k];
+    }
+    for (int i = 0; i < n; ++i) bucket[head[key_of[i]]++] = i;
+    for (int k = 0; k < kKeys; ++k) head[k] = start[k];   // consumed prefix of each bucket
     std::vector<char> taken(n, 0);
     int pos = 0, nd = 0;
     for (int i = 0; i < n; ++i) {   // Alg.1 LOOP: peek the FIFO head's key ...
         if (taken[i]) continue;
         if (nd >= max_descs) return SLIM_EINVAL;
-        std::vector<int> &bk = buckets[key_of[i]];
-        size_t &h = head[key_of[i]];
+        const int k = key_of[i];
         slim_launch_desc d;
         d.seg = q[i].seg;
         d.r = q[i].w_req;
         d.r_prev = q[i].seg == 0 ? q[i].w_req : q[i].w_prev;
         d.first = pos;
         d.batch = 0;
-        while (h < bk.size() && d.batch < B_max) {   // ... FORM-BATCH: up to B_max with that key, FIFO order
-            const int j = bk[h++];
+        while (head[k] < start[k + 1] && d.batch < B_max) {   // ... FORM-BATCH: up to B_max with that key, FIFO order
+            const int j = bucket[head[k]++];
             taken[j] = 1;
             order[pos++] = static_cast<uint32_t>(j);
             d.batch++;

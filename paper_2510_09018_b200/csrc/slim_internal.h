@@ -123,11 +123,15 @@ struct HaloArgs {
     // (mean, M2) over the tile's pixels of that image, at gn_part[(n*tiles_per_img + ti)*(c_out/16) + g];
     // nullptr = off.  The GN apply kernel then merges them (launch_gn_apply_part).
     float2 *gn_part;
+    // streamed-weight multicast: a cluster of bmc CTAs (1 = off) works on bmc consecutive M tiles of one
+    // N tile; each CTA loads 1/bmc of every B stage (rows rank*n_tile/bmc.., tmBh: box [ck, n_tile/bmc, 1])
+    // and multicasts it to all, so the cluster reads each weight byte from L2 once instead of bmc times
+    int bmc;
 };
 size_t conv_halo_smem_bytes(const HaloArgs &a);
 cudaError_t launch_conv_halo(const HaloArgs &a, const CUtensorMap &tmA, const CUtensorMap &tmB,
                              const CUtensorMap &tmRes, const CUtensorMap &tmOut, const CUtensorMap &tmA1,
-                             const CUtensorMap &tmB1, int grid, cudaStream_t stream, bool pdl);
+                             const CUtensorMap &tmB1, const CUtensorMap &tmBh, int grid, cudaStream_t stream, bool pdl);
 cudaError_t launch_conv_umma(const ConvArgs &a, const CUtensorMap &tmA0, const CUtensorMap &tmB0,
                              const CUtensorMap &tmA1, const CUtensorMap &tmB1, const CUtensorMap &tmRes,
                              const CUtensorMap &tmOut, int grid, cudaStream_t stream, bool pdl);

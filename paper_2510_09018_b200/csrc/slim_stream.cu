@@ -14,6 +14,7 @@
 // gathers straight from the caller's images.  Each lane owns a slab (gathered batch), an out
 // buffer (the batch's outputs before the scatter) and a forward workspace, all sized for B_max.
 #include <chrono>
+#include <cmath>
 #include <cstring>
 #include <vector>
 
@@ -47,10 +48,10 @@ struct slim_stream {
 
 namespace {
 
-int width_slot(const slim_config &c, float r) {
+int width_slot(const slim_config &c, float r) {   // same matching as slim_pack's key validation
     for (int i = 0; i < c.n_widths; ++i)
-        if (c.widths[i] == r) return i;
-    return -1;
+        if (std::fabs(c.widths[i] - r) < 1e-6f) return i;
+    return 0;   // (unreachable: slim_pack rejected the stream)
 }
 
 }  // namespace
@@ -145,6 +146,7 @@ slim_status slim_stream_run(slim_stream *x, const void *images, const float *tup
     const int b = x->buf;
     if (x->order_ev_live[b] && cudaEventSynchronize(x->order_ev[b]) != cudaSuccess) return SLIM_ECUDA;
     uint32_t *oh = x->order_h[b];
+    const auto tp = std::chrono::steady_clock::now();
     // 1. Alg. 1 l.3-4 per segment: key (s, w_s, w_{s-1}) batches, FIFO order
     for (int s = 0; s < 4; ++s) {
         for (int i = 0; i < n; ++i)
@@ -205,7 +207,7 @@ slim_status slim_stream_run(slim_stream *x, const void *images, const float *tup
     if (stats) {
         stats->batches = batches;
         stats->launches = static_cast<int>(slim_launch_count(x->ctx) - l0);
-        stats->pack_seconds = std::chrono::duration<double>(t1 - t0).count();
+        stats->pack_seconds = std::chrono::duration<double>(t1 - tp).count();
         stats->host_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     }
     return slim_last_error(x->ctx);

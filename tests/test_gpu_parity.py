@@ -380,6 +380,47 @@ def test_cluster_multicast_path_parity(params, ref):
     assert float(out.stdout.strip().splitlines()[-1]) <= TAU_BF16
 
 
+@pytest.mark.parametrize("bmc", [2, 4])
+def test_halo_weight_multicast_bitwise(bmc, tmp_path):
+    """Streamed-weight multicast (clusters of bmc CTAs share each B stage, SLIM_HALO_BMC): every
+    segment 1-3 output for all (r_prev, r) at B = 13 and 64 is bitwise the unclustered kernel's (same
+    MMA order; only who loads the weights changes), and the oracle agrees on a sample."""
+    import subprocess, sys, os
+    code = (
+        "import sys, numpy as np, torch, synth, oracle, paper_2510_09018_b200 as slim\n"
+        "w, bn = synth.make_weights(), synth.make_bn()\n"
+        "net = slim.SlimNet(w, bn, max_batch=64)\n"
+        "W = synth.WIDTHS\n"
+        "outs = {}\n"
+        "for seg in (1, 2, 3):\n"
+        "    H = 32 >> (seg - 1)\n"
+        "    for rp in W:\n"
+        "        C = synth.active_channels(rp, synth.BASE_CHANNELS[seg - 1])\n"
+        "        g = np.random.default_rng(91 + seg)\n"
+        "        x = synth.round_bf16(np.abs(g.standard_normal((64, H, H, C), dtype=np.float32)))\n"
+        "        xd = torch.from_numpy(x).to(torch.bfloat16).cuda()\n"
+        "        for r in W:\n"
+        "            for B in (13, 64):\n"
+        "                outs[f'{seg}_{rp}_{r}_{B}'] = net.forward(seg, xd[:B].contiguous(), rp, r).float().cpu().numpy()\n"
+        "        if rp == 1.0:\n"
+        "            ref = oracle.Model(w, bn).segment(seg, x[:3], rp, 1.0)\n"
+        "            err = oracle.per_image_rel_err(outs[f'{seg}_{rp}_1.0_13'][:3], ref)\n"
+        "            assert err.max() <= 2e-2, (seg, err.max())\n"
+        "np.savez(sys.argv[1], **outs)\n"
+    )
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for m in (1, bmc):
+        f = str(tmp_path / f"bmc{m}.npz")
+        env = dict(os.environ, SLIM_HALO_BMC=str(m), SLIM_NO_FUSED="1")
+        out = subprocess.run([sys.executable, "-c", code, f], env=env, capture_output=True, text=True, timeout=600,
+                             cwd=root)
+        assert out.returncode == 0, out.stderr[-2000:]
+        res[m] = np.load(f)
+    for k in res[1].files:
+        assert np.array_equal(res[1][k], res[bmc][k]), k
+
+
 def test_splitk_cluster_path_parity():
     """The split-K conv (cluster of CTAs over K, fp32 partials reduced through DSMEM; chosen by a
     cost model, forced here with SLIM_SPLITK_FORCE) matches the oracle on segments 1-3 for every
