@@ -43,7 +43,9 @@ constexpr int kHaloThreadsSmall = (4 + 8) * 32;
 // kVar: 0 = plain / residual epilogue, 1 = + projection shortcut, 2 = + fused average pool,
 // 3 = stride-2 conv (parity planes), 4 = three shifted halo boxes (no kw accumulators), see below
 // (compile-time, so the common variant carries none of the other two's code)
-template <bool kNarrow, int kVar, bool kSmall = false>
+// kClu: 0 = one CTA per tile (no cluster instructions compiled in: a kernel holding cta_group::2 /
+// multicast code must be launched as a cluster), 1 = streamed-weight multicast (a.bmc), 2 = 2-SM pair
+template <bool kNarrow, int kVar, bool kSmall = false, int kClu = 0>
 __global__ void __launch_bounds__(kSmall ? kHaloThreadsSmall : kHaloThreads, kSmall ? 2 : 1)
     conv_halo_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmRes, const __grid_constant__ CUtensorMap tmOut,
@@ -108,17 +110,23 @@ __global__ void __launch_bounds__(kSmall ? kHaloThreadsSmall : kHaloThreads, kSm
 #define TD(role, tile, pt) \
     if (td && (tile) < 64) td[(role) * 256 + (tile) * 4 + (pt)] = gtimer()
     if (tr && threadIdx.x == 0) tr[0] = gtimer();
+    // 2-SM pair: rank 0 (leader) issues the M = 256 MMAs; the producers of both CTAs signal the leader's
+    // full barriers, the leader's commits arrive on both CTAs' empty / t_full barriers, and the peer's
+    // accumulator release is relayed onto the leader's t_empty by the peer's (otherwise idle) MMA warp
+    constexpr bool pair = kClu == 2;
+    const uint32_t prank = pair ? cluster_ctarank() : 0u;
+    const bool leader_cta = prank == 0;
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < 4; ++i) {
             mbar_init(a_full(i), 1);
             mbar_init(a_empty(i), 1);
             mbar_init(b_full(i), 1);
-            mbar_init(b_empty(i), a.bmc);   // B multicast: every CTA of the cluster frees the slot
+            mbar_init(b_empty(i), kClu == 1 ? a.bmc : 1);   // B multicast: every CTA of the cluster frees the slot
         }
         for (int i = 0; i < 4; ++i) {
             mbar_init(t_full(i), 1);
-            mbar_init(t_empty(i), EPIT / n_grp);
+            mbar_init(t_empty(i), EPIT / n_grp + (pair && leader_cta ? 1 : 0));
             mbar_init(r_full(i), 1);
             mbar_init(r_empty(i), EPIT / n_grp);
         }
@@ -129,10 +137,19 @@ __global__ void __launch_bounds__(kSmall ? kHaloThreadsSmall : kHaloThreads, kSm
         if (n_res) prefetch_tmap(&tmRes);
     }
     if (warp == 1) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                     "r"(a.tmem_cols)
-                     : "memory");
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+        if (pair) {   // both CTAs of the pair allocate (same columns): the pair MMA writes both TMEMs
+            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                             smem_u32(tmem_slot)),
+                         "r"(a.tmem_cols)
+                         : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+        } else {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                             smem_u32(tmem_slot)),
+                         "r"(a.tmem_cols)
+                         : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+        }
     }
     for (int i = threadIdx.x; i < a.c_out; i += blockDim.x) {
         sBN[i] = a.scale[i];
@@ -144,8 +161,9 @@ __global__ void __launch_bounds__(kSmall ? kHaloThreadsSmall : kHaloThreads, kSm
     }
     // weight-stationary B does not depend on the previous kernel: start it before the PDL wait
     __syncthreads();
-    const uint16_t bmask = static_cast<uint16_t>((1u << a.bmc) - 1u);
-    if (a.bmc > 1) cluster_sync_all();   // every CTA's barriers exist before a peer multicasts / commits into them
+    const int bmc = kClu == 1 ? a.bmc : 1;
+    const uint16_t bmask = static_cast<uint16_t>((1u << bmc) - 1u);
+    if (kClu != 0) cluster_sync_all();   // every CTA's barriers exist before a peer multicasts / commits into them
     if (a.stationary && warp == 2 && lane == 0) {
         // exact box bytes (the slot itself is rounded up to 1 KiB)
         mbar_expect_tx(b_full(0), static_cast<uint32_t>(a.n_chunks) * 9u * a.n_tile * RBK);
@@ -192,6 +210,11 @@ __global__ void __launch_bounds__(kSmall ? kHaloThreadsSmall : kHaloThreads, kSm
                                 ph ^= 1;
                             }
                         }
+                    } else if (pair) {   // own tile's halo; the leader's a_full counts both CTAs' bytes
+                        mbar_wait(a_empty(s), ph ^ 1);
+                        const uint32_t lb = mapa_u32(a_full(s), 0);
+                        if (leader_cta) mbar_expect_tx_cluster(lb, 2u * a.a_bytes);
+                        tma_load_4d_pair(sA + s * a.a_slot, &tmA, lb, ch * CK, 0, n * a.tile_imgs, h0 - 1);
                     } else {
                         mbar_wait(a_empty(s), ph ^ 1);
                         if (ch == 0) TD(0, ti, 2);
@@ -230,6 +253,18 @@ __global__ void __launch_bounds__(kSmall ? kHaloThreadsSmall : kHaloThreads, kSm
                 const int co0 = (t / a.m_tiles) * a.n_tile;
                 for (int cp = 0; proj && cp < a.n_chunks_p; ++cp) {
                     mbar_wait(a_empty(s), ph ^ 1);
+                    if (pair) {   // own 128 px + HALF of the 1x1 weights (tmB1 box: n_tile/2 rows)
+                        const uint32_t lb = mapa_u32(a_full(s), 0);
+                        if (leader_cta) mbar_expect_tx_cluster(lb, 2u * 16384u + static_cast<uint32_t>(a.n_tile) * 128u);
+                        tma_load_4d_pair(sA + s * a.a_slot, &tmA1, lb, cp * kChunk, 0, n * a.tile_imgs, 2 * h0);
+                        tma_load_3d_pair(sA + s * a.a_slot + 16384u, &tmB1, lb, cp * kChunk, 0,
+                                         co0 + static_cast<int>(prank) * (a.n_tile / 2));
+                        if (++s == a.sa) {
+                            s = 0;
+                            ph ^= 1;
+                        }
+                        continue;
+                    }
                     mbar_expect_tx(a_full(s), 16384u + static_cast<uint32_t>(a.n_tile) * 128u);
                     tma_load_4d(sA + s * a.a_slot, &tmA1, a_full(s), cp * kChunk, 0, n * a.tile_imgs, 2 * h0);
                     tma_load_3d(sA + s * a.a_slot + 16384u, &tmB1, a_full(s), cp * kChunk, 0, co0);
@@ -272,8 +307,8 @@ __global__ void __launch_bounds__(kSmall ? kHaloThreadsSmall : kHaloThreads, kSm
             int s = 0;
             uint32_t ph = 0;
             // multicast: this CTA's share of each stage = rows [rank*hrows, +hrows) of every tap block
-            const int hrows = a.n_tile / a.bmc;
-            const uint32_t rank = a.bmc > 1 ? cluster_ctarank() : 0u;
+            const int hrows = a.n_tile / bmc;
+            const uint32_t rank = kClu == 1 ? cluster_ctarank() : 0u;
             const uint32_t tapb = static_cast<uint32_t>(a.n_tile) * RBK, hoff = rank * hrows * RBK;
             for (int t = blockIdx.x; t < total; t += gridDim.x) {
                 const int co0 = (t / a.m_tiles) * a.n_tile;
@@ -281,8 +316,25 @@ __global__ void __launch_bounds__(kSmall ? kHaloThreadsSmall : kHaloThreads, kSm
                     for (int kq = 0; kq < 3; ++kq) {
                         const int kh = s2 ? (kq == 0 ? 0 : (kq == 1 ? 2 : 1)) : kq;   // s2 consumes kh 0, 2, 1
                         mbar_wait(b_empty(s), ph ^ 1);
+                        if (pair) {
+                            // this CTA's half of the stage: rows [rank*1.5n, (rank+1)*1.5n) of the three adjacent
+                            // tap blocks = three half-blocks j = 3*rank + i (tap j/2, rows (j%2)*n/2 ..)
+                            const uint32_t lb = mapa_u32(b_full(s), 0);
+                            if (leader_cta) mbar_expect_tx_cluster(lb, 3u * a.n_tile * RBK);
+                            const uint32_t hb = static_cast<uint32_t>(a.n_tile / 2) * RBK;
+                            for (int i = 0; i < 3; ++i) {
+                                const int j = 3 * static_cast<int>(prank) + i;
+                                tma_load_3d_pair(sB + s * a.b_bytes + i * hb, &tmBh, lb, ch * CK,
+                                                 co0 + (j & 1) * (a.n_tile / 2), kh * 3 + (j >> 1));
+                            }
+                            if (++s == a.sb) {
+                                s = 0;
+                                ph ^= 1;
+                            }
+                            continue;
+                        }
                         mbar_expect_tx(b_full(s), 3u * a.n_tile * RBK);   // all bmc shares land in every CTA
-                        if (a.bmc > 1) {   // tap blocks in the consumer's order (s2: kw = 0, 2, 1)
+                        if (kClu == 1) {   // tap blocks in the consumer's order (s2: kw = 0, 2, 1)
                             for (int j = 0; j < 3; ++j)
                                 tma_load_3d_mc(sB + s * a.b_bytes + j * tapb + hoff, &tmBh, b_full(s), ch * CK,
                                                co0 + static_cast<int>(rank) * hrows,
@@ -302,6 +354,18 @@ __global__ void __launch_bounds__(kSmall ? kHaloThreadsSmall : kHaloThreads, kSm
                     }
             }
         }
+    } else if (warp == 1 && pair && !leader_cta) {
+        // ===================== pair peer: accumulator-release relay =================
+        // the leader's MMA may overwrite an accumulator stage only when BOTH CTAs' epilogues have
+        // drained it: forward each completion of this CTA's t_empty(stage) to the leader's
+        if (lane == 0) {
+            int it = 0;
+            for (int t = blockIdx.x; t < total; t += gridDim.x, ++it) {
+                const int as = it % a.acc_stages;
+                mbar_wait(t_empty(as), static_cast<uint32_t>(it / a.acc_stages) & 1u);
+                mbar_arrive_cluster(mapa_u32(t_empty(as), 0));
+            }
+        }
     } else if (warp == 1) {
         // ===================== MMA issuer ===========================================
         // Lean issue loop: descriptors are base + offset adds (start-address field, 16-B
@@ -311,8 +375,18 @@ __global__ void __launch_bounds__(kSmall ? kHaloThreadsSmall : kHaloThreads, kSm
         {   // the whole warp runs the loop (uniform operands); one elected lane issues
             // kw_fuse taps per MMA: N = kw_fuse * n_tile covers adjacent accumulators / B tap blocks
             const int kf = a.kw_fuse;
-            const uint32_t idesc = umma_idesc_bf16(kTileM, a.n_tile * kf);
-            const uint32_t idesc_r = umma_idesc_bf16(kTileM, a.n_tile * (kf == 2 ? 1 : kf));
+            // pair: M = 256 over the CTA pair; commits arrive on both CTAs' barriers
+            auto mma = [&](uint32_t d, uint64_t ad, uint64_t bd, uint32_t id, uint32_t acc) {
+                if (pair) umma_bf16_pair(d, ad, bd, id, acc);
+                else umma_bf16(d, ad, bd, id, acc);
+            };
+            auto commit = [&](uint32_t bar) {
+                if (pair) umma_commit_pair(bar, 3);
+                else umma_commit(bar);
+            };
+            const int kTileMM = pair ? 2 * kTileM : kTileM;
+            const uint32_t idesc = umma_idesc_bf16(kTileMM, a.n_tile * kf);
+            const uint32_t idesc_r = umma_idesc_bf16(kTileMM, a.n_tile * (kf == 2 ? 1 : kf));
             const uint32_t tap16 = static_cast<uint32_t>(a.n_tile * RBK) >> 4;   // one tap's B tile, 16-B units
             const uint32_t row16 = static_cast<uint32_t>(a.row_px * RBK) >> 4;   // one halo row (tile_imgs x W px)
             const uint64_t adesc0 = umma_desc_kmajor(sA, RBK), bdesc0 = umma_desc_kmajor(sB, RBK);
@@ -366,7 +440,7 @@ __global__ void __launch_bounds__(kSmall ? kHaloThreadsSmall : kHaloThreads, kSm
                                 __syncwarp();
                                 if (!a.stationary) {
                                     if (elect_one()) {
-                                        if (a.bmc > 1) umma_commit_mc(b_empty(bs), bmask);
+                                        if (kClu == 1) umma_commit_mc(b_empty(bs), bmask);
                                         else umma_commit(b_empty(bs));
                                     }
                                     __syncwarp();
@@ -499,11 +573,11 @@ __global__ void __launch_bounds__(kSmall ? kHaloThreadsSmall : kHaloThreads, kSm
 #pragma unroll
                                         for (int kk = 0; kk < 4; ++kk)
                                             if (kk < nk)
-                                                umma_bf16(acc + kw * accs, adk + 2 * kk, bd + kw * tap16 + 2 * kk,
-                                                          kw ? idesc_r : idesc, (ch | kh | kk) != 0);
+                                                mma(acc + kw * accs, adk + 2 * kk, bd + kw * tap16 + 2 * kk,
+                                                    kw ? idesc_r : idesc, (ch | kh | kk) != 0);
                                 }
-                                if (a.bmc > 1) umma_commit_mc(b_empty(bs), bmask);   // frees the slot cluster-wide
-                                else umma_commit(b_empty(bs));
+                                if (kClu == 1) umma_commit_mc(b_empty(bs), bmask);   // frees the slot cluster-wide
+                                else commit(b_empty(bs));
                             }
                             __syncwarp();
                             if (++bs == a.sb) {
@@ -513,7 +587,7 @@ __global__ void __launch_bounds__(kSmall ? kHaloThreadsSmall : kHaloThreads, kSm
                         }
                     }
                     if (ch == 0 && lane == 0) TD(3, ti, 1);
-                    if (elect_one()) umma_commit(a_empty(s));
+                    if (elect_one()) commit(a_empty(s));
                     __syncwarp();
                     if (ch == 0 && lane == 0) TD(3, ti, 2);
                     if (++s == a.sa) {
@@ -522,7 +596,7 @@ __global__ void __launch_bounds__(kSmall ? kHaloThreadsSmall : kHaloThreads, kSm
                     }
                 }
                 if (proj) {
-                    const uint32_t idesc_p = umma_idesc_bf16(kTileM, a.n_tile);
+                    const uint32_t idesc_p = umma_idesc_bf16(kTileMM, a.n_tile);
                     const uint64_t pdesc0 = umma_desc_kmajor(sA, 128);
                     for (int cp = 0; cp < a.n_chunks_p; ++cp) {
                         const int nk = min(4, (a.c_in_p - cp * kChunk + 15) >> 4);
@@ -531,9 +605,8 @@ __global__ void __launch_bounds__(kSmall ? kHaloThreadsSmall : kHaloThreads, kSm
                         if (elect_one()) {
                             const uint64_t ad = pdesc0 + s * a_slot16;
                             for (int kk = 0; kk < nk; ++kk)
-                                umma_bf16(acc + 3 * accs, ad + 2 * kk, ad + (16384u >> 4) + 2 * kk, idesc_p,
-                                          (cp | kk) != 0);
-                            umma_commit(a_empty(s));
+                                mma(acc + 3 * accs, ad + 2 * kk, ad + (16384u >> 4) + 2 * kk, idesc_p, (cp | kk) != 0);
+                            commit(a_empty(s));
                         }
                         __syncwarp();
                         if (++s == a.sa) {
@@ -542,7 +615,7 @@ __global__ void __launch_bounds__(kSmall ? kHaloThreadsSmall : kHaloThreads, kSm
                         }
                     }
                 }
-                if (elect_one()) umma_commit(t_full(as));
+                if (elect_one()) commit(t_full(as));
                 __syncwarp();
                 if (lane == 0) {
                     TD(1, ti, 3);
@@ -799,11 +872,15 @@ __global__ void __launch_bounds__(kSmall ? kHaloThreadsSmall : kHaloThreads, kSm
 
     tc_fence_before();
     __syncthreads();
-    if (a.bmc > 1) cluster_sync_all();   // no CTA leaves while a peer may still multicast / commit into it
+    if (kClu != 0) cluster_sync_all();   // no CTA leaves while a peer may still multicast / commit into it
     if (warp == 1) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(a.tmem_cols)
-                     : "memory");
+        if (pair)
+            asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(a.tmem_cols)
+                         : "memory");
+        else
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(a.tmem_cols)
+                         : "memory");
     }
     if (tr && threadIdx.x == 0) tr[6] = gtimer();
 }
@@ -830,14 +907,25 @@ cudaError_t launch_conv_halo(const HaloArgs &a, const CUtensorMap &tmA, const CU
                                   conv_halo_kernel<true, 3>, conv_halo_kernel<true, 4>, conv_halo_kernel<true, 5>}};
     static const Fn small_fns[4] = {conv_halo_kernel<true, 0, true>, conv_halo_kernel<true, 1, true>,
                                     conv_halo_kernel<true, 2, true>, conv_halo_kernel<true, 3, true>};
+    // cluster variants (streamed weights only: 64-channel boxes, plain / projection / pool / stride 2)
+    static const Fn mc_fns[4] = {conv_halo_kernel<false, 0, false, 1>, conv_halo_kernel<false, 1, false, 1>,
+                                 conv_halo_kernel<false, 2, false, 1>, conv_halo_kernel<false, 3, false, 1>};
+    static const Fn pair_fns[3] = {conv_halo_kernel<false, 0, false, 2>, conv_halo_kernel<false, 1, false, 2>,
+                                   conv_halo_kernel<false, 2, false, 2>};
     static bool attr_set = false;
     if (!attr_set) {
+        auto big = [](Fn f) {
+            cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+            cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+            return e;
+        };
         for (int m = 0; m < 2; ++m)
-            for (int v = 0; v < 6; ++v) {
-                cudaError_t e = cudaFuncSetAttribute(fns[m][v], cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-                if (e != cudaSuccess) return e;
-                cudaFuncSetAttribute(fns[m][v], cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-            }
+            for (int v = 0; v < 6; ++v)
+                if (cudaError_t e = big(fns[m][v]); e != cudaSuccess) return e;
+        for (int v = 0; v < 4; ++v)
+            if (cudaError_t e = big(mc_fns[v]); e != cudaSuccess) return e;
+        for (int v = 0; v < 3; ++v)
+            if (cudaError_t e = big(pair_fns[v]); e != cudaSuccess) return e;
         for (int v = 0; v < 4; ++v) {
             cudaError_t e = cudaFuncSetAttribute(small_fns[v], cudaFuncAttributeMaxDynamicSharedMemorySize, 113 * 1024);
             if (e != cudaSuccess) return e;
@@ -854,17 +942,28 @@ cudaError_t launch_conv_halo(const HaloArgs &a, const CUtensorMap &tmA, const CU
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
     attr[1].id = cudaLaunchAttributeClusterDimension;
-    attr[1].val.clusterDim.x = a.bmc;
+    attr[1].val.clusterDim.x = a.pair ? 2 : a.bmc;
     attr[1].val.clusterDim.y = 1;
     attr[1].val.clusterDim.z = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = a.bmc > 1 ? 2 : 1;
+    cfg.numAttrs = (a.bmc > 1 || a.pair) ? 2 : 1;
     if (a.bmc > 1 && (grid % a.bmc || a.m_tiles % a.bmc || a.stationary || a.small)) return cudaErrorInvalidValue;
+    if (a.pair && (grid % 2 || a.m_tiles % 2 || a.stationary || a.small || a.bmc > 1 || a.kw_fuse != 3 || a.stride2 ||
+                   a.x3 || a.n_tile % 16))
+        return cudaErrorInvalidValue;
     const bool narrow = a.ck != kChunk || a.co_chunk != kChunk;
     const int var = a.stride2 ? 3 : (a.x3 == 1 ? 4 : (a.x3 == 2 ? 5 : (a.epi == EPI_BN_PROJ_RELU ? 1 : (a.pool_out ? 2 : 0))));
     if (a.small) {
-        if (var > 3) return cudaErrorInvalidValue;
+        if (var > 3 || a.bmc > 1 || a.pair) return cudaErrorInvalidValue;
         return cudaLaunchKernelEx(&cfg, small_fns[var], tmA, tmB, tmRes, tmOut, tmA1, tmB1, tmBh, a);
+    }
+    if (a.pair) {
+        if (narrow || var > 2) return cudaErrorInvalidValue;
+        return cudaLaunchKernelEx(&cfg, pair_fns[var], tmA, tmB, tmRes, tmOut, tmA1, tmB1, tmBh, a);
+    }
+    if (a.bmc > 1) {
+        if (narrow || var > 3) return cudaErrorInvalidValue;
+        return cudaLaunchKernelEx(&cfg, mc_fns[var], tmA, tmB, tmRes, tmOut, tmA1, tmB1, tmBh, a);
     }
     return cudaLaunchKernelEx(&cfg, fns[narrow ? 1 : 0][var], tmA, tmB, tmRes, tmOut, tmA1, tmB1, tmBh, a);
 }

@@ -601,6 +601,19 @@ slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, i
     } else {
         a.b_bytes = r1k(3u * a.n_tile * a.rbk);
     }
+    // 2-SM MMA (cta_group::2, kernels_halo.cu): a CTA pair on consecutive M tiles of one N tile, one
+    // M = 256 MMA per k-step, each CTA holding half of every B stage -- the layer's weight bytes from L2
+    // and into each SM halve (streamed-weight layers: segments 1-3 at the wide widths).  SLIM_HALO_PAIR=0
+    // turns it off (A/B).
+    static const int pair_env = getenv("SLIM_HALO_PAIR") ? atoi(getenv("SLIM_HALO_PAIR")) : 0;
+    const bool wide_boxes = a.ck == kChunk && a.co_chunk == kChunk;   // (the cluster variants are compiled for these)
+    const bool pair = pair_env != 0 && wide_boxes && !a.stationary && !small && !a.x3 && !s2 && a.kw_fuse == 3 && a.m_tiles % 2 == 0 &&
+                      a.n_tile % 16 == 0 && !a.gn_part &&
+                      grid_cap(ctx, ri, std::min(ctx->num_sms, a.m_tiles * a.n_tiles), cc.seg) >= 2;
+    if (pair) {
+        a.pair = 1;
+        a.b_bytes = r1k(3u * (a.n_tile / 2) * a.rbk);
+    }
     // fit: A slots 2..4, B slots 2..4 (streaming), residual slots 2 -> 1 if tight
     for (;;) {
         const size_t res = chunk * a.res_slots;
@@ -631,7 +644,7 @@ slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, i
             a.sa = 2;
             left -= 2 * a.a_slot;
             a.sb = static_cast<int>(left / a.b_bytes);
-            a.sb = a.sb > 4 ? 4 : a.sb;
+            a.sb = a.sb > 4 ? 4 : a.sb;   // (the kernel has 4 barrier slots per ring)
             if (a.sb >= 4 && left - 4 * a.b_bytes >= a.a_slot) a.sa = 3;
         }
         break;
@@ -674,6 +687,7 @@ slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, i
     int grid = ctx->num_sms * (two ? 2 : 1);
     if (grid > total) grid = total;
     grid = grid_cap(ctx, ri, grid, cc.seg);
+    if (a.pair) grid -= grid % 2;   // (>= 2: checked with the pair decision)
     // streamed weights: clusters of bmc CTAs on consecutive M tiles of one N tile share each B stage
     // (TMA multicast) -- the weight bytes one launch pulls from L2 drop by bmc.  Opt-in (SLIM_HALO_BMC=2|4):
     // bit-identical, but measured no faster (B=1024 r=1 seg 2/3 convs 84/80 us either way; B=128 chains
@@ -682,7 +696,10 @@ slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, i
     static const int bmc_env = getenv("SLIM_HALO_BMC") ? atoi(getenv("SLIM_HALO_BMC")) : 1;
     a.bmc = 1;
     CUtensorMap tBh = tA;
-    if ((bmc_env == 2 || bmc_env == 4) && !a.stationary && !small && !a.x3 && a.m_tiles % bmc_env == 0 &&
+    if (a.pair) {
+        if (!encode_w_taps(ctx, &tBh, L, cc.c_in, c_out, a.n_tile / 2, 1, a.ck))
+            return fail(ctx, SLIM_ECUDA, "cuTensorMapEncodeTiled(halo W pair half) failed");
+    } else if ((bmc_env == 2 || bmc_env == 4) && wide_boxes && !a.stationary && !small && !a.x3 && a.m_tiles % bmc_env == 0 &&
         (a.n_tile / bmc_env) % 8 == 0 && grid >= bmc_env) {
         if (!encode_w_taps(ctx, &tBh, L, cc.c_in, c_out, a.n_tile / bmc_env, 1, a.ck))
             return fail(ctx, SLIM_ECUDA, "cuTensorMapEncodeTiled(halo W share) failed");
@@ -698,7 +715,7 @@ slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, i
     if (proj) {
         if (!encode_act_rowmajor(ctx, &tA1, cc.xp, B, cc.Hp, cc.Wp, cc.c_in_p, a.tile_imgs, a.rows, kChunk, 2))
             return fail(ctx, SLIM_ECUDA, "cuTensorMapEncodeTiled(halo proj A) failed");
-        if (!encode_w(ctx, &tB1, *cc.Lp, cc.c_in_p, c_out, a.n_tile, kChunk))
+        if (!encode_w(ctx, &tB1, *cc.Lp, cc.c_in_p, c_out, a.pair ? a.n_tile / 2 : a.n_tile, kChunk))
             return fail(ctx, SLIM_ECUDA, "cuTensorMapEncodeTiled(halo proj W) failed");
     }
     cudaError_t e = launch_conv_halo(a, tA, *tB, tRes, tOut, tA1, tB1, tBh, grid, st, ctx->pdl && !ctx->prof_on);

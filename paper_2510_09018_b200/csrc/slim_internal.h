@@ -127,6 +127,11 @@ struct HaloArgs {
     // N tile; each CTA loads 1/bmc of every B stage (rows rank*n_tile/bmc.., tmBh: box [ck, n_tile/bmc, 1])
     // and multicasts it to all, so the cluster reads each weight byte from L2 once instead of bmc times
     int bmc;
+    // 2-SM MMA (cta_group::2): a CTA pair (cluster of 2) on consecutive M tiles of one N tile issues ONE
+    // M = 256 MMA from the even CTA; each CTA loads its own A tile and HALF of every B stage (1.5 n_tile
+    // rows, tmBh: box [ck, n_tile/2, 1]), so the pair pulls each weight byte from L2 once and each SM
+    // ingests half of it.  Needs streamed B, kw_fuse == 3, bmc == 1.
+    int pair;
 };
 size_t conv_halo_smem_bytes(const HaloArgs &a);
 cudaError_t launch_conv_halo(const HaloArgs &a, const CUtensorMap &tmA, const CUtensorMap &tmB,

@@ -380,11 +380,9 @@ def test_cluster_multicast_path_parity(params, ref):
     assert float(out.stdout.strip().splitlines()[-1]) <= TAU_BF16
 
 
-@pytest.mark.parametrize("bmc", [2, 4])
-def test_halo_weight_multicast_bitwise(bmc, tmp_path):
-    """Streamed-weight multicast (clusters of bmc CTAs share each B stage, SLIM_HALO_BMC): every
-    segment 1-3 output for all (r_prev, r) at B = 13 and 64 is bitwise the unclustered kernel's (same
-    MMA order; only who loads the weights changes), and the oracle agrees on a sample."""
+def _seg123_outputs_under_env(tmp_path, variants):
+    """Every segment 1-3 output for all (r_prev, r) at B = 13 and 64 (per-layer kernels), once per env
+    variant, each run in its own process (the knobs are read once); the oracle checks a sample."""
     import subprocess, sys, os
     code = (
         "import sys, numpy as np, torch, synth, oracle, paper_2510_09018_b200 as slim\n"
@@ -409,16 +407,36 @@ def test_halo_weight_multicast_bitwise(bmc, tmp_path):
         "np.savez(sys.argv[1], **outs)\n"
     )
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    res = {}
-    for m in (1, bmc):
-        f = str(tmp_path / f"bmc{m}.npz")
-        env = dict(os.environ, SLIM_HALO_BMC=str(m), SLIM_NO_FUSED="1")
+    res = []
+    for i, var in enumerate(variants):
+        f = str(tmp_path / f"v{i}.npz")
+        env = dict(os.environ, SLIM_NO_FUSED="1", **var)
         out = subprocess.run([sys.executable, "-c", code, f], env=env, capture_output=True, text=True, timeout=600,
                              cwd=root)
         assert out.returncode == 0, out.stderr[-2000:]
-        res[m] = np.load(f)
-    for k in res[1].files:
-        assert np.array_equal(res[1][k], res[bmc][k]), k
+        res.append(np.load(f))
+    return res
+
+
+@pytest.mark.parametrize("bmc", [2, 4])
+def test_halo_weight_multicast_bitwise(bmc, tmp_path):
+    """Streamed-weight multicast (clusters of bmc CTAs share each B stage, SLIM_HALO_BMC): every
+    segment 1-3 output for all (r_prev, r) at B = 13 and 64 is bitwise the unclustered kernel's (same
+    MMA order; only who loads the weights changes), and the oracle agrees on a sample."""
+    base, mc = _seg123_outputs_under_env(tmp_path, [dict(SLIM_HALO_BMC="1", SLIM_HALO_PAIR="0"),
+                                                    dict(SLIM_HALO_BMC=str(bmc), SLIM_HALO_PAIR="0")])
+    for k in base.files:
+        assert np.array_equal(base[k], mc[k]), k
+
+
+def test_halo_pair_mma_bitwise(tmp_path):
+    """2-SM MMA (cta_group::2, SLIM_HALO_PAIR): a CTA pair issues one M = 256 MMA per k-step with each
+    CTA holding half of every weight stage.  Every segment 1-3 output for all (r_prev, r) at B = 13 and
+    64 is bitwise the one-CTA kernel's (each output row's K order is unchanged), and the oracle agrees
+    on a sample -- so the choice cannot break batch independence."""
+    one, two = _seg123_outputs_under_env(tmp_path, [dict(SLIM_HALO_PAIR="0"), dict(SLIM_HALO_PAIR="1")])
+    for k in one.files:
+        assert np.array_equal(one[k], two[k]), k
 
 
 def test_splitk_cluster_path_parity():
