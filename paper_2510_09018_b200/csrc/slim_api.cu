@@ -1293,7 +1293,18 @@ slim_status run_segment(slim_ctx *ctx, int seg, int ri_prev, int ri, int B, cons
     // 1 = fused and capped to the share, 2 = fused and uncapped.
     static const int fused_part = getenv("SLIM_FUSED_PART") ? atoi(getenv("SLIM_FUSED_PART")) : 0;
     const bool partitioned = grid_cap(ctx, ri, ctx->num_sms, seg) < ctx->num_sms;
-    const bool fused_on = ((fused_env >> seg) & 1) != 0 && !(partitioned && fused_part == 0);
+    // Large batches (BN mode): a fused unit is a per-CTA latency chain, so once the units fill the SMs
+    // several times over the per-layer kernels' throughput wins (profiles/r02_fused_thresh.txt, each
+    // width alone): seg 1 C <= 32 fused up to B = 1024, C = 64 up to 192; seg 2 C <= 64 up to 512,
+    // C = 128 up to 128; seg 3 up to 256.  Both paths are bit-identical, so this is a pure speed choice.
+    // SLIM_FUSED_BMAX (A/B) overrides the limit for every segment (0 = no limit).
+    static const int bmax_env = getenv("SLIM_FUSED_BMAX") ? atoi(getenv("SLIM_FUSED_BMAX")) : -1;
+    const int fused_bmax = bmax_env >= 0 ? (bmax_env ? bmax_env : (1 << 30))
+                           : gn ? (1 << 30)
+                           : seg == 1 ? (C <= 32 ? 1024 : 192)
+                           : seg == 2 ? (C <= 64 ? 512 : 128)
+                                      : 256;
+    const bool fused_on = ((fused_env >> seg) & 1) != 0 && !(partitioned && fused_part == 0) && B <= fused_bmax;
     // GroupNorm: the kernel's two-pass statistics (per image and 16-channel group), same condition
     if (seg > 0 && bf && (!gn || !no_fused_gn) && !no_fused && fused_on && S.fimg[ri_prev][ri]) {
         FusedSegArgs fa{};
