@@ -90,15 +90,16 @@ __global__ void __launch_bounds__(kSmall ? kHaloThreadsSmall : kHaloThreads, kSm
     uint64_t *bars = reinterpret_cast<uint64_t *>(sBN + (proj ? 4 : 2) * a.c_out);
     const uint32_t bar0 = smem_u32(bars);
     // barriers: a_full[4] a_empty[4] b_full[4] b_empty[4] t_full[4] t_empty[4] r_full[4] r_empty[4]
+    // (the B ring has up to kMaxSB slots: the pair variant's half stages are deeper in flight)
     auto a_full = [&](int i) { return bar0 + 8u * i; };
     auto a_empty = [&](int i) { return bar0 + 8u * (4 + i); };
     auto b_full = [&](int i) { return bar0 + 8u * (8 + i); };
-    auto b_empty = [&](int i) { return bar0 + 8u * (12 + i); };
-    auto t_full = [&](int i) { return bar0 + 8u * (16 + i); };
-    auto t_empty = [&](int i) { return bar0 + 8u * (20 + i); };
-    auto r_full = [&](int i) { return bar0 + 8u * (24 + i); };
-    auto r_empty = [&](int i) { return bar0 + 8u * (28 + i); };
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 32);
+    auto b_empty = [&](int i) { return bar0 + 8u * (8 + kMaxSB + i); };
+    auto t_full = [&](int i) { return bar0 + 8u * (8 + 2 * kMaxSB + i); };
+    auto t_empty = [&](int i) { return bar0 + 8u * (12 + 2 * kMaxSB + i); };
+    auto r_full = [&](int i) { return bar0 + 8u * (16 + 2 * kMaxSB + i); };
+    auto r_empty = [&](int i) { return bar0 + 8u * (20 + 2 * kMaxSB + i); };
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + kHaloBars);
     // GroupNorm statistics partials (a.gn_part): [tile group][16-ch group of the tile][lane quarter][image]
     float4 *sGN = reinterpret_cast<float4 *>((reinterpret_cast<uintptr_t>(tmem_slot + 4) + 15) & ~uintptr_t(15));
     const int gn_ng = a.n_tile / 16, gn_ni = a.tile_imgs;
@@ -121,6 +122,8 @@ __global__ void __launch_bounds__(kSmall ? kHaloThreadsSmall : kHaloThreads, kSm
         for (int i = 0; i < 4; ++i) {
             mbar_init(a_full(i), 1);
             mbar_init(a_empty(i), 1);
+        }
+        for (int i = 0; i < kMaxSB; ++i) {
             mbar_init(b_full(i), 1);
             mbar_init(b_empty(i), kClu == 1 ? a.bmc : 1);   // B multicast: every CTA of the cluster frees the slot
         }
@@ -213,7 +216,7 @@ __global__ void __launch_bounds__(kSmall ? kHaloThreadsSmall : kHaloThreads, kSm
                     } else if (pair) {   // own tile's halo; the leader's a_full counts both CTAs' bytes
                         mbar_wait(a_empty(s), ph ^ 1);
                         const uint32_t lb = mapa_u32(a_full(s), 0);
-                        if (leader_cta) mbar_expect_tx_cluster(lb, 2u * a.a_bytes);
+                        if (leader_cta) mbar_expect_tx(a_full(s), 2u * a.a_bytes);
                         tma_load_4d_pair(sA + s * a.a_slot, &tmA, lb, ch * CK, 0, n * a.tile_imgs, h0 - 1);
                     } else {
                         mbar_wait(a_empty(s), ph ^ 1);
@@ -255,7 +258,7 @@ __global__ void __launch_bounds__(kSmall ? kHaloThreadsSmall : kHaloThreads, kSm
                     mbar_wait(a_empty(s), ph ^ 1);
                     if (pair) {   // own 128 px + HALF of the 1x1 weights (tmB1 box: n_tile/2 rows)
                         const uint32_t lb = mapa_u32(a_full(s), 0);
-                        if (leader_cta) mbar_expect_tx_cluster(lb, 2u * 16384u + static_cast<uint32_t>(a.n_tile) * 128u);
+                        if (leader_cta) mbar_expect_tx(a_full(s), 2u * 16384u + static_cast<uint32_t>(a.n_tile) * 128u);
                         tma_load_4d_pair(sA + s * a.a_slot, &tmA1, lb, cp * kChunk, 0, n * a.tile_imgs, 2 * h0);
                         tma_load_3d_pair(sA + s * a.a_slot + 16384u, &tmB1, lb, cp * kChunk, 0,
                                          co0 + static_cast<int>(prank) * (a.n_tile / 2));
@@ -317,16 +320,13 @@ __global__ void __launch_bounds__(kSmall ? kHaloThreadsSmall : kHaloThreads, kSm
                         const int kh = s2 ? (kq == 0 ? 0 : (kq == 1 ? 2 : 1)) : kq;   // s2 consumes kh 0, 2, 1
                         mbar_wait(b_empty(s), ph ^ 1);
                         if (pair) {
-                            // this CTA's half of the stage: rows [rank*1.5n, (rank+1)*1.5n) of the three adjacent
-                            // tap blocks = three half-blocks j = 3*rank + i (tap j/2, rows (j%2)*n/2 ..)
+                            // the pair MMA's N = 3n rows are ordered [kw0 | kw1 | kw2 of channels 0..n/2) then
+                            // [kw0 | kw1 | kw2 of channels n/2..n): this CTA's half is ONE box [ck, n/2, 3 taps]
+                            // (the epilogue reads the accumulators in that column order)
                             const uint32_t lb = mapa_u32(b_full(s), 0);
-                            if (leader_cta) mbar_expect_tx_cluster(lb, 3u * a.n_tile * RBK);
-                            const uint32_t hb = static_cast<uint32_t>(a.n_tile / 2) * RBK;
-                            for (int i = 0; i < 3; ++i) {
-                                const int j = 3 * static_cast<int>(prank) + i;
-                                tma_load_3d_pair(sB + s * a.b_bytes + i * hb, &tmBh, lb, ch * CK,
-                                                 co0 + (j & 1) * (a.n_tile / 2), kh * 3 + (j >> 1));
-                            }
+                            if (leader_cta) mbar_expect_tx(b_full(s), 3u * a.n_tile * RBK);
+                            tma_load_3d_pair(sB + s * a.b_bytes, &tmBh, lb, ch * CK,
+                                             co0 + static_cast<int>(prank) * (a.n_tile / 2), kh * 3);
                             if (++s == a.sb) {
                                 s = 0;
                                 ph ^= 1;
@@ -669,11 +669,15 @@ __global__ void __launch_bounds__(kSmall ? kHaloThreadsSmall : kHaloThreads, kSm
             const uint32_t col0 = static_cast<uint32_t>(as * a.stage_cols);
             for (int g = g0; g < a.n_tile / 16 && !(a.debug & 16); g += gstep) {
                 uint32_t v0[16], v1[16], v2[16];
-                tmem_ld16(lane_addr + col0 + g * 16, v0);
+                // kw accumulator columns of channels g*16..: pair mode interleaves the two channel halves
+                // ([kw0 kw1 kw2] of the first n/2 channels, then of the second), else kw * acc_stride + channel
+                const int hn = pair ? a.n_tile / 2 : a.acc_stride;
+                const uint32_t cb = col0 + static_cast<uint32_t>(pair ? (g * 16 / hn) * 3 * hn + (g * 16) % hn : g * 16);
+                tmem_ld16(lane_addr + cb, v0);
                 if (x2) tmem_ld16(lane_addr + col0 + a.acc_stride + g * 16, v2);   // acc_m, acc_2
                 if (!x3 && !x2) {
-                    tmem_ld16(lane_addr + col0 + a.acc_stride + g * 16, v1);
-                    tmem_ld16(lane_addr + col0 + 2 * a.acc_stride + g * 16, v2);
+                    tmem_ld16(lane_addr + cb + hn, v1);
+                    tmem_ld16(lane_addr + cb + 2 * hn, v2);
                 }
                 tmem_wait_ld();
                 reg_fence16(v0);
@@ -892,7 +896,7 @@ size_t conv_halo_smem_bytes(const HaloArgs &a) {
     const int n_res = (a.epi == EPI_BN_ADD_RELU) ? a.res_slots : 0;
     return 1024 + static_cast<size_t>(a.sa) * a.a_slot + static_cast<size_t>(a.sb) * a.b_bytes +
            chunk * (a.epi_groups + n_res) +
-           (a.epi == EPI_BN_PROJ_RELU ? 16 : 8) * static_cast<size_t>(a.c_out) + 8 * 32 + 16 +
+           (a.epi == EPI_BN_PROJ_RELU ? 16 : 8) * static_cast<size_t>(a.c_out) + 8 * kHaloBars + 16 +
            (a.gn_part ? static_cast<size_t>(a.epi_groups) * (a.n_tile / 16) * 4 * a.tile_imgs * 16 + 16 : 0);
 }
 

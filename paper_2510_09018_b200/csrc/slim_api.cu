@@ -490,6 +490,16 @@ slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, i
         nt = c_out / splitn;
         narrow_out = true;
     }
+    // Widths whose channel count is not a multiple of 64 above 64 (r = 0.75: 96 at segment 1): one N
+    // tile of 96 gives 3 x 96 accumulator columns, so only ONE accumulator stage fits TMEM and the MMA
+    // of tile i+1 cannot overlap the epilogue of tile i.  Narrower N tiles with exact-width output boxes
+    // restore 2-4 stages.  SLIM_HALO_SPLITW = 0 (off) | 32 | 48 (A/B).
+    static const int splitw_env = getenv("SLIM_HALO_SPLITW") ? atoi(getenv("SLIM_HALO_SPLITW")) : 0;
+    if (!narrow_out && nt == 1 && 3 * c_out > 256 && c_out % 64 && splitw_env > 0 && c_out % splitw_env == 0 &&
+        splitw_env % 16 == 0) {
+        nt = c_out / splitw_env;
+        narrow_out = true;
+    }
     // (the SMs to fill are this width's share when instances are partitioned, slim_set_sm_share)
     const int fill_sms = grid_cap(ctx, ri, ctx->num_sms, cc.seg);
     if (!no_fill && a.m_tiles * nt * 10 < fill_sms * 8 && !cc.pool_out)
@@ -515,7 +525,9 @@ slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, i
     a.ck = proj ? kChunk : hch(cc.c_in);
     a.rbk = 2 * a.ck;
     a.n_chunks = (cc.c_in + a.ck - 1) / a.ck;
-    a.co_chunk = narrow_out ? a.n_tile : hch(a.n_tile);
+    // exact-width output boxes: the widest 64 / 32 / 16-channel box dividing the tile (a 48-channel tile
+    // stores three 16-channel boxes: the staging rows must be a swizzle span of 32, 64 or 128 B)
+    a.co_chunk = narrow_out ? (a.n_tile % 64 == 0 ? 64 : (a.n_tile % 32 == 0 ? 32 : 16)) : hch(a.n_tile);
     a.rbo = 2 * a.co_chunk;
     a.epi = cc.epi;
     a.scale = L.scale[ri];
@@ -587,7 +599,7 @@ slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, i
     static const bool no_gn_part = getenv("SLIM_GN_PART") == nullptr || getenv("SLIM_GN_NO_PART") != nullptr;
     a.gn_part = (cc.gn_part && !no_gn_part && !proj && !cc.pool_out && !small && !a.x3) ? cc.gn_part : nullptr;
     auto fixed0 = [&]() {
-        return 1024 + chunk * a.epi_groups + (proj ? 16 : 8) * static_cast<size_t>(c_out) + 8 * 32 + 16 +
+        return 1024 + chunk * a.epi_groups + (proj ? 16 : 8) * static_cast<size_t>(c_out) + 8 * kHaloBars + 16 +
                (a.gn_part ? static_cast<size_t>(a.epi_groups) * (a.n_tile / 16) * 4 * a.tile_imgs * 16 + 16 : 0);
     };
     auto r1k = [](uint32_t x) { return (x + 1023u) & ~1023u; };
@@ -644,8 +656,9 @@ slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, i
             a.sa = 2;
             left -= 2 * a.a_slot;
             a.sb = static_cast<int>(left / a.b_bytes);
-            a.sb = a.sb > 4 ? 4 : a.sb;   // (the kernel has 4 barrier slots per ring)
-            if (a.sb >= 4 && left - 4 * a.b_bytes >= a.a_slot) a.sa = 3;
+            const int sb_max = a.pair ? kMaxSB : 4;   // pair: half-size stages, twice as many in flight
+            a.sb = a.sb > sb_max ? sb_max : a.sb;
+            if (a.sb >= 4 && left - a.sb * a.b_bytes >= a.a_slot) a.sa = 3;
         }
         break;
     }
@@ -697,7 +710,7 @@ slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, i
     a.bmc = 1;
     CUtensorMap tBh = tA;
     if (a.pair) {
-        if (!encode_w_taps(ctx, &tBh, L, cc.c_in, c_out, a.n_tile / 2, 1, a.ck))
+        if (!encode_w_taps(ctx, &tBh, L, cc.c_in, c_out, a.n_tile / 2, 3, a.ck))
             return fail(ctx, SLIM_ECUDA, "cuTensorMapEncodeTiled(halo W pair half) failed");
     } else if ((bmc_env == 2 || bmc_env == 4) && wide_boxes && !a.stationary && !small && !a.x3 && a.m_tiles % bmc_env == 0 &&
         (a.n_tile / bmc_env) % 8 == 0 && grid >= bmc_env) {

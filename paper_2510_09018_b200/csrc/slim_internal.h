@@ -133,6 +133,8 @@ struct HaloArgs {
     // ingests half of it.  Needs streamed B, kw_fuse == 3, bmc == 1.
     int pair;
 };
+constexpr int kMaxSB = 8;                    // halo kernel: B ring slots (barrier pairs) at most
+constexpr int kHaloBars = 24 + 2 * kMaxSB;   // a_full/empty[4] b_full/empty[kMaxSB] t_full/empty[4] r_full/empty[4]
 size_t conv_halo_smem_bytes(const HaloArgs &a);
 cudaError_t launch_conv_halo(const HaloArgs &a, const CUtensorMap &tmA, const CUtensorMap &tmB,
                              const CUtensorMap &tmRes, const CUtensorMap &tmOut, const CUtensorMap &tmA1,

@@ -23,10 +23,10 @@ __device__ __forceinline__ uint32_t elect_one() {
     return pred;
 }
 template <int PAIR>
-__global__ void mma_rate(int n_iter, int N, unsigned long long *out) {
+__global__ void mma_rate(int n_iter, int N, int commit_every_kh, unsigned long long *out) {
     extern __shared__ __align__(1024) uint8_t sm[];
     uint8_t *s = (uint8_t *)(((uintptr_t)sm + 1023) & ~(uintptr_t)1023);
-    __shared__ uint64_t bar;
+    __shared__ uint64_t bar, dummy;
     __shared__ uint32_t tslot;
     uint32_t rank = 0;
     if (PAIR) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
@@ -39,7 +39,11 @@ __global__ void mma_rate(int n_iter, int N, unsigned long long *out) {
             asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
         }
     }
-    if (threadIdx.x == 0) { asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar))); asm volatile("fence.mbarrier_init.release.cluster;"); }
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1000000;" ::"r"(smem_u32(&dummy)));   // never completes
+        asm volatile("fence.mbarrier_init.release.cluster;");
+    }
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
     if (PAIR) asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
@@ -52,7 +56,7 @@ __global__ void mma_rate(int n_iter, int N, unsigned long long *out) {
         for (int it = 0; it < n_iter; ++it) {
             if (elect_one()) {
 #pragma unroll
-                for (int kh = 0; kh < 3; ++kh)
+                for (int kh = 0; kh < 3; ++kh) {
 #pragma unroll
                     for (int kk = 0; kk < 4; ++kk) {
                         const uint32_t acc = (it | kh | kk) != 0;
@@ -61,6 +65,11 @@ __global__ void mma_rate(int n_iter, int N, unsigned long long *out) {
                         else
                             asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(tm), "l"(ad + kh * 256 + 2 * kk), "l"(bd + 2 * kk), "r"(idesc), "r"(acc));
                     }
+                    if (commit_every_kh) {   // a per-stage release, as a streamed-weight ring does
+                        if (PAIR) asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(smem_u32(&dummy)), "h"((uint16_t)3));
+                        else asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&dummy)));
+                    }
+                }
             }
             __syncwarp();
         }
@@ -91,6 +100,7 @@ int main() {
     CK(cudaFuncSetAttribute(mma_rate<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 140000));
     CK(cudaFuncSetAttribute(mma_rate<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 140000));
     const int iters = 200;
+    for (int ce : {0, 1})
     for (int N : {64, 128, 192, 256}) {
         for (int pair = 0; pair < 2; ++pair) {
             cudaLaunchConfig_t cfg{};
@@ -105,15 +115,15 @@ int main() {
             cfg.attrs = at;
             cfg.numAttrs = 1;
             for (int rep = 0; rep < 2; ++rep) {
-                if (pair) CK(cudaLaunchKernelEx(&cfg, mma_rate<1>, iters, N, d_out));
-                else CK(cudaLaunchKernelEx(&cfg, mma_rate<0>, iters, N, d_out));
+                if (pair) CK(cudaLaunchKernelEx(&cfg, mma_rate<1>, iters, N, ce, d_out));
+                else CK(cudaLaunchKernelEx(&cfg, mma_rate<0>, iters, N, ce, d_out));
             }
             CK(cudaDeviceSynchronize());
             CK(cudaMemcpy(h.data(), d_out, sms * 8, cudaMemcpyDeviceToHost));
             const double cyc = (double)h[0] / (iters * 12);
             // per-SM work per instruction: 128 x N x 16 MACs either way
-            printf("%s N=%3d: %.1f cycles per MMA instruction (floor 128*N/256 = %d per SM)\n",
-                   pair ? "pair M=256 (cta_group::2)" : "one  M=128 (cta_group::1)", N, cyc, 128 * N / 256);
+            printf("%s commit/4 MMAs=%d N=%3d: %.1f cycles per MMA instruction (floor 128*N/256 = %d per SM)\n",
+                   pair ? "pair M=256 (cta_group::2)" : "one  M=128 (cta_group::1)", ce, N, cyc, 128 * N / 256);
         }
     }
     return 0;
