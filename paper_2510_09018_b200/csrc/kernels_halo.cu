@@ -45,7 +45,10 @@ constexpr int kHaloThreadsSmall = (4 + 8) * 32;
 // (compile-time, so the common variant carries none of the other two's code)
 // kClu: 0 = one CTA per tile (no cluster instructions compiled in: a kernel holding cta_group::2 /
 // multicast code must be launched as a cluster), 1 = streamed-weight multicast (a.bmc), 2 = 2-SM pair
-template <bool kNarrow, int kVar, bool kSmall = false, int kClu = 0>
+// kGN: GroupNorm in the epilogue for layers whose tile covers whole images (segments 2-3):
+// pass 1 reduces each (image, 16-channel group)'s statistics from the TMEM-resident fp32 accumulators,
+// pass 2 normalises (y*A + Bc, A = rstd*gamma, Bc = beta - mean*A) in place of the BN affine
+template <bool kNarrow, int kVar, bool kSmall = false, int kClu = 0, bool kGN = false>
 __global__ void __launch_bounds__(kSmall ? kHaloThreadsSmall : kHaloThreads, kSmall ? 2 : 1)
     conv_halo_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmRes, const __grid_constant__ CUtensorMap tmOut,
@@ -667,6 +670,91 @@ __global__ void __launch_bounds__(kSmall ? kHaloThreadsSmall : kHaloThreads, kSm
             if (leader) TD(2, ti, 2);
             const uint8_t *resp = pRes + rs * chunk_bytes;
             const uint32_t col0 = static_cast<uint32_t>(as * a.stage_cols);
+            // GN statistics partials of this tile group: [g][lane quarter][image] (then the projection's)
+            float4 *sG = kGN ? sGN + static_cast<size_t>(grp) * gn_ng * 4 * gn_ni * (proj ? 2 : 1) : nullptr;
+            if constexpr (kGN) {
+                // (K, S1, S2) of this thread's 16 values shifted by K = the image's first lane's first value
+                // (keeps the sums of squares from cancelling), summed over the warp's lanes of the same image
+                // in a fixed butterfly, parked per (g, quarter, image); merged in pass 2
+                auto park = [&](const float (&y)[16], float4 *dst) {
+                    const float K = __shfl_sync(0xffffffffu, y[0], ((lane % a.row_px) / a.W) * a.W);
+                    const unsigned long long K2 = f2pk(-K, -K);
+                    unsigned long long s1 = 0ull, s2q = 0ull;
+#pragma unroll
+                    for (int i = 0; i < 16; i += 2) {
+                        const unsigned long long d = fadd2(f2pk(y[i], y[i + 1]), K2);
+                        s1 = fadd2(s1, d);
+                        s2q = ffma2(d, d, s2q);
+                    }
+                    float a1, b1, a2, b2;
+                    f2upk(s1, a1, b1);
+                    f2upk(s2q, a2, b2);
+                    float S1 = a1 + b1, S2 = a2 + b2;
+                    for (int ofs = 1; ofs < 32; ofs <<= 1) {
+                        if (ofs >= a.W && ofs < a.row_px) continue;   // would mix images of the tile
+                        S1 += __shfl_xor_sync(0xffffffffu, S1, ofs);
+                        S2 += __shfl_xor_sync(0xffffffffu, S2, ofs);
+                    }
+                    if (lane < a.row_px && lane % a.W == 0) dst[lane / a.W] = make_float4(K, S1, S2, 0.f);
+                };
+                for (int g = g0; g < a.n_tile / 16; g += gstep) {
+                    uint32_t v0[16], v1[16], v2[16];
+                    tmem_ld16(lane_addr + col0 + g * 16, v0);
+                    tmem_ld16(lane_addr + col0 + a.acc_stride + g * 16, v1);
+                    tmem_ld16(lane_addr + col0 + 2 * a.acc_stride + g * 16, v2);
+                    tmem_wait_ld();
+                    reg_fence16(v0);
+                    reg_fence16(v1);
+                    reg_fence16(v2);
+                    float y[16];
+                    if (s2) {   // acc_kw0[w-1] + acc_kw2[w] + acc_kw1[w] (as in pass 2)
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) {
+                            const float left = __shfl_up_sync(0xffffffffu, __uint_as_float(v0[i]), 1);
+                            y[i] = fmaf(mL, left, __uint_as_float(v1[i]) + __uint_as_float(v2[i]));
+                        }
+                    } else {
+                        const unsigned long long mL2 = f2pk(mL, mL), mR2 = f2pk(mR, mR);
+#pragma unroll
+                        for (int i = 0; i < 16; i += 2) {
+                            const float l0 = __shfl_up_sync(0xffffffffu, __uint_as_float(v0[i]), 1);
+                            const float l1 = __shfl_up_sync(0xffffffffu, __uint_as_float(v0[i + 1]), 1);
+                            const float r0 = __shfl_down_sync(0xffffffffu, __uint_as_float(v2[i]), 1);
+                            const float r1 = __shfl_down_sync(0xffffffffu, __uint_as_float(v2[i + 1]), 1);
+                            f2upk(ffma2(mR2, f2pk(r0, r1),
+                                        ffma2(mL2, f2pk(l0, l1), f2pk(__uint_as_float(v1[i]), __uint_as_float(v1[i + 1])))),
+                                  y[i], y[i + 1]);
+                        }
+                    }
+                    park(y, sG + (g * 4 + q) * gn_ni);
+                    if (proj) {   // the projection shortcut's own GroupNorm statistics
+                        tmem_ld16(lane_addr + col0 + 3 * a.acc_stride + g * 16, v0);
+                        tmem_wait_ld();
+                        reg_fence16(v0);
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) y[i] = __uint_as_float(v0[i]);
+                        park(y, sG + (gn_ng + g) * 4 * gn_ni + q * gn_ni);
+                    }
+                }
+                named_bar_sync(1 + grp, gthreads);
+            }
+            // GN: (mean, rstd) of this thread's image for 16-channel group g from the four quarter partials
+            // (equal counts, fixed merge order: bitwise batch independent); base = the layer's or projection's
+            auto gn_stats = [&](int g, int base) {
+                const float4 *pq = sG + ((base + g) * 4) * gn_ni + (lane % a.row_px) / a.W;
+                const float cq = 16.f * 32.f * static_cast<float>(a.W) / static_cast<float>(a.row_px);
+                auto quarter = [&](const float4 v) {
+                    const float m = v.y / cq;
+                    return make_float2(v.x + m, fmaf(-v.y, m, v.z));
+                };
+                auto merge = [](float2 x, float2 y2, float c) {
+                    const float d = y2.x - x.x;
+                    return make_float2((x.x + y2.x) * 0.5f, (x.y + y2.y) + d * d * (c * 0.5f));
+                };
+                const float2 tot = merge(merge(quarter(pq[0]), quarter(pq[gn_ni]), cq),
+                                         merge(quarter(pq[2 * gn_ni]), quarter(pq[3 * gn_ni]), cq), 2.f * cq);
+                return make_float2(tot.x, rsqrtf(tot.y / (4.f * cq) + a.gn_eps));
+            };
             for (int g = g0; g < a.n_tile / 16 && !(a.debug & 16); g += gstep) {
                 uint32_t v0[16], v1[16], v2[16];
                 // kw accumulator columns of channels g*16..: pair mode interleaves the two channel halves
@@ -688,6 +776,18 @@ __global__ void __launch_bounds__(kSmall ? kHaloThreadsSmall : kHaloThreads, kSm
                 }
                 const int cl = g * 16, cg = co0 + cl;
                 float f[16];
+                // BN: per-channel scale / shift from smem; GN: per (image, channel) A = rstd*gamma, Bc = beta - mean*A
+                float gA[kGN ? 16 : 1], gB[kGN ? 16 : 1];
+                if constexpr (kGN) {
+                    const float2 ms = gn_stats(g, 0);
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        gA[i] = ms.y * s0[cg + i];
+                        gB[i] = fmaf(-ms.x, gA[i], t0[cg + i]);
+                    }
+                }
+                auto SC = [&](int i) { if constexpr (kGN) return make_float2(gA[i], gA[i + 1]); else return *reinterpret_cast<const float2 *>(s0 + cg + i); };
+                auto SH = [&](int i) { if constexpr (kGN) return make_float2(gB[i], gB[i + 1]); else return *reinterpret_cast<const float2 *>(t0 + cg + i); };
                 if (x2) {   // out[w] = acc_m[w] + acc_2[w+1], then BN (packed fp32x2)
                     const unsigned long long mR2 = f2pk(mR, mR);
 #pragma unroll
@@ -713,8 +813,8 @@ __global__ void __launch_bounds__(kSmall ? kHaloThreadsSmall : kHaloThreads, kSm
                         const float r1 = __shfl_down_sync(0xffffffffu, __uint_as_float(v2[i + 1]), 1);
                         const unsigned long long y = ffma2(
                             mR2, f2pk(r0, r1), ffma2(mL2, f2pk(l0, l1), f2pk(__uint_as_float(v1[i]), __uint_as_float(v1[i + 1]))));
-                        const float2 sc = *reinterpret_cast<const float2 *>(s0 + cg + i);
-                        const float2 sh = *reinterpret_cast<const float2 *>(t0 + cg + i);
+                        const float2 sc = SC(i);
+                        const float2 sh = SH(i);
                         f2upk(ffma2(y, f2pk(sc.x, sc.y), f2pk(sh.x, sh.y)), f[i], f[i + 1]);
                     }
                 }
@@ -732,17 +832,26 @@ __global__ void __launch_bounds__(kSmall ? kHaloThreadsSmall : kHaloThreads, kSm
                         const float right = __shfl_down_sync(0xffffffffu, __uint_as_float(v2[i]), 1);
                         y = fmaf(mR, right, fmaf(mL, left, __uint_as_float(v1[i])));
                     }
-                    f[i] = fmaf(y, s0[cg + i], t0[cg + i]);
+                    if constexpr (kGN) f[i] = fmaf(y, gA[i], gB[i]);
+                    else f[i] = fmaf(y, s0[cg + i], t0[cg + i]);
                 }
                 if (proj) {   // + s_sc * proj + t_sc (the shortcut's own BN)
                     tmem_ld16(lane_addr + col0 + 3 * a.acc_stride + g * 16, v0);
                     tmem_wait_ld();
                     reg_fence16(v0);
                     const float *s1 = sBN + 2 * a.c_out, *t1 = sBN + 3 * a.c_out;
+                    if constexpr (kGN) {   // the shortcut's GroupNorm: its own statistics, gamma / beta
+                        const float2 ms = gn_stats(g, gn_ng);
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) {
+                            gA[i] = ms.y * s1[cg + i];
+                            gB[i] = fmaf(-ms.x, gA[i], t1[cg + i]);
+                        }
+                    }
 #pragma unroll
                     for (int i = 0; i < 16; i += 2) {   // f + (s1 * p + t1), pairwise packed
-                        const float2 sc = *reinterpret_cast<const float2 *>(s1 + cg + i);
-                        const float2 sh = *reinterpret_cast<const float2 *>(t1 + cg + i);
+                        const float2 sc = kGN ? SC(i) : *reinterpret_cast<const float2 *>(s1 + cg + i);
+                        const float2 sh = kGN ? SH(i) : *reinterpret_cast<const float2 *>(t1 + cg + i);
                         const unsigned long long pr =
                             ffma2(f2pk(__uint_as_float(v0[i]), __uint_as_float(v0[i + 1])), f2pk(sc.x, sc.y),
                                   f2pk(sh.x, sh.y));
@@ -897,6 +1006,9 @@ size_t conv_halo_smem_bytes(const HaloArgs &a) {
     return 1024 + static_cast<size_t>(a.sa) * a.a_slot + static_cast<size_t>(a.sb) * a.b_bytes +
            chunk * (a.epi_groups + n_res) +
            (a.epi == EPI_BN_PROJ_RELU ? 16 : 8) * static_cast<size_t>(a.c_out) + 8 * kHaloBars + 16 +
+           (a.gn_fuse ? static_cast<size_t>(a.epi_groups) * (a.n_tile / 16) * 4 * a.tile_imgs * 16 *
+                            (a.epi == EPI_BN_PROJ_RELU ? 2 : 1) + 16
+                      : 0) +
            (a.gn_part ? static_cast<size_t>(a.epi_groups) * (a.n_tile / 16) * 4 * a.tile_imgs * 16 + 16 : 0);
 }
 
@@ -916,6 +1028,11 @@ cudaError_t launch_conv_halo(const HaloArgs &a, const CUtensorMap &tmA, const CU
                                  conv_halo_kernel<false, 2, false, 1>, conv_halo_kernel<false, 3, false, 1>};
     static const Fn pair_fns[3] = {conv_halo_kernel<false, 0, false, 2>, conv_halo_kernel<false, 1, false, 2>,
                                    conv_halo_kernel<false, 2, false, 2>};
+    // GroupNorm in the epilogue (whole-image tiles): plain / projection / pool / stride 2
+    static const Fn gn_fns[2][4] = {{conv_halo_kernel<false, 0, false, 0, true>, conv_halo_kernel<false, 1, false, 0, true>,
+                                     conv_halo_kernel<false, 2, false, 0, true>, conv_halo_kernel<false, 3, false, 0, true>},
+                                    {conv_halo_kernel<true, 0, false, 0, true>, conv_halo_kernel<true, 1, false, 0, true>,
+                                     conv_halo_kernel<true, 2, false, 0, true>, conv_halo_kernel<true, 3, false, 0, true>}};
     static bool attr_set = false;
     if (!attr_set) {
         auto big = [](Fn f) {
@@ -930,6 +1047,9 @@ cudaError_t launch_conv_halo(const HaloArgs &a, const CUtensorMap &tmA, const CU
             if (cudaError_t e = big(mc_fns[v]); e != cudaSuccess) return e;
         for (int v = 0; v < 3; ++v)
             if (cudaError_t e = big(pair_fns[v]); e != cudaSuccess) return e;
+        for (int m = 0; m < 2; ++m)
+            for (int v = 0; v < 4; ++v)
+                if (cudaError_t e = big(gn_fns[m][v]); e != cudaSuccess) return e;
         for (int v = 0; v < 4; ++v) {
             cudaError_t e = cudaFuncSetAttribute(small_fns[v], cudaFuncAttributeMaxDynamicSharedMemorySize, 113 * 1024);
             if (e != cudaSuccess) return e;
@@ -960,6 +1080,10 @@ cudaError_t launch_conv_halo(const HaloArgs &a, const CUtensorMap &tmA, const CU
     if (a.small) {
         if (var > 3 || a.bmc > 1 || a.pair) return cudaErrorInvalidValue;
         return cudaLaunchKernelEx(&cfg, small_fns[var], tmA, tmB, tmRes, tmOut, tmA1, tmB1, tmBh, a);
+    }
+    if (a.gn_fuse) {
+        if (var > 3 || a.pair || a.bmc > 1 || a.tiles_per_img != 1 || a.kw_fuse != 3 || a.gn_part) return cudaErrorInvalidValue;
+        return cudaLaunchKernelEx(&cfg, gn_fns[narrow ? 1 : 0][var], tmA, tmB, tmRes, tmOut, tmA1, tmB1, tmBh, a);
     }
     if (a.pair) {
         if (narrow || var > 2) return cudaErrorInvalidValue;

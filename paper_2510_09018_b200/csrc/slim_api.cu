@@ -370,6 +370,7 @@ struct ConvCall {
     int epi = EPI_BN_RELU;
     float relu_lo = 0.f;                     // -inf: no ReLU (GroupNorm mode: raw pre-norm output)
     float2 *gn_part = nullptr;               // GroupNorm mode: where the conv may write statistics partials
+    bool gn_fuse = false;                    // GroupNorm mode: normalise in the epilogue (halo, whole-image tiles)
     mutable bool gn_stats = false;           // set when the launched kernel wrote them (halo path)
     mutable int gn_tiles_per_img = 0;        // their tiling (partials per image per group)
 };
@@ -465,7 +466,7 @@ slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, i
     }
     a.row_px = a.tile_imgs * W;
     // fused pool: one image row per TMEM lane quarter (the 4x4 images of the last segment)
-    if (cc.pool_out && (a.tile_imgs == 1 || a.row_px != 32 || a.rows != 4)) return SLIM_EUNSUPPORTED;
+    if (cc.pool_out && (a.tile_imgs == 1 || a.row_px != 32 || a.rows != 4 || proj)) return SLIM_EUNSUPPORTED;   // (no pool + projection variant)
     a.pool_out = cc.pool_out;
     a.relu_lo = cc.relu_lo;
     // N tile <= 128: three accumulators of it must fit the 512 TMEM columns
@@ -532,6 +533,14 @@ slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, i
     a.epi = cc.epi;
     a.scale = L.scale[ri];
     a.shift = L.shift[ri];
+    if (cc.gn_fuse) {   // GroupNorm in the epilogue: the tile must hold whole images (their full statistics)
+        if (a.tiles_per_img != 1 || small) return SLIM_EUNSUPPORTED;
+        a.gn_fuse = 1;
+        a.gn_eps = c.bn_eps;
+        a.scale = L.gn_gamma[ri];
+        a.shift = L.gn_beta[ri];
+        a.relu_lo = 0.f;
+    }
     // kw taps share one MMA (N = k*n_tile <= 256, the three accumulators adjacent in TMEM, the
     // tap blocks of B adjacent in smem) unless SLIM_HALO_NOFUSE
     static const bool nofuse = getenv("SLIM_HALO_NOFUSE") != nullptr;
@@ -540,7 +549,7 @@ slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, i
     // single-chunk layers (seg 0); measured 15% slower there (3x A traffic, N=64 MMAs): SLIM_HALO_X3=1
     static const int x3_env = getenv("SLIM_HALO_X3") ? atoi(getenv("SLIM_HALO_X3")) : -1;
     // x2 (two boxes, two accumulators, 2/3 of the TMEM reads): SLIM_HALO_X3=2, measured 5% slower at seg 0
-    const bool xbox_ok = !small && !s2 && !proj && !cc.pool_out && cc.c_in <= kChunk && nt == 1 && 9 * a.n_tile * 128 <= 100 * 1024 &&
+    const bool xbox_ok = !a.gn_fuse && !small && !s2 && !proj && !cc.pool_out && cc.c_in <= kChunk && nt == 1 && 9 * a.n_tile * 128 <= 100 * 1024 &&
                          2 * a.n_tile <= 256;   // (weights stationary)
     const int xmode = !xbox_ok ? 0 : (x3_env >= 0 ? x3_env : 0);   // both measured slower than kw accumulators
     const bool x3 = xmode == 1, x2 = xmode == 2;
@@ -577,8 +586,8 @@ slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, i
 
     if (proj) {   // a projection chunk = 128 px x 64 ch + its n_tile x 64 weights in one slot
         if (a.ck != kChunk) return SLIM_EUNSUPPORTED;
-        a.scale1 = cc.Lp->scale[ri];
-        a.shift1 = cc.Lp->shift[ri];
+        a.scale1 = a.gn_fuse ? cc.Lp->gn_gamma[ri] : cc.Lp->scale[ri];
+        a.shift1 = a.gn_fuse ? cc.Lp->gn_beta[ri] : cc.Lp->shift[ri];
         a.c_in_p = cc.c_in_p;
         a.n_chunks_p = (cc.c_in_p + kChunk - 1) / kChunk;
         a.a_slot = std::max<uint32_t>(a.a_slot, 16384u + static_cast<uint32_t>(a.n_tile) * 128u);
@@ -597,10 +606,12 @@ slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, i
     // apply costs the same launch as the reduction kernel it replaces (GN CFG2 step 663 k vs 716 k images/s,
     // tools/gpu_runs/r02_gnpart.sh); kept as the measured alternative.
     static const bool no_gn_part = getenv("SLIM_GN_PART") == nullptr || getenv("SLIM_GN_NO_PART") != nullptr;
-    a.gn_part = (cc.gn_part && !no_gn_part && !proj && !cc.pool_out && !small && !a.x3) ? cc.gn_part : nullptr;
+    a.gn_part = (cc.gn_part && !no_gn_part && !proj && !cc.pool_out && !small && !a.x3 && !a.gn_fuse) ? cc.gn_part : nullptr;
     auto fixed0 = [&]() {
         return 1024 + chunk * a.epi_groups + (proj ? 16 : 8) * static_cast<size_t>(c_out) + 8 * kHaloBars + 16 +
-               (a.gn_part ? static_cast<size_t>(a.epi_groups) * (a.n_tile / 16) * 4 * a.tile_imgs * 16 + 16 : 0);
+               (a.gn_part ? static_cast<size_t>(a.epi_groups) * (a.n_tile / 16) * 4 * a.tile_imgs * 16 + 16 : 0) +
+               (a.gn_fuse ? static_cast<size_t>(a.epi_groups) * (a.n_tile / 16) * 4 * a.tile_imgs * 16 * (proj ? 2 : 1) + 16
+                          : 0);
     };
     auto r1k = [](uint32_t x) { return (x + 1023u) & ~1023u; };
     const uint32_t all_w = r1k(static_cast<uint32_t>(a.n_chunks) * 9u * a.n_tile * a.rbk);
@@ -619,7 +630,7 @@ slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, i
     // turns it off (A/B).
     static const int pair_env = getenv("SLIM_HALO_PAIR") ? atoi(getenv("SLIM_HALO_PAIR")) : 0;
     const bool wide_boxes = a.ck == kChunk && a.co_chunk == kChunk;   // (the cluster variants are compiled for these)
-    const bool pair = pair_env != 0 && wide_boxes && !a.stationary && !small && !a.x3 && !s2 && a.kw_fuse == 3 && a.m_tiles % 2 == 0 &&
+    const bool pair = pair_env != 0 && !a.gn_fuse && wide_boxes && !a.stationary && !small && !a.x3 && !s2 && a.kw_fuse == 3 && a.m_tiles % 2 == 0 &&
                       a.n_tile % 16 == 0 && !a.gn_part &&
                       grid_cap(ctx, ri, std::min(ctx->num_sms, a.m_tiles * a.n_tiles), cc.seg) >= 2;
     if (pair) {
@@ -1470,6 +1481,33 @@ slim_status run_segment(slim_ctx *ctx, int seg, int ri_prev, int ri, int B, cons
             c2.epi = EPI_BN_ADD_RELU;
             c2.res = cur;
         }
+        // GroupNorm in the conv epilogue where a tile holds whole images (segments 2-3, halo kernel):
+        // t = ReLU(GN1(conv1(x))) and out = ReLU(GN2(conv2(t)) + [GN_p(proj(x)) | x]) [pooled] -- two
+        // launches per block instead of four or five.  SLIM_GN_EPI=0 keeps the separate GN kernels (A/B).
+        static const bool gn_epi = !getenv("SLIM_GN_EPI") || atoi(getenv("SLIM_GN_EPI")) != 0;
+        bool gn_c1_done = false;
+        if (gn && bf && gn_epi && H * H < kTileM) {
+            ConvCall g1 = c1;
+            g1.gn_fuse = true;
+            const slim_status sg = conv_halo_bf16(ctx, st, g1, ri, B);
+            if (sg != SLIM_OK && sg != SLIM_EUNSUPPORTED) return sg;
+            gn_c1_done = sg == SLIM_OK;
+            if (gn_c1_done) {
+                ConvCall g2 = c2;
+                g2.gn_fuse = true;
+                const bool last = seg == 3 && b == nb - 1;
+                if (last) g2.pool_out = reinterpret_cast<float *>(dst);   // the head is then the FC alone
+                const slim_status s2 = conv_halo_bf16(ctx, st, g2, ri, B);
+                if (s2 != SLIM_OK && s2 != SLIM_EUNSUPPORTED) return s2;
+                if (s2 == SLIM_OK) {
+                    if (last) gn_pooled = reinterpret_cast<float *>(dst);
+                    cur = dst;
+                    curH = H;
+                    curC = C;
+                    continue;
+                }
+            }
+        }
         if (gn) {
             // t = ReLU(GN1(conv1(x))): conv writes raw into T, GN in place.  u = conv2(t) raw into dst;
             // the projection (raw) reuses T once conv2 has read it; then dst = ReLU(GN2(u) + shortcut).
@@ -1478,12 +1516,15 @@ slim_status run_segment(slim_ctx *ctx, int seg, int ri_prev, int ri, int B, cons
             float2 *part = bf ? reinterpret_cast<float2 *>(static_cast<char *>(ws) + 3 * buf) : nullptr;
             c1.relu_lo = relu_lo;
             c1.gn_part = part;
-            slim_status s1 = bf ? conv_bf16(ctx, st, c1, ri, B) : conv_f32(ctx, st, c1, ri, B);
-            if (s1) return s1;
-            s1 = c1.gn_stats ? gn_apply_part(ctx, st, seg, bi.c1, S.L[bi.c1], ri, B, H, C, T, part, c1.gn_tiles_per_img,
-                                             nullptr, T)
-                             : gn_apply(ctx, st, seg, bi.c1, S.L[bi.c1], nullptr, ri, B, H, C, T, nullptr, nullptr, T, true);
-            if (s1) return s1;
+            slim_status s1 = SLIM_OK;
+            if (!gn_c1_done) {   // (else conv1 already wrote T = ReLU(GN1(.)) above)
+                s1 = bf ? conv_bf16(ctx, st, c1, ri, B) : conv_f32(ctx, st, c1, ri, B);
+                if (s1) return s1;
+                s1 = c1.gn_stats ? gn_apply_part(ctx, st, seg, bi.c1, S.L[bi.c1], ri, B, H, C, T, part, c1.gn_tiles_per_img,
+                                                 nullptr, T)
+                                 : gn_apply(ctx, st, seg, bi.c1, S.L[bi.c1], nullptr, ri, B, H, C, T, nullptr, nullptr, T, true);
+                if (s1) return s1;
+            }
             ConvCall u = c2;
             u.epi = EPI_BN_RELU;
             u.relu_lo = relu_lo;

@@ -132,6 +132,11 @@ struct HaloArgs {
     // rows, tmBh: box [ck, n_tile/2, 1]), so the pair pulls each weight byte from L2 once and each SM
     // ingests half of it.  Needs streamed B, kw_fuse == 3, bmc == 1.
     int pair;
+    // GroupNorm in the epilogue (GN mode): tiles that cover whole images (tiles_per_img == 1,
+    // segments 2-3) reduce each (image, 16-channel group)'s statistics from the fp32 accumulators and
+    // normalise with scale = gamma, shift = beta (scale1 / shift1: the projection's); relu_lo = 0
+    int gn_fuse;
+    float gn_eps;
 };
 constexpr int kMaxSB = 8;                    // halo kernel: B ring slots (barrier pairs) at most
 constexpr int kHaloBars = 24 + 2 * kMaxSB;   // a_full/empty[4] b_full/empty[kMaxSB] t_full/empty[4] r_full/empty[4]

@@ -632,3 +632,21 @@ def test_fused_segments_bitwise_equal_per_layer(seg):
     got = out["fused"]["9_0.5_0.25"]
     got = got.view(np.float32) if seg == 3 else (got.astype(np.int32).astype(np.uint32) << 16).view(np.float32)
     _check(got[:3], ref.segment(seg, x[:3], 0.5, 0.25), TAU_BF16, f"fused seg{seg}")
+
+
+@pytest.mark.parametrize("blocks", [(1, 1, 1, 1), (2, 1, 1, 3)])
+def test_other_depths(blocks):
+    """BasicBlocks per segment other than (2, 2, 2, 2): with one block in segment 3 its only block is the
+    down-sampling one, so the network's last conv carries the projection and cannot pool in its
+    epilogue (the head pools); chain and segment 3 within tolerance of the oracle."""
+    w = synth.make_weights(blocks=blocks)
+    bn = synth.make_bn(blocks=blocks)
+    n = slim.SlimNet(w, bn, max_batch=16, blocks_per_seg=blocks)
+    oref = oracle.Model(w, bn, blocks=blocks)
+    x = synth.make_images(9, offset=43)
+    tup = (0.5, 1.0, 0.25, 0.75)
+    xd = torch.from_numpy(x).to(torch.bfloat16).cuda()
+    got = n.forward_chain(xd, tup).cpu().numpy()
+    err = oracle.per_image_rel_err(got, oref.chain(x, tup))
+    assert err.max() <= TAU_BF16, err.max()
+    n.close()
