@@ -109,6 +109,13 @@ __global__ void __launch_bounds__(kSmall ? kHaloThreadsSmall : kHaloThreads, kSm
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int total = a.m_tiles * a.n_tiles;
+    // GN image pairs (a.gn_pairs, segment 1: an image is two M tiles): the CTA takes both tiles of an image
+    // back to back (its it-th tile is 2u + (it & 1)), so both accumulators are in TMEM for the statistics
+    const bool prs = kGN && a.gn_pairs;
+    auto tile_at = [&](int it) {
+        if (!prs) return static_cast<int>(blockIdx.x) + it * static_cast<int>(gridDim.x);
+        return 2 * (static_cast<int>(blockIdx.x) + (it >> 1) * static_cast<int>(gridDim.x)) + (it & 1);
+    };
     unsigned long long *tr = a.trace ? a.trace + blockIdx.x * 8 : nullptr;
     unsigned long long *td = (a.trace && blockIdx.x == 0) ? a.trace + 2048 : nullptr;   // per-tile detail, CTA 0
 #define TD(role, tile, pt) \
@@ -199,10 +206,9 @@ __global__ void __launch_bounds__(kSmall ? kHaloThreadsSmall : kHaloThreads, kSm
         if (lane == 0) {
             int s = 0;
             uint32_t ph = 0;
-            for (int t = blockIdx.x; t < total; t += gridDim.x) {
+            for (int ti = 0, t; (t = tile_at(ti)) < total; ++ti) {
                 const int mt = t % a.m_tiles;
                 const int n = mt / tiles_per_img, h0 = (mt - n * tiles_per_img) * a.rows;
-                const int ti = (t - blockIdx.x) / gridDim.x;
                 TD(0, ti, 0);
                 for (int ch = 0; ch < a.n_chunks && !s2; ++ch) {
                     if (x3 || x2) {   // one slot per kw-shifted box (x2: shifts 0 then -1)
@@ -287,10 +293,9 @@ __global__ void __launch_bounds__(kSmall ? kHaloThreadsSmall : kHaloThreads, kSm
         if (lane == 0 && n_res) {
             int rs = 0;
             uint32_t rph = 0;
-            for (int t = blockIdx.x; t < total; t += gridDim.x) {
+            for (int ti = 0, t; (t = tile_at(ti)) < total; ++ti) {
                 const int mt = t % a.m_tiles, nt = t / a.m_tiles;
                 const int n = mt / tiles_per_img, h0 = (mt - n * tiles_per_img) * a.rows, co0 = nt * a.n_tile;
-                const int ti = (t - blockIdx.x) / gridDim.x;
                 mbar_wait(r_empty(rs), rph ^ 1);
                 TD(0, ti, 1);
                 if (a.debug & 8) {
@@ -316,7 +321,7 @@ __global__ void __launch_bounds__(kSmall ? kHaloThreadsSmall : kHaloThreads, kSm
             const int hrows = a.n_tile / bmc;
             const uint32_t rank = kClu == 1 ? cluster_ctarank() : 0u;
             const uint32_t tapb = static_cast<uint32_t>(a.n_tile) * RBK, hoff = rank * hrows * RBK;
-            for (int t = blockIdx.x; t < total; t += gridDim.x) {
+            for (int ti = 0, t; (t = tile_at(ti)) < total; ++ti) {
                 const int co0 = (t / a.m_tiles) * a.n_tile;
                 for (int ch = 0; ch < a.n_chunks; ++ch)
                     for (int kq = 0; kq < 3; ++kq) {
@@ -402,8 +407,7 @@ __global__ void __launch_bounds__(kSmall ? kHaloThreadsSmall : kHaloThreads, kSm
                 mbar_wait(b_full(0), 0);
                 tc_fence_after();
             }
-            for (int t = blockIdx.x; t < total; t += gridDim.x) {
-                const int ti = (t - blockIdx.x) / gridDim.x;
+            for (int ti = 0, t; (t = tile_at(ti)) < total; ++ti) {
                 if (lane == 0) TD(1, ti, 0);
                 mbar_wait(t_empty(as), aph ^ 1);
                 if (lane == 0) TD(1, ti, 1);
@@ -654,10 +658,9 @@ __global__ void __launch_bounds__(kSmall ? kHaloThreadsSmall : kHaloThreads, kSm
         const uint32_t sOutG = sOut + grp * chunk_bytes;
         uint8_t *pOutG = pOut + grp * chunk_bytes;
         const float mL = w > 0 ? 1.f : 0.f, mR = w < a.W - 1 ? 1.f : 0.f;   // conv zero padding in W
-        for (int t = blockIdx.x + grp * gridDim.x; t < total; t += n_grp * gridDim.x) {
+        for (int ti = grp, t; (t = tile_at(ti)) < total; ti += n_grp) {
             const int mt = t % a.m_tiles, nt = t / a.m_tiles;
             const int n = mt / tiles_per_img, h0 = (mt - n * tiles_per_img) * a.rows, co0 = nt * a.n_tile;
-            const int ti = (t - blockIdx.x) / gridDim.x;
             const int as = ti % a.acc_stages, rs = n_res ? ti % n_res : 0;
             const uint32_t aph = (ti / a.acc_stages) & 1, rph = n_res ? (ti / n_res) & 1 : 0;
             mbar_wait(t_full(as), aph);
@@ -670,9 +673,12 @@ __global__ void __launch_bounds__(kSmall ? kHaloThreadsSmall : kHaloThreads, kSm
             if (leader) TD(2, ti, 2);
             const uint8_t *resp = pRes + rs * chunk_bytes;
             const uint32_t col0 = static_cast<uint32_t>(as * a.stage_cols);
-            // GN statistics partials of this tile group: [g][lane quarter][image] (then the projection's)
-            float4 *sG = kGN ? sGN + static_cast<size_t>(grp) * gn_ng * 4 * gn_ni * (proj ? 2 : 1) : nullptr;
-            if constexpr (kGN) {
+            // GN statistics partials of this tile group: [g][tile of the pair][lane quarter][image] (then the
+            // projection's); image pairs: the even tile computes them for both tiles (both accumulators are in
+            // TMEM: acc_stages == 2), the odd tile reuses them
+            const int pm = prs ? 2 : 1;
+            float4 *sG = kGN ? sGN + static_cast<size_t>(grp) * gn_ng * pm * 4 * gn_ni * (proj ? 2 : 1) : nullptr;
+            if (kGN && !(prs && (ti & 1))) {
                 // (K, S1, S2) of this thread's 16 values shifted by K = the image's first lane's first value
                 // (keeps the sums of squares from cancelling), summed over the warp's lanes of the same image
                 // in a fixed butterfly, parked per (g, quarter, image); merged in pass 2
@@ -697,11 +703,17 @@ __global__ void __launch_bounds__(kSmall ? kHaloThreadsSmall : kHaloThreads, kSm
                     }
                     if (lane < a.row_px && lane % a.W == 0) dst[lane / a.W] = make_float4(K, S1, S2, 0.f);
                 };
-                for (int g = g0; g < a.n_tile / 16; g += gstep) {
+                if (prs) {   // the image's second tile (next stage) must have landed too
+                    mbar_wait(t_full(as + 1), aph);
+                    tc_fence_after();
+                }
+                for (int gi = g0; gi < pm * (a.n_tile / 16); gi += gstep) {
+                    const int g = gi % (a.n_tile / 16), h = gi / (a.n_tile / 16);   // h: tile of the pair
+                    const uint32_t cs = col0 + static_cast<uint32_t>(h * a.stage_cols);
                     uint32_t v0[16], v1[16], v2[16];
-                    tmem_ld16(lane_addr + col0 + g * 16, v0);
-                    tmem_ld16(lane_addr + col0 + a.acc_stride + g * 16, v1);
-                    tmem_ld16(lane_addr + col0 + 2 * a.acc_stride + g * 16, v2);
+                    tmem_ld16(lane_addr + cs + g * 16, v0);
+                    tmem_ld16(lane_addr + cs + a.acc_stride + g * 16, v1);
+                    tmem_ld16(lane_addr + cs + 2 * a.acc_stride + g * 16, v2);
                     tmem_wait_ld();
                     reg_fence16(v0);
                     reg_fence16(v1);
@@ -726,14 +738,14 @@ __global__ void __launch_bounds__(kSmall ? kHaloThreadsSmall : kHaloThreads, kSm
                                   y[i], y[i + 1]);
                         }
                     }
-                    park(y, sG + (g * 4 + q) * gn_ni);
+                    park(y, sG + ((g * pm + h) * 4 + q) * gn_ni);
                     if (proj) {   // the projection shortcut's own GroupNorm statistics
-                        tmem_ld16(lane_addr + col0 + 3 * a.acc_stride + g * 16, v0);
+                        tmem_ld16(lane_addr + cs + 3 * a.acc_stride + g * 16, v0);
                         tmem_wait_ld();
                         reg_fence16(v0);
 #pragma unroll
                         for (int i = 0; i < 16; ++i) y[i] = __uint_as_float(v0[i]);
-                        park(y, sG + (gn_ng + g) * 4 * gn_ni + q * gn_ni);
+                        park(y, sG + (((gn_ng + g) * pm + h) * 4 + q) * gn_ni);
                     }
                 }
                 named_bar_sync(1 + grp, gthreads);
@@ -741,7 +753,7 @@ __global__ void __launch_bounds__(kSmall ? kHaloThreadsSmall : kHaloThreads, kSm
             // GN: (mean, rstd) of this thread's image for 16-channel group g from the four quarter partials
             // (equal counts, fixed merge order: bitwise batch independent); base = the layer's or projection's
             auto gn_stats = [&](int g, int base) {
-                const float4 *pq = sG + ((base + g) * 4) * gn_ni + (lane % a.row_px) / a.W;
+                const float4 *pq = sG + ((base + g) * pm * 4) * gn_ni + (lane % a.row_px) / a.W;
                 const float cq = 16.f * 32.f * static_cast<float>(a.W) / static_cast<float>(a.row_px);
                 auto quarter = [&](const float4 v) {
                     const float m = v.y / cq;
@@ -751,9 +763,13 @@ __global__ void __launch_bounds__(kSmall ? kHaloThreadsSmall : kHaloThreads, kSm
                     const float d = y2.x - x.x;
                     return make_float2((x.x + y2.x) * 0.5f, (x.y + y2.y) + d * d * (c * 0.5f));
                 };
-                const float2 tot = merge(merge(quarter(pq[0]), quarter(pq[gn_ni]), cq),
-                                         merge(quarter(pq[2 * gn_ni]), quarter(pq[3 * gn_ni]), cq), 2.f * cq);
-                return make_float2(tot.x, rsqrtf(tot.y / (4.f * cq) + a.gn_eps));
+                auto four = [&](const float4 *p4) {
+                    return merge(merge(quarter(p4[0]), quarter(p4[gn_ni]), cq),
+                                 merge(quarter(p4[2 * gn_ni]), quarter(p4[3 * gn_ni]), cq), 2.f * cq);
+                };
+                float2 tot = four(pq);
+                if (prs) tot = merge(tot, four(pq + 4 * gn_ni), 4.f * cq);   // the image's two tiles
+                return make_float2(tot.x, rsqrtf(tot.y / (4.f * pm * cq) + a.gn_eps));
             };
             for (int g = g0; g < a.n_tile / 16 && !(a.debug & 16); g += gstep) {
                 uint32_t v0[16], v1[16], v2[16];
@@ -1007,7 +1023,7 @@ size_t conv_halo_smem_bytes(const HaloArgs &a) {
            chunk * (a.epi_groups + n_res) +
            (a.epi == EPI_BN_PROJ_RELU ? 16 : 8) * static_cast<size_t>(a.c_out) + 8 * kHaloBars + 16 +
            (a.gn_fuse ? static_cast<size_t>(a.epi_groups) * (a.n_tile / 16) * 4 * a.tile_imgs * 16 *
-                            (a.epi == EPI_BN_PROJ_RELU ? 2 : 1) + 16
+                            (a.epi == EPI_BN_PROJ_RELU ? 2 : 1) * (a.gn_pairs ? 2 : 1) + 16
                       : 0) +
            (a.gn_part ? static_cast<size_t>(a.epi_groups) * (a.n_tile / 16) * 4 * a.tile_imgs * 16 + 16 : 0);
 }
@@ -1082,7 +1098,9 @@ cudaError_t launch_conv_halo(const HaloArgs &a, const CUtensorMap &tmA, const CU
         return cudaLaunchKernelEx(&cfg, small_fns[var], tmA, tmB, tmRes, tmOut, tmA1, tmB1, tmBh, a);
     }
     if (a.gn_fuse) {
-        if (var > 3 || a.pair || a.bmc > 1 || a.tiles_per_img != 1 || a.kw_fuse != 3 || a.gn_part) return cudaErrorInvalidValue;
+        if (var > 3 || a.pair || a.bmc > 1 || a.tiles_per_img != (a.gn_pairs ? 2 : 1) || a.kw_fuse != 3 || a.gn_part ||
+            (a.gn_pairs && (a.acc_stages != 2 || a.epi_groups != 1 || grid * 2 > a.m_tiles * a.n_tiles)))
+            return cudaErrorInvalidValue;
         return cudaLaunchKernelEx(&cfg, gn_fns[narrow ? 1 : 0][var], tmA, tmB, tmRes, tmOut, tmA1, tmB1, tmBh, a);
     }
     if (a.pair) {

@@ -534,7 +534,9 @@ slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, i
     a.scale = L.scale[ri];
     a.shift = L.shift[ri];
     if (cc.gn_fuse) {   // GroupNorm in the epilogue: the tile must hold whole images (their full statistics)
-        if (a.tiles_per_img != 1 || small) return SLIM_EUNSUPPORTED;
+        // or, as an image pair, a CTA takes both M tiles of one image (segment 1)
+        if ((a.tiles_per_img != 1 && a.tiles_per_img != 2) || small) return SLIM_EUNSUPPORTED;
+        a.gn_pairs = a.tiles_per_img == 2 ? 1 : 0;
         a.gn_fuse = 1;
         a.gn_eps = c.bn_eps;
         a.scale = L.gn_gamma[ri];
@@ -576,6 +578,10 @@ slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, i
     const int tmem_max = small ? 256 : 512;
     a.acc_stages = (4 * a.stage_cols <= tmem_max && max_stages >= 4) ? 4
                                                                       : (2 * a.stage_cols <= tmem_max && max_stages >= 2 ? 2 : 1);
+    if (a.gn_pairs) {   // both tiles of an image resident: exactly two stages, one tile group
+        if (2 * a.stage_cols > tmem_max) return SLIM_EUNSUPPORTED;
+        a.acc_stages = 2;
+    }
     if (a.stage_cols > tmem_max) small = false;   // (cannot happen for c_out <= 64)
     int cols = a.acc_stages * a.stage_cols, tc = 32;
     while (tc < cols) tc <<= 1;
@@ -595,7 +601,7 @@ slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, i
     a.n_out_chunks = static_cast<uint32_t>((a.n_tile + a.co_chunk - 1) / a.co_chunk);
     const size_t chunk = static_cast<size_t>(a.n_out_chunks) * 128 * a.rbo;
     static const bool one_group = getenv("SLIM_HALO_EPI1") != nullptr;
-    a.epi_groups = one_group ? 1 : a.acc_stages;
+    a.epi_groups = (one_group || a.gn_pairs) ? 1 : a.acc_stages;
     if (small && a.epi_groups > 2) a.epi_groups = 2;   // 8 epilogue warps: one or two tile groups
     a.small = small ? 1 : 0;
     const bool two = small;
@@ -610,7 +616,8 @@ slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, i
     auto fixed0 = [&]() {
         return 1024 + chunk * a.epi_groups + (proj ? 16 : 8) * static_cast<size_t>(c_out) + 8 * kHaloBars + 16 +
                (a.gn_part ? static_cast<size_t>(a.epi_groups) * (a.n_tile / 16) * 4 * a.tile_imgs * 16 + 16 : 0) +
-               (a.gn_fuse ? static_cast<size_t>(a.epi_groups) * (a.n_tile / 16) * 4 * a.tile_imgs * 16 * (proj ? 2 : 1) + 16
+               (a.gn_fuse ? static_cast<size_t>(a.epi_groups) * (a.n_tile / 16) * 4 * a.tile_imgs * 16 * (proj ? 2 : 1) *
+                                    (a.gn_pairs ? 2 : 1) + 16
                           : 0);
     };
     auto r1k = [](uint32_t x) { return (x + 1023u) & ~1023u; };
@@ -710,6 +717,7 @@ slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, i
     const int total = a.m_tiles * a.n_tiles;
     int grid = ctx->num_sms * (two ? 2 : 1);
     if (grid > total) grid = total;
+    if (a.gn_pairs && grid > total / 2) grid = total / 2;   // a CTA's tiles come in image pairs
     grid = grid_cap(ctx, ri, grid, cc.seg);
     if (a.pair) grid -= grid % 2;   // (>= 2: checked with the pair decision)
     // streamed weights: clusters of bmc CTAs on consecutive M tiles of one N tile share each B stage
@@ -1486,7 +1494,11 @@ slim_status run_segment(slim_ctx *ctx, int seg, int ri_prev, int ri, int B, cons
         // launches per block instead of four or five.  SLIM_GN_EPI=0 keeps the separate GN kernels (A/B).
         static const bool gn_epi = !getenv("SLIM_GN_EPI") || atoi(getenv("SLIM_GN_EPI")) != 0;
         bool gn_c1_done = false;
-        if (gn && bf && gn_epi && H * H < kTileM) {
+        // Segment 1 (two M tiles per image) as image pairs -- one CTA takes both tiles, both accumulators
+        // resident -- is opt-in (SLIM_GN_PAIRS=1): parity green but measured slower (r = 1 GN seg 1
+        // 98 -> 103 us, GN CFG2 766 k -> 650 k: the pair serialises MMA and epilogue per image)
+        static const bool gn_pairs = getenv("SLIM_GN_PAIRS") && atoi(getenv("SLIM_GN_PAIRS")) != 0;
+        if (gn && bf && gn_epi && (H * H < kTileM || (gn_pairs && H * H == 2 * kTileM))) {
             ConvCall g1 = c1;
             g1.gn_fuse = true;
             const slim_status sg = conv_halo_bf16(ctx, st, g1, ri, B);

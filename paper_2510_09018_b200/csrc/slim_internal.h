@@ -137,6 +137,7 @@ struct HaloArgs {
     // normalise with scale = gamma, shift = beta (scale1 / shift1: the projection's); relu_lo = 0
     int gn_fuse;
     float gn_eps;
+    int gn_pairs;   // GN with two M tiles per image (segment 1): one CTA takes both (acc_stages 2, one tile group)
 };
 constexpr int kMaxSB = 8;                    // halo kernel: B ring slots (barrier pairs) at most
 constexpr int kHaloBars = 24 + 2 * kMaxSB;   // a_full/empty[4] b_full/empty[kMaxSB] t_full/empty[4] r_full/empty[4]

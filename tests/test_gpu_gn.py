@@ -237,3 +237,34 @@ def test_fused_segments_gn_parity(seg):
             worst = max(worst, float(err.max()))
     net.close()
     assert worst <= 2e-2, worst
+
+
+def test_gn_epilogue_image_pairs_opt_in():
+    """SLIM_GN_PAIRS=1: segment 1's GroupNorm in the conv epilogue with one CTA taking both M tiles of an
+    image (statistics over the two TMEM-resident accumulators) -- within tolerance of the oracle for every
+    (r_prev, r) it accepts, and bitwise batch independent."""
+    import os, subprocess, sys
+    code = (
+        "import numpy as np, torch, synth, oracle, paper_2510_09018_b200 as slim\n"
+        "w, bn = synth.make_weights(), synth.make_bn()\n"
+        "net = slim.SlimNet(w, bn, max_batch=32, norm='gn')\n"
+        "ref = oracle.Model(w, bn, norm='gn')\n"
+        "worst = 0.0\n"
+        "for rp in synth.WIDTHS:\n"
+        "    C = synth.active_channels(rp, synth.BASE_CHANNELS[0])\n"
+        "    g = np.random.default_rng(7)\n"
+        "    x = synth.round_bf16(np.abs(g.standard_normal((9, 32, 32, C), dtype=np.float32)))\n"
+        "    xd = torch.from_numpy(x).to(torch.bfloat16).cuda()\n"
+        "    for r in synth.WIDTHS:\n"
+        "        got = net.forward(1, xd, rp, r).float().cpu().numpy()\n"
+        "        err = oracle.per_image_rel_err(got, ref.segment(1, x, rp, r))\n"
+        "        worst = max(worst, float(err.max()))\n"
+        "        one = net.forward(1, xd[4:5].contiguous(), rp, r).float().cpu().numpy()\n"
+        "        assert np.array_equal(one[0], got[4]), (rp, r)\n"
+        "print(worst)\n"
+    )
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, SLIM_GN_PAIRS="1", SLIM_NO_FUSED="1")
+    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert float(out.stdout.strip().splitlines()[-1]) <= TAU_BF16
