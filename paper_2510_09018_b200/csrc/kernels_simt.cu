@@ -371,8 +371,11 @@ __device__ __forceinline__ void f32_gemm_part(const GemmTile &g, const float *__
         if (s + 1 < steps) load(s + 1);
 #pragma unroll
         for (int kk = 0; kk < kGK; ++kk) {
-            const float4 a0 = *reinterpret_cast<const float4 *>(&As[b][kk][g.tx * 8]);
-            const float4 a1 = *reinterpret_cast<const float4 *>(&As[b][kk][g.tx * 8 + 4]);
+            // pixels tx*4 .. +3 and kGM/2 + tx*4 .. +3: each LDS.128 of the warp reads one contiguous run
+            // (tx*8 .. +7 put the lanes 32 B apart: two bank wavefronts per 128 B, ncu: 40 % of the
+            // shared-load wavefronts were conflicts)
+            const float4 a0 = *reinterpret_cast<const float4 *>(&As[b][kk][g.tx * 4]);
+            const float4 a1 = *reinterpret_cast<const float4 *>(&As[b][kk][kGM / 2 + g.tx * 4]);
             const float4 bv = *reinterpret_cast<const float4 *>(&Bs[b][kk][g.ty * 4]);
             const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
             const float bw[4] = {bv.x, bv.y, bv.z, bv.w};
@@ -394,7 +397,7 @@ __device__ __forceinline__ void conv_f32_gemm_tile(const ConvF32Args &a, int bx,
     const int n0 = by * kGN;
     const long npix = static_cast<long>(a.B) * a.Ho * a.Wo;
     GemmTile g;
-    g.tx = tid & 15;          // compute: pixels tx*8 .. +7, channels ty*4 .. +3
+    g.tx = tid & 15;          // compute: pixels tx*4 .. +3 and 64 + tx*4 .. +3, channels ty*4 .. +3
     g.ty = tid >> 4;
     g.lp = tid >> 1;          // A loader: pixel lp, channels lc .. lc+7 of the 16-channel step
     g.lc = (tid & 1) * 8;
@@ -429,8 +432,8 @@ __device__ __forceinline__ void conv_f32_gemm_tile(const ConvF32Args &a, int bx,
     const float sc1[4] = {s1.x, s1.y, s1.z, s1.w}, sh1[4] = {t1.x, t1.y, t1.z, t1.w};
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-        const long p = m0 + tx * 8 + i;
-        if (p >= npix) break;
+        const long p = m0 + (i < 4 ? tx * 4 + i : kGM / 2 + tx * 4 + i - 4);
+        if (p >= npix) continue;
         const size_t o = static_cast<size_t>(p) * a.c_out + c;
         float r[4] = {0.f, 0.f, 0.f, 0.f};
         if (a.epi == EPI_BN_ADD_RELU) {
@@ -466,7 +469,7 @@ __device__ __forceinline__ void conv_f32_gemm256_tile(const ConvF32Args &a, int 
     __shared__ __align__(16) float As[2][kGK][kWM + 4];
     __shared__ __align__(16) float Bs[2][kGK][kGN + 4];
     const int tid = threadIdx.x;
-    const int tx = tid & 31, ty = tid >> 5;       // compute: pixels tx*8 .. +7, channels ty*8 .. +7
+    const int tx = tid & 31, ty = tid >> 5;       // compute: pixels tx*4 .. +3, 128 + tx*4 .. +3; channels ty*8 .. +7
     const long m0 = static_cast<long>(bx) * kWM;
     const int n0 = by * kGN;
     const long npix = static_cast<long>(a.B) * a.Ho * a.Wo;
@@ -519,8 +522,8 @@ __device__ __forceinline__ void conv_f32_gemm256_tile(const ConvF32Args &a, int 
         if (s + 1 < steps) load(s + 1);
 #pragma unroll
         for (int kk = 0; kk < kGK; ++kk) {
-            const float4 a0 = *reinterpret_cast<const float4 *>(&As[b][kk][tx * 8]);
-            const float4 a1 = *reinterpret_cast<const float4 *>(&As[b][kk][tx * 8 + 4]);
+            const float4 a0 = *reinterpret_cast<const float4 *>(&As[b][kk][tx * 4]);   // conflict-free runs
+            const float4 a1 = *reinterpret_cast<const float4 *>(&As[b][kk][kWM / 2 + tx * 4]);
             const float4 b0 = *reinterpret_cast<const float4 *>(&Bs[b][kk][ty * 8]);
             const float4 b1 = *reinterpret_cast<const float4 *>(&Bs[b][kk][ty * 8 + 4]);
             const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
@@ -537,8 +540,8 @@ __device__ __forceinline__ void conv_f32_gemm256_tile(const ConvF32Args &a, int 
     if (c >= a.c_out) return;   // c_out is a multiple of 16: a thread's 8 channels are all valid or none
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-        const long p = m0 + tx * 8 + i;
-        if (p >= npix) break;
+        const long p = m0 + (i < 4 ? tx * 4 + i : kWM / 2 + tx * 4 + i - 4);
+        if (p >= npix) continue;
         const size_t o = static_cast<size_t>(p) * a.c_out + c;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
