@@ -643,8 +643,10 @@ cudaError_t launch_scatter(const void *src, const uint32_t *idx, int n, size_t r
 cudaError_t launch_conv_f32(const ConvF32Args &a, cudaStream_t s) {
     const long npix = static_cast<long>(a.B) * a.Ho * a.Wo;
     static const bool direct = getenv("SLIM_F32_DIRECT") != nullptr;   // A/B: the direct-conv kernel
-    static const bool narrow = getenv("SLIM_F32_GEMM128") != nullptr;   // A/B: the 128 x 64 tile only
-    if (!direct && !narrow && a.c_in % kGK == 0 && a.epi != EPI_BN_PROJ_RELU && a.c_out % 16 == 0 &&
+    // the 256 x 64 tile (8 x 8 per thread, 167 registers: one CTA per SM) measured 1.7 % slower than the
+    // 128 x 64 tile (8 x 4, two CTAs per SM) once both read A conflict-free: opt-in SLIM_F32_GEMM256=1
+    static const bool wide = getenv("SLIM_F32_GEMM256") != nullptr;
+    if (!direct && wide && a.c_in % kGK == 0 && a.epi != EPI_BN_PROJ_RELU && a.c_out % 16 == 0 &&
         npix >= 148L * kWM) {
         const int gx = static_cast<int>((npix + kWM - 1) / kWM), gy = (a.c_out + kGN - 1) / kGN;
         const int grid = (a.max_ctas > 0 && a.max_ctas < gx * gy) ? a.max_ctas : gx * gy;

@@ -83,7 +83,8 @@ struct slim_ctx {
         uint64_t n_kernels;
     };
     bool graph_mode = false;
-    bool pdl = true;   // programmatic dependent launch between consecutive kernels (off while profiling)
+    // programmatic dependent launch between consecutive kernels (off while profiling); SLIM_PDL=0 (A/B)
+    bool pdl = !getenv("SLIM_PDL") || atoi(getenv("SLIM_PDL")) != 0;
     cudaStream_t cap_stream = nullptr;
     std::mutex graph_mu;
     std::unordered_map<std::string, GraphEntry> graphs;
