@@ -196,8 +196,32 @@ __global__ void __launch_bounds__(kSmall ? kHaloThreadsSmall : kHaloThreads, kSm
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
-    if (warp != 2) pdl_wait();   // the weight producer does not depend on the previous kernel
+    // the weight producer does not depend on the previous kernel; with flag_in nobody waits for the whole
+    // previous grid -- the A / residual producers wait per tile on its flags instead
+    if (warp != 2 && !a.flag_in) pdl_wait();
+    if (a.flag_zero) {   // later layers' counters (their previous use is complete: we waited for our predecessor)
+        if (warp != 2)
+            for (int i = blockIdx.x * (blockDim.x - 32) + (threadIdx.x - (warp > 2 ? 32 : 0)); i < a.flag_zero_n;
+                 i += gridDim.x * (blockDim.x - 32))
+                a.flag_zero[i] = 0u;
+        __threadfence();
+        __syncthreads();
+    }
     pdl_launch_dependents();
+    // wait until the previous layer's M tiles that M tile mt reads (its halo rows) are finished
+    auto wait_inputs = [&](int mt) {
+        if (!a.flag_in) return;
+        const int tpi = a.tiles_per_img;
+        const int lo = tpi > 1 ? (mt / tpi) * tpi : mt, hi = tpi > 1 ? lo + tpi - 1 : mt;
+        for (int m = max(lo, mt - 1); m <= min(hi, mt + 1); ++m) {
+            uint32_t spins = 0;
+            while (ld_acquire_gpu(a.flag_in + m) < static_cast<uint32_t>(a.flag_in_target)) {
+                __nanosleep(64);
+                if (++spins > (1u << 26)) __trap();   // a lost dependency must not hang the GPU
+            }
+        }
+        fence_proxy_async_global();   // the TMA loads that follow see those tiles' TMA stores
+    };
     if (tr && threadIdx.x == 0) tr[1] = gtimer();
     const int tiles_per_img = a.tiles_per_img;
 
@@ -209,6 +233,7 @@ __global__ void __launch_bounds__(kSmall ? kHaloThreadsSmall : kHaloThreads, kSm
             for (int ti = 0, t; (t = tile_at(ti)) < total; ++ti) {
                 const int mt = t % a.m_tiles;
                 const int n = mt / tiles_per_img, h0 = (mt - n * tiles_per_img) * a.rows;
+                wait_inputs(mt);
                 TD(0, ti, 0);
                 for (int ch = 0; ch < a.n_chunks && !s2; ++ch) {
                     if (x3 || x2) {   // one slot per kw-shifted box (x2: shifts 0 then -1)
@@ -296,6 +321,7 @@ __global__ void __launch_bounds__(kSmall ? kHaloThreadsSmall : kHaloThreads, kSm
             for (int ti = 0, t; (t = tile_at(ti)) < total; ++ti) {
                 const int mt = t % a.m_tiles, nt = t / a.m_tiles;
                 const int n = mt / tiles_per_img, h0 = (mt - n * tiles_per_img) * a.rows, co0 = nt * a.n_tile;
+                wait_inputs(mt);   // (the residual is older than the input: transitively finished)
                 mbar_wait(r_empty(rs), rph ^ 1);
                 TD(0, ti, 1);
                 if (a.debug & 8) {
@@ -658,6 +684,9 @@ __global__ void __launch_bounds__(kSmall ? kHaloThreadsSmall : kHaloThreads, kSm
         const uint32_t sOutG = sOut + grp * chunk_bytes;
         uint8_t *pOutG = pOut + grp * chunk_bytes;
         const float mL = w > 0 ? 1.f : 0.f, mR = w < a.W - 1 ? 1.f : 0.f;   // conv zero padding in W
+        // (flag_out) the group's last two tiles: a tile is published once its store has completed, checked when
+        // the group's next-but-one tile starts (wait_group 1: never stalls on the store just issued)
+        int prev_mt = -1, prev2_mt = -1;
         for (int ti = grp, t; (t = tile_at(ti)) < total; ti += n_grp) {
             const int mt = t % a.m_tiles, nt = t / a.m_tiles;
             const int n = mt / tiles_per_img, h0 = (mt - n * tiles_per_img) * a.rows, co0 = nt * a.n_tile;
@@ -666,6 +695,12 @@ __global__ void __launch_bounds__(kSmall ? kHaloThreadsSmall : kHaloThreads, kSm
             mbar_wait(t_full(as), aph);
             if (leader) TD(2, ti, 0);
             tc_fence_after();
+            if (leader && a.flag_out && prev2_mt >= 0) {   // the tile before the previous one: its store is complete
+                bulk_wait1();                               // (the previous tile's may still be in flight)
+                fence_proxy_async_global();
+                red_release_gpu_add(a.flag_out + prev2_mt, 1u);
+                prev2_mt = -1;
+            }
             if (leader) bulk_wait_read0();   // this group's previous store has left the staging tile
             if (leader) TD(2, ti, 1);
             named_bar_sync(1 + grp, gthreads);
@@ -993,9 +1028,16 @@ __global__ void __launch_bounds__(kSmall ? kHaloThreadsSmall : kHaloThreads, kSm
                     tma_store_4d(&tmOut, sOutG + j * oc_bytes, co0 + j * CO_CHUNK, 0, n * a.tile_imgs, h0);
                 bulk_commit();
             }
+            prev2_mt = prev_mt;
+            prev_mt = mt;
         }
         if (tr && leader) tr[4] = gtimer();
         if (leader) bulk_wait0();
+        if (leader && a.flag_out) {
+            fence_proxy_async_global();
+            if (prev2_mt >= 0) red_release_gpu_add(a.flag_out + prev2_mt, 1u);
+            if (prev_mt >= 0) red_release_gpu_add(a.flag_out + prev_mt, 1u);
+        }
         if (tr && leader) tr[5] = gtimer();
     }
 

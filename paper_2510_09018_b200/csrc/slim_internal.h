@@ -138,6 +138,15 @@ struct HaloArgs {
     int gn_fuse;
     float gn_eps;
     int gn_pairs;   // GN with two M tiles per image (segment 1): one CTA takes both (acc_stages 2, one tile group)
+    // Tile-granular dependencies between consecutive halo convs of a segment (same M tiling) instead of
+    // waiting for the whole previous grid (griddepcontrol.wait): flag_in[mt] counts the previous layer's
+    // finished (mt, any N tile) tiles; a tile waits until its input M tiles (mt-1..mt+1 of the same image,
+    // or mt for whole-image tiles) reach flag_in_target (= that layer's n_tiles).  flag_out: this layer's
+    // counters (one red.release per finished tile, after its TMA store completed).  flag_zero: counters
+    // of later layers this kernel clears (after its own griddepcontrol.wait, before it lets dependents
+    // launch).  All nullptr = the plain PDL dependency.
+    uint32_t *flag_in, *flag_out, *flag_zero;
+    int flag_in_target, flag_zero_n;
 };
 constexpr int kMaxSB = 8;                    // halo kernel: B ring slots (barrier pairs) at most
 constexpr int kHaloBars = 24 + 2 * kMaxSB;   // a_full/empty[4] b_full/empty[kMaxSB] t_full/empty[4] r_full/empty[4]

@@ -650,3 +650,12 @@ def test_other_depths(blocks):
     err = oracle.per_image_rel_err(got, oref.chain(x, tup))
     assert err.max() <= TAU_BF16, err.max()
     n.close()
+
+
+def test_tile_flags_bitwise(tmp_path):
+    """Opt-in tile-granular dependencies between a segment's halo convs (SLIM_TILE_FLAGS=1: block 1's convs
+    wait per tile on counters the previous conv releases after each tile's TMA store, instead of on the
+    whole previous grid): every segment output bitwise equal to the default PDL ordering."""
+    one, two = _seg123_outputs_under_env(tmp_path, [dict(SLIM_TILE_FLAGS="0"), dict(SLIM_TILE_FLAGS="1")])
+    for k in one.files:
+        assert np.array_equal(one[k], two[k]), k
