@@ -213,12 +213,21 @@ __global__ void __launch_bounds__(kSmall ? kHaloThreadsSmall : kHaloThreads, kSm
         if (!a.flag_in) return;
         const int tpi = a.tiles_per_img;
         const int lo = tpi > 1 ? (mt / tpi) * tpi : mt, hi = tpi > 1 ? lo + tpi - 1 : mt;
-        for (int m = max(lo, mt - 1); m <= min(hi, mt + 1); ++m) {
-            uint32_t spins = 0;
-            while (ld_acquire_gpu(a.flag_in + m) < static_cast<uint32_t>(a.flag_in_target)) {
-                __nanosleep(64);
-                if (++spins > (1u << 26)) __trap();   // a lost dependency must not hang the GPU
+        // the (up to three) counters are loaded together: one L2 round trip per poll, not three -- the producer
+        // issues a tile every ~1.2 us, so serial acquires would make it the bottleneck
+        const int m0 = max(lo, mt - 1), m2 = min(hi, mt + 1);
+        const uint32_t tgt = static_cast<uint32_t>(a.flag_in_target);
+        for (uint32_t spins = 0;; ++spins) {
+            // relaxed loads (an acquire load would hold back the next one), then one acquire fence
+            const uint32_t f0 = ld_relaxed_gpu(a.flag_in + m0);
+            const uint32_t f1 = m0 + 1 <= m2 ? ld_relaxed_gpu(a.flag_in + m0 + 1) : tgt;
+            const uint32_t f2 = m0 + 2 <= m2 ? ld_relaxed_gpu(a.flag_in + m0 + 2) : tgt;
+            if (f0 >= tgt && f1 >= tgt && f2 >= tgt) {
+                fence_acq_rel_gpu();
+                break;
             }
+            __nanosleep(64);
+            if (spins > (1u << 26)) __trap();   // a lost dependency must not hang the GPU
         }
         fence_proxy_async_global();   // the TMA loads that follow see those tiles' TMA stores
     };

@@ -1464,9 +1464,13 @@ slim_status run_segment(slim_ctx *ctx, int seg, int ri_prev, int ri, int B, cons
     // Tile-granular dependencies inside a segment (BN, bf16, two blocks, all four convs on the halo kernel
     // with one M tiling): block 1's convs start a tile as soon as the tiles of the previous conv it reads
     // are finished, instead of waiting for that whole grid; block 0's conv1 clears the counters.
-    // Opt-in (SLIM_TILE_FLAGS=1): bitwise equal, but measured slower (r = 1 B = 128 segment 0 61 -> 71 us,
-    // CFG2 1.21 -> 1.13 M images/s): the persistent one-CTA-per-SM grids overlap only at their tails, and
-    // every tile then pays acquire loads of its input tiles' counters on the producer's critical path.
+    // Opt-in (SLIM_TILE_FLAGS=1): bitwise equal, but measured slower (r = 1 B = 128 segment 0 61 -> 70 us,
+    // B = 1024 357 -> 407 us, CFG2 1.21 -> 1.11 M images/s) with serial acquires, parallel relaxed polls +
+    // one acquire fence, and the producer's publication two tiles behind alike: the cost grows with the
+    // tile count (~0.45 us per tile of a flagged layer), i.e. it is per tile, not per boundary -- most
+    // likely the async-proxy fence each consumer tile needs before its TMA loads, which waits for the
+    // producer warp's TMA loads already in flight; and the persistent one-CTA-per-SM grids only overlap
+    // at their tails anyway.
     static const bool tile_flags = getenv("SLIM_TILE_FLAGS") && atoi(getenv("SLIM_TILE_FLAGS")) != 0;
     uint32_t *flags = nullptr;
     int flag_nt[4] = {0, 0, 0, 0}, flag_m = 0;
