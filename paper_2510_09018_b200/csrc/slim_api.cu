@@ -1467,10 +1467,10 @@ slim_status run_segment(slim_ctx *ctx, int seg, int ri_prev, int ri, int B, cons
     // Opt-in (SLIM_TILE_FLAGS=1): bitwise equal, but measured slower (r = 1 B = 128 segment 0 61 -> 70 us,
     // B = 1024 357 -> 407 us, CFG2 1.21 -> 1.11 M images/s) with serial acquires, parallel relaxed polls +
     // one acquire fence, and the producer's publication two tiles behind alike: the cost grows with the
-    // tile count (~0.45 us per tile of a flagged layer), i.e. it is per tile, not per boundary -- most
-    // likely the async-proxy fence each consumer tile needs before its TMA loads, which waits for the
-    // producer warp's TMA loads already in flight; and the persistent one-CTA-per-SM grids only overlap
-    // at their tails anyway.
+    // tile count (~0.45 us per tile of a flagged layer), i.e. it is per tile, not per boundary; removing
+    // either async-proxy fence (an A/B only -- they are needed for correctness) changes nothing, so the
+    // cost is structural (the dependents' producers start loading while the previous grid still runs);
+    // and the persistent one-CTA-per-SM grids only overlap at their tails anyway.
     static const bool tile_flags = getenv("SLIM_TILE_FLAGS") && atoi(getenv("SLIM_TILE_FLAGS")) != 0;
     uint32_t *flags = nullptr;
     int flag_nt[4] = {0, 0, 0, 0}, flag_m = 0;
