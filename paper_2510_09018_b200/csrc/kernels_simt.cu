@@ -14,6 +14,8 @@
 
 #include <cuda_bf16.h>
 
+#include <algorithm>
+
 namespace slim {
 namespace {
 
@@ -334,10 +336,14 @@ struct GemmTile {   // per-thread loader / compute coordinates of conv_f32_gemm_
 // acc += the GEMM of one conv part (K = k*k*cin in steps of 16 channels of one tap)
 __device__ __forceinline__ void f32_gemm_part(const GemmTile &g, const float *__restrict__ x, const float *__restrict__ w,
                                               int H, int W, int cin, int k, int st, int pad, int cin_full,
-                                              float (*As)[kGK][kGM + 4], float (*Bs)[kGK][kGN + 4], float (&acc)[8][4]) {
-    const int csteps = cin / kGK, steps = k * k * csteps;
+                                              float (*As)[kGK][kGM + 4], float (*Bs)[kGK][kGN + 4], float (&acc)[8][4],
+                                              int split = 0, int nsplit = 1) {
+    const int csteps = cin / kGK, steps_all = k * k * csteps;
+    // split-K: this CTA's consecutive range of the K steps (the whole range when nsplit == 1)
+    const int s_lo = steps_all * split / nsplit, steps = steps_all * (split + 1) / nsplit - s_lo;
     float4 ra0, ra1, rb;
     auto load = [&](int s) {
+        s += s_lo;
         const int tap = s / csteps, c0 = (s - tap * csteps) * kGK, kh = tap / k, kw = tap - kh * k;
         const int ih = st * g.poh + kh - pad, iw = st * g.pw + kw - pad;
         const bool ok = g.pok && ih >= 0 && ih < H && iw >= 0 && iw < W;
@@ -389,7 +395,7 @@ __device__ __forceinline__ void f32_gemm_part(const GemmTile &g, const float *__
     }
 }
 
-__device__ __forceinline__ void conv_f32_gemm_tile(const ConvF32Args &a, int bx, int by) {
+__device__ __forceinline__ void conv_f32_gemm_tile(const ConvF32Args &a, int bx, int by, int split = 0) {
     __shared__ __align__(16) float As[2][kGK][kGM + 4];
     __shared__ __align__(16) float Bs[2][kGK][kGN + 4];
     const int tid = threadIdx.x;
@@ -418,10 +424,29 @@ __device__ __forceinline__ void conv_f32_gemm_tile(const ConvF32Args &a, int bx,
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc0[i][j] = acc1[i][j] = 0.f;
     const int nparts = a.epi == EPI_BN_PROJ_RELU ? 2 : 1;
-    f32_gemm_part(g, a.x, a.w, a.H, a.W, a.c_in, a.k, a.stride, a.pad, a.cin_full, As, Bs, acc0);
-    if (nparts == 2) f32_gemm_part(g, a.x1, a.w1, a.H1, a.W1, a.c_in1, 1, a.stride1, 0, a.cin1_full, As, Bs, acc1);
+    const int ks = a.ksplit > 1 ? a.ksplit : 1;
+    f32_gemm_part(g, a.x, a.w, a.H, a.W, a.c_in, a.k, a.stride, a.pad, a.cin_full, As, Bs, acc0, split, ks);
+    // (split-K: the projection shortcut is computed whole by split 0, into its own partial slot ks)
+    const bool do_proj = nparts == 2 && split == 0;
+    if (do_proj) f32_gemm_part(g, a.x1, a.w1, a.H1, a.W1, a.c_in1, 1, a.stride1, 0, a.cin1_full, As, Bs, acc1);
     const int c = n0 + ty * 4;
     if (c >= a.c_out) return;   // c_out is a multiple of 16: a thread's 4 channels are all valid or none
+    if (ks > 1) {   // raw partial sums of this K range; conv_f32_splitk_reduce applies the epilogue
+        float *dst = a.part + static_cast<size_t>(split) * npix * a.c_out;
+        float *dstp = a.part + static_cast<size_t>(ks) * npix * a.c_out;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const long p = m0 + (i < 4 ? tx * 4 + i : kGM / 2 + tx * 4 + i - 4);
+            if (p < npix) {
+                *reinterpret_cast<float4 *>(dst + static_cast<size_t>(p) * a.c_out + c) =
+                    make_float4(acc0[i][0], acc0[i][1], acc0[i][2], acc0[i][3]);
+                if (do_proj)
+                    *reinterpret_cast<float4 *>(dstp + static_cast<size_t>(p) * a.c_out + c) =
+                        make_float4(acc1[i][0], acc1[i][1], acc1[i][2], acc1[i][3]);
+            }
+        }
+        return;
+    }
     const float4 s0 = *reinterpret_cast<const float4 *>(a.scale0 + c), t0 = *reinterpret_cast<const float4 *>(a.shift0 + c);
     float4 s1 = make_float4(0.f, 0.f, 0.f, 0.f), t1 = s1;
     if (nparts == 2) {
@@ -456,8 +481,10 @@ __device__ __forceinline__ void conv_f32_gemm_tile(const ConvF32Args &a, int bx,
 
 // persistent over (M tile, N tile): the grid may be capped (SM share of the width, max_ctas)
 __global__ void __launch_bounds__(kGThreads) conv_f32_gemm_kernel(const ConvF32Args a, int gx, int gy) {
-    for (int t = blockIdx.x; t < gx * gy; t += gridDim.x) {
-        conv_f32_gemm_tile(a, t % gx, t / gx);
+    const int ks = a.ksplit > 1 ? a.ksplit : 1;
+    for (int t = blockIdx.x; t < gx * gy * ks; t += gridDim.x) {
+        const int tt = t % (gx * gy);
+        conv_f32_gemm_tile(a, tt % gx, tt / gx, t / (gx * gy));
         __syncthreads();
     }
 }
@@ -640,6 +667,41 @@ cudaError_t launch_scatter(const void *src, const uint32_t *idx, int n, size_t r
                                           dst_stride / 16);
     return cudaGetLastError();
 }
+// split-K reduce + epilogue: out = max(sum_split part * scale + shift + res, relu_lo), the partials summed
+// in split order (one float4 of 4 channels per thread)
+__global__ void conv_f32_splitk_reduce(const ConvF32Args a) {
+    const size_t npix = static_cast<size_t>(a.B) * a.Ho * a.Wo, n4 = npix * a.c_out / 4;
+    for (size_t v = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; v < n4; v += gridDim.x * blockDim.x) {
+        const size_t o = v * 4;
+        const int c = static_cast<int>(o % a.c_out);
+        float4 s = *reinterpret_cast<const float4 *>(a.part + o);
+        for (int k = 1; k < a.ksplit; ++k) {
+            const float4 q = *reinterpret_cast<const float4 *>(a.part + k * npix * a.c_out + o);
+            s.x += q.x;
+            s.y += q.y;
+            s.z += q.z;
+            s.w += q.w;
+        }
+        float f[4] = {s.x, s.y, s.z, s.w}, r[4] = {0.f, 0.f, 0.f, 0.f};
+        if (a.epi == EPI_BN_ADD_RELU) {
+            const float4 rv = *reinterpret_cast<const float4 *>(a.res + o);
+            r[0] = rv.x;
+            r[1] = rv.y;
+            r[2] = rv.z;
+            r[3] = rv.w;
+        }
+        if (a.epi == EPI_BN_PROJ_RELU) {   // + the shortcut's BN of its raw projection (slot ksplit)
+            const float4 q = *reinterpret_cast<const float4 *>(a.part + a.ksplit * npix * a.c_out + o);
+            const float qq[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) r[j] = fmaf(qq[j], a.scale1[c + j], a.shift1[c + j]);
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) f[j] = fmaxf(fmaf(f[j], a.scale0[c + j], a.shift0[c + j]) + r[j], a.relu_lo);
+        *reinterpret_cast<float4 *>(a.out + o) = make_float4(f[0], f[1], f[2], f[3]);
+    }
+}
+
 cudaError_t launch_conv_f32(const ConvF32Args &a, cudaStream_t s) {
     const long npix = static_cast<long>(a.B) * a.Ho * a.Wo;
     static const bool direct = getenv("SLIM_F32_DIRECT") != nullptr;   // A/B: the direct-conv kernel
@@ -655,8 +717,16 @@ cudaError_t launch_conv_f32(const ConvF32Args &a, cudaStream_t s) {
     }
     if (!direct && a.c_in % kGK == 0 && (a.epi != EPI_BN_PROJ_RELU || a.c_in1 % kGK == 0) && a.c_out % 16 == 0) {
         const int gx = static_cast<int>((npix + kGM - 1) / kGM), gy = (a.c_out + kGN - 1) / kGN;
-        const int grid = (a.max_ctas > 0 && a.max_ctas < gx * gy) ? a.max_ctas : gx * gy;
-        conv_f32_gemm_kernel<<<grid, kGThreads, 0, s>>>(a, gx, gy);
+        const int ks = (a.ksplit > 1 && a.part) ? a.ksplit : 1;
+        ConvF32Args b = a;
+        b.ksplit = ks;
+        const int work = gx * gy * ks;
+        const int grid = (a.max_ctas > 0 && a.max_ctas < work) ? a.max_ctas : work;
+        conv_f32_gemm_kernel<<<grid, kGThreads, 0, s>>>(b, gx, gy);
+        if (ks > 1) {
+            const size_t n4 = static_cast<size_t>(npix) * a.c_out / 4;
+            conv_f32_splitk_reduce<<<static_cast<unsigned>(std::min<size_t>((n4 + 255) / 256, 148 * 8)), 256, 0, s>>>(b);
+        }
         return cudaGetLastError();
     }
     dim3 grid(static_cast<unsigned>((npix + 63) / 64), (a.c_out + 31) / 32);

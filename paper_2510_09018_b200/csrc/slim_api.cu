@@ -184,8 +184,21 @@ size_t gn_part_bytes(const slim_config &c, int s, float r, int B) {
 size_t tile_flag_bytes(const slim_config &c, int B) {
     return c.dtype == SLIM_BF16 ? round256(2 * static_cast<size_t>(B) * 8 * sizeof(uint32_t)) : 0;
 }
+// FP32 mode split-K (ConvF32Args::ksplit): K splits of segment s's layers -- every layer of a segment has the
+// same output tiling -- from the tile count at max_batch (never B: the summation order is batch independent)
+int f32_ksplit(const slim_config &c, int s, float r) {
+    if (c.dtype != SLIM_FP32 || getenv("SLIM_F32_NO_SPLITK")) return 1;
+    const int H = seg_hw(c, s), C = slim_act_channels(r, c.base_channels[s]);
+    const long tiles = (static_cast<long>(c.max_batch) * H * H + 127) / 128 * ((C + 63) / 64);
+    return tiles >= 148 ? 1 : static_cast<int>(std::min<long>(4, std::max<long>(1, 296 / tiles)));
+}
+size_t f32_part_bytes(const slim_config &c, int s, float r, int B) {
+    const int ks = f32_ksplit(c, s, r);
+    return ks > 1 ? round256((ks + 1) * act_bytes(c, s, r, B)) : 0;   // + the projection's slot
+}
 size_t seg_ws_bytes(const slim_config &c, int s, float r, int B) {
-    return 3 * round256(act_bytes(c, s, r, B)) + gn_part_bytes(c, s, r, B) + tile_flag_bytes(c, B);
+    return 3 * round256(act_bytes(c, s, r, B)) + gn_part_bytes(c, s, r, B) + tile_flag_bytes(c, B) +
+           f32_part_bytes(c, s, r, B);
 }
 
 uint16_t f2bf(float f) {   // round-to-nearest-even (NaN kept NaN)
@@ -380,6 +393,7 @@ struct ConvCall {
     uint32_t *flag_in = nullptr, *flag_out = nullptr, *flag_zero = nullptr;
     int flag_in_target = 0, flag_zero_n = 0;
     HaloArgs *dry = nullptr;
+    float *f32_part = nullptr;               // FP32 mode: split-K partials (workspace), nullptr = no split
     mutable bool gn_stats = false;           // set when the launched kernel wrote them (halo path)
     mutable int gn_tiles_per_img = 0;        // their tiling (partials per image per group)
 };
@@ -1146,6 +1160,8 @@ slim_status conv_f32(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, int ri,
     a.out = static_cast<float *>(cc.out);
     a.epi = cc.epi;
     a.relu_lo = cc.relu_lo;
+    a.ksplit = cc.f32_part ? f32_ksplit(c, cc.seg, c.widths[ri]) : 1;
+    a.part = cc.f32_part;
     {   // SM share of this width (< 1, or SLIM_GRID_CAP): 2 resident GEMM CTAs per SM of the share,
         // persistent over tiles; at the full share: one CTA per tile (max_ctas = 0)
         const int cap = grid_cap(ctx, ri, ctx->num_sms, cc.seg);
@@ -1277,6 +1293,11 @@ slim_status run_segment(slim_ctx *ctx, int seg, int ri_prev, int ri, int B, cons
     const int C = slim_act_channels(r, c.base_channels[seg]);
     const size_t buf = round256(act_bytes(c, seg, r, B));
     char *bufs[3] = {static_cast<char *>(ws), static_cast<char *>(ws) + buf, static_cast<char *>(ws) + 2 * buf};
+    // FP32 mode: split-K partials after the buffers (f32_part_bytes)
+    float *f32_part = (!bf && f32_ksplit(c, seg, r) > 1)
+                          ? reinterpret_cast<float *>(static_cast<char *>(ws) + 3 * buf + gn_part_bytes(c, seg, r, B) +
+                                                      tile_flag_bytes(c, B))
+                          : nullptr;
     const void *cur = in;
     int curH = (seg == 0) ? H : (H * 2);
     int curC = (seg == 0) ? c.in_channels : slim_act_channels(c.widths[ri_prev], c.base_channels[seg - 1]);
@@ -1549,6 +1570,7 @@ slim_status run_segment(slim_ctx *ctx, int seg, int ri_prev, int ri, int B, cons
         c1.c_in = curC;
         c1.out = T;
         c1.epi = EPI_BN_RELU;
+        c1.f32_part = f32_part;
         // the network's last conv pools in its epilogue (BF16 mode): the segment-3 output
         // never goes to memory; the head is then the FC alone
         const bool fuse_pool = !gn && bf && seg == 3 && b == nb - 1 && H * H <= 32 && 32 % (H * H) == 0;
@@ -1561,6 +1583,7 @@ slim_status run_segment(slim_ctx *ctx, int seg, int ri_prev, int ri, int B, cons
         c2.H = c2.W = H;
         c2.c_in = C;
         c2.out = dst;
+        c2.f32_part = f32_part;
         if (fuse_pool) c2.pool_out = reinterpret_cast<float *>(dst);
         if (down) {
             c2.epi = EPI_BN_PROJ_RELU;
@@ -1644,6 +1667,7 @@ slim_status run_segment(slim_ctx *ctx, int seg, int ri_prev, int ri, int B, cons
                 p.out = T;
                 p.epi = EPI_BN_RELU;
                 p.relu_lo = relu_lo;
+                p.f32_part = f32_part;
                 s1 = bf ? conv_bf16(ctx, st, p, ri, B) : conv_f32(ctx, st, p, ri, B);
                 if (s1) return s1;
                 yp = T;

@@ -244,6 +244,12 @@ struct ConvF32Args {
     int epi;
     float relu_lo;                               // 0 = ReLU, -inf = raw pre-norm output (GroupNorm mode)
     int max_ctas;                                // persistent-grid cap of the GEMM kernels (0 = one CTA per tile)
+    // split-K (layers without a projection whose tiles leave most SMs idle): ksplit CTAs per tile take
+    // consecutive ranges of the K steps and write raw fp32 partials part[split][pixel][c_out]; a reduce
+    // kernel sums them in split order (deterministic) and applies the epilogue.  ksplit depends on the
+    // layer shape and max_batch only (never on B), so the summation order is batch independent.
+    int ksplit;
+    float *part;
 };
 cudaError_t launch_conv_f32(const ConvF32Args &a, cudaStream_t s);
 cudaError_t launch_stem_f32(const float *in, const float *w, int cin_full, const float *scale,
