@@ -659,3 +659,15 @@ def test_tile_flags_bitwise(tmp_path):
     one, two = _seg123_outputs_under_env(tmp_path, [dict(SLIM_TILE_FLAGS="0"), dict(SLIM_TILE_FLAGS="1")])
     for k in one.files:
         assert np.array_equal(one[k], two[k]), k
+
+
+def test_fp32_split_k_batch_independence_bitwise(net32):
+    """FP32 mode's split-K (under-filled layers of segments 2-3: K ranges per split, partials reduced in
+    split order) picks its split count from the layer shape and max_batch only, so an image's logits are
+    bitwise the same in a batch of 1, 7 or 16 (max_batch 64: segments 2-3 split)."""
+    x = synth.make_images(16, offset=23)
+    tup = (1.0, 0.5, 1.0, 0.25)
+    full = net32.forward_chain(_dev(x, torch.float32), tup).cpu().numpy()
+    for B in (1, 7):
+        part = net32.forward_chain(_dev(x[:B], torch.float32), tup).cpu().numpy()
+        assert np.array_equal(part, full[:B]), B
