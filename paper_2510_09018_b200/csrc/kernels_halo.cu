@@ -278,17 +278,31 @@ __global__ void __launch_bounds__(kSmall ? kHaloThreadsSmall : kHaloThreads, kSm
                     const uint32_t oplane = static_cast<uint32_t>((a.rows + 1) * a.row_px) * RBK;
                     const uint32_t eplane = static_cast<uint32_t>(a.rows * a.row_px) * RBK;
                     mbar_wait(a_empty(s), ph ^ 1);
-                    mbar_expect_tx(a_full(s), 2u * oplane);
-                    tma_load_4d(sA + s * a.a_slot, &tmA1, a_full(s), ch * CK, 1, n * a.tile_imgs, 2 * h0 - 1);
-                    tma_load_4d(sA + s * a.a_slot + oplane, &tmA1, a_full(s), ch * CK, 0, n * a.tile_imgs, 2 * h0 - 1);
+                    if (pair) {   // own planes; the leader's a_full counts both CTAs' bytes
+                        const uint32_t lb = mapa_u32(a_full(s), 0);
+                        if (leader_cta) mbar_expect_tx(a_full(s), 4u * oplane);
+                        tma_load_4d_pair(sA + s * a.a_slot, &tmA1, lb, ch * CK, 1, n * a.tile_imgs, 2 * h0 - 1);
+                        tma_load_4d_pair(sA + s * a.a_slot + oplane, &tmA1, lb, ch * CK, 0, n * a.tile_imgs, 2 * h0 - 1);
+                    } else {
+                        mbar_expect_tx(a_full(s), 2u * oplane);
+                        tma_load_4d(sA + s * a.a_slot, &tmA1, a_full(s), ch * CK, 1, n * a.tile_imgs, 2 * h0 - 1);
+                        tma_load_4d(sA + s * a.a_slot + oplane, &tmA1, a_full(s), ch * CK, 0, n * a.tile_imgs, 2 * h0 - 1);
+                    }
                     if (++s == a.sa) {
                         s = 0;
                         ph ^= 1;
                     }
                     mbar_wait(a_empty(s), ph ^ 1);
-                    mbar_expect_tx(a_full(s), 2u * eplane);
-                    tma_load_4d(sA + s * a.a_slot, &tmA, a_full(s), ch * CK, 1, n * a.tile_imgs, 2 * h0);
-                    tma_load_4d(sA + s * a.a_slot + eplane, &tmA, a_full(s), ch * CK, 0, n * a.tile_imgs, 2 * h0);
+                    if (pair) {
+                        const uint32_t lb = mapa_u32(a_full(s), 0);
+                        if (leader_cta) mbar_expect_tx(a_full(s), 4u * eplane);
+                        tma_load_4d_pair(sA + s * a.a_slot, &tmA, lb, ch * CK, 1, n * a.tile_imgs, 2 * h0);
+                        tma_load_4d_pair(sA + s * a.a_slot + eplane, &tmA, lb, ch * CK, 0, n * a.tile_imgs, 2 * h0);
+                    } else {
+                        mbar_expect_tx(a_full(s), 2u * eplane);
+                        tma_load_4d(sA + s * a.a_slot, &tmA, a_full(s), ch * CK, 1, n * a.tile_imgs, 2 * h0);
+                        tma_load_4d(sA + s * a.a_slot + eplane, &tmA, a_full(s), ch * CK, 0, n * a.tile_imgs, 2 * h0);
+                    }
                     if (++s == a.sa) {
                         s = 0;
                         ph ^= 1;
@@ -368,8 +382,15 @@ __global__ void __launch_bounds__(kSmall ? kHaloThreadsSmall : kHaloThreads, kSm
                             // (the epilogue reads the accumulators in that column order)
                             const uint32_t lb = mapa_u32(b_full(s), 0);
                             if (leader_cta) mbar_expect_tx(b_full(s), 3u * a.n_tile * RBK);
-                            tma_load_3d_pair(sB + s * a.b_bytes, &tmBh, lb, ch * CK,
-                                             co0 + static_cast<int>(prank) * (a.n_tile / 2), kh * 3);
+                            if (s2) {   // stride 2: [kw0 | kw2] (N = 2n) split by tap, kw1 (N = n) by channel half:
+                                        // this CTA holds tap kw0 (rank 0) or kw2 (rank 1), then its half of kw1
+                                tma_load_3d_pair(sB + s * a.b_bytes, &tmB, lb, ch * CK, co0, kh * 3 + (prank ? 2 : 0));
+                                tma_load_3d_pair(sB + s * a.b_bytes + static_cast<uint32_t>(a.n_tile) * RBK, &tmBh, lb,
+                                                 ch * CK, co0 + static_cast<int>(prank) * (a.n_tile / 2), kh * 3 + 1);
+                            } else {
+                                tma_load_3d_pair(sB + s * a.b_bytes, &tmBh, lb, ch * CK,
+                                                 co0 + static_cast<int>(prank) * (a.n_tile / 2), kh * 3);
+                            }
                             if (++s == a.sb) {
                                 s = 0;
                                 ph ^= 1;
@@ -449,7 +470,9 @@ __global__ void __launch_bounds__(kSmall ? kHaloThreadsSmall : kHaloThreads, kSm
                 tc_fence_after();
                 const uint32_t acc = tmem_base + static_cast<uint32_t>(as * a.stage_cols);
                 if (s2) {
-                    const uint32_t idesc2 = umma_idesc_bf16(kTileM, 2 * a.n_tile), idesc1 = umma_idesc_bf16(kTileM, a.n_tile);
+                    const uint32_t idesc2 = umma_idesc_bf16(kTileMM, 2 * a.n_tile), idesc1 = umma_idesc_bf16(kTileMM, a.n_tile);
+                    // pair: B of [kw0 | kw2] = this CTA's n rows at the slot start, kw1 = its n/2 rows after them
+                    const uint32_t kw1_off16 = pair ? static_cast<uint32_t>(a.n_tile * RBK) >> 4 : 2 * tap16;
                     const uint32_t oplane16 = static_cast<uint32_t>((a.rows + 1) * a.row_px * RBK) >> 4;
                     const uint32_t eplane16 = static_cast<uint32_t>(a.rows * a.row_px * RBK) >> 4;
                     for (int ch = 0; ch < a.n_chunks; ++ch) {
@@ -474,16 +497,16 @@ __global__ void __launch_bounds__(kSmall ? kHaloThreadsSmall : kHaloThreads, kSm
                                     for (int kk = 0; kk < nk; ++kk) {
                                         const bool accum = (ch | kh | kk) != 0;
                                         // odd columns -> [acc_kw0 | acc_kw2], even columns -> acc_kw1
-                                        umma_bf16(acc, ad + roff + 2 * kk, bk + 2 * kk, idesc2, accum);
-                                        umma_bf16(acc + 2 * accs, ad + plane16 + roff + 2 * kk, bk + 2 * tap16 + 2 * kk,
-                                                  idesc1, accum);
+                                        mma(acc, ad + roff + 2 * kk, bk + 2 * kk, idesc2, accum);
+                                        mma(acc + 2 * accs, ad + plane16 + roff + 2 * kk, bk + kw1_off16 + 2 * kk, idesc1,
+                                            accum);
                                     }
                                 }
                                 __syncwarp();
                                 if (!a.stationary) {
                                     if (elect_one()) {
                                         if (kClu == 1) umma_commit_mc(b_empty(bs), bmask);
-                                        else umma_commit(b_empty(bs));
+                                        else commit(b_empty(bs));
                                     }
                                     __syncwarp();
                                     if (++bs == a.sb) {
@@ -492,7 +515,7 @@ __global__ void __launch_bounds__(kSmall ? kHaloThreadsSmall : kHaloThreads, kSm
                                     }
                                 }
                             }
-                            if (elect_one()) umma_commit(a_empty(s));
+                            if (elect_one()) commit(a_empty(s));
                             __syncwarp();
                             if (++s == a.sa) {
                                 s = 0;
@@ -819,8 +842,10 @@ __global__ void __launch_bounds__(kSmall ? kHaloThreadsSmall : kHaloThreads, kSm
                 uint32_t v0[16], v1[16], v2[16];
                 // kw accumulator columns of channels g*16..: pair mode interleaves the two channel halves
                 // ([kw0 kw1 kw2] of the first n/2 channels, then of the second), else kw * acc_stride + channel
-                const int hn = pair ? a.n_tile / 2 : a.acc_stride;
-                const uint32_t cb = col0 + static_cast<uint32_t>(pair ? (g * 16 / hn) * 3 * hn + (g * 16) % hn : g * 16);
+                // (stride 2: each of its two MMAs splits N in natural order -- columns as in the one-CTA kernel)
+                constexpr bool ilv = pair && !s2;
+                const int hn = ilv ? a.n_tile / 2 : a.acc_stride;
+                const uint32_t cb = col0 + static_cast<uint32_t>(ilv ? (g * 16 / hn) * 3 * hn + (g * 16) % hn : g * 16);
                 tmem_ld16(lane_addr + cb, v0);
                 if (x2) tmem_ld16(lane_addr + col0 + a.acc_stride + g * 16, v2);   // acc_m, acc_2
                 if (!x3 && !x2) {
@@ -1093,8 +1118,8 @@ cudaError_t launch_conv_halo(const HaloArgs &a, const CUtensorMap &tmA, const CU
     // cluster variants (streamed weights only: 64-channel boxes, plain / projection / pool / stride 2)
     static const Fn mc_fns[4] = {conv_halo_kernel<false, 0, false, 1>, conv_halo_kernel<false, 1, false, 1>,
                                  conv_halo_kernel<false, 2, false, 1>, conv_halo_kernel<false, 3, false, 1>};
-    static const Fn pair_fns[3] = {conv_halo_kernel<false, 0, false, 2>, conv_halo_kernel<false, 1, false, 2>,
-                                   conv_halo_kernel<false, 2, false, 2>};
+    static const Fn pair_fns[4] = {conv_halo_kernel<false, 0, false, 2>, conv_halo_kernel<false, 1, false, 2>,
+                                   conv_halo_kernel<false, 2, false, 2>, conv_halo_kernel<false, 3, false, 2>};
     // GroupNorm in the epilogue (whole-image tiles): plain / projection / pool / stride 2
     static const Fn gn_fns[2][4] = {{conv_halo_kernel<false, 0, false, 0, true>, conv_halo_kernel<false, 1, false, 0, true>,
                                      conv_halo_kernel<false, 2, false, 0, true>, conv_halo_kernel<false, 3, false, 0, true>},
@@ -1112,7 +1137,7 @@ cudaError_t launch_conv_halo(const HaloArgs &a, const CUtensorMap &tmA, const CU
                 if (cudaError_t e = big(fns[m][v]); e != cudaSuccess) return e;
         for (int v = 0; v < 4; ++v)
             if (cudaError_t e = big(mc_fns[v]); e != cudaSuccess) return e;
-        for (int v = 0; v < 3; ++v)
+        for (int v = 0; v < 4; ++v)
             if (cudaError_t e = big(pair_fns[v]); e != cudaSuccess) return e;
         for (int m = 0; m < 2; ++m)
             for (int v = 0; v < 4; ++v)
@@ -1139,8 +1164,8 @@ cudaError_t launch_conv_halo(const HaloArgs &a, const CUtensorMap &tmA, const CU
     cfg.attrs = attr;
     cfg.numAttrs = (a.bmc > 1 || a.pair) ? 2 : 1;
     if (a.bmc > 1 && (grid % a.bmc || a.m_tiles % a.bmc || a.stationary || a.small)) return cudaErrorInvalidValue;
-    if (a.pair && (grid % 2 || a.m_tiles % 2 || a.stationary || a.small || a.bmc > 1 || a.kw_fuse != 3 || a.stride2 ||
-                   a.x3 || a.n_tile % 16))
+    if (a.pair && (grid % 2 || a.m_tiles % 2 || a.stationary || a.small || a.bmc > 1 || a.kw_fuse != 3 || a.x3 ||
+                   a.n_tile % 16))
         return cudaErrorInvalidValue;
     const bool narrow = a.ck != kChunk || a.co_chunk != kChunk;
     const int var = a.stride2 ? 3 : (a.x3 == 1 ? 4 : (a.x3 == 2 ? 5 : (a.epi == EPI_BN_PROJ_RELU ? 1 : (a.pool_out ? 2 : 0))));
@@ -1155,7 +1180,7 @@ cudaError_t launch_conv_halo(const HaloArgs &a, const CUtensorMap &tmA, const CU
         return cudaLaunchKernelEx(&cfg, gn_fns[narrow ? 1 : 0][var], tmA, tmB, tmRes, tmOut, tmA1, tmB1, tmBh, a);
     }
     if (a.pair) {
-        if (narrow || var > 2) return cudaErrorInvalidValue;
+        if (narrow || var > 3) return cudaErrorInvalidValue;
         return cudaLaunchKernelEx(&cfg, pair_fns[var], tmA, tmB, tmRes, tmOut, tmA1, tmB1, tmBh, a);
     }
     if (a.bmc > 1) {

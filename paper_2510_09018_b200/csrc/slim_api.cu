@@ -658,9 +658,14 @@ slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, i
     // M = 256 MMA per k-step, each CTA holding half of every B stage -- the layer's weight bytes from L2
     // and into each SM halve (streamed-weight layers: segments 1-3 at the wide widths).  SLIM_HALO_PAIR=0
     // turns it off (A/B).
-    static const int pair_env = getenv("SLIM_HALO_PAIR") ? atoi(getenv("SLIM_HALO_PAIR")) : 0;
+    // Default: on from B = 1024 (same-box CFG3 A/B: +3-6 % per chain at B >= 1024 for every width, mixed
+    // at B = 256-512, -1.6 % in the B = 128 CFG2 step; bit-identical either way, so the choice may depend on B).
+    // SLIM_HALO_PAIR: 0 = off, 1 = every eligible layer, 2 = the stride-2 convs only.
+    static const int pair_env = getenv("SLIM_HALO_PAIR") ? atoi(getenv("SLIM_HALO_PAIR")) : -1;
+    const int pair_mode = pair_env >= 0 ? pair_env : (B >= 1024 && c_out >= 192 ? 1 : 0);   // (r = 0.25 seg 3: slower)
     const bool wide_boxes = a.ck == kChunk && a.co_chunk == kChunk;   // (the cluster variants are compiled for these)
-    const bool pair = pair_env != 0 && !a.gn_fuse && wide_boxes && !a.stationary && !small && !a.x3 && !s2 && a.kw_fuse == 3 && a.m_tiles % 2 == 0 &&
+    const bool pair = pair_mode != 0 && (pair_mode != 2 || s2) && !a.gn_fuse && wide_boxes && !a.stationary && !small && !a.x3 &&
+                      a.kw_fuse == 3 && a.m_tiles % 2 == 0 &&
                       a.n_tile % 16 == 0 && !a.gn_part &&
                       grid_cap(ctx, ri, std::min(ctx->num_sms, a.m_tiles * a.n_tiles), cc.seg) >= 2;
     if (pair) {
@@ -761,7 +766,7 @@ slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, i
     a.bmc = 1;
     CUtensorMap tBh = tA;
     if (a.pair) {
-        if (!encode_w_taps(ctx, &tBh, L, cc.c_in, c_out, a.n_tile / 2, 3, a.ck))
+        if (!encode_w_taps(ctx, &tBh, L, cc.c_in, c_out, a.n_tile / 2, s2 ? 1 : 3, a.ck))
             return fail(ctx, SLIM_ECUDA, "cuTensorMapEncodeTiled(halo W pair half) failed");
     } else if ((bmc_env == 2 || bmc_env == 4) && wide_boxes && !a.stationary && !small && !a.x3 && a.m_tiles % bmc_env == 0 &&
         (a.n_tile / bmc_env) % 8 == 0 && grid >= bmc_env) {
