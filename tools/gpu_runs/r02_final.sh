@@ -12,6 +12,8 @@ timeout 600 python bench.py --workload cfg1 > gpurun_out/rf_cfg1_line.json 2>/de
 timeout 600 python bench.py --workload stream > gpurun_out/rf_stream_line.json 2>/dev/null
 timeout 900 python bench.py --workload sweep > gpurun_out/rf_sweep.json 2>/dev/null
 timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/rf_reference_line.json 2>/dev/null
+$NCU --set full --clock-control none -k "regex:conv_|fused_kernel|stem_|fc_kernel" -s 18 -c 18 -o /tmp/rf_b4096_r1 python tools/profile_chain.py --widths 1.0 --batch 4096 --reps 2 > gpurun_out/rf_ncu_b4096.log 2>&1
+$NCU -i /tmp/rf_b4096_r1.ncu-rep --page raw --csv > gpurun_out/rf_b4096_r1_raw.csv
 echo lines rc=$?
 $NCU --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/rf_launches_bench.csv \
     python bench.py --steps 3 --warmup 3 --no-cpu --energy-seconds 0 --e2e-steps 1 --profile-steps 1 --width-events 0 > gpurun_out/rf_launch_bench.log 2>&1
