@@ -662,7 +662,8 @@ slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, i
     // at B = 256-512, -1.6 % in the B = 128 CFG2 step; bit-identical either way, so the choice may depend on B).
     // SLIM_HALO_PAIR: 0 = off, 1 = every eligible layer, 2 = the stride-2 convs only.
     static const int pair_env = getenv("SLIM_HALO_PAIR") ? atoi(getenv("SLIM_HALO_PAIR")) : -1;
-    const int pair_mode = pair_env >= 0 ? pair_env : (B >= 1024 && c_out >= 192 ? 1 : 0);   // (r = 0.25 seg 3: slower)
+    // (128-channel layers only at segment 1: at segments 2-3 (r = 0.25 / 0.5) they measured slower)
+    const int pair_mode = pair_env >= 0 ? pair_env : (B >= 1024 && (c_out >= 192 || cc.seg == 1) ? 1 : 0);
     const bool wide_boxes = a.ck == kChunk && a.co_chunk == kChunk;   // (the cluster variants are compiled for these)
     const bool pair = pair_mode != 0 && (pair_mode != 2 || s2) && !a.gn_fuse && wide_boxes && !a.stationary && !small && !a.x3 &&
                       a.kw_fuse == 3 && a.m_tiles % 2 == 0 &&
