@@ -112,6 +112,22 @@ __global__ void __launch_bounds__(kSmall ? kHaloThreadsSmall : kHaloThreads, kSm
     // GN image pairs (a.gn_pairs, segment 1: an image is two M tiles): the CTA takes both tiles of an image
     // back to back (its it-th tile is 2u + (it & 1)), so both accumulators are in TMEM for the statistics
     const bool prs = kGN && a.gn_pairs;
+    // tile t -> (M tile, N tile): M-fastest by default; a.nfast: N-fastest, so the n_tiles tiles that read
+    // the same input rows run at the same time on neighbouring CTAs and the input comes from DRAM once
+    // (large batches); pair / image-pair modes keep their two tiles (t, t+1) on consecutive M tiles
+    auto decode = [&](int t, int &mt, int &nt) {
+        if (!a.nfast) {
+            mt = t % a.m_tiles;
+            nt = t / a.m_tiles;
+        } else if (kClu == 2 || prs) {   // (pair)
+            const int u = t >> 1;
+            mt = 2 * (u / a.n_tiles) + (t & 1);
+            nt = u % a.n_tiles;
+        } else {
+            mt = t / a.n_tiles;
+            nt = t % a.n_tiles;
+        }
+    };
     auto tile_at = [&](int it) {
         if (!prs) return static_cast<int>(blockIdx.x) + it * static_cast<int>(gridDim.x);
         return 2 * (static_cast<int>(blockIdx.x) + (it >> 1) * static_cast<int>(gridDim.x)) + (it & 1);
@@ -240,7 +256,8 @@ __global__ void __launch_bounds__(kSmall ? kHaloThreadsSmall : kHaloThreads, kSm
             int s = 0;
             uint32_t ph = 0;
             for (int ti = 0, t; (t = tile_at(ti)) < total; ++ti) {
-                const int mt = t % a.m_tiles;
+                int mt, nt_unused;
+                decode(t, mt, nt_unused);
                 const int n = mt / tiles_per_img, h0 = (mt - n * tiles_per_img) * a.rows;
                 wait_inputs(mt);
                 TD(0, ti, 0);
@@ -310,7 +327,9 @@ __global__ void __launch_bounds__(kSmall ? kHaloThreadsSmall : kHaloThreads, kSm
                 }
                 // projection chunks: the stride-2 sampled block input (128 px x 64 ch) and its
                 // 1x1 weights (n_tile x 64) share one A slot
-                const int co0 = (t / a.m_tiles) * a.n_tile;
+                int mt_unused, nt_b;
+                decode(t, mt_unused, nt_b);
+                const int co0 = nt_b * a.n_tile;
                 for (int cp = 0; proj && cp < a.n_chunks_p; ++cp) {
                     mbar_wait(a_empty(s), ph ^ 1);
                     if (pair) {   // own 128 px + HALF of the 1x1 weights (tmB1 box: n_tile/2 rows)
@@ -342,7 +361,8 @@ __global__ void __launch_bounds__(kSmall ? kHaloThreadsSmall : kHaloThreads, kSm
             int rs = 0;
             uint32_t rph = 0;
             for (int ti = 0, t; (t = tile_at(ti)) < total; ++ti) {
-                const int mt = t % a.m_tiles, nt = t / a.m_tiles;
+                int mt, nt;
+                decode(t, mt, nt);
                 const int n = mt / tiles_per_img, h0 = (mt - n * tiles_per_img) * a.rows, co0 = nt * a.n_tile;
                 wait_inputs(mt);   // (the residual is older than the input: transitively finished)
                 mbar_wait(r_empty(rs), rph ^ 1);
@@ -371,7 +391,9 @@ __global__ void __launch_bounds__(kSmall ? kHaloThreadsSmall : kHaloThreads, kSm
             const uint32_t rank = kClu == 1 ? cluster_ctarank() : 0u;
             const uint32_t tapb = static_cast<uint32_t>(a.n_tile) * RBK, hoff = rank * hrows * RBK;
             for (int ti = 0, t; (t = tile_at(ti)) < total; ++ti) {
-                const int co0 = (t / a.m_tiles) * a.n_tile;
+                int mt_unused, nt_b;
+                decode(t, mt_unused, nt_b);
+                const int co0 = nt_b * a.n_tile;
                 for (int ch = 0; ch < a.n_chunks; ++ch)
                     for (int kq = 0; kq < 3; ++kq) {
                         const int kh = s2 ? (kq == 0 ? 0 : (kq == 1 ? 2 : 1)) : kq;   // s2 consumes kh 0, 2, 1
@@ -720,7 +742,8 @@ __global__ void __launch_bounds__(kSmall ? kHaloThreadsSmall : kHaloThreads, kSm
         // the group's next-but-one tile starts (wait_group 1: never stalls on the store just issued)
         int prev_mt = -1, prev2_mt = -1;
         for (int ti = grp, t; (t = tile_at(ti)) < total; ti += n_grp) {
-            const int mt = t % a.m_tiles, nt = t / a.m_tiles;
+            int mt, nt;
+            decode(t, mt, nt);
             const int n = mt / tiles_per_img, h0 = (mt - n * tiles_per_img) * a.rows, co0 = nt * a.n_tile;
             const int as = ti % a.acc_stages, rs = n_res ? ti % n_res : 0;
             const uint32_t aph = (ti / a.acc_stages) & 1, rph = n_res ? (ti / n_res) & 1 : 0;

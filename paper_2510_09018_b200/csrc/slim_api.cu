@@ -758,6 +758,13 @@ slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, i
     if (a.gn_pairs && grid > total / 2) grid = total / 2;   // a CTA's tiles come in image pairs
     grid = grid_cap(ctx, ri, grid, cc.seg);
     if (a.pair) grid -= grid % 2;   // (>= 2: checked with the pair decision)
+    // tile order: SLIM_HALO_NFAST = 1 N-fastest, 0 M-fastest, unset = auto (see below)
+    static const int nfast_env = getenv("SLIM_HALO_NFAST") ? atoi(getenv("SLIM_HALO_NFAST")) : -1;
+    // auto: N-fastest once the layer's input no longer fits L2 (126 MB): then the M-fastest order streams the
+    // input from DRAM once per N tile (B = 4096: r = 1 chain 4.95 -> 4.60 ms, r = 0.75 3.55 -> 3.44 ms), while
+    // with an L2-resident input it keeps each weight tile hot (B = 1024: M-fastest 5 % faster); bit-identical
+    const double in_bytes = 2.0 * B * cc.H * cc.W * cc.c_in;
+    a.nfast = (a.n_tiles > 1 && (nfast_env == 1 || (nfast_env < 0 && in_bytes > 96e6))) ? 1 : 0;
     // streamed weights: clusters of bmc CTAs on consecutive M tiles of one N tile share each B stage
     // (TMA multicast) -- the weight bytes one launch pulls from L2 drop by bmc.  Opt-in (SLIM_HALO_BMC=2|4):
     // bit-identical, but measured no faster (B=1024 r=1 seg 2/3 convs 84/80 us either way; B=128 chains
@@ -774,6 +781,7 @@ slim_status conv_halo_bf16(slim_ctx *ctx, cudaStream_t st, const ConvCall &cc, i
         if (!encode_w_taps(ctx, &tBh, L, cc.c_in, c_out, a.n_tile / bmc_env, 1, a.ck))
             return fail(ctx, SLIM_ECUDA, "cuTensorMapEncodeTiled(halo W share) failed");
         a.bmc = bmc_env;
+        a.nfast = 0;   // (the multicast clusters take M-consecutive tiles of one N tile)
         grid -= grid % bmc_env;
     }
     double flops, bytes;

@@ -145,6 +145,7 @@ struct HaloArgs {
     // counters (one red.release per finished tile, after its TMA store completed).  flag_zero: counters
     // of later layers this kernel clears (after its own griddepcontrol.wait, before it lets dependents
     // launch).  All nullptr = the plain PDL dependency.
+    int nfast;   // N-fastest tile order (the N tiles of an M tile on neighbouring CTAs); 0 = M-fastest
     uint32_t *flag_in, *flag_out, *flag_zero;
     int flag_in_target, flag_zero_n;
 };

@@ -671,3 +671,14 @@ def test_fp32_split_k_batch_independence_bitwise(net32):
     for B in (1, 7):
         part = net32.forward_chain(_dev(x[:B], torch.float32), tup).cpu().numpy()
         assert np.array_equal(part, full[:B]), B
+
+
+def test_halo_tile_order_bitwise(tmp_path):
+    """N-fastest tile order (SLIM_HALO_NFAST=1; the n_tiles tiles of an M tile on neighbouring CTAs), with
+    and without the 2-SM pairing: every segment 1-3 output bitwise the default order's."""
+    base, nf, nfp = _seg123_outputs_under_env(tmp_path, [dict(SLIM_HALO_NFAST="0", SLIM_HALO_PAIR="0"),
+                                                         dict(SLIM_HALO_NFAST="1", SLIM_HALO_PAIR="0"),
+                                                         dict(SLIM_HALO_NFAST="1", SLIM_HALO_PAIR="1")])
+    for k in base.files:
+        assert np.array_equal(base[k], nf[k]), k
+        assert np.array_equal(base[k], nfp[k]), k
