@@ -733,7 +733,12 @@ def run_stream(args):
         k += 1
         if k % 8 == 0:
             torch.cuda.synchronize()
-            if time.perf_counter() - t0 >= args.energy_seconds:
+            stop = time.perf_counter() - t0 >= args.energy_seconds
+            if world > 1:   # every step ticks a collective: all ranks must leave the loop at the same step
+                f = torch.tensor([1.0 if stop else 0.0], device=_coll_dev(dev))
+                dist.all_reduce(f, op=dist.ReduceOp.MAX)
+                stop = float(f.item()) > 0
+            if stop:
                 break
     torch.cuda.synchronize()
     sampler.stop()
